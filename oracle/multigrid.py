@@ -1,0 +1,325 @@
+"""DtN-based geometric multigrid hierarchy and V-cycle (Section 3).
+
+Levels are numbered k = N (finest, order p) down to 1 (coarsest).  Every
+operator is a global sparse matrix over the *free* trace dofs of its level,
+built literally from the paper's formulas:
+
+  p-coarsening, for p > 1:
+      I_N = J_N, Q_{N-1} = J_N^*, A_{N-1} = J_N^* A_N J_N      (Eq. ANm1)
+  h-coarsening by 2x2 agglomeration:
+      E_k = E_{k,I} (+) E_{k,B}, M_{k-1} subset M_{k,B}        (Eq. 3.2)
+      I_k = [-A_II^-1 A_IB J_k ; J_k]                          (Eq. 3.3)
+      Q_{k-1} = [-J_k^* A_BI A_II^-1 , J_k^*]                  (Eq. 3.5)
+      A_{k-1} = J_k^*(A_BB - A_BI A_II^-1 A_IB) J_k            (Eq. Akm1)
+  local correction T_k = [A_II^-1 0; 0 0]                      (Eq. 3.11)
+  V-cycle = Algorithm 1, B_1 = A_1^-1 by a direct solver.
+
+Readings: adjoints are matrix transposes (Q5); J_k is nodal P1
+interpolation along straight macro-edges split in halves (O7); coarse
+macro-edges on dOmega carry no dofs (Dirichlet); A_II^-1 is formed per
+macro-element block because A_II is block diagonal across macros
+("completely local to each macro-element"); smoothers:
+edge block-Jacobi and Chebyshev on D_B^-1 A with
+bounds [lambda_max/30, lambda_max] (Q8, Q11).
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.linalg as sla
+import scipy.sparse as sp
+
+from . import mesh
+from .basis import gll_nodes
+
+BLOCK_JACOBI = 0
+CHEBYSHEV = 1
+
+
+# --------------------------------------------------------------------------
+# injections J
+# --------------------------------------------------------------------------
+
+def p_injection_full(n: int, p: int) -> sp.csr_matrix:
+    """J_N: P^1 -> P^p on every edge (nodal interpolation at GLL nodes).
+
+    Fine dof (e, a) = (1 - s_a) * coarse (e, 0) + s_a * coarse (e, 1).
+    """
+    s = gll_nodes(p)
+    E = mesh.n_edges(n)
+    k = p + 1
+    rows, cols, vals = [], [], []
+    for a in range(k):
+        rows += [np.arange(E) * k + a] * 2
+        cols += [np.arange(E) * 2 + 0, np.arange(E) * 2 + 1]
+        vals += [np.full(E, 1.0 - s[a]), np.full(E, s[a])]
+    return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                         shape=(E * k, E * 2)).tocsr()
+
+
+def h_injection_full(n: int) -> sp.csr_matrix:
+    """J_k: coarse P1 macro-edge functions -> fine P1 on its two halves.
+
+    Coarse H_c(I,J) = fine H(2I,2J) u H(2I+1,2J); V_c(I,J) = V(2I,2J) u V(2I,2J+1)
+    (first half = lower coordinate).  Nodal evaluation at the fine nodes:
+    first half gets (c0, (c0+c1)/2), second half ((c0+c1)/2, c1).
+    """
+    nc = n // 2
+    rows, cols, vals = [], [], []
+    I, J = np.meshgrid(np.arange(nc), np.arange(nc + 1), indexing="xy")
+    I, J = I.ravel(), J.ravel()
+    halves = []
+    # horizontal coarse edges
+    ce = mesh.hedge(nc, I, J)
+    halves.append((ce, mesh.hedge(n, 2 * I, 2 * J), mesh.hedge(n, 2 * I + 1, 2 * J)))
+    I, J = np.meshgrid(np.arange(nc + 1), np.arange(nc), indexing="xy")
+    I, J = I.ravel(), J.ravel()
+    ce = mesh.vedge(nc, I, J)
+    halves.append((ce, mesh.vedge(n, 2 * I, 2 * J), mesh.vedge(n, 2 * I, 2 * J + 1)))
+    for ce, f0, f1 in halves:
+        c0, c1 = 2 * ce, 2 * ce + 1
+        entries = [(2 * f0, c0, 1.0), (2 * f0 + 1, c0, 0.5), (2 * f0 + 1, c1, 0.5),
+                   (2 * f1, c0, 0.5), (2 * f1, c1, 0.5), (2 * f1 + 1, c1, 1.0)]
+        for r, c, v in entries:
+            rows.append(r)
+            cols.append(c)
+            vals.append(np.full(len(r), v))
+    return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                         shape=(mesh.n_edges(n) * 2, mesh.n_edges(nc) * 2)).tocsr()
+
+
+def interior_edge_mask(n: int) -> np.ndarray:
+    """Fine edges interior to the 2x2 macro-elements of the coarser level:
+    vertical lines x = odd, horizontal lines y = odd (E_{k,I})."""
+    mask = np.zeros(mesh.n_edges(n), dtype=bool)
+    i = np.arange(n)
+    odd = np.arange(1, n, 2)
+    J, I = np.meshgrid(odd, i, indexing="ij")
+    mask[mesh.hedge(n, I.ravel(), J.ravel())] = True
+    J, I = np.meshgrid(i, odd, indexing="ij")
+    mask[mesh.vedge(n, I.ravel(), J.ravel())] = True
+    return mask
+
+
+def macro_interior_edges(n: int) -> np.ndarray:
+    """[nmacro, 4] interior fine edge ids per macro (I,J), macro id J*nc+I."""
+    nc = n // 2
+    J, I = np.divmod(np.arange(nc * nc), nc)
+    return np.stack([mesh.hedge(n, 2 * I, 2 * J + 1), mesh.hedge(n, 2 * I + 1, 2 * J + 1),
+                     mesh.vedge(n, 2 * I + 1, 2 * J), mesh.vedge(n, 2 * I + 1, 2 * J + 1)], axis=1)
+
+
+# --------------------------------------------------------------------------
+# levels
+# --------------------------------------------------------------------------
+
+class Level:
+    def __init__(self, n, p, A, free):
+        self.n, self.p = n, p
+        self.A = A.tocsr()
+        self.free = free                # full dof ids of the free dofs (sorted)
+        self.kind = None                # transfer to the coarser level: 'p' | 'h' | None
+        self.lam_max = None
+
+    @property
+    def k1(self):
+        return self.p + 1
+
+    # ---- edge blocks for block-Jacobi ----
+    def build_edge_blocks(self):
+        k = self.k1
+        nfe = len(self.free) // k
+        A = self.A
+        idx = np.arange(len(self.free)).reshape(nfe, k)
+        D = np.empty((nfe, k, k))
+        Ad = A.toarray() if A.shape[0] <= 4096 else None
+        for a in range(k):
+            for b in range(k):
+                if Ad is not None:
+                    D[:, a, b] = Ad[idx[:, a], idx[:, b]]
+                else:
+                    D[:, a, b] = np.asarray(A[idx[:, a], idx[:, b]]).ravel()
+        self.D = D
+
+    def apply_Dinv(self, r):
+        k = self.k1
+        return np.linalg.solve(self.D, r.reshape(-1, k, 1)).reshape(-1)
+
+    def apply_D(self, v):
+        k = self.k1
+        return np.einsum("eab,eb->ea", self.D, v.reshape(-1, k)).reshape(-1)
+
+
+def _block_inverse(A_II: sp.csr_matrix, blocks: np.ndarray) -> sp.csr_matrix:
+    """A_II^-1 for a block-diagonal A_II; `blocks` [nb, bs] are positions."""
+    nb, bs = blocks.shape
+    Ad = np.empty((nb, bs, bs))
+    for a in range(bs):
+        row = A_II[blocks[:, a]]
+        for b in range(bs):
+            Ad[:, a, b] = np.asarray(row[np.arange(nb), blocks[:, b]]).ravel()
+    inv = np.linalg.inv(Ad)
+    rows = np.repeat(blocks, bs, axis=1).ravel()
+    cols = np.tile(blocks, (1, bs)).ravel()
+    return sp.coo_matrix((inv.ravel(), (rows, cols)), shape=A_II.shape).tocsr()
+
+
+def _positions(sub: np.ndarray, full_sorted: np.ndarray) -> np.ndarray:
+    pos = np.searchsorted(full_sorted, sub)
+    assert np.all(full_sorted[pos] == sub)
+    return pos
+
+
+class Hierarchy:
+    """MG hierarchy from the finest trace operator A_N (free dofs)."""
+
+    def __init__(self, A_N, n, p, n_h_levels=0, smoother=BLOCK_JACOBI, nu_pre=2, nu_post=2,
+                 omega=1.0, cheb_ratio=30.0, lmax_iters=20, lmax_safety=1.05,
+                 step3=True, step5=False, nu_doubling=False, all_free=False):
+        self.smoother = smoother
+        self.nu_pre, self.nu_post = nu_pre, nu_post
+        self.omega = omega
+        self.cheb_ratio = cheb_ratio
+        self.step3, self.step5 = step3, step5
+        self.nu_doubling = nu_doubling
+        # all_free=True: no Dirichlet elimination (Neumann-type patch, used by
+        # the DtN pins); the coarsest operator is then singular (constants).
+        free_of = (lambda nn, pp: np.arange(mesh.n_edges(nn) * (pp + 1))) if all_free else mesh.free_dofs
+        self.all_free = all_free
+        levels = [Level(n, p, A_N, free_of(n, p))]
+        # p-coarsening: Eq. ANm1
+        if p > 1:
+            fine = levels[-1]
+            Jf = p_injection_full(n, p)
+            cfree = free_of(n, 1)
+            J = Jf[fine.free][:, cfree].tocsr()
+            fine.kind, fine.J = "p", J
+            levels.append(Level(n, 1, (J.T @ fine.A @ J).tocsr(), cfree))
+        # h-coarsening: Eq. Akm1 down to a 2x2 macro mesh (or n_h_levels)
+        nh = 0
+        while levels[-1].n > 2 and levels[-1].n % 2 == 0 and (n_h_levels <= 0 or nh < n_h_levels):
+            fine = levels[-1]
+            nf = fine.n
+            nc = nf // 2
+            dof_edge = fine.free // 2
+            imask = interior_edge_mask(nf)[dof_edge]
+            I_pos = np.nonzero(imask)[0]
+            B_pos = np.nonzero(~imask)[0]
+            A = fine.A
+            A_II = A[I_pos][:, I_pos].tocsr()
+            A_IB = A[I_pos][:, B_pos].tocsr()
+            A_BI = A[B_pos][:, I_pos].tocsr()
+            A_BB = A[B_pos][:, B_pos].tocsr()
+            # A_II is block diagonal over macros: 4 interior edges x 2 dofs each
+            medges = macro_interior_edges(nf)
+            mdofs = (medges[:, :, None] * 2 + np.arange(2)[None, None, :]).reshape(-1, 8)
+            blocks = _positions(mdofs.ravel(), fine.free[I_pos]).reshape(-1, 8)
+            AII_inv = _block_inverse(A_II, blocks)
+            cfree = free_of(nc, 1)
+            J = h_injection_full(nf)[fine.free[B_pos]][:, cfree].tocsr()
+            Ac = J.T @ (A_BB - A_BI @ AII_inv @ A_IB) @ J
+            fine.kind = "h"
+            fine.I_pos, fine.B_pos = I_pos, B_pos
+            fine.A_II, fine.A_IB, fine.A_BI, fine.A_BB = A_II, A_IB, A_BI, A_BB
+            fine.AII_inv, fine.J, fine.macro_blocks = AII_inv, J, blocks
+            levels.append(Level(nc, 1, Ac.tocsr(), cfree))
+            nh += 1
+        self.levels = levels                 # levels[0] = finest (k = N)
+        coarsest = levels[-1]
+        self.A1_dense = coarsest.A.toarray()
+        self.A1_chol = None if all_free else sla.cho_factor(self.A1_dense, lower=True)
+        for L in levels[:-1]:
+            L.build_edge_blocks()
+            if smoother == CHEBYSHEV:
+                L.lam_max = lmax_safety * self.estimate_lambda_max(L, lmax_iters)
+
+    # ---- Q11: power iteration on D_B^-1 A ----
+    @staticmethod
+    def estimate_lambda_max(L: Level, iters: int) -> float:
+        i = L.free
+        v = 1.0 + (i % 7) / 7.0
+        for _ in range(iters):
+            v = L.apply_Dinv(L.A @ v)
+            v = v / np.linalg.norm(v)
+        return float(v @ (L.A @ v)) / float(v @ L.apply_D(v))
+
+    @property
+    def N(self):
+        return len(self.levels)
+
+    # ---- transfers ----
+    def prolong(self, li, ec):
+        """I_k e_c (Eq. 3.3 / 3.4); li indexes self.levels (0 = finest)."""
+        L = self.levels[li]
+        if L.kind == "p":
+            return L.J @ ec
+        e = np.zeros(len(L.free))
+        eB = L.J @ ec
+        e[L.B_pos] = eB
+        e[L.I_pos] = -(L.AII_inv @ (L.A_IB @ eB))
+        return e
+
+    def restrict(self, li, r):
+        """Q_{k-1} r (Eq. 3.5 / 3.6) -- full formula incl. the interior term."""
+        L = self.levels[li]
+        if L.kind == "p":
+            return L.J.T @ r
+        rI, rB = r[L.I_pos], r[L.B_pos]
+        return L.J.T @ (rB - L.A_BI @ (L.AII_inv @ rI))
+
+    def local_correction(self, li, r):
+        """T_k r = [A_II^-1 r_I ; 0] (Eq. 3.11)."""
+        L = self.levels[li]
+        e = np.zeros(len(L.free))
+        e[L.I_pos] = L.AII_inv @ r[L.I_pos]
+        return e
+
+    def coarse_solve(self, r):
+        return sla.cho_solve(self.A1_chol, r)
+
+    # ---- smoothers G_{k,m} ----
+    def smooth(self, li, e, r, steps):
+        """`steps` smoothing iterations on A_k e = r starting from e."""
+        L = self.levels[li]
+        A = L.A
+        if self.smoother == BLOCK_JACOBI:
+            for _ in range(steps):
+                e = e + self.omega * L.apply_Dinv(r - A @ e)
+            return e
+        # Chebyshev on D^-1 A over [b/ratio, b] (O8)
+        b = L.lam_max
+        a = b / self.cheb_ratio
+        theta, delta = 0.5 * (b + a), 0.5 * (b - a)
+        sigma = theta / delta
+        rho = 1.0 / sigma
+        d = L.apply_Dinv(r - A @ e) / theta
+        e = e + d
+        for _ in range(1, steps):
+            rho_new = 1.0 / (2.0 * sigma - rho)
+            d = rho_new * rho * d + (2.0 * rho_new / delta) * L.apply_Dinv(r - A @ e)
+            e = e + d
+            rho = rho_new
+        return e
+
+    def _nu(self, li, nu):
+        if not self.nu_doubling:
+            return nu
+        return nu * (2 ** li)       # m_{k-1} = 2 m_k (beta_0 = beta_1 = 2)
+
+    # ---- Algorithm 1 ----
+    def vcycle(self, r, li=0):
+        """B_k(r_k), Algorithm 1 steps 1-6 (step 5 only if self.step5)."""
+        if li == self.N - 1:
+            return self.coarse_solve(r)
+        L = self.levels[li]
+        A = L.A
+        e = np.zeros_like(r)                                          # step 1
+        e = self.smooth(li, e, r, self._nu(li, self.nu_pre))          # step 2
+        has_interior = L.kind == "h"
+        if has_interior and self.step3:
+            e = e + self.local_correction(li, r - A @ e)              # step 3
+        ec = self.vcycle(self.restrict(li, r - A @ e), li + 1)        # step 4
+        e = e + self.prolong(li, ec)
+        if has_interior and self.step5:
+            e = e + self.local_correction(li, r - A @ e)              # step 5
+        e = self.smooth(li, e, r, self._nu(li, self.nu_post))         # step 6
+        return e
