@@ -1,0 +1,213 @@
+/*
+ * mgdtn.h -- C ABI of the B200-native DtN geometric multigrid for hybridized
+ * high-order finite elements (Wildey, Muralikrishnan, Bui-Thanh,
+ * arXiv:1811.09909, "Unified geometric multigrid algorithm for hybridized
+ * high-order finite element methods").
+ *
+ * The library solves the trace (skeleton) system  A lambda = g  (PAPER.md:321-325,
+ * Eq. `trace_linear_system`) of  -div(K grad q) = f,  q = g_D on dOmega
+ * (Eq. `primal_elliptic`) on a structured nx x ny mesh of
+ * squares, with CG preconditioned by one multigrid V-cycle (Algorithm 1,
+ * PAPER.md:941-963) whose coarse operators and transfers are built only from
+ * the fine-scale element DtN maps.
+ *
+ * Conventions (all functions):
+ *   - Return an int status: MG_OK (0) or a negative MG_ERR_*; never abort,
+ *     never throw across the ABI.  mg_last_error() gives a message,
+ *     mg_last_error_index() the offending element / edge (or -1).
+ *   - Array arguments are DEVICE pointers owned by the caller and borrowed
+ *     for the duration of the call, unless the name ends in _host.
+ *   - All device work is issued on the ctx stream (mg_build_hierarchy's
+ *     `cuda_stream`, a cudaStream_t or NULL = legacy default stream).
+ *     mg_apply / mg_vcycle / mg_assemble_rhs / mg_setup_dtn are asynchronous;
+ *     mg_pcg_solve and the *_host calls synchronise the stream.
+ *   - The library allocates no device memory: everything lives in one
+ *     caller-allocated workspace (mg_workspace_bytes / mg_bind_workspace)
+ *     that must stay alive until mg_destroy.
+ *
+ * Numbering (layout contract of every trace vector):
+ *   element (i,j), 0<=i<nx, 0<=j<ny: id = j*nx + i
+ *   horizontal edge H(i,j), 0<=i<nx, 0<=j<=ny: id = j*nx + i
+ *   vertical   edge V(i,j), 0<=i<=nx, 0<=j<ny: id = nx*(ny+1) + j*(nx+1) + i
+ *   trace dof (edge e, node a) = e*(p_k+1) + a; nodes are the GLL points of the
+ *   edge in its global orientation (+x for horizontal, +y for vertical).
+ *   A level-k vector has nedges_k*(p_k+1) doubles; entries on dOmega are
+ *   Dirichlet: ignored on input and written as 0 by mg_apply / mg_vcycle /
+ *   mg_pcg_solve (the Dirichlet values themselves come from mg_assemble_rhs).
+ *
+ * Levels use the paper's numbering: level N (= mg_num_levels) is the finest
+ * (order p); if p > 1 level N-1 is the P1 space on the same mesh (p-coarsening,
+ * PAPER.md:383-407); below that each level agglomerates 2x2 macro-elements
+ * down to level 1 (a 2x2 macro mesh, 8 dofs, unless
+ * n_h_levels stops earlier).  Level 1 is solved directly.
+ */
+#ifndef MGDTN_H
+#define MGDTN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors are negative) ---- */
+enum {
+  MG_OK = 0,
+  MG_ERR_ARG = -1,              /* bad argument (NULL, out of range) */
+  MG_ERR_SHAPE = -2,            /* mesh not coarsenable / sizes inconsistent */
+  MG_ERR_SINGULAR_LOCAL = -3,   /* a local (element) solve broke down */
+  MG_ERR_NOT_SPD = -4,          /* Cholesky of a local block / edge block / A_1 failed */
+  MG_ERR_CUDA = -5,             /* CUDA runtime error (message has the CUDA string) */
+  MG_ERR_NCCL = -6,             /* reserved: multi-GPU communicator error */
+  MG_ERR_STATE = -7,            /* call order violated (e.g. solve before setup) */
+  MG_ERR_WORKSPACE = -8,        /* workspace missing, too small or misaligned */
+  MG_ERR_UNSUPPORTED = -9       /* valid request this build does not implement */
+};
+
+/* ---- solve outcomes (not errors; SPEC krylov "returns a status, never panics") ---- */
+enum { MG_CONVERGED = 0, MG_MAXIT = 1, MG_DIVERGED = 2, MG_BREAKDOWN = 3 };
+
+/* ---- hybridized method per element ---- */
+enum { MG_HDG = 0,      /* Eqs. HDG, HDG_flux */
+       MG_SIPG_H = 1 }; /* Eq. SIPG_H, s_f = 1 */
+
+/* ---- smoothers ---- */
+enum { MG_SMOOTH_BLOCK_JACOBI = 0,  /* edge blocks, e += omega D_B^-1 (r - A e) */
+       MG_SMOOTH_CHEBYSHEV = 1 };   /* Chebyshev on D_B^-1 A over [lmax/ratio, lmax] */
+
+/* Structured mesh of nx x ny squares of side h with lower-left corner (x0,y0).
+ * nx and ny must be even and divisible by 2^(number of h-levels). */
+typedef struct {
+  int32_t nx, ny;
+  double x0, y0, h;
+} mg_quad_mesh;
+
+/* Element-block partition for multi-GPU runs (reserved; NULL or nranks == 1
+ * selects the single-GPU path, the only one this build implements). */
+typedef struct {
+  int32_t rank, nranks, px, py;
+  const uint8_t* nccl_id;
+} mg_partition;
+
+/* Smoother configuration.  V(nu_pre, nu_post); the Chebyshev "steps" are the
+ * polynomial degree.  lambda_max of D_B^-1 A_k is estimated per level by
+ * `lmax_iters` power iterations from v_i = 1 + (i mod 7)/7 (i = global dof
+ * id), Rayleigh quotient in the D_B inner product, times `lmax_safety`
+ * (SURVEY.md 8(c) Q11).  omega applies to block-Jacobi only (paper: 1). */
+typedef struct {
+  int32_t kind;
+  int32_t nu_pre, nu_post;      /* 0 <= nu <= 8 */
+  double omega;                 /* block-Jacobi damping, default 1 */
+  double cheb_ratio;            /* lambda_min = lambda_max / ratio, default 30 */
+  int32_t lmax_iters;           /* default 20 */
+  double lmax_safety;           /* default 1.05 */
+} mg_smoother_cfg;
+
+/* Build the level structure (host only; no device work).  p in 1..4.
+ * n_h_levels = 0 coarsens until the macro mesh is 2 x 2 (or until a side
+ * becomes odd).  Errors: MG_ERR_ARG, MG_ERR_SHAPE, MG_ERR_UNSUPPORTED
+ * (partition with nranks > 1, nx != ny layouts the coarsening cannot reach). */
+int mg_build_hierarchy(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
+                       const mg_partition* part, void* cuda_stream, void** out_ctx);
+
+/* Bytes of device workspace the ctx needs (256-byte aligned pointer). */
+int mg_workspace_bytes(const void* ctx, size_t* bytes);
+
+/* Bind the caller-allocated device workspace (kept alive until mg_destroy). */
+int mg_bind_workspace(void* ctx, void* dev_ptr, size_t bytes);
+
+/* Batched element-local setup and the whole hierarchy (PAPER.md:305-316,
+ * 572-811, 1050-1067):
+ *   per element: local static condensation -> DtN map S_T (FP64),
+ *   p-coarsening S_T^(1) = J_p^T S_T J_p (Eq. ANm1),
+ *   per 2x2 agglomerate: A_II^-1, P_M = -A_II^-1 A_IB J, coarse DtN (Eq. Akm1),
+ *   edge-block diagonals D_e^-1, Chebyshev lambda_max, coarsest A_1^-1.
+ * K[ne] > 0 (scalar permeability per element), method[ne] in {MG_HDG,
+ * MG_SIPG_H}, tau[ne] > 0 (stabilisation of the element's own flux,
+ * Eq. HDG_flux / IPDG_flux), all device arrays in element-id order.
+ * Errors: MG_ERR_NOT_SPD / MG_ERR_SINGULAR_LOCAL with the element index
+ * (detected asynchronously; reported by the next synchronising call). */
+int mg_setup_dtn(void* ctx, const double* K, const int8_t* method, const double* tau,
+                 const mg_smoother_cfg* smoother);
+
+/* Right-hand side of the trace system and the Dirichlet trace values.
+ * f_qp: [ne][nq][nq] samples of f at the tensor Gauss-Legendre points of each
+ *   element (nq = p+4 per direction, point order [qy][qx]), or NULL -> f = f_const.
+ * gD_qp: [2*nx+2*ny][nq] samples of g_D on the boundary edges (order: bottom
+ *   H(i,0) i=0..nx-1, top H(i,ny), left V(0,j) j=0..ny-1, right V(nx,j); nq
+ *   Gauss points along the edge's global orientation), or NULL -> g_D = 0.
+ * Outputs (device, ndof_N doubles each):
+ *   g: sum_T G_T^T b_T - A_FD lambda_D on free dofs, 0 on dOmega;
+ *   lambda_bc: per-edge L2 projection of g_D on dOmega (reading Q4), 0 elsewhere
+ *   (may be NULL).  The full trace solution is lambda_free + lambda_bc. */
+int mg_assemble_rhs(void* ctx, const double* f_qp, double f_const, const double* gD_qp,
+                    double* g, double* lambda_bc);
+
+/* y = A_level x (level in 1..N), x, y device [ndof_level], x != y. */
+int mg_apply(void* ctx, int32_t level, const double* x, double* y);
+
+/* z = B_N r: one V-cycle of Algorithm 1 with the step-3 local correction
+ * from e = 0.  r, z device [ndof_N]. */
+int mg_vcycle(void* ctx, const double* r, double* z);
+
+/* Per-operator entry points (for parity checks of single steps):
+ *   mg_smooth:        e <- nsteps smoother iterations on A_level e = r (in place)
+ *   mg_local_correct: e += T_k res  (Eq. 3.11; level must have a coarser h-level)
+ *   mg_restrict:      rc = Q_{k-1} res  (Eqs. 3.5/3.6, full formula)
+ *   mg_prolong:       e += I_k ec       (Eqs. 3.3/3.4)
+ * level = k (the finer of the two levels for restrict/prolong). */
+int mg_smooth(void* ctx, int32_t level, const double* r, double* e, int32_t nsteps);
+int mg_local_correct(void* ctx, int32_t level, const double* res, double* e);
+int mg_restrict(void* ctx, int32_t level, const double* res, double* rc);
+int mg_prolong(void* ctx, int32_t level, const double* ec, double* e);
+
+/* MG-preconditioned CG on A lambda = g from lambda_0 = 0 (north star).
+ * Stops when ||r_k||_2 <= rtol ||g||_2 (recursive residual, free dofs;
+ * PAPER.md:1012-1015 normalisation) or after maxit iterations.
+ * g, lambda: device [ndof_N].  Host outputs (may be NULL): iters, relres
+ * (recursive), solve_status (MG_CONVERGED / MG_MAXIT / MG_DIVERGED /
+ * MG_BREAKDOWN), resid_hist [maxit+1].  Synchronises the stream. */
+int mg_pcg_solve(void* ctx, const double* g, double* lambda, double rtol, int32_t maxit,
+                 int32_t* iters, double* relres, int32_t* solve_status, double* resid_hist);
+
+/* The whole user call with HOST buffers: copy K/method/tau/f/g_D to the
+ * device, setup, rhs, PCG, copy the full trace solution (free + Dirichlet)
+ * back.  lambda_host [ndof_N].  f_qp_host / gD_qp_host may be NULL. */
+int mg_solve_host(void* ctx, const double* K_host, const int8_t* method_host,
+                  const double* tau_host, const double* f_qp_host, double f_const,
+                  const double* gD_qp_host, const mg_smoother_cfg* smoother, double rtol,
+                  int32_t maxit, double* lambda_host, int32_t* iters, double* relres,
+                  int32_t* solve_status);
+
+/* Device staging for mg_solve_host (inputs + outputs of one call):
+ * bytes for K, tau, method, g, lambda and, if requested, the f / g_D samples. */
+int mg_staging_bytes(const void* ctx, int32_t with_f, int32_t with_gD, size_t* bytes);
+int mg_bind_staging(void* ctx, void* dev_ptr, size_t bytes);
+
+/* Introspection. */
+int mg_num_levels(const void* ctx, int32_t* nlevels);
+int mg_level_info(const void* ctx, int32_t level, int32_t* nx, int32_t* ny, int32_t* p,
+                  int64_t* ndof);
+/* Element DtN maps of a level as dense [ne][m][m] (m = 4(p_k+1)), element-id
+ * order (dst device).  mg_debug_set_element_dtn overwrites them (test hook;
+ * the symmetric part's upper triangle is what is stored). */
+int mg_copy_element_dtn(const void* ctx, int32_t level, double* dst);
+int mg_debug_set_element_dtn(void* ctx, int32_t level, const double* src);
+/* Chebyshev lambda_max estimate of a level (host out; 0 if not Chebyshev). */
+int mg_level_lambda_max(const void* ctx, int32_t level, double* lam);
+/* Number of kernel launches issued by the last mg_pcg_solve (timing claims). */
+int mg_last_launch_count(const void* ctx, int64_t* launches);
+/* Kernel launches issued through this ctx since it was built. */
+int mg_total_launch_count(const void* ctx, int64_t* launches);
+/* 1 (default): replay each PCG iteration as two captured CUDA graphs; 0: eager launches. */
+int mg_set_use_graphs(void* ctx, int32_t on);
+
+const char* mg_last_error(const void* ctx);
+int64_t mg_last_error_index(const void* ctx);
+void mg_destroy(void* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MGDTN_H */

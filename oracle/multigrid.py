@@ -196,7 +196,9 @@ class Hierarchy:
             levels.append(Level(n, 1, (J.T @ fine.A @ J).tocsr(), cfree))
         # h-coarsening: Eq. Akm1 down to a 2x2 macro mesh (or n_h_levels)
         nh = 0
-        while levels[-1].n > 2 and levels[-1].n % 2 == 0 and (n_h_levels <= 0 or nh < n_h_levels):
+        # agglomerate while the coarse mesh stays even (n % 4 == 0) -- a 2x2
+        # macro mesh at the bottom for n = 2^L (reading Q14)
+        while levels[-1].n > 2 and levels[-1].n % 4 == 0 and (n_h_levels <= 0 or nh < n_h_levels):
             fine = levels[-1]
             nf = fine.n
             nc = nf // 2

@@ -1,0 +1,11 @@
+"""B200-native DtN geometric multigrid for hybridized high-order FEM
+(arXiv:1811.09909): MG-V-cycle-preconditioned CG on the trace system, all
+steps in hand-written sm_100a CUDA kernels behind the C ABI include/mgdtn.h.
+
+    from paper_1811_09909_b200 import MGSolver, SmootherConfig
+"""
+from .mgdtn import (MG_HDG, MG_SIPG_H, MG_SMOOTH_BLOCK_JACOBI, MG_SMOOTH_CHEBYSHEV, LIB_PATH,
+                    MGError, MGSolver, SmootherConfig, load_library, smoother_from_config)
+
+__all__ = ["MGSolver", "SmootherConfig", "MGError", "load_library", "LIB_PATH", "MG_HDG",
+           "MG_SIPG_H", "MG_SMOOTH_BLOCK_JACOBI", "MG_SMOOTH_CHEBYSHEV", "smoother_from_config"]

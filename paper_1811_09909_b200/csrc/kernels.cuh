@@ -1,0 +1,175 @@
+// Device data layout, indexing helpers and kernel launchers (sm_100a, FP64).
+//
+// Element DtN maps of a level are stored packed-symmetric (upper triangle,
+// row-major, npk = m(m+1)/2 entries, m = 4(p+1)) and element-interleaved in
+// chunks of 32 same-colour elements:
+//     S[((colour*nchunk + chunk)*npk + kk)*32 + lane]
+// so that one warp-wide load of entry kk of 32 consecutive elements is one
+// contiguous 256-byte segment.  Colour = (i+j) mod 2 (checkerboard: elements of
+// one colour share no edge), index within the colour s = j*(nx/2) + (i>>1),
+// chunk = s/32, lane = s%32.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mgdtn {
+
+constexpr int MAX_NU = 8;      // max smoothing steps per side
+constexpr int MAX_K1 = 5;      // p <= 4
+
+// smoothing update modes of the colour-1 apply pass
+enum ApplyMode : int {
+  AM_W0 = 0,      // pass 0: y[e] = (S_T x_T)[e]
+  AM_APPLY = 1,   // pass 1: y[e] += (S_T x_T)[e]  (+ optional dot x.y)
+  AM_RESID = 2,   // pass 1: w[e] = r[e] - (w[e] + (S_T x_T)[e])
+  AM_SMOOTH = 3   // pass 1: d = c1 d + c2 Dinv (r - A x)_e ; x[e] += d  (in place)
+};
+
+struct LevelDev {
+  int nx, ny, p, k1, m, npk;
+  int64_t ne, nedge, ndof;
+  int nchunk;              // chunks of 32 per colour
+  double* S;               // interleaved packed DtN
+  double* Dinv;            // [nedge][k1*k1]
+  double* coef;            // [2*MAX_NU] smoothing coefficients (c1_j, c2_j), device
+  int smoother;            // 0 BJ, 1 Chebyshev (d vector used)
+};
+
+// ---------------------------------------------------------------- indexing
+__host__ __device__ __forceinline__ int64_t hedge(int nx, int i, int j) {
+  return (int64_t)j * nx + i;
+}
+__host__ __device__ __forceinline__ int64_t vedge(int nx, int ny, int i, int j) {
+  return (int64_t)nx * (ny + 1) + (int64_t)j * (nx + 1) + i;
+}
+__host__ __device__ __forceinline__ int pk_index(int i, int j, int m) {  // i <= j
+  return i * (2 * m - i + 1) / 2 + (j - i);
+}
+__host__ __device__ __forceinline__ int64_t s_offset(int nchunk, int npk, int colour, int64_t s,
+                                                     int kk) {
+  int64_t chunk = s >> 5;
+  int lane = (int)(s & 31);
+  return (((int64_t)colour * nchunk + chunk) * npk + kk) * 32 + lane;
+}
+// element (i,j) -> (colour, s)
+__host__ __device__ __forceinline__ void elem_slot(int nx, int i, int j, int& colour,
+                                                   int64_t& s) {
+  colour = (i + j) & 1;
+  s = (int64_t)j * (nx >> 1) + (i >> 1);
+}
+// (colour, s) -> element (i,j)
+__host__ __device__ __forceinline__ void slot_elem(int nx, int colour, int64_t s, int& i,
+                                                   int& j) {
+  int nxh = nx >> 1;
+  j = (int)(s / nxh);
+  i = 2 * (int)(s - (int64_t)j * nxh) + ((j + colour) & 1);
+}
+// the 4 edges {bottom, right, top, left} of element (i,j) and their dOmega flags
+__host__ __device__ __forceinline__ void elem_edges(int nx, int ny, int i, int j, int64_t e[4],
+                                                    bool bd[4]) {
+  e[0] = hedge(nx, i, j);
+  e[1] = vedge(nx, ny, i + 1, j);
+  e[2] = hedge(nx, i, j + 1);
+  e[3] = vedge(nx, ny, i, j);
+  bd[0] = (j == 0);
+  bd[1] = (i == nx - 1);
+  bd[2] = (j == ny - 1);
+  bd[3] = (i == 0);
+}
+// edge id -> is it on dOmega
+__host__ __device__ __forceinline__ bool edge_on_boundary(int nx, int ny, int64_t e) {
+  int64_t nh = (int64_t)nx * (ny + 1);
+  if (e < nh) {
+    int j = (int)(e / nx);
+    return j == 0 || j == ny;
+  }
+  int64_t r = e - nh;
+  int i = (int)(r % (nx + 1));
+  return i == 0 || i == nx;
+}
+
+// ---------------------------------------------------------------- device error slot
+struct DevError {
+  int code;        // 0 = none, else MG_ERR_*
+  int pad;
+  long long index; // element / edge index
+};
+__device__ __forceinline__ void report_error(DevError* err, int code, long long index) {
+  if (atomicCAS(&err->code, 0, code) == 0) err->index = index;
+}
+
+// reference tables on the device (one set per p)
+struct RefDev {
+  int p, k1, nv, m, nqf;
+  const double *G, *F, *P, *E, *W, *H, *LN, *Nl, *fq, *ew, *H1inv, *Jp;
+};
+
+// ---------------------------------------------------------------- launchers
+// all launchers return the number of kernels launched (for launch counting)
+int launch_apply(const LevelDev& L, int colour, int mode, const double* x, double* y,
+                 const double* r, double* d, int step, double* partials, int dot_grid,
+                 cudaStream_t st);
+int apply_grid(const LevelDev& L);   // blocks of the colour passes (partials length)
+
+int launch_local_dtn(const LevelDev& L, const RefDev& R, double h, const double* K,
+                     const int8_t* method, const double* tau, DevError* err, cudaStream_t st);
+int launch_local_rhs(const LevelDev& L, const RefDev& R, double h, const double* K,
+                     const int8_t* method, const double* tau, const double* f_qp,
+                     double f_const, const double* lamD, double* g, DevError* err,
+                     cudaStream_t st);
+int launch_dirichlet(const LevelDev& L, const RefDev& R, const double* gD_qp, double* lamD,
+                     cudaStream_t st);
+int launch_p_coarsen(const LevelDev& F, const LevelDev& C, const double* Jp, cudaStream_t st);
+int launch_agglomerate(const LevelDev& F, const LevelDev& C, double* KIIinv, double* Pm,
+                       DevError* err, cudaStream_t st);
+int launch_edge_blocks(const LevelDev& L, DevError* err, cudaStream_t st);
+int launch_dense_to_packed(const LevelDev& L, const double* src, cudaStream_t st);
+int launch_packed_to_dense(const LevelDev& L, double* dst, cudaStream_t st);
+
+// MG transfer / smoothing kernels
+int launch_smooth_first(const LevelDev& L, const double* r, double* e, double* d,
+                        cudaStream_t st);
+int launch_lc_restrict(const LevelDev& F, const double* res, double* e, const double* KIIinv,
+                       const double* Pm, double* cbuf, bool do_lc, bool do_restrict,
+                       cudaStream_t st);
+int launch_restrict_edges(const LevelDev& F, const LevelDev& C, const double* res,
+                          const double* cbuf, double* rc, bool fuse_first, double* ec,
+                          double* dc, cudaStream_t st);
+int launch_prolong_macro(const LevelDev& F, const LevelDev& C, const double* ec,
+                         const double* Pm, double* e, cudaStream_t st);
+int launch_p_restrict(const LevelDev& F, const LevelDev& C, const double* Jp,
+                      const double* res, double* rc, bool fuse_first, double* ec, double* dc,
+                      cudaStream_t st);
+int launch_p_prolong(const LevelDev& F, const double* Jp, const double* ec, double* e,
+                     cudaStream_t st);
+int launch_coarse_assemble_factor(const LevelDev& L, const int* fpos, int nf, double* A1,
+                                  double* A1inv, DevError* err, cudaStream_t st);
+int launch_coarse_solve(const LevelDev& L, const int* fidx, int nf, const double* A1inv,
+                        const double* r, double* e, cudaStream_t st);
+
+// vectors / reductions (grid-stride, deterministic two-stage reductions)
+int vec_grid(int64_t n);
+int launch_dot(const double* a, const double* b, int64_t n, double* partials, int grid,
+               cudaStream_t st);
+// out[slot] = sum(partials[0:n]); then op: 0 none, 1 alpha = s[0]/sum (breakdown check),
+// 2 beta = sum/s[0] and s[0] = sum
+int launch_reduce(const double* partials, int n, double* scal, int slot, int op,
+                  DevError* err, cudaStream_t st);
+int launch_pcg_update(double* x, double* r, const double* p, const double* ap,
+                      const double* scal, int64_t n, double* partials, int grid,
+                      cudaStream_t st);
+int launch_pcg_pupdate(double* p, const double* z, const double* scal, int64_t n,
+                       cudaStream_t st);
+int launch_pow_init(const LevelDev& L, double* v, cudaStream_t st);
+int launch_edge_dinv(const LevelDev& L, const double* y, double* u, double* partials,
+                     int grid, cudaStream_t st);
+int launch_scale_by_norm(double* v, const double* u, int64_t n, const double* scal, int slot,
+                         cudaStream_t st);
+int launch_lmax_finish(const double* scal, double safety, double ratio, int nu_max,
+                       double* lam_out, double* coef, cudaStream_t st);
+int launch_set_bj_coef(double omega, double* coef, cudaStream_t st);
+int launch_copy(double* dst, const double* src, int64_t n, cudaStream_t st);
+int launch_zero(double* dst, int64_t n, cudaStream_t st);
+int launch_add(double* dst, const double* src, int64_t n, cudaStream_t st);
+
+}  // namespace mgdtn

@@ -1,0 +1,914 @@
+// C-ABI implementation (include/mgdtn.h): level structure, workspace carve-up,
+// setup sequence, V-cycle (Algorithm 1), PCG driver and the
+// CUDA-graph capture of the per-iteration kernel sequences.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mgdtn.h"
+#include "kernels.cuh"
+#include "refelem.h"
+
+namespace mgdtn {
+
+enum LevelKind { KIND_COARSEST = 0, KIND_P = 1, KIND_H = 2 };
+
+struct HostLevel {
+  LevelDev d{};
+  int kind = KIND_COARSEST;
+  double h = 0.0;
+  size_t o_S = 0, o_Dinv = 0, o_coef = 0, o_lam = 0, o_r = 0, o_e = 0, o_w = 0, o_d = 0;
+  size_t o_KIIinv = 0, o_Pm = 0, o_cbuf = 0;
+  double *KIIinv = nullptr, *Pm = nullptr, *cbuf = nullptr;
+  double *r = nullptr, *e = nullptr, *w = nullptr, *dv = nullptr, *lam = nullptr;
+};
+
+struct Ctx {
+  mg_quad_mesh mesh{};
+  int p = 1;
+  std::vector<HostLevel> lev;   // lev[0] = finest (paper's level N)
+  cudaStream_t st = nullptr;
+  RefTables ref;
+  size_t ref_doubles = 0;
+  // workspace
+  char* ws = nullptr;
+  size_t ws_bytes = 0, ws_need = 0;
+  size_t o_err = 0, o_ref = 0, o_part = 0, o_scal = 0, o_sscal = 0, o_x = 0, o_p = 0, o_ap = 0,
+         o_lamD = 0, o_g = 0, o_fpos = 0, o_fidx = 0, o_A1 = 0, o_A1inv = 0, o_K = 0, o_tau = 0,
+         o_meth = 0;
+  int nf = 0;
+  int npart = 0;
+  RefDev refdev{};
+  DevError* err = nullptr;
+  double *part = nullptr, *scal = nullptr, *sscal = nullptr, *x = nullptr, *pv = nullptr,
+         *ap = nullptr, *lamD = nullptr, *gbuf = nullptr, *A1 = nullptr, *A1inv = nullptr;
+  int *fpos = nullptr, *fidx = nullptr;
+  double *Kc = nullptr, *tauc = nullptr;   // internal copies of the element data (rhs)
+  int8_t* methc = nullptr;
+  // staging for mg_solve_host
+  char* stg = nullptr;
+  size_t stg_bytes = 0;
+  // state
+  bool setup_done = false;
+  mg_smoother_cfg sm{};
+  std::string last_err;
+  long long last_idx = -1;
+  long long launches = 0, last_solve_launches = 0;
+  double* pinned = nullptr;
+  cudaGraphExec_t gA = nullptr, gB = nullptr;
+  long long nA = 0, nB = 0;       // kernels per graph
+  bool use_graphs = true;
+};
+
+static int fail(Ctx* c, int code, const std::string& msg, long long idx = -1) {
+  if (c) {
+    c->last_err = msg;
+    c->last_idx = idx;
+  }
+  return code;
+}
+
+static int cuda_check(Ctx* c, cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return MG_OK;
+  return fail(c, MG_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr)                                   \
+  do {                                             \
+    int _rc = cuda_check(c, (expr), #expr);        \
+    if (_rc != MG_OK) return _rc;                  \
+  } while (0)
+
+#define RC(expr)                                   \
+  do {                                             \
+    int _rc = (expr);                              \
+    if (_rc != MG_OK) return _rc;                  \
+  } while (0)
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// ---------------------------------------------------------------- hierarchy
+static void init_level(HostLevel& L, int nx, int ny, int p, double h, int kind) {
+  LevelDev& d = L.d;
+  d.nx = nx;
+  d.ny = ny;
+  d.p = p;
+  d.k1 = p + 1;
+  d.m = 4 * (p + 1);
+  d.npk = d.m * (d.m + 1) / 2;
+  d.ne = (int64_t)nx * ny;
+  d.nedge = (int64_t)nx * (ny + 1) + (int64_t)(nx + 1) * ny;
+  d.ndof = d.nedge * d.k1;
+  d.nchunk = (int)((d.ne / 2 + 31) / 32);
+  L.h = h;
+  L.kind = kind;
+}
+
+static void layout(Ctx* c) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + (bytes ? bytes : 8));
+    return o;
+  };
+  c->o_err = take(sizeof(DevError));
+  c->o_ref = take(c->ref_doubles * sizeof(double));
+  c->npart = 2 * 148 * 8 + 64;
+  c->o_part = take((size_t)c->npart * sizeof(double));
+  c->o_scal = take(16 * sizeof(double));
+  c->o_sscal = take(16 * sizeof(double));
+  const int64_t ndofN = c->lev[0].d.ndof;
+  c->o_x = take(ndofN * sizeof(double));
+  c->o_p = take(ndofN * sizeof(double));
+  c->o_ap = take(ndofN * sizeof(double));
+  c->o_lamD = take(ndofN * sizeof(double));
+  c->o_g = take(ndofN * sizeof(double));
+  c->o_K = take(c->lev[0].d.ne * sizeof(double));
+  c->o_tau = take(c->lev[0].d.ne * sizeof(double));
+  c->o_meth = take(c->lev[0].d.ne * sizeof(int8_t));
+  for (auto& L : c->lev) {
+    const LevelDev& d = L.d;
+    L.o_S = take((size_t)2 * d.nchunk * d.npk * 32 * sizeof(double));
+    L.o_Dinv = take((size_t)d.nedge * d.k1 * d.k1 * sizeof(double));
+    L.o_coef = take(2 * MAX_NU * sizeof(double));
+    L.o_lam = take(sizeof(double));
+    L.o_r = take(d.ndof * sizeof(double));
+    L.o_e = take(d.ndof * sizeof(double));
+    L.o_w = take(d.ndof * sizeof(double));
+    L.o_d = take(d.ndof * sizeof(double));
+    if (L.kind == KIND_H) {
+      int64_t nmac = (int64_t)(d.nx / 2) * (d.ny / 2);
+      L.o_KIIinv = take(nmac * 64 * sizeof(double));
+      L.o_Pm = take(nmac * 64 * sizeof(double));
+      L.o_cbuf = take(nmac * 8 * sizeof(double));
+    }
+  }
+  const HostLevel& C1 = c->lev.back();
+  c->o_fpos = take(C1.d.ndof * sizeof(int));
+  c->o_fidx = take((size_t)c->nf * sizeof(int));
+  c->o_A1 = take((size_t)c->nf * c->nf * sizeof(double));
+  c->o_A1inv = take((size_t)c->nf * c->nf * sizeof(double));
+  c->ws_need = off;
+}
+
+static void bind_pointers(Ctx* c) {
+  char* b = c->ws;
+  auto D = [&](size_t o) { return reinterpret_cast<double*>(b + o); };
+  c->err = reinterpret_cast<DevError*>(b + c->o_err);
+  c->part = D(c->o_part);
+  c->scal = D(c->o_scal);
+  c->sscal = D(c->o_sscal);
+  c->x = D(c->o_x);
+  c->pv = D(c->o_p);
+  c->ap = D(c->o_ap);
+  c->lamD = D(c->o_lamD);
+  c->gbuf = D(c->o_g);
+  c->fpos = reinterpret_cast<int*>(b + c->o_fpos);
+  c->fidx = reinterpret_cast<int*>(b + c->o_fidx);
+  c->A1 = D(c->o_A1);
+  c->A1inv = D(c->o_A1inv);
+  c->Kc = D(c->o_K);
+  c->tauc = D(c->o_tau);
+  c->methc = reinterpret_cast<int8_t*>(b + c->o_meth);
+  for (auto& L : c->lev) {
+    L.d.S = D(L.o_S);
+    L.d.Dinv = D(L.o_Dinv);
+    L.d.coef = D(L.o_coef);
+    L.lam = D(L.o_lam);
+    L.r = D(L.o_r);
+    L.e = D(L.o_e);
+    L.w = D(L.o_w);
+    L.dv = D(L.o_d);
+    if (L.kind == KIND_H) {
+      L.KIIinv = D(L.o_KIIinv);
+      L.Pm = D(L.o_Pm);
+      L.cbuf = D(L.o_cbuf);
+    }
+  }
+  // reference tables
+  double* R = D(c->o_ref);
+  const RefTables& T = c->ref;
+  size_t o = 0;
+  auto put = [&](const std::vector<double>& v) {
+    const double* p = R + o;
+    o += v.size();
+    return p;
+  };
+  RefDev& rd = c->refdev;
+  rd.p = T.p;
+  rd.k1 = T.k1;
+  rd.nv = T.nv;
+  rd.m = T.m;
+  rd.nqf = T.nqf;
+  rd.G = put(T.G);
+  rd.F = put(T.F);
+  rd.P = put(T.P);
+  rd.E = put(T.E);
+  rd.W = put(T.W);
+  rd.H = put(T.H);
+  rd.LN = put(T.LN);
+  rd.Nl = put(T.Nl);
+  rd.fq = put(T.fq);
+  rd.ew = put(T.ew);
+  rd.H1inv = put(T.H1inv);
+  rd.Jp = put(T.Jp);
+}
+
+static int upload_static(Ctx* c) {
+  // reference tables
+  std::vector<double> all;
+  const RefTables& T = c->ref;
+  for (const auto* v : {&T.G, &T.F, &T.P, &T.E, &T.W, &T.H, &T.LN, &T.Nl, &T.fq, &T.ew, &T.H1inv,
+                        &T.Jp})
+    all.insert(all.end(), v->begin(), v->end());
+  CK(cudaMemcpyAsync(c->ws + c->o_ref, all.data(), all.size() * sizeof(double),
+                     cudaMemcpyHostToDevice, c->st));
+  // coarsest free-dof maps
+  const LevelDev& d = c->lev.back().d;
+  std::vector<int> fpos(d.ndof, -1), fidx;
+  for (int64_t e = 0; e < d.nedge; ++e) {
+    if (edge_on_boundary(d.nx, d.ny, e)) continue;
+    for (int a = 0; a < d.k1; ++a) {
+      fpos[e * d.k1 + a] = (int)fidx.size();
+      fidx.push_back((int)(e * d.k1 + a));
+    }
+  }
+  CK(cudaMemcpyAsync(c->fpos, fpos.data(), fpos.size() * sizeof(int), cudaMemcpyHostToDevice,
+                     c->st));
+  if (!fidx.empty())
+    CK(cudaMemcpyAsync(c->fidx, fidx.data(), fidx.size() * sizeof(int), cudaMemcpyHostToDevice,
+                       c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return MG_OK;
+}
+
+static void drop_graphs(Ctx* c) {
+  if (c->gA) cudaGraphExecDestroy(c->gA);
+  if (c->gB) cudaGraphExecDestroy(c->gB);
+  c->gA = c->gB = nullptr;
+}
+
+static int check_device_error(Ctx* c) {
+  DevError h{};
+  CK(cudaMemcpyAsync(&h, c->err, sizeof(DevError), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (h.code == 0) return MG_OK;
+  CK(cudaMemsetAsync(c->err, 0, sizeof(DevError), c->st));
+  switch (h.code) {
+    case -4:
+      return fail(c, MG_ERR_NOT_SPD,
+                  "Cholesky failed (local block, edge block, macro A_II or A_1); index "
+                  "(element / edge / macro; -2 = coarsest) reported",
+                  h.index);
+    case -1:
+      return fail(c, MG_ERR_ARG, "invalid K / tau / method at element", h.index);
+    default:
+      return fail(c, MG_ERR_SINGULAR_LOCAL, "device error", h.index);
+  }
+}
+
+// ---------------------------------------------------------------- apply / smoothing building blocks
+static inline void apply_full(Ctx* c, const HostLevel& L, const double* x, double* y,
+                              double* partials) {
+  c->launches += launch_apply(L.d, 0, AM_W0, x, y, nullptr, nullptr, 0, nullptr, 0, c->st);
+  c->launches += launch_apply(L.d, 1, AM_APPLY, x, y, nullptr, nullptr, 0, partials, 0, c->st);
+}
+
+static inline void smooth_step(Ctx* c, HostLevel& L, int step) {
+  c->launches += launch_apply(L.d, 0, AM_W0, L.e, L.w, nullptr, nullptr, 0, nullptr, 0, c->st);
+  c->launches += launch_apply(L.d, 1, AM_SMOOTH, L.e, L.w, L.r, L.dv, step, nullptr, 0, c->st);
+}
+
+static inline void residual(Ctx* c, HostLevel& L) {  // L.w = L.r - A L.e
+  c->launches += launch_apply(L.d, 0, AM_W0, L.e, L.w, nullptr, nullptr, 0, nullptr, 0, c->st);
+  c->launches += launch_apply(L.d, 1, AM_RESID, L.e, L.w, L.r, nullptr, 0, nullptr, 0, c->st);
+}
+
+// V-cycle B_k (Algorithm 1) on level li with input L.r, output L.e.
+// `first_done`: the first pre-smoothing step (from e = 0) was fused into the
+// restriction kernel of the finer level.  Step 3 (local correction) and the
+// restriction share one residual: Q_{k-1} A_k T_k = 0, so Q(r - A e2) equals
+// Q(r - A e1).
+static void vcycle_level(Ctx* c, int li, bool first_done) {
+  HostLevel& L = c->lev[li];
+  const int nlev = (int)c->lev.size();
+  if (li == nlev - 1) {
+    c->launches += launch_coarse_solve(L.d, c->fidx, c->nf, c->A1inv, L.r, L.e, c->st);
+    return;
+  }
+  const int nu_pre = c->sm.nu_pre, nu_post = c->sm.nu_post;
+  int s0 = 0;
+  if (nu_pre > 0) {
+    if (!first_done) c->launches += launch_smooth_first(L.d, L.r, L.e, L.dv, c->st);
+    s0 = 1;
+  } else {
+    c->launches += launch_zero(L.e, L.d.ndof, c->st);
+  }
+  for (int s = s0; s < nu_pre; ++s) smooth_step(c, L, s);
+  residual(c, L);  // L.w = r - A e1
+  HostLevel& C = c->lev[li + 1];
+  const bool fuse = (li + 1 < nlev - 1) && nu_pre > 0;
+  if (L.kind == KIND_H) {
+    c->launches += launch_lc_restrict(L.d, L.w, L.e, L.KIIinv, L.Pm, L.cbuf, true, true, c->st);
+    c->launches += launch_restrict_edges(L.d, C.d, L.w, L.cbuf, C.r, fuse, C.e, C.dv, c->st);
+  } else {
+    c->launches += launch_p_restrict(L.d, C.d, c->refdev.Jp, L.w, C.r, fuse, C.e, C.dv, c->st);
+  }
+  vcycle_level(c, li + 1, fuse);
+  if (L.kind == KIND_H)
+    c->launches += launch_prolong_macro(L.d, C.d, C.e, L.Pm, L.e, c->st);
+  else
+    c->launches += launch_p_prolong(L.d, c->refdev.Jp, C.e, L.e, c->st);
+  for (int s = 0; s < nu_post; ++s) smooth_step(c, L, s);
+}
+
+// ---------------------------------------------------------------- setup
+static int setup_impl(Ctx* c, const double* K, const int8_t* method, const double* tau) {
+  cudaStream_t st = c->st;
+  CK(cudaMemsetAsync(c->err, 0, sizeof(DevError), st));
+  HostLevel& F = c->lev[0];
+  const int64_t ne = F.d.ne;
+  CK(cudaMemcpyAsync(c->Kc, K, ne * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(c->tauc, tau, ne * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(c->methc, method, ne * sizeof(int8_t), cudaMemcpyDeviceToDevice, st));
+  c->launches += launch_local_dtn(F.d, c->refdev, F.h, c->Kc, c->methc, c->tauc, c->err, st);
+  for (size_t li = 0; li + 1 < c->lev.size(); ++li) {
+    HostLevel& L = c->lev[li];
+    HostLevel& C = c->lev[li + 1];
+    if (L.kind == KIND_P)
+      c->launches += launch_p_coarsen(L.d, C.d, c->refdev.Jp, st);
+    else
+      c->launches += launch_agglomerate(L.d, C.d, L.KIIinv, L.Pm, c->err, st);
+  }
+  const int nlev = (int)c->lev.size();
+  int numax = std::max(c->sm.nu_pre, c->sm.nu_post);
+  if (numax < 1) numax = 1;
+  for (int li = 0; li < nlev - 1; ++li) {
+    HostLevel& L = c->lev[li];
+    L.d.smoother = c->sm.kind;
+    c->launches += launch_edge_blocks(L.d, c->err, st);
+    if (c->sm.kind == MG_SMOOTH_BLOCK_JACOBI) {
+      c->launches += launch_set_bj_coef(c->sm.omega, L.d.coef, st);
+      continue;
+    }
+    // Chebyshev: lambda_max of D_B^-1 A_k by power iteration (Q11)
+    const int vg = vec_grid(L.d.nedge);
+    c->launches += launch_pow_init(L.d, L.e, st);
+    for (int it = 0; it < c->sm.lmax_iters; ++it) {
+      apply_full(c, L, L.e, L.w, nullptr);
+      c->launches += launch_edge_dinv(L.d, L.w, L.r, c->part, vg, st);
+      c->launches += launch_reduce(c->part, vg, c->sscal, 6, 0, nullptr, st);
+      c->launches += launch_reduce(c->part + vg, vg, c->sscal, 7, 0, nullptr, st);
+      c->launches += launch_scale_by_norm(L.e, L.r, L.d.ndof, c->sscal, 6, st);
+    }
+    const int ag = apply_grid(L.d);
+    apply_full(c, L, L.e, L.w, c->part);
+    c->launches += launch_reduce(c->part, ag, c->sscal, 8, 0, nullptr, st);
+    c->launches += launch_lmax_finish(c->sscal, c->sm.lmax_safety, c->sm.cheb_ratio, numax, L.lam,
+                                      L.d.coef, st);
+  }
+  c->lev.back().d.smoother = c->sm.kind;
+  c->launches += launch_coarse_assemble_factor(c->lev.back().d, c->fpos, c->nf, c->A1, c->A1inv,
+                                               c->err, st);
+  CK(cudaGetLastError());
+  // e / w / d vectors must hold 0 on dOmega: zero them once
+  for (auto& L : c->lev) {
+    CK(cudaMemsetAsync(L.e, 0, L.d.ndof * sizeof(double), st));
+    CK(cudaMemsetAsync(L.w, 0, L.d.ndof * sizeof(double), st));
+    CK(cudaMemsetAsync(L.dv, 0, L.d.ndof * sizeof(double), st));
+    CK(cudaMemsetAsync(L.r, 0, L.d.ndof * sizeof(double), st));
+  }
+  RC(check_device_error(c));
+  c->setup_done = true;
+  return MG_OK;
+}
+
+// ---------------------------------------------------------------- PCG
+// scal: [0] rz, [1] pAp, [2] rr, [3] alpha, [4] beta, [5] gg
+static void pcg_iter_A(Ctx* c) {  // Ap, alpha, x/r update, rr
+  HostLevel& F = c->lev[0];
+  const int ag = apply_grid(F.d);
+  const int vg = vec_grid(F.d.ndof);
+  apply_full(c, F, c->pv, c->ap, c->part);
+  c->launches += launch_reduce(c->part, ag, c->scal, 1, 1, nullptr, c->st);
+  c->launches += launch_pcg_update(c->x, F.r, c->pv, c->ap, c->scal, F.d.ndof, c->part, vg, c->st);
+  c->launches += launch_reduce(c->part, vg, c->scal, 2, 0, nullptr, c->st);
+}
+
+static void pcg_iter_B(Ctx* c) {  // z = B r, beta, p update
+  HostLevel& F = c->lev[0];
+  const int vg = vec_grid(F.d.ndof);
+  vcycle_level(c, 0, false);
+  c->launches += launch_dot(F.r, F.e, F.d.ndof, c->part, vg, c->st);
+  c->launches += launch_reduce(c->part, vg, c->scal, 0, 2, nullptr, c->st);
+  c->launches += launch_pcg_pupdate(c->pv, F.e, c->scal, F.d.ndof, c->st);
+}
+
+static int capture(Ctx* c, void (*body)(Ctx*), cudaGraphExec_t* out, long long* nk) {
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+  const long long before = c->launches;
+  body(c);
+  *nk = c->launches - before;   // kernels in the graph, counted when it runs
+  c->launches = before;
+  CK(cudaStreamEndCapture(c->st, &g));
+  cudaError_t e = cudaGraphInstantiate(out, g, 0);
+  cudaGraphDestroy(g);
+  CK(e);
+  return MG_OK;
+}
+
+static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int maxit,
+                    int* iters_out, double* relres_out, int* status_out, double* hist) {
+  HostLevel& F = c->lev[0];
+  cudaStream_t st = c->st;
+  const int64_t n = F.d.ndof;
+  const int vg = vec_grid(n);
+  const long long l0 = c->launches;
+  if (c->use_graphs && !c->gA) {
+    RC(capture(c, pcg_iter_A, &c->gA, &c->nA));
+    RC(capture(c, pcg_iter_B, &c->gB, &c->nB));
+  }
+  c->launches += launch_copy(F.r, g, n, st);
+  CK(cudaMemsetAsync(c->x, 0, n * sizeof(double), st));
+  c->launches += launch_dot(F.r, F.r, n, c->part, vg, st);
+  c->launches += launch_reduce(c->part, vg, c->scal, 5, 0, nullptr, st);
+  CK(cudaMemcpyAsync(c->pinned, c->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const double gg = c->pinned[5];
+  const double gnorm = std::sqrt(gg);
+  int status = MG_MAXIT, it = 0;
+  double rel = 0.0;
+  if (hist) hist[0] = gg > 0 ? 1.0 : 0.0;
+  if (!(gg > 0.0)) {   // g = 0 -> lambda = 0 in 0 iterations
+    CK(cudaMemsetAsync(lambda, 0, n * sizeof(double), st));
+    CK(cudaStreamSynchronize(st));
+    if (iters_out) *iters_out = 0;
+    if (relres_out) *relres_out = 0.0;
+    if (status_out) *status_out = MG_CONVERGED;
+    c->last_solve_launches = c->launches - l0;
+    return MG_OK;
+  }
+  // z = B r ; rz = r.z ; p = z
+  vcycle_level(c, 0, false);
+  c->launches += launch_dot(F.r, F.e, n, c->part, vg, st);
+  c->launches += launch_reduce(c->part, vg, c->scal, 0, 0, nullptr, st);
+  c->launches += launch_copy(c->pv, F.e, n, st);
+  CK(cudaGetLastError());
+  for (it = 1; it <= maxit; ++it) {
+    if (c->use_graphs) {
+      CK(cudaGraphLaunch(c->gA, st));
+      c->launches += c->nA;
+    } else {
+      pcg_iter_A(c);
+    }
+    CK(cudaMemcpyAsync(c->pinned, c->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const double pAp = c->pinned[1], rr = c->pinned[2];
+    rel = std::sqrt(rr) / gnorm;
+    if (hist) hist[it] = rel;
+    if (!(pAp > 0.0) || !std::isfinite(rr)) {
+      status = MG_BREAKDOWN;
+      break;
+    }
+    if (rel <= rtol) {
+      status = MG_CONVERGED;
+      break;
+    }
+    if (rel > 1e6) {
+      status = MG_DIVERGED;
+      break;
+    }
+    if (it == maxit) break;
+    if (c->use_graphs) {
+      CK(cudaGraphLaunch(c->gB, st));
+      c->launches += c->nB;
+    } else {
+      pcg_iter_B(c);
+    }
+  }
+  if (it > maxit) it = maxit;
+  c->launches += launch_copy(lambda, c->x, n, st);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  if (iters_out) *iters_out = it;
+  if (relres_out) *relres_out = rel;
+  if (status_out) *status_out = status;
+  c->last_solve_launches = c->launches - l0;
+  return MG_OK;
+}
+
+static int rhs_impl(Ctx* c, const double* f_qp, double f_const, const double* gD_qp, double* g,
+                    double* lambda_bc) {
+  HostLevel& F = c->lev[0];
+  cudaStream_t st = c->st;
+  const int64_t n = F.d.ndof;
+  CK(cudaMemsetAsync(c->lamD, 0, n * sizeof(double), st));
+  if (gD_qp) c->launches += launch_dirichlet(F.d, c->refdev, gD_qp, c->lamD, st);
+  CK(cudaMemsetAsync(g, 0, n * sizeof(double), st));
+  c->launches += launch_local_rhs(F.d, c->refdev, F.h, c->Kc, c->methc, c->tauc, f_qp, f_const,
+                                  gD_qp ? c->lamD : nullptr, g, c->err, st);
+  if (lambda_bc)
+    CK(cudaMemcpyAsync(lambda_bc, c->lamD, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+
+static HostLevel* level_of(Ctx* c, int level) {
+  const int N = (int)c->lev.size();
+  if (level < 1 || level > N) return nullptr;
+  return &c->lev[N - level];
+}
+
+}  // namespace mgdtn
+
+using namespace mgdtn;
+
+// ============================================================================ C ABI
+extern "C" {
+
+int mg_build_hierarchy(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
+                       const mg_partition* part, void* cuda_stream, void** out_ctx) {
+  if (!mesh || !out_ctx) return MG_ERR_ARG;
+  *out_ctx = nullptr;
+  if (part && part->nranks > 1) return MG_ERR_UNSUPPORTED;
+  if (p < 1 || p > 4) return MG_ERR_ARG;
+  const int nx = mesh->nx, ny = mesh->ny;
+  if (nx < 2 || ny < 2 || (nx & 1) || (ny & 1) || !(mesh->h > 0)) return MG_ERR_SHAPE;
+  Ctx* c = new Ctx();
+  c->mesh = *mesh;
+  c->p = p;
+  c->st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  try {
+    c->ref = build_ref_tables(p);
+  } catch (const std::exception&) {
+    delete c;
+    return MG_ERR_ARG;
+  }
+  const RefTables& T = c->ref;
+  c->ref_doubles = T.G.size() + T.F.size() + T.P.size() + T.E.size() + T.W.size() + T.H.size() +
+                   T.LN.size() + T.Nl.size() + T.fq.size() + T.ew.size() + T.H1inv.size() +
+                   T.Jp.size();
+  // levels: finest (order p), the p-level (P1, same mesh) if p > 1, then 2x2
+  // agglomeration while both sides stay even
+  int cx = nx, cy = ny;
+  double h = mesh->h;
+  HostLevel top;
+  init_level(top, cx, cy, p, h, KIND_COARSEST);
+  c->lev.push_back(top);
+  if (p > 1) {
+    c->lev.back().kind = KIND_P;
+    HostLevel L1;
+    init_level(L1, cx, cy, 1, h, KIND_COARSEST);
+    c->lev.push_back(L1);
+  }
+  int nh = 0;
+  while (cx > 2 && cy > 2 && (cx % 4 == 0) && (cy % 4 == 0) &&
+         (n_h_levels <= 0 || nh < n_h_levels)) {
+    c->lev.back().kind = KIND_H;
+    cx /= 2;
+    cy /= 2;
+    h *= 2;
+    HostLevel L;
+    init_level(L, cx, cy, 1, h, KIND_COARSEST);
+    c->lev.push_back(L);
+    ++nh;
+  }
+  const LevelDev& d1 = c->lev.back().d;
+  c->nf = (int)(((int64_t)cx * (cy - 1) + (int64_t)(cx - 1) * cy) * d1.k1);
+  if (c->nf > 4096) {   // dense coarsest solve limit
+    delete c;
+    return MG_ERR_SHAPE;
+  }
+  layout(c);   // host only: no CUDA call until mg_bind_workspace
+  *out_ctx = c;
+  return MG_OK;
+}
+
+int mg_workspace_bytes(const void* ctx, size_t* bytes) {
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (!c || !bytes) return MG_ERR_ARG;
+  *bytes = c->ws_need;
+  return MG_OK;
+}
+
+int mg_bind_workspace(void* ctx, void* dev_ptr, size_t bytes) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !dev_ptr) return MG_ERR_ARG;
+  if (bytes < c->ws_need) return fail(c, MG_ERR_WORKSPACE, "workspace too small");
+  if (reinterpret_cast<uintptr_t>(dev_ptr) & 255)
+    return fail(c, MG_ERR_WORKSPACE, "workspace must be 256-byte aligned");
+  drop_graphs(c);
+  if (!c->pinned) CK(cudaMallocHost(&c->pinned, 16 * sizeof(double)));
+  c->ws = static_cast<char*>(dev_ptr);
+  c->ws_bytes = bytes;
+  c->setup_done = false;
+  bind_pointers(c);
+  CK(cudaMemsetAsync(c->ws, 0, c->ws_need, c->st));
+  return upload_static(c);
+}
+
+int mg_setup_dtn(void* ctx, const double* K, const int8_t* method, const double* tau,
+                 const mg_smoother_cfg* smoother) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c) return MG_ERR_ARG;
+  if (!c->ws) return fail(c, MG_ERR_WORKSPACE, "no workspace bound");
+  if (!K || !method || !tau || !smoother) return fail(c, MG_ERR_ARG, "NULL argument");
+  mg_smoother_cfg sm = *smoother;
+  if (sm.kind != MG_SMOOTH_BLOCK_JACOBI && sm.kind != MG_SMOOTH_CHEBYSHEV)
+    return fail(c, MG_ERR_ARG, "unknown smoother kind");
+  if (sm.nu_pre < 0 || sm.nu_post < 0 || sm.nu_pre > MAX_NU || sm.nu_post > MAX_NU)
+    return fail(c, MG_ERR_ARG, "nu out of range (0..8)");
+  if (!(sm.omega > 0)) sm.omega = 1.0;
+  if (!(sm.cheb_ratio > 1)) sm.cheb_ratio = 30.0;
+  if (sm.lmax_iters <= 0) sm.lmax_iters = 20;
+  if (!(sm.lmax_safety > 0)) sm.lmax_safety = 1.05;
+  if (sm.nu_pre != c->sm.nu_pre || sm.nu_post != c->sm.nu_post || sm.kind != c->sm.kind)
+    drop_graphs(c);
+  c->sm = sm;
+  c->setup_done = false;
+  return setup_impl(c, K, method, tau);
+}
+
+int mg_assemble_rhs(void* ctx, const double* f_qp, double f_const, const double* gD_qp,
+                    double* g, double* lambda_bc) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !g) return MG_ERR_ARG;
+  if (!c->setup_done) return fail(c, MG_ERR_STATE, "mg_setup_dtn must precede mg_assemble_rhs");
+  return rhs_impl(c, f_qp, f_const, gD_qp, g, lambda_bc);
+}
+
+int mg_apply(void* ctx, int32_t level, const double* x, double* y) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !x || !y || x == y) return MG_ERR_ARG;
+  if (!c->setup_done) return fail(c, MG_ERR_STATE, "setup first");
+  HostLevel* L = level_of(c, level);
+  if (!L) return fail(c, MG_ERR_ARG, "level out of range");
+  apply_full(c, *L, x, y, nullptr);
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+
+int mg_vcycle(void* ctx, const double* r, double* z) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !r || !z) return MG_ERR_ARG;
+  if (!c->setup_done) return fail(c, MG_ERR_STATE, "setup first");
+  HostLevel& F = c->lev[0];
+  c->launches += launch_copy(F.r, r, F.d.ndof, c->st);
+  vcycle_level(c, 0, false);
+  c->launches += launch_copy(z, F.e, F.d.ndof, c->st);
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+
+int mg_smooth(void* ctx, int32_t level, const double* r, double* e, int32_t nsteps) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !r || !e || nsteps < 0 || nsteps > MAX_NU) return MG_ERR_ARG;
+  if (!c->setup_done) return fail(c, MG_ERR_STATE, "setup first");
+  HostLevel* L = level_of(c, level);
+  if (!L || L == &c->lev.back()) return fail(c, MG_ERR_ARG, "no smoother on this level");
+  c->launches += launch_copy(L->r, r, L->d.ndof, c->st);
+  c->launches += launch_copy(L->e, e, L->d.ndof, c->st);
+  for (int s = 0; s < nsteps; ++s) smooth_step(c, *L, s);
+  c->launches += launch_copy(e, L->e, L->d.ndof, c->st);
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+
+int mg_local_correct(void* ctx, int32_t level, const double* res, double* e) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !res || !e) return MG_ERR_ARG;
+  if (!c->setup_done) return fail(c, MG_ERR_STATE, "setup first");
+  HostLevel* L = level_of(c, level);
+  if (!L || L->kind != KIND_H) return fail(c, MG_ERR_ARG, "level has no interior dofs");
+  c->launches += launch_lc_restrict(L->d, res, e, L->KIIinv, L->Pm, L->cbuf, true, false, c->st);
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+
+int mg_restrict(void* ctx, int32_t level, const double* res, double* rc) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !res || !rc) return MG_ERR_ARG;
+  if (!c->setup_done) return fail(c, MG_ERR_STATE, "setup first");
+  HostLevel* L = level_of(c, level);
+  if (!L || L->kind == KIND_COARSEST) return fail(c, MG_ERR_ARG, "no coarser level");
+  HostLevel& C = *(L + 1);
+  if (L->kind == KIND_H) {
+    c->launches += launch_lc_restrict(L->d, res, nullptr, L->KIIinv, L->Pm, L->cbuf, false, true,
+                                      c->st);
+    c->launches += launch_restrict_edges(L->d, C.d, res, L->cbuf, rc, false, nullptr, nullptr,
+                                         c->st);
+  } else {
+    c->launches += launch_p_restrict(L->d, C.d, c->refdev.Jp, res, rc, false, nullptr, nullptr,
+                                     c->st);
+  }
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+
+int mg_prolong(void* ctx, int32_t level, const double* ec, double* e) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !ec || !e) return MG_ERR_ARG;
+  if (!c->setup_done) return fail(c, MG_ERR_STATE, "setup first");
+  HostLevel* L = level_of(c, level);
+  if (!L || L->kind == KIND_COARSEST) return fail(c, MG_ERR_ARG, "no coarser level");
+  HostLevel& C = *(L + 1);
+  if (L->kind == KIND_H)
+    c->launches += launch_prolong_macro(L->d, C.d, ec, L->Pm, e, c->st);
+  else
+    c->launches += launch_p_prolong(L->d, c->refdev.Jp, ec, e, c->st);
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+
+int mg_pcg_solve(void* ctx, const double* g, double* lambda, double rtol, int32_t maxit,
+                 int32_t* iters, double* relres, int32_t* solve_status, double* resid_hist) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !g || !lambda || maxit < 1 || !(rtol > 0)) return MG_ERR_ARG;
+  if (!c->setup_done) return fail(c, MG_ERR_STATE, "setup first");
+  int it = 0, stt = 0;
+  double rel = 0;
+  RC(pcg_impl(c, g, lambda, rtol, maxit, &it, &rel, &stt, resid_hist));
+  if (iters) *iters = it;
+  if (relres) *relres = rel;
+  if (solve_status) *solve_status = stt;
+  return MG_OK;
+}
+
+int mg_staging_bytes(const void* ctx, int32_t with_f, int32_t with_gD, size_t* bytes) {
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (!c || !bytes) return MG_ERR_ARG;
+  const LevelDev& d = c->lev[0].d;
+  const int nq = c->p + 4;
+  size_t b = 0;
+  b += align_up(d.ne * sizeof(double)) * 2 + align_up(d.ne);                 // K, tau, method
+  b += align_up(d.ndof * sizeof(double)) * 2;                                // g, lambda
+  if (with_f) b += align_up((size_t)d.ne * nq * nq * sizeof(double));
+  if (with_gD) b += align_up((size_t)(2 * d.nx + 2 * d.ny) * nq * sizeof(double));
+  *bytes = b;
+  return MG_OK;
+}
+
+int mg_bind_staging(void* ctx, void* dev_ptr, size_t bytes) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !dev_ptr) return MG_ERR_ARG;
+  if (reinterpret_cast<uintptr_t>(dev_ptr) & 255)
+    return fail(c, MG_ERR_WORKSPACE, "staging must be 256-byte aligned");
+  c->stg = static_cast<char*>(dev_ptr);
+  c->stg_bytes = bytes;
+  return MG_OK;
+}
+
+int mg_solve_host(void* ctx, const double* K_host, const int8_t* method_host,
+                  const double* tau_host, const double* f_qp_host, double f_const,
+                  const double* gD_qp_host, const mg_smoother_cfg* smoother, double rtol,
+                  int32_t maxit, double* lambda_host, int32_t* iters, double* relres,
+                  int32_t* solve_status) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !K_host || !method_host || !tau_host || !lambda_host || !smoother) return MG_ERR_ARG;
+  size_t need = 0;
+  mg_staging_bytes(c, f_qp_host != nullptr, gD_qp_host != nullptr, &need);
+  if (!c->stg || c->stg_bytes < need) return fail(c, MG_ERR_WORKSPACE, "staging not bound / too small");
+  const LevelDev& d = c->lev[0].d;
+  const int nq = c->p + 4;
+  char* b = c->stg;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    char* p = b + o;
+    o += align_up(bytes);
+    return p;
+  };
+  double* Kd = reinterpret_cast<double*>(take(d.ne * sizeof(double)));
+  double* taud = reinterpret_cast<double*>(take(d.ne * sizeof(double)));
+  int8_t* md = reinterpret_cast<int8_t*>(take(d.ne));
+  double* gd = reinterpret_cast<double*>(take(d.ndof * sizeof(double)));
+  double* lamd = reinterpret_cast<double*>(take(d.ndof * sizeof(double)));
+  double* fd = f_qp_host ? reinterpret_cast<double*>(take((size_t)d.ne * nq * nq * sizeof(double)))
+                         : nullptr;
+  double* gDd = gD_qp_host
+                    ? reinterpret_cast<double*>(take((size_t)(2 * d.nx + 2 * d.ny) * nq * sizeof(double)))
+                    : nullptr;
+  cudaStream_t st = c->st;
+  CK(cudaMemcpyAsync(Kd, K_host, d.ne * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(taud, tau_host, d.ne * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(md, method_host, d.ne, cudaMemcpyHostToDevice, st));
+  if (fd)
+    CK(cudaMemcpyAsync(fd, f_qp_host, (size_t)d.ne * nq * nq * sizeof(double),
+                       cudaMemcpyHostToDevice, st));
+  if (gDd)
+    CK(cudaMemcpyAsync(gDd, gD_qp_host, (size_t)(2 * d.nx + 2 * d.ny) * nq * sizeof(double),
+                       cudaMemcpyHostToDevice, st));
+  RC(mg_setup_dtn(c, Kd, md, taud, smoother));
+  RC(rhs_impl(c, fd, f_const, gDd, gd, nullptr));
+  int it = 0, stt = 0;
+  double rel = 0;
+  RC(pcg_impl(c, gd, lamd, rtol, maxit, &it, &rel, &stt, nullptr));
+  // full trace: free part + Dirichlet values (c->lamD is 0 off dOmega, lamd is 0 on it)
+  c->launches += launch_add(lamd, c->lamD, d.ndof, st);
+  CK(cudaMemcpyAsync(lambda_host, lamd, d.ndof * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (iters) *iters = it;
+  if (relres) *relres = rel;
+  if (solve_status) *solve_status = stt;
+  return MG_OK;
+}
+
+int mg_num_levels(const void* ctx, int32_t* nlevels) {
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (!c || !nlevels) return MG_ERR_ARG;
+  *nlevels = (int32_t)c->lev.size();
+  return MG_OK;
+}
+
+int mg_level_info(const void* ctx, int32_t level, int32_t* nx, int32_t* ny, int32_t* p,
+                  int64_t* ndof) {
+  Ctx* c = const_cast<Ctx*>(static_cast<const Ctx*>(ctx));
+  if (!c) return MG_ERR_ARG;
+  HostLevel* L = level_of(c, level);
+  if (!L) return MG_ERR_ARG;
+  if (nx) *nx = L->d.nx;
+  if (ny) *ny = L->d.ny;
+  if (p) *p = L->d.p;
+  if (ndof) *ndof = L->d.ndof;
+  return MG_OK;
+}
+
+int mg_copy_element_dtn(const void* ctx, int32_t level, double* dst) {
+  Ctx* c = const_cast<Ctx*>(static_cast<const Ctx*>(ctx));
+  if (!c || !dst) return MG_ERR_ARG;
+  if (!c->ws) return fail(c, MG_ERR_WORKSPACE, "no workspace bound");
+  HostLevel* L = level_of(c, level);
+  if (!L) return MG_ERR_ARG;
+  c->launches += launch_packed_to_dense(L->d, dst, c->st);
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+
+int mg_debug_set_element_dtn(void* ctx, int32_t level, const double* src) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !src) return MG_ERR_ARG;
+  if (!c->ws) return fail(c, MG_ERR_WORKSPACE, "no workspace bound");
+  HostLevel* L = level_of(c, level);
+  if (!L) return MG_ERR_ARG;
+  c->launches += launch_dense_to_packed(L->d, src, c->st);
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+
+int mg_level_lambda_max(const void* ctx, int32_t level, double* lam) {
+  Ctx* c = const_cast<Ctx*>(static_cast<const Ctx*>(ctx));
+  if (!c || !lam) return MG_ERR_ARG;
+  HostLevel* L = level_of(c, level);
+  if (!L) return MG_ERR_ARG;
+  *lam = 0.0;
+  if (c->sm.kind != MG_SMOOTH_CHEBYSHEV || L == &c->lev.back()) return MG_OK;
+  CK(cudaMemcpyAsync(lam, L->lam, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return MG_OK;
+}
+
+int mg_last_launch_count(const void* ctx, int64_t* launches) {
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (!c || !launches) return MG_ERR_ARG;
+  *launches = c->last_solve_launches;
+  return MG_OK;
+}
+
+int mg_total_launch_count(const void* ctx, int64_t* launches) {
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (!c || !launches) return MG_ERR_ARG;
+  *launches = c->launches;
+  return MG_OK;
+}
+
+int mg_set_use_graphs(void* ctx, int32_t on) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c) return MG_ERR_ARG;
+  c->use_graphs = on != 0;
+  return MG_OK;
+}
+
+const char* mg_last_error(const void* ctx) {
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  return c ? c->last_err.c_str() : "null context";
+}
+
+int64_t mg_last_error_index(const void* ctx) {
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  return c ? c->last_idx : -1;
+}
+
+void mg_destroy(void* ctx) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c) return;
+  drop_graphs(c);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,45 @@
+// Host-side reference-element tables for the element-local solves.
+//
+// Unit square, volume space Q^p with GLL nodal basis (index i = b*(p+1)+a,
+// a along x), trace space P^p per edge with GLL nodes in the edge's global
+// orientation, local edges {0 bottom, 1 right, 2 top, 3 left}.  Exact Gauss
+// quadrature.  The element matrices of a side-h square depend only on
+// (K, tau*h) (SURVEY.md 8(c) "Scaling"), so these h-free tables plus two
+// scalars per element fully determine each local solve (PAPER.md:184-199,
+// 230-233, 305-316).
+#pragma once
+#include <vector>
+
+namespace mgdtn {
+
+struct RefTables {
+  int p = 0, k1 = 0, nv = 0, m = 0;
+  std::vector<double> gll;            // [k1]
+  // HDG staged elimination (u eliminated first):
+  //   Q = K*G + t*F, R = K*P + t*E, S0 = K*W + t*H, t = tau*h
+  std::vector<double> G, F;           // [nv*nv]
+  std::vector<double> P, E;           // [nv*m]
+  std::vector<double> W, H;           // [m*m]
+  // SIPG-H: Q = K*LN + t*F, R = t*E - K*Nl, S0 = t*H, LN = L - N - N^T
+  std::vector<double> LN;             // [nv*nv]
+  std::vector<double> Nl;             // [nv*m]
+  // source quadrature on the input sampling grid (p+4 Gauss per direction):
+  //   fw_i = h^2 * sum_{qy,qx} fq[qy,qx,i] * f(qy,qx)
+  int nqf = 0;
+  std::vector<double> fq;             // [nqf*nqf*nv] (weights folded in)
+  // boundary-data projection: lambda = H1inv * (sum_q ew[q,a] g_q)
+  std::vector<double> ew;             // [nqf*k1] (weights folded in)
+  std::vector<double> H1inv;          // [k1*k1]
+  // p-injection J_p: fine node a from P1 endpoint values (c0, c1)
+  std::vector<double> Jp;             // [k1*2]
+};
+
+// Builds the tables for order p (1..4).  Pure host C++ (Legendre recurrences,
+// Newton iterations, dense Cholesky), no library calls.
+RefTables build_ref_tables(int p);
+
+// 1D helpers (exposed for tests of the host code)
+std::vector<double> gll_nodes01(int p);
+void gauss01(int nq, std::vector<double>& x, std::vector<double>& w);
+
+}  // namespace mgdtn

@@ -1,0 +1,332 @@
+"""Thin ctypes binding of libmgdtn.so (include/mgdtn.h), same names as the C ABI.
+
+Argument marshalling only: every step of the method runs in the library's
+CUDA kernels.  PyTorch provides device memory (the caller-owned workspace),
+the stream and pinned host buffers.  There is no CPU fallback: if the shared
+library or a CUDA device is missing, construction raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmgdtn.so")
+
+MG_OK = 0
+MG_HDG, MG_SIPG_H = 0, 1
+MG_SMOOTH_BLOCK_JACOBI, MG_SMOOTH_CHEBYSHEV = 0, 1
+STATUS = {0: "converged", 1: "maxit", 2: "diverged", 3: "breakdown"}
+ERRORS = {-1: "MG_ERR_ARG", -2: "MG_ERR_SHAPE", -3: "MG_ERR_SINGULAR_LOCAL", -4: "MG_ERR_NOT_SPD",
+          -5: "MG_ERR_CUDA", -6: "MG_ERR_NCCL", -7: "MG_ERR_STATE", -8: "MG_ERR_WORKSPACE",
+          -9: "MG_ERR_UNSUPPORTED"}
+
+
+class mg_quad_mesh(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("x0", C.c_double), ("y0", C.c_double),
+                ("h", C.c_double)]
+
+
+class mg_partition(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("px", C.c_int32), ("py", C.c_int32),
+                ("nccl_id", C.c_void_p)]
+
+
+class mg_smoother_cfg(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("nu_pre", C.c_int32), ("nu_post", C.c_int32),
+                ("omega", C.c_double), ("cheb_ratio", C.c_double), ("lmax_iters", C.c_int32),
+                ("lmax_safety", C.c_double)]
+
+
+# exported symbols and their argtypes (must match include/mgdtn.h)
+_P = C.c_void_p
+_SIGS = {
+    "mg_build_hierarchy": [C.POINTER(mg_quad_mesh), C.c_int32, C.c_int32, C.POINTER(mg_partition), _P,
+                           C.POINTER(C.c_void_p)],
+    "mg_workspace_bytes": [_P, C.POINTER(C.c_size_t)],
+    "mg_bind_workspace": [_P, _P, C.c_size_t],
+    "mg_setup_dtn": [_P, _P, _P, _P, C.POINTER(mg_smoother_cfg)],
+    "mg_assemble_rhs": [_P, _P, C.c_double, _P, _P, _P],
+    "mg_apply": [_P, C.c_int32, _P, _P],
+    "mg_vcycle": [_P, _P, _P],
+    "mg_smooth": [_P, C.c_int32, _P, _P, C.c_int32],
+    "mg_local_correct": [_P, C.c_int32, _P, _P],
+    "mg_restrict": [_P, C.c_int32, _P, _P],
+    "mg_prolong": [_P, C.c_int32, _P, _P],
+    "mg_pcg_solve": [_P, _P, _P, C.c_double, C.c_int32, C.POINTER(C.c_int32),
+                     C.POINTER(C.c_double), C.POINTER(C.c_int32), _P],
+    "mg_solve_host": [_P, _P, _P, _P, _P, C.c_double, _P, C.POINTER(mg_smoother_cfg), C.c_double,
+                      C.c_int32, _P, C.POINTER(C.c_int32), C.POINTER(C.c_double), C.POINTER(C.c_int32)],
+    "mg_staging_bytes": [_P, C.c_int32, C.c_int32, C.POINTER(C.c_size_t)],
+    "mg_bind_staging": [_P, _P, C.c_size_t],
+    "mg_num_levels": [_P, C.POINTER(C.c_int32)],
+    "mg_level_info": [_P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                      C.POINTER(C.c_int32), C.POINTER(C.c_int64)],
+    "mg_copy_element_dtn": [_P, C.c_int32, _P],
+    "mg_debug_set_element_dtn": [_P, C.c_int32, _P],
+    "mg_level_lambda_max": [_P, C.c_int32, C.POINTER(C.c_double)],
+    "mg_last_launch_count": [_P, C.POINTER(C.c_int64)],
+    "mg_total_launch_count": [_P, C.POINTER(C.c_int64)],
+    "mg_set_use_graphs": [_P, C.c_int32],
+    "mg_last_error": [_P],
+    "mg_last_error_index": [_P],
+    "mg_destroy": [_P],
+}
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libmgdtn.so (raises if absent -- there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run `python -m paper_1811_09909_b200.build` "
+                          "(or __graft_entry__.build()) first")
+    lib = C.CDLL(path)
+    for name, args in _SIGS.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = C.c_int
+    lib.mg_last_error.restype = C.c_char_p
+    lib.mg_last_error_index.restype = C.c_int64
+    lib.mg_destroy.restype = None
+    _lib = lib
+    return lib
+
+
+class MGError(RuntimeError):
+    pass
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+@dataclass
+class SmootherConfig:
+    kind: int = MG_SMOOTH_BLOCK_JACOBI
+    nu_pre: int = 2
+    nu_post: int = 2
+    omega: float = 1.0
+    cheb_ratio: float = 30.0
+    lmax_iters: int = 20
+    lmax_safety: float = 1.05
+
+    def c(self):
+        return mg_smoother_cfg(self.kind, self.nu_pre, self.nu_post, self.omega, self.cheb_ratio,
+                               self.lmax_iters, self.lmax_safety)
+
+
+class MGSolver:
+    """One context of the C ABI on the current CUDA device/stream."""
+
+    def __init__(self, nx: int, ny: int | None = None, p: int = 1, h: float | None = None,
+                 n_h_levels: int = 0, device="cuda", stream: torch.cuda.Stream | None = None):
+        if not torch.cuda.is_available():
+            raise MGError("MGSolver needs a CUDA device (no CPU fallback)")
+        self.lib = load_library()
+        ny = nx if ny is None else ny
+        self.device = torch.device(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.nx, self.ny, self.p = nx, ny, p
+        mesh = mg_quad_mesh(nx, ny, 0.0, 0.0, h if h is not None else 1.0 / nx)
+        ctx = C.c_void_p()
+        rc = self.lib.mg_build_hierarchy(C.byref(mesh), p, n_h_levels, None,
+                                         C.c_void_p(self.stream.cuda_stream), C.byref(ctx))
+        if rc != MG_OK:
+            raise MGError(f"mg_build_hierarchy failed: {ERRORS.get(rc, rc)}")
+        self.ctx = ctx
+        nb = C.c_size_t()
+        self._chk(self.lib.mg_workspace_bytes(self.ctx, C.byref(nb)), "mg_workspace_bytes")
+        self.workspace = torch.empty(nb.value, dtype=torch.uint8, device=self.device)
+        self._chk(self.lib.mg_bind_workspace(self.ctx, _ptr(self.workspace), nb.value),
+                  "mg_bind_workspace")
+        self.staging = None
+        nl = C.c_int32()
+        self._chk(self.lib.mg_num_levels(self.ctx, C.byref(nl)), "mg_num_levels")
+        self.nlevels = nl.value
+
+    # ------------------------------------------------------------------ helpers
+    def _chk(self, rc, what):
+        if rc != MG_OK:
+            msg = self.lib.mg_last_error(self.ctx).decode() if getattr(self, "ctx", None) else ""
+            idx = self.lib.mg_last_error_index(self.ctx) if getattr(self, "ctx", None) else -1
+            raise MGError(f"{what}: {ERRORS.get(rc, rc)}: {msg} (index {idx})")
+
+    def level_info(self, level: int):
+        nx, ny, p, nd = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
+        self._chk(self.lib.mg_level_info(self.ctx, level, C.byref(nx), C.byref(ny), C.byref(p),
+                                         C.byref(nd)), "mg_level_info")
+        return dict(nx=nx.value, ny=ny.value, p=p.value, ndof=nd.value)
+
+    def ndof(self, level: int | None = None) -> int:
+        return self.level_info(self.nlevels if level is None else level)["ndof"]
+
+    def _vec(self, level=None):
+        return torch.zeros(self.ndof(level), dtype=torch.float64, device=self.device)
+
+    @staticmethod
+    def _dev(x, dtype):
+        return x.to(dtype=dtype).contiguous() if torch.is_tensor(x) else torch.as_tensor(
+            np.ascontiguousarray(x), dtype=dtype)
+
+    def _d(self, x, dtype=torch.float64):
+        if x is None:
+            return None
+        t = self._dev(x, dtype)
+        return t.to(self.device) if t.device != self.device else t
+
+    # ------------------------------------------------------------------ ABI calls
+    def setup(self, K, method, tau, smoother: SmootherConfig | None = None):
+        sm = smoother or SmootherConfig()
+        self._K = self._d(K)
+        self._m = self._d(method, torch.int8)
+        self._tau = self._d(tau)
+        cfg = sm.c()
+        self._chk(self.lib.mg_setup_dtn(self.ctx, _ptr(self._K), _ptr(self._m), _ptr(self._tau),
+                                        C.byref(cfg)), "mg_setup_dtn")
+
+    def assemble_rhs(self, f_qp=None, f_const=0.0, gD_qp=None):
+        g = self._vec()
+        lam_bc = self._vec()
+        f = self._d(f_qp)
+        gd = self._d(gD_qp)
+        self._chk(self.lib.mg_assemble_rhs(self.ctx, _ptr(f), float(f_const), _ptr(gd), _ptr(g),
+                                           _ptr(lam_bc)), "mg_assemble_rhs")
+        return g, lam_bc
+
+    def apply(self, level: int, x, y=None):
+        x = self._d(x)
+        y = self._vec(level) if y is None else y
+        self._chk(self.lib.mg_apply(self.ctx, level, _ptr(x), _ptr(y)), "mg_apply")
+        return y
+
+    def vcycle(self, r, z=None):
+        r = self._d(r)
+        z = self._vec() if z is None else z
+        self._chk(self.lib.mg_vcycle(self.ctx, _ptr(r), _ptr(z)), "mg_vcycle")
+        return z
+
+    def smooth(self, level: int, r, e, nsteps: int):
+        r = self._d(r)
+        e = self._d(e).clone()
+        self._chk(self.lib.mg_smooth(self.ctx, level, _ptr(r), _ptr(e), nsteps), "mg_smooth")
+        return e
+
+    def local_correct(self, level: int, res, e):
+        res = self._d(res)
+        e = self._d(e).clone()
+        self._chk(self.lib.mg_local_correct(self.ctx, level, _ptr(res), _ptr(e)), "mg_local_correct")
+        return e
+
+    def restrict(self, level: int, res):
+        res = self._d(res)
+        rc = self._vec(level - 1)
+        self._chk(self.lib.mg_restrict(self.ctx, level, _ptr(res), _ptr(rc)), "mg_restrict")
+        return rc
+
+    def prolong(self, level: int, ec, e):
+        ec = self._d(ec)
+        e = self._d(e).clone()
+        self._chk(self.lib.mg_prolong(self.ctx, level, _ptr(ec), _ptr(e)), "mg_prolong")
+        return e
+
+    def pcg_solve(self, g, rtol=1e-10, maxit=2000, lam=None, history=False):
+        g = self._d(g)
+        lam = self._vec() if lam is None else lam
+        it, rel, st = C.c_int32(), C.c_double(), C.c_int32()
+        hist = np.zeros(maxit + 1) if history else None
+        hp = hist.ctypes.data_as(C.c_void_p) if history else None
+        self._chk(self.lib.mg_pcg_solve(self.ctx, _ptr(g), _ptr(lam), rtol, maxit, C.byref(it),
+                                        C.byref(rel), C.byref(st), hp), "mg_pcg_solve")
+        info = dict(iters=it.value, relres=rel.value, status=STATUS[st.value])
+        if history:
+            info["hist"] = hist[: it.value + 1]
+        return lam, info
+
+    def bind_staging(self, with_f: bool, with_gD: bool):
+        nb = C.c_size_t()
+        self._chk(self.lib.mg_staging_bytes(self.ctx, int(with_f), int(with_gD), C.byref(nb)),
+                  "mg_staging_bytes")
+        if self.staging is None or self.staging.numel() < nb.value:
+            self.staging = torch.empty(nb.value, dtype=torch.uint8, device=self.device)
+            self._chk(self.lib.mg_bind_staging(self.ctx, _ptr(self.staging), nb.value),
+                      "mg_bind_staging")
+
+    def solve_host(self, K, method, tau, f_qp=None, f_const=0.0, gD_qp=None,
+                   smoother: SmootherConfig | None = None, rtol=1e-10, maxit=2000, out=None):
+        """The user call with HOST buffers (numpy or pinned CPU tensors)."""
+        def host(a, dt):
+            if a is None:
+                return None
+            if torch.is_tensor(a):
+                assert a.device.type == "cpu" and a.is_contiguous()
+                return a
+            return np.ascontiguousarray(a, dtype=dt)
+
+        def hp(a):
+            if a is None:
+                return None
+            return C.c_void_p(a.data_ptr()) if torch.is_tensor(a) else a.ctypes.data_as(C.c_void_p)
+        K, method, tau = host(K, np.float64), host(method, np.int8), host(tau, np.float64)
+        f_qp, gD_qp = host(f_qp, np.float64), host(gD_qp, np.float64)
+        self.bind_staging(f_qp is not None, gD_qp is not None)
+        out = np.empty(self.ndof()) if out is None else out
+        cfg = (smoother or SmootherConfig()).c()
+        it, rel, st = C.c_int32(), C.c_double(), C.c_int32()
+        self._chk(self.lib.mg_solve_host(self.ctx, hp(K), hp(method), hp(tau), hp(f_qp), float(f_const),
+                                         hp(gD_qp), C.byref(cfg), rtol, maxit, hp(out), C.byref(it),
+                                         C.byref(rel), C.byref(st)), "mg_solve_host")
+        return out, dict(iters=it.value, relres=rel.value, status=STATUS[st.value])
+
+    def element_dtn(self, level: int):
+        info = self.level_info(level)
+        m = 4 * (info["p"] + 1)
+        out = torch.empty((info["nx"] * info["ny"], m, m), dtype=torch.float64, device=self.device)
+        self._chk(self.lib.mg_copy_element_dtn(self.ctx, level, _ptr(out)), "mg_copy_element_dtn")
+        return out
+
+    def set_element_dtn(self, level: int, S):
+        S = self._d(S)
+        self._chk(self.lib.mg_debug_set_element_dtn(self.ctx, level, _ptr(S)),
+                  "mg_debug_set_element_dtn")
+
+    def lambda_max(self, level: int) -> float:
+        v = C.c_double()
+        self._chk(self.lib.mg_level_lambda_max(self.ctx, level, C.byref(v)), "mg_level_lambda_max")
+        return v.value
+
+    def last_launch_count(self) -> int:
+        v = C.c_int64()
+        self._chk(self.lib.mg_last_launch_count(self.ctx, C.byref(v)), "mg_last_launch_count")
+        return v.value
+
+    def total_launch_count(self) -> int:
+        v = C.c_int64()
+        self._chk(self.lib.mg_total_launch_count(self.ctx, C.byref(v)), "mg_total_launch_count")
+        return v.value
+
+    def use_graphs(self, on: bool):
+        self._chk(self.lib.mg_set_use_graphs(self.ctx, int(on)), "mg_set_use_graphs")
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.mg_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def smoother_from_config(cfg) -> SmootherConfig:
+    """SmootherConfig of a workloads.Config (V(nu, nu), BJ or Chebyshev)."""
+    return SmootherConfig(kind=cfg.smoother, nu_pre=cfg.nu, nu_post=cfg.nu)

@@ -1,0 +1,244 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the
+same seeded inputs (BASELINE.json north star: <= 1e-12 relative L2 per
+operator apply and per V-cycle; <= 1e-9 on the converged trace solution with
+iteration counts within +-1)."""
+import numpy as np
+import pytest
+import torch
+
+import workloads as W
+from oracle import assembly, krylov, multigrid
+from oracle import element as el
+
+pytestmark = pytest.mark.gpu
+
+TOL_OP = 1e-12
+TOL_SOL = 1e-9
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    from paper_1811_09909_b200 import build
+    build.build()
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def rel(a, b):
+    a = np.asarray(a, float)
+    b = np.asarray(b, float)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+class Case:
+    """One problem set up identically on both sides."""
+
+    def __init__(self, cfg_index, n, p=None, smoother=None, nu=None):
+        from paper_1811_09909_b200 import MGSolver, SmootherConfig
+        c = W.scaled_config(cfg_index, n) if W.CONFIGS[cfg_index].n != n else W.CONFIGS[cfg_index]
+        if p is not None:
+            c.p = p
+        if smoother is not None:
+            c.smoother = smoother
+        if nu is not None:
+            c.nu = nu
+        self.cfg = c
+        pr = W.make_problem(c)
+        self.pr = pr
+        self.ts = assembly.TraceSystem(c.n, c.p, pr.K, pr.method, pr.tau, pr.f_qp, pr.f_const, pr.gD_qp)
+        self.H = multigrid.Hierarchy(self.ts.A, c.n, c.p, smoother=c.smoother, nu_pre=c.nu, nu_post=c.nu)
+        self.gpu = MGSolver(c.n, p=c.p)
+        self.sm = SmootherConfig(kind=c.smoother, nu_pre=c.nu, nu_post=c.nu)
+        self.gpu.setup(pr.K, pr.method, pr.tau, self.sm)
+        self.N = self.gpu.nlevels
+        assert self.N == self.H.N
+
+    def olev(self, level):
+        return self.H.levels[self.N - level]
+
+    def vec(self, level, seed):
+        return W.random_trace_vector(self.gpu.ndof(level), seed)
+
+    def free(self, level):
+        return self.olev(level).free
+
+
+CASES = [(1, 8), (2, 16), (3, 16), (4, 16), (5, 16)]
+
+
+@pytest.fixture(scope="module", params=CASES, ids=[f"c{a}n{b}" for a, b in CASES])
+def case(request):
+    return Case(*request.param)
+
+
+def test_element_dtn_parity(case):
+    """H1: element DtN maps S_T (batched local solves) vs the oracle."""
+    S = case.gpu.element_dtn(case.N).cpu().numpy()
+    So = case.ts.S
+    err = np.abs(S - So).max(axis=(1, 2)) / np.abs(So).max(axis=(1, 2))
+    assert err.max() <= TOL_OP, err.max()
+
+
+def test_apply_parity_every_level(case):
+    """H6 on every level (fine DtN maps, p-coarsened and Galerkin coarse DtN)."""
+    for level in range(case.N, 0, -1):
+        x = case.vec(level, case.cfg.seed_vec + level)
+        y = case.gpu.apply(level, torch.from_numpy(x)).cpu().numpy()
+        L = case.olev(level)
+        fr = L.free
+        yo = L.A @ x[fr]
+        assert rel(y[fr], yo) <= TOL_OP, (level, rel(y[fr], yo))
+        bd = np.setdiff1d(np.arange(len(y)), fr)
+        assert np.all(y[bd] == 0.0)
+
+
+def test_apply_with_oracle_dtn_injected(case):
+    """The fine apply alone, fed the oracle's S_T through the test hook."""
+    gpu = case.gpu
+    gpu.set_element_dtn(case.N, torch.from_numpy(case.ts.S))
+    x = case.vec(case.N, 7)
+    y = gpu.apply(case.N, torch.from_numpy(x)).cpu().numpy()
+    fr = case.ts.free
+    assert rel(y[fr], case.ts.A @ x[fr]) <= TOL_OP
+    case.gpu.setup(case.pr.K, case.pr.method, case.pr.tau, case.sm)   # restore
+
+
+def test_smoother_parity(case):
+    for level in range(case.N, 1, -1):
+        L = case.olev(level)
+        r = case.vec(level, 100 + level)
+        e0 = case.vec(level, 200 + level)
+        for steps in (1, 2, 3):
+            e = case.gpu.smooth(level, torch.from_numpy(r), torch.from_numpy(e0), steps).cpu().numpy()
+            eo = case.H.smooth(case.N - level, e0[L.free], r[L.free], steps)
+            assert rel(e[L.free], eo) <= TOL_OP, (level, steps, rel(e[L.free], eo))
+
+
+def test_transfer_parity(case):
+    for level in range(case.N, 1, -1):
+        li = case.N - level
+        L = case.olev(level)
+        Lc = case.olev(level - 1)
+        res = case.vec(level, 300 + level)
+        rc = case.gpu.restrict(level, torch.from_numpy(res)).cpu().numpy()
+        assert rel(rc[Lc.free], case.H.restrict(li, res[L.free])) <= TOL_OP, level
+        ec = case.vec(level - 1, 400 + level)
+        e0 = case.vec(level, 500 + level)
+        e = case.gpu.prolong(level, torch.from_numpy(ec), torch.from_numpy(e0)).cpu().numpy()
+        eo = e0[L.free] + case.H.prolong(li, ec[Lc.free])
+        assert rel(e[L.free], eo) <= TOL_OP, level
+        if L.kind == "h":
+            e = case.gpu.local_correct(level, torch.from_numpy(res), torch.from_numpy(e0)).cpu().numpy()
+            eo = e0[L.free] + case.H.local_correction(li, res[L.free])
+            assert rel(e[L.free], eo) <= TOL_OP, level
+
+
+def test_chebyshev_lambda_max_parity(case):
+    if case.cfg.smoother != 1:
+        pytest.skip("block-Jacobi")
+    for level in range(case.N, 1, -1):
+        lam = case.gpu.lambda_max(level)
+        assert abs(lam - case.olev(level).lam_max) <= 1e-12 * lam, level
+
+
+def test_vcycle_parity(case):
+    r = case.vec(case.N, 600)
+    z = case.gpu.vcycle(torch.from_numpy(r)).cpu().numpy()
+    fr = case.ts.free
+    zo = case.H.vcycle(r[fr])
+    assert rel(z[fr], zo) <= TOL_OP, rel(z[fr], zo)
+    bd = np.setdiff1d(np.arange(len(z)), fr)
+    assert np.all(z[bd] == 0.0)
+
+
+def test_rhs_parity(case):
+    pr = case.pr
+    g, lam_bc = case.gpu.assemble_rhs(pr.f_qp, pr.f_const, pr.gD_qp)
+    g = g.cpu().numpy()
+    lam_bc = lam_bc.cpu().numpy()
+    fr = case.ts.free
+    assert rel(g[fr], case.ts.g) <= TOL_OP
+    assert np.allclose(lam_bc, case.ts.lam_D, rtol=0, atol=1e-13 * max(1, np.abs(case.ts.lam_D).max()))
+
+
+def test_pcg_parity(case):
+    pr = case.pr
+    g, lam_bc = case.gpu.assemble_rhs(pr.f_qp, pr.f_const, pr.gD_qp)
+    lam, info = case.gpu.pcg_solve(g, rtol=case.cfg.rtol, maxit=2000)
+    res = krylov.pcg(case.ts.A, case.H.vcycle, case.ts.g, rtol=case.cfg.rtol, maxit=2000)
+    assert info["status"] == "converged"
+    assert abs(info["iters"] - res["iters"]) <= 1, (info, res["iters"])
+    lam_full = (lam + lam_bc).cpu().numpy()
+    ref = case.ts.to_full(res["x"])
+    assert rel(lam_full, ref) <= TOL_SOL, rel(lam_full, ref)
+    # the GPU solution solves the oracle's system to the requested tolerance
+    fr = case.ts.free
+    true_rel = np.linalg.norm(case.ts.g - case.ts.A @ lam.cpu().numpy()[fr]) / np.linalg.norm(case.ts.g)
+    assert true_rel <= 3 * case.cfg.rtol
+
+
+def test_solve_host_matches_device_path(case):
+    pr = case.pr
+    lam_h, info = case.gpu.solve_host(pr.K, pr.method, pr.tau, pr.f_qp, pr.f_const, pr.gD_qp,
+                                      case.sm, rtol=case.cfg.rtol)
+    g, lam_bc = case.gpu.assemble_rhs(pr.f_qp, pr.f_const, pr.gD_qp)
+    lam, info2 = case.gpu.pcg_solve(g, rtol=case.cfg.rtol)
+    assert info["iters"] == info2["iters"]
+    assert np.array_equal(lam_h, (lam + lam_bc).cpu().numpy())
+
+
+# ---------------------------------------------------------------- edge cases
+def test_zero_rhs_zero_iterations():
+    from paper_1811_09909_b200 import MGSolver, SmootherConfig
+    s = MGSolver(8, p=2)
+    s.setup(np.ones(64), np.zeros(64, np.int8), np.ones(64), SmootherConfig())
+    lam, info = s.pcg_solve(torch.zeros(s.ndof(), dtype=torch.float64, device="cuda"))
+    assert info["iters"] == 0 and info["status"] == "converged"
+    assert torch.count_nonzero(lam).item() == 0
+
+
+@pytest.mark.parametrize("n,p", [(2, 1), (2, 3), (4, 2), (6, 1), (12, 2), (10, 4)])
+def test_small_and_ragged_meshes(n, p):
+    """n = 2 (the direct level only), n = 6 / 10 / 12 (coarsening stops at an
+    odd or non-2x2 macro mesh, dense coarsest), element counts that are not a
+    multiple of 32 (ragged chunk tails)."""
+    from paper_1811_09909_b200 import MGSolver, SmootherConfig
+    c = W.Config(1, "edge", n=n, p=p, nu=2, smoother=0)
+    pr = W.make_problem(c)
+    ts = assembly.TraceSystem(n, p, pr.K, pr.method, pr.tau, pr.f_qp)
+    H = multigrid.Hierarchy(ts.A, n, p, smoother=0, nu_pre=2, nu_post=2)
+    s = MGSolver(n, p=p)
+    assert s.nlevels == H.N
+    s.setup(pr.K, pr.method, pr.tau, SmootherConfig())
+    x = W.random_trace_vector(s.ndof(), 5)
+    y = s.apply(s.nlevels, torch.from_numpy(x)).cpu().numpy()
+    assert rel(y[ts.free], ts.A @ x[ts.free]) <= TOL_OP
+    z = s.vcycle(torch.from_numpy(x)).cpu().numpy()
+    assert rel(z[ts.free], H.vcycle(x[ts.free])) <= TOL_OP
+    g, _ = s.assemble_rhs(pr.f_qp)
+    lam, info = s.pcg_solve(g)
+    res = krylov.pcg(ts.A, H.vcycle, ts.g)
+    assert abs(info["iters"] - res["iters"]) <= 1
+    assert rel(lam.cpu().numpy()[ts.free], res["x"]) <= TOL_SOL
+
+
+def test_sipg_not_spd_is_reported():
+    """An under-penalised SIPG-H element makes a local or edge block
+    indefinite: the setup returns MG_ERR_NOT_SPD instead of producing garbage."""
+    from paper_1811_09909_b200 import MGError, MGSolver, SmootherConfig
+    s = MGSolver(8, p=3)
+    ne = 64
+    tau = np.full(ne, 1e-3)
+    with pytest.raises(MGError, match="NOT_SPD"):
+        s.setup(np.ones(ne), np.ones(ne, np.int8), tau, SmootherConfig())
+
+
+def test_launch_counts_reported():
+    from paper_1811_09909_b200 import MGSolver, SmootherConfig
+    c = W.CONFIGS[1]
+    pr = W.make_problem(c)
+    s = MGSolver(8, p=1)
+    s.setup(pr.K, pr.method, pr.tau, SmootherConfig())
+    g, _ = s.assemble_rhs(pr.f_qp)
+    _, info = s.pcg_solve(g)
+    assert s.last_launch_count() > 10 * info["iters"]
