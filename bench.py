@@ -1,0 +1,324 @@
+#!/usr/bin/env python3
+"""Benchmark: fine trace DoFs/s of the whole MG-PCG hot path (BASELINE.json
+metric), one JSON line on rank 0.
+
+A step = one pass of the whole hot path over one synthetic problem with its
+inputs (K, method, tau, f samples) already resident in HBM: batched element
+DtN setup + p/h hierarchy + smoother setup (mg_setup_dtn), right-hand side
+(mg_assemble_rhs) and the MG-preconditioned CG solve to 1e-10 (mg_pcg_solve).
+value = trace DoFs (all edges x (p+1), as BASELINE.json counts them) of all
+ranks / max-over-ranks device time per step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
+
+--impl reference times the CPU oracle (oracle/, plain numpy/scipy FP64) on a
+bounded sample of the same workload (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+L2_FLUSH_BYTES = 256 << 20
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def _dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"bench_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
+        under = [s for s in sm if s > 0]
+        return {"sm_mhz": float(np.median(under)) if under else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] + [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_sample_n(cfg, budget_s: float) -> int:
+    """Largest power-of-two sub-mesh (<= cfg.n) the oracle finishes in ~budget_s
+    (calibrated: config-2 recipe at n=256 takes ~20 s on an 8-core host)."""
+    n = cfg.n
+    est = 20.0 * (n / 256.0) ** 2 * ((cfg.p + 1) / 5.0) ** 3
+    while n > 16 and est > budget_s:
+        n //= 2
+        est /= 4.0
+    return n
+
+
+def run_oracle_step(cfg):
+    from oracle import driver
+    pr = W.make_problem(cfg)
+    t0 = time.perf_counter()
+    res = driver.solve_problem(pr)
+    t1 = time.perf_counter()
+    return t1 - t0, res["iters"]
+
+
+def reference_arm(args, cfg):
+    rank, world, _ = _dist_env()
+    if rank != 0:
+        return 0
+    per_step = 180.0 / max(1, args.steps + args.warmup)
+    ns = oracle_sample_n(cfg, per_step)
+    sc = W.scaled_config(cfg.index, ns) if ns != cfg.n else cfg
+    for _ in range(args.warmup):
+        run_oracle_step(sc)
+    times, its = [], []
+    for _ in range(args.steps):
+        t, it = run_oracle_step(sc)
+        times.append(t)
+        its.append(it)
+    tstep = float(np.mean(times))
+    value = sc.trace_dofs / tstep
+    sample = (f"oracle setup+rhs+PCG on the config-{cfg.index} recipe at n={ns} "
+              f"({sc.trace_dofs} trace dofs, {its[-1]} PCG iterations) per step")
+    line = {
+        "impl": "reference", "metric": "fine trace DoFs/s in MG-PCG solve to 1e-10", "value": value,
+        "unit": "trace DoF/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tstep * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "n": cfg.n, "p": cfg.p, "sample_n": ns},
+        "cpu_baseline": {"value": value, "unit": "trace DoF/s", "cores": cpu_threads(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "trace DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, help="BASELINE.json config index (1-5)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true")
+    args = ap.parse_args()
+    cfg = W.CONFIGS[args.config]
+    if args.impl == "reference":
+        return reference_arm(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1811_09909_b200 import MGSolver, smoother_from_config
+
+    rank, world, local = _dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---- inputs resident in HBM (weak scaling: every rank solves its own problem)
+    pr = W.make_problem(cfg)
+    K = torch.from_numpy(pr.K).to(dev)
+    meth = torch.from_numpy(pr.method).to(dev)
+    tau = torch.from_numpy(pr.tau).to(dev)
+    fq = None if pr.f_qp is None else torch.from_numpy(pr.f_qp).to(dev)
+    gD = None if pr.gD_qp is None else torch.from_numpy(pr.gD_qp).to(dev)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        s = MGSolver(cfg.n, p=cfg.p, device=dev, stream=stream)
+    if args.no_graphs:
+        s.use_graphs(False)
+    sm = smoother_from_config(cfg)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    st = {}
+
+    def step():
+        s.setup(K, meth, tau, sm)
+        g, lam_bc = s.assemble_rhs(fq, pr.f_const, gD)
+        lam, info = s.pcg_solve(g, rtol=cfg.rtol, maxit=4000)
+        st["info"] = info
+        return lam
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        clocks = ClockSampler(local)
+        clocks.start()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        launches0 = s.total_launch_count()
+        for k in range(args.steps):
+            flush.fill_(float(k))                     # evict L2 between steps (outside the window)
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize(dev)
+        launches = s.total_launch_count() - launches0
+        ck = clocks.stop()
+        t_ms = sum(a.elapsed_time(b) for a, b in ev)
+        if world > 1:
+            tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_ms = float(tt.item())
+            dist.barrier()
+    ms_per_step = t_ms / args.steps
+    info = st["info"]
+    value = world * cfg.trace_dofs / (ms_per_step * 1e-3)
+
+    # ---- phase breakdown + dominant-kernel roofline (fine-level apply, 2 colour passes)
+    with torch.cuda.stream(stream):
+        def timed(fn, reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            tot = 0.0
+            for _ in range(reps):
+                flush.fill_(1.0)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                torch.cuda.synchronize(dev)
+                tot += a.elapsed_time(b)
+            return tot / reps
+        t_setup = timed(lambda: s.setup(K, meth, tau, sm), 3)
+        g, _ = s.assemble_rhs(fq, pr.f_const, gD)
+        t_solve = timed(lambda: s.pcg_solve(g, rtol=cfg.rtol, maxit=4000), 3)
+        x = torch.rand(s.ndof(), dtype=torch.float64, device=dev)
+        y = torch.empty_like(x)
+        N = s.nlevels
+        t_apply = timed(lambda: s.apply(N, x, y), 10)
+    ne = cfg.n * cfg.n
+    m = 4 * (cfg.p + 1)
+    npk = m * (m + 1) // 2
+    ndof = s.ndof()
+    alg_bytes = ne * 8 * npk + 16 * ndof           # packed S_T + x read + y write
+    peaks = _peaks()
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = alg_bytes / (t_apply * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(cfg.name)
+
+    # ---- end to end through the C ABI with HOST buffers (h2d inputs, d2h solution)
+    e2e = None
+    if rank == 0:
+        Kh = torch.from_numpy(pr.K).pin_memory()
+        mh = torch.from_numpy(pr.method).pin_memory()
+        th = torch.from_numpy(pr.tau).pin_memory()
+        fh = None if pr.f_qp is None else torch.from_numpy(pr.f_qp).pin_memory()
+        gh = None if pr.gD_qp is None else torch.from_numpy(pr.gD_qp).pin_memory()
+        out = torch.empty(ndof, dtype=torch.float64).pin_memory()
+        with torch.cuda.stream(stream):
+            s.solve_host(Kh, mh, th, fh, pr.f_const, gh, sm, cfg.rtol, 4000, out=out.numpy())
+            te = []
+            for _ in range(max(1, min(args.steps, 3))):
+                flush.fill_(2.0)
+                torch.cuda.synchronize(dev)
+                t0 = time.perf_counter()
+                s.solve_host(Kh, mh, th, fh, pr.f_const, gh, sm, cfg.rtol, 4000, out=out.numpy())
+                te.append(time.perf_counter() - t0)
+        h2d = 8 * ne * 2 + ne + (0 if fh is None else 8 * fh.numel()) + (0 if gh is None else 8 * gh.numel())
+        e2e = {"value": cfg.trace_dofs / float(np.mean(te)), "unit": "trace DoF/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * ndof)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ns = oracle_sample_n(cfg, 30.0)
+        sc = W.scaled_config(cfg.index, ns) if ns != cfg.n else cfg
+        t, its = run_oracle_step(sc)
+        cpu = {"value": sc.trace_dofs / t, "unit": "trace DoF/s", "cores": cpu_threads(), "kind": "oracle",
+               "sample": f"one oracle setup+rhs+PCG solve of the config-{cfg.index} recipe at n={ns} "
+                         f"({sc.trace_dofs} trace dofs, {its} iterations, {t:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": "fine trace DoFs/s in MG-PCG solve to 1e-10", "value": value, "unit": "trace DoF/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "n": cfg.n, "p": cfg.p, "trace_dofs": cfg.trace_dofs,
+                       "smoother": "chebyshev" if cfg.smoother else "block-jacobi", "nu": cfg.nu,
+                       "rtol": cfg.rtol, "parallelism": f"replicas{world}" if world > 1 else "1gpu",
+                       "l2": "256 MiB flush between steps (outside the per-step event window)",
+                       "step": "setup_dtn + assemble_rhs + pcg_solve"},
+            "iters": info["iters"], "solve_status": info["status"], "relres": info["relres"],
+            "phases_ms": {"setup": t_setup, "solve": t_solve, "fine_apply": t_apply},
+            "solve_only_dofs_per_s": cfg.trace_dofs / (t_solve * 1e-3),
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_apply<4,*> fine-level colour passes (mg_apply, both colours)",
+                         "alg_bytes_per_apply": alg_bytes,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in peaks
+                         else "fallback 6650 GB/s (B200_PROFILING.md)"},
+            "clocks": ck, "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -496,6 +496,18 @@ int launch_zero(double* dst, int64_t n, cudaStream_t st) {
   return 1;
 }
 
+// dst = src with the dOmega (Dirichlet) entries set to 0 (inputs are ignored there)
+__global__ void k_copy_masked(LevelDev L, double* dst, const double* __restrict__ src) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.ndof;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = edge_on_boundary(L.nx, L.ny, i / L.k1) ? 0.0 : src[i];
+}
+
+int launch_copy_masked(const LevelDev& L, double* dst, const double* src, cudaStream_t st) {
+  k_copy_masked<<<vec_grid(L.ndof), 256, 0, st>>>(L, dst, src);
+  return 1;
+}
+
 __global__ void k_add(double* dst, const double* __restrict__ src, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)

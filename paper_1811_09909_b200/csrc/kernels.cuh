@@ -170,6 +170,7 @@ int launch_lmax_finish(const double* scal, double safety, double ratio, int nu_m
 int launch_set_bj_coef(double omega, double* coef, cudaStream_t st);
 int launch_copy(double* dst, const double* src, int64_t n, cudaStream_t st);
 int launch_zero(double* dst, int64_t n, cudaStream_t st);
+int launch_copy_masked(const LevelDev& L, double* dst, const double* src, cudaStream_t st);
 int launch_add(double* dst, const double* src, int64_t n, cudaStream_t st);
 
 }  // namespace mgdtn

@@ -430,11 +430,12 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
   const int64_t n = F.d.ndof;
   const int vg = vec_grid(n);
   const long long l0 = c->launches;
+  if (c->st == nullptr) c->use_graphs = false;   // legacy stream cannot be captured
   if (c->use_graphs && !c->gA) {
     RC(capture(c, pcg_iter_A, &c->gA, &c->nA));
     RC(capture(c, pcg_iter_B, &c->gB, &c->nB));
   }
-  c->launches += launch_copy(F.r, g, n, st);
+  c->launches += launch_copy_masked(F.d, F.r, g, st);
   CK(cudaMemsetAsync(c->x, 0, n * sizeof(double), st));
   c->launches += launch_dot(F.r, F.r, n, c->part, vg, st);
   c->launches += launch_reduce(c->part, vg, c->scal, 5, 0, nullptr, st);
@@ -659,7 +660,7 @@ int mg_vcycle(void* ctx, const double* r, double* z) {
   if (!c || !r || !z) return MG_ERR_ARG;
   if (!c->setup_done) return fail(c, MG_ERR_STATE, "setup first");
   HostLevel& F = c->lev[0];
-  c->launches += launch_copy(F.r, r, F.d.ndof, c->st);
+  c->launches += launch_copy_masked(F.d, F.r, r, c->st);
   vcycle_level(c, 0, false);
   c->launches += launch_copy(z, F.e, F.d.ndof, c->st);
   CK(cudaGetLastError());
@@ -672,8 +673,8 @@ int mg_smooth(void* ctx, int32_t level, const double* r, double* e, int32_t nste
   if (!c->setup_done) return fail(c, MG_ERR_STATE, "setup first");
   HostLevel* L = level_of(c, level);
   if (!L || L == &c->lev.back()) return fail(c, MG_ERR_ARG, "no smoother on this level");
-  c->launches += launch_copy(L->r, r, L->d.ndof, c->st);
-  c->launches += launch_copy(L->e, e, L->d.ndof, c->st);
+  c->launches += launch_copy_masked(L->d, L->r, r, c->st);
+  c->launches += launch_copy_masked(L->d, L->e, e, c->st);
   for (int s = 0; s < nsteps; ++s) smooth_step(c, *L, s);
   c->launches += launch_copy(e, L->e, L->d.ndof, c->st);
   CK(cudaGetLastError());

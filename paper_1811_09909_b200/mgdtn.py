@@ -123,8 +123,26 @@ class SmootherConfig:
                                self.lmax_iters, self.lmax_safety)
 
 
+class _Ordered:
+    """Order the library stream after the caller's current stream and back."""
+
+    def __init__(self, stream, device):
+        self.s = stream
+        self.cur = torch.cuda.current_stream(device)
+
+    def __enter__(self):
+        if self.cur != self.s:
+            self.s.wait_stream(self.cur)
+        return self
+
+    def __exit__(self, *exc):
+        if self.cur != self.s:
+            self.cur.wait_stream(self.s)
+        return False
+
+
 class MGSolver:
-    """One context of the C ABI on the current CUDA device/stream."""
+    """One context of the C ABI on a CUDA device (own stream unless given)."""
 
     def __init__(self, nx: int, ny: int | None = None, p: int = 1, h: float | None = None,
                  n_h_levels: int = 0, device="cuda", stream: torch.cuda.Stream | None = None):
@@ -133,7 +151,11 @@ class MGSolver:
         self.lib = load_library()
         ny = nx if ny is None else ny
         self.device = torch.device(device)
-        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        # the library works on its own (capturable) stream; every call orders it
+        # after the caller's current stream and the caller after it (_Ordered)
+        self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
         self.nx, self.ny, self.p = nx, ny, p
         mesh = mg_quad_mesh(nx, ny, 0.0, 0.0, h if h is not None else 1.0 / nx)
         ctx = C.c_void_p()
@@ -145,14 +167,24 @@ class MGSolver:
         nb = C.c_size_t()
         self._chk(self.lib.mg_workspace_bytes(self.ctx, C.byref(nb)), "mg_workspace_bytes")
         self.workspace = torch.empty(nb.value, dtype=torch.uint8, device=self.device)
-        self._chk(self.lib.mg_bind_workspace(self.ctx, _ptr(self.workspace), nb.value),
-                  "mg_bind_workspace")
+        with self._ordered():
+            rc = self.lib.mg_bind_workspace(self.ctx, _ptr(self.workspace), nb.value)
+        self._chk(rc, "mg_bind_workspace")
         self.staging = None
         nl = C.c_int32()
         self._chk(self.lib.mg_num_levels(self.ctx, C.byref(nl)), "mg_num_levels")
         self.nlevels = nl.value
 
     # ------------------------------------------------------------------ helpers
+    def _ordered(self):
+        return _Ordered(self.stream, self.device)
+
+    def _call(self, name, *args):
+        """Call an ABI function ordered against the caller's stream; raise on error."""
+        with self._ordered():
+            rc = getattr(self.lib, name)(self.ctx, *args)
+        self._chk(rc, name)
+
     def _chk(self, rc, what):
         if rc != MG_OK:
             msg = self.lib.mg_last_error(self.ctx).decode() if getattr(self, "ctx", None) else ""
@@ -189,52 +221,52 @@ class MGSolver:
         self._m = self._d(method, torch.int8)
         self._tau = self._d(tau)
         cfg = sm.c()
-        self._chk(self.lib.mg_setup_dtn(self.ctx, _ptr(self._K), _ptr(self._m), _ptr(self._tau),
-                                        C.byref(cfg)), "mg_setup_dtn")
+        self._call("mg_setup_dtn", _ptr(self._K), _ptr(self._m), _ptr(self._tau),
+                                        C.byref(cfg))
 
     def assemble_rhs(self, f_qp=None, f_const=0.0, gD_qp=None):
         g = self._vec()
         lam_bc = self._vec()
         f = self._d(f_qp)
         gd = self._d(gD_qp)
-        self._chk(self.lib.mg_assemble_rhs(self.ctx, _ptr(f), float(f_const), _ptr(gd), _ptr(g),
-                                           _ptr(lam_bc)), "mg_assemble_rhs")
+        self._call("mg_assemble_rhs", _ptr(f), float(f_const), _ptr(gd), _ptr(g),
+                                           _ptr(lam_bc))
         return g, lam_bc
 
     def apply(self, level: int, x, y=None):
         x = self._d(x)
         y = self._vec(level) if y is None else y
-        self._chk(self.lib.mg_apply(self.ctx, level, _ptr(x), _ptr(y)), "mg_apply")
+        self._call("mg_apply", level, _ptr(x), _ptr(y))
         return y
 
     def vcycle(self, r, z=None):
         r = self._d(r)
         z = self._vec() if z is None else z
-        self._chk(self.lib.mg_vcycle(self.ctx, _ptr(r), _ptr(z)), "mg_vcycle")
+        self._call("mg_vcycle", _ptr(r), _ptr(z))
         return z
 
     def smooth(self, level: int, r, e, nsteps: int):
         r = self._d(r)
         e = self._d(e).clone()
-        self._chk(self.lib.mg_smooth(self.ctx, level, _ptr(r), _ptr(e), nsteps), "mg_smooth")
+        self._call("mg_smooth", level, _ptr(r), _ptr(e), nsteps)
         return e
 
     def local_correct(self, level: int, res, e):
         res = self._d(res)
         e = self._d(e).clone()
-        self._chk(self.lib.mg_local_correct(self.ctx, level, _ptr(res), _ptr(e)), "mg_local_correct")
+        self._call("mg_local_correct", level, _ptr(res), _ptr(e))
         return e
 
     def restrict(self, level: int, res):
         res = self._d(res)
         rc = self._vec(level - 1)
-        self._chk(self.lib.mg_restrict(self.ctx, level, _ptr(res), _ptr(rc)), "mg_restrict")
+        self._call("mg_restrict", level, _ptr(res), _ptr(rc))
         return rc
 
     def prolong(self, level: int, ec, e):
         ec = self._d(ec)
         e = self._d(e).clone()
-        self._chk(self.lib.mg_prolong(self.ctx, level, _ptr(ec), _ptr(e)), "mg_prolong")
+        self._call("mg_prolong", level, _ptr(ec), _ptr(e))
         return e
 
     def pcg_solve(self, g, rtol=1e-10, maxit=2000, lam=None, history=False):
@@ -243,8 +275,8 @@ class MGSolver:
         it, rel, st = C.c_int32(), C.c_double(), C.c_int32()
         hist = np.zeros(maxit + 1) if history else None
         hp = hist.ctypes.data_as(C.c_void_p) if history else None
-        self._chk(self.lib.mg_pcg_solve(self.ctx, _ptr(g), _ptr(lam), rtol, maxit, C.byref(it),
-                                        C.byref(rel), C.byref(st), hp), "mg_pcg_solve")
+        self._call("mg_pcg_solve", _ptr(g), _ptr(lam), rtol, maxit, C.byref(it),
+                                        C.byref(rel), C.byref(st), hp)
         info = dict(iters=it.value, relres=rel.value, status=STATUS[st.value])
         if history:
             info["hist"] = hist[: it.value + 1]
@@ -280,26 +312,25 @@ class MGSolver:
         out = np.empty(self.ndof()) if out is None else out
         cfg = (smoother or SmootherConfig()).c()
         it, rel, st = C.c_int32(), C.c_double(), C.c_int32()
-        self._chk(self.lib.mg_solve_host(self.ctx, hp(K), hp(method), hp(tau), hp(f_qp), float(f_const),
+        self._call("mg_solve_host", hp(K), hp(method), hp(tau), hp(f_qp), float(f_const),
                                          hp(gD_qp), C.byref(cfg), rtol, maxit, hp(out), C.byref(it),
-                                         C.byref(rel), C.byref(st)), "mg_solve_host")
+                                         C.byref(rel), C.byref(st))
         return out, dict(iters=it.value, relres=rel.value, status=STATUS[st.value])
 
     def element_dtn(self, level: int):
         info = self.level_info(level)
         m = 4 * (info["p"] + 1)
         out = torch.empty((info["nx"] * info["ny"], m, m), dtype=torch.float64, device=self.device)
-        self._chk(self.lib.mg_copy_element_dtn(self.ctx, level, _ptr(out)), "mg_copy_element_dtn")
+        self._call("mg_copy_element_dtn", level, _ptr(out))
         return out
 
     def set_element_dtn(self, level: int, S):
         S = self._d(S)
-        self._chk(self.lib.mg_debug_set_element_dtn(self.ctx, level, _ptr(S)),
-                  "mg_debug_set_element_dtn")
+        self._call("mg_debug_set_element_dtn", level, _ptr(S))
 
     def lambda_max(self, level: int) -> float:
         v = C.c_double()
-        self._chk(self.lib.mg_level_lambda_max(self.ctx, level, C.byref(v)), "mg_level_lambda_max")
+        self._call("mg_level_lambda_max", level, C.byref(v))
         return v.value
 
     def last_launch_count(self) -> int:
