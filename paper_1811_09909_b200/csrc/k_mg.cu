@@ -318,13 +318,12 @@ __global__ void k_reduce(const double* __restrict__ partials, int n, double* sca
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += partials[i];
   s = block_sum(s);
   if (threadIdx.x == 0) {
-    scal[slot] = s;
-    if (op == 1) {  // alpha = rz / pAp (pAp <= 0 is checked by the host: breakdown)
+    if (op == 1) {          // alpha = rz / pAp (pAp <= 0 is checked by the host: breakdown)
       scal[3] = scal[0] / s;
-    } else if (op == 2) {  // beta = rz_new / rz_old ; rz = rz_new
+    } else if (op == 2) {   // beta = rz_new / rz_old, then rz = rz_new
       scal[4] = s / scal[0];
-      scal[0] = s;
     }
+    scal[slot] = s;
   }
 }
 

@@ -346,8 +346,7 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
       c->launches += launch_agglomerate(L.d, C.d, L.KIIinv, L.Pm, c->err, st);
   }
   const int nlev = (int)c->lev.size();
-  int numax = std::max(c->sm.nu_pre, c->sm.nu_post);
-  if (numax < 1) numax = 1;
+  const int numax = MAX_NU;   // coefficients for any step count (mg_smooth may exceed nu)
   for (int li = 0; li < nlev - 1; ++li) {
     HostLevel& L = c->lev[li];
     L.d.smoother = c->sm.kind;

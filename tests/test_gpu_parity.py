@@ -177,6 +177,22 @@ def test_pcg_parity(case):
     assert true_rel <= 3 * case.cfg.rtol
 
 
+def test_pcg_eager_equals_graph_replay(case):
+    """The CUDA-graph replay of an iteration and eager launches give bit-identical
+    results (deterministic reductions, same kernel sequence)."""
+    pr = case.pr
+    g, _ = case.gpu.assemble_rhs(pr.f_qp, pr.f_const, pr.gD_qp)
+    lam1, i1 = case.gpu.pcg_solve(g, rtol=case.cfg.rtol, history=True)
+    case.gpu.use_graphs(False)
+    try:
+        lam2, i2 = case.gpu.pcg_solve(g, rtol=case.cfg.rtol, history=True)
+    finally:
+        case.gpu.use_graphs(True)
+    assert i1["iters"] == i2["iters"]
+    assert torch.equal(lam1, lam2)
+    assert np.array_equal(i1["hist"], i2["hist"])
+
+
 def test_solve_host_matches_device_path(case):
     pr = case.pr
     lam_h, info = case.gpu.solve_host(pr.K, pr.method, pr.tau, pr.f_qp, pr.f_const, pr.gD_qp,
