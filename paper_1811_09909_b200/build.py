@@ -16,13 +16,13 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
 
-SOURCES = ["k_apply.cu", "k_setup.cu", "k_mg.cu", "mgdtn.cu", "refelem.cpp"]
+SOURCES = ["k_apply.cu", "k_setup.cu", "k_mg.cu", "k_coarse.cu", "mgdtn.cu", "refelem.cpp"]
 
 
 def _compile(src: str) -> str:
     out = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
     path = os.path.join(CSRC, src)
-    deps = [path] + [os.path.join(CSRC, h) for h in ("kernels.cuh", "refelem.h")] + \
+    deps = [path] + [os.path.join(CSRC, h) for h in ("kernels.cuh", "bodies.cuh", "tail.h", "refelem.h")] + \
         [os.path.join(ROOT, "include", "mgdtn.h")]
     if os.path.exists(out) and all(os.path.getmtime(out) >= os.path.getmtime(d) for d in deps):
         return out

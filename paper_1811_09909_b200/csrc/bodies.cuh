@@ -1,0 +1,385 @@
+// Device bodies of the V-cycle operations, written as grid-stride loops over
+// (t0, nt) so that the same code runs as a standalone kernel (t0 = global
+// thread id, nt = grid threads) and inside the cluster-resident coarse-tail
+// kernel k_coarse_tail (t0 = rank in the cluster, nt = cluster threads).
+//
+// Transfers: p-level I_N = J_N, Q_{N-1} = J_N^T (per
+// edge); h-levels I_k = [P_M ; J], Q_{k-1} = [P_M^T , J^T] with
+// P_M = -A_II^-1 A_IB J per macro.  Local correction T_k = [A_II^-1 0; 0 0]
+// (Eq. 3.11) per macro.  Smoothers on edge blocks.
+#pragma once
+#include "kernels.cuh"
+
+namespace mgdtn {
+
+// ---------------------------------------------------------------- apply pieces
+template <int K1>
+__device__ __forceinline__ void gather_x(const double* x, const int64_t ed[4], const bool bd[4],
+                                         double* xv) {
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+#pragma unroll
+    for (int a = 0; a < K1; ++a) xv[f * K1 + a] = bd[f] ? 0.0 : x[ed[f] * K1 + a];
+  }
+}
+
+// Epilogue of one element, in two phases so that no load waits behind a store
+// (y / x / d are plain pointers the compiler must assume may alias):
+//   epi_load  -- every value the epilogue reads (y, r, d) is loaded up front
+//                (before the matvec; in the TMA kernel before the stage wait):
+//                AM_APPLY: t = y;  AM_RESID / AM_SMOOTH: t = r - y;  AM_SMOOTH: dd = d
+//   epi_store -- AM_W0: y = y_T;  AM_APPLY: y = t + y_T (dot += x.y);
+//                AM_RESID: y = t - y_T = r - A x;
+//                AM_SMOOTH: res = t - y_T, dn = c2 D_e^-1 res (+ c1 dd), d = dn, x += dn
+// Edges on dOmega: y written as 0 (W0/APPLY/RESID), untouched by AM_SMOOTH.
+// NC: r may be read through the non-coherent path (true unless r is written
+// earlier in the same kernel, as in k_coarse_tail).
+template <int K1, int MODE, bool NC = true>
+__device__ __forceinline__ void epi_load(const LevelDev& L, const int64_t ed[4], const bool bd[4],
+                                         const double* y, const double* __restrict__ r,
+                                         const double* d, double* t, double* dd) {
+  if (MODE == AM_W0) return;
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const int64_t base = ed[f] * K1;
+#pragma unroll
+    for (int a = 0; a < K1; ++a) {
+      const double yo = bd[f] ? 0.0 : y[base + a];
+      if (MODE == AM_APPLY) t[f * K1 + a] = yo;
+      else t[f * K1 + a] = bd[f] ? 0.0 : (NC ? __ldg(r + base + a) : r[base + a]) - yo;
+      if (MODE == AM_SMOOTH) dd[f * K1 + a] = (bd[f] || L.smoother != 1) ? 0.0 : d[base + a];
+    }
+  }
+}
+
+template <int K1, int MODE, bool DOT>
+__device__ __forceinline__ void epi_store(const LevelDev& L, const int64_t ed[4], const bool bd[4],
+                                          const double* xv, const double* yv, const double* t,
+                                          const double* dd, const double* x, double* y, double* d,
+                                          int step, double c1, double c2, double& dot) {
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const int64_t base = ed[f] * K1;
+    if (MODE == AM_W0) {
+#pragma unroll
+      for (int a = 0; a < K1; ++a) y[base + a] = bd[f] ? 0.0 : yv[f * K1 + a];
+    } else if (MODE == AM_APPLY) {
+#pragma unroll
+      for (int a = 0; a < K1; ++a) {
+        const double v = bd[f] ? 0.0 : t[f * K1 + a] + yv[f * K1 + a];
+        y[base + a] = v;
+        if (DOT) dot = fma(xv[f * K1 + a], v, dot);
+      }
+    } else if (MODE == AM_RESID) {
+#pragma unroll
+      for (int a = 0; a < K1; ++a) y[base + a] = bd[f] ? 0.0 : t[f * K1 + a] - yv[f * K1 + a];
+    } else {  // AM_SMOOTH: x is updated in place (x aliases the smoothed iterate)
+      if (!bd[f]) {
+        double res[K1];
+#pragma unroll
+        for (int a = 0; a < K1; ++a) res[a] = t[f * K1 + a] - yv[f * K1 + a];
+        const double* Di = L.Dinv + ed[f];   // SoA: coalesced across neighbouring elements
+        double* xo = const_cast<double*>(x);
+#pragma unroll
+        for (int a = 0; a < K1; ++a) {
+          double c = 0.0;
+#pragma unroll
+          for (int b = 0; b < K1; ++b) c = fma(__ldg(Di + (a * K1 + b) * L.nedge), res[b], c);
+          double dn = c2 * c;
+          if (L.smoother == 1) {
+            if (step > 0) dn = fma(c1, dd[f * K1 + a], dn);
+            d[base + a] = dn;
+          }
+          xo[base + a] = xv[f * K1 + a] + dn;
+        }
+      }
+    }
+  }
+}
+
+// y_T = S_T x_T from a packed symmetric S_T whose entry kk sits at Sp[kk * 32]
+template <int M, typename LD>
+__device__ __forceinline__ void packed_matvec(const double* xv, double* yv, LD load) {
+#pragma unroll
+  for (int a = 0; a < M; ++a) yv[a] = 0.0;
+#pragma unroll
+  for (int a = 0; a < M; ++a) {
+#pragma unroll
+    for (int b = a; b < M; ++b) {
+      const int kk = a * (2 * M - a + 1) / 2 + (b - a);
+      const double sv = load(kk);
+      yv[a] = fma(sv, xv[b], yv[a]);
+      if (b != a) yv[b] = fma(sv, xv[a], yv[b]);
+    }
+  }
+}
+
+// one colour pass over the elements (thread per element, plain loads; used for
+// the L2-resident coarse levels inside k_coarse_tail)
+template <int P, int MODE, bool NC = true>
+__device__ __forceinline__ void apply_pass_body(const LevelDev& L, int colour, const double* x,
+                                                double* y, const double* r, double* d, int step,
+                                                int64_t t0, int64_t nt) {
+  constexpr int K1 = P + 1, M = 4 * K1, NPK = M * (M + 1) / 2;
+  const int64_t nec = L.ne >> 1;
+  double c1 = 0.0, c2 = 0.0;
+  if (MODE == AM_SMOOTH) {
+    c1 = L.coef[2 * step];
+    c2 = L.coef[2 * step + 1];
+  }
+  double dot = 0.0;
+  for (int64_t s = t0; s < nec; s += nt) {
+    int i, j;
+    slot_elem(L.nx, colour, s, i, j);
+    int64_t ed[4];
+    bool bd[4];
+    elem_edges(L.nx, L.ny, i, j, ed, bd);
+    double xv[M], yv[M], t[M], dd[M];
+    gather_x<K1>(x, ed, bd, xv);
+    epi_load<K1, MODE, NC>(L, ed, bd, y, r, d, t, dd);
+    const double* Sp = L.S + ((((int64_t)colour * L.nchunk + (s >> 5)) * NPK) << 5) + (s & 31);
+    packed_matvec<M>(xv, yv, [&](int kk) { return Sp[kk << 5]; });
+    epi_store<K1, MODE, false>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot);
+  }
+}
+
+// ---------------------------------------------------------------- smoothing, first step
+// e = 0 -> first smoothing step needs no apply: e = c2_0 Dinv r (d = e for Chebyshev).
+__device__ __forceinline__ void smooth_first_body(const LevelDev& L, const double* __restrict__ r,
+                                                  double* e, double* d, int64_t t0, int64_t nt) {
+  const int K1 = L.k1;
+  const double c2 = L.coef[1];
+  for (int64_t ed = t0; ed < L.nedge; ed += nt) {
+    if (edge_on_boundary(L.nx, L.ny, ed)) continue;
+    const double* Di = L.Dinv + ed;
+    for (int a = 0; a < K1; ++a) {
+      double c = 0.0;
+      for (int b = 0; b < K1; ++b) c = fma(Di[(a * K1 + b) * L.nedge], r[ed * K1 + b], c);
+      double v = c2 * c;
+      e[ed * K1 + a] = v;
+      if (L.smoother == 1) d[ed * K1 + a] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- local correction + restriction (macro part)
+__device__ __forceinline__ void macro_interior_edges(const LevelDev& F, int I, int J,
+                                                     int64_t ie[4]) {
+  ie[0] = hedge(F.nx, 2 * I, 2 * J + 1);
+  ie[1] = hedge(F.nx, 2 * I + 1, 2 * J + 1);
+  ie[2] = vedge(F.nx, F.ny, 2 * I + 1, 2 * J);
+  ie[3] = vedge(F.nx, F.ny, 2 * I + 1, 2 * J + 1);
+}
+
+// step 3 (e_I += A_II^-1 res_I per macro) and the macro part of Q_{k-1}
+// (cbuf = P_M^T res_I per macro)
+__device__ __forceinline__ void lc_restrict_body(const LevelDev& F, const double* __restrict__ res,
+                                                 double* e, const double* __restrict__ KIIinv,
+                                                 const double* __restrict__ Pm, double* cbuf,
+                                                 int do_lc, int do_restrict, int64_t t0,
+                                                 int64_t nt) {
+  const int nxc = F.nx >> 1;
+  const int64_t nmac = (int64_t)nxc * (F.ny >> 1);
+  for (int64_t M = t0; M < nmac; M += nt) {
+    const int I = (int)(M % nxc), J = (int)(M / nxc);
+    int64_t ie[4];
+    macro_interior_edges(F, I, J, ie);
+    double rI[8];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      rI[2 * l] = res[ie[l] * 2];
+      rI[2 * l + 1] = res[ie[l] * 2 + 1];
+    }
+    if (do_lc) {
+      const double* Ki = KIIinv + M * 64;
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        double c = 0.0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) c = fma(Ki[a * 8 + b], rI[b], c);
+        e[ie[a >> 1] * 2 + (a & 1)] += c;
+      }
+    }
+    if (do_restrict) {
+      const double* P = Pm + M * 64;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        double acc = 0.0;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) acc = fma(P[a * 8 + c], rI[a], acc);
+        cbuf[M * 8 + c] = acc;
+      }
+    }
+  }
+}
+
+// restriction, coarse-edge part: rc = J^T res_B + sum_{M adjacent} (P_M^T res_I)[slot];
+// optionally fused with the coarse level's first smoothing step.
+__device__ __forceinline__ void restrict_edges_body(const LevelDev& F, const LevelDev& C,
+                                                    const double* __restrict__ res,
+                                                    const double* __restrict__ cbuf, double* rc,
+                                                    int fuse, double* ec, double* dc, int64_t t0,
+                                                    int64_t nt) {
+  const int nxc = C.nx, nyc = C.ny;
+  const int64_t nh = (int64_t)nxc * (nyc + 1);
+  const double c2 = fuse ? C.coef[1] : 0.0;
+  for (int64_t E = t0; E < C.nedge; E += nt) {
+    double v0 = 0.0, v1 = 0.0;
+    bool bnd;
+    if (E < nh) {
+      const int J = (int)(E / nxc), I = (int)(E % nxc);
+      bnd = (J == 0 || J == nyc);
+      if (!bnd) {
+        const int64_t f0 = hedge(F.nx, 2 * I, 2 * J), f1 = hedge(F.nx, 2 * I + 1, 2 * J);
+        const double a0 = res[f0 * 2], a1 = res[f0 * 2 + 1], b0 = res[f1 * 2], b1 = res[f1 * 2 + 1];
+        v0 = a0 + 0.5 * a1 + 0.5 * b0;
+        v1 = 0.5 * a1 + 0.5 * b0 + b1;
+        const int64_t Mb = (int64_t)(J - 1) * nxc + I, Ma = (int64_t)J * nxc + I;
+        v0 += cbuf[Mb * 8 + 4] + cbuf[Ma * 8 + 0];
+        v1 += cbuf[Mb * 8 + 5] + cbuf[Ma * 8 + 1];
+      }
+    } else {
+      const int64_t rr = E - nh;
+      const int J = (int)(rr / (nxc + 1)), I = (int)(rr % (nxc + 1));
+      bnd = (I == 0 || I == nxc);
+      if (!bnd) {
+        const int64_t f0 = vedge(F.nx, F.ny, 2 * I, 2 * J), f1 = vedge(F.nx, F.ny, 2 * I, 2 * J + 1);
+        const double a0 = res[f0 * 2], a1 = res[f0 * 2 + 1], b0 = res[f1 * 2], b1 = res[f1 * 2 + 1];
+        v0 = a0 + 0.5 * a1 + 0.5 * b0;
+        v1 = 0.5 * a1 + 0.5 * b0 + b1;
+        const int64_t Ml = (int64_t)J * nxc + (I - 1), Mr = (int64_t)J * nxc + I;
+        v0 += cbuf[Ml * 8 + 2] + cbuf[Mr * 8 + 6];
+        v1 += cbuf[Ml * 8 + 3] + cbuf[Mr * 8 + 7];
+      }
+    }
+    rc[E * 2] = v0;
+    rc[E * 2 + 1] = v1;
+    if (fuse && !bnd) {
+      const double* Di = C.Dinv + E;
+      const int64_t sd = C.nedge;
+      double e0 = c2 * (Di[0] * v0 + Di[sd] * v1);
+      double e1 = c2 * (Di[2 * sd] * v0 + Di[3 * sd] * v1);
+      ec[E * 2] = e0;
+      ec[E * 2 + 1] = e1;
+      if (C.smoother == 1) {
+        dc[E * 2] = e0;
+        dc[E * 2 + 1] = e1;
+      }
+    }
+  }
+}
+
+// prolongation (macro): e_I += P_M e_c(M); e_B += J e_c on the macro's bottom and
+// left macro-edges (every interior macro-edge is the bottom or left edge of
+// exactly one macro).
+__device__ __forceinline__ void prolong_macro_body(const LevelDev& F, const LevelDev& C,
+                                                   const double* __restrict__ ec,
+                                                   const double* __restrict__ Pm, double* e,
+                                                   int64_t t0, int64_t nt) {
+  const int nxc = C.nx, nyc = C.ny;
+  const int64_t nmac = (int64_t)nxc * nyc;
+  for (int64_t M = t0; M < nmac; M += nt) {
+    const int I = (int)(M % nxc), J = (int)(M / nxc);
+    int64_t ce[4];
+    bool cb[4];
+    elem_edges(nxc, nyc, I, J, ce, cb);
+    double c[8];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      c[2 * f] = cb[f] ? 0.0 : ec[ce[f] * 2];
+      c[2 * f + 1] = cb[f] ? 0.0 : ec[ce[f] * 2 + 1];
+    }
+    int64_t ie[4];
+    macro_interior_edges(F, I, J, ie);
+    const double* P = Pm + M * 64;
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      double acc = 0.0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) acc = fma(P[a * 8 + b], c[b], acc);
+      e[ie[a >> 1] * 2 + (a & 1)] += acc;
+    }
+    if (!cb[0]) {  // bottom macro-edge
+      const double c0 = c[0], c1 = c[1], cm = 0.5 * (c0 + c1);
+      const int64_t f0 = hedge(F.nx, 2 * I, 2 * J), f1 = hedge(F.nx, 2 * I + 1, 2 * J);
+      e[f0 * 2] += c0;
+      e[f0 * 2 + 1] += cm;
+      e[f1 * 2] += cm;
+      e[f1 * 2 + 1] += c1;
+    }
+    if (!cb[3]) {  // left macro-edge
+      const double c0 = c[6], c1 = c[7], cm = 0.5 * (c0 + c1);
+      const int64_t f0 = vedge(F.nx, F.ny, 2 * I, 2 * J), f1 = vedge(F.nx, F.ny, 2 * I, 2 * J + 1);
+      e[f0 * 2] += c0;
+      e[f0 * 2 + 1] += cm;
+      e[f1 * 2] += cm;
+      e[f1 * 2 + 1] += c1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- p-level transfers (per edge)
+__device__ __forceinline__ void p_restrict_body(const LevelDev& F, const LevelDev& C,
+                                                const double* __restrict__ Jp,
+                                                const double* __restrict__ res, double* rc,
+                                                int fuse, double* ec, double* dc, int64_t t0,
+                                                int64_t nt) {
+  const int K1 = F.k1;
+  const double c2 = fuse ? C.coef[1] : 0.0;
+  for (int64_t E = t0; E < F.nedge; E += nt) {
+    if (edge_on_boundary(F.nx, F.ny, E)) {
+      rc[E * 2] = 0.0;
+      rc[E * 2 + 1] = 0.0;
+      continue;
+    }
+    double v0 = 0.0, v1 = 0.0;
+    for (int a = 0; a < K1; ++a) {
+      const double x = res[E * K1 + a];
+      v0 = fma(Jp[a * 2], x, v0);
+      v1 = fma(Jp[a * 2 + 1], x, v1);
+    }
+    rc[E * 2] = v0;
+    rc[E * 2 + 1] = v1;
+    if (fuse) {
+      const double* Di = C.Dinv + E;
+      const int64_t sd = C.nedge;
+      double e0 = c2 * (Di[0] * v0 + Di[sd] * v1);
+      double e1 = c2 * (Di[2 * sd] * v0 + Di[3 * sd] * v1);
+      ec[E * 2] = e0;
+      ec[E * 2 + 1] = e1;
+      if (C.smoother == 1) {
+        dc[E * 2] = e0;
+        dc[E * 2 + 1] = e1;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void p_prolong_body(const LevelDev& F, const double* __restrict__ Jp,
+                                               const double* __restrict__ ec, double* e,
+                                               int64_t t0, int64_t nt) {
+  const int K1 = F.k1;
+  for (int64_t E = t0; E < F.nedge; E += nt) {
+    if (edge_on_boundary(F.nx, F.ny, E)) continue;
+    const double c0 = ec[E * 2], c1 = ec[E * 2 + 1];
+    for (int a = 0; a < K1; ++a) e[E * K1 + a] += fma(Jp[a * 2], c0, Jp[a * 2 + 1] * c1);
+  }
+}
+
+// ---------------------------------------------------------------- coarsest solve, vectors
+__device__ __forceinline__ void coarse_solve_body(const int* __restrict__ fidx, int nf,
+                                                  const double* __restrict__ Ainv,
+                                                  const double* __restrict__ r, double* e,
+                                                  int64_t t0, int64_t nt) {
+  for (int64_t t = t0; t < nf; t += nt) {
+    double acc = 0.0;
+    for (int c = 0; c < nf; ++c) acc += Ainv[t * nf + c] * r[fidx[c]];
+    e[fidx[t]] = acc;
+  }
+}
+
+__device__ __forceinline__ void zero_body(double* dst, int64_t n, int64_t t0, int64_t nt) {
+  for (int64_t i = t0; i < n; i += nt) dst[i] = 0.0;
+}
+
+}  // namespace mgdtn

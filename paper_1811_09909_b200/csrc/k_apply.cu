@@ -4,11 +4,25 @@
 // elements (which share no edge with each other) read-modify-write them and
 // run the fused epilogue (residual, smoothing update, dot product).
 //
-// Thread per element; the packed symmetric S_T (npk = m(m+1)/2 doubles) is
-// streamed once with L1-bypassing, L2-evict-first loads (warp-contiguous 256 B
-// segments, see kernels.cuh); x_T (m values) is gathered from the 4 edges.
-// HBM-bound: 8*npk bytes per element against 2*m*m flops.
-#include "kernels.cuh"
+// HBM-bound: 8*npk bytes of packed S_T per element against 2*m*m flops.
+//
+// k_apply_tma (default): persistent one-warp CTAs.  Each CTA owns every
+// gridDim-th chunk of 32 same-colour elements and streams the chunks' packed
+// S_T (npk*256 contiguous bytes, kernels.cuh layout) into an NST-stage
+// shared-memory ring with cp.async.bulk (TMA bulk copy) + mbarrier
+// complete_tx, so that NST chunks (~100 KB per CTA, ~200 KB per SM) are in
+// flight independently of the thread count.  Lane l computes element
+// 32*chunk + l from shared memory (conflict-free: entry kk of the 32 lanes is
+// 256 contiguous bytes).  Launched with programmatic dependent launch inside
+// the solve: the S_T prefetch (S_T is immutable during a solve) overlaps the
+// previous kernel's tail; griddepcontrol.wait precedes every x / y access.
+//
+// k_apply_ldg: the first version (thread per element, direct L1-bypassing
+// loads), kept for A/B measurement (MGDTN_APPLY=ldg).
+#include <cstdlib>
+#include <cstring>
+
+#include "bodies.cuh"
 
 namespace mgdtn {
 
@@ -26,17 +40,169 @@ __device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
   return v;
 }
 
+// ---------------------------------------------------------------- PTX helpers (TMA bulk + mbarrier + PDL)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- TMA-pipelined apply
+template <int P>
+struct TmaCfg {
+  static constexpr int K1 = P + 1, M = 4 * K1, NPK = M * (M + 1) / 2;
+  static constexpr int CHUNK_BYTES = NPK * 32 * 8;
+  // stages per one-warp CTA: ~100 KB of S_T in flight per CTA, 2 CTAs per SM
+  static constexpr int NST = P == 4 ? 2 : P == 3 ? 3 : P == 2 ? 5 : 6;
+  static constexpr int SMEM = NST * CHUNK_BYTES;
+};
+
 template <int P, int MODE, bool DOT>
-__global__ void __launch_bounds__(128) k_apply(const LevelDev L, int colour,
-                                               const double* x, double* y,
-                                               const double* __restrict__ r, double* d,
-                                               int step, double* __restrict__ partials) {
+__global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, const double* x,
+                                                  double* y, const double* __restrict__ r,
+                                                  double* d, int step,
+                                                  double* __restrict__ partials, int early) {
+  using C = TmaCfg<P>;
+  constexpr int K1 = C::K1, M = C::M, NPK = C::NPK, NST = C::NST;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bars[NST];
+  double* stage_buf = reinterpret_cast<double*>(smem_raw);
+  const int lane = threadIdx.x;
+  const int64_t nec = L.ne >> 1;
+  const int nchunk = (int)((nec + 31) >> 5);
+  const double* Sbase = L.S + (int64_t)colour * L.nchunk * NPK * 32;
+  const uint64_t pol = evict_first_policy();
+  // chunks of this CTA: c_k = blockIdx.x + k * gridDim.x
+  const int nmine = (int)blockIdx.x < nchunk ? (nchunk - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto issue = [&](int k) {   // lane 0: chunk k of this CTA into stage k % NST
+    const int c = (int)blockIdx.x + k * (int)gridDim.x;
+    const int s = k % NST;
+    mbar_expect_tx(&bars[s], C::CHUNK_BYTES);
+    tma_bulk_g2s(stage_buf + (size_t)s * NPK * 32, Sbase + (int64_t)c * NPK * 32, C::CHUNK_BYTES,
+                 &bars[s], pol);
+  };
+  if (early) {   // S_T is immutable during a solve: prefetch before the dependency wait
+    if (lane == 0)
+      for (int k = 0; k < NST && k < nmine; ++k) issue(k);
+    pdl_trigger();
+    pdl_wait();
+  } else {
+    pdl_wait();
+    if (lane == 0)
+      for (int k = 0; k < NST && k < nmine; ++k) issue(k);
+    pdl_trigger();
+  }
+  double c1 = 0.0, c2 = 0.0;
+  if (MODE == AM_SMOOTH) {
+    c1 = L.coef[2 * step];
+    c2 = L.coef[2 * step + 1];
+  }
+  double dot = 0.0;
+  for (int k = 0; k < nmine; ++k) {
+    const int c = (int)blockIdx.x + k * (int)gridDim.x;
+    const int64_t s = (int64_t)c * 32 + lane;
+    const bool act = s < nec;
+    int64_t ed[4] = {0, 0, 0, 0};
+    bool bd[4] = {true, true, true, true};
+    double xv[M], yv[M], t[M], dd[M];
+#pragma unroll
+    for (int a = 0; a < M; ++a) {
+      xv[a] = 0.0;
+      yv[a] = 0.0;
+      t[a] = 0.0;
+      dd[a] = 0.0;
+    }
+    if (act) {   // every global read of the element, independent of the stage: overlaps the wait
+      int i, j;
+      slot_elem(L.nx, colour, s, i, j);
+      elem_edges(L.nx, L.ny, i, j, ed, bd);
+      gather_x<K1>(x, ed, bd, xv);
+      epi_load<K1, MODE>(L, ed, bd, y, r, d, t, dd);
+    }
+    const int st = k % NST;
+    mbar_wait(&bars[st], (uint32_t)((k / NST) & 1));
+    const double* Sp = stage_buf + (size_t)st * NPK * 32 + lane;
+#pragma unroll
+    for (int a = 0; a < M; ++a) {
+#pragma unroll
+      for (int b = a; b < M; ++b) {
+        const int kk = a * (2 * M - a + 1) / 2 + (b - a);
+        const double sv = Sp[kk * 32];
+        yv[a] = fma(sv, xv[b], yv[a]);
+        if (b != a) yv[b] = fma(sv, xv[a], yv[b]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && k + NST < nmine) {
+      fence_proxy_async();
+      issue(k + NST);
+    }
+    if (act) epi_store<K1, MODE, DOT>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot);
+  }
+  if (DOT) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if (lane == 0) partials[blockIdx.x] = dot;
+  }
+}
+
+// ---------------------------------------------------------------- direct-load apply (A/B)
+template <int P, int MODE, bool DOT>
+__global__ void __launch_bounds__(128) k_apply_ldg(const LevelDev L, int colour,
+                                                   const double* x, double* y,
+                                                   const double* __restrict__ r, double* d,
+                                                   int step, double* __restrict__ partials,
+                                                   int early) {
+  (void)early;
   constexpr int K1 = P + 1;
   constexpr int M = 4 * K1;
   constexpr int NPK = M * (M + 1) / 2;
   const int64_t nec = L.ne >> 1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const uint64_t pol = evict_first_policy();
+  pdl_wait();
+  pdl_trigger();
   double c1 = 0.0, c2 = 0.0;
   if (MODE == AM_SMOOTH) {
     c1 = L.coef[2 * step];
@@ -49,12 +215,9 @@ __global__ void __launch_bounds__(128) k_apply(const LevelDev L, int colour,
     int64_t ed[4];
     bool bd[4];
     elem_edges(L.nx, L.ny, i, j, ed, bd);
-    double xv[M], yv[M];
-#pragma unroll
-    for (int f = 0; f < 4; ++f) {
-#pragma unroll
-      for (int a = 0; a < K1; ++a) xv[f * K1 + a] = bd[f] ? 0.0 : x[ed[f] * K1 + a];
-    }
+    double xv[M], yv[M], t[M], dd[M];
+    gather_x<K1>(x, ed, bd, xv);
+    epi_load<K1, MODE>(L, ed, bd, y, r, d, t, dd);
 #pragma unroll
     for (int a = 0; a < M; ++a) yv[a] = 0.0;
     const double* Sp = L.S + ((((int64_t)colour * L.nchunk + (s >> 5)) * NPK) << 5) + (s & 31);
@@ -68,45 +231,7 @@ __global__ void __launch_bounds__(128) k_apply(const LevelDev L, int colour,
         if (b != a) yv[b] = fma(sv, xv[a], yv[b]);
       }
     }
-#pragma unroll
-    for (int f = 0; f < 4; ++f) {
-      const int64_t base = ed[f] * K1;
-      if (MODE == AM_W0) {
-#pragma unroll
-        for (int a = 0; a < K1; ++a) y[base + a] = bd[f] ? 0.0 : yv[f * K1 + a];
-      } else if (MODE == AM_APPLY) {
-#pragma unroll
-        for (int a = 0; a < K1; ++a) {
-          double v = bd[f] ? 0.0 : y[base + a] + yv[f * K1 + a];
-          y[base + a] = v;
-          if (DOT) dot = fma(xv[f * K1 + a], v, dot);
-        }
-      } else if (MODE == AM_RESID) {
-#pragma unroll
-        for (int a = 0; a < K1; ++a)
-          y[base + a] = bd[f] ? 0.0 : r[base + a] - (y[base + a] + yv[f * K1 + a]);
-      } else {  // AM_SMOOTH: x is updated in place (x aliases the smoothed iterate)
-        if (!bd[f]) {
-          double res[K1];
-#pragma unroll
-          for (int a = 0; a < K1; ++a) res[a] = r[base + a] - (y[base + a] + yv[f * K1 + a]);
-          const double* Di = L.Dinv + ed[f] * (K1 * K1);
-          double* xo = const_cast<double*>(x);
-#pragma unroll
-          for (int a = 0; a < K1; ++a) {
-            double c = 0.0;
-#pragma unroll
-            for (int b = 0; b < K1; ++b) c = fma(Di[a * K1 + b], res[b], c);
-            double dn = c2 * c;
-            if (L.smoother == 1) {
-              if (step > 0) dn = fma(c1, d[base + a], dn);
-              d[base + a] = dn;
-            }
-            xo[base + a] = xv[f * K1 + a] + dn;
-          }
-        }
-      }
-    }
+    epi_store<K1, MODE, DOT>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot);
   }
   if (DOT) {
     __shared__ double red[4];
@@ -118,45 +243,96 @@ __global__ void __launch_bounds__(128) k_apply(const LevelDev L, int colour,
   }
 }
 
+// ---------------------------------------------------------------- host side
+static bool use_ldg() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MGDTN_APPLY");
+    v = (e && std::strcmp(e, "ldg") == 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
 int apply_grid(const LevelDev& L) {
-  int64_t nec = L.ne / 2;
-  int64_t g = (nec + 127) / 128;
-  const int64_t gmax = 148 * 8;
-  return (int)(g < gmax ? (g > 0 ? g : 1) : gmax);
+  const int64_t nec = L.ne / 2;
+  if (use_ldg()) {
+    int64_t g = (nec + 127) / 128;
+    const int64_t gmax = 148 * 8;
+    return (int)(g < gmax ? (g > 0 ? g : 1) : gmax);
+  }
+  const int64_t nchunk = (nec + 31) / 32;
+  const int64_t gmax = 148 * 2;   // two ~100 KB one-warp CTAs per SM
+  return (int)(nchunk < gmax ? (nchunk > 0 ? nchunk : 1) : gmax);
+}
+
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, bool pdl,
+                     cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+template <int P, int MODE, bool DOT>
+static void launch_one(const LevelDev& L, int colour, const double* x, double* y, const double* r,
+                       double* d, int step, double* partials, int grid, bool pdl,
+                       cudaStream_t st) {
+  if (use_ldg()) {
+    launch_k(k_apply_ldg<P, MODE, DOT>, grid, 128, 0, pdl, st, L, colour, x, y, r, d, step,
+             partials, 0);
+    return;
+  }
+  using C = TmaCfg<P>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_apply_tma<P, MODE, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::SMEM);
+    attr_set = true;
+  }
+  launch_k(k_apply_tma<P, MODE, DOT>, grid, 32, (size_t)C::SMEM, pdl, st, L, colour, x, y, r, d,
+           step, partials, pdl ? 1 : 0);
 }
 
 template <int P>
 static void dispatch_apply(const LevelDev& L, int colour, int mode, const double* x, double* y,
                            const double* r, double* d, int step, double* partials, int grid,
-                           cudaStream_t st) {
+                           bool pdl, cudaStream_t st) {
   switch (mode) {
     case AM_W0:
-      k_apply<P, AM_W0, false><<<grid, 128, 0, st>>>(L, colour, x, y, r, d, step, partials);
+      launch_one<P, AM_W0, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
       break;
     case AM_APPLY:
       if (partials)
-        k_apply<P, AM_APPLY, true><<<grid, 128, 0, st>>>(L, colour, x, y, r, d, step, partials);
+        launch_one<P, AM_APPLY, true>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
       else
-        k_apply<P, AM_APPLY, false><<<grid, 128, 0, st>>>(L, colour, x, y, r, d, step, partials);
+        launch_one<P, AM_APPLY, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
       break;
     case AM_RESID:
-      k_apply<P, AM_RESID, false><<<grid, 128, 0, st>>>(L, colour, x, y, r, d, step, partials);
+      launch_one<P, AM_RESID, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
       break;
     default:
-      k_apply<P, AM_SMOOTH, false><<<grid, 128, 0, st>>>(L, colour, x, y, r, d, step, partials);
+      launch_one<P, AM_SMOOTH, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
       break;
   }
 }
 
 int launch_apply(const LevelDev& L, int colour, int mode, const double* x, double* y,
-                 const double* r, double* d, int step, double* partials, int dot_grid,
+                 const double* r, double* d, int step, double* partials, bool pdl,
                  cudaStream_t st) {
-  int grid = dot_grid > 0 ? dot_grid : apply_grid(L);
+  const int grid = apply_grid(L);
   switch (L.p) {
-    case 1: dispatch_apply<1>(L, colour, mode, x, y, r, d, step, partials, grid, st); break;
-    case 2: dispatch_apply<2>(L, colour, mode, x, y, r, d, step, partials, grid, st); break;
-    case 3: dispatch_apply<3>(L, colour, mode, x, y, r, d, step, partials, grid, st); break;
-    default: dispatch_apply<4>(L, colour, mode, x, y, r, d, step, partials, grid, st); break;
+    case 1: dispatch_apply<1>(L, colour, mode, x, y, r, d, step, partials, grid, pdl, st); break;
+    case 2: dispatch_apply<2>(L, colour, mode, x, y, r, d, step, partials, grid, pdl, st); break;
+    case 3: dispatch_apply<3>(L, colour, mode, x, y, r, d, step, partials, grid, pdl, st); break;
+    default: dispatch_apply<4>(L, colour, mode, x, y, r, d, step, partials, grid, pdl, st); break;
   }
   return 1;
 }

@@ -1,0 +1,138 @@
+// Coarse tail of the V-cycle (Algorithm 1) as ONE launch.
+//
+// Below ~64x64 macro-elements a level's work is a few microseconds of L2
+// traffic, but Algorithm 1 needs ~11 dependent steps per level (smoothing
+// passes, residual, local correction, restriction, prolongation), each of
+// which costs a kernel launch.  k_coarse_tail runs every remaining level --
+// down-sweep, the coarsest direct solve B_1 = A_1^-1 and
+// the up-sweep -- inside one thread-block cluster whose CTAs are separated by
+// hardware cluster barriers (barrier.cluster arrive.release / wait.acquire)
+// instead of kernel boundaries.  The operations are the same device bodies as
+// the standalone kernels (bodies.cuh), in the same order, so results are
+// identical to the launch-per-step V-cycle up to nothing (same arithmetic,
+// same summation order per output).
+#include <cooperative_groups.h>
+
+#include <cstdlib>
+
+#include "bodies.cuh"
+#include "tail.h"
+
+namespace cg = cooperative_groups;
+
+namespace mgdtn {
+
+constexpr int TAIL_TPB = 512;
+
+__global__ void __launch_bounds__(TAIL_TPB, 1) k_coarse_tail(const __grid_constant__ TailParams P) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int64_t t0 = (int64_t)cl.block_rank() * TAIL_TPB + threadIdx.x;
+  const int64_t nt = (int64_t)cl.num_blocks() * TAIL_TPB;
+  auto sync = [&]() { cl.sync(); };
+  const int nlev = P.nlev;
+  // ---- down-sweep: pre-smoothing, residual, step 3 + restriction
+  for (int li = 0; li < nlev - 1; ++li) {
+    const TailLevel& L = P.lev[li];
+    const TailLevel& C = P.lev[li + 1];
+    int s0 = 0;
+    if (P.nu_pre > 0) {
+      const bool first_done = li == 0 ? P.first_fused != 0 : true;
+      if (!first_done) {
+        smooth_first_body(L.d, L.r, L.e, L.dv, t0, nt);
+        sync();
+      }
+      s0 = 1;
+    } else {
+      zero_body(L.e, L.d.ndof, t0, nt);
+      sync();
+    }
+    for (int s = s0; s < P.nu_pre; ++s) {
+      apply_pass_body<1, AM_W0, false>(L.d, 0, L.e, L.w, nullptr, nullptr, 0, t0, nt);
+      sync();
+      apply_pass_body<1, AM_SMOOTH, false>(L.d, 1, L.e, L.w, L.r, L.dv, s, t0, nt);
+      sync();
+    }
+    apply_pass_body<1, AM_W0, false>(L.d, 0, L.e, L.w, nullptr, nullptr, 0, t0, nt);
+    sync();
+    apply_pass_body<1, AM_RESID, false>(L.d, 1, L.e, L.w, L.r, nullptr, 0, t0, nt);
+    sync();
+    lc_restrict_body(L.d, L.w, L.e, L.KIIinv, L.Pm, L.cbuf, 1, 1, t0, nt);
+    sync();
+    const int fuse = (li + 1 < nlev - 1) && P.nu_pre > 0;
+    restrict_edges_body(L.d, C.d, L.w, L.cbuf, C.r, fuse, C.e, C.dv, t0, nt);
+    sync();
+  }
+  // ---- coarsest: B_1 = A_1^-1
+  {
+    const TailLevel& B = P.lev[nlev - 1];
+    coarse_solve_body(P.fidx, P.nf, P.A1inv, B.r, B.e, t0, nt);
+    sync();
+  }
+  // ---- up-sweep: prolongation (step 4) and post-smoothing
+  for (int li = nlev - 2; li >= 0; --li) {
+    const TailLevel& L = P.lev[li];
+    const TailLevel& C = P.lev[li + 1];
+    prolong_macro_body(L.d, C.d, C.e, L.Pm, L.e, t0, nt);
+    sync();
+    for (int s = 0; s < P.nu_post; ++s) {
+      apply_pass_body<1, AM_W0, false>(L.d, 0, L.e, L.w, nullptr, nullptr, 0, t0, nt);
+      sync();
+      apply_pass_body<1, AM_SMOOTH, false>(L.d, 1, L.e, L.w, L.r, L.dv, s, t0, nt);
+      sync();
+    }
+  }
+}
+
+int tail_cluster_size() {
+  static int cs = 0;
+  if (cs == 0) {
+    const char* e = std::getenv("MGDTN_TAIL_CLUSTER");
+    int want = e ? std::atoi(e) : 16;
+    if (want != 1 && want != 2 && want != 4 && want != 8 && want != 16) want = 16;
+    if (want > 8) {
+      if (cudaFuncSetAttribute(k_coarse_tail, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+          cudaSuccess) {
+        cudaGetLastError();
+        want = 8;
+      }
+    }
+    // make sure a cluster of this size can be resident
+    while (want > 1) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(want);
+      cfg.blockDim = dim3(TAIL_TPB);
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = want;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, k_coarse_tail, &cfg) == cudaSuccess && ncl > 0) break;
+      cudaGetLastError();
+      want /= 2;
+    }
+    cs = want;
+  }
+  return cs;
+}
+
+int launch_coarse_tail(const TailParams& P, cudaStream_t st) {
+  const int cs = tail_cluster_size();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cs);
+  cfg.blockDim = dim3(TAIL_TPB);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_coarse_tail, P);
+  return 1;
+}
+
+}  // namespace mgdtn

@@ -4,7 +4,7 @@
 // edge); h-levels I_k = [P_M ; J], Q_{k-1} = [P_M^T , J^T] with
 // P_M = -A_II^-1 A_IB J per macro.  Local correction T_k = [A_II^-1 0; 0 0]
 // (Eq. 3.11) per macro.  Reductions are deterministic two-stage trees.
-#include "kernels.cuh"
+#include "bodies.cuh"
 
 namespace mgdtn {
 
@@ -14,23 +14,12 @@ static inline int cap_grid(int64_t work, int threads, int cap) {
   return (int)(g < cap ? g : cap);
 }
 
-// ---------------------------------------------------------------- smoothing, first step
-// e = 0 -> first smoothing step needs no apply: e = c2_0 Dinv r (d = e for Chebyshev).
+#define GTID ((int64_t)blockIdx.x * blockDim.x + threadIdx.x)
+#define GNT ((int64_t)gridDim.x * blockDim.x)
+
+// ---------------------------------------------------------------- V-cycle operations (bodies.cuh)
 __global__ void k_smooth_first(LevelDev L, const double* __restrict__ r, double* e, double* d) {
-  const int K1 = L.k1;
-  const double c2 = L.coef[1];
-  for (int64_t ed = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ed < L.nedge;
-       ed += (int64_t)gridDim.x * blockDim.x) {
-    if (edge_on_boundary(L.nx, L.ny, ed)) continue;
-    const double* Di = L.Dinv + ed * K1 * K1;
-    for (int a = 0; a < K1; ++a) {
-      double c = 0.0;
-      for (int b = 0; b < K1; ++b) c = fma(Di[a * K1 + b], r[ed * K1 + b], c);
-      double v = c2 * c;
-      e[ed * K1 + a] = v;
-      if (L.smoother == 1) d[ed * K1 + a] = v;
-    }
-  }
+  smooth_first_body(L, r, e, d, GTID, GNT);
 }
 
 int launch_smooth_first(const LevelDev& L, const double* r, double* e, double* d,
@@ -39,52 +28,10 @@ int launch_smooth_first(const LevelDev& L, const double* r, double* e, double* d
   return 1;
 }
 
-// ---------------------------------------------------------------- local correction + restriction (macro part)
-__device__ __forceinline__ void macro_interior_edges(const LevelDev& F, int I, int J,
-                                                     int64_t ie[4]) {
-  ie[0] = hedge(F.nx, 2 * I, 2 * J + 1);
-  ie[1] = hedge(F.nx, 2 * I + 1, 2 * J + 1);
-  ie[2] = vedge(F.nx, F.ny, 2 * I + 1, 2 * J);
-  ie[3] = vedge(F.nx, F.ny, 2 * I + 1, 2 * J + 1);
-}
-
 __global__ void k_lc_restrict(LevelDev F, const double* __restrict__ res, double* e,
                               const double* __restrict__ KIIinv, const double* __restrict__ Pm,
                               double* cbuf, int do_lc, int do_restrict) {
-  const int nxc = F.nx >> 1;
-  const int64_t nmac = (int64_t)nxc * (F.ny >> 1);
-  for (int64_t M = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; M < nmac;
-       M += (int64_t)gridDim.x * blockDim.x) {
-    const int I = (int)(M % nxc), J = (int)(M / nxc);
-    int64_t ie[4];
-    macro_interior_edges(F, I, J, ie);
-    double rI[8];
-#pragma unroll
-    for (int l = 0; l < 4; ++l) {
-      rI[2 * l] = res[ie[l] * 2];
-      rI[2 * l + 1] = res[ie[l] * 2 + 1];
-    }
-    if (do_lc) {
-      const double* Ki = KIIinv + M * 64;
-#pragma unroll
-      for (int a = 0; a < 8; ++a) {
-        double c = 0.0;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) c = fma(Ki[a * 8 + b], rI[b], c);
-        e[ie[a >> 1] * 2 + (a & 1)] += c;
-      }
-    }
-    if (do_restrict) {
-      const double* P = Pm + M * 64;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        double acc = 0.0;
-#pragma unroll
-        for (int a = 0; a < 8; ++a) acc = fma(P[a * 8 + c], rI[a], acc);
-        cbuf[M * 8 + c] = acc;
-      }
-    }
-  }
+  lc_restrict_body(F, res, e, KIIinv, Pm, cbuf, do_lc, do_restrict, GTID, GNT);
 }
 
 int launch_lc_restrict(const LevelDev& F, const double* res, double* e, const double* KIIinv,
@@ -96,59 +43,10 @@ int launch_lc_restrict(const LevelDev& F, const double* res, double* e, const do
   return 1;
 }
 
-// ---------------------------------------------------------------- restriction (coarse-edge part)
-// rc = J^T res_B + sum_{M adjacent} (P_M^T res_I)[slot]; optionally fused with the
-// coarse level's first smoothing step.
 __global__ void k_restrict_edges(LevelDev F, LevelDev C, const double* __restrict__ res,
                                  const double* __restrict__ cbuf, double* rc, int fuse,
                                  double* ec, double* dc) {
-  const int nxc = C.nx, nyc = C.ny;
-  const int64_t nh = (int64_t)nxc * (nyc + 1);
-  const double c2 = fuse ? C.coef[1] : 0.0;
-  for (int64_t E = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; E < C.nedge;
-       E += (int64_t)gridDim.x * blockDim.x) {
-    double v0 = 0.0, v1 = 0.0;
-    bool bnd;
-    if (E < nh) {
-      const int J = (int)(E / nxc), I = (int)(E % nxc);
-      bnd = (J == 0 || J == nyc);
-      if (!bnd) {
-        const int64_t f0 = hedge(F.nx, 2 * I, 2 * J), f1 = hedge(F.nx, 2 * I + 1, 2 * J);
-        const double a0 = res[f0 * 2], a1 = res[f0 * 2 + 1], b0 = res[f1 * 2], b1 = res[f1 * 2 + 1];
-        v0 = a0 + 0.5 * a1 + 0.5 * b0;
-        v1 = 0.5 * a1 + 0.5 * b0 + b1;
-        const int64_t Mb = (int64_t)(J - 1) * nxc + I, Ma = (int64_t)J * nxc + I;
-        v0 += cbuf[Mb * 8 + 4] + cbuf[Ma * 8 + 0];
-        v1 += cbuf[Mb * 8 + 5] + cbuf[Ma * 8 + 1];
-      }
-    } else {
-      const int64_t rr = E - nh;
-      const int J = (int)(rr / (nxc + 1)), I = (int)(rr % (nxc + 1));
-      bnd = (I == 0 || I == nxc);
-      if (!bnd) {
-        const int64_t f0 = vedge(F.nx, F.ny, 2 * I, 2 * J), f1 = vedge(F.nx, F.ny, 2 * I, 2 * J + 1);
-        const double a0 = res[f0 * 2], a1 = res[f0 * 2 + 1], b0 = res[f1 * 2], b1 = res[f1 * 2 + 1];
-        v0 = a0 + 0.5 * a1 + 0.5 * b0;
-        v1 = 0.5 * a1 + 0.5 * b0 + b1;
-        const int64_t Ml = (int64_t)J * nxc + (I - 1), Mr = (int64_t)J * nxc + I;
-        v0 += cbuf[Ml * 8 + 2] + cbuf[Mr * 8 + 6];
-        v1 += cbuf[Ml * 8 + 3] + cbuf[Mr * 8 + 7];
-      }
-    }
-    rc[E * 2] = v0;
-    rc[E * 2 + 1] = v1;
-    if (fuse && !bnd) {
-      const double* Di = C.Dinv + E * 4;
-      double e0 = c2 * (Di[0] * v0 + Di[1] * v1);
-      double e1 = c2 * (Di[2] * v0 + Di[3] * v1);
-      ec[E * 2] = e0;
-      ec[E * 2 + 1] = e1;
-      if (C.smoother == 1) {
-        dc[E * 2] = e0;
-        dc[E * 2 + 1] = e1;
-      }
-    }
-  }
+  restrict_edges_body(F, C, res, cbuf, rc, fuse, ec, dc, GTID, GNT);
 }
 
 int launch_restrict_edges(const LevelDev& F, const LevelDev& C, const double* res,
@@ -159,52 +57,9 @@ int launch_restrict_edges(const LevelDev& F, const LevelDev& C, const double* re
   return 1;
 }
 
-// ---------------------------------------------------------------- prolongation (macro)
-// e_I += P_M e_c(M); e_B += J e_c on the macro's bottom and left macro-edges
-// (every interior macro-edge is the bottom or left edge of exactly one macro).
 __global__ void k_prolong_macro(LevelDev F, LevelDev C, const double* __restrict__ ec,
                                 const double* __restrict__ Pm, double* e) {
-  const int nxc = C.nx, nyc = C.ny;
-  const int64_t nmac = (int64_t)nxc * nyc;
-  for (int64_t M = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; M < nmac;
-       M += (int64_t)gridDim.x * blockDim.x) {
-    const int I = (int)(M % nxc), J = (int)(M / nxc);
-    int64_t ce[4];
-    bool cb[4];
-    elem_edges(nxc, nyc, I, J, ce, cb);
-    double c[8];
-#pragma unroll
-    for (int f = 0; f < 4; ++f) {
-      c[2 * f] = cb[f] ? 0.0 : ec[ce[f] * 2];
-      c[2 * f + 1] = cb[f] ? 0.0 : ec[ce[f] * 2 + 1];
-    }
-    int64_t ie[4];
-    macro_interior_edges(F, I, J, ie);
-    const double* P = Pm + M * 64;
-#pragma unroll
-    for (int a = 0; a < 8; ++a) {
-      double acc = 0.0;
-#pragma unroll
-      for (int b = 0; b < 8; ++b) acc = fma(P[a * 8 + b], c[b], acc);
-      e[ie[a >> 1] * 2 + (a & 1)] += acc;
-    }
-    if (!cb[0]) {  // bottom macro-edge
-      const double c0 = c[0], c1 = c[1], cm = 0.5 * (c0 + c1);
-      const int64_t f0 = hedge(F.nx, 2 * I, 2 * J), f1 = hedge(F.nx, 2 * I + 1, 2 * J);
-      e[f0 * 2] += c0;
-      e[f0 * 2 + 1] += cm;
-      e[f1 * 2] += cm;
-      e[f1 * 2 + 1] += c1;
-    }
-    if (!cb[3]) {  // left macro-edge
-      const double c0 = c[6], c1 = c[7], cm = 0.5 * (c0 + c1);
-      const int64_t f0 = vedge(F.nx, F.ny, 2 * I, 2 * J), f1 = vedge(F.nx, F.ny, 2 * I, 2 * J + 1);
-      e[f0 * 2] += c0;
-      e[f0 * 2 + 1] += cm;
-      e[f1 * 2] += cm;
-      e[f1 * 2 + 1] += c1;
-    }
-  }
+  prolong_macro_body(F, C, ec, Pm, e, GTID, GNT);
 }
 
 int launch_prolong_macro(const LevelDev& F, const LevelDev& C, const double* ec,
@@ -214,39 +69,10 @@ int launch_prolong_macro(const LevelDev& F, const LevelDev& C, const double* ec,
   return 1;
 }
 
-// ---------------------------------------------------------------- p-level transfers (per edge)
 __global__ void k_p_restrict(LevelDev F, LevelDev C, const double* __restrict__ Jp,
                              const double* __restrict__ res, double* rc, int fuse, double* ec,
                              double* dc) {
-  const int K1 = F.k1;
-  const double c2 = fuse ? C.coef[1] : 0.0;
-  for (int64_t E = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; E < F.nedge;
-       E += (int64_t)gridDim.x * blockDim.x) {
-    if (edge_on_boundary(F.nx, F.ny, E)) {
-      rc[E * 2] = 0.0;
-      rc[E * 2 + 1] = 0.0;
-      continue;
-    }
-    double v0 = 0.0, v1 = 0.0;
-    for (int a = 0; a < K1; ++a) {
-      const double x = res[E * K1 + a];
-      v0 = fma(Jp[a * 2], x, v0);
-      v1 = fma(Jp[a * 2 + 1], x, v1);
-    }
-    rc[E * 2] = v0;
-    rc[E * 2 + 1] = v1;
-    if (fuse) {
-      const double* Di = C.Dinv + E * 4;
-      double e0 = c2 * (Di[0] * v0 + Di[1] * v1);
-      double e1 = c2 * (Di[2] * v0 + Di[3] * v1);
-      ec[E * 2] = e0;
-      ec[E * 2 + 1] = e1;
-      if (C.smoother == 1) {
-        dc[E * 2] = e0;
-        dc[E * 2 + 1] = e1;
-      }
-    }
-  }
+  p_restrict_body(F, C, Jp, res, rc, fuse, ec, dc, GTID, GNT);
 }
 
 int launch_p_restrict(const LevelDev& F, const LevelDev& C, const double* Jp,
@@ -259,13 +85,7 @@ int launch_p_restrict(const LevelDev& F, const LevelDev& C, const double* Jp,
 
 __global__ void k_p_prolong(LevelDev F, const double* __restrict__ Jp,
                             const double* __restrict__ ec, double* e) {
-  const int K1 = F.k1;
-  for (int64_t E = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; E < F.nedge;
-       E += (int64_t)gridDim.x * blockDim.x) {
-    if (edge_on_boundary(F.nx, F.ny, E)) continue;
-    const double c0 = ec[E * 2], c1 = ec[E * 2 + 1];
-    for (int a = 0; a < K1; ++a) e[E * K1 + a] += fma(Jp[a * 2], c0, Jp[a * 2 + 1] * c1);
-  }
+  p_prolong_body(F, Jp, ec, e, GTID, GNT);
 }
 
 int launch_p_prolong(const LevelDev& F, const double* Jp, const double* ec, double* e,
@@ -318,8 +138,9 @@ __global__ void k_reduce(const double* __restrict__ partials, int n, double* sca
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += partials[i];
   s = block_sum(s);
   if (threadIdx.x == 0) {
-    if (op == 1) {          // alpha = rz / pAp (pAp <= 0 is checked by the host: breakdown)
-      scal[3] = scal[0] / s;
+    if (op == 1) {          // alpha = rz / pAp; pAp <= 0 is a breakdown (checked by
+                            // k_pcg_check): alpha = 0 keeps x unchanged
+      scal[3] = s > 0.0 ? scal[0] / s : 0.0;
     } else if (op == 2) {   // beta = rz_new / rz_old, then rz = rz_new
       scal[4] = s / scal[0];
     }
@@ -371,6 +192,55 @@ int launch_pcg_pupdate(double* p, const double* z, const double* scal, int64_t n
   return 1;
 }
 
+// ---------------------------------------------------------------- device-side PCG control
+// istate: [0] iteration count, [1] solve status, [2] maxit.  scal[9] = rtol.
+// The whole solve is one CUDA graph whose loop is a conditional WHILE node:
+// this kernel ends every iteration (PAPER.md:1012-1015 normalisation
+// ||r_k|| / ||g||) and decides whether the body runs again -- no host round
+// trip per iteration.  Status codes match include/mgdtn.h.
+__global__ void k_pcg_init(int* istate, double* scal, double rtol, int maxit) {
+  istate[0] = 0;
+  istate[1] = 1;   // MG_MAXIT until decided
+  istate[2] = maxit;
+  scal[9] = rtol;
+}
+
+int launch_pcg_init(int* istate, double* scal, double rtol, int maxit, cudaStream_t st) {
+  k_pcg_init<<<1, 1, 0, st>>>(istate, scal, rtol, maxit);
+  return 1;
+}
+
+__global__ void k_pcg_check(const double* __restrict__ scal, int* istate, double* hist,
+                            int hist_cap, cudaGraphConditionalHandle h) {
+  const double gg = scal[5];
+  int cont = 0;
+  if (!(gg > 0.0)) {   // g = 0 -> lambda = 0 in 0 iterations
+    istate[0] = 0;
+    istate[1] = 0;
+    if (hist_cap > 0) hist[0] = 0.0;
+  } else {
+    const int it = istate[0] + 1;
+    istate[0] = it;
+    if (it == 1 && hist_cap > 0) hist[0] = 1.0;
+    const double pAp = scal[1], rr = scal[2], rtol = scal[9];
+    const double rel = sqrt(rr / gg);
+    if (it < hist_cap) hist[it] = rel;
+    int status = 1;               // MG_MAXIT
+    if (!(pAp > 0.0) || !isfinite(rr)) status = 3;        // MG_BREAKDOWN
+    else if (rel <= rtol) status = 0;                      // MG_CONVERGED
+    else if (rel > 1e6) status = 2;                        // MG_DIVERGED
+    else if (it < istate[2]) cont = 1;
+    istate[1] = status;
+  }
+  cudaGraphSetConditional(h, cont);
+}
+
+int launch_pcg_check(const double* scal, int* istate, double* hist, int hist_cap,
+                     cudaGraphConditionalHandle h, cudaStream_t st) {
+  k_pcg_check<<<1, 1, 0, st>>>(scal, istate, hist, hist_cap, h);
+  return 1;
+}
+
 // ---------------------------------------------------------------- lambda_max (Q11)
 __global__ void k_pow_init(LevelDev L, double* v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.ndof;
@@ -396,10 +266,10 @@ __global__ void k_edge_dinv(LevelDev L, const double* __restrict__ y, double* u,
       for (int a = 0; a < K1; ++a) u[ed * K1 + a] = 0.0;
       continue;
     }
-    const double* Di = L.Dinv + ed * K1 * K1;
+    const double* Di = L.Dinv + ed;
     for (int a = 0; a < K1; ++a) {
       double c = 0.0;
-      for (int b = 0; b < K1; ++b) c = fma(Di[a * K1 + b], y[ed * K1 + b], c);
+      for (int b = 0; b < K1; ++b) c = fma(Di[(a * K1 + b) * L.nedge], y[ed * K1 + b], c);
       u[ed * K1 + a] = c;
       s_uu = fma(c, c, s_uu);
       s_uy = fma(c, y[ed * K1 + a], s_uy);

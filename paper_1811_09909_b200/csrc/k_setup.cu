@@ -1,7 +1,7 @@
 // Setup kernels: batched element-local static condensation (H1), the
 // right-hand side, p-coarsening (H2), per-agglomerate Galerkin coarse DtN
 // (H3), edge-block diagonals (H4) and the coarsest dense factor (H5).
-#include "kernels.cuh"
+#include "bodies.cuh"
 
 namespace mgdtn {
 
@@ -460,9 +460,10 @@ __global__ void k_edge_blocks(LevelDev L, DevError* err) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < L.nedge;
        e += (int64_t)gridDim.x * blockDim.x) {
     double D[MAX_K1 * MAX_K1];
-    double* out = L.Dinv + e * K1 * K1;
+    double* out = L.Dinv + e;   // SoA, stride nedge
+    const int64_t sd = L.nedge;
     if (edge_on_boundary(L.nx, L.ny, e)) {
-      for (int q = 0; q < K1 * K1; ++q) out[q] = 0.0;
+      for (int q = 0; q < K1 * K1; ++q) out[q * sd] = 0.0;
       continue;
     }
     int ei[2], ej[2], ef[2];
@@ -513,7 +514,7 @@ __global__ void k_edge_blocks(LevelDev L, DevError* err) {
         for (int k = a + 1; k < K1; ++k) s -= Lc[k * K1 + a] * v[k];
         v[a] = s / Lc[a * K1 + a];
       }
-      for (int a = 0; a < K1; ++a) out[a * K1 + c] = v[a];
+      for (int a = 0; a < K1; ++a) out[(a * K1 + c) * sd] = v[a];
     }
   }
 }
@@ -634,11 +635,7 @@ int launch_coarse_assemble_factor(const LevelDev& L, const int* fpos, int nf, do
 __global__ void k_coarse_solve(const int* __restrict__ fidx, int nf,
                                const double* __restrict__ Ainv, const double* __restrict__ r,
                                double* e) {
-  for (int t = threadIdx.x; t < nf; t += blockDim.x) {
-    double acc = 0.0;
-    for (int c = 0; c < nf; ++c) acc += Ainv[t * nf + c] * r[fidx[c]];
-    e[fidx[t]] = acc;
-  }
+  coarse_solve_body(fidx, nf, Ainv, r, e, threadIdx.x, blockDim.x);
 }
 
 int launch_coarse_solve(const LevelDev& L, const int* fidx, int nf, const double* A1inv,

@@ -30,7 +30,7 @@ struct LevelDev {
   int64_t ne, nedge, ndof;
   int nchunk;              // chunks of 32 per colour
   double* S;               // interleaved packed DtN
-  double* Dinv;            // [nedge][k1*k1]
+  double* Dinv;            // SoA [k1*k1][nedge]: entry (a,b) of edge e at (a*k1+b)*nedge + e
   double* coef;            // [2*MAX_NU] smoothing coefficients (c1_j, c2_j), device
   int smoother;            // 0 BJ, 1 Chebyshev (d vector used)
 };
@@ -106,8 +106,10 @@ struct RefDev {
 
 // ---------------------------------------------------------------- launchers
 // all launchers return the number of kernels launched (for launch counting)
+// pdl: programmatic dependent launch; the S_T prefetch then starts before the
+// previous kernel finishes, so the previous kernel must not write this level's S_T.
 int launch_apply(const LevelDev& L, int colour, int mode, const double* x, double* y,
-                 const double* r, double* d, int step, double* partials, int dot_grid,
+                 const double* r, double* d, int step, double* partials, bool pdl,
                  cudaStream_t st);
 int apply_grid(const LevelDev& L);   // blocks of the colour passes (partials length)
 
@@ -160,6 +162,9 @@ int launch_pcg_update(double* x, double* r, const double* p, const double* ap,
                       cudaStream_t st);
 int launch_pcg_pupdate(double* p, const double* z, const double* scal, int64_t n,
                        cudaStream_t st);
+int launch_pcg_init(int* istate, double* scal, double rtol, int maxit, cudaStream_t st);
+int launch_pcg_check(const double* scal, int* istate, double* hist, int hist_cap,
+                     cudaGraphConditionalHandle h, cudaStream_t st);
 int launch_pow_init(const LevelDev& L, double* v, cudaStream_t st);
 int launch_edge_dinv(const LevelDev& L, const double* y, double* u, double* partials,
                      int grid, cudaStream_t st);

@@ -5,6 +5,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -13,6 +14,7 @@
 #include "../../include/mgdtn.h"
 #include "kernels.cuh"
 #include "refelem.h"
+#include "tail.h"
 
 namespace mgdtn {
 
@@ -60,9 +62,15 @@ struct Ctx {
   long long last_idx = -1;
   long long launches = 0, last_solve_launches = 0;
   double* pinned = nullptr;
-  cudaGraphExec_t gA = nullptr, gB = nullptr;
-  long long nA = 0, nB = 0;       // kernels per graph
+  cudaGraphExec_t gS = nullptr;   // whole PCG solve: prologue + conditional WHILE loop
+  cudaGraphConditionalHandle cond = 0;
+  long long nPro = 0, nBody = 0;  // kernels in the prologue / in one loop iteration
   bool use_graphs = true;
+  int tail_start = -1;            // first level run by k_coarse_tail (-1: none)
+  TailParams tail{};
+  size_t o_ist = 0, o_hist = 0;
+  int* ist = nullptr;             // device PCG state (k_pcg_check)
+  double* dhist = nullptr;        // device residual history [HIST_CAP]
 };
 
 static int fail(Ctx* c, int code, const std::string& msg, long long idx = -1) {
@@ -91,6 +99,8 @@ static int cuda_check(Ctx* c, cudaError_t e, const char* where) {
   } while (0)
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+constexpr int HIST_CAP = 16384;   // device residual history; larger maxit -> host loop
 
 // ---------------------------------------------------------------- hierarchy
 static void init_level(HostLevel& L, int nx, int ny, int p, double h, int kind) {
@@ -122,6 +132,8 @@ static void layout(Ctx* c) {
   c->o_part = take((size_t)c->npart * sizeof(double));
   c->o_scal = take(16 * sizeof(double));
   c->o_sscal = take(16 * sizeof(double));
+  c->o_ist = take(4 * sizeof(int));
+  c->o_hist = take(HIST_CAP * sizeof(double));
   const int64_t ndofN = c->lev[0].d.ndof;
   c->o_x = take(ndofN * sizeof(double));
   c->o_p = take(ndofN * sizeof(double));
@@ -163,6 +175,8 @@ static void bind_pointers(Ctx* c) {
   c->part = D(c->o_part);
   c->scal = D(c->o_scal);
   c->sscal = D(c->o_sscal);
+  c->ist = reinterpret_cast<int*>(b + c->o_ist);
+  c->dhist = D(c->o_hist);
   c->x = D(c->o_x);
   c->pv = D(c->o_p);
   c->ap = D(c->o_ap);
@@ -219,6 +233,50 @@ static void bind_pointers(Ctx* c) {
   rd.Jp = put(T.Jp);
 }
 
+// Levels from tail_start down run as one cluster-resident launch (k_coarse.cu):
+// p = 1 levels with at most MGDTN_TAIL_NE elements (default 64 x 64; 0 = off).
+static void plan_tail(Ctx* c) {
+  const char* env = std::getenv("MGDTN_TAIL_NE");
+  const long long tail_ne = env ? std::atoll(env) : 4096;
+  const int nlev = (int)c->lev.size();
+  c->tail_start = -1;
+  if (tail_ne <= 0) return;
+  for (int li = 0; li < nlev; ++li) {
+    const LevelDev& d = c->lev[li].d;
+    if (d.p == 1 && d.ne <= tail_ne && nlev - li >= 2 && nlev - li <= MAX_TAIL &&
+        (li == 0 || c->lev[li - 1].kind == KIND_H || c->lev[li - 1].kind == KIND_P)) {
+      bool all_h = true;
+      for (int k = li; k < nlev - 1; ++k) all_h = all_h && c->lev[k].kind == KIND_H;
+      if (all_h) {
+        c->tail_start = li;
+        break;
+      }
+    }
+  }
+}
+
+static void fill_tail(Ctx* c) {
+  if (c->tail_start < 0) return;
+  TailParams& T = c->tail;
+  const int nlev = (int)c->lev.size();
+  T.nlev = nlev - c->tail_start;
+  T.fidx = c->fidx;
+  T.nf = c->nf;
+  T.A1inv = c->A1inv;
+  for (int k = 0; k < T.nlev; ++k) {
+    const HostLevel& L = c->lev[c->tail_start + k];
+    TailLevel& t = T.lev[k];
+    t.d = L.d;
+    t.r = L.r;
+    t.e = L.e;
+    t.w = L.w;
+    t.dv = L.dv;
+    t.KIIinv = L.KIIinv;
+    t.Pm = L.Pm;
+    t.cbuf = L.cbuf;
+  }
+}
+
 static int upload_static(Ctx* c) {
   // reference tables
   std::vector<double> all;
@@ -248,9 +306,8 @@ static int upload_static(Ctx* c) {
 }
 
 static void drop_graphs(Ctx* c) {
-  if (c->gA) cudaGraphExecDestroy(c->gA);
-  if (c->gB) cudaGraphExecDestroy(c->gB);
-  c->gA = c->gB = nullptr;
+  if (c->gS) cudaGraphExecDestroy(c->gS);
+  c->gS = nullptr;
 }
 
 static int check_device_error(Ctx* c) {
@@ -275,18 +332,18 @@ static int check_device_error(Ctx* c) {
 // ---------------------------------------------------------------- apply / smoothing building blocks
 static inline void apply_full(Ctx* c, const HostLevel& L, const double* x, double* y,
                               double* partials) {
-  c->launches += launch_apply(L.d, 0, AM_W0, x, y, nullptr, nullptr, 0, nullptr, 0, c->st);
-  c->launches += launch_apply(L.d, 1, AM_APPLY, x, y, nullptr, nullptr, 0, partials, 0, c->st);
+  c->launches += launch_apply(L.d, 0, AM_W0, x, y, nullptr, nullptr, 0, nullptr, true, c->st);
+  c->launches += launch_apply(L.d, 1, AM_APPLY, x, y, nullptr, nullptr, 0, partials, true, c->st);
 }
 
 static inline void smooth_step(Ctx* c, HostLevel& L, int step) {
-  c->launches += launch_apply(L.d, 0, AM_W0, L.e, L.w, nullptr, nullptr, 0, nullptr, 0, c->st);
-  c->launches += launch_apply(L.d, 1, AM_SMOOTH, L.e, L.w, L.r, L.dv, step, nullptr, 0, c->st);
+  c->launches += launch_apply(L.d, 0, AM_W0, L.e, L.w, nullptr, nullptr, 0, nullptr, true, c->st);
+  c->launches += launch_apply(L.d, 1, AM_SMOOTH, L.e, L.w, L.r, L.dv, step, nullptr, true, c->st);
 }
 
 static inline void residual(Ctx* c, HostLevel& L) {  // L.w = L.r - A L.e
-  c->launches += launch_apply(L.d, 0, AM_W0, L.e, L.w, nullptr, nullptr, 0, nullptr, 0, c->st);
-  c->launches += launch_apply(L.d, 1, AM_RESID, L.e, L.w, L.r, nullptr, 0, nullptr, 0, c->st);
+  c->launches += launch_apply(L.d, 0, AM_W0, L.e, L.w, nullptr, nullptr, 0, nullptr, true, c->st);
+  c->launches += launch_apply(L.d, 1, AM_RESID, L.e, L.w, L.r, nullptr, 0, nullptr, true, c->st);
 }
 
 // V-cycle B_k (Algorithm 1) on level li with input L.r, output L.e.
@@ -297,6 +354,15 @@ static inline void residual(Ctx* c, HostLevel& L) {  // L.w = L.r - A L.e
 static void vcycle_level(Ctx* c, int li, bool first_done) {
   HostLevel& L = c->lev[li];
   const int nlev = (int)c->lev.size();
+  if (li == c->tail_start) {   // this level and every coarser one: one launch
+    TailParams& T = c->tail;
+    T.nu_pre = c->sm.nu_pre;
+    T.nu_post = c->sm.nu_post;
+    T.first_fused = first_done ? 1 : 0;
+    for (int k = 0; k < T.nlev; ++k) T.lev[k].d = c->lev[c->tail_start + k].d;   // smoother kind
+    c->launches += launch_coarse_tail(T, c->st);
+    return;
+  }
   if (li == nlev - 1) {
     c->launches += launch_coarse_solve(L.d, c->fidx, c->nf, c->A1inv, L.r, L.e, c->st);
     return;
@@ -408,15 +474,67 @@ static void pcg_iter_B(Ctx* c) {  // z = B r, beta, p update
   c->launches += launch_pcg_pupdate(c->pv, F.e, c->scal, F.d.ndof, c->st);
 }
 
-static int capture(Ctx* c, void (*body)(Ctx*), cudaGraphExec_t* out, long long* nk) {
+// Rotated PCG loop (same kernel sequence as the textbook loop):
+//   prologue: x = 0; gg = g.g; z = B r; rz = r.z; p = z; A-part; check
+//   body:     B-part (z = B r, beta, p = z + beta p); A-part; check
+static void pcg_prologue(Ctx* c) {
+  HostLevel& F = c->lev[0];
+  const int64_t n = F.d.ndof;
+  const int vg = vec_grid(n);
+  c->launches += launch_zero(c->x, n, c->st);
+  c->launches += launch_dot(F.r, F.r, n, c->part, vg, c->st);
+  c->launches += launch_reduce(c->part, vg, c->scal, 5, 0, nullptr, c->st);
+  vcycle_level(c, 0, false);
+  c->launches += launch_dot(F.r, F.e, n, c->part, vg, c->st);
+  c->launches += launch_reduce(c->part, vg, c->scal, 0, 0, nullptr, c->st);
+  c->launches += launch_copy(c->pv, F.e, n, c->st);
+  pcg_iter_A(c);
+  c->launches += launch_pcg_check(c->scal, c->ist, c->dhist, HIST_CAP, c->cond, c->st);
+}
+
+static void pcg_body(Ctx* c) {
+  pcg_iter_B(c);
+  pcg_iter_A(c);
+  c->launches += launch_pcg_check(c->scal, c->ist, c->dhist, HIST_CAP, c->cond, c->st);
+}
+
+// One graph for the whole solve: the prologue, then a conditional WHILE node
+// whose body is one PCG iteration; k_pcg_check sets the loop condition on the
+// device, so the host synchronises once per solve instead of once per iteration.
+static int capture_solve(Ctx* c) {
   cudaGraph_t g = nullptr;
-  CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
-  const long long before = c->launches;
-  body(c);
-  *nk = c->launches - before;   // kernels in the graph, counted when it runs
-  c->launches = before;
-  CK(cudaStreamEndCapture(c->st, &g));
-  cudaError_t e = cudaGraphInstantiate(out, g, 0);
+  CK(cudaGraphCreate(&g, 0));
+  CK(cudaGraphConditionalHandleCreate(&c->cond, g, 0, cudaGraphCondAssignDefault));
+  const long long l0 = c->launches;
+  CK(cudaStreamBeginCaptureToGraph(c->st, g, nullptr, nullptr, 0,
+                                   cudaStreamCaptureModeThreadLocal));
+  pcg_prologue(c);
+  c->nPro = c->launches - l0;
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  cudaError_t e = cudaStreamGetCaptureInfo(c->st, &cs, nullptr, nullptr, &deps, &nd);
+  std::vector<cudaGraphNode_t> dv(deps, deps + (e == cudaSuccess ? nd : 0));
+  cudaGraph_t gc = nullptr;
+  cudaError_t e2 = cudaStreamEndCapture(c->st, &gc);
+  c->launches = l0;
+  CK(e);
+  CK(e2);
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = c->cond;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cn;
+  CK(cudaGraphAddNode(&cn, g, dv.data(), dv.size(), &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(c->st, body, nullptr, nullptr, 0,
+                                   cudaStreamCaptureModeThreadLocal));
+  pcg_body(c);
+  c->nBody = c->launches - l0;
+  c->launches = l0;
+  CK(cudaStreamEndCapture(c->st, &body));
+  e = cudaGraphInstantiate(&c->gS, g, 0);
   cudaGraphDestroy(g);
   CK(e);
   return MG_OK;
@@ -430,20 +548,46 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
   const int vg = vec_grid(n);
   const long long l0 = c->launches;
   if (c->st == nullptr) c->use_graphs = false;   // legacy stream cannot be captured
-  if (c->use_graphs && !c->gA) {
-    RC(capture(c, pcg_iter_A, &c->gA, &c->nA));
-    RC(capture(c, pcg_iter_B, &c->gB, &c->nB));
-  }
   c->launches += launch_copy_masked(F.d, F.r, g, st);
-  CK(cudaMemsetAsync(c->x, 0, n * sizeof(double), st));
+  int status = MG_MAXIT, it = 0;
+  double rel = 0.0;
+  if (c->use_graphs && maxit < HIST_CAP) {
+    if (!c->gS) RC(capture_solve(c));
+    c->launches += launch_pcg_init(c->ist, c->scal, rtol, maxit, st);
+    CK(cudaGraphLaunch(c->gS, st));
+    CK(cudaMemcpyAsync(c->pinned, c->ist, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int hs[2];
+    std::memcpy(hs, c->pinned, sizeof(hs));
+    it = hs[0];
+    status = hs[1];
+    c->launches += c->nPro + (it > 1 ? (long long)(it - 1) * c->nBody : 0);
+    std::vector<double> hv(it + 1);
+    CK(cudaMemcpyAsync(hv.data(), c->dhist, (it + 1) * sizeof(double), cudaMemcpyDeviceToHost,
+                       st));
+    if (it == 0) {   // g = 0: lambda = 0
+      CK(cudaMemsetAsync(lambda, 0, n * sizeof(double), st));
+    } else {
+      c->launches += launch_copy(lambda, c->x, n, st);
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    rel = hv[it];
+    if (hist) std::memcpy(hist, hv.data(), (it + 1) * sizeof(double));
+    if (iters_out) *iters_out = it;
+    if (relres_out) *relres_out = rel;
+    if (status_out) *status_out = status;
+    c->last_solve_launches = c->launches - l0;
+    return MG_OK;
+  }
+  // eager host-driven loop (use_graphs off, legacy stream, or maxit >= HIST_CAP):
+  // the same kernel sequence, with a host round trip per iteration
+  c->launches += launch_zero(c->x, n, st);
   c->launches += launch_dot(F.r, F.r, n, c->part, vg, st);
   c->launches += launch_reduce(c->part, vg, c->scal, 5, 0, nullptr, st);
   CK(cudaMemcpyAsync(c->pinned, c->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const double gg = c->pinned[5];
-  const double gnorm = std::sqrt(gg);
-  int status = MG_MAXIT, it = 0;
-  double rel = 0.0;
   if (hist) hist[0] = gg > 0 ? 1.0 : 0.0;
   if (!(gg > 0.0)) {   // g = 0 -> lambda = 0 in 0 iterations
     CK(cudaMemsetAsync(lambda, 0, n * sizeof(double), st));
@@ -461,16 +605,11 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
   c->launches += launch_copy(c->pv, F.e, n, st);
   CK(cudaGetLastError());
   for (it = 1; it <= maxit; ++it) {
-    if (c->use_graphs) {
-      CK(cudaGraphLaunch(c->gA, st));
-      c->launches += c->nA;
-    } else {
-      pcg_iter_A(c);
-    }
+    pcg_iter_A(c);
     CK(cudaMemcpyAsync(c->pinned, c->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const double pAp = c->pinned[1], rr = c->pinned[2];
-    rel = std::sqrt(rr) / gnorm;
+    rel = std::sqrt(rr / gg);
     if (hist) hist[it] = rel;
     if (!(pAp > 0.0) || !std::isfinite(rr)) {
       status = MG_BREAKDOWN;
@@ -485,12 +624,7 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
       break;
     }
     if (it == maxit) break;
-    if (c->use_graphs) {
-      CK(cudaGraphLaunch(c->gB, st));
-      c->launches += c->nB;
-    } else {
-      pcg_iter_B(c);
-    }
+    pcg_iter_B(c);
   }
   if (it > maxit) it = maxit;
   c->launches += launch_copy(lambda, c->x, n, st);
@@ -586,6 +720,7 @@ int mg_build_hierarchy(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
     return MG_ERR_SHAPE;
   }
   layout(c);   // host only: no CUDA call until mg_bind_workspace
+  plan_tail(c);
   *out_ctx = c;
   return MG_OK;
 }
@@ -609,6 +744,7 @@ int mg_bind_workspace(void* ctx, void* dev_ptr, size_t bytes) {
   c->ws_bytes = bytes;
   c->setup_done = false;
   bind_pointers(c);
+  fill_tail(c);
   CK(cudaMemsetAsync(c->ws, 0, c->ws_need, c->st));
   return upload_static(c);
 }
@@ -857,6 +993,9 @@ int mg_debug_set_element_dtn(void* ctx, int32_t level, const double* src) {
   if (!L) return MG_ERR_ARG;
   c->launches += launch_dense_to_packed(L->d, src, c->st);
   CK(cudaGetLastError());
+  // the apply kernels prefetch S_T before their dependency wait (PDL): make the
+  // new S_T complete before any later launch
+  CK(cudaStreamSynchronize(c->st));
   return MG_OK;
 }
 

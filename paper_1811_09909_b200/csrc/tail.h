@@ -1,0 +1,28 @@
+// Parameters of the cluster-resident coarse tail of the V-cycle (k_coarse.cu).
+#pragma once
+#include "kernels.cuh"
+
+namespace mgdtn {
+
+constexpr int MAX_TAIL = 16;
+
+struct TailLevel {
+  LevelDev d;
+  double *r, *e, *w, *dv;        // level vectors (r input, e output of B_k)
+  double *KIIinv, *Pm, *cbuf;    // per-macro A_II^-1, P_M, restriction buffer (h-levels)
+};
+
+struct TailParams {
+  int nlev;              // levels in the tail; lev[nlev-1] is the coarsest (direct solve)
+  int nu_pre, nu_post;
+  int first_fused;       // lev[0]'s first pre-smoothing step was done by the upstream restriction
+  const int* fidx;       // coarsest free-dof map and explicit inverse
+  int nf;
+  const double* A1inv;
+  TailLevel lev[MAX_TAIL];
+};
+
+int launch_coarse_tail(const TailParams& P, cudaStream_t st);
+int tail_cluster_size();
+
+}  // namespace mgdtn
