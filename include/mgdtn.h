@@ -193,6 +193,10 @@ int mg_level_info(const void* ctx, int32_t level, int32_t* nx, int32_t* ny, int3
  * order (dst device).  mg_debug_set_element_dtn overwrites them (test hook;
  * the symmetric part's upper triangle is what is stored). */
 int mg_copy_element_dtn(const void* ctx, int32_t level, double* dst);
+/* Element DtN maps of selected elements of a level (full-size parity sampling):
+ * elems: device int64 [n] element ids (j*nx+i), dst: device [n][m][m]. */
+int mg_gather_element_dtn(const void* ctx, int32_t level, const int64_t* elems, int64_t n,
+                          double* dst);
 int mg_debug_set_element_dtn(void* ctx, int32_t level, const double* src);
 /* Chebyshev lambda_max estimate of a level (host out; 0 if not Chebyshev). */
 int mg_level_lambda_max(const void* ctx, int32_t level, double* lam);

@@ -56,6 +56,19 @@ def p_injection_full(n: int, p: int) -> sp.csr_matrix:
                          shape=(E * k, E * 2)).tocsr()
 
 
+def p_coarsen_element(S: np.ndarray, p: int) -> np.ndarray:
+    """Element form of Eq. ANm1: S^(1)_T = J_p^T S_T J_p for
+    a batch S [ne, 4(p+1), 4(p+1)] of order-p element DtN maps, J_p the
+    per-edge P1 -> P^p nodal injection of p_injection_full (local dof f*(p+1)+a
+    <- (1 - s_a) c_(f,0) + s_a c_(f,1)).  Summed over elements this is the
+    global J_N^T A_N J_N (pinned against it in tests/test_oracle_multigrid.py).
+    """
+    s = gll_nodes(p)
+    j1 = np.stack([1.0 - s, s], axis=1)            # [(p+1), 2]
+    J = np.kron(np.eye(4), j1)                     # [4(p+1), 8]
+    return np.einsum("ai,eab,bj->eij", J, S, J)
+
+
 def h_injection_full(n: int) -> sp.csr_matrix:
     """J_k: coarse P1 macro-edge functions -> fine P1 on its two halves.
 

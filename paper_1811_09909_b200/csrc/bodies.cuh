@@ -31,6 +31,7 @@ __device__ __forceinline__ void gather_x(const double* x, const int64_t ed[4], c
 //   epi_store -- AM_W0: y = y_T;  AM_APPLY: y = t + y_T (dot += x.y);
 //                AM_RESID: y = t - y_T = r - A x;
 //                AM_SMOOTH: res = t - y_T, dn = c2 D_e^-1 res (+ c1 dd), d = dn, x += dn
+//                AM_DINV: y = t + y_T = A x, x = D_e^-1 (A x) (dot += x_new . y)
 // Edges on dOmega: y written as 0 (W0/APPLY/RESID), untouched by AM_SMOOTH.
 // NC: r may be read through the non-coherent path (true unless r is written
 // earlier in the same kernel, as in k_coarse_tail).
@@ -45,7 +46,7 @@ __device__ __forceinline__ void epi_load(const LevelDev& L, const int64_t ed[4],
 #pragma unroll
     for (int a = 0; a < K1; ++a) {
       const double yo = bd[f] ? 0.0 : y[base + a];
-      if (MODE == AM_APPLY) t[f * K1 + a] = yo;
+      if (MODE == AM_APPLY || MODE == AM_DINV) t[f * K1 + a] = yo;
       else t[f * K1 + a] = bd[f] ? 0.0 : (NC ? __ldg(r + base + a) : r[base + a]) - yo;
       if (MODE == AM_SMOOTH) dd[f * K1 + a] = (bd[f] || L.smoother != 1) ? 0.0 : d[base + a];
     }
@@ -73,6 +74,28 @@ __device__ __forceinline__ void epi_store(const LevelDev& L, const int64_t ed[4]
     } else if (MODE == AM_RESID) {
 #pragma unroll
       for (int a = 0; a < K1; ++a) y[base + a] = bd[f] ? 0.0 : t[f * K1 + a] - yv[f * K1 + a];
+    } else if (MODE == AM_DINV) {  // power iteration on D^-1 A: x <- D^-1 A x in place
+      if (!bd[f]) {
+        double yf[K1];
+#pragma unroll
+        for (int a = 0; a < K1; ++a) {
+          yf[a] = t[f * K1 + a] + yv[f * K1 + a];
+          y[base + a] = yf[a];
+        }
+        const double* Di = L.Dinv + ed[f];
+        double* xo = const_cast<double*>(x);
+#pragma unroll
+        for (int a = 0; a < K1; ++a) {
+          double c = 0.0;
+#pragma unroll
+          for (int b = 0; b < K1; ++b) c = fma(__ldg(Di + (a * K1 + b) * L.nedge), yf[b], c);
+          xo[base + a] = c;
+          if (DOT) dot = fma(c, yf[a], dot);   // v_{k+1} . D v_{k+1}  (D v_{k+1} = A v_k)
+        }
+      } else {
+#pragma unroll
+        for (int a = 0; a < K1; ++a) y[base + a] = 0.0;
+      }
     } else {  // AM_SMOOTH: x is updated in place (x aliases the smoothed iterate)
       if (!bd[f]) {
         double res[K1];
@@ -116,10 +139,10 @@ __device__ __forceinline__ void packed_matvec(const double* xv, double* yv, LD l
 
 // one colour pass over the elements (thread per element, plain loads; used for
 // the L2-resident coarse levels inside k_coarse_tail)
-template <int P, int MODE, bool NC = true>
-__device__ __forceinline__ void apply_pass_body(const LevelDev& L, int colour, const double* x,
-                                                double* y, const double* r, double* d, int step,
-                                                int64_t t0, int64_t nt) {
+template <int P, int MODE, bool NC = true, bool DOT = false>
+__device__ __forceinline__ double apply_pass_body(const LevelDev& L, int colour, const double* x,
+                                                  double* y, const double* r, double* d, int step,
+                                                  int64_t t0, int64_t nt) {
   constexpr int K1 = P + 1, M = 4 * K1, NPK = M * (M + 1) / 2;
   const int64_t nec = L.ne >> 1;
   double c1 = 0.0, c2 = 0.0;
@@ -139,7 +162,16 @@ __device__ __forceinline__ void apply_pass_body(const LevelDev& L, int colour, c
     epi_load<K1, MODE, NC>(L, ed, bd, y, r, d, t, dd);
     const double* Sp = L.S + ((((int64_t)colour * L.nchunk + (s >> 5)) * NPK) << 5) + (s & 31);
     packed_matvec<M>(xv, yv, [&](int kk) { return Sp[kk << 5]; });
-    epi_store<K1, MODE, false>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot);
+    epi_store<K1, MODE, DOT>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot);
+  }
+  return dot;
+}
+
+// power-iteration start vector (Q11): v_i = 1 + (i mod 7)/7 on free dofs, i = dof id
+__device__ __forceinline__ void pow_init_body(const LevelDev& L, double* v, int64_t t0, int64_t nt) {
+  for (int64_t i = t0; i < L.ndof; i += nt) {
+    const int64_t e = i / L.k1;
+    v[i] = edge_on_boundary(L.nx, L.ny, e) ? 0.0 : 1.0 + (double)(i % 7) / 7.0;
   }
 }
 
@@ -380,6 +412,30 @@ __device__ __forceinline__ void coarse_solve_body(const int* __restrict__ fidx, 
 
 __device__ __forceinline__ void zero_body(double* dst, int64_t n, int64_t t0, int64_t nt) {
   for (int64_t i = t0; i < n; i += nt) dst[i] = 0.0;
+}
+
+// Power iteration (Q11) without per-step normalisation: v_{k+1} = D^-1 A v_k
+// (the Rayleigh quotient is scale invariant).  scal[7] = v.Dv (v = v_last,
+// D v_last = A v_{last-1}), scal[8] = v.Av.  lambda_hat = safety * v.Av / v.Dv.
+// Chebyshev coefficients (O8): theta = (b+a)/2, delta = (b-a)/2, sigma = theta/delta,
+// step 0: c1 = 0, c2 = 1/theta; step k: rho_k = 1/(2 sigma - rho_{k-1}),
+// c1 = rho_k rho_{k-1}, c2 = 2 rho_k / delta.
+__device__ __forceinline__ void lmax_finish_body(double vAv, double vDv, double safety,
+                                                 double ratio, int nu_max, double* lam_out,
+                                                 double* coef) {
+  const double lam = safety * vAv / vDv;
+  *lam_out = lam;
+  const double b = lam, a = lam / ratio;
+  const double theta = 0.5 * (b + a), delta = 0.5 * (b - a), sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  coef[0] = 0.0;
+  coef[1] = 1.0 / theta;
+  for (int k = 1; k < nu_max; ++k) {
+    const double rn = 1.0 / (2.0 * sigma - rho);
+    coef[2 * k] = rn * rho;
+    coef[2 * k + 1] = 2.0 * rn / delta;
+    rho = rn;
+  }
 }
 
 }  // namespace mgdtn

@@ -77,28 +77,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
 
 // ---------------------------------------------------------------- TMA-pipelined apply
 template <int P>
 struct TmaCfg {
   static constexpr int K1 = P + 1, M = 4 * K1, NPK = M * (M + 1) / 2;
   static constexpr int CHUNK_BYTES = NPK * 32 * 8;
-  // stages per one-warp CTA: ~100 KB of S_T in flight per CTA, 2 CTAs per SM
-  static constexpr int NST = P == 4 ? 2 : P == 3 ? 3 : P == 2 ? 5 : 6;
-  static constexpr int SMEM = NST * CHUNK_BYTES;
+  // stages per one-warp CTA and CTAs per SM (measured sweep, profiles/r01_tma_sweep.jsonl):
+  // more resident warps hide the x-gather / y read-modify-write latency better
+  // than deeper per-CTA rings
+  static constexpr int NST = P == 4 ? 2 : P == 3 ? 2 : P == 2 ? 2 : 4;
+  static constexpr int CPS = P == 4 ? 2 : P == 3 ? 3 : P == 2 ? 4 : 6;
 };
 
-template <int P, int MODE, bool DOT>
+template <int P, int MODE, bool DOT, int NST>
 __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, const double* x,
                                                   double* y, const double* __restrict__ r,
                                                   double* d, int step,
                                                   double* __restrict__ partials, int early) {
   using C = TmaCfg<P>;
-  constexpr int K1 = C::K1, M = C::M, NPK = C::NPK, NST = C::NST;
+  constexpr int K1 = C::K1, M = C::M, NPK = C::NPK;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bars[NST];
   double* stage_buf = reinterpret_cast<double*>(smem_raw);
@@ -253,6 +251,22 @@ static bool use_ldg() {
   return v == 1;
 }
 
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+static int tma_cps(int p) {   // CTAs per SM (tuning knob MGDTN_TMA_CPS, 0 = per-p default)
+  static int v = -1;
+  if (v < 0) v = env_int("MGDTN_TMA_CPS", 0);
+  if (v > 0) return v;
+  return p == 4 ? TmaCfg<4>::CPS : p == 3 ? TmaCfg<3>::CPS : p == 2 ? TmaCfg<2>::CPS : TmaCfg<1>::CPS;
+}
+static int tma_nst() {   // stages per CTA (tuning knob MGDTN_TMA_NST, 0 = per-p default)
+  static int v = -1;
+  if (v < 0) v = env_int("MGDTN_TMA_NST", 0);
+  return v;
+}
+
 int apply_grid(const LevelDev& L) {
   const int64_t nec = L.ne / 2;
   if (use_ldg()) {
@@ -261,24 +275,23 @@ int apply_grid(const LevelDev& L) {
     return (int)(g < gmax ? (g > 0 ? g : 1) : gmax);
   }
   const int64_t nchunk = (nec + 31) / 32;
-  const int64_t gmax = 148 * 2;   // two ~100 KB one-warp CTAs per SM
+  const int64_t gmax = 148 * tma_cps(L.p);
   return (int)(nchunk < gmax ? (nchunk > 0 ? nchunk : 1) : gmax);
 }
 
-template <typename... KArgs, typename... Args>
-static void launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, bool pdl,
-                     cudaStream_t st, Args... args) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+template <int P, int MODE, bool DOT, int NST>
+static void launch_tma(const LevelDev& L, int colour, const double* x, double* y, const double* r,
+                       double* d, int step, double* partials, int grid, bool pdl,
+                       cudaStream_t st) {
+  const size_t smem = (size_t)NST * TmaCfg<P>::CHUNK_BYTES;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_apply_tma<P, MODE, DOT, NST>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  launch_ex(k_apply_tma<P, MODE, DOT, NST>, grid, 32, smem, pdl, st, L, colour, x, y, r, d, step,
+           partials, pdl ? 1 : 0);
 }
 
 template <int P, int MODE, bool DOT>
@@ -286,19 +299,20 @@ static void launch_one(const LevelDev& L, int colour, const double* x, double* y
                        double* d, int step, double* partials, int grid, bool pdl,
                        cudaStream_t st) {
   if (use_ldg()) {
-    launch_k(k_apply_ldg<P, MODE, DOT>, grid, 128, 0, pdl, st, L, colour, x, y, r, d, step,
+    launch_ex(k_apply_ldg<P, MODE, DOT>, grid, 128, 0, pdl, st, L, colour, x, y, r, d, step,
              partials, 0);
     return;
   }
   using C = TmaCfg<P>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_apply_tma<P, MODE, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         C::SMEM);
-    attr_set = true;
+  int nst = tma_nst();
+  if (nst <= 0 || nst * C::CHUNK_BYTES > 220 * 1024) nst = C::NST;
+  switch (nst) {
+    case 2: launch_tma<P, MODE, DOT, 2>(L, colour, x, y, r, d, step, partials, grid, pdl, st); break;
+    case 3: launch_tma<P, MODE, DOT, 3>(L, colour, x, y, r, d, step, partials, grid, pdl, st); break;
+    case 4: launch_tma<P, MODE, DOT, 4>(L, colour, x, y, r, d, step, partials, grid, pdl, st); break;
+    case 5: launch_tma<P, MODE, DOT, 5>(L, colour, x, y, r, d, step, partials, grid, pdl, st); break;
+    default: launch_tma<P, MODE, DOT, 6>(L, colour, x, y, r, d, step, partials, grid, pdl, st); break;
   }
-  launch_k(k_apply_tma<P, MODE, DOT>, grid, 32, (size_t)C::SMEM, pdl, st, L, colour, x, y, r, d,
-           step, partials, pdl ? 1 : 0);
 }
 
 template <int P>
@@ -317,6 +331,12 @@ static void dispatch_apply(const LevelDev& L, int colour, int mode, const double
       break;
     case AM_RESID:
       launch_one<P, AM_RESID, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
+      break;
+    case AM_DINV:
+      if (partials)
+        launch_one<P, AM_DINV, true>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
+      else
+        launch_one<P, AM_DINV, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
       break;
     default:
       launch_one<P, AM_SMOOTH, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);

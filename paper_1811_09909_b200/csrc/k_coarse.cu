@@ -25,10 +25,17 @@ namespace mgdtn {
 constexpr int TAIL_TPB = 512;
 
 __global__ void __launch_bounds__(TAIL_TPB, 1) k_coarse_tail(const __grid_constant__ TailParams P) {
+  pdl_enter();
   cg::cluster_group cl = cg::this_cluster();
   const int64_t t0 = (int64_t)cl.block_rank() * TAIL_TPB + threadIdx.x;
   const int64_t nt = (int64_t)cl.num_blocks() * TAIL_TPB;
-  auto sync = [&]() { cl.sync(); };
+  // one CTA: a CTA barrier keeps the (small, L1-resident) level data in L1;
+  // a cluster barrier's acquire invalidates it
+  const bool single = cl.num_blocks() == 1;
+  auto sync = [&]() {
+    if (single) __syncthreads();
+    else cl.sync();
+  };
   const int nlev = P.nlev;
   // ---- down-sweep: pre-smoothing, residual, step 3 + restriction
   for (int li = 0; li < nlev - 1; ++li) {
@@ -83,12 +90,70 @@ __global__ void __launch_bounds__(TAIL_TPB, 1) k_coarse_tail(const __grid_consta
   }
 }
 
+// deterministic cluster-wide sum: CTA sums (fixed shuffle tree) -> part[rank]
+// -> every thread adds part[0..ncta) in order
+__device__ double cluster_sum(cg::cluster_group& cl, double v, double* part) {
+  __shared__ double red[TAIL_TPB / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < TAIL_TPB / 32; ++w) s += red[w];
+    part[cl.block_rank()] = s;
+  }
+  if (cl.num_blocks() == 1) __syncthreads();
+  else cl.sync();
+  double s = 0.0;
+  for (unsigned b = 0; b < cl.num_blocks(); ++b) s += part[b];
+  if (cl.num_blocks() == 1) __syncthreads();   // part / red reusable afterwards
+  else cl.sync();
+  return s;
+}
+
+// Chebyshev lambda_max of D_B^-1 A_k (Q11) for every tail level except the
+// coarsest: power iteration v <- D^-1 A v (AM_DINV epilogue, in place), then
+// lambda = safety * v.Av / v.Dv and the Chebyshev coefficients.
+__global__ void __launch_bounds__(TAIL_TPB, 1)
+    k_tail_lmax(const __grid_constant__ TailParams P, int iters, double safety, double ratio,
+                int nu_max, double* part) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int64_t t0 = (int64_t)cl.block_rank() * TAIL_TPB + threadIdx.x;
+  const int64_t nt = (int64_t)cl.num_blocks() * TAIL_TPB;
+  const bool single = cl.num_blocks() == 1;
+  auto sync = [&]() {
+    if (single) __syncthreads();
+    else cl.sync();
+  };
+  for (int li = 0; li < P.nlev - 1; ++li) {
+    const TailLevel& L = P.lev[li];
+    pow_init_body(L.d, L.e, t0, nt);
+    sync();
+    double vDv_t = 0.0;
+    for (int it = 0; it < iters; ++it) {
+      apply_pass_body<1, AM_W0, false>(L.d, 0, L.e, L.w, nullptr, nullptr, 0, t0, nt);
+      sync();
+      vDv_t = apply_pass_body<1, AM_DINV, false, true>(L.d, 1, L.e, L.w, nullptr, nullptr, 0, t0, nt);
+      sync();
+    }
+    const double vDv = cluster_sum(cl, vDv_t, part);
+    apply_pass_body<1, AM_W0, false>(L.d, 0, L.e, L.w, nullptr, nullptr, 0, t0, nt);
+    sync();
+    const double vAv_t =
+        apply_pass_body<1, AM_APPLY, false, true>(L.d, 1, L.e, L.w, nullptr, nullptr, 0, t0, nt);
+    const double vAv = cluster_sum(cl, vAv_t, part);
+    if (t0 == 0) lmax_finish_body(vAv, vDv, safety, ratio, nu_max, L.lam, L.d.coef);
+    sync();
+  }
+}
+
 int tail_cluster_size() {
   static int cs = 0;
   if (cs == 0) {
     const char* e = std::getenv("MGDTN_TAIL_CLUSTER");
-    int want = e ? std::atoi(e) : 16;
-    if (want != 1 && want != 2 && want != 4 && want != 8 && want != 16) want = 16;
+    int want = e ? std::atoi(e) : 1;
+    if (want != 1 && want != 2 && want != 4 && want != 8 && want != 16) want = 1;
     if (want > 8) {
       if (cudaFuncSetAttribute(k_coarse_tail, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
           cudaSuccess) {
@@ -118,7 +183,8 @@ int tail_cluster_size() {
   return cs;
 }
 
-int launch_coarse_tail(const TailParams& P, cudaStream_t st) {
+int launch_tail_lmax(const TailParams& P, int iters, double safety, double ratio, int nu_max,
+                     double* part, cudaStream_t st) {
   const int cs = tail_cluster_size();
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(cs);
@@ -131,6 +197,26 @@ int launch_coarse_tail(const TailParams& P, cudaStream_t st) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  if (cs > 8) cudaFuncSetAttribute(k_tail_lmax, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchKernelEx(&cfg, k_tail_lmax, P, iters, safety, ratio, nu_max, part);
+  return 1;
+}
+
+int launch_coarse_tail(const TailParams& P, cudaStream_t st) {
+  const int cs = tail_cluster_size();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cs);
+  cfg.blockDim = dim3(TAIL_TPB);
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
   cudaLaunchKernelEx(&cfg, k_coarse_tail, P);
   return 1;
 }

@@ -4,9 +4,20 @@
 // edge); h-levels I_k = [P_M ; J], Q_{k-1} = [P_M^T , J^T] with
 // P_M = -A_II^-1 A_IB J per macro.  Local correction T_k = [A_II^-1 0; 0 0]
 // (Eq. 3.11) per macro.  Reductions are deterministic two-stage trees.
+#include <cstdlib>
+
 #include "bodies.cuh"
 
 namespace mgdtn {
+
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MGDTN_PDL");
+    v = (e && std::atoi(e) == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
 
 static inline int cap_grid(int64_t work, int threads, int cap) {
   int64_t g = (work + threads - 1) / threads;
@@ -19,18 +30,20 @@ static inline int cap_grid(int64_t work, int threads, int cap) {
 
 // ---------------------------------------------------------------- V-cycle operations (bodies.cuh)
 __global__ void k_smooth_first(LevelDev L, const double* __restrict__ r, double* e, double* d) {
+  pdl_enter();
   smooth_first_body(L, r, e, d, GTID, GNT);
 }
 
 int launch_smooth_first(const LevelDev& L, const double* r, double* e, double* d,
                         cudaStream_t st) {
-  k_smooth_first<<<cap_grid(L.nedge, 128, 148 * 8), 128, 0, st>>>(L, r, e, d);
+  launch_ex(k_smooth_first, cap_grid(L.nedge, 128, 148 * 8), 128, 0, true, st, L, r, e, d);
   return 1;
 }
 
 __global__ void k_lc_restrict(LevelDev F, const double* __restrict__ res, double* e,
                               const double* __restrict__ KIIinv, const double* __restrict__ Pm,
                               double* cbuf, int do_lc, int do_restrict) {
+  pdl_enter();
   lc_restrict_body(F, res, e, KIIinv, Pm, cbuf, do_lc, do_restrict, GTID, GNT);
 }
 
@@ -38,7 +51,7 @@ int launch_lc_restrict(const LevelDev& F, const double* res, double* e, const do
                        const double* Pm, double* cbuf, bool do_lc, bool do_restrict,
                        cudaStream_t st) {
   int64_t nmac = (int64_t)(F.nx / 2) * (F.ny / 2);
-  k_lc_restrict<<<cap_grid(nmac, 128, 148 * 8), 128, 0, st>>>(F, res, e, KIIinv, Pm, cbuf,
+  launch_ex(k_lc_restrict, cap_grid(nmac, 128, 148 * 8), 128, 0, true, st, F, res, e, KIIinv, Pm, cbuf,
                                                               do_lc, do_restrict);
   return 1;
 }
@@ -46,51 +59,55 @@ int launch_lc_restrict(const LevelDev& F, const double* res, double* e, const do
 __global__ void k_restrict_edges(LevelDev F, LevelDev C, const double* __restrict__ res,
                                  const double* __restrict__ cbuf, double* rc, int fuse,
                                  double* ec, double* dc) {
+  pdl_enter();
   restrict_edges_body(F, C, res, cbuf, rc, fuse, ec, dc, GTID, GNT);
 }
 
 int launch_restrict_edges(const LevelDev& F, const LevelDev& C, const double* res,
                           const double* cbuf, double* rc, bool fuse_first, double* ec,
                           double* dc, cudaStream_t st) {
-  k_restrict_edges<<<cap_grid(C.nedge, 128, 148 * 8), 128, 0, st>>>(F, C, res, cbuf, rc,
+  launch_ex(k_restrict_edges, cap_grid(C.nedge, 128, 148 * 8), 128, 0, true, st, F, C, res, cbuf, rc,
                                                                     fuse_first, ec, dc);
   return 1;
 }
 
 __global__ void k_prolong_macro(LevelDev F, LevelDev C, const double* __restrict__ ec,
                                 const double* __restrict__ Pm, double* e) {
+  pdl_enter();
   prolong_macro_body(F, C, ec, Pm, e, GTID, GNT);
 }
 
 int launch_prolong_macro(const LevelDev& F, const LevelDev& C, const double* ec,
                          const double* Pm, double* e, cudaStream_t st) {
   int64_t nmac = (int64_t)C.nx * C.ny;
-  k_prolong_macro<<<cap_grid(nmac, 128, 148 * 8), 128, 0, st>>>(F, C, ec, Pm, e);
+  launch_ex(k_prolong_macro, cap_grid(nmac, 128, 148 * 8), 128, 0, true, st, F, C, ec, Pm, e);
   return 1;
 }
 
 __global__ void k_p_restrict(LevelDev F, LevelDev C, const double* __restrict__ Jp,
                              const double* __restrict__ res, double* rc, int fuse, double* ec,
                              double* dc) {
+  pdl_enter();
   p_restrict_body(F, C, Jp, res, rc, fuse, ec, dc, GTID, GNT);
 }
 
 int launch_p_restrict(const LevelDev& F, const LevelDev& C, const double* Jp,
                       const double* res, double* rc, bool fuse_first, double* ec, double* dc,
                       cudaStream_t st) {
-  k_p_restrict<<<cap_grid(F.nedge, 128, 148 * 8), 128, 0, st>>>(F, C, Jp, res, rc, fuse_first,
+  launch_ex(k_p_restrict, cap_grid(F.nedge, 128, 148 * 8), 128, 0, true, st, F, C, Jp, res, rc, fuse_first,
                                                                 ec, dc);
   return 1;
 }
 
 __global__ void k_p_prolong(LevelDev F, const double* __restrict__ Jp,
                             const double* __restrict__ ec, double* e) {
+  pdl_enter();
   p_prolong_body(F, Jp, ec, e, GTID, GNT);
 }
 
 int launch_p_prolong(const LevelDev& F, const double* Jp, const double* ec, double* e,
                      cudaStream_t st) {
-  k_p_prolong<<<cap_grid(F.nedge, 128, 148 * 8), 128, 0, st>>>(F, Jp, ec, e);
+  launch_ex(k_p_prolong, cap_grid(F.nedge, 128, 148 * 8), 128, 0, true, st, F, Jp, ec, e);
   return 1;
 }
 
@@ -117,6 +134,7 @@ int vec_grid(int64_t n) { return cap_grid(n, 256, 148 * 4); }
 
 __global__ void k_dot(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
                       double* partials) {
+  pdl_enter();
   double s = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -127,13 +145,14 @@ __global__ void k_dot(const double* __restrict__ a, const double* __restrict__ b
 
 int launch_dot(const double* a, const double* b, int64_t n, double* partials, int grid,
                cudaStream_t st) {
-  k_dot<<<grid, 256, 0, st>>>(a, b, n, partials);
+  launch_ex(k_dot, grid, 256, 0, true, st, a, b, n, partials);
   return 1;
 }
 
 // scal layout (PCG): [0] rz, [1] pAp, [2] rr, [3] alpha, [4] beta, [5] gg, [6..] misc
 __global__ void k_reduce(const double* __restrict__ partials, int n, double* scal, int slot,
                          int op) {
+  pdl_enter();
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += partials[i];
   s = block_sum(s);
@@ -151,13 +170,14 @@ __global__ void k_reduce(const double* __restrict__ partials, int n, double* sca
 int launch_reduce(const double* partials, int n, double* scal, int slot, int op, DevError* err,
                   cudaStream_t st) {
   (void)err;
-  k_reduce<<<1, 1024, 0, st>>>(partials, n, scal, slot, op);
+  launch_ex(k_reduce, 1, 1024, 0, true, st, partials, n, scal, slot, op);
   return 1;
 }
 
 __global__ void k_pcg_update(double* x, double* r, const double* __restrict__ p,
                              const double* __restrict__ ap, const double* __restrict__ scal,
                              int64_t n, double* partials) {
+  pdl_enter();
   const double alpha = scal[3];
   double s = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -174,12 +194,13 @@ __global__ void k_pcg_update(double* x, double* r, const double* __restrict__ p,
 int launch_pcg_update(double* x, double* r, const double* p, const double* ap,
                       const double* scal, int64_t n, double* partials, int grid,
                       cudaStream_t st) {
-  k_pcg_update<<<grid, 256, 0, st>>>(x, r, p, ap, scal, n, partials);
+  launch_ex(k_pcg_update, grid, 256, 0, true, st, x, r, p, ap, scal, n, partials);
   return 1;
 }
 
 __global__ void k_pcg_pupdate(double* p, const double* __restrict__ z,
                               const double* __restrict__ scal, int64_t n) {
+  pdl_enter();
   const double beta = scal[4];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -188,7 +209,7 @@ __global__ void k_pcg_pupdate(double* p, const double* __restrict__ z,
 
 int launch_pcg_pupdate(double* p, const double* z, const double* scal, int64_t n,
                        cudaStream_t st) {
-  k_pcg_pupdate<<<vec_grid(n), 256, 0, st>>>(p, z, scal, n);
+  launch_ex(k_pcg_pupdate, vec_grid(n), 256, 0, true, st, p, z, scal, n);
   return 1;
 }
 
@@ -199,6 +220,7 @@ int launch_pcg_pupdate(double* p, const double* z, const double* scal, int64_t n
 // ||r_k|| / ||g||) and decides whether the body runs again -- no host round
 // trip per iteration.  Status codes match include/mgdtn.h.
 __global__ void k_pcg_init(int* istate, double* scal, double rtol, int maxit) {
+  pdl_enter();
   istate[0] = 0;
   istate[1] = 1;   // MG_MAXIT until decided
   istate[2] = maxit;
@@ -206,12 +228,13 @@ __global__ void k_pcg_init(int* istate, double* scal, double rtol, int maxit) {
 }
 
 int launch_pcg_init(int* istate, double* scal, double rtol, int maxit, cudaStream_t st) {
-  k_pcg_init<<<1, 1, 0, st>>>(istate, scal, rtol, maxit);
+  launch_ex(k_pcg_init, 1, 1, 0, true, st, istate, scal, rtol, maxit);
   return 1;
 }
 
 __global__ void k_pcg_check(const double* __restrict__ scal, int* istate, double* hist,
                             int hist_cap, cudaGraphConditionalHandle h) {
+  pdl_enter();
   const double gg = scal[5];
   int cont = 0;
   if (!(gg > 0.0)) {   // g = 0 -> lambda = 0 in 0 iterations
@@ -237,27 +260,23 @@ __global__ void k_pcg_check(const double* __restrict__ scal, int* istate, double
 
 int launch_pcg_check(const double* scal, int* istate, double* hist, int hist_cap,
                      cudaGraphConditionalHandle h, cudaStream_t st) {
-  k_pcg_check<<<1, 1, 0, st>>>(scal, istate, hist, hist_cap, h);
+  launch_ex(k_pcg_check, 1, 1, 0, true, st, scal, istate, hist, hist_cap, h);
   return 1;
 }
 
 // ---------------------------------------------------------------- lambda_max (Q11)
 __global__ void k_pow_init(LevelDev L, double* v) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.ndof;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = i / L.k1;
-    v[i] = edge_on_boundary(L.nx, L.ny, e) ? 0.0 : 1.0 + (double)(i % 7) / 7.0;
-  }
-}
+  pdl_enter(); pow_init_body(L, v, GTID, GNT); }
 
 int launch_pow_init(const LevelDev& L, double* v, cudaStream_t st) {
-  k_pow_init<<<vec_grid(L.ndof), 256, 0, st>>>(L, v);
+  launch_ex(k_pow_init, vec_grid(L.ndof), 256, 0, true, st, L, v);
   return 1;
 }
 
 // u = Dinv y per edge; partials[2*b] = sum u.u, partials[2*b+1] = sum u.y
 __global__ void k_edge_dinv(LevelDev L, const double* __restrict__ y, double* u,
                             double* partials) {
+  pdl_enter();
   const int K1 = L.k1;
   double s_uu = 0.0, s_uy = 0.0;
   for (int64_t ed = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ed < L.nedge;
@@ -283,12 +302,13 @@ __global__ void k_edge_dinv(LevelDev L, const double* __restrict__ y, double* u,
 
 int launch_edge_dinv(const LevelDev& L, const double* y, double* u, double* partials,
                      int grid, cudaStream_t st) {
-  k_edge_dinv<<<grid, 256, 0, st>>>(L, y, u, partials);
+  launch_ex(k_edge_dinv, grid, 256, 0, true, st, L, y, u, partials);
   return 1;
 }
 
 __global__ void k_scale_by_norm(double* v, const double* __restrict__ u, int64_t n,
                                 const double* __restrict__ scal, int slot) {
+  pdl_enter();
   const double inv = 1.0 / sqrt(scal[slot]);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -297,40 +317,24 @@ __global__ void k_scale_by_norm(double* v, const double* __restrict__ u, int64_t
 
 int launch_scale_by_norm(double* v, const double* u, int64_t n, const double* scal, int slot,
                          cudaStream_t st) {
-  k_scale_by_norm<<<vec_grid(n), 256, 0, st>>>(v, u, n, scal, slot);
+  launch_ex(k_scale_by_norm, vec_grid(n), 256, 0, true, st, v, u, n, scal, slot);
   return 1;
 }
 
-// scal[6] = u.u (last), scal[7] = u.y_prev (last), scal[8] = v.Av:
-// lambda_hat = v.Av / v.Dv with v = u/|u| -> v.Dv = u.y_prev / u.u.
-// Chebyshev coefficients (O8): theta = (b+a)/2, delta = (b-a)/2, sigma = theta/delta,
-// step 0: c1 = 0, c2 = 1/theta; step k: rho_k = 1/(2 sigma - rho_{k-1}),
-// c1 = rho_k rho_{k-1}, c2 = 2 rho_k / delta.
 __global__ void k_lmax_finish(const double* __restrict__ scal, double safety, double ratio,
                               int nu_max, double* lam_out, double* coef) {
-  const double vDv = scal[7] / scal[6];
-  const double lam = safety * scal[8] / vDv;
-  *lam_out = lam;
-  const double b = lam, a = lam / ratio;
-  const double theta = 0.5 * (b + a), delta = 0.5 * (b - a), sigma = theta / delta;
-  double rho = 1.0 / sigma;
-  coef[0] = 0.0;
-  coef[1] = 1.0 / theta;
-  for (int k = 1; k < nu_max; ++k) {
-    const double rn = 1.0 / (2.0 * sigma - rho);
-    coef[2 * k] = rn * rho;
-    coef[2 * k + 1] = 2.0 * rn / delta;
-    rho = rn;
-  }
+  pdl_enter();
+  lmax_finish_body(scal[8], scal[7], safety, ratio, nu_max, lam_out, coef);
 }
 
 int launch_lmax_finish(const double* scal, double safety, double ratio, int nu_max,
                        double* lam_out, double* coef, cudaStream_t st) {
-  k_lmax_finish<<<1, 1, 0, st>>>(scal, safety, ratio, nu_max, lam_out, coef);
+  launch_ex(k_lmax_finish, 1, 1, 0, true, st, scal, safety, ratio, nu_max, lam_out, coef);
   return 1;
 }
 
 __global__ void k_set_bj_coef(double omega, double* coef) {
+  pdl_enter();
   int k = threadIdx.x;
   if (k < MAX_NU) {
     coef[2 * k] = 0.0;
@@ -339,52 +343,56 @@ __global__ void k_set_bj_coef(double omega, double* coef) {
 }
 
 int launch_set_bj_coef(double omega, double* coef, cudaStream_t st) {
-  k_set_bj_coef<<<1, 32, 0, st>>>(omega, coef);
+  launch_ex(k_set_bj_coef, 1, 32, 0, true, st, omega, coef);
   return 1;
 }
 
 __global__ void k_copy(double* dst, const double* __restrict__ src, int64_t n) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = src[i];
 }
 
 int launch_copy(double* dst, const double* src, int64_t n, cudaStream_t st) {
-  k_copy<<<vec_grid(n), 256, 0, st>>>(dst, src, n);
+  launch_ex(k_copy, vec_grid(n), 256, 0, true, st, dst, src, n);
   return 1;
 }
 
 __global__ void k_zero(double* dst, int64_t n) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = 0.0;
 }
 
 int launch_zero(double* dst, int64_t n, cudaStream_t st) {
-  k_zero<<<vec_grid(n), 256, 0, st>>>(dst, n);
+  launch_ex(k_zero, vec_grid(n), 256, 0, true, st, dst, n);
   return 1;
 }
 
 // dst = src with the dOmega (Dirichlet) entries set to 0 (inputs are ignored there)
 __global__ void k_copy_masked(LevelDev L, double* dst, const double* __restrict__ src) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.ndof;
        i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = edge_on_boundary(L.nx, L.ny, i / L.k1) ? 0.0 : src[i];
 }
 
 int launch_copy_masked(const LevelDev& L, double* dst, const double* src, cudaStream_t st) {
-  k_copy_masked<<<vec_grid(L.ndof), 256, 0, st>>>(L, dst, src);
+  launch_ex(k_copy_masked, vec_grid(L.ndof), 256, 0, true, st, L, dst, src);
   return 1;
 }
 
 __global__ void k_add(double* dst, const double* __restrict__ src, int64_t n) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     dst[i] += src[i];
 }
 
 int launch_add(double* dst, const double* src, int64_t n, cudaStream_t st) {
-  k_add<<<vec_grid(n), 256, 0, st>>>(dst, src, n);
+  launch_ex(k_add, vec_grid(n), 256, 0, true, st, dst, src, n);
   return 1;
 }
 

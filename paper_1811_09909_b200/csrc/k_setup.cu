@@ -9,56 +9,18 @@ namespace mgdtn {
 // H1: element DtN maps.  PAPER.md:305-316 ("express the local volume unknowns
 // ... element-by-element, as a function of the skeletal unknowns"); HDG
 // Eqs. HDG/HDG_flux, SIPG-H Eq. SIPG_H.
-// One warp per element, local matrices in shared memory:
-//   Q = K G + t F (HDG) | K LN + t F (SIPG),  R = K P + t E | t E - K Nl,
-//   Q = L L^T,  Y = L^-1 R,  S_T = S0 - Y^T Y,  S0 = K W + t H | t H,  t = tau h.
+// After eliminating u (HDG) the local problem of a side-h square is
+//   Q q = R lambda + f_w,  flux = R^T q - S0 lambda,   Q = K A + t F, t = tau h,
+// so S_T = S0 - R^T Q^-1 R and b_T = R^T Q^-1 f_w.  The pencil (A, F) is
+// diagonalised once per p on the host (refelem.h RefTables::Pencil:
+// T Q T^T = diag(d_i), d_i = K lam_i + t mu_i), which turns the batched
+// per-element factorisation into a sum of rank-1 terms with per-element weights:
+//   S_T[a][b] = S0[a][b] - sum_i w_ia w_ib / d_i,   w_i = t At_i + K Bk_i.
+// CTA = M/2 warps on one chunk of 32 same-colour elements (the S_T layout of
+// kernels.cuh); lane = element, warp w owns rows w and M-1-w (balanced), so each
+// packed entry is written by one lane as a coalesced 256-byte warp store.  No
+// factorisation, no serial dependency: ~NV*NPK*2 FMA per element.
 // ============================================================================
-template <int P>
-struct LocalShape {
-  static constexpr int K1 = P + 1, NV = K1 * K1, M = 4 * K1, NPK = M * (M + 1) / 2;
-};
-
-constexpr int LOC_WARPS = 4;
-
-template <int P>
-__device__ __forceinline__ bool local_factor(const RefDev& R, double Kc, double t, int meth,
-                                             double* Q, double* Rm, int lane) {
-  using Sh = LocalShape<P>;
-  constexpr int NV = Sh::NV, M = Sh::M;
-  for (int idx = lane; idx < NV * NV; idx += 32)
-    Q[idx] = (meth == 0 ? Kc * R.G[idx] : Kc * R.LN[idx]) + t * R.F[idx];
-  for (int idx = lane; idx < NV * M; idx += 32)
-    Rm[idx] = meth == 0 ? fma(Kc, R.P[idx], t * R.E[idx]) : t * R.E[idx] - Kc * R.Nl[idx];
-  __syncwarp();
-  bool ok = true;
-  // right-looking Cholesky, lower triangle in place
-  for (int jc = 0; jc < NV; ++jc) {
-    double dj = Q[jc * NV + jc];
-    if (!(dj > 0.0)) ok = false;
-    dj = sqrt(fmax(dj, 1e-300));
-    __syncwarp();
-    if (lane == 0) Q[jc * NV + jc] = dj;
-    for (int i = jc + 1 + lane; i < NV; i += 32) Q[i * NV + jc] /= dj;
-    __syncwarp();
-    const int nt = NV - jc - 1;
-    for (int q = lane; q < nt * nt; q += 32) {
-      int ii = jc + 1 + q / nt, cc = jc + 1 + q % nt;
-      if (cc <= ii) Q[ii * NV + cc] -= Q[ii * NV + jc] * Q[cc * NV + jc];
-    }
-    __syncwarp();
-  }
-  // Y = L^-1 R, lanes over the m columns
-  if (lane < M) {
-    for (int i = 0; i < NV; ++i) {
-      double s = Rm[i * M + lane];
-      for (int k = 0; k < i; ++k) s -= Q[i * NV + k] * Rm[k * M + lane];
-      Rm[i * M + lane] = s / Q[i * NV + i];
-    }
-  }
-  __syncwarp();
-  return ok;
-}
-
 __device__ __forceinline__ void pk_row_col(int kk, int m, int& i, int& j) {
   i = 0;
   int rowlen = m;
@@ -71,135 +33,176 @@ __device__ __forceinline__ void pk_row_col(int kk, int m, int& i, int& j) {
 }
 
 template <int P>
-__global__ void __launch_bounds__(32 * LOC_WARPS) k_local_dtn(LevelDev L, RefDev R, double h,
+struct LocalShape {
+  static constexpr int K1 = P + 1, NV = K1 * K1, M = 4 * K1, NPK = M * (M + 1) / 2;
+};
+
+template <int P>
+__global__ void __launch_bounds__(32 * (2 * (P + 1))) k_local_dtn(LevelDev L, RefDev R, double h,
                                                               const double* __restrict__ K,
                                                               const int8_t* __restrict__ method,
                                                               const double* __restrict__ tau,
                                                               DevError* err) {
   using Sh = LocalShape<P>;
-  constexpr int NV = Sh::NV, M = Sh::M, NPK = Sh::NPK;
-  __shared__ double smQ[LOC_WARPS][NV * NV];
-  __shared__ double smR[LOC_WARPS][NV * M];
+  constexpr int NV = Sh::NV, M = Sh::M, NPK = Sh::NPK, NW = M / 2;
+  __shared__ double sAt[2][NV * M], sBk[2][NV * M];
+  __shared__ double sW[M * M], sH[M * M];
+  __shared__ double sc[NV][32];   // 1 / d_i per lane-element
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* Q = smQ[w];
-  double* Rm = smR[w];
-  for (int64_t e = (int64_t)blockIdx.x * LOC_WARPS + w; e < L.ne;
-       e += (int64_t)gridDim.x * LOC_WARPS) {
-    const double Kc = K[e];
-    const double t = tau[e] * h;
-    const int meth = method[e];
-    if (!(Kc > 0.0) || !(t > 0.0) || (meth != 0 && meth != 1)) {
-      if (lane == 0) report_error(err, -1, e);
-      continue;
+  for (int q = threadIdx.x; q < NV * M; q += blockDim.x) {
+    sAt[0][q] = R.pAt[0][q];
+    sAt[1][q] = R.pAt[1][q];
+    sBk[0][q] = R.pBk[0][q];
+    sBk[1][q] = R.pBk[1][q];
+  }
+  for (int q = threadIdx.x; q < M * M; q += blockDim.x) {
+    sW[q] = R.W[q];
+    sH[q] = R.H[q];
+  }
+  const int64_t nec = L.ne >> 1;
+  const int64_t nchunk_tot = 2 * (int64_t)L.nchunk;
+  for (int64_t cc = blockIdx.x; cc < nchunk_tot; cc += gridDim.x) {
+    const int colour = (int)(cc / L.nchunk);
+    const int64_t chunk = cc - (int64_t)colour * L.nchunk;
+    const int64_t s = chunk * 32 + lane;
+    const bool act = s < nec;
+    double Kc = 1.0, t = 1.0;
+    int meth = 0;
+    int64_t e = -1;
+    if (act) {
+      int i, j;
+      slot_elem(L.nx, colour, s, i, j);
+      e = (int64_t)j * L.nx + i;
+      Kc = K[e];
+      t = tau[e] * h;
+      meth = method[e];
+      if (!(Kc > 0.0) || !(t > 0.0) || (meth != 0 && meth != 1)) {
+        if (w == 0) report_error(err, -1, e);
+        Kc = 1.0;
+        t = 1.0;
+        meth = 0;
+      }
     }
-    bool ok = local_factor<P>(R, Kc, t, meth, Q, Rm, lane);
-    if (!ok && lane == 0) report_error(err, -4, e);
-    const int i = (int)(e % L.nx), j = (int)(e / L.nx);
-    int colour;
-    int64_t s;
-    elem_slot(L.nx, i, j, colour, s);
-    double* dst = L.S + s_offset(L.nchunk, NPK, colour, s, 0);
-    for (int kk = lane; kk < NPK; kk += 32) {
-      int a, b;
-      pk_row_col(kk, M, a, b);
-      double v = (meth == 0 ? Kc * R.W[a * M + b] : 0.0) + t * R.H[a * M + b];
-      for (int r = 0; r < NV; ++r) v -= Rm[r * M + a] * Rm[r * M + b];
-      dst[(int64_t)kk * 32] = v;
+    __syncthreads();   // sc of the previous chunk consumed; tables loaded
+    for (int i = w; i < NV; i += NW) {
+      const double d = fma(Kc, R.plam[meth][i], t * R.pmu[meth][i]);
+      if (act && !(d > 0.0)) report_error(err, -4, e);   // Q not SPD (under-penalised)
+      sc[i][lane] = 1.0 / d;
     }
-    __syncwarp();
+    __syncthreads();
+    const double* At = sAt[meth];
+    const double* Bk = sBk[meth];
+    double* dst = L.S + (((int64_t)colour * L.nchunk + chunk) * NPK) * 32 + lane;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int a = half == 0 ? w : M - 1 - w;
+      double acc[M];
+#pragma unroll
+      for (int b = 0; b < M; ++b)
+        acc[b] = (meth == 0 ? Kc * sW[a * M + b] : 0.0) + t * sH[a * M + b];
+      for (int i = 0; i < NV; ++i) {
+        const double wa = fma(t, At[i * M + a], Kc * Bk[i * M + a]) * sc[i][lane];
+#pragma unroll
+        for (int b = 0; b < M; ++b)
+          if (b >= a) acc[b] = fma(-wa, fma(t, At[i * M + b], Kc * Bk[i * M + b]), acc[b]);
+      }
+      if (act) {
+        const int base = a * (2 * M - a + 1) / 2 - a;   // kk(a, b) = base + b
+#pragma unroll
+        for (int b = 0; b < M; ++b)
+          if (b >= a) dst[(int64_t)(base + b) * 32] = acc[b];
+      }
+    }
   }
 }
 
 int launch_local_dtn(const LevelDev& L, const RefDev& R, double h, const double* K,
                      const int8_t* method, const double* tau, DevError* err, cudaStream_t st) {
-  int64_t g = (L.ne + LOC_WARPS - 1) / LOC_WARPS;
-  int grid = (int)(g < 148 * 32 ? g : 148 * 32);
+  const int64_t nct = 2 * (int64_t)L.nchunk;
+  const int grid = (int)(nct < 148 * 8 ? nct : 148 * 8);
   switch (L.p) {
-    case 1: k_local_dtn<1><<<grid, 32 * LOC_WARPS, 0, st>>>(L, R, h, K, method, tau, err); break;
-    case 2: k_local_dtn<2><<<grid, 32 * LOC_WARPS, 0, st>>>(L, R, h, K, method, tau, err); break;
-    case 3: k_local_dtn<3><<<grid, 32 * LOC_WARPS, 0, st>>>(L, R, h, K, method, tau, err); break;
-    default: k_local_dtn<4><<<grid, 32 * LOC_WARPS, 0, st>>>(L, R, h, K, method, tau, err); break;
+    case 1: k_local_dtn<1><<<grid, 32 * 4, 0, st>>>(L, R, h, K, method, tau, err); break;
+    case 2: k_local_dtn<2><<<grid, 32 * 6, 0, st>>>(L, R, h, K, method, tau, err); break;
+    case 3: k_local_dtn<3><<<grid, 32 * 8, 0, st>>>(L, R, h, K, method, tau, err); break;
+    default: k_local_dtn<4><<<grid, 32 * 10, 0, st>>>(L, R, h, K, method, tau, err); break;
   }
   return 1;
 }
 
 // ============================================================================
-// Right-hand side: b_T = R^T Q^-1 f_w (flux rows at lambda = 0), minus the
-// Dirichlet lift S_T lambda_D, scattered with the same 2-colour rule as the
-// apply (colour 0 writes, colour 1 adds, reading Q4).
+// Right-hand side: b_T = R^T Q^-1 f_w = sum_i w_i f'_i / d_i (pencil form, see
+// H1; f'_i = h^2 sum_q fqT[q][i] f_q from the (p+4)^2 Gauss samples), minus
+// the Dirichlet lift S_T lambda_D (stored S_T) on elements touching dOmega;
+// scattered with the 2-colour rule of the apply (colour 0 writes, colour 1
+// adds, reading Q4).  Thread per element.
 // ============================================================================
 template <int P>
-__global__ void __launch_bounds__(32 * LOC_WARPS) k_local_rhs(
+__global__ void __launch_bounds__(128) k_local_rhs(
     LevelDev L, RefDev R, double h, const double* __restrict__ K,
     const int8_t* __restrict__ method, const double* __restrict__ tau,
     const double* __restrict__ f_qp, double f_const, const double* __restrict__ lamD, double* g,
     int colour) {
   using Sh = LocalShape<P>;
-  constexpr int NV = Sh::NV, M = Sh::M, K1 = Sh::K1;
-  __shared__ double smQ[LOC_WARPS][NV * NV];
-  __shared__ double smR[LOC_WARPS][NV * M];
-  __shared__ double smv[LOC_WARPS][NV + 2 * M];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* Q = smQ[w];
-  double* Rm = smR[w];
-  double* z = smv[w];
-  double* lamT = smv[w] + NV;
-  double* bT = smv[w] + NV + M;
+  constexpr int NV = Sh::NV, M = Sh::M, K1 = Sh::K1, NPK = Sh::NPK;
   const int64_t nec = L.ne >> 1;
-  const int nq = R.nqf;
-  for (int64_t s = (int64_t)blockIdx.x * LOC_WARPS + w; s < nec;
-       s += (int64_t)gridDim.x * LOC_WARPS) {
+  const int nq2 = R.nqf * R.nqf;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nec;
+       s += (int64_t)gridDim.x * blockDim.x) {
     int i, j;
     slot_elem(L.nx, colour, s, i, j);
     const int64_t e = (int64_t)j * L.nx + i;
     const double Kc = K[e], t = tau[e] * h;
-    const int meth = method[e];
-    local_factor<P>(R, Kc, t, meth, Q, Rm, lane);
+    const int meth = method[e] == 1 ? 1 : 0;
+    const double* fqT = R.pfq[meth];
+    double fp[NV];
+#pragma unroll
+    for (int a = 0; a < NV; ++a) fp[a] = 0.0;
+    for (int q = 0; q < nq2; ++q) {
+      const double fv = f_qp ? f_qp[e * nq2 + q] : f_const;
+#pragma unroll
+      for (int a = 0; a < NV; ++a) fp[a] = fma(fqT[q * NV + a], fv, fp[a]);
+    }
+#pragma unroll
+    for (int a = 0; a < NV; ++a)
+      fp[a] *= h * h / fma(Kc, R.plam[meth][a], t * R.pmu[meth][a]);
+    double b[M];
+#pragma unroll
+    for (int a = 0; a < M; ++a) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < NV; ++q)
+        acc = fma(fma(t, R.pAt[meth][q * M + a], Kc * R.pBk[meth][q * M + a]), fp[q], acc);
+      b[a] = acc;
+    }
     int64_t ed[4];
     bool bd[4];
     elem_edges(L.nx, L.ny, i, j, ed, bd);
-    // f_w = h^2 sum_q fq[q][i] f_q
-    for (int a = lane; a < NV; a += 32) {
-      double acc = 0.0;
-      for (int q = 0; q < nq * nq; ++q)
-        acc += R.fq[q * NV + a] * (f_qp ? f_qp[e * nq * nq + q] : f_const);
-      z[a] = h * h * acc;
-    }
-    for (int c = lane; c < M; c += 32) {
-      int f = c / K1;
-      lamT[c] = (bd[f] && lamD) ? lamD[ed[f] * K1 + (c % K1)] : 0.0;
-    }
-    __syncwarp();
-    if (lane == 0) {  // z = L^-1 f_w
-      for (int a = 0; a < NV; ++a) {
-        double sacc = z[a];
-        for (int k = 0; k < a; ++k) sacc -= Q[a * NV + k] * z[k];
-        z[a] = sacc / Q[a * NV + a];
+    if (lamD && (bd[0] || bd[1] || bd[2] || bd[3])) {   // b -= S_T lambda_D
+      double lt[M];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int a = 0; a < K1; ++a) lt[f * K1 + a] = bd[f] ? lamD[ed[f] * K1 + a] : 0.0;
+      const double* Sp = L.S + ((((int64_t)colour * L.nchunk + (s >> 5)) * NPK) << 5) + (s & 31);
+#pragma unroll
+      for (int a = 0; a < M; ++a) {
+#pragma unroll
+        for (int c = a; c < M; ++c) {
+          const double sv = Sp[(int64_t)(a * (2 * M - a + 1) / 2 + (c - a)) * 32];
+          b[a] = fma(-sv, lt[c], b[a]);
+          if (c != a) b[c] = fma(-sv, lt[a], b[c]);
+        }
       }
     }
-    __syncwarp();
-    if (lane < M) {
-      // b = Y^T z - S lamD,  S = S0 - Y^T Y
-      double b = 0.0;
-      for (int r = 0; r < NV; ++r) b += Rm[r * M + lane] * z[r];
-      double sl = 0.0;
-      for (int c = 0; c < M; ++c) {
-        if (lamT[c] == 0.0) continue;
-        double sv = (meth == 0 ? Kc * R.W[lane * M + c] : 0.0) + t * R.H[lane * M + c];
-        for (int r = 0; r < NV; ++r) sv -= Rm[r * M + lane] * Rm[r * M + c];
-        sl += sv * lamT[c];
-      }
-      bT[lane] = b - sl;
-    }
-    __syncwarp();
-    if (lane < M) {
-      int f = lane / K1;
-      if (!bd[f]) {
-        int64_t idx = ed[f] * K1 + (lane % K1);
-        g[idx] = colour == 0 ? bT[lane] : g[idx] + bT[lane];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      if (bd[f]) continue;
+#pragma unroll
+      for (int a = 0; a < K1; ++a) {
+        const int64_t idx = ed[f] * K1 + a;
+        g[idx] = colour == 0 ? b[f * K1 + a] : g[idx] + b[f * K1 + a];
       }
     }
-    __syncwarp();
   }
 }
 
@@ -208,14 +211,15 @@ int launch_local_rhs(const LevelDev& L, const RefDev& R, double h, const double*
                      double f_const, const double* lamD, double* g, DevError* err,
                      cudaStream_t st) {
   (void)err;
-  int64_t gsz = (L.ne / 2 + LOC_WARPS - 1) / LOC_WARPS;
-  int grid = (int)(gsz < 148 * 32 ? gsz : 148 * 32);
+  int64_t gsz = (L.ne / 2 + 127) / 128;
+  int grid = (int)(gsz < 148 * 16 ? gsz : 148 * 16);
+  if (grid < 1) grid = 1;
   for (int c = 0; c < 2; ++c) {
     switch (L.p) {
-      case 1: k_local_rhs<1><<<grid, 32 * LOC_WARPS, 0, st>>>(L, R, h, K, method, tau, f_qp, f_const, lamD, g, c); break;
-      case 2: k_local_rhs<2><<<grid, 32 * LOC_WARPS, 0, st>>>(L, R, h, K, method, tau, f_qp, f_const, lamD, g, c); break;
-      case 3: k_local_rhs<3><<<grid, 32 * LOC_WARPS, 0, st>>>(L, R, h, K, method, tau, f_qp, f_const, lamD, g, c); break;
-      default: k_local_rhs<4><<<grid, 32 * LOC_WARPS, 0, st>>>(L, R, h, K, method, tau, f_qp, f_const, lamD, g, c); break;
+      case 1: k_local_rhs<1><<<grid, 128, 0, st>>>(L, R, h, K, method, tau, f_qp, f_const, lamD, g, c); break;
+      case 2: k_local_rhs<2><<<grid, 128, 0, st>>>(L, R, h, K, method, tau, f_qp, f_const, lamD, g, c); break;
+      case 3: k_local_rhs<3><<<grid, 128, 0, st>>>(L, R, h, K, method, tau, f_qp, f_const, lamD, g, c); break;
+      default: k_local_rhs<4><<<grid, 128, 0, st>>>(L, R, h, K, method, tau, f_qp, f_const, lamD, g, c); break;
     }
   }
   return 2;
@@ -562,6 +566,34 @@ int launch_packed_to_dense(const LevelDev& L, double* dst, cudaStream_t st) {
   return 1;
 }
 
+// selected elements, dense [n][m][m]
+__global__ void k_gather_dense(LevelDev L, const int64_t* __restrict__ elems, int64_t n,
+                               double* __restrict__ dst) {
+  const int m = L.m;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n * m * m;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = q / (m * m);
+    const int ab = (int)(q % (m * m)), a = ab / m, b = ab % m;
+    const int64_t e = elems[t];
+    if (e < 0 || e >= L.ne) {
+      dst[q] = 0.0;
+      continue;
+    }
+    int colour;
+    int64_t s;
+    elem_slot(L.nx, (int)(e % L.nx), (int)(e / L.nx), colour, s);
+    dst[q] = pk_get(L.S + s_offset(L.nchunk, L.npk, colour, s, 0), m, a, b);
+  }
+}
+
+int launch_gather_dense(const LevelDev& L, const int64_t* elems, int64_t n, double* dst,
+                        cudaStream_t st) {
+  const int64_t tot = n * L.m * L.m;
+  int grid = (int)((tot + 127) / 128 < 1184 ? (tot + 127) / 128 : 1184);
+  k_gather_dense<<<grid > 0 ? grid : 1, 128, 0, st>>>(L, elems, n, dst);
+  return 1;
+}
+
 // ============================================================================
 // H5: coarsest level, B_1 = A_1^-1 by a direct solver.
 // One CTA assembles the dense free-dof matrix, factors it (Cholesky) and
@@ -635,13 +667,14 @@ int launch_coarse_assemble_factor(const LevelDev& L, const int* fpos, int nf, do
 __global__ void k_coarse_solve(const int* __restrict__ fidx, int nf,
                                const double* __restrict__ Ainv, const double* __restrict__ r,
                                double* e) {
+  pdl_enter();
   coarse_solve_body(fidx, nf, Ainv, r, e, threadIdx.x, blockDim.x);
 }
 
 int launch_coarse_solve(const LevelDev& L, const int* fidx, int nf, const double* A1inv,
                         const double* r, double* e, cudaStream_t st) {
   (void)L;
-  k_coarse_solve<<<1, 256, 0, st>>>(fidx, nf, A1inv, r, e);
+  launch_ex(k_coarse_solve, 1, 256, 0, true, st, fidx, nf, A1inv, r, e);
   return 1;
 }
 

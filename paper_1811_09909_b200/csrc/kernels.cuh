@@ -22,7 +22,8 @@ enum ApplyMode : int {
   AM_W0 = 0,      // pass 0: y[e] = (S_T x_T)[e]
   AM_APPLY = 1,   // pass 1: y[e] += (S_T x_T)[e]  (+ optional dot x.y)
   AM_RESID = 2,   // pass 1: w[e] = r[e] - (w[e] + (S_T x_T)[e])
-  AM_SMOOTH = 3   // pass 1: d = c1 d + c2 Dinv (r - A x)_e ; x[e] += d  (in place)
+  AM_SMOOTH = 3,  // pass 1: d = c1 d + c2 Dinv (r - A x)_e ; x[e] += d  (in place)
+  AM_DINV = 4     // pass 1: y[e] = (A x)_e ; x[e] = Dinv (A x)_e (in place; power iteration)
 };
 
 struct LevelDev {
@@ -102,7 +103,42 @@ __device__ __forceinline__ void report_error(DevError* err, int code, long long 
 struct RefDev {
   int p, k1, nv, m, nqf;
   const double *G, *F, *P, *E, *W, *H, *LN, *Nl, *fq, *ew, *H1inv, *Jp;
+  // pencil tables per method (refelem.h RefTables::Pencil): [0] HDG, [1] SIPG-H
+  const double *plam[2], *pmu[2], *pAt[2], *pBk[2], *pfq[2];
 };
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every solve-path kernel is launched with programmatic stream serialization
+// and starts with pdl_enter(): it may be scheduled while its predecessor is
+// still running (hiding the launch latency of the long chain of small V-cycle
+// kernels) but waits for the predecessor's completion and memory flush before
+// touching any data.  In a kernel launched without the attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_enter() {
+  pdl_wait();
+  pdl_trigger();
+}
+
+bool pdl_enabled();   // MGDTN_PDL=0 turns programmatic dependent launch off (A/B)
+
+template <typename... KArgs, typename... Args>
+inline void launch_ex(void (*kern)(KArgs...), int grid, int block, size_t smem, bool pdl,
+                      cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // ---------------------------------------------------------------- launchers
 // all launchers return the number of kernels launched (for launch counting)
@@ -127,6 +163,8 @@ int launch_agglomerate(const LevelDev& F, const LevelDev& C, double* KIIinv, dou
 int launch_edge_blocks(const LevelDev& L, DevError* err, cudaStream_t st);
 int launch_dense_to_packed(const LevelDev& L, const double* src, cudaStream_t st);
 int launch_packed_to_dense(const LevelDev& L, double* dst, cudaStream_t st);
+int launch_gather_dense(const LevelDev& L, const int64_t* elems, int64_t n, double* dst,
+                        cudaStream_t st);
 
 // MG transfer / smoothing kernels
 int launch_smooth_first(const LevelDev& L, const double* r, double* e, double* d,

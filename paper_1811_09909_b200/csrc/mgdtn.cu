@@ -67,6 +67,8 @@ struct Ctx {
   long long nPro = 0, nBody = 0;  // kernels in the prologue / in one loop iteration
   bool use_graphs = true;
   int tail_start = -1;            // first level run by k_coarse_tail (-1: none)
+  bool tail_vcycle = true;        // V-cycle levels >= tail_start through k_coarse_tail
+  bool tail_lmax = true;          // their Chebyshev power iterations through k_tail_lmax
   TailParams tail{};
   size_t o_ist = 0, o_hist = 0;
   int* ist = nullptr;             // device PCG state (k_pcg_check)
@@ -231,13 +233,31 @@ static void bind_pointers(Ctx* c) {
   rd.ew = put(T.ew);
   rd.H1inv = put(T.H1inv);
   rd.Jp = put(T.Jp);
+  for (int k = 0; k < 2; ++k) {
+    rd.plam[k] = put(T.pen[k].lam);
+    rd.pmu[k] = put(T.pen[k].mu);
+    rd.pAt[k] = put(T.pen[k].At);
+    rd.pBk[k] = put(T.pen[k].Bk);
+    rd.pfq[k] = put(T.pen[k].fqT);
+  }
 }
 
-// Levels from tail_start down run as one cluster-resident launch (k_coarse.cu):
-// p = 1 levels with at most MGDTN_TAIL_NE elements (default 64 x 64; 0 = off).
+// Levels from tail_start down run as ONE launch of k_coarse_tail (k_coarse.cu):
+// p = 1 levels with at most MGDTN_TAIL_NE elements (default 256 = 16 x 16; 0 =
+// off), one CTA whose level data stay in L1 (profiles/r01_ab_tail.txt: a
+// single CTA over <= 16x16 levels beats the per-step launches; multi-CTA
+// clusters and larger tails lose to them).  MGDTN_TAIL_VCYCLE=0 /
+// MGDTN_TAIL_LMAX=0 keep the V-cycle / the Chebyshev power iteration on launches.
+static int env_or(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
 static void plan_tail(Ctx* c) {
   const char* env = std::getenv("MGDTN_TAIL_NE");
-  const long long tail_ne = env ? std::atoll(env) : 4096;
+  const long long tail_ne = env ? std::atoll(env) : 256;
+  c->tail_vcycle = env_or("MGDTN_TAIL_VCYCLE", 1) == 1;
+  c->tail_lmax = env_or("MGDTN_TAIL_LMAX", 1) == 1;
   const int nlev = (int)c->lev.size();
   c->tail_start = -1;
   if (tail_ne <= 0) return;
@@ -274,6 +294,7 @@ static void fill_tail(Ctx* c) {
     t.KIIinv = L.KIIinv;
     t.Pm = L.Pm;
     t.cbuf = L.cbuf;
+    t.lam = L.lam;
   }
 }
 
@@ -284,6 +305,9 @@ static int upload_static(Ctx* c) {
   for (const auto* v : {&T.G, &T.F, &T.P, &T.E, &T.W, &T.H, &T.LN, &T.Nl, &T.fq, &T.ew, &T.H1inv,
                         &T.Jp})
     all.insert(all.end(), v->begin(), v->end());
+  for (int k = 0; k < 2; ++k)
+    for (const auto* v : {&T.pen[k].lam, &T.pen[k].mu, &T.pen[k].At, &T.pen[k].Bk, &T.pen[k].fqT})
+      all.insert(all.end(), v->begin(), v->end());
   CK(cudaMemcpyAsync(c->ws + c->o_ref, all.data(), all.size() * sizeof(double),
                      cudaMemcpyHostToDevice, c->st));
   // coarsest free-dof maps
@@ -354,7 +378,7 @@ static inline void residual(Ctx* c, HostLevel& L) {  // L.w = L.r - A L.e
 static void vcycle_level(Ctx* c, int li, bool first_done) {
   HostLevel& L = c->lev[li];
   const int nlev = (int)c->lev.size();
-  if (li == c->tail_start) {   // this level and every coarser one: one launch
+  if (c->tail_vcycle && li == c->tail_start) {   // this level and every coarser one: one launch
     TailParams& T = c->tail;
     T.nu_pre = c->sm.nu_pre;
     T.nu_post = c->sm.nu_post;
@@ -421,21 +445,29 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
       c->launches += launch_set_bj_coef(c->sm.omega, L.d.coef, st);
       continue;
     }
-    // Chebyshev: lambda_max of D_B^-1 A_k by power iteration (Q11)
-    const int vg = vec_grid(L.d.nedge);
+    if (c->tail_lmax && li >= c->tail_start && c->tail_start >= 0) continue;   // k_tail_lmax below
+    // Chebyshev: lambda_max of D_B^-1 A_k by power iteration (Q11):
+    // v <- D^-1 A v in place (colour-1 epilogue AM_DINV), no per-step normalisation
+    const int ag = apply_grid(L.d);
     c->launches += launch_pow_init(L.d, L.e, st);
     for (int it = 0; it < c->sm.lmax_iters; ++it) {
-      apply_full(c, L, L.e, L.w, nullptr);
-      c->launches += launch_edge_dinv(L.d, L.w, L.r, c->part, vg, st);
-      c->launches += launch_reduce(c->part, vg, c->sscal, 6, 0, nullptr, st);
-      c->launches += launch_reduce(c->part + vg, vg, c->sscal, 7, 0, nullptr, st);
-      c->launches += launch_scale_by_norm(L.e, L.r, L.d.ndof, c->sscal, 6, st);
+      const bool last = it + 1 == c->sm.lmax_iters;
+      c->launches += launch_apply(L.d, 0, AM_W0, L.e, L.w, nullptr, nullptr, 0, nullptr, true, st);
+      c->launches += launch_apply(L.d, 1, AM_DINV, L.e, L.w, nullptr, nullptr, 0,
+                                  last ? c->part : nullptr, true, st);
     }
-    const int ag = apply_grid(L.d);
+    c->launches += launch_reduce(c->part, ag, c->sscal, 7, 0, nullptr, st);   // v.Dv
     apply_full(c, L, L.e, L.w, c->part);
-    c->launches += launch_reduce(c->part, ag, c->sscal, 8, 0, nullptr, st);
+    c->launches += launch_reduce(c->part, ag, c->sscal, 8, 0, nullptr, st);   // v.Av
     c->launches += launch_lmax_finish(c->sscal, c->sm.lmax_safety, c->sm.cheb_ratio, numax, L.lam,
                                       L.d.coef, st);
+  }
+  if (c->sm.kind == MG_SMOOTH_CHEBYSHEV && c->tail_lmax && c->tail_start >= 0 &&
+      c->tail_start < nlev - 1) {
+    TailParams& T = c->tail;
+    for (int k = 0; k < T.nlev; ++k) T.lev[k].d = c->lev[c->tail_start + k].d;
+    c->launches += launch_tail_lmax(T, c->sm.lmax_iters, c->sm.lmax_safety, c->sm.cheb_ratio,
+                                    numax, c->part, st);
   }
   c->lev.back().d.smoother = c->sm.kind;
   c->launches += launch_coarse_assemble_factor(c->lev.back().d, c->fpos, c->nf, c->A1, c->A1inv,
@@ -688,6 +720,9 @@ int mg_build_hierarchy(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
   c->ref_doubles = T.G.size() + T.F.size() + T.P.size() + T.E.size() + T.W.size() + T.H.size() +
                    T.LN.size() + T.Nl.size() + T.fq.size() + T.ew.size() + T.H1inv.size() +
                    T.Jp.size();
+  for (int k = 0; k < 2; ++k)
+    c->ref_doubles += T.pen[k].lam.size() + T.pen[k].mu.size() + T.pen[k].At.size() +
+                      T.pen[k].Bk.size() + T.pen[k].fqT.size();
   // levels: finest (order p), the p-level (P1, same mesh) if p > 1, then 2x2
   // agglomeration while both sides stay even
   int cx = nx, cy = ny;
@@ -981,6 +1016,19 @@ int mg_copy_element_dtn(const void* ctx, int32_t level, double* dst) {
   HostLevel* L = level_of(c, level);
   if (!L) return MG_ERR_ARG;
   c->launches += launch_packed_to_dense(L->d, dst, c->st);
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+
+int mg_gather_element_dtn(const void* ctx, int32_t level, const int64_t* elems, int64_t n,
+                          double* dst) {
+  Ctx* c = const_cast<Ctx*>(static_cast<const Ctx*>(ctx));
+  if (!c || !elems || !dst || n < 0) return MG_ERR_ARG;
+  if (!c->ws) return fail(c, MG_ERR_WORKSPACE, "no workspace bound");
+  HostLevel* L = level_of(c, level);
+  if (!L) return MG_ERR_ARG;
+  if (n == 0) return MG_OK;
+  c->launches += launch_gather_dense(L->d, elems, n, dst, c->st);
   CK(cudaGetLastError());
   return MG_OK;
 }

@@ -115,6 +115,149 @@ static std::vector<double> spd_solve(std::vector<double> A, int n, std::vector<d
   return B;
 }
 
+// cyclic Jacobi eigen-decomposition of a symmetric n x n matrix (accurate to a
+// few ulps of ||A||): A = V diag(lam) V^T, V column-major in v[row*n + col]
+static void jacobi_eig(std::vector<double> A, int n, std::vector<double>& lam,
+                       std::vector<double>& V) {
+  V.assign(n * n, 0.0);
+  for (int i = 0; i < n; ++i) V[i * n + i] = 1.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        tot += A[i * n + j] * A[i * n + j];
+        if (i != j) off += A[i * n + j] * A[i * n + j];
+      }
+    if (off <= 1e-34 * tot) break;
+    for (int pp = 0; pp < n; ++pp)
+      for (int q = pp + 1; q < n; ++q) {
+        const double apq = A[pp * n + q];
+        if (apq == 0.0) continue;
+        const double th = (A[q * n + q] - A[pp * n + pp]) / (2.0 * apq);
+        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
+        for (int k = 0; k < n; ++k) {   // columns pp, q
+          const double akp = A[k * n + pp], akq = A[k * n + q];
+          A[k * n + pp] = cs * akp - sn * akq;
+          A[k * n + q] = sn * akp + cs * akq;
+        }
+        for (int k = 0; k < n; ++k) {   // rows pp, q
+          const double apk = A[pp * n + k], aqk = A[q * n + k];
+          A[pp * n + k] = cs * apk - sn * aqk;
+          A[q * n + k] = sn * apk + cs * aqk;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double vkp = V[k * n + pp], vkq = V[k * n + q];
+          V[k * n + pp] = cs * vkp - sn * vkq;
+          V[k * n + q] = sn * vkp + cs * vkq;
+        }
+      }
+  }
+  lam.assign(n, 0.0);
+  for (int i = 0; i < n; ++i) lam[i] = A[i * n + i];
+}
+
+// lower Cholesky factor (false if not SPD with margin)
+static bool cholesky(const std::vector<double>& B, int n, std::vector<double>& Lc, double margin) {
+  Lc.assign(n * n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    double d = B[j * n + j];
+    for (int k = 0; k < j; ++k) d -= Lc[j * n + k] * Lc[j * n + k];
+    if (!(d > margin * B[j * n + j])) return false;
+    d = std::sqrt(d);
+    Lc[j * n + j] = d;
+    for (int i = j + 1; i < n; ++i) {
+      double s = B[i * n + j];
+      for (int k = 0; k < j; ++k) s -= Lc[i * n + k] * Lc[j * n + k];
+      Lc[i * n + j] = s / d;
+    }
+  }
+  return true;
+}
+
+// pencil tables (refelem.h RefTables::Pencil) for Q = K A + t F with
+// w = t E + K Bm (rows of the local right-hand sides)
+static RefTables::Pencil make_pencil(const std::vector<double>& A, const std::vector<double>& F,
+                                     const std::vector<double>& E, const std::vector<double>& Bm,
+                                     const std::vector<double>& fq, int nv, int m, int nqf2) {
+  RefTables::Pencil P;
+  std::vector<double> B(nv * nv), Lc;
+  for (P.c = 1.0;; P.c *= 2.0) {
+    for (int i = 0; i < nv * nv; ++i) B[i] = A[i] + P.c * F[i];
+    if (cholesky(B, nv, Lc, 1e-3)) break;
+    if (P.c > 1e6) throw std::runtime_error("no SPD pencil");
+  }
+  // Linv (lower triangular)
+  std::vector<double> Li(nv * nv, 0.0);
+  for (int c = 0; c < nv; ++c)
+    for (int i = 0; i < nv; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) s -= Lc[i * nv + k] * Li[k * nv + c];
+      Li[i * nv + c] = s / Lc[i * nv + i];
+    }
+  // C = Li A Li^T
+  std::vector<double> LA(nv * nv, 0.0), C(nv * nv, 0.0);
+  for (int i = 0; i < nv; ++i)
+    for (int j = 0; j < nv; ++j) {
+      double s = 0;
+      for (int k = 0; k <= i; ++k) s += Li[i * nv + k] * A[k * nv + j];
+      LA[i * nv + j] = s;
+    }
+  for (int i = 0; i < nv; ++i)
+    for (int j = 0; j < nv; ++j) {
+      double s = 0;
+      for (int k = 0; k <= j; ++k) s += LA[i * nv + k] * Li[j * nv + k];
+      C[i * nv + j] = s;
+    }
+  for (int i = 0; i < nv; ++i)
+    for (int j = 0; j < i; ++j) C[i * nv + j] = C[j * nv + i] = 0.5 * (C[i * nv + j] + C[j * nv + i]);
+  std::vector<double> ev, V;
+  jacobi_eig(C, nv, ev, V);
+  // T = V^T Li
+  std::vector<double> T(nv * nv, 0.0);
+  for (int i = 0; i < nv; ++i)
+    for (int j = 0; j < nv; ++j) {
+      double s = 0;
+      for (int k = j; k < nv; ++k) s += V[k * nv + i] * Li[k * nv + j];
+      T[i * nv + j] = s;
+    }
+  auto quad = [&](const std::vector<double>& X, int i) {
+    double s = 0;
+    for (int a = 0; a < nv; ++a) {
+      double r = 0;
+      for (int b = 0; b < nv; ++b) r += X[a * nv + b] * T[i * nv + b];
+      s += T[i * nv + a] * r;
+    }
+    return s;
+  };
+  P.lam.assign(nv, 0.0);
+  P.mu.assign(nv, 0.0);
+  for (int i = 0; i < nv; ++i) {
+    P.lam[i] = quad(A, i);
+    P.mu[i] = quad(F, i);
+  }
+  P.At.assign(nv * m, 0.0);
+  P.Bk.assign(nv * m, 0.0);
+  for (int i = 0; i < nv; ++i)
+    for (int a = 0; a < m; ++a) {
+      double s1 = 0, s2 = 0;
+      for (int k = 0; k < nv; ++k) {
+        s1 += T[i * nv + k] * E[k * m + a];
+        s2 += T[i * nv + k] * Bm[k * m + a];
+      }
+      P.At[i * m + a] = s1;
+      P.Bk[i * m + a] = s2;
+    }
+  P.fqT.assign(nqf2 * nv, 0.0);
+  for (int q = 0; q < nqf2; ++q)
+    for (int i = 0; i < nv; ++i) {
+      double s = 0;
+      for (int k = 0; k < nv; ++k) s += T[i * nv + k] * fq[q * nv + k];
+      P.fqT[q * nv + i] = s;
+    }
+  return P;
+}
+
 RefTables build_ref_tables(int p) {
   if (p < 1 || p > 4) throw std::runtime_error("p must be in 1..4");
   RefTables T;
@@ -249,6 +392,10 @@ RefTables build_ref_tables(int p) {
     T.Jp[a * 2 + 0] = 1.0 - nd[a];
     T.Jp[a * 2 + 1] = nd[a];
   }
+  std::vector<double> mNl(nv * m);
+  for (int i = 0; i < nv * m; ++i) mNl[i] = -T.Nl[i];
+  T.pen[0] = make_pencil(T.G, T.F, T.E, T.P, T.fq, nv, m, T.nqf * T.nqf);
+  T.pen[1] = make_pencil(T.LN, T.F, T.E, mNl, T.fq, nv, m, T.nqf * T.nqf);
   return T;
 }
 

@@ -32,6 +32,21 @@ struct RefTables {
   std::vector<double> H1inv;          // [k1*k1]
   // p-injection J_p: fine node a from P1 endpoint values (c0, c1)
   std::vector<double> Jp;             // [k1*2]
+  // Simultaneous diagonalisation of the local pencil (A, F), A = G (HDG) or LN
+  // (SIPG-H): with B = A + c F SPD (B = L L^T), C = L^-1 A L^-T = V diag V^T and
+  // T = V^T L^-1, every local matrix Q = K A + t F becomes T Q T^T =
+  // diag(K lam_i + t mu_i) (lam_i = (T A T^T)_ii, mu_i = (T F T^T)_ii, taken as
+  // Rayleigh quotients, not 1 - ..., so F-null modes keep mu_i ~ 1e-30).  Hence
+  //   S_T = S0 - sum_i w_i w_i^T / (K lam_i + t mu_i),  w_i = t At_i + K Bk_i,
+  //   b_T = sum_i w_i f'_i / (K lam_i + t mu_i),      f'_i = h^2 sum_q fqT[q,i] f_q,
+  // with At = T E, Bk = T P (HDG) or -T Nl (SIPG-H); S0 = K W + t H (HDG), t H (SIPG-H).
+  struct Pencil {
+    double c = 1.0;
+    std::vector<double> lam, mu;      // [nv]
+    std::vector<double> At, Bk;       // [nv*m]
+    std::vector<double> fqT;          // [nqf*nqf*nv]
+  };
+  Pencil pen[2];                      // [0] HDG, [1] SIPG-H
 };
 
 // Builds the tables for order p (1..4).  Pure host C++ (Legendre recurrences,

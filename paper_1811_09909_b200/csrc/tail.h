@@ -10,6 +10,7 @@ struct TailLevel {
   LevelDev d;
   double *r, *e, *w, *dv;        // level vectors (r input, e output of B_k)
   double *KIIinv, *Pm, *cbuf;    // per-macro A_II^-1, P_M, restriction buffer (h-levels)
+  double* lam;                   // Chebyshev lambda_max estimate (device scalar)
 };
 
 struct TailParams {
@@ -23,6 +24,10 @@ struct TailParams {
 };
 
 int launch_coarse_tail(const TailParams& P, cudaStream_t st);
+// Chebyshev lambda_max (Q11) of every tail level but the coarsest, one launch;
+// part: >= cluster-size doubles of scratch.
+int launch_tail_lmax(const TailParams& P, int iters, double safety, double ratio, int nu_max,
+                     double* part, cudaStream_t st);
 int tail_cluster_size();
 
 }  // namespace mgdtn

@@ -67,6 +67,7 @@ _SIGS = {
     "mg_level_info": [_P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                       C.POINTER(C.c_int32), C.POINTER(C.c_int64)],
     "mg_copy_element_dtn": [_P, C.c_int32, _P],
+    "mg_gather_element_dtn": [_P, C.c_int32, _P, C.c_int64, _P],
     "mg_debug_set_element_dtn": [_P, C.c_int32, _P],
     "mg_level_lambda_max": [_P, C.c_int32, C.POINTER(C.c_double)],
     "mg_last_launch_count": [_P, C.POINTER(C.c_int64)],
@@ -322,6 +323,15 @@ class MGSolver:
         m = 4 * (info["p"] + 1)
         out = torch.empty((info["nx"] * info["ny"], m, m), dtype=torch.float64, device=self.device)
         self._call("mg_copy_element_dtn", level, _ptr(out))
+        return out
+
+    def gather_element_dtn(self, level: int, elems):
+        """Dense DtN maps [n][m][m] of the given element ids (full-size sampling)."""
+        info = self.level_info(level)
+        m = 4 * (info["p"] + 1)
+        idx = self._d(elems, torch.int64)
+        out = torch.empty((idx.numel(), m, m), dtype=torch.float64, device=self.device)
+        self._call("mg_gather_element_dtn", level, _ptr(idx), idx.numel(), _ptr(out))
         return out
 
     def set_element_dtn(self, level: int, S):

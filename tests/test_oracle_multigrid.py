@@ -282,3 +282,28 @@ def test_paper_without_local_correction_diverges():
         mg, gm = _example1(2 ** L, 1, gold["tau"], step3=False)
         assert mg == "*"
         assert abs(gm - gold["gmres"]["1"][li]) <= 2, (L, gm)
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_element_p_coarsening_sums_to_global_galerkin(p):
+    """Element-wise J_p^T S_T J_p (used to sample full-size parity) assembled
+    over a heterogeneous mesh equals the global Galerkin product J_N^T A_N J_N
+    of Eq. ANm1 restricted to the free dofs (the hierarchy's level N-1)."""
+    from oracle import assembly, mesh
+    from oracle import element as el
+    n = 8
+    rng = np.random.default_rng(11)
+    K = 10.0 ** rng.uniform(-2, 2, n * n)
+    meth = (rng.random(n * n) < 0.3).astype(np.int8)
+    tau = np.where(meth == 1, 10.0 * p * p * K * n, 1.0)
+    S = el.element_dtn(p, K, meth, tau, 1.0 / n)
+    A1_elem = assembly.assemble_full(n, 1, multigrid.p_coarsen_element(S, p))
+    fr1 = mesh.free_dofs(n, 1)
+    A = assembly.assemble_full(n, p, S)
+    fr = mesh.free_dofs(n, p)
+    J = multigrid.p_injection_full(n, p)
+    glob = (J.T @ A @ J).tocsr()[fr1][:, fr1]
+    dense_e = A1_elem[fr1][:, fr1].toarray()
+    assert np.abs(dense_e - glob.toarray()).max() <= 1e-12 * np.abs(dense_e).max()
+    H = multigrid.Hierarchy(A[fr][:, fr], n, p, smoother=0)
+    assert np.abs(H.levels[1].A.toarray() - dense_e).max() <= 1e-12 * np.abs(dense_e).max()
