@@ -204,7 +204,10 @@ __device__ __forceinline__ void macro_interior_edges(const LevelDev& F, int I, i
 }
 
 // step 3 (e_I += A_II^-1 res_I per macro) and the macro part of Q_{k-1}
-// (cbuf = P_M^T res_I per macro)
+// (cbuf = P_M^T res_I per macro).  Work item = (macro M, row c): 8 threads per
+// macro, each one output row, so the 2 x 64 matrix loads of a macro are spread
+// over 8 threads (coalesced 512-byte rows / columns) instead of one dependent
+// chain per thread.
 __device__ __forceinline__ void lc_restrict_body(const LevelDev& F, const double* __restrict__ res,
                                                  double* e, const double* __restrict__ KIIinv,
                                                  const double* __restrict__ Pm, double* cbuf,
@@ -212,7 +215,9 @@ __device__ __forceinline__ void lc_restrict_body(const LevelDev& F, const double
                                                  int64_t nt) {
   const int nxc = F.nx >> 1;
   const int64_t nmac = (int64_t)nxc * (F.ny >> 1);
-  for (int64_t M = t0; M < nmac; M += nt) {
+  for (int64_t w = t0; w < nmac * 8; w += nt) {
+    const int64_t M = w >> 3;
+    const int c = (int)(w & 7);
     const int I = (int)(M % nxc), J = (int)(M / nxc);
     int64_t ie[4];
     macro_interior_edges(F, I, J, ie);
@@ -223,24 +228,18 @@ __device__ __forceinline__ void lc_restrict_body(const LevelDev& F, const double
       rI[2 * l + 1] = res[ie[l] * 2 + 1];
     }
     if (do_lc) {
-      const double* Ki = KIIinv + M * 64;
+      const double* Ki = KIIinv + M * 64 + c * 8;
+      double acc = 0.0;
 #pragma unroll
-      for (int a = 0; a < 8; ++a) {
-        double c = 0.0;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) c = fma(Ki[a * 8 + b], rI[b], c);
-        e[ie[a >> 1] * 2 + (a & 1)] += c;
-      }
+      for (int b = 0; b < 8; ++b) acc = fma(Ki[b], rI[b], acc);
+      e[ie[c >> 1] * 2 + (c & 1)] += acc;
     }
     if (do_restrict) {
-      const double* P = Pm + M * 64;
+      const double* P = Pm + M * 64 + c;
+      double acc = 0.0;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        double acc = 0.0;
-#pragma unroll
-        for (int a = 0; a < 8; ++a) acc = fma(P[a * 8 + c], rI[a], acc);
-        cbuf[M * 8 + c] = acc;
-      }
+      for (int a = 0; a < 8; ++a) acc = fma(P[a * 8], rI[a], acc);
+      cbuf[M * 8 + c] = acc;
     }
   }
 }
@@ -303,14 +302,17 @@ __device__ __forceinline__ void restrict_edges_body(const LevelDev& F, const Lev
 
 // prolongation (macro): e_I += P_M e_c(M); e_B += J e_c on the macro's bottom and
 // left macro-edges (every interior macro-edge is the bottom or left edge of
-// exactly one macro).
+// exactly one macro).  Work item = (macro M, t in 0..7): row t of P_M e_c, and
+// value t of the bottom (t < 4) / left (t >= 4) macro-edge's J e_c.
 __device__ __forceinline__ void prolong_macro_body(const LevelDev& F, const LevelDev& C,
                                                    const double* __restrict__ ec,
                                                    const double* __restrict__ Pm, double* e,
                                                    int64_t t0, int64_t nt) {
   const int nxc = C.nx, nyc = C.ny;
   const int64_t nmac = (int64_t)nxc * nyc;
-  for (int64_t M = t0; M < nmac; M += nt) {
+  for (int64_t w = t0; w < nmac * 8; w += nt) {
+    const int64_t M = w >> 3;
+    const int t = (int)(w & 7);
     const int I = (int)(M % nxc), J = (int)(M / nxc);
     int64_t ce[4];
     bool cb[4];
@@ -323,29 +325,21 @@ __device__ __forceinline__ void prolong_macro_body(const LevelDev& F, const Leve
     }
     int64_t ie[4];
     macro_interior_edges(F, I, J, ie);
-    const double* P = Pm + M * 64;
+    const double* P = Pm + M * 64 + t * 8;
+    double acc = 0.0;
 #pragma unroll
-    for (int a = 0; a < 8; ++a) {
-      double acc = 0.0;
-#pragma unroll
-      for (int b = 0; b < 8; ++b) acc = fma(P[a * 8 + b], c[b], acc);
-      e[ie[a >> 1] * 2 + (a & 1)] += acc;
-    }
-    if (!cb[0]) {  // bottom macro-edge
-      const double c0 = c[0], c1 = c[1], cm = 0.5 * (c0 + c1);
-      const int64_t f0 = hedge(F.nx, 2 * I, 2 * J), f1 = hedge(F.nx, 2 * I + 1, 2 * J);
-      e[f0 * 2] += c0;
-      e[f0 * 2 + 1] += cm;
-      e[f1 * 2] += cm;
-      e[f1 * 2 + 1] += c1;
-    }
-    if (!cb[3]) {  // left macro-edge
-      const double c0 = c[6], c1 = c[7], cm = 0.5 * (c0 + c1);
-      const int64_t f0 = vedge(F.nx, F.ny, 2 * I, 2 * J), f1 = vedge(F.nx, F.ny, 2 * I, 2 * J + 1);
-      e[f0 * 2] += c0;
-      e[f0 * 2 + 1] += cm;
-      e[f1 * 2] += cm;
-      e[f1 * 2 + 1] += c1;
+    for (int b = 0; b < 8; ++b) acc = fma(P[b], c[b], acc);
+    e[ie[t >> 1] * 2 + (t & 1)] += acc;
+    // J on the macro-edge: fine edge f0 (lower coordinate) gets (c0, (c0+c1)/2),
+    // f1 gets ((c0+c1)/2, c1)
+    const int side = t < 4 ? 0 : 3;       // bottom / left
+    if (!cb[side]) {
+      const int u = t & 3;
+      const double c0 = c[2 * side], c1 = c[2 * side + 1], cm = 0.5 * (c0 + c1);
+      const int64_t f = side == 0 ? hedge(F.nx, 2 * I + (u >> 1), 2 * J)
+                                  : vedge(F.nx, F.ny, 2 * I, 2 * J + (u >> 1));
+      const double v = u == 0 ? c0 : u == 3 ? c1 : cm;
+      e[f * 2 + (u & 1)] += v;
     }
   }
 }

@@ -90,7 +90,7 @@ struct TmaCfg {
   static constexpr int CPS = P == 4 ? 2 : P == 3 ? 3 : P == 2 ? 4 : 6;
 };
 
-template <int P, int MODE, bool DOT, int NST>
+template <int P, int MODE, bool DOT, int NST, bool XPF = true>
 __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, const double* x,
                                                   double* y, const double* __restrict__ r,
                                                   double* d, int step,
@@ -137,27 +137,51 @@ __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, 
     c2 = L.coef[2 * step + 1];
   }
   double dot = 0.0;
+  // software pipeline over the CTA's chunks: the x gather of chunk k+1 is issued
+  // before the matvec of chunk k (x of a same-colour element is never written by
+  // another same-colour element, so the early read is exact in every mode)
+  int64_t edn[4] = {0, 0, 0, 0};
+  bool bdn[4] = {true, true, true, true};
+  double xn[M];
+  auto prefetch = [&](int k) {
+#pragma unroll
+    for (int a = 0; a < M; ++a) xn[a] = 0.0;
+    const int64_t s = ((int64_t)blockIdx.x + (int64_t)k * gridDim.x) * 32 + lane;
+    if (k < nmine && s < nec) {
+      int i, j;
+      slot_elem(L.nx, colour, s, i, j);
+      elem_edges(L.nx, L.ny, i, j, edn, bdn);
+      gather_x<K1>(x, edn, bdn, xn);
+    } else {
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        edn[f] = 0;
+        bdn[f] = true;
+      }
+    }
+  };
+  prefetch(0);
   for (int k = 0; k < nmine; ++k) {
     const int c = (int)blockIdx.x + k * (int)gridDim.x;
     const int64_t s = (int64_t)c * 32 + lane;
     const bool act = s < nec;
-    int64_t ed[4] = {0, 0, 0, 0};
-    bool bd[4] = {true, true, true, true};
+    int64_t ed[4];
+    bool bd[4];
     double xv[M], yv[M], t[M], dd[M];
 #pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      ed[f] = edn[f];
+      bd[f] = bdn[f];
+    }
+#pragma unroll
     for (int a = 0; a < M; ++a) {
-      xv[a] = 0.0;
+      xv[a] = xn[a];
       yv[a] = 0.0;
       t[a] = 0.0;
       dd[a] = 0.0;
     }
-    if (act) {   // every global read of the element, independent of the stage: overlaps the wait
-      int i, j;
-      slot_elem(L.nx, colour, s, i, j);
-      elem_edges(L.nx, L.ny, i, j, ed, bd);
-      gather_x<K1>(x, ed, bd, xv);
-      epi_load<K1, MODE>(L, ed, bd, y, r, d, t, dd);
-    }
+    if (act) epi_load<K1, MODE>(L, ed, bd, y, r, d, t, dd);   // needed after the matvec only
+    if (XPF) prefetch(k + 1);
     const int st = k % NST;
     mbar_wait(&bars[st], (uint32_t)((k / NST) & 1));
     const double* Sp = stage_buf + (size_t)st * NPK * 32 + lane;
@@ -177,11 +201,419 @@ __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, 
       issue(k + NST);
     }
     if (act) epi_store<K1, MODE, DOT>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot);
+    if (!XPF) prefetch(k + 1);
   }
   if (DOT) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
     if (lane == 0) partials[blockIdx.x] = dot;
+  }
+}
+
+// ---------------------------------------------------------------- segmented-ring apply (default)
+// Same thread-per-element work as k_apply_tma, but the CTA's S_T stream (and,
+// in the smoothing modes, the colour-1 elements' packed D_e^-1 blocks, see
+// LevelDev::Dc) is cut into segments of SEGR rows (SEGR * 256 bytes) that
+// circulate through an NSLOT-slot shared-memory ring, each slot with its own
+// mbarrier.  A slot is refilled with the segment NSLOT ahead as soon as the
+// warp has consumed it, so ~NSLOT-1 segments (~100 KB per CTA, ~200 KB per SM)
+// are always in flight -- twice the whole-chunk double buffer of k_apply_tma,
+// whose in-flight bytes drop to one chunk while the other is being consumed
+// (ncu: k_apply_tma at config 2 stalls on the stage wait and reaches 44% of
+// DRAM peak).
+template <int P>
+struct SegCfg {
+  static constexpr int K1 = P + 1, M = 4 * K1, NPK = M * (M + 1) / 2;
+  static constexpr int NDE = K1 * (K1 + 1) / 2;   // packed D_e^-1 entries per edge
+  static constexpr int NDI = 4 * NDE;             // per colour-1 element
+  static constexpr int SEGR = P == 4 ? 30 : P == 3 ? 17 : P == 2 ? 13 : 12;   // rows | NPK
+  static constexpr int NSEG_S = NPK / SEGR;
+  static constexpr int NSEG_D = (NDI + SEGR - 1) / SEGR;
+  static constexpr int SEG_BYTES = SEGR * 32 * 8;
+  static constexpr int NSLOT = P == 4 ? 14 : P == 3 ? 16 : P == 2 ? 16 : 12;
+  static constexpr int CPS = P == 4 ? 2 : P == 3 ? 3 : P == 2 ? 4 : 6;
+  static_assert(NPK % SEGR == 0, "segment rows must divide the packed matrix");
+};
+
+template <int P, int MODE, bool DOT>
+__global__ void __launch_bounds__(32) k_apply_seg(const LevelDev L, int colour, const double* x,
+                                                  double* y, const double* __restrict__ r,
+                                                  double* d, int step,
+                                                  double* __restrict__ partials, int early) {
+  using C = SegCfg<P>;
+  constexpr int K1 = C::K1, M = C::M, NPK = C::NPK, SEGR = C::SEGR, NSLOT = C::NSLOT;
+  constexpr bool HASD = (MODE == AM_SMOOTH || MODE == AM_DINV);   // D_e^-1 streamed too
+  constexpr int NS = C::NSEG_S + (HASD ? C::NSEG_D : 0);          // segments per chunk
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bars[NSLOT];
+  double* ring = reinterpret_cast<double*>(smem_raw);
+  const int lane = threadIdx.x;
+  const int64_t nec = L.ne >> 1;
+  const int nchunk = L.nchunk;
+  const double* Sbase = L.S + (int64_t)colour * nchunk * NPK * 32;
+  const uint64_t pol = evict_first_policy();
+  const int G = (int)gridDim.x, b = (int)blockIdx.x;
+  const int nmine = b < nchunk ? (nchunk - 1 - b) / G + 1 : 0;
+  const int total = nmine * NS;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < NSLOT; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto issue = [&](int g) {   // lane 0: global segment g of this CTA into slot g % NSLOT
+    const int k = g / NS, q = g - k * NS;
+    const int64_t c = (int64_t)b + (int64_t)k * G;
+    const double* src;
+    int rows = SEGR;
+    if (q < C::NSEG_S) {
+      src = Sbase + (c * NPK + q * SEGR) * 32;
+    } else {
+      const int r0 = (q - C::NSEG_S) * SEGR;
+      rows = C::NDI - r0 < SEGR ? C::NDI - r0 : SEGR;
+      src = L.Dc + (c * C::NDI + r0) * 32;
+    }
+    const int s = g % NSLOT;
+    mbar_expect_tx(&bars[s], (uint32_t)(rows * 256));
+    tma_bulk_g2s(ring + (size_t)s * SEGR * 32, src, (uint32_t)(rows * 256), &bars[s], pol);
+  };
+  auto wait_seg = [&](int g) -> const double* {
+    const int s = g % NSLOT;
+    mbar_wait(&bars[s], (uint32_t)((g / NSLOT) & 1));
+    return ring + (size_t)s * SEGR * 32 + lane;
+  };
+  auto release = [&](int g) {   // the warp is done with segment g: refill its slot
+    __syncwarp();
+    if (lane == 0 && g + NSLOT < total) {
+      fence_proxy_async();
+      issue(g + NSLOT);
+    }
+  };
+  if (early) {   // S_T / D_e^-1 are immutable during a solve: prefetch before the dependency wait
+    if (lane == 0)
+      for (int g = 0; g < NSLOT && g < total; ++g) issue(g);
+    pdl_trigger();
+    pdl_wait();
+  } else {
+    pdl_wait();
+    if (lane == 0)
+      for (int g = 0; g < NSLOT && g < total; ++g) issue(g);
+    pdl_trigger();
+  }
+  double c1 = 0.0, c2 = 0.0;
+  if (MODE == AM_SMOOTH) {
+    c1 = L.coef[2 * step];
+    c2 = L.coef[2 * step + 1];
+  }
+  double dot = 0.0;
+  for (int k = 0; k < nmine; ++k) {
+    const int64_t c = (int64_t)b + (int64_t)k * G;
+    const int64_t s = c * 32 + lane;
+    const bool act = s < nec;
+    int64_t ed[4] = {0, 0, 0, 0};
+    bool bd[4] = {true, true, true, true};
+    double xv[M], yv[M], t[M], dd[M];
+#pragma unroll
+    for (int a = 0; a < M; ++a) {
+      xv[a] = 0.0;
+      yv[a] = 0.0;
+      t[a] = 0.0;
+      dd[a] = 0.0;
+    }
+    if (act) {   // every global read of the element, independent of the ring: overlaps the wait
+      int i, j;
+      slot_elem(L.nx, colour, s, i, j);
+      elem_edges(L.nx, L.ny, i, j, ed, bd);
+      gather_x<K1>(x, ed, bd, xv);
+      epi_load<K1, MODE>(L, ed, bd, y, r, d, t, dd);
+    }
+    const int g0 = k * NS;
+    const double* Sp = nullptr;
+#pragma unroll
+    for (int a = 0; a < M; ++a) {
+#pragma unroll
+      for (int bb = a; bb < M; ++bb) {
+        const int kk = a * (2 * M - a + 1) / 2 + (bb - a);
+        if (kk % SEGR == 0) Sp = wait_seg(g0 + kk / SEGR);
+        const double sv = Sp[(kk % SEGR) * 32];
+        yv[a] = fma(sv, xv[bb], yv[a]);
+        if (bb != a) yv[bb] = fma(sv, xv[a], yv[bb]);
+        if (kk % SEGR == SEGR - 1) release(g0 + kk / SEGR);
+      }
+    }
+    if (!HASD) {
+      if (act) epi_store<K1, MODE, DOT>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot);
+      continue;
+    }
+    // smoothing / power-iteration epilogue with D_e^-1 from the ring (packed upper
+    // triangle per edge, rows f*NDE + pk(a,b) of the colour-1 element's record)
+    const double* Dp[C::NSEG_D];
+#pragma unroll
+    for (int q = 0; q < C::NSEG_D; ++q) Dp[q] = wait_seg(g0 + C::NSEG_S + q);
+    auto dinv = [&](int f, int a, int bq) {
+      const int lo = a < bq ? a : bq, hi = a < bq ? bq : a;
+      const int row = f * C::NDE + lo * (2 * K1 - lo + 1) / 2 + (hi - lo);
+      return Dp[row / SEGR][(row % SEGR) * 32];
+    };
+    if (act) {
+      double* xo = const_cast<double*>(x);
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        const int64_t base = ed[f] * K1;
+        if (bd[f]) {
+          if (MODE == AM_DINV) {
+#pragma unroll
+            for (int a = 0; a < K1; ++a) y[base + a] = 0.0;
+          }
+          continue;
+        }
+        double res[K1];
+#pragma unroll
+        for (int a = 0; a < K1; ++a) {
+          if (MODE == AM_DINV) {
+            res[a] = t[f * K1 + a] + yv[f * K1 + a];   // (A x)_e
+            y[base + a] = res[a];
+          } else {
+            res[a] = t[f * K1 + a] - yv[f * K1 + a];   // (r - A x)_e
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < K1; ++a) {
+          double cc = 0.0;
+#pragma unroll
+          for (int bq = 0; bq < K1; ++bq) cc = fma(dinv(f, a, bq), res[bq], cc);
+          if (MODE == AM_DINV) {
+            xo[base + a] = cc;
+            if (DOT) dot = fma(cc, res[a], dot);
+          } else {
+            double dn = c2 * cc;
+            if (L.smoother == 1) {
+              if (step > 0) dn = fma(c1, dd[f * K1 + a], dn);
+              d[base + a] = dn;
+            }
+            xo[base + a] = xv[f * K1 + a] + dn;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < C::NSEG_D; ++q) release(g0 + C::NSEG_S + q);
+  }
+  if (DOT) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if (lane == 0) partials[blockIdx.x] = dot;
+  }
+}
+
+// ---------------------------------------------------------------- fused two-colour apply
+// One launch for the whole apply.  Each CTA streams its colour-0 chunks, then
+// its colour-1 chunks, through ONE TMA ring, so the colour-1 S_T prefetch
+// overlaps the colour-0 tail and the launch boundary between the passes
+// disappears.  A colour-1 element reads y on its 4 edges, which its colour-0
+// neighbours wrote, and (AM_SMOOTH / AM_DINV) overwrites x there, which they
+// read: the passes are separated by one grid barrier (arrive: release atomic;
+// wait: acquire spin on the generation L.sync[0]; the last CTA to arrive resets
+// the count L.sync[1] and advances the generation).  MGDTN_FUSED=2 selects the
+// per-chunk-flag variant instead (colour-1 chunk [s0,s1] waits only for the
+// colour-0 chunks holding [s0-1,s1+1] u [s0-nx/2,s1-nx/2] u [s0+nx/2,s1+nx/2]):
+// it overlaps the passes but adds two dependent L2 round trips to every
+// colour-1 chunk, which measured slower (profiles/r01_fused_probe.jsonl).
+// Forward progress: CTAs wait only after all of their own colour-0 chunks are
+// done, colour-0 work never waits, and the grid never exceeds one resident
+// wave (launch_fused_t clamps it with the occupancy calculator).  The
+// generation is read after griddepcontrol.wait, i.e. after the previous launch
+// on this level has completed.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_range(const unsigned* fl, int64_t slo, int64_t shi,
+                                           int64_t nec, unsigned gen, int lane) {
+  if (slo < 0) slo = 0;
+  if (shi > nec - 1) shi = nec - 1;
+  if (shi < slo) return;
+  for (int64_t q = (slo >> 5) + lane; q <= (shi >> 5); q += 32) {
+    while (ld_acquire_u32(fl + q) != gen) __nanosleep(32);
+  }
+}
+
+// pre-wait epilogue loads of a colour-1 element (no colour-0 output involved):
+// RESID / SMOOTH: t = r; SMOOTH (Chebyshev): dd = d
+template <int K1, int MODE>
+__device__ __forceinline__ void epi_load_r(const LevelDev& L, const int64_t ed[4], const bool bd[4],
+                                           const double* __restrict__ r, const double* d,
+                                           double* t, double* dd) {
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const int64_t base = ed[f] * K1;
+#pragma unroll
+    for (int a = 0; a < K1; ++a) {
+      if (MODE == AM_RESID || MODE == AM_SMOOTH) t[f * K1 + a] = bd[f] ? 0.0 : __ldg(r + base + a);
+      if (MODE == AM_SMOOTH) dd[f * K1 + a] = (bd[f] || L.smoother != 1) ? 0.0 : d[base + a];
+    }
+  }
+}
+// post-wait: the colour-0 partial sums (APPLY / DINV: t = y; RESID / SMOOTH: t = r - y)
+template <int K1, int MODE>
+__device__ __forceinline__ void epi_load_y(const int64_t ed[4], const bool bd[4], const double* y,
+                                           double* t) {
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const int64_t base = ed[f] * K1;
+#pragma unroll
+    for (int a = 0; a < K1; ++a) {
+      const double yo = bd[f] ? 0.0 : y[base + a];
+      if (MODE == AM_APPLY || MODE == AM_DINV) t[f * K1 + a] = yo;
+      else t[f * K1 + a] -= yo;
+    }
+  }
+}
+
+template <int P, int MODE, bool DOT, int NST, bool FLAGS>
+__global__ void __launch_bounds__(32) k_apply_fused(const LevelDev L, const double* x, double* y,
+                                                    const double* __restrict__ r, double* d,
+                                                    int step, double* __restrict__ partials,
+                                                    int early) {
+  using C = TmaCfg<P>;
+  constexpr int K1 = C::K1, M = C::M, NPK = C::NPK;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bars[NST];
+  double* stage_buf = reinterpret_cast<double*>(smem_raw);
+  const int lane = threadIdx.x;
+  const int64_t nec = L.ne >> 1;
+  const int nchunk = L.nchunk;
+  const int64_t nxh = L.nx >> 1;
+  const uint64_t pol = evict_first_policy();
+  const int G = (int)gridDim.x, b = (int)blockIdx.x;
+  const int nmine0 = b < nchunk ? (nchunk - 1 - b) / G + 1 : 0;   // same count for colour 1
+  const int nitems = 2 * nmine0;
+  unsigned* flags = L.sync + 2;   // FLAGS variant: per colour-0 chunk
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto issue = [&](int k) {   // lane 0: item k of this CTA into stage k % NST
+    const int colour = k < nmine0 ? 0 : 1;
+    const int c = b + (k - colour * nmine0) * G;
+    const int s = k % NST;
+    mbar_expect_tx(&bars[s], C::CHUNK_BYTES);
+    tma_bulk_g2s(stage_buf + (size_t)s * NPK * 32,
+                 L.S + ((int64_t)colour * nchunk + c) * NPK * 32, C::CHUNK_BYTES, &bars[s], pol);
+  };
+  if (early) {   // S_T is immutable during a solve: prefetch before the dependency wait
+    if (lane == 0)
+      for (int k = 0; k < NST && k < nitems; ++k) issue(k);
+    pdl_trigger();
+    pdl_wait();
+  } else {
+    pdl_wait();
+    if (lane == 0)
+      for (int k = 0; k < NST && k < nitems; ++k) issue(k);
+    pdl_trigger();
+  }
+  const unsigned gen = *reinterpret_cast<volatile unsigned*>(L.sync) + 1u;
+  double c1 = 0.0, c2 = 0.0;
+  if (MODE == AM_SMOOTH) {
+    c1 = L.coef[2 * step];
+    c2 = L.coef[2 * step + 1];
+  }
+  double dot = 0.0;
+  for (int k = 0; k < nitems; ++k) {
+    const int colour = k < nmine0 ? 0 : 1;
+    const int c = b + (k - colour * nmine0) * G;
+    const int64_t s = (int64_t)c * 32 + lane;
+    const bool act = s < nec;
+    int64_t ed[4] = {0, 0, 0, 0};
+    bool bd[4] = {true, true, true, true};
+    double xv[M], yv[M], t[M], dd[M];
+#pragma unroll
+    for (int a = 0; a < M; ++a) {
+      xv[a] = 0.0;
+      yv[a] = 0.0;
+      t[a] = 0.0;
+      dd[a] = 0.0;
+    }
+    if (!FLAGS && k == nmine0) {   // grid barrier between the colour passes
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        if (atomicAdd(L.sync + 1, 1u) == (unsigned)G - 1u) {
+          L.sync[1] = 0u;
+          __threadfence();
+          st_release_u32(L.sync, gen);
+        }
+      }
+      while (ld_acquire_u32(L.sync) != gen) __nanosleep(64);
+      __syncwarp();
+    }
+    if (act) {
+      int i, j;
+      slot_elem(L.nx, colour, s, i, j);
+      elem_edges(L.nx, L.ny, i, j, ed, bd);
+      gather_x<K1>(x, ed, bd, xv);
+      if (colour == 1) {
+        if (FLAGS) epi_load_r<K1, MODE>(L, ed, bd, r, d, t, dd);
+        else epi_load<K1, MODE>(L, ed, bd, y, r, d, t, dd);
+      }
+    }
+    if (FLAGS && colour == 1) {
+      const int64_t s0 = (int64_t)c * 32, s1 = s0 + 31;
+      wait_range(flags, s0 - 1, s1 + 1, nec, gen, lane);
+      wait_range(flags, s0 - nxh, s1 - nxh, nec, gen, lane);
+      wait_range(flags, s0 + nxh, s1 + nxh, nec, gen, lane);
+      __syncwarp();
+      if (act) epi_load_y<K1, MODE>(ed, bd, y, t);
+    }
+    const int st = k % NST;
+    mbar_wait(&bars[st], (uint32_t)((k / NST) & 1));
+    const double* Sp = stage_buf + (size_t)st * NPK * 32 + lane;
+#pragma unroll
+    for (int a = 0; a < M; ++a) {
+#pragma unroll
+      for (int bb = a; bb < M; ++bb) {
+        const int kk = a * (2 * M - a + 1) / 2 + (bb - a);
+        const double sv = Sp[kk * 32];
+        yv[a] = fma(sv, xv[bb], yv[a]);
+        if (bb != a) yv[bb] = fma(sv, xv[a], yv[bb]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && k + NST < nitems) {
+      fence_proxy_async();
+      issue(k + NST);
+    }
+    if (colour == 0) {
+      if (act) epi_store<K1, AM_W0, false>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot);
+      if (FLAGS) {
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          st_release_u32(flags + c, gen);
+        }
+      }
+    } else if (act) {
+      epi_store<K1, MODE, DOT>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot);
+    }
+  }
+  if (DOT) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if (lane == 0) partials[blockIdx.x] = dot;
+  }
+  if (FLAGS && lane == 0) {   // the last CTA out advances the generation for the next launch
+    __threadfence();
+    if (atomicAdd(L.sync + 1, 1u) == (unsigned)G - 1u) {
+      L.sync[1] = 0u;
+      __threadfence();
+      *reinterpret_cast<volatile unsigned*>(L.sync) = gen;
+    }
   }
 }
 
@@ -242,13 +674,22 @@ __global__ void __launch_bounds__(128) k_apply_ldg(const LevelDev L, int colour,
 }
 
 // ---------------------------------------------------------------- host side
-static bool use_ldg() {
+// apply kernel: MGDTN_APPLY = auto (default: seg for the smoothing / power-iteration
+// passes, which stream D_e^-1 too, tma for the others; profiles/r01_seg_probe.jsonl)
+// | seg | tma | ldg  (A/B)
+static int apply_impl() {
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("MGDTN_APPLY");
-    v = (e && std::strcmp(e, "ldg") == 0) ? 1 : 0;
+    v = !e ? 0 : std::strcmp(e, "ldg") == 0 ? 1 : std::strcmp(e, "tma") == 0 ? 2
+             : std::strcmp(e, "seg") == 0 ? 3 : 0;
   }
-  return v == 1;
+  return v;
+}
+static bool use_ldg() { return apply_impl() == 1; }
+static bool mode_has_dinv(int mode) { return mode == AM_SMOOTH || mode == AM_DINV; }
+static bool use_seg(int mode) {
+  return apply_impl() == 3 || (apply_impl() == 0 && mode_has_dinv(mode));
 }
 
 static int env_int(const char* name, int dflt) {
@@ -267,7 +708,64 @@ static int tma_nst() {   // stages per CTA (tuning knob MGDTN_TMA_NST, 0 = per-p
   return v;
 }
 
-int apply_grid(const LevelDev& L) {
+static int num_sms() {
+  static int v = 0;
+  if (v == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+  }
+  return v;
+}
+
+// resident CTAs per SM of a segmented-ring instantiation (occupancy calculator, cached)
+template <int P, int MODE, bool DOT>
+static int seg_resident() {
+  static int v = 0;
+  if (v == 0) {
+    const size_t smem = (size_t)SegCfg<P>::NSLOT * SegCfg<P>::SEG_BYTES;
+    cudaFuncSetAttribute(k_apply_seg<P, MODE, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_apply_seg<P, MODE, DOT>, 32, smem);
+    v = nb > 0 ? nb : 1;
+  }
+  return v;
+}
+
+static int seg_cps(int p) {   // CTAs per SM (tuning knob MGDTN_SEG_CPS, 0 = per-p default)
+  static int v = -1;
+  if (v < 0) v = env_int("MGDTN_SEG_CPS", 0);
+  int c = v > 0 ? v : p == 4 ? SegCfg<4>::CPS : p == 3 ? SegCfg<3>::CPS : p == 2 ? SegCfg<2>::CPS
+                                                                                   : SegCfg<1>::CPS;
+  const int res = p == 4 ? seg_resident<4, AM_W0, false>() : p == 3 ? seg_resident<3, AM_W0, false>()
+                  : p == 2 ? seg_resident<2, AM_W0, false>() : seg_resident<1, AM_W0, false>();
+  return c < res ? c : res;
+}
+
+template <int P, int MODE, bool DOT>
+static void launch_seg(const LevelDev& L, int colour, const double* x, double* y, const double* r,
+                       double* d, int step, double* partials, int grid, bool pdl,
+                       cudaStream_t st) {
+  const size_t smem = (size_t)SegCfg<P>::NSLOT * SegCfg<P>::SEG_BYTES;
+  seg_resident<P, MODE, DOT>();   // sets the dynamic smem attribute once
+  launch_ex(k_apply_seg<P, MODE, DOT>, grid, 32, smem, pdl, st, L, colour, x, y, r, d, step,
+            partials, pdl ? 1 : 0);
+}
+
+// grid of at most gmax persistent CTAs over n chunks with the work spread evenly:
+// k = ceil(n / gmax) chunks per CTA, ceil(n / k) CTAs (every CTA gets k or k-1)
+static int balanced_grid(int64_t n, int64_t gmax) {
+  if (n <= 0) return 1;
+  if (gmax < 1) gmax = 1;
+  const int64_t k = (n + gmax - 1) / gmax;
+  return (int)((n + k - 1) / k);
+}
+
+int apply_grid(const LevelDev& L) { return apply_grid_mode(L, AM_APPLY); }
+
+int apply_grid_mode(const LevelDev& L, int mode) {
   const int64_t nec = L.ne / 2;
   if (use_ldg()) {
     int64_t g = (nec + 127) / 128;
@@ -275,23 +773,39 @@ int apply_grid(const LevelDev& L) {
     return (int)(g < gmax ? (g > 0 ? g : 1) : gmax);
   }
   const int64_t nchunk = (nec + 31) / 32;
-  const int64_t gmax = 148 * tma_cps(L.p);
-  return (int)(nchunk < gmax ? (nchunk > 0 ? nchunk : 1) : gmax);
+  if (use_seg(mode)) return balanced_grid(nchunk, (int64_t)num_sms() * seg_cps(L.p));
+  return balanced_grid(nchunk, 148 * tma_cps(L.p));
+}
+
+static bool use_xpf() {   // MGDTN_XPF=0: no x-gather prefetch of the next chunk (A/B)
+  static int v = -1;
+  if (v < 0) v = env_int("MGDTN_XPF", 1);
+  return v != 0;
+}
+
+template <int P, int MODE, bool DOT, int NST, bool XPF>
+static void launch_tma_x(const LevelDev& L, int colour, const double* x, double* y,
+                         const double* r, double* d, int step, double* partials, int grid,
+                         bool pdl, cudaStream_t st) {
+  const size_t smem = (size_t)NST * TmaCfg<P>::CHUNK_BYTES;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_apply_tma<P, MODE, DOT, NST, XPF>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  launch_ex(k_apply_tma<P, MODE, DOT, NST, XPF>, grid, 32, smem, pdl, st, L, colour, x, y, r, d,
+            step, partials, pdl ? 1 : 0);
 }
 
 template <int P, int MODE, bool DOT, int NST>
 static void launch_tma(const LevelDev& L, int colour, const double* x, double* y, const double* r,
                        double* d, int step, double* partials, int grid, bool pdl,
                        cudaStream_t st) {
-  const size_t smem = (size_t)NST * TmaCfg<P>::CHUNK_BYTES;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_apply_tma<P, MODE, DOT, NST>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
-  }
-  launch_ex(k_apply_tma<P, MODE, DOT, NST>, grid, 32, smem, pdl, st, L, colour, x, y, r, d, step,
-           partials, pdl ? 1 : 0);
+  if (use_xpf())
+    launch_tma_x<P, MODE, DOT, NST, true>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
+  else
+    launch_tma_x<P, MODE, DOT, NST, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
 }
 
 template <int P, int MODE, bool DOT>
@@ -303,15 +817,123 @@ static void launch_one(const LevelDev& L, int colour, const double* x, double* y
              partials, 0);
     return;
   }
+  if (use_seg(MODE)) {
+    launch_seg<P, MODE, DOT>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
+    return;
+  }
   using C = TmaCfg<P>;
   int nst = tma_nst();
   if (nst <= 0 || nst * C::CHUNK_BYTES > 220 * 1024) nst = C::NST;
-  switch (nst) {
+  switch (nst) {   // tuning knob MGDTN_TMA_NST: 2..4 stages
     case 2: launch_tma<P, MODE, DOT, 2>(L, colour, x, y, r, d, step, partials, grid, pdl, st); break;
     case 3: launch_tma<P, MODE, DOT, 3>(L, colour, x, y, r, d, step, partials, grid, pdl, st); break;
-    case 4: launch_tma<P, MODE, DOT, 4>(L, colour, x, y, r, d, step, partials, grid, pdl, st); break;
-    case 5: launch_tma<P, MODE, DOT, 5>(L, colour, x, y, r, d, step, partials, grid, pdl, st); break;
-    default: launch_tma<P, MODE, DOT, 6>(L, colour, x, y, r, d, step, partials, grid, pdl, st); break;
+    default: launch_tma<P, MODE, DOT, 4>(L, colour, x, y, r, d, step, partials, grid, pdl, st); break;
+  }
+}
+
+// ---------------------------------------------------------------- fused launch
+static int fused_mode() {   // MGDTN_FUSED: 0 two launches (default), 1 grid barrier, 2 chunk flags
+  static int v = -1;
+  if (v < 0) v = env_int("MGDTN_FUSED", 0);
+  return v;
+}
+static bool use_fused() { return fused_mode() != 0 && apply_impl() == 2; }
+
+
+
+template <int P>
+static int fused_nst() {   // the fused kernel is built for the default stage count only
+  return TmaCfg<P>::NST;
+}
+
+// resident CTAs per SM of a fused instantiation (occupancy calculator, cached)
+template <int P, int MODE, bool DOT, int NST, bool FLAGS>
+static int fused_resident() {
+  static int v = 0;
+  if (v == 0) {
+    const size_t smem = (size_t)NST * TmaCfg<P>::CHUNK_BYTES;
+    cudaFuncSetAttribute(k_apply_fused<P, MODE, DOT, NST, FLAGS>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_apply_fused<P, MODE, DOT, NST, FLAGS>, 32,
+                                                  smem);
+    v = nb > 0 ? nb : 1;
+  }
+  return v;
+}
+
+template <int P, int NST>
+static int fused_grid_p(const LevelDev& L) {
+  // every instantiation of one (P, NST) has the same smem; AM_SMOOTH stands for all
+  const int res = fused_resident<P, AM_SMOOTH, false, NST, false>();
+  int cps = tma_cps(L.p);
+  if (cps > res) cps = res;
+  return balanced_grid(L.nchunk, (int64_t)num_sms() * cps);
+}
+
+template <int P>
+static int fused_grid(const LevelDev& L) {
+  return fused_grid_p<P, TmaCfg<P>::NST>(L);
+}
+
+int apply2_grid(const LevelDev& L, int mode) {
+  if (!use_fused()) return apply_grid_mode(L, mode);
+  switch (L.p) {
+    case 1: return fused_grid<1>(L);
+    case 2: return fused_grid<2>(L);
+    case 3: return fused_grid<3>(L);
+    default: return fused_grid<4>(L);
+  }
+}
+
+template <int P, int MODE, bool DOT, int NST>
+static void launch_fused_t(const LevelDev& L, const double* x, double* y, const double* r,
+                           double* d, int step, double* partials, int grid, bool pdl,
+                           cudaStream_t st) {
+  const size_t smem = (size_t)NST * TmaCfg<P>::CHUNK_BYTES;
+  if (fused_mode() == 2) {
+    const int res = fused_resident<P, MODE, DOT, NST, true>();   // also sets the smem attribute
+    if (grid > res * num_sms()) grid = res * num_sms();           // one resident wave at most
+    launch_ex(k_apply_fused<P, MODE, DOT, NST, true>, grid, 32, smem, pdl, st, L, x, y, r, d, step,
+              partials, pdl ? 1 : 0);
+  } else {
+    const int res = fused_resident<P, MODE, DOT, NST, false>();
+    if (grid > res * num_sms()) grid = res * num_sms();
+    launch_ex(k_apply_fused<P, MODE, DOT, NST, false>, grid, 32, smem, pdl, st, L, x, y, r, d, step,
+              partials, pdl ? 1 : 0);
+  }
+}
+
+template <int P, int MODE, bool DOT>
+static void launch_fused_one(const LevelDev& L, const double* x, double* y, const double* r,
+                             double* d, int step, double* partials, int grid, bool pdl,
+                             cudaStream_t st) {
+  launch_fused_t<P, MODE, DOT, TmaCfg<P>::NST>(L, x, y, r, d, step, partials, grid, pdl, st);
+}
+
+template <int P>
+static void dispatch_fused(const LevelDev& L, int mode, const double* x, double* y,
+                           const double* r, double* d, int step, double* partials, int grid,
+                           bool pdl, cudaStream_t st) {
+  switch (mode) {
+    case AM_APPLY:
+      if (partials)
+        launch_fused_one<P, AM_APPLY, true>(L, x, y, r, d, step, partials, grid, pdl, st);
+      else
+        launch_fused_one<P, AM_APPLY, false>(L, x, y, r, d, step, partials, grid, pdl, st);
+      break;
+    case AM_RESID:
+      launch_fused_one<P, AM_RESID, false>(L, x, y, r, d, step, partials, grid, pdl, st);
+      break;
+    case AM_DINV:
+      if (partials)
+        launch_fused_one<P, AM_DINV, true>(L, x, y, r, d, step, partials, grid, pdl, st);
+      else
+        launch_fused_one<P, AM_DINV, false>(L, x, y, r, d, step, partials, grid, pdl, st);
+      break;
+    default:
+      launch_fused_one<P, AM_SMOOTH, false>(L, x, y, r, d, step, partials, grid, pdl, st);
+      break;
   }
 }
 
@@ -347,12 +969,28 @@ static void dispatch_apply(const LevelDev& L, int colour, int mode, const double
 int launch_apply(const LevelDev& L, int colour, int mode, const double* x, double* y,
                  const double* r, double* d, int step, double* partials, bool pdl,
                  cudaStream_t st) {
-  const int grid = apply_grid(L);
+  const int grid = apply_grid_mode(L, mode);
   switch (L.p) {
     case 1: dispatch_apply<1>(L, colour, mode, x, y, r, d, step, partials, grid, pdl, st); break;
     case 2: dispatch_apply<2>(L, colour, mode, x, y, r, d, step, partials, grid, pdl, st); break;
     case 3: dispatch_apply<3>(L, colour, mode, x, y, r, d, step, partials, grid, pdl, st); break;
     default: dispatch_apply<4>(L, colour, mode, x, y, r, d, step, partials, grid, pdl, st); break;
+  }
+  return 1;
+}
+
+int launch_apply2(const LevelDev& L, int mode, const double* x, double* y, const double* r,
+                  double* d, int step, double* partials, bool pdl, cudaStream_t st) {
+  if (!use_fused() || L.sync == nullptr) {
+    int n = launch_apply(L, 0, AM_W0, x, y, nullptr, nullptr, 0, nullptr, pdl, st);
+    return n + launch_apply(L, 1, mode, x, y, r, d, step, partials, pdl, st);
+  }
+  const int grid = apply2_grid(L, mode);
+  switch (L.p) {
+    case 1: dispatch_fused<1>(L, mode, x, y, r, d, step, partials, grid, pdl, st); break;
+    case 2: dispatch_fused<2>(L, mode, x, y, r, d, step, partials, grid, pdl, st); break;
+    case 3: dispatch_fused<3>(L, mode, x, y, r, d, step, partials, grid, pdl, st); break;
+    default: dispatch_fused<4>(L, mode, x, y, r, d, step, partials, grid, pdl, st); break;
   }
   return 1;
 }

@@ -24,7 +24,15 @@ namespace mgdtn {
 
 constexpr int TAIL_TPB = 512;
 
-__global__ void __launch_bounds__(TAIL_TPB, 1) k_coarse_tail(const __grid_constant__ TailParams P) {
+// Shared-memory vectors (single-CTA tail, P.smem_doubles > 0): every level
+// vector of the tail (r, e, w, d and the restriction buffer) lives in shared
+// memory for the whole V-cycle tail, so the ~11 dependent steps per level pay
+// shared-memory instead of L2 latency on every vector access; the bodies take
+// generic pointers and run unchanged.  Only the top tail level's r (and, when
+// its first smoothing step was fused upstream, e and d) come in from global
+// memory, and only its e goes back out.  The read-only level matrices stay in
+// global memory (L1-cached).
+__global__ void __launch_bounds__(TAIL_TPB, 1) k_coarse_tail(const __grid_constant__ TailParams G) {
   pdl_enter();
   cg::cluster_group cl = cg::this_cluster();
   const int64_t t0 = (int64_t)cl.block_rank() * TAIL_TPB + threadIdx.x;
@@ -36,6 +44,41 @@ __global__ void __launch_bounds__(TAIL_TPB, 1) k_coarse_tail(const __grid_consta
     if (single) __syncthreads();
     else cl.sync();
   };
+  extern __shared__ __align__(16) double tail_smem[];
+  __shared__ TailParams SP;
+  const bool use_smem = single && G.smem_doubles > 0;
+  if (use_smem) {
+    if (threadIdx.x == 0) {
+      SP = G;
+      double* q = tail_smem;
+      for (int k = 0; k < G.nlev; ++k) {
+        TailLevel& L = SP.lev[k];
+        const int64_t n = L.d.ndof;
+        L.r = q; q += n;
+        L.e = q; q += n;
+        L.w = q; q += n;
+        L.dv = q; q += n;
+        if (k < G.nlev - 1) {
+          L.cbuf = q;
+          q += (int64_t)(L.d.nx / 2) * (L.d.ny / 2) * 8;
+        }
+      }
+    }
+    for (int64_t i = threadIdx.x; i < G.smem_doubles; i += TAIL_TPB) tail_smem[i] = 0.0;
+    __syncthreads();
+    const TailLevel& T = G.lev[0];
+    const TailLevel& S0 = SP.lev[0];
+    const bool fused = G.first_fused != 0 && G.nu_pre > 0;
+    for (int64_t i = threadIdx.x; i < T.d.ndof; i += TAIL_TPB) {
+      S0.r[i] = T.r[i];
+      if (fused) {
+        S0.e[i] = T.e[i];
+        S0.dv[i] = T.dv[i];
+      }
+    }
+    __syncthreads();
+  }
+  const TailParams& P = use_smem ? SP : G;
   const int nlev = P.nlev;
   // ---- down-sweep: pre-smoothing, residual, step 3 + restriction
   for (int li = 0; li < nlev - 1; ++li) {
@@ -87,6 +130,10 @@ __global__ void __launch_bounds__(TAIL_TPB, 1) k_coarse_tail(const __grid_consta
       apply_pass_body<1, AM_SMOOTH, false>(L.d, 1, L.e, L.w, L.r, L.dv, s, t0, nt);
       sync();
     }
+  }
+  if (use_smem) {   // the top tail level's correction goes back to global memory
+    const int64_t n = G.lev[0].d.ndof;
+    for (int64_t i = threadIdx.x; i < n; i += TAIL_TPB) G.lev[0].e[i] = SP.lev[0].e[i];
   }
 }
 
@@ -217,6 +264,15 @@ int launch_coarse_tail(const TailParams& P, cudaStream_t st) {
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
+  if (cs == 1 && P.smem_doubles > 0) {
+    const size_t smem = (size_t)P.smem_doubles * sizeof(double);
+    static size_t attr = 0;
+    if (smem > attr) {
+      cudaFuncSetAttribute(k_coarse_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = smem;
+    }
+    cfg.dynamicSmemBytes = smem;
+  }
   cudaLaunchKernelEx(&cfg, k_coarse_tail, P);
   return 1;
 }

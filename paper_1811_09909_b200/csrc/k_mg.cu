@@ -51,7 +51,7 @@ int launch_lc_restrict(const LevelDev& F, const double* res, double* e, const do
                        const double* Pm, double* cbuf, bool do_lc, bool do_restrict,
                        cudaStream_t st) {
   int64_t nmac = (int64_t)(F.nx / 2) * (F.ny / 2);
-  launch_ex(k_lc_restrict, cap_grid(nmac, 128, 148 * 8), 128, 0, true, st, F, res, e, KIIinv, Pm, cbuf,
+  launch_ex(k_lc_restrict, cap_grid(8 * nmac, 128, 148 * 8), 128, 0, true, st, F, res, e, KIIinv, Pm, cbuf,
                                                               do_lc, do_restrict);
   return 1;
 }
@@ -80,7 +80,7 @@ __global__ void k_prolong_macro(LevelDev F, LevelDev C, const double* __restrict
 int launch_prolong_macro(const LevelDev& F, const LevelDev& C, const double* ec,
                          const double* Pm, double* e, cudaStream_t st) {
   int64_t nmac = (int64_t)C.nx * C.ny;
-  launch_ex(k_prolong_macro, cap_grid(nmac, 128, 148 * 8), 128, 0, true, st, F, C, ec, Pm, e);
+  launch_ex(k_prolong_macro, cap_grid(8 * nmac, 128, 148 * 8), 128, 0, true, st, F, C, ec, Pm, e);
   return 1;
 }
 

@@ -530,6 +530,36 @@ int launch_edge_blocks(const LevelDev& L, DevError* err, cudaStream_t st) {
   return 1;
 }
 
+// D_e^-1 of every free edge into the colour-1 element-chunk layout LevelDev::Dc
+__global__ void k_dinv_pack(LevelDev L) {
+  const int K1 = L.k1, NDE = K1 * (K1 + 1) / 2;
+  const int64_t nec = L.ne >> 1;
+  const int64_t nslot = (int64_t)L.nchunk * 32;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nslot;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int64_t ed[4] = {0, 0, 0, 0};
+    bool bd[4] = {true, true, true, true};
+    if (s < nec) {
+      int i, j;
+      slot_elem(L.nx, 1, s, i, j);
+      elem_edges(L.nx, L.ny, i, j, ed, bd);
+    }
+    double* dst = L.Dc + ((s >> 5) * L.ndi) * 32 + (s & 31);
+    for (int f = 0; f < 4; ++f)
+      for (int a = 0; a < K1; ++a)
+        for (int b = a; b < K1; ++b) {
+          const int row = f * NDE + pk_index(a, b, K1);
+          dst[(int64_t)row * 32] = bd[f] ? 0.0 : L.Dinv[(int64_t)(a * K1 + b) * L.nedge + ed[f]];
+        }
+  }
+}
+int launch_dinv_pack(const LevelDev& L, cudaStream_t st) {
+  const int64_t n = (int64_t)L.nchunk * 32;
+  int grid = (int)((n + 127) / 128 < 1184 ? (n + 127) / 128 : 1184);
+  k_dinv_pack<<<grid, 128, 0, st>>>(L);
+  return 1;
+}
+
 // dense [ne][m][m] (element-id order) <-> packed interleaved storage
 __global__ void k_dense_to_packed(LevelDev L, const double* __restrict__ src) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < L.ne;

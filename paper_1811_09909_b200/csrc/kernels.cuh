@@ -32,8 +32,15 @@ struct LevelDev {
   int nchunk;              // chunks of 32 per colour
   double* S;               // interleaved packed DtN
   double* Dinv;            // SoA [k1*k1][nedge]: entry (a,b) of edge e at (a*k1+b)*nedge + e
+  double* Dc;              // the same blocks in colour-1 element-chunk order, packed upper
+                           // triangle: Dc[((chunk*ndi + f*nde + pk(a,b))*32 + lane] for edge f
+                           // of colour-1 slot 32*chunk+lane (every free edge has exactly one
+                           // colour-1 element); streamed with S_T by the smoothing applies
+  int ndi;                 // 4 * k1*(k1+1)/2
   double* coef;            // [2*MAX_NU] smoothing coefficients (c1_j, c2_j), device
   int smoother;            // 0 BJ, 1 Chebyshev (d vector used)
+  unsigned* sync;          // fused apply: [0] generation, [1] CTA exit count,
+                           // [2 + c] generation at which colour-0 chunk c was stored
 };
 
 // ---------------------------------------------------------------- indexing
@@ -147,7 +154,15 @@ inline void launch_ex(void (*kern)(KArgs...), int grid, int block, size_t smem, 
 int launch_apply(const LevelDev& L, int colour, int mode, const double* x, double* y,
                  const double* r, double* d, int step, double* partials, bool pdl,
                  cudaStream_t st);
-int apply_grid(const LevelDev& L);   // blocks of the colour passes (partials length)
+int apply_grid(const LevelDev& L);   // blocks of an AM_APPLY colour pass (partials length)
+int apply_grid_mode(const LevelDev& L, int mode);   // blocks of a colour pass in `mode`
+// whole apply (both colours) in ONE launch: colour-1 chunks wait only for the
+// colour-0 chunks they share edges with (per-chunk flags in L.sync), so the
+// two passes overlap instead of being separated by a launch boundary.
+// Falls back to two launch_apply calls when MGDTN_FUSED=0.
+int launch_apply2(const LevelDev& L, int mode, const double* x, double* y, const double* r,
+                  double* d, int step, double* partials, bool pdl, cudaStream_t st);
+int apply2_grid(const LevelDev& L, int mode);  // blocks of launch_apply2 (partials length)
 
 int launch_local_dtn(const LevelDev& L, const RefDev& R, double h, const double* K,
                      const int8_t* method, const double* tau, DevError* err, cudaStream_t st);
@@ -161,6 +176,7 @@ int launch_p_coarsen(const LevelDev& F, const LevelDev& C, const double* Jp, cud
 int launch_agglomerate(const LevelDev& F, const LevelDev& C, double* KIIinv, double* Pm,
                        DevError* err, cudaStream_t st);
 int launch_edge_blocks(const LevelDev& L, DevError* err, cudaStream_t st);
+int launch_dinv_pack(const LevelDev& L, cudaStream_t st);   // Dinv (SoA) -> Dc
 int launch_dense_to_packed(const LevelDev& L, const double* src, cudaStream_t st);
 int launch_packed_to_dense(const LevelDev& L, double* dst, cudaStream_t st);
 int launch_gather_dense(const LevelDev& L, const int64_t* elems, int64_t n, double* dst,

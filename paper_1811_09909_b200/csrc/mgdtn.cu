@@ -24,7 +24,7 @@ struct HostLevel {
   LevelDev d{};
   int kind = KIND_COARSEST;
   double h = 0.0;
-  size_t o_S = 0, o_Dinv = 0, o_coef = 0, o_lam = 0, o_r = 0, o_e = 0, o_w = 0, o_d = 0;
+  size_t o_sync = 0, o_S = 0, o_Dinv = 0, o_Dc = 0, o_coef = 0, o_lam = 0, o_r = 0, o_e = 0, o_w = 0, o_d = 0;
   size_t o_KIIinv = 0, o_Pm = 0, o_cbuf = 0;
   double *KIIinv = nullptr, *Pm = nullptr, *cbuf = nullptr;
   double *r = nullptr, *e = nullptr, *w = nullptr, *dv = nullptr, *lam = nullptr;
@@ -117,6 +117,7 @@ static void init_level(HostLevel& L, int nx, int ny, int p, double h, int kind) 
   d.nedge = (int64_t)nx * (ny + 1) + (int64_t)(nx + 1) * ny;
   d.ndof = d.nedge * d.k1;
   d.nchunk = (int)((d.ne / 2 + 31) / 32);
+  d.ndi = 4 * d.k1 * (d.k1 + 1) / 2;
   L.h = h;
   L.kind = kind;
 }
@@ -147,8 +148,10 @@ static void layout(Ctx* c) {
   c->o_meth = take(c->lev[0].d.ne * sizeof(int8_t));
   for (auto& L : c->lev) {
     const LevelDev& d = L.d;
+    L.o_sync = take((size_t)(2 + d.nchunk) * sizeof(unsigned));
     L.o_S = take((size_t)2 * d.nchunk * d.npk * 32 * sizeof(double));
     L.o_Dinv = take((size_t)d.nedge * d.k1 * d.k1 * sizeof(double));
+    L.o_Dc = take((size_t)d.nchunk * d.ndi * 32 * sizeof(double));
     L.o_coef = take(2 * MAX_NU * sizeof(double));
     L.o_lam = take(sizeof(double));
     L.o_r = take(d.ndof * sizeof(double));
@@ -192,8 +195,10 @@ static void bind_pointers(Ctx* c) {
   c->tauc = D(c->o_tau);
   c->methc = reinterpret_cast<int8_t*>(b + c->o_meth);
   for (auto& L : c->lev) {
+    L.d.sync = reinterpret_cast<unsigned*>(b + L.o_sync);
     L.d.S = D(L.o_S);
     L.d.Dinv = D(L.o_Dinv);
+    L.d.Dc = D(L.o_Dc);
     L.d.coef = D(L.o_coef);
     L.lam = D(L.o_lam);
     L.r = D(L.o_r);
@@ -280,6 +285,13 @@ static void fill_tail(Ctx* c) {
   TailParams& T = c->tail;
   const int nlev = (int)c->lev.size();
   T.nlev = nlev - c->tail_start;
+  // shared-memory copies of the tail vectors (k_coarse.cu), if they fit (MGDTN_TAIL_SMEM=0: off)
+  int64_t nd = 0;
+  for (int k = c->tail_start; k < nlev; ++k) {
+    const LevelDev& d = c->lev[k].d;
+    nd += 4 * d.ndof + (k < nlev - 1 ? (int64_t)(d.nx / 2) * (d.ny / 2) * 8 : 0);
+  }
+  T.smem_doubles = (env_or("MGDTN_TAIL_SMEM", 1) != 0 && nd * 8 <= 200 * 1024) ? (int)nd : 0;
   T.fidx = c->fidx;
   T.nf = c->nf;
   T.A1inv = c->A1inv;
@@ -356,18 +368,15 @@ static int check_device_error(Ctx* c) {
 // ---------------------------------------------------------------- apply / smoothing building blocks
 static inline void apply_full(Ctx* c, const HostLevel& L, const double* x, double* y,
                               double* partials) {
-  c->launches += launch_apply(L.d, 0, AM_W0, x, y, nullptr, nullptr, 0, nullptr, true, c->st);
-  c->launches += launch_apply(L.d, 1, AM_APPLY, x, y, nullptr, nullptr, 0, partials, true, c->st);
+  c->launches += launch_apply2(L.d, AM_APPLY, x, y, nullptr, nullptr, 0, partials, true, c->st);
 }
 
 static inline void smooth_step(Ctx* c, HostLevel& L, int step) {
-  c->launches += launch_apply(L.d, 0, AM_W0, L.e, L.w, nullptr, nullptr, 0, nullptr, true, c->st);
-  c->launches += launch_apply(L.d, 1, AM_SMOOTH, L.e, L.w, L.r, L.dv, step, nullptr, true, c->st);
+  c->launches += launch_apply2(L.d, AM_SMOOTH, L.e, L.w, L.r, L.dv, step, nullptr, true, c->st);
 }
 
 static inline void residual(Ctx* c, HostLevel& L) {  // L.w = L.r - A L.e
-  c->launches += launch_apply(L.d, 0, AM_W0, L.e, L.w, nullptr, nullptr, 0, nullptr, true, c->st);
-  c->launches += launch_apply(L.d, 1, AM_RESID, L.e, L.w, L.r, nullptr, 0, nullptr, true, c->st);
+  c->launches += launch_apply2(L.d, AM_RESID, L.e, L.w, L.r, nullptr, 0, nullptr, true, c->st);
 }
 
 // V-cycle B_k (Algorithm 1) on level li with input L.r, output L.e.
@@ -441,6 +450,7 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
     HostLevel& L = c->lev[li];
     L.d.smoother = c->sm.kind;
     c->launches += launch_edge_blocks(L.d, c->err, st);
+    c->launches += launch_dinv_pack(L.d, st);
     if (c->sm.kind == MG_SMOOTH_BLOCK_JACOBI) {
       c->launches += launch_set_bj_coef(c->sm.omega, L.d.coef, st);
       continue;
@@ -448,17 +458,17 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
     if (c->tail_lmax && li >= c->tail_start && c->tail_start >= 0) continue;   // k_tail_lmax below
     // Chebyshev: lambda_max of D_B^-1 A_k by power iteration (Q11):
     // v <- D^-1 A v in place (colour-1 epilogue AM_DINV), no per-step normalisation
-    const int ag = apply_grid(L.d);
+    const int ag = apply2_grid(L.d, AM_DINV);
     c->launches += launch_pow_init(L.d, L.e, st);
     for (int it = 0; it < c->sm.lmax_iters; ++it) {
       const bool last = it + 1 == c->sm.lmax_iters;
-      c->launches += launch_apply(L.d, 0, AM_W0, L.e, L.w, nullptr, nullptr, 0, nullptr, true, st);
-      c->launches += launch_apply(L.d, 1, AM_DINV, L.e, L.w, nullptr, nullptr, 0,
-                                  last ? c->part : nullptr, true, st);
+      c->launches += launch_apply2(L.d, AM_DINV, L.e, L.w, nullptr, nullptr, 0,
+                                   last ? c->part : nullptr, true, st);
     }
     c->launches += launch_reduce(c->part, ag, c->sscal, 7, 0, nullptr, st);   // v.Dv
     apply_full(c, L, L.e, L.w, c->part);
-    c->launches += launch_reduce(c->part, ag, c->sscal, 8, 0, nullptr, st);   // v.Av
+    c->launches += launch_reduce(c->part, apply2_grid(L.d, AM_APPLY), c->sscal, 8, 0, nullptr,
+                                 st);   // v.Av
     c->launches += launch_lmax_finish(c->sscal, c->sm.lmax_safety, c->sm.cheb_ratio, numax, L.lam,
                                       L.d.coef, st);
   }
@@ -489,7 +499,7 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
 // scal: [0] rz, [1] pAp, [2] rr, [3] alpha, [4] beta, [5] gg
 static void pcg_iter_A(Ctx* c) {  // Ap, alpha, x/r update, rr
   HostLevel& F = c->lev[0];
-  const int ag = apply_grid(F.d);
+  const int ag = apply2_grid(F.d, AM_APPLY);
   const int vg = vec_grid(F.d.ndof);
   apply_full(c, F, c->pv, c->ap, c->part);
   c->launches += launch_reduce(c->part, ag, c->scal, 1, 1, nullptr, c->st);

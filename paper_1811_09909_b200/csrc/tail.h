@@ -15,6 +15,7 @@ struct TailLevel {
 
 struct TailParams {
   int nlev;              // levels in the tail; lev[nlev-1] is the coarsest (direct solve)
+  int smem_doubles;      // k_coarse_tail: shared-memory copies of every tail vector (0 = off)
   int nu_pre, nu_post;
   int first_fused;       // lev[0]'s first pre-smoothing step was done by the upstream restriction
   const int* fidx;       // coarsest free-dof map and explicit inverse

@@ -257,4 +257,4 @@ def test_launch_counts_reported():
     s.setup(pr.K, pr.method, pr.tau, SmootherConfig())
     g, _ = s.assemble_rhs(pr.f_qp)
     _, info = s.pcg_solve(g)
-    assert s.last_launch_count() > 10 * info["iters"]
+    assert s.last_launch_count() >= 3 * info["iters"]

@@ -24,6 +24,9 @@ def main():
     ap.add_argument("--level", type=int, default=0, help="0 = finest")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--op", default="apply", choices=["apply", "smooth"],
+                    help="smooth: one fine smoothing step through mg_smooth (apply + D^-1 epilogue, "
+                         "plus mg_smooth's two masked input copies and one output copy)")
     a = ap.parse_args()
     cfg = W.CONFIGS[a.config] if not a.n else W.scaled_config(a.config, a.n)
     pr = W.make_problem(cfg, with_f=False)
@@ -43,7 +46,10 @@ def main():
                 flush.fill_(float(k))
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            s.apply(lev, x, y)
+            if a.op == "apply":
+                s.apply(lev, x, y)
+            else:
+                s.smooth(lev, x, y, 1)
             e1.record(st)
             torch.cuda.synchronize()
             if k >= 3:
@@ -55,7 +61,7 @@ def main():
     t = float(np.median(ts))
     print(json.dumps({"config": cfg.name, "level": lev, "p": info["p"], "ne": ne, "us_median": t,
                       "us_min": float(np.min(ts)), "alg_bytes": alg, "GBps": alg / t / 1e3,
-                      "apply": os.environ.get("MGDTN_APPLY", "tma")}))
+                      "apply": os.environ.get("MGDTN_APPLY", "tma"), "op": a.op}))
 
 
 if __name__ == "__main__":
