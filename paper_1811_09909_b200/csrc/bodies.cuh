@@ -170,8 +170,8 @@ __device__ __forceinline__ double apply_pass_body(const LevelDev& L, int colour,
 // power-iteration start vector (Q11): v_i = 1 + (i mod 7)/7 on free dofs, i = dof id
 __device__ __forceinline__ void pow_init_body(const LevelDev& L, double* v, int64_t t0, int64_t nt) {
   for (int64_t i = t0; i < L.ndof; i += nt) {
-    const int64_t e = i / L.k1;
-    v[i] = edge_on_boundary(L.nx, L.ny, e) ? 0.0 : 1.0 + (double)(i % 7) / 7.0;
+    const int64_t e = (unsigned)i / (unsigned)L.k1;
+    v[i] = edge_on_boundary(L.nx, L.ny, e) ? 0.0 : 1.0 + (double)((unsigned)i % 7u) / 7.0;
   }
 }
 
@@ -218,7 +218,7 @@ __device__ __forceinline__ void lc_restrict_body(const LevelDev& F, const double
   for (int64_t w = t0; w < nmac * 8; w += nt) {
     const int64_t M = w >> 3;
     const int c = (int)(w & 7);
-    const int I = (int)(M % nxc), J = (int)(M / nxc);
+    const int J = (int)((unsigned)M / (unsigned)nxc), I = (int)M - J * nxc;
     int64_t ie[4];
     macro_interior_edges(F, I, J, ie);
     double rI[8];
@@ -258,7 +258,7 @@ __device__ __forceinline__ void restrict_edges_body(const LevelDev& F, const Lev
     double v0 = 0.0, v1 = 0.0;
     bool bnd;
     if (E < nh) {
-      const int J = (int)(E / nxc), I = (int)(E % nxc);
+      const int J = (int)((unsigned)E / (unsigned)nxc), I = (int)E - J * nxc;
       bnd = (J == 0 || J == nyc);
       if (!bnd) {
         const int64_t f0 = hedge(F.nx, 2 * I, 2 * J), f1 = hedge(F.nx, 2 * I + 1, 2 * J);
@@ -271,7 +271,7 @@ __device__ __forceinline__ void restrict_edges_body(const LevelDev& F, const Lev
       }
     } else {
       const int64_t rr = E - nh;
-      const int J = (int)(rr / (nxc + 1)), I = (int)(rr % (nxc + 1));
+      const int J = (int)((unsigned)rr / (unsigned)(nxc + 1)), I = (int)rr - J * (nxc + 1);
       bnd = (I == 0 || I == nxc);
       if (!bnd) {
         const int64_t f0 = vedge(F.nx, F.ny, 2 * I, 2 * J), f1 = vedge(F.nx, F.ny, 2 * I, 2 * J + 1);
@@ -313,7 +313,7 @@ __device__ __forceinline__ void prolong_macro_body(const LevelDev& F, const Leve
   for (int64_t w = t0; w < nmac * 8; w += nt) {
     const int64_t M = w >> 3;
     const int t = (int)(w & 7);
-    const int I = (int)(M % nxc), J = (int)(M / nxc);
+    const int J = (int)((unsigned)M / (unsigned)nxc), I = (int)M - J * nxc;
     int64_t ce[4];
     bool cb[4];
     elem_edges(nxc, nyc, I, J, ce, cb);

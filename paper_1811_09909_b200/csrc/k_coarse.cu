@@ -32,7 +32,10 @@ constexpr int TAIL_TPB = 512;
 // its first smoothing step was fused upstream, e and d) come in from global
 // memory, and only its e goes back out.  The read-only level matrices stay in
 // global memory (L1-cached).
-__global__ void __launch_bounds__(TAIL_TPB, 1) k_coarse_tail(const __grid_constant__ TailParams G) {
+template <bool BASIS>
+__device__ __forceinline__ void k_coarse_tail_t(const TailParams& G,
+                                                             const int* __restrict__ tfidx, int nfb,
+                                                             double* Bt) {
   pdl_enter();
   cg::cluster_group cl = cg::this_cluster();
   const int64_t t0 = (int64_t)cl.block_rank() * TAIL_TPB + threadIdx.x;
@@ -68,12 +71,19 @@ __global__ void __launch_bounds__(TAIL_TPB, 1) k_coarse_tail(const __grid_consta
     __syncthreads();
     const TailLevel& T = G.lev[0];
     const TailLevel& S0 = SP.lev[0];
-    const bool fused = G.first_fused != 0 && G.nu_pre > 0;
-    for (int64_t i = threadIdx.x; i < T.d.ndof; i += TAIL_TPB) {
-      S0.r[i] = T.r[i];
-      if (fused) {
-        S0.e[i] = T.e[i];
-        S0.dv[i] = T.dv[i];
+    if (BASIS) {   // r = unit vector on free dof tfidx[blockIdx.x]; e starts at 0
+      if (threadIdx.x == 0) {
+        S0.r[tfidx[blockIdx.x]] = 1.0;
+        SP.first_fused = 0;
+      }
+    } else {
+      const bool fused = G.first_fused != 0 && G.nu_pre > 0;
+      for (int64_t i = threadIdx.x; i < T.d.ndof; i += TAIL_TPB) {
+        S0.r[i] = T.r[i];
+        if (fused) {
+          S0.e[i] = T.e[i];
+          S0.dv[i] = T.dv[i];
+        }
       }
     }
     __syncthreads();
@@ -131,10 +141,55 @@ __global__ void __launch_bounds__(TAIL_TPB, 1) k_coarse_tail(const __grid_consta
       sync();
     }
   }
-  if (use_smem) {   // the top tail level's correction goes back to global memory
+  if (BASIS) {   // column blockIdx.x of B_tail
+    for (int i = threadIdx.x; i < nfb; i += TAIL_TPB)
+      Bt[(int64_t)i * nfb + blockIdx.x] = SP.lev[0].e[tfidx[i]];
+  } else if (use_smem) {   // the top tail level's correction goes back to global memory
     const int64_t n = G.lev[0].d.ndof;
     for (int64_t i = threadIdx.x; i < n; i += TAIL_TPB) G.lev[0].e[i] = SP.lev[0].e[i];
   }
+}
+
+__global__ void __launch_bounds__(TAIL_TPB, 1) k_coarse_tail(const __grid_constant__ TailParams G) {
+  k_coarse_tail_t<false>(G, nullptr, 0, nullptr);
+}
+__global__ void __launch_bounds__(TAIL_TPB, 1) k_tail_basis(const __grid_constant__ TailParams G,
+                                                            const int* __restrict__ tfidx, int nfb,
+                                                            double* Bt) {
+  k_coarse_tail_t<true>(G, tfidx, nfb, Bt);
+}
+
+// e = B_tail r on the free dofs of the top tail level: one warp per row, lanes
+// stride the row (coalesced), fixed shuffle tree (deterministic)
+__global__ void __launch_bounds__(256) k_tail_dense(const int* __restrict__ tfidx, int nf,
+                                                    const double* __restrict__ Bt,
+                                                    const double* __restrict__ r, double* e) {
+  pdl_enter();
+  const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (warp >= nf) return;
+  const double* row = Bt + (int64_t)warp * nf;
+  double acc = 0.0;
+  for (int j = lane; j < nf; j += 32) acc = fma(row[j], r[tfidx[j]], acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) e[tfidx[warp]] = acc;
+}
+
+int launch_tail_dense(const int* tfidx, int nf, const double* Bt, const double* r, double* e,
+                      cudaStream_t st) {
+  launch_ex(k_tail_dense, (nf + 7) / 8, 256, 0, true, st, tfidx, nf, Bt, r, e);
+  return 1;
+}
+
+int launch_tail_basis(const TailParams& P, const int* tfidx, int nf, double* Bt, cudaStream_t st) {
+  const size_t smem = (size_t)P.smem_doubles * sizeof(double);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(k_tail_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  k_tail_basis<<<nf, TAIL_TPB, smem, st>>>(P, tfidx, nf, Bt);
+  return 1;
 }
 
 // deterministic cluster-wide sum: CTA sums (fixed shuffle tree) -> part[rank]

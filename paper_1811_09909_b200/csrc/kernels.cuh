@@ -66,11 +66,12 @@ __host__ __device__ __forceinline__ void elem_slot(int nx, int i, int j, int& co
   s = (int64_t)j * (nx >> 1) + (i >> 1);
 }
 // (colour, s) -> element (i,j)
+// (32-bit unsigned division: every slot / edge / dof index of a level is < 2^32)
 __host__ __device__ __forceinline__ void slot_elem(int nx, int colour, int64_t s, int& i,
                                                    int& j) {
-  int nxh = nx >> 1;
-  j = (int)(s / nxh);
-  i = 2 * (int)(s - (int64_t)j * nxh) + ((j + colour) & 1);
+  const unsigned nxh = (unsigned)(nx >> 1), su = (unsigned)s;
+  j = (int)(su / nxh);
+  i = 2 * (int)(su - (unsigned)j * nxh) + ((j + colour) & 1);
 }
 // the 4 edges {bottom, right, top, left} of element (i,j) and their dOmega flags
 __host__ __device__ __forceinline__ void elem_edges(int nx, int ny, int i, int j, int64_t e[4],
@@ -86,14 +87,13 @@ __host__ __device__ __forceinline__ void elem_edges(int nx, int ny, int i, int j
 }
 // edge id -> is it on dOmega
 __host__ __device__ __forceinline__ bool edge_on_boundary(int nx, int ny, int64_t e) {
-  int64_t nh = (int64_t)nx * (ny + 1);
-  if (e < nh) {
-    int j = (int)(e / nx);
-    return j == 0 || j == ny;
+  const unsigned nh = (unsigned)nx * (unsigned)(ny + 1), eu = (unsigned)e;
+  if (eu < nh) {
+    const unsigned j = eu / (unsigned)nx;
+    return j == 0 || j == (unsigned)ny;
   }
-  int64_t r = e - nh;
-  int i = (int)(r % (nx + 1));
-  return i == 0 || i == nx;
+  const unsigned i = (eu - nh) % (unsigned)(nx + 1);
+  return i == 0 || i == (unsigned)nx;
 }
 
 // ---------------------------------------------------------------- device error slot

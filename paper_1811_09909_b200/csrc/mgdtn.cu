@@ -69,6 +69,11 @@ struct Ctx {
   int tail_start = -1;            // first level run by k_coarse_tail (-1: none)
   bool tail_vcycle = true;        // V-cycle levels >= tail_start through k_coarse_tail
   bool tail_lmax = true;          // their Chebyshev power iterations through k_tail_lmax
+  bool tail_dense = false;        // B_tail as an explicit matrix (k_tail_basis / k_tail_dense)
+  int nft = 0;                    // free dofs of the top tail level
+  size_t o_Bt = 0, o_tfidx = 0;
+  double* Bt = nullptr;
+  int* tfidx = nullptr;
   TailParams tail{};
   size_t o_ist = 0, o_hist = 0;
   int* ist = nullptr;             // device PCG state (k_pcg_check)
@@ -170,6 +175,10 @@ static void layout(Ctx* c) {
   c->o_fidx = take((size_t)c->nf * sizeof(int));
   c->o_A1 = take((size_t)c->nf * c->nf * sizeof(double));
   c->o_A1inv = take((size_t)c->nf * c->nf * sizeof(double));
+  if (c->tail_dense) {
+    c->o_Bt = take((size_t)c->nft * c->nft * sizeof(double));
+    c->o_tfidx = take((size_t)c->nft * sizeof(int));
+  }
   c->ws_need = off;
 }
 
@@ -191,6 +200,10 @@ static void bind_pointers(Ctx* c) {
   c->fidx = reinterpret_cast<int*>(b + c->o_fidx);
   c->A1 = D(c->o_A1);
   c->A1inv = D(c->o_A1inv);
+  if (c->tail_dense) {
+    c->Bt = D(c->o_Bt);
+    c->tfidx = reinterpret_cast<int*>(b + c->o_tfidx);
+  }
   c->Kc = D(c->o_K);
   c->tauc = D(c->o_tau);
   c->methc = reinterpret_cast<int8_t*>(b + c->o_meth);
@@ -280,6 +293,21 @@ static void plan_tail(Ctx* c) {
   }
 }
 
+// B_tail explicit (MGDTN_TAIL_DENSE, default on): the whole tail V-cycle is a
+// fixed linear operator on the top tail level's free dofs; it is tabulated once
+// per setup (one tail V-cycle per unit vector, all columns in one launch) and
+// applied as one dense matvec per V-cycle.
+static void plan_tail_dense(Ctx* c) {
+  c->tail_dense = false;
+  c->nft = 0;
+  if (c->tail_start < 0 || !c->tail_vcycle || env_or("MGDTN_TAIL_DENSE", 1) == 0) return;
+  const LevelDev& d = c->lev[c->tail_start].d;
+  const int64_t nf = ((int64_t)d.nx * (d.ny - 1) + (int64_t)(d.nx - 1) * d.ny) * d.k1;
+  if (nf <= 0 || nf > 2048) return;
+  c->nft = (int)nf;
+  c->tail_dense = true;
+}
+
 static void fill_tail(Ctx* c) {
   if (c->tail_start < 0) return;
   TailParams& T = c->tail;
@@ -292,6 +320,7 @@ static void fill_tail(Ctx* c) {
     nd += 4 * d.ndof + (k < nlev - 1 ? (int64_t)(d.nx / 2) * (d.ny / 2) * 8 : 0);
   }
   T.smem_doubles = (env_or("MGDTN_TAIL_SMEM", 1) != 0 && nd * 8 <= 200 * 1024) ? (int)nd : 0;
+  if (T.smem_doubles == 0) c->tail_dense = false;   // the basis kernel needs shared-memory vectors
   T.fidx = c->fidx;
   T.nf = c->nf;
   T.A1inv = c->A1inv;
@@ -337,6 +366,16 @@ static int upload_static(Ctx* c) {
   if (!fidx.empty())
     CK(cudaMemcpyAsync(c->fidx, fidx.data(), fidx.size() * sizeof(int), cudaMemcpyHostToDevice,
                        c->st));
+  if (c->tail_dense) {
+    const LevelDev& t = c->lev[c->tail_start].d;
+    std::vector<int> tf;
+    for (int64_t e = 0; e < t.nedge; ++e) {
+      if (edge_on_boundary(t.nx, t.ny, e)) continue;
+      for (int a = 0; a < t.k1; ++a) tf.push_back((int)(e * t.k1 + a));
+    }
+    CK(cudaMemcpyAsync(c->tfidx, tf.data(), tf.size() * sizeof(int), cudaMemcpyHostToDevice,
+                       c->st));
+  }
   CK(cudaStreamSynchronize(c->st));
   return MG_OK;
 }
@@ -387,6 +426,10 @@ static inline void residual(Ctx* c, HostLevel& L) {  // L.w = L.r - A L.e
 static void vcycle_level(Ctx* c, int li, bool first_done) {
   HostLevel& L = c->lev[li];
   const int nlev = (int)c->lev.size();
+  if (c->tail_dense && li == c->tail_start) {   // this level and every coarser one: e = B_tail r
+    c->launches += launch_tail_dense(c->tfidx, c->nft, c->Bt, L.r, L.e, c->st);
+    return;
+  }
   if (c->tail_vcycle && li == c->tail_start) {   // this level and every coarser one: one launch
     TailParams& T = c->tail;
     T.nu_pre = c->sm.nu_pre;
@@ -411,7 +454,7 @@ static void vcycle_level(Ctx* c, int li, bool first_done) {
   for (int s = s0; s < nu_pre; ++s) smooth_step(c, L, s);
   residual(c, L);  // L.w = r - A e1
   HostLevel& C = c->lev[li + 1];
-  const bool fuse = (li + 1 < nlev - 1) && nu_pre > 0;
+  const bool fuse = (li + 1 < nlev - 1) && nu_pre > 0 && !(c->tail_dense && li + 1 == c->tail_start);
   if (L.kind == KIND_H) {
     c->launches += launch_lc_restrict(L.d, L.w, L.e, L.KIIinv, L.Pm, L.cbuf, true, true, c->st);
     c->launches += launch_restrict_edges(L.d, C.d, L.w, L.cbuf, C.r, fuse, C.e, C.dv, c->st);
@@ -489,6 +532,15 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
     CK(cudaMemsetAsync(L.w, 0, L.d.ndof * sizeof(double), st));
     CK(cudaMemsetAsync(L.dv, 0, L.d.ndof * sizeof(double), st));
     CK(cudaMemsetAsync(L.r, 0, L.d.ndof * sizeof(double), st));
+  }
+  if (c->tail_dense) {
+    TailParams& T = c->tail;
+    T.nu_pre = c->sm.nu_pre;
+    T.nu_post = c->sm.nu_post;
+    T.first_fused = 0;
+    for (int k = 0; k < T.nlev; ++k) T.lev[k].d = c->lev[c->tail_start + k].d;
+    c->launches += launch_tail_basis(T, c->tfidx, c->nft, c->Bt, st);
+    CK(cudaGetLastError());
   }
   RC(check_device_error(c));
   c->setup_done = true;
@@ -764,8 +816,9 @@ int mg_build_hierarchy(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
     delete c;
     return MG_ERR_SHAPE;
   }
-  layout(c);   // host only: no CUDA call until mg_bind_workspace
   plan_tail(c);
+  plan_tail_dense(c);
+  layout(c);   // host only: no CUDA call until mg_bind_workspace
   *out_ctx = c;
   return MG_OK;
 }

@@ -25,6 +25,12 @@ struct TailParams {
 };
 
 int launch_coarse_tail(const TailParams& P, cudaStream_t st);
+// B_tail as a dense matrix (setup): column j = the tail V-cycle applied to the
+// unit vector on free dof tfidx[j] of the top tail level; Bt row-major [nf][nf]
+int launch_tail_basis(const TailParams& P, const int* tfidx, int nf, double* Bt, cudaStream_t st);
+// e = B_tail r on the top tail level's free dofs (warp per row, deterministic)
+int launch_tail_dense(const int* tfidx, int nf, const double* Bt, const double* r, double* e,
+                      cudaStream_t st);
 // Chebyshev lambda_max (Q11) of every tail level but the coarsest, one launch;
 // part: >= cluster-size doubles of scratch.
 int launch_tail_lmax(const TailParams& P, int iters, double safety, double ratio, int nu_max,
