@@ -59,7 +59,7 @@ enum {
   MG_ERR_SINGULAR_LOCAL = -3,   /* a local (element) solve broke down */
   MG_ERR_NOT_SPD = -4,          /* Cholesky of a local block / edge block / A_1 failed */
   MG_ERR_CUDA = -5,             /* CUDA runtime error (message has the CUDA string) */
-  MG_ERR_NCCL = -6,             /* reserved: multi-GPU communicator error */
+  MG_ERR_NCCL = -6,             /* multi-GPU communicator (NCCL / loopback) error */
   MG_ERR_STATE = -7,            /* call order violated (e.g. solve before setup) */
   MG_ERR_WORKSPACE = -8,        /* workspace missing, too small or misaligned */
   MG_ERR_UNSUPPORTED = -9       /* valid request this build does not implement */
@@ -83,12 +83,50 @@ typedef struct {
   double x0, y0, h;
 } mg_quad_mesh;
 
-/* Element-block partition for multi-GPU runs (reserved; NULL or nranks == 1
- * selects the single-GPU path, the only one this build implements). */
+/* Element-block partition for multi-GPU runs (NULL or
+ * nranks == 1 selects the single-GPU path).  One rank per GPU; rank
+ * r = ry*px + rx holds the global elements [rx*nx/px, (rx+1)*nx/px) x
+ * [ry*ny/py, (ry+1)*ny/py) of every level down to the gather level and the
+ * whole of every coarser level.  On a rank, mg_quad_mesh stays the GLOBAL mesh;
+ * every element array (K, method, tau, f samples) is the rank's block in local
+ * element order (local id = jl*(nx/px) + il), every trace vector is the block's
+ * local edge numbering (the header's numbering on the nx/px x ny/py block), and
+ * interface edges are held by both ranks with identical values; g_D samples are
+ * the block's 2*(nx/px)+2*(ny/py) boundary edges (interface ones ignored).
+ * Dots count an interface edge once (the rank below / to the left owns it).
+ *   nccl_id:   128 bytes from mg_get_nccl_unique_id on rank 0, the same on every
+ *              rank (the caller broadcasts it, e.g. torch.distributed)
+ *   gather_ne: replicate levels with <= gather_ne global elements (0: 16384)
+ *   loopback:  NULL, or a hub from mg_loopback_create (nranks virtual ranks in one
+ *              process on one GPU, each driven by its own host thread -- tests) */
 typedef struct {
   int32_t rank, nranks, px, py;
   const uint8_t* nccl_id;
+  int32_t gather_ne;
+  void* loopback;
 } mg_partition;
+
+/* NCCL unique id (rank 0), MG_ERR_NCCL if libnccl.so.2 cannot be loaded. */
+int mg_get_nccl_unique_id(uint8_t out[128]);
+/* Loopback communicator hub for nranks virtual ranks on one GPU (tests). */
+void* mg_loopback_create(int32_t nranks);
+void mg_loopback_destroy(void* hub);
+
+/* Host-only partition plan (no device work; for checking the decomposition):
+ * nlevels, the paper-numbered level of the first replicated level (0: none)
+ * and, per level k = 1..nlevels, info[8*(k-1) ..] = {nx, ny, ox, oy, gnx, gny,
+ * dmask, imask}: this rank's block dims, its element offset in the global
+ * level, the global level dims, the sides on dOmega and the partition-interface
+ * sides (bit f: 0 bottom, 1 right, 2 top, 3 left). */
+int mg_partition_plan(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
+                      const mg_partition* part, int32_t max_levels, int32_t* nlevels,
+                      int32_t* gather_level, int32_t* info);
+/* Global edge ids (in halo-message order) of interface side `side` of a level's
+ * block: the neighbour's matching side must list the same ids in the same order.
+ * global_edges may be NULL (count only). */
+int mg_partition_side_edges(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
+                            const mg_partition* part, int32_t level, int32_t side,
+                            int64_t* global_edges, int32_t* count);
 
 /* Smoother configuration.  V(nu_pre, nu_post); the Chebyshev "steps" are the
  * polynomial degree.  lambda_max of D_B^-1 A_k is estimated per level by
@@ -106,8 +144,10 @@ typedef struct {
 
 /* Build the level structure (host only; no device work).  p in 1..4.
  * n_h_levels = 0 coarsens until the macro mesh is 2 x 2 (or until a side
- * becomes odd).  Errors: MG_ERR_ARG, MG_ERR_SHAPE, MG_ERR_UNSUPPORTED
- * (partition with nranks > 1, nx != ny layouts the coarsening cannot reach). */
+ * becomes odd).  With a partition (nranks > 1) it also creates the communicator
+ * (collective: every rank calls it).  Errors: MG_ERR_ARG, MG_ERR_SHAPE,
+ * MG_ERR_NCCL.  On a partitioned ctx every call that launches work is
+ * collective (all ranks call it in the same order). */
 int mg_build_hierarchy(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
                        const mg_partition* part, void* cuda_stream, void** out_ctx);
 

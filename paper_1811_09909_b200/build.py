@@ -16,13 +16,13 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
 
-SOURCES = ["k_apply.cu", "k_setup.cu", "k_mg.cu", "k_coarse.cu", "mgdtn.cu", "refelem.cpp"]
+SOURCES = ["k_apply.cu", "k_setup.cu", "k_mg.cu", "k_coarse.cu", "k_part.cu", "comm.cu", "mgdtn.cu", "refelem.cpp"]
 
 
 def _compile(src: str) -> str:
     out = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
     path = os.path.join(CSRC, src)
-    deps = [path] + [os.path.join(CSRC, h) for h in ("kernels.cuh", "bodies.cuh", "tail.h", "refelem.h")] + \
+    deps = [path] + [os.path.join(CSRC, h) for h in ("kernels.cuh", "bodies.cuh", "tail.h", "refelem.h", "comm.h")] + \
         [os.path.join(ROOT, "include", "mgdtn.h")]
     if os.path.exists(out) and all(os.path.getmtime(out) >= os.path.getmtime(d) for d in deps):
         return out
@@ -42,7 +42,7 @@ def build(verbose: bool = False) -> str:
         objs = list(ex.map(_compile, SOURCES))
     if os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(o) for o in objs):
         return LIB
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -35,13 +35,24 @@ __device__ __forceinline__ void gather_x(const double* x, const int64_t ed[4], c
 // Edges on dOmega: y written as 0 (W0/APPLY/RESID), untouched by AM_SMOOTH.
 // NC: r may be read through the non-coherent path (true unless r is written
 // earlier in the same kernel, as in k_coarse_tail).
+// itf: bit f set if edge f is a partition interface edge (multi-GPU): the
+// colour-1 pass stores only this rank's partial sum there (y = y_T) and the
+// interface epilogue (k_itf_epilogue) finishes it after the halo exchange.
 template <int K1, int MODE, bool NC = true>
 __device__ __forceinline__ void epi_load(const LevelDev& L, const int64_t ed[4], const bool bd[4],
                                          const double* y, const double* __restrict__ r,
-                                         const double* d, double* t, double* dd) {
+                                         const double* d, double* t, double* dd, int itf = 0) {
   if (MODE == AM_W0) return;
 #pragma unroll
   for (int f = 0; f < 4; ++f) {
+    if ((itf >> f) & 1) {
+#pragma unroll
+      for (int a = 0; a < K1; ++a) {
+        t[f * K1 + a] = 0.0;
+        dd[f * K1 + a] = 0.0;
+      }
+      continue;
+    }
     const int64_t base = ed[f] * K1;
 #pragma unroll
     for (int a = 0; a < K1; ++a) {
@@ -57,10 +68,16 @@ template <int K1, int MODE, bool DOT>
 __device__ __forceinline__ void epi_store(const LevelDev& L, const int64_t ed[4], const bool bd[4],
                                           const double* xv, const double* yv, const double* t,
                                           const double* dd, const double* x, double* y, double* d,
-                                          int step, double c1, double c2, double& dot) {
+                                          int step, double c1, double c2, double& dot,
+                                          int itf = 0) {
 #pragma unroll
   for (int f = 0; f < 4; ++f) {
     const int64_t base = ed[f] * K1;
+    if (MODE != AM_W0 && ((itf >> f) & 1)) {   // partial sum only; finished after the halo
+#pragma unroll
+      for (int a = 0; a < K1; ++a) y[base + a] = yv[f * K1 + a];
+      continue;
+    }
     if (MODE == AM_W0) {
 #pragma unroll
       for (int a = 0; a < K1; ++a) y[base + a] = bd[f] ? 0.0 : yv[f * K1 + a];
@@ -156,7 +173,7 @@ __device__ __forceinline__ double apply_pass_body(const LevelDev& L, int colour,
     slot_elem(L.nx, colour, s, i, j);
     int64_t ed[4];
     bool bd[4];
-    elem_edges(L.nx, L.ny, i, j, ed, bd);
+    elem_edges(L.nx, L.ny, i, j, ed, bd, L.dmask);
     double xv[M], yv[M], t[M], dd[M];
     gather_x<K1>(x, ed, bd, xv);
     epi_load<K1, MODE, NC>(L, ed, bd, y, r, d, t, dd);
@@ -167,11 +184,13 @@ __device__ __forceinline__ double apply_pass_body(const LevelDev& L, int colour,
   return dot;
 }
 
-// power-iteration start vector (Q11): v_i = 1 + (i mod 7)/7 on free dofs, i = dof id
+// power-iteration start vector (Q11): v_i = 1 + (i mod 7)/7 on free dofs, i = GLOBAL
+// dof id (the same vector on 1 GPU and on any partition; duplicated interface dofs agree)
 __device__ __forceinline__ void pow_init_body(const LevelDev& L, double* v, int64_t t0, int64_t nt) {
   for (int64_t i = t0; i < L.ndof; i += nt) {
     const int64_t e = (unsigned)i / (unsigned)L.k1;
-    v[i] = edge_on_boundary(L.nx, L.ny, e) ? 0.0 : 1.0 + (double)((unsigned)i % 7u) / 7.0;
+    const int64_t gi = global_edge(L, e) * L.k1 + (i - e * L.k1);
+    v[i] = edge_on_boundary(L.nx, L.ny, e, L.dmask) ? 0.0 : 1.0 + (double)(gi % 7) / 7.0;
   }
 }
 
@@ -182,7 +201,7 @@ __device__ __forceinline__ void smooth_first_body(const LevelDev& L, const doubl
   const int K1 = L.k1;
   const double c2 = L.coef[1];
   for (int64_t ed = t0; ed < L.nedge; ed += nt) {
-    if (edge_on_boundary(L.nx, L.ny, ed)) continue;
+    if (edge_on_boundary(L.nx, L.ny, ed, L.dmask)) continue;
     const double* Di = L.Dinv + ed;
     for (int a = 0; a < K1; ++a) {
       double c = 0.0;
@@ -256,36 +275,43 @@ __device__ __forceinline__ void restrict_edges_body(const LevelDev& F, const Lev
   const double c2 = fuse ? C.coef[1] : 0.0;
   for (int64_t E = t0; E < C.nedge; E += nt) {
     double v0 = 0.0, v1 = 0.0;
-    bool bnd;
+    // coarse edge on a local mesh side: on dOmega (no dofs) or a partition interface
+    // (J^T res only here; the two adjacent macros' P_M^T terms live on two ranks and
+    // are added by k_restrict_itf after the halo exchange)
+    const int sd = edge_side(nxc, nyc, E);
+    const bool bnd = sd >= 0 && ((C.dmask >> sd) & 1);
+    const bool itf = sd >= 0 && !bnd;
     if (E < nh) {
       const int J = (int)((unsigned)E / (unsigned)nxc), I = (int)E - J * nxc;
-      bnd = (J == 0 || J == nyc);
       if (!bnd) {
         const int64_t f0 = hedge(F.nx, 2 * I, 2 * J), f1 = hedge(F.nx, 2 * I + 1, 2 * J);
         const double a0 = res[f0 * 2], a1 = res[f0 * 2 + 1], b0 = res[f1 * 2], b1 = res[f1 * 2 + 1];
         v0 = a0 + 0.5 * a1 + 0.5 * b0;
         v1 = 0.5 * a1 + 0.5 * b0 + b1;
-        const int64_t Mb = (int64_t)(J - 1) * nxc + I, Ma = (int64_t)J * nxc + I;
-        v0 += cbuf[Mb * 8 + 4] + cbuf[Ma * 8 + 0];
-        v1 += cbuf[Mb * 8 + 5] + cbuf[Ma * 8 + 1];
+        if (!itf) {
+          const int64_t Mb = (int64_t)(J - 1) * nxc + I, Ma = (int64_t)J * nxc + I;
+          v0 += cbuf[Mb * 8 + 4] + cbuf[Ma * 8 + 0];
+          v1 += cbuf[Mb * 8 + 5] + cbuf[Ma * 8 + 1];
+        }
       }
     } else {
       const int64_t rr = E - nh;
       const int J = (int)((unsigned)rr / (unsigned)(nxc + 1)), I = (int)rr - J * (nxc + 1);
-      bnd = (I == 0 || I == nxc);
       if (!bnd) {
         const int64_t f0 = vedge(F.nx, F.ny, 2 * I, 2 * J), f1 = vedge(F.nx, F.ny, 2 * I, 2 * J + 1);
         const double a0 = res[f0 * 2], a1 = res[f0 * 2 + 1], b0 = res[f1 * 2], b1 = res[f1 * 2 + 1];
         v0 = a0 + 0.5 * a1 + 0.5 * b0;
         v1 = 0.5 * a1 + 0.5 * b0 + b1;
-        const int64_t Ml = (int64_t)J * nxc + (I - 1), Mr = (int64_t)J * nxc + I;
-        v0 += cbuf[Ml * 8 + 2] + cbuf[Mr * 8 + 6];
-        v1 += cbuf[Ml * 8 + 3] + cbuf[Mr * 8 + 7];
+        if (!itf) {
+          const int64_t Ml = (int64_t)J * nxc + (I - 1), Mr = (int64_t)J * nxc + I;
+          v0 += cbuf[Ml * 8 + 2] + cbuf[Mr * 8 + 6];
+          v1 += cbuf[Ml * 8 + 3] + cbuf[Mr * 8 + 7];
+        }
       }
     }
     rc[E * 2] = v0;
     rc[E * 2 + 1] = v1;
-    if (fuse && !bnd) {
+    if (fuse && !bnd && !itf) {
       const double* Di = C.Dinv + E;
       const int64_t sd = C.nedge;
       double e0 = c2 * (Di[0] * v0 + Di[sd] * v1);
@@ -316,7 +342,7 @@ __device__ __forceinline__ void prolong_macro_body(const LevelDev& F, const Leve
     const int J = (int)((unsigned)M / (unsigned)nxc), I = (int)M - J * nxc;
     int64_t ce[4];
     bool cb[4];
-    elem_edges(nxc, nyc, I, J, ce, cb);
+    elem_edges(nxc, nyc, I, J, ce, cb, C.dmask);
     double c[8];
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
@@ -353,7 +379,7 @@ __device__ __forceinline__ void p_restrict_body(const LevelDev& F, const LevelDe
   const int K1 = F.k1;
   const double c2 = fuse ? C.coef[1] : 0.0;
   for (int64_t E = t0; E < F.nedge; E += nt) {
-    if (edge_on_boundary(F.nx, F.ny, E)) {
+    if (edge_on_boundary(F.nx, F.ny, E, F.dmask)) {
       rc[E * 2] = 0.0;
       rc[E * 2 + 1] = 0.0;
       continue;
@@ -386,7 +412,7 @@ __device__ __forceinline__ void p_prolong_body(const LevelDev& F, const double* 
                                                int64_t t0, int64_t nt) {
   const int K1 = F.k1;
   for (int64_t E = t0; E < F.nedge; E += nt) {
-    if (edge_on_boundary(F.nx, F.ny, E)) continue;
+    if (edge_on_boundary(F.nx, F.ny, E, F.dmask)) continue;
     const double c0 = ec[E * 2], c1 = ec[E * 2 + 1];
     for (int a = 0; a < K1; ++a) e[E * K1 + a] += fma(Jp[a * 2], c0, Jp[a * 2 + 1] * c1);
   }

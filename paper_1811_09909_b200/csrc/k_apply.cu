@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, 
   // another same-colour element, so the early read is exact in every mode)
   int64_t edn[4] = {0, 0, 0, 0};
   bool bdn[4] = {true, true, true, true};
+  int itfn = 0;
   double xn[M];
   auto prefetch = [&](int k) {
 #pragma unroll
@@ -150,9 +151,11 @@ __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, 
     if (k < nmine && s < nec) {
       int i, j;
       slot_elem(L.nx, colour, s, i, j);
-      elem_edges(L.nx, L.ny, i, j, edn, bdn);
+      elem_edges(L.nx, L.ny, i, j, edn, bdn, L.dmask);
+      itfn = elem_itf(L.nx, L.ny, i, j, L.imask);
       gather_x<K1>(x, edn, bdn, xn);
     } else {
+      itfn = 0;
 #pragma unroll
       for (int f = 0; f < 4; ++f) {
         edn[f] = 0;
@@ -167,6 +170,7 @@ __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, 
     const bool act = s < nec;
     int64_t ed[4];
     bool bd[4];
+    const int itf = itfn;
     double xv[M], yv[M], t[M], dd[M];
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
@@ -180,7 +184,7 @@ __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, 
       t[a] = 0.0;
       dd[a] = 0.0;
     }
-    if (act) epi_load<K1, MODE>(L, ed, bd, y, r, d, t, dd);   // needed after the matvec only
+    if (act) epi_load<K1, MODE>(L, ed, bd, y, r, d, t, dd, itf);   // needed after the matvec only
     if (XPF) prefetch(k + 1);
     const int st = k % NST;
     mbar_wait(&bars[st], (uint32_t)((k / NST) & 1));
@@ -200,7 +204,7 @@ __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, 
       fence_proxy_async();
       issue(k + NST);
     }
-    if (act) epi_store<K1, MODE, DOT>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot);
+    if (act) epi_store<K1, MODE, DOT>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot, itf);
     if (!XPF) prefetch(k + 1);
   }
   if (DOT) {
@@ -312,6 +316,7 @@ __global__ void __launch_bounds__(32) k_apply_seg(const LevelDev L, int colour, 
     const bool act = s < nec;
     int64_t ed[4] = {0, 0, 0, 0};
     bool bd[4] = {true, true, true, true};
+    int itf = 0;
     double xv[M], yv[M], t[M], dd[M];
 #pragma unroll
     for (int a = 0; a < M; ++a) {
@@ -323,9 +328,10 @@ __global__ void __launch_bounds__(32) k_apply_seg(const LevelDev L, int colour, 
     if (act) {   // every global read of the element, independent of the ring: overlaps the wait
       int i, j;
       slot_elem(L.nx, colour, s, i, j);
-      elem_edges(L.nx, L.ny, i, j, ed, bd);
+      elem_edges(L.nx, L.ny, i, j, ed, bd, L.dmask);
+      itf = elem_itf(L.nx, L.ny, i, j, L.imask);
       gather_x<K1>(x, ed, bd, xv);
-      epi_load<K1, MODE>(L, ed, bd, y, r, d, t, dd);
+      epi_load<K1, MODE>(L, ed, bd, y, r, d, t, dd, itf);
     }
     const int g0 = k * NS;
     const double* Sp = nullptr;
@@ -342,7 +348,7 @@ __global__ void __launch_bounds__(32) k_apply_seg(const LevelDev L, int colour, 
       }
     }
     if (!HASD) {
-      if (act) epi_store<K1, MODE, DOT>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot);
+      if (act) epi_store<K1, MODE, DOT>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot, itf);
       continue;
     }
     // smoothing / power-iteration epilogue with D_e^-1 from the ring (packed upper
@@ -365,6 +371,11 @@ __global__ void __launch_bounds__(32) k_apply_seg(const LevelDev L, int colour, 
 #pragma unroll
             for (int a = 0; a < K1; ++a) y[base + a] = 0.0;
           }
+          continue;
+        }
+        if ((itf >> f) & 1) {   // partition interface: partial sum, finished after the halo
+#pragma unroll
+          for (int a = 0; a < K1; ++a) y[base + a] = yv[f * K1 + a];
           continue;
         }
         double res[K1];
@@ -556,7 +567,7 @@ __global__ void __launch_bounds__(32) k_apply_fused(const LevelDev L, const doub
     if (act) {
       int i, j;
       slot_elem(L.nx, colour, s, i, j);
-      elem_edges(L.nx, L.ny, i, j, ed, bd);
+      elem_edges(L.nx, L.ny, i, j, ed, bd, L.dmask);
       gather_x<K1>(x, ed, bd, xv);
       if (colour == 1) {
         if (FLAGS) epi_load_r<K1, MODE>(L, ed, bd, r, d, t, dd);
@@ -644,10 +655,11 @@ __global__ void __launch_bounds__(128) k_apply_ldg(const LevelDev L, int colour,
     slot_elem(L.nx, colour, s, i, j);
     int64_t ed[4];
     bool bd[4];
-    elem_edges(L.nx, L.ny, i, j, ed, bd);
+    elem_edges(L.nx, L.ny, i, j, ed, bd, L.dmask);
+    const int itf = elem_itf(L.nx, L.ny, i, j, L.imask);
     double xv[M], yv[M], t[M], dd[M];
     gather_x<K1>(x, ed, bd, xv);
-    epi_load<K1, MODE>(L, ed, bd, y, r, d, t, dd);
+    epi_load<K1, MODE>(L, ed, bd, y, r, d, t, dd, itf);
 #pragma unroll
     for (int a = 0; a < M; ++a) yv[a] = 0.0;
     const double* Sp = L.S + ((((int64_t)colour * L.nchunk + (s >> 5)) * NPK) << 5) + (s & 31);
@@ -661,7 +673,7 @@ __global__ void __launch_bounds__(128) k_apply_ldg(const LevelDev L, int colour,
         if (b != a) yv[b] = fma(sv, xv[a], yv[b]);
       }
     }
-    epi_store<K1, MODE, DOT>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot);
+    epi_store<K1, MODE, DOT>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot, itf);
   }
   if (DOT) {
     __shared__ double red[4];
@@ -981,7 +993,7 @@ int launch_apply(const LevelDev& L, int colour, int mode, const double* x, doubl
 
 int launch_apply2(const LevelDev& L, int mode, const double* x, double* y, const double* r,
                   double* d, int step, double* partials, bool pdl, cudaStream_t st) {
-  if (!use_fused() || L.sync == nullptr) {
+  if (!use_fused() || L.sync == nullptr || L.imask != 0) {   // fused: single GPU only
     int n = launch_apply(L, 0, AM_W0, x, y, nullptr, nullptr, 0, nullptr, pdl, st);
     return n + launch_apply(L, 1, mode, x, y, r, d, step, partials, pdl, st);
   }

@@ -132,20 +132,32 @@ __device__ __forceinline__ double block_sum(double v) {
 
 int vec_grid(int64_t n) { return cap_grid(n, 256, 148 * 4); }
 
+// OwnMask: dofs of non-owned partition-interface edges are skipped, so a global
+// dot product counts every duplicated dof once (nomask == 0: single GPU)
+struct OwnMask {
+  int nx, ny, k1, nomask;
+};
+static OwnMask own_mask(const LevelDev* L) {
+  return L ? OwnMask{L->nx, L->ny, L->k1, nonowned_mask(L->imask)} : OwnMask{1, 1, 1, 0};
+}
+__device__ __forceinline__ bool counted(const OwnMask& o, int64_t i) {
+  return !o.nomask || edge_counted(o.nx, o.ny, (unsigned)i / (unsigned)o.k1, o.nomask);
+}
+
 __global__ void k_dot(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
-                      double* partials) {
+                      double* partials, OwnMask om) {
   pdl_enter();
   double s = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    s = fma(a[i], b[i], s);
+    if (counted(om, i)) s = fma(a[i], b[i], s);
   s = block_sum(s);
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
 int launch_dot(const double* a, const double* b, int64_t n, double* partials, int grid,
-               cudaStream_t st) {
-  launch_ex(k_dot, grid, 256, 0, true, st, a, b, n, partials);
+               cudaStream_t st, const LevelDev* L) {
+  launch_ex(k_dot, grid, 256, 0, true, st, a, b, n, partials, own_mask(L));
   return 1;
 }
 
@@ -176,7 +188,7 @@ int launch_reduce(const double* partials, int n, double* scal, int slot, int op,
 
 __global__ void k_pcg_update(double* x, double* r, const double* __restrict__ p,
                              const double* __restrict__ ap, const double* __restrict__ scal,
-                             int64_t n, double* partials) {
+                             int64_t n, double* partials, OwnMask om) {
   pdl_enter();
   const double alpha = scal[3];
   double s = 0.0;
@@ -185,7 +197,7 @@ __global__ void k_pcg_update(double* x, double* r, const double* __restrict__ p,
     x[i] = fma(alpha, p[i], x[i]);
     const double ri = fma(-alpha, ap[i], r[i]);
     r[i] = ri;
-    s = fma(ri, ri, s);
+    if (counted(om, i)) s = fma(ri, ri, s);
   }
   s = block_sum(s);
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
@@ -193,8 +205,25 @@ __global__ void k_pcg_update(double* x, double* r, const double* __restrict__ p,
 
 int launch_pcg_update(double* x, double* r, const double* p, const double* ap,
                       const double* scal, int64_t n, double* partials, int grid,
-                      cudaStream_t st) {
-  launch_ex(k_pcg_update, grid, 256, 0, true, st, x, r, p, ap, scal, n, partials);
+                      cudaStream_t st, const LevelDev* L) {
+  launch_ex(k_pcg_update, grid, 256, 0, true, st, x, r, p, ap, scal, n, partials, own_mask(L));
+  return 1;
+}
+
+// scalar op of k_reduce on an already reduced (all-reduced) value scal[src]:
+// op 1: alpha = scal[0] / s; op 2: beta = s / scal[0]; then scal[dst] = s
+__global__ void k_scalar_op(double* scal, int src, int dst, int op) {
+  pdl_enter();
+  if (threadIdx.x == 0) {
+    const double s = scal[src];
+    if (op == 1) scal[3] = s > 0.0 ? scal[0] / s : 0.0;
+    else if (op == 2) scal[4] = s / scal[0];
+    scal[dst] = s;
+  }
+}
+
+int launch_scalar_op(double* scal, int src, int dst, int op, cudaStream_t st) {
+  launch_ex(k_scalar_op, 1, 32, 0, true, st, scal, src, dst, op);
   return 1;
 }
 
@@ -281,7 +310,7 @@ __global__ void k_edge_dinv(LevelDev L, const double* __restrict__ y, double* u,
   double s_uu = 0.0, s_uy = 0.0;
   for (int64_t ed = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ed < L.nedge;
        ed += (int64_t)gridDim.x * blockDim.x) {
-    if (edge_on_boundary(L.nx, L.ny, ed)) {
+    if (edge_on_boundary(L.nx, L.ny, ed, L.dmask)) {
       for (int a = 0; a < K1; ++a) u[ed * K1 + a] = 0.0;
       continue;
     }
@@ -376,7 +405,7 @@ __global__ void k_copy_masked(LevelDev L, double* dst, const double* __restrict_
   pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.ndof;
        i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = edge_on_boundary(L.nx, L.ny, i / L.k1) ? 0.0 : src[i];
+    dst[i] = edge_on_boundary(L.nx, L.ny, (unsigned)i / (unsigned)L.k1, L.dmask) ? 0.0 : src[i];
 }
 
 int launch_copy_masked(const LevelDev& L, double* dst, const double* src, cudaStream_t st) {

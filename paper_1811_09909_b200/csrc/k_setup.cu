@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(128) k_local_rhs(
     }
     int64_t ed[4];
     bool bd[4];
-    elem_edges(L.nx, L.ny, i, j, ed, bd);
+    elem_edges(L.nx, L.ny, i, j, ed, bd, L.dmask);
     if (lamD && (bd[0] || bd[1] || bd[2] || bd[3])) {   // b -= S_T lambda_D
       double lt[M];
 #pragma unroll
@@ -231,10 +231,15 @@ __global__ void k_dirichlet(LevelDev L, RefDev R, const double* __restrict__ gD,
   const int K1 = L.k1, nq = R.nqf;
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
     int64_t e;
-    if (b < L.nx) e = hedge(L.nx, b, 0);
-    else if (b < 2 * L.nx) e = hedge(L.nx, b - L.nx, L.ny);
-    else if (b < 2 * L.nx + L.ny) e = vedge(L.nx, L.ny, 0, b - 2 * L.nx);
-    else e = vedge(L.nx, L.ny, L.nx, b - 2 * L.nx - L.ny);
+    int side;
+    if (b < L.nx) { e = hedge(L.nx, b, 0); side = 0; }
+    else if (b < 2 * L.nx) { e = hedge(L.nx, b - L.nx, L.ny); side = 2; }
+    else if (b < 2 * L.nx + L.ny) { e = vedge(L.nx, L.ny, 0, b - 2 * L.nx); side = 3; }
+    else { e = vedge(L.nx, L.ny, L.nx, b - 2 * L.nx - L.ny); side = 1; }
+    if (!((L.dmask >> side) & 1)) {   // partition interface: not on dOmega
+      for (int a = 0; a < K1; ++a) lamD[e * K1 + a] = 0.0;
+      continue;
+    }
     double mom[MAX_K1];
     for (int a = 0; a < K1; ++a) {
       double acc = 0.0;
@@ -466,7 +471,8 @@ __global__ void k_edge_blocks(LevelDev L, DevError* err) {
     double D[MAX_K1 * MAX_K1];
     double* out = L.Dinv + e;   // SoA, stride nedge
     const int64_t sd = L.nedge;
-    if (edge_on_boundary(L.nx, L.ny, e)) {
+    const int side = edge_side(L.nx, L.ny, e);
+    if (side >= 0 && ((L.dmask >> side) & 1)) {
       for (int q = 0; q < K1 * K1; ++q) out[q * sd] = 0.0;
       continue;
     }
@@ -483,6 +489,8 @@ __global__ void k_edge_blocks(LevelDev L, DevError* err) {
     }
     for (int q = 0; q < K1 * K1; ++q) D[q] = 0.0;
     for (int t = 0; t < 2; ++t) {
+      // on a partition interface one of the two elements lives on the neighbour rank
+      if (ei[t] < 0 || ei[t] >= L.nx || ej[t] < 0 || ej[t] >= L.ny) continue;
       int colour;
       int64_t s;
       elem_slot(L.nx, ei[t], ej[t], colour, s);
@@ -490,36 +498,13 @@ __global__ void k_edge_blocks(LevelDev L, DevError* err) {
       for (int a = 0; a < K1; ++a)
         for (int b = 0; b < K1; ++b) D[a * K1 + b] += pk_get(src, m, ef[t] * K1 + a, ef[t] * K1 + b);
     }
-    // Cholesky + explicit inverse
-    double Lc[MAX_K1 * MAX_K1];
-    bool ok = true;
-    for (int j = 0; j < K1; ++j) {
-      double d = D[j * K1 + j];
-      for (int k = 0; k < j; ++k) d -= Lc[j * K1 + k] * Lc[j * K1 + k];
-      if (!(d > 0.0)) { ok = false; d = 1e-300; }
-      d = sqrt(d);
-      Lc[j * K1 + j] = d;
-      for (int i = j + 1; i < K1; ++i) {
-        double s = D[i * K1 + j];
-        for (int k = 0; k < j; ++k) s -= Lc[i * K1 + k] * Lc[j * K1 + k];
-        Lc[i * K1 + j] = s / d;
-      }
+    if (side >= 0) {   // interface: this rank's partial block; inverted after the halo (k_part.cu)
+      for (int q = 0; q < K1 * K1; ++q) out[q * sd] = D[q];
+      continue;
     }
-    if (!ok) report_error(err, -4, e);
-    for (int c = 0; c < K1; ++c) {
-      double v[MAX_K1];
-      for (int a = 0; a < K1; ++a) {
-        double s = (a == c) ? 1.0 : 0.0;
-        for (int k = 0; k < a; ++k) s -= Lc[a * K1 + k] * v[k];
-        v[a] = s / Lc[a * K1 + a];
-      }
-      for (int a = K1 - 1; a >= 0; --a) {
-        double s = v[a];
-        for (int k = a + 1; k < K1; ++k) s -= Lc[k * K1 + a] * v[k];
-        v[a] = s / Lc[a * K1 + a];
-      }
-      for (int a = 0; a < K1; ++a) out[(a * K1 + c) * sd] = v[a];
-    }
+    double inv[MAX_K1 * MAX_K1];
+    if (!chol_inverse(D, K1, inv)) report_error(err, -4, e);
+    for (int q = 0; q < K1 * K1; ++q) out[q * sd] = inv[q];
   }
 }
 
@@ -542,7 +527,7 @@ __global__ void k_dinv_pack(LevelDev L) {
     if (s < nec) {
       int i, j;
       slot_elem(L.nx, 1, s, i, j);
-      elem_edges(L.nx, L.ny, i, j, ed, bd);
+      elem_edges(L.nx, L.ny, i, j, ed, bd, L.dmask);
     }
     double* dst = L.Dc + ((s >> 5) * L.ndi) * 32 + (s & 31);
     for (int f = 0; f < 4; ++f)
@@ -642,7 +627,7 @@ __global__ void k_coarse_factor(LevelDev L, const int* __restrict__ fpos, int nf
       const double* src = L.S + s_offset(L.nchunk, L.npk, colour, s, 0);
       int64_t ed[4];
       bool bd[4];
-      elem_edges(L.nx, L.ny, i, j, ed, bd);
+      elem_edges(L.nx, L.ny, i, j, ed, bd, L.dmask);
       int gi[4 * MAX_K1];
       for (int f = 0; f < 4; ++f)
         for (int a = 0; a < L.k1; ++a) gi[f * L.k1 + a] = fpos[ed[f] * L.k1 + a];

@@ -10,6 +10,7 @@
 // chunk = s/32, lane = s%32.
 #pragma once
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 
 namespace mgdtn {
@@ -41,7 +42,28 @@ struct LevelDev {
   int smoother;            // 0 BJ, 1 Chebyshev (d vector used)
   unsigned* sync;          // fused apply: [0] generation, [1] CTA exit count,
                            // [2 + c] generation at which colour-0 chunk c was stored
+  // partitioned levels (multi-GPU): local sides 0 bottom, 1 right, 2 top, 3 left
+  int dmask;               // sides on the global boundary dOmega (Dirichlet); 15 on one GPU
+  int imask;               // sides that are partition interfaces (15 & ~dmask on a rank, or 0)
+  int ox, oy, gnx, gny;    // this block's element offset in the global level and the global
+                           // level's dims (0, 0, nx, ny on one GPU)
 };
+
+// global edge id of local edge e of a level block (power-iteration start vector)
+__host__ __device__ __forceinline__ int64_t global_edge(const LevelDev& L, int64_t e) {
+  const int64_t nh = (int64_t)L.nx * (L.ny + 1);
+  if (e < nh) {
+    const int j = (int)(e / L.nx), i = (int)(e - (int64_t)j * L.nx);
+    return (int64_t)(L.oy + j) * L.gnx + (L.ox + i);
+  }
+  const int64_t r = e - nh;
+  const int j = (int)(r / (L.nx + 1)), i = (int)(r - (int64_t)j * (L.nx + 1));
+  return (int64_t)L.gnx * (L.gny + 1) + (int64_t)(L.oy + j) * (L.gnx + 1) + (L.ox + i);
+}
+
+// non-owned interface sides: an interface edge is counted in dot products by
+// one rank only, the one below / to the left of it
+__host__ __device__ __forceinline__ int nonowned_mask(int imask) { return imask & 9; }
 
 // ---------------------------------------------------------------- indexing
 __host__ __device__ __forceinline__ int64_t hedge(int nx, int i, int j) {
@@ -74,26 +96,54 @@ __host__ __device__ __forceinline__ void slot_elem(int nx, int colour, int64_t s
   i = 2 * (int)(su - (unsigned)j * nxh) + ((j + colour) & 1);
 }
 // the 4 edges {bottom, right, top, left} of element (i,j) and their dOmega flags
+// (dmask: which local mesh sides lie on dOmega; the others are partition interfaces)
 __host__ __device__ __forceinline__ void elem_edges(int nx, int ny, int i, int j, int64_t e[4],
-                                                    bool bd[4]) {
+                                                    bool bd[4], int dmask = 15) {
   e[0] = hedge(nx, i, j);
   e[1] = vedge(nx, ny, i + 1, j);
   e[2] = hedge(nx, i, j + 1);
   e[3] = vedge(nx, ny, i, j);
-  bd[0] = (j == 0);
-  bd[1] = (i == nx - 1);
-  bd[2] = (j == ny - 1);
-  bd[3] = (i == 0);
+  bd[0] = (j == 0) && (dmask & 1);
+  bd[1] = (i == nx - 1) && (dmask & 2);
+  bd[2] = (j == ny - 1) && (dmask & 4);
+  bd[3] = (i == 0) && (dmask & 8);
 }
-// edge id -> is it on dOmega
-__host__ __device__ __forceinline__ bool edge_on_boundary(int nx, int ny, int64_t e) {
+// interface bits of element (i,j): bit f set if its edge f lies on a partition interface
+__host__ __device__ __forceinline__ int elem_itf(int nx, int ny, int i, int j, int imask) {
+  if (!imask) return 0;
+  return ((j == 0) ? (imask & 1) : 0) | ((i == nx - 1) ? (imask & 2) : 0) |
+         ((j == ny - 1) ? (imask & 4) : 0) | ((i == 0) ? (imask & 8) : 0);
+}
+// local side of edge e: -1 if not on the local mesh boundary, else 0 bottom, 1 right, 2 top, 3 left
+__host__ __device__ __forceinline__ int edge_side(int nx, int ny, int64_t e) {
   const unsigned nh = (unsigned)nx * (unsigned)(ny + 1), eu = (unsigned)e;
   if (eu < nh) {
     const unsigned j = eu / (unsigned)nx;
-    return j == 0 || j == (unsigned)ny;
+    return j == 0 ? 0 : j == (unsigned)ny ? 2 : -1;
   }
   const unsigned i = (eu - nh) % (unsigned)(nx + 1);
-  return i == 0 || i == (unsigned)nx;
+  return i == 0 ? 3 : i == (unsigned)nx ? 1 : -1;
+}
+// edge id -> is it on dOmega
+__host__ __device__ __forceinline__ bool edge_on_boundary(int nx, int ny, int64_t e,
+                                                          int dmask = 15) {
+  const int sd = edge_side(nx, ny, e);
+  return sd >= 0 && ((dmask >> sd) & 1);
+}
+// edge id -> counted by this rank in global dot products (not a non-owned interface edge)
+__host__ __device__ __forceinline__ bool edge_counted(int nx, int ny, int64_t e, int nomask) {
+  if (!nomask) return true;
+  const int sd = edge_side(nx, ny, e);
+  return sd < 0 || !((nomask >> sd) & 1);
+}
+// interface edges of side f in their order along the side (the neighbour rank's
+// matching side lists the same global edges in the same order)
+__host__ __device__ __forceinline__ int side_len(int nx, int ny, int f) {
+  return (f == 0 || f == 2) ? nx : ny;
+}
+__host__ __device__ __forceinline__ int64_t side_edge(int nx, int ny, int f, int q) {
+  return f == 0 ? hedge(nx, q, 0) : f == 2 ? hedge(nx, q, ny) : f == 3 ? vedge(nx, ny, 0, q)
+                                                                      : vedge(nx, ny, nx, q);
 }
 
 // ---------------------------------------------------------------- device error slot
@@ -104,6 +154,42 @@ struct DevError {
 };
 __device__ __forceinline__ void report_error(DevError* err, int code, long long index) {
   if (atomicCAS(&err->code, 0, code) == 0) err->index = index;
+}
+
+// explicit inverse of an SPD k x k block (row-major) by Cholesky; false if not SPD
+__host__ __device__ __forceinline__ bool chol_inverse(const double* D, int K1, double* inv) {
+  double Lc[MAX_K1 * MAX_K1];
+  bool ok = true;
+  for (int j = 0; j < K1; ++j) {
+    double d = D[j * K1 + j];
+    for (int k = 0; k < j; ++k) d -= Lc[j * K1 + k] * Lc[j * K1 + k];
+    if (!(d > 0.0)) {
+      ok = false;
+      d = 1e-300;
+    }
+    d = sqrt(d);
+    Lc[j * K1 + j] = d;
+    for (int i = j + 1; i < K1; ++i) {
+      double s = D[i * K1 + j];
+      for (int k = 0; k < j; ++k) s -= Lc[i * K1 + k] * Lc[j * K1 + k];
+      Lc[i * K1 + j] = s / d;
+    }
+  }
+  for (int c = 0; c < K1; ++c) {
+    double v[MAX_K1];
+    for (int a = 0; a < K1; ++a) {
+      double s = (a == c) ? 1.0 : 0.0;
+      for (int k = 0; k < a; ++k) s -= Lc[a * K1 + k] * v[k];
+      v[a] = s / Lc[a * K1 + a];
+    }
+    for (int a = K1 - 1; a >= 0; --a) {
+      double s = v[a];
+      for (int k = a + 1; k < K1; ++k) s -= Lc[k * K1 + a] * v[k];
+      v[a] = s / Lc[a * K1 + a];
+    }
+    for (int a = 0; a < K1; ++a) inv[a * K1 + c] = v[a];
+  }
+  return ok;
 }
 
 // reference tables on the device (one set per p)
@@ -205,15 +291,17 @@ int launch_coarse_solve(const LevelDev& L, const int* fidx, int nf, const double
 
 // vectors / reductions (grid-stride, deterministic two-stage reductions)
 int vec_grid(int64_t n);
+// L (optional): skip the non-owned partition-interface dofs of that level
 int launch_dot(const double* a, const double* b, int64_t n, double* partials, int grid,
-               cudaStream_t st);
+               cudaStream_t st, const LevelDev* L = nullptr);
+int launch_scalar_op(double* scal, int src, int dst, int op, cudaStream_t st);
 // out[slot] = sum(partials[0:n]); then op: 0 none, 1 alpha = s[0]/sum (breakdown check),
 // 2 beta = sum/s[0] and s[0] = sum
 int launch_reduce(const double* partials, int n, double* scal, int slot, int op,
                   DevError* err, cudaStream_t st);
 int launch_pcg_update(double* x, double* r, const double* p, const double* ap,
                       const double* scal, int64_t n, double* partials, int grid,
-                      cudaStream_t st);
+                      cudaStream_t st, const LevelDev* L = nullptr);
 int launch_pcg_pupdate(double* p, const double* z, const double* scal, int64_t n,
                        cudaStream_t st);
 int launch_pcg_init(int* istate, double* scal, double rtol, int maxit, cudaStream_t st);
@@ -231,5 +319,30 @@ int launch_copy(double* dst, const double* src, int64_t n, cudaStream_t st);
 int launch_zero(double* dst, int64_t n, cudaStream_t st);
 int launch_copy_masked(const LevelDev& L, double* dst, const double* src, cudaStream_t st);
 int launch_add(double* dst, const double* src, int64_t n, cudaStream_t st);
+
+// ---------------------------------------------------------------- partitioned levels (k_part.cu)
+int itf_stride(const LevelDev& L);     // doubles per side in a halo buffer
+int eblk_stride(const LevelDev& L);    // doubles per side in an edge-block halo buffer
+__host__ __device__ int64_t itf_edges(const LevelDev& L);
+int itf_blocks();                      // partial-sum slots of launch_itf_epilogue
+int launch_itf_pack(const LevelDev& L, const double* y, double* send, cudaStream_t st);
+int launch_itf_epilogue(const LevelDev& L, int mode, double* x, double* y, const double* r,
+                        double* d, int step, const double* recv, double* partials,
+                        cudaStream_t st);
+int launch_restrict_halo_pack(const LevelDev& C, const double* cbuf, double* send,
+                              cudaStream_t st);
+int launch_restrict_halo_finish(const LevelDev& C, double* rc, const double* send,
+                                const double* recv, bool fuse, double* ec, double* dc,
+                                cudaStream_t st);
+int launch_prolong_itf(const LevelDev& F, const LevelDev& C, const double* ec, double* e,
+                       cudaStream_t st);
+int launch_eblk_pack(const LevelDev& L, double* send, cudaStream_t st);
+int launch_eblk_finish(const LevelDev& L, const double* recv, DevError* err, cudaStream_t st);
+int launch_gather_vec(const LevelDev& G, int bx, int by, int px, int py, int64_t ndof_loc,
+                      const double* all, double* out, cudaStream_t st);
+int launch_scatter_vec(const LevelDev& Lc, int ox, int oy, int nxg, int nyg, const double* glob,
+                       double* loc, cudaStream_t st);
+int launch_gather_S(const LevelDev& G, int bx, int by, int px, const double* dense,
+                    cudaStream_t st);
 
 }  // namespace mgdtn

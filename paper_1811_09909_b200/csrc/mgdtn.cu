@@ -3,6 +3,7 @@
 // CUDA-graph capture of the per-iteration kernel sequences.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -12,6 +13,7 @@
 #include <vector>
 
 #include "../../include/mgdtn.h"
+#include "comm.h"
 #include "kernels.cuh"
 #include "refelem.h"
 #include "tail.h"
@@ -78,7 +80,19 @@ struct Ctx {
   size_t o_ist = 0, o_hist = 0;
   int* ist = nullptr;             // device PCG state (k_pcg_check)
   double* dhist = nullptr;        // device residual history [HIST_CAP]
+  // ---- element-block partition over ranks; nranks == 1: single GPU
+  Comm* comm = nullptr;
+  int rank = 0, nranks = 1, px = 1, py = 1, rx = 0, ry = 0;
+  int nbr[4] = {-1, -1, -1, -1};   // neighbour rank across local side f (bottom, right, top, left)
+  int Lg = -1;                     // first replicated level (every rank holds it whole); the
+                                   // levels above it hold this rank's element block only
+  HostLevel lgl;                   // this rank's block of level Lg (restriction / prolongation)
+  size_t o_hs = 0, o_hr = 0, o_gall = 0, o_sden = 0, o_sall = 0, halo_doubles = 0;
+  int comm_rc = 0;                 // first communicator failure (reported by the next sync point)
+  double *hsend = nullptr, *hrecv = nullptr, *gall = nullptr, *sden = nullptr, *sall = nullptr;
 };
+
+static bool partitioned(const Ctx* c) { return c->nranks > 1; }
 
 static int fail(Ctx* c, int code, const std::string& msg, long long idx = -1) {
   if (c) {
@@ -122,6 +136,12 @@ static void init_level(HostLevel& L, int nx, int ny, int p, double h, int kind) 
   d.nedge = (int64_t)nx * (ny + 1) + (int64_t)(nx + 1) * ny;
   d.ndof = d.nedge * d.k1;
   d.nchunk = (int)((d.ne / 2 + 31) / 32);
+  d.dmask = 15;
+  d.imask = 0;
+  d.ox = 0;
+  d.oy = 0;
+  d.gnx = nx;
+  d.gny = ny;
   d.ndi = 4 * d.k1 * (d.k1 + 1) / 2;
   L.h = h;
   L.kind = kind;
@@ -179,6 +199,26 @@ static void layout(Ctx* c) {
     c->o_Bt = take((size_t)c->nft * c->nft * sizeof(double));
     c->o_tfidx = take((size_t)c->nft * sizeof(int));
   }
+  if (partitioned(c)) {
+    HostLevel& G = c->lgl;
+    const LevelDev& d = G.d;
+    G.o_sync = take((size_t)(2 + d.nchunk) * sizeof(unsigned));
+    G.o_S = take((size_t)2 * d.nchunk * d.npk * 32 * sizeof(double));
+    G.o_r = take(d.ndof * sizeof(double));
+    G.o_e = take(d.ndof * sizeof(double));
+    size_t hd = 0;
+    for (int li = 0; li < c->Lg; ++li) {
+      const LevelDev& l = c->lev[li].d;
+      hd = std::max(hd, (size_t)4 * std::max(l.nx, l.ny) * l.k1 * l.k1);
+    }
+    hd = std::max(hd, (size_t)4 * std::max(d.nx, d.ny) * d.k1 * d.k1);
+    c->halo_doubles = hd;
+    c->o_hs = take(hd * sizeof(double));
+    c->o_hr = take(hd * sizeof(double));
+    c->o_gall = take((size_t)c->nranks * d.ndof * sizeof(double));
+    c->o_sden = take((size_t)d.ne * 64 * sizeof(double));
+    c->o_sall = take((size_t)c->nranks * d.ne * 64 * sizeof(double));
+  }
   c->ws_need = off;
 }
 
@@ -203,6 +243,18 @@ static void bind_pointers(Ctx* c) {
   if (c->tail_dense) {
     c->Bt = D(c->o_Bt);
     c->tfidx = reinterpret_cast<int*>(b + c->o_tfidx);
+  }
+  if (partitioned(c)) {
+    HostLevel& G = c->lgl;
+    G.d.sync = reinterpret_cast<unsigned*>(b + G.o_sync);
+    G.d.S = D(G.o_S);
+    G.r = D(G.o_r);
+    G.e = D(G.o_e);
+    c->hsend = D(c->o_hs);
+    c->hrecv = D(c->o_hr);
+    c->gall = D(c->o_gall);
+    c->sden = D(c->o_sden);
+    c->sall = D(c->o_sall);
   }
   c->Kc = D(c->o_K);
   c->tauc = D(c->o_tau);
@@ -279,7 +331,7 @@ static void plan_tail(Ctx* c) {
   const int nlev = (int)c->lev.size();
   c->tail_start = -1;
   if (tail_ne <= 0) return;
-  for (int li = 0; li < nlev; ++li) {
+  for (int li = c->Lg > 0 ? c->Lg : 0; li < nlev; ++li) {   // replicated levels only
     const LevelDev& d = c->lev[li].d;
     if (d.p == 1 && d.ne <= tail_ne && nlev - li >= 2 && nlev - li <= MAX_TAIL &&
         (li == 0 || c->lev[li - 1].kind == KIND_H || c->lev[li - 1].kind == KIND_P)) {
@@ -389,6 +441,7 @@ static int check_device_error(Ctx* c) {
   DevError h{};
   CK(cudaMemcpyAsync(&h, c->err, sizeof(DevError), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
+  if (c->comm_rc) return c->comm_rc;
   if (h.code == 0) return MG_OK;
   CK(cudaMemsetAsync(c->err, 0, sizeof(DevError), c->st));
   switch (h.code) {
@@ -404,18 +457,118 @@ static int check_device_error(Ctx* c) {
   }
 }
 
+// ---------------------------------------------------------------- communication (partitioned levels)
+static void comm_fail(Ctx* c, int rc) {
+  if (rc != 0 && c->comm_rc == 0) {
+    c->comm_rc = MG_ERR_NCCL;
+    c->last_err = "communicator: " + (c->comm ? c->comm->err : std::string("none"));
+  }
+}
+
+// exchange c->hsend -> c->hrecv with the neighbours across the interface sides of
+// level d: `per` doubles per interface edge, side stride `stride` doubles
+static void halo_exchange(Ctx* c, const LevelDev& d, int stride, int per) {
+  int cnt[4];
+  for (int f = 0; f < 4; ++f) cnt[f] = ((d.imask >> f) & 1) ? side_len(d.nx, d.ny, f) * per : 0;
+  comm_fail(c, c->comm->halo(c->nbr, c->hsend, c->hrecv, stride, cnt, c->st));
+}
+
+// scal[slot] = sum of partials over every rank (then the k_reduce op)
+static void reduce_scal(Ctx* c, const double* partials, int n, double* scal, int slot, int op) {
+  if (!partitioned(c)) {
+    c->launches += launch_reduce(partials, n, scal, slot, op, nullptr, c->st);
+    return;
+  }
+  constexpr int TMP = 14;
+  c->launches += launch_reduce(partials, n, scal, TMP, 0, nullptr, c->st);
+  comm_fail(c, c->comm->allreduce_sum(scal + TMP, 1, c->st));
+  c->launches += launch_scalar_op(scal, TMP, slot, op, c->st);
+}
+
 // ---------------------------------------------------------------- apply / smoothing building blocks
+// one apply in `mode` (bodies.cuh epilogues); on a partitioned level the colour
+// passes leave partial sums on the interface edges, which are exchanged and
+// finished by k_itf_epilogue (k_part.cu)
+static void apply_mode(Ctx* c, const HostLevel& L, int mode, const double* x, double* y,
+                       const double* r, double* d, int step, double* partials) {
+  c->launches += launch_apply2(L.d, mode, x, y, r, d, step, partials, true, c->st);
+  if (L.d.imask) {
+    c->launches += launch_itf_pack(L.d, y, c->hsend, c->st);
+    halo_exchange(c, L.d, itf_stride(L.d), L.d.k1);
+    c->launches += launch_itf_epilogue(L.d, mode, const_cast<double*>(x), y, r, d, step, c->hrecv,
+                                       partials ? partials + apply2_grid(L.d, mode) : nullptr,
+                                       c->st);
+  }
+}
+// number of dot-product partials apply_mode writes
+static int apply_parts(const LevelDev& d, int mode) {
+  return apply2_grid(d, mode) + (d.imask ? itf_blocks() : 0);
+}
+
 static inline void apply_full(Ctx* c, const HostLevel& L, const double* x, double* y,
                               double* partials) {
-  c->launches += launch_apply2(L.d, AM_APPLY, x, y, nullptr, nullptr, 0, partials, true, c->st);
+  apply_mode(c, L, AM_APPLY, x, y, nullptr, nullptr, 0, partials);
 }
 
 static inline void smooth_step(Ctx* c, HostLevel& L, int step) {
-  c->launches += launch_apply2(L.d, AM_SMOOTH, L.e, L.w, L.r, L.dv, step, nullptr, true, c->st);
+  apply_mode(c, L, AM_SMOOTH, L.e, L.w, L.r, L.dv, step, nullptr);
 }
 
 static inline void residual(Ctx* c, HostLevel& L) {  // L.w = L.r - A L.e
-  c->launches += launch_apply2(L.d, AM_RESID, L.e, L.w, L.r, nullptr, 0, nullptr, true, c->st);
+  apply_mode(c, L, AM_RESID, L.e, L.w, L.r, nullptr, 0, nullptr);
+}
+
+// is level li+1 the gather level (li the last partitioned level)?
+static inline bool gathers(const Ctx* c, int li) { return partitioned(c) && li + 1 == c->Lg; }
+
+// rc = Q_{k-1} res from level li into level li+1 (Eqs. 3.5 / 3.6); with do_lc,
+// also step 3 (e_I += A_II^-1 res_I, Eq. 3.11) on level li.  At the gather level
+// the result goes into this rank's block (lgl), then every rank's block is
+// all-gathered into the replicated level Lg.
+static void restrict_level(Ctx* c, int li, const double* res, double* e, bool do_lc, double* rc,
+                           bool fuse) {
+  HostLevel& L = c->lev[li];
+  const bool gat = gathers(c, li);
+  HostLevel& C = gat ? c->lgl : c->lev[li + 1];
+  double* rcl = gat ? c->lgl.r : rc;
+  if (gat) fuse = false;
+  if (L.kind == KIND_H) {
+    c->launches += launch_lc_restrict(L.d, res, e, L.KIIinv, L.Pm, L.cbuf, do_lc, true, c->st);
+    c->launches += launch_restrict_edges(L.d, C.d, res, L.cbuf, rcl, fuse, C.e, C.dv, c->st);
+    if (C.d.imask) {
+      c->launches += launch_restrict_halo_pack(C.d, L.cbuf, c->hsend, c->st);
+      halo_exchange(c, C.d, itf_stride(C.d), 2);
+      c->launches += launch_restrict_halo_finish(C.d, rcl, c->hsend, c->hrecv, fuse, C.e, C.dv,
+                                                 c->st);
+    }
+  } else {
+    c->launches += launch_p_restrict(L.d, C.d, c->refdev.Jp, res, rcl, fuse, C.e, C.dv, c->st);
+  }
+  if (gat) {
+    const LevelDev& B = c->lgl.d;
+    comm_fail(c, c->comm->allgather(c->lgl.r, c->gall, (size_t)B.ndof, c->st));
+    c->launches += launch_gather_vec(c->lev[c->Lg].d, B.nx, B.ny, c->px, c->py, B.ndof, c->gall,
+                                     rc, c->st);
+  }
+}
+
+// e += I_k ec (Eqs. 3.3 / 3.4) from level li+1 into level li
+static void prolong_level(Ctx* c, int li, const double* ec, double* e) {
+  HostLevel& L = c->lev[li];
+  const bool gat = gathers(c, li);
+  HostLevel& C = gat ? c->lgl : c->lev[li + 1];
+  const double* ecl = ec;
+  if (gat) {   // this rank's block of the replicated coarse correction
+    const LevelDev& G = c->lev[c->Lg].d;
+    c->launches += launch_scatter_vec(C.d, C.d.ox, C.d.oy, G.nx, G.ny, ec, c->lgl.e, c->st);
+    ecl = c->lgl.e;
+  }
+  if (L.kind == KIND_H) {
+    c->launches += launch_prolong_macro(L.d, C.d, ecl, L.Pm, e, c->st);
+    if (C.d.imask) c->launches += launch_prolong_itf(L.d, C.d, ecl, e, c->st);
+  } else {
+    c->launches += launch_p_prolong(L.d, c->refdev.Jp, ecl, e, c->st);
+  }
 }
 
 // V-cycle B_k (Algorithm 1) on level li with input L.r, output L.e.
@@ -454,18 +607,11 @@ static void vcycle_level(Ctx* c, int li, bool first_done) {
   for (int s = s0; s < nu_pre; ++s) smooth_step(c, L, s);
   residual(c, L);  // L.w = r - A e1
   HostLevel& C = c->lev[li + 1];
-  const bool fuse = (li + 1 < nlev - 1) && nu_pre > 0 && !(c->tail_dense && li + 1 == c->tail_start);
-  if (L.kind == KIND_H) {
-    c->launches += launch_lc_restrict(L.d, L.w, L.e, L.KIIinv, L.Pm, L.cbuf, true, true, c->st);
-    c->launches += launch_restrict_edges(L.d, C.d, L.w, L.cbuf, C.r, fuse, C.e, C.dv, c->st);
-  } else {
-    c->launches += launch_p_restrict(L.d, C.d, c->refdev.Jp, L.w, C.r, fuse, C.e, C.dv, c->st);
-  }
+  const bool fuse = (li + 1 < nlev - 1) && nu_pre > 0 &&
+                    !(c->tail_dense && li + 1 == c->tail_start) && !gathers(c, li);
+  restrict_level(c, li, L.w, L.e, true, C.r, fuse);
   vcycle_level(c, li + 1, fuse);
-  if (L.kind == KIND_H)
-    c->launches += launch_prolong_macro(L.d, C.d, C.e, L.Pm, L.e, c->st);
-  else
-    c->launches += launch_p_prolong(L.d, c->refdev.Jp, C.e, L.e, c->st);
+  prolong_level(c, li, C.e, L.e);
   for (int s = 0; s < nu_post; ++s) smooth_step(c, L, s);
 }
 
@@ -482,10 +628,19 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
   for (size_t li = 0; li + 1 < c->lev.size(); ++li) {
     HostLevel& L = c->lev[li];
     HostLevel& C = c->lev[li + 1];
-    if (L.kind == KIND_P)
+    if (L.kind == KIND_P) {
       c->launches += launch_p_coarsen(L.d, C.d, c->refdev.Jp, st);
-    else
+    } else if (gathers(c, (int)li)) {
+      // gather level: this rank's macros' coarse DtN maps, all-gathered into the
+      // replicated level (every rank then builds the coarser levels redundantly)
+      HostLevel& B = c->lgl;
+      c->launches += launch_agglomerate(L.d, B.d, L.KIIinv, L.Pm, c->err, st);
+      c->launches += launch_packed_to_dense(B.d, c->sden, st);
+      comm_fail(c, c->comm->allgather(c->sden, c->sall, (size_t)B.d.ne * 64, st));
+      c->launches += launch_gather_S(C.d, B.d.nx, B.d.ny, c->px, c->sall, st);
+    } else {
       c->launches += launch_agglomerate(L.d, C.d, L.KIIinv, L.Pm, c->err, st);
+    }
   }
   const int nlev = (int)c->lev.size();
   const int numax = MAX_NU;   // coefficients for any step count (mg_smooth may exceed nu)
@@ -493,6 +648,11 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
     HostLevel& L = c->lev[li];
     L.d.smoother = c->sm.kind;
     c->launches += launch_edge_blocks(L.d, c->err, st);
+    if (L.d.imask) {   // interface edge blocks: D_e = D_own + D_remote, then inverted
+      c->launches += launch_eblk_pack(L.d, c->hsend, st);
+      halo_exchange(c, L.d, eblk_stride(L.d), L.d.k1 * L.d.k1);
+      c->launches += launch_eblk_finish(L.d, c->hrecv, c->err, st);
+    }
     c->launches += launch_dinv_pack(L.d, st);
     if (c->sm.kind == MG_SMOOTH_BLOCK_JACOBI) {
       c->launches += launch_set_bj_coef(c->sm.omega, L.d.coef, st);
@@ -501,17 +661,14 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
     if (c->tail_lmax && li >= c->tail_start && c->tail_start >= 0) continue;   // k_tail_lmax below
     // Chebyshev: lambda_max of D_B^-1 A_k by power iteration (Q11):
     // v <- D^-1 A v in place (colour-1 epilogue AM_DINV), no per-step normalisation
-    const int ag = apply2_grid(L.d, AM_DINV);
     c->launches += launch_pow_init(L.d, L.e, st);
     for (int it = 0; it < c->sm.lmax_iters; ++it) {
       const bool last = it + 1 == c->sm.lmax_iters;
-      c->launches += launch_apply2(L.d, AM_DINV, L.e, L.w, nullptr, nullptr, 0,
-                                   last ? c->part : nullptr, true, st);
+      apply_mode(c, L, AM_DINV, L.e, L.w, nullptr, nullptr, 0, last ? c->part : nullptr);
     }
-    c->launches += launch_reduce(c->part, ag, c->sscal, 7, 0, nullptr, st);   // v.Dv
+    reduce_scal(c, c->part, apply_parts(L.d, AM_DINV), c->sscal, 7, 0);   // v.Dv
     apply_full(c, L, L.e, L.w, c->part);
-    c->launches += launch_reduce(c->part, apply2_grid(L.d, AM_APPLY), c->sscal, 8, 0, nullptr,
-                                 st);   // v.Av
+    reduce_scal(c, c->part, apply_parts(L.d, AM_APPLY), c->sscal, 8, 0);  // v.Av
     c->launches += launch_lmax_finish(c->sscal, c->sm.lmax_safety, c->sm.cheb_ratio, numax, L.lam,
                                       L.d.coef, st);
   }
@@ -533,6 +690,10 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
     CK(cudaMemsetAsync(L.dv, 0, L.d.ndof * sizeof(double), st));
     CK(cudaMemsetAsync(L.r, 0, L.d.ndof * sizeof(double), st));
   }
+  if (partitioned(c)) {
+    CK(cudaMemsetAsync(c->lgl.r, 0, c->lgl.d.ndof * sizeof(double), st));
+    CK(cudaMemsetAsync(c->lgl.e, 0, c->lgl.d.ndof * sizeof(double), st));
+  }
   if (c->tail_dense) {
     TailParams& T = c->tail;
     T.nu_pre = c->sm.nu_pre;
@@ -551,20 +712,20 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
 // scal: [0] rz, [1] pAp, [2] rr, [3] alpha, [4] beta, [5] gg
 static void pcg_iter_A(Ctx* c) {  // Ap, alpha, x/r update, rr
   HostLevel& F = c->lev[0];
-  const int ag = apply2_grid(F.d, AM_APPLY);
   const int vg = vec_grid(F.d.ndof);
   apply_full(c, F, c->pv, c->ap, c->part);
-  c->launches += launch_reduce(c->part, ag, c->scal, 1, 1, nullptr, c->st);
-  c->launches += launch_pcg_update(c->x, F.r, c->pv, c->ap, c->scal, F.d.ndof, c->part, vg, c->st);
-  c->launches += launch_reduce(c->part, vg, c->scal, 2, 0, nullptr, c->st);
+  reduce_scal(c, c->part, apply_parts(F.d, AM_APPLY), c->scal, 1, 1);
+  c->launches += launch_pcg_update(c->x, F.r, c->pv, c->ap, c->scal, F.d.ndof, c->part, vg, c->st,
+                                   &F.d);
+  reduce_scal(c, c->part, vg, c->scal, 2, 0);
 }
 
 static void pcg_iter_B(Ctx* c) {  // z = B r, beta, p update
   HostLevel& F = c->lev[0];
   const int vg = vec_grid(F.d.ndof);
   vcycle_level(c, 0, false);
-  c->launches += launch_dot(F.r, F.e, F.d.ndof, c->part, vg, c->st);
-  c->launches += launch_reduce(c->part, vg, c->scal, 0, 2, nullptr, c->st);
+  c->launches += launch_dot(F.r, F.e, F.d.ndof, c->part, vg, c->st, &F.d);
+  reduce_scal(c, c->part, vg, c->scal, 0, 2);
   c->launches += launch_pcg_pupdate(c->pv, F.e, c->scal, F.d.ndof, c->st);
 }
 
@@ -576,11 +737,11 @@ static void pcg_prologue(Ctx* c) {
   const int64_t n = F.d.ndof;
   const int vg = vec_grid(n);
   c->launches += launch_zero(c->x, n, c->st);
-  c->launches += launch_dot(F.r, F.r, n, c->part, vg, c->st);
-  c->launches += launch_reduce(c->part, vg, c->scal, 5, 0, nullptr, c->st);
+  c->launches += launch_dot(F.r, F.r, n, c->part, vg, c->st, &F.d);
+  reduce_scal(c, c->part, vg, c->scal, 5, 0);
   vcycle_level(c, 0, false);
-  c->launches += launch_dot(F.r, F.e, n, c->part, vg, c->st);
-  c->launches += launch_reduce(c->part, vg, c->scal, 0, 0, nullptr, c->st);
+  c->launches += launch_dot(F.r, F.e, n, c->part, vg, c->st, &F.d);
+  reduce_scal(c, c->part, vg, c->scal, 0, 0);
   c->launches += launch_copy(c->pv, F.e, n, c->st);
   pcg_iter_A(c);
   c->launches += launch_pcg_check(c->scal, c->ist, c->dhist, HIST_CAP, c->cond, c->st);
@@ -645,7 +806,7 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
   c->launches += launch_copy_masked(F.d, F.r, g, st);
   int status = MG_MAXIT, it = 0;
   double rel = 0.0;
-  if (c->use_graphs && maxit < HIST_CAP) {
+  if (c->use_graphs && maxit < HIST_CAP && !partitioned(c)) {
     if (!c->gS) RC(capture_solve(c));
     c->launches += launch_pcg_init(c->ist, c->scal, rtol, maxit, st);
     CK(cudaGraphLaunch(c->gS, st));
@@ -677,8 +838,8 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
   // eager host-driven loop (use_graphs off, legacy stream, or maxit >= HIST_CAP):
   // the same kernel sequence, with a host round trip per iteration
   c->launches += launch_zero(c->x, n, st);
-  c->launches += launch_dot(F.r, F.r, n, c->part, vg, st);
-  c->launches += launch_reduce(c->part, vg, c->scal, 5, 0, nullptr, st);
+  c->launches += launch_dot(F.r, F.r, n, c->part, vg, st, &F.d);
+  reduce_scal(c, c->part, vg, c->scal, 5, 0);
   CK(cudaMemcpyAsync(c->pinned, c->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const double gg = c->pinned[5];
@@ -694,8 +855,8 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
   }
   // z = B r ; rz = r.z ; p = z
   vcycle_level(c, 0, false);
-  c->launches += launch_dot(F.r, F.e, n, c->part, vg, st);
-  c->launches += launch_reduce(c->part, vg, c->scal, 0, 0, nullptr, st);
+  c->launches += launch_dot(F.r, F.e, n, c->part, vg, st, &F.d);
+  reduce_scal(c, c->part, vg, c->scal, 0, 0);
   c->launches += launch_copy(c->pv, F.e, n, st);
   CK(cudaGetLastError());
   for (it = 1; it <= maxit; ++it) {
@@ -741,6 +902,12 @@ static int rhs_impl(Ctx* c, const double* f_qp, double f_const, const double* gD
   CK(cudaMemsetAsync(g, 0, n * sizeof(double), st));
   c->launches += launch_local_rhs(F.d, c->refdev, F.h, c->Kc, c->methc, c->tauc, f_qp, f_const,
                                   gD_qp ? c->lamD : nullptr, g, c->err, st);
+  if (F.d.imask) {   // g = sum_T G_T^T b_T: interface edges sum both ranks' elements
+    c->launches += launch_itf_pack(F.d, g, c->hsend, st);
+    halo_exchange(c, F.d, itf_stride(F.d), F.d.k1);
+    c->launches += launch_itf_epilogue(F.d, AM_APPLY, nullptr, g, nullptr, nullptr, 0, c->hrecv,
+                                       nullptr, st);
+  }
   if (lambda_bc)
     CK(cudaMemcpyAsync(lambda_bc, c->lamD, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
   CK(cudaGetLastError());
@@ -760,11 +927,111 @@ using namespace mgdtn;
 // ============================================================================ C ABI
 extern "C" {
 
+}  // extern "C"
+
+namespace mgdtn {
+// Level structure (host only).  One GPU: finest (order p), the p-level (P1,
+// same mesh) if p > 1, then 2x2 agglomeration while both sides stay divisible
+// by 4.  Partitioned: the same global
+// sequence of levels; each rank holds its px x py element block of every level
+// down to the gather level Lg -- the first level whose global element count is
+// <= gather_ne, or whose blocks could not be agglomerated again, or the coarsest
+// -- and every level from Lg down is replicated on all ranks.
+static int build_levels(Ctx* c, const mg_quad_mesh* mesh, int p, int n_h_levels,
+                        const mg_partition* part) {
+  const int nx = mesh->nx, ny = mesh->ny;
+  const int nranks = part ? part->nranks : 1;
+  if (nranks > 1) {
+    if (part->px < 1 || part->py < 1 || part->px * part->py != nranks || part->rank < 0 ||
+        part->rank >= nranks)
+      return fail(c, MG_ERR_ARG, "partition: px * py must equal nranks, 0 <= rank < nranks");
+    if (nx % part->px || ny % part->py || ((nx / part->px) & 1) || ((ny / part->py) & 1))
+      return fail(c, MG_ERR_SHAPE, "partition: element blocks must have even sides");
+    c->nranks = nranks;
+    c->rank = part->rank;
+    c->px = part->px;
+    c->py = part->py;
+    c->rx = c->rank % c->px;
+    c->ry = c->rank / c->px;
+    c->nbr[0] = c->ry > 0 ? c->rank - c->px : -1;
+    c->nbr[1] = c->rx < c->px - 1 ? c->rank + 1 : -1;
+    c->nbr[2] = c->ry < c->py - 1 ? c->rank + c->px : -1;
+    c->nbr[3] = c->rx > 0 ? c->rank - 1 : -1;
+  }
+  int dmask = 15;
+  for (int f = 0; f < 4; ++f)
+    if (c->nbr[f] >= 0) dmask &= ~(1 << f);
+  const int imask = 15 & ~dmask;
+  const int64_t gather_ne = (part && part->gather_ne > 0) ? part->gather_ne : 16384;
+  auto local = [&](HostLevel& L, int gx, int gy) {   // this rank's block of a gx x gy level
+    LevelDev& d = L.d;
+    d.dmask = dmask;
+    d.imask = imask;
+    d.ox = c->rx * d.nx;
+    d.oy = c->ry * d.ny;
+    d.gnx = gx;
+    d.gny = gy;
+  };
+  int gx = nx, gy = ny;
+  int cx = nx / c->px, cy = ny / c->py;
+  double h = mesh->h;
+  HostLevel top;
+  init_level(top, cx, cy, p, h, KIND_COARSEST);
+  if (partitioned(c)) local(top, gx, gy);
+  c->lev.push_back(top);
+  if (p > 1) {
+    c->lev.back().kind = KIND_P;
+    HostLevel L1;
+    init_level(L1, cx, cy, 1, h, KIND_COARSEST);
+    if (partitioned(c)) local(L1, gx, gy);
+    c->lev.push_back(L1);
+  }
+  int nh = 0;
+  while (gx > 2 && gy > 2 && (gx % 4 == 0) && (gy % 4 == 0) &&
+         (n_h_levels <= 0 || nh < n_h_levels)) {
+    c->lev.back().kind = KIND_H;
+    const int ngx = gx / 2, ngy = gy / 2;
+    h *= 2;
+    HostLevel L;
+    if (partitioned(c) && c->Lg < 0) {
+      const int ncx = cx / 2, ncy = cy / 2;
+      const bool more = ngx > 2 && ngy > 2 && (ngx % 4 == 0) && (ngy % 4 == 0) &&
+                        (n_h_levels <= 0 || nh + 1 < n_h_levels);
+      const bool stay = more && (int64_t)ngx * ngy > gather_ne && ncx % 2 == 0 && ncy % 2 == 0;
+      if (stay) {
+        init_level(L, ncx, ncy, 1, h, KIND_COARSEST);
+        local(L, ngx, ngy);
+        cx = ncx;
+        cy = ncy;
+      } else {   // gather: this rank's block of the new level + the replicated level
+        init_level(c->lgl, ncx, ncy, 1, h, KIND_COARSEST);
+        local(c->lgl, ngx, ngy);
+        init_level(L, ngx, ngy, 1, h, KIND_COARSEST);
+        c->Lg = (int)c->lev.size();
+      }
+    } else {
+      init_level(L, ngx, ngy, 1, h, KIND_COARSEST);
+    }
+    c->lev.push_back(L);
+    gx = ngx;
+    gy = ngy;
+    ++nh;
+  }
+  if (partitioned(c) && c->Lg < 0)
+    return fail(c, MG_ERR_SHAPE, "partition: the hierarchy needs at least one 2x2 coarsening");
+  const LevelDev& d1 = c->lev.back().d;
+  c->nf = (int)(((int64_t)d1.nx * (d1.ny - 1) + (int64_t)(d1.nx - 1) * d1.ny) * d1.k1);
+  if (c->nf > 4096) return fail(c, MG_ERR_SHAPE, "coarsest level too large for the dense solve");
+  return MG_OK;
+}
+}  // namespace mgdtn
+
+extern "C" {
+
 int mg_build_hierarchy(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
                        const mg_partition* part, void* cuda_stream, void** out_ctx) {
   if (!mesh || !out_ctx) return MG_ERR_ARG;
   *out_ctx = nullptr;
-  if (part && part->nranks > 1) return MG_ERR_UNSUPPORTED;
   if (p < 1 || p > 4) return MG_ERR_ARG;
   const int nx = mesh->nx, ny = mesh->ny;
   if (nx < 2 || ny < 2 || (nx & 1) || (ny & 1) || !(mesh->h > 0)) return MG_ERR_SHAPE;
@@ -785,36 +1052,29 @@ int mg_build_hierarchy(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
   for (int k = 0; k < 2; ++k)
     c->ref_doubles += T.pen[k].lam.size() + T.pen[k].mu.size() + T.pen[k].At.size() +
                       T.pen[k].Bk.size() + T.pen[k].fqT.size();
-  // levels: finest (order p), the p-level (P1, same mesh) if p > 1, then 2x2
-  // agglomeration while both sides stay even
-  int cx = nx, cy = ny;
-  double h = mesh->h;
-  HostLevel top;
-  init_level(top, cx, cy, p, h, KIND_COARSEST);
-  c->lev.push_back(top);
-  if (p > 1) {
-    c->lev.back().kind = KIND_P;
-    HostLevel L1;
-    init_level(L1, cx, cy, 1, h, KIND_COARSEST);
-    c->lev.push_back(L1);
-  }
-  int nh = 0;
-  while (cx > 2 && cy > 2 && (cx % 4 == 0) && (cy % 4 == 0) &&
-         (n_h_levels <= 0 || nh < n_h_levels)) {
-    c->lev.back().kind = KIND_H;
-    cx /= 2;
-    cy /= 2;
-    h *= 2;
-    HostLevel L;
-    init_level(L, cx, cy, 1, h, KIND_COARSEST);
-    c->lev.push_back(L);
-    ++nh;
-  }
-  const LevelDev& d1 = c->lev.back().d;
-  c->nf = (int)(((int64_t)cx * (cy - 1) + (int64_t)(cx - 1) * cy) * d1.k1);
-  if (c->nf > 4096) {   // dense coarsest solve limit
+  int rc = build_levels(c, mesh, p, n_h_levels, part);
+  if (rc != MG_OK) {
     delete c;
-    return MG_ERR_SHAPE;
+    return rc;
+  }
+  if (partitioned(c)) {   // the communicator: loopback hub (tests) or NCCL (one process per GPU)
+    if (part->loopback) {
+      c->comm = make_loopback_comm(static_cast<LoopbackHub*>(part->loopback), c->rank);
+    } else {
+      if (!part->nccl_id) {
+        delete c;
+        return MG_ERR_ARG;
+      }
+      int dev = 0;
+      cudaGetDevice(&dev);
+      std::string err;
+      c->comm = make_nccl_comm(part->nccl_id, c->rank, c->nranks, dev, err);
+      if (!c->comm) {
+        delete c;
+        return MG_ERR_NCCL;
+      }
+    }
+    c->use_graphs = false;   // host-driven PCG loop (collectives between iterations)
   }
   plan_tail(c);
   plan_tail_dense(c);
@@ -822,6 +1082,56 @@ int mg_build_hierarchy(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
   *out_ctx = c;
   return MG_OK;
 }
+
+int mg_partition_plan(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
+                      const mg_partition* part, int32_t max_levels, int32_t* nlevels,
+                      int32_t* gather_level, int32_t* info) {
+  if (!mesh || !part || !nlevels || !gather_level || !info || max_levels < 1) return MG_ERR_ARG;
+  if (p < 1 || p > 4) return MG_ERR_ARG;
+  Ctx c;
+  int rc = build_levels(&c, mesh, p, n_h_levels, part);
+  if (rc != MG_OK) return rc;
+  const int N = (int)c.lev.size();
+  *nlevels = N;
+  *gather_level = c.Lg < 0 ? 0 : N - c.Lg;   // paper numbering of the first replicated level
+  for (int k = 0; k < N && k < max_levels; ++k) {
+    const LevelDev& d = c.lev[N - 1 - k].d;   // info[k] = level k+1 (paper numbering)
+    int32_t* o = info + 8 * k;
+    o[0] = d.nx; o[1] = d.ny; o[2] = d.ox; o[3] = d.oy;
+    o[4] = d.gnx; o[5] = d.gny; o[6] = d.dmask; o[7] = d.imask;
+  }
+  return MG_OK;
+}
+
+int mg_partition_side_edges(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
+                            const mg_partition* part, int32_t level, int32_t side,
+                            int64_t* global_edges, int32_t* count) {
+  if (!mesh || !part || !count || side < 0 || side > 3) return MG_ERR_ARG;
+  Ctx c;
+  int rc = build_levels(&c, mesh, p, n_h_levels, part);
+  if (rc != MG_OK) return rc;
+  const int N = (int)c.lev.size();
+  if (level < 1 || level > N) return MG_ERR_ARG;
+  const LevelDev& d = c.lev[N - level].d;
+  if (!((d.imask >> side) & 1)) {
+    *count = 0;
+    return MG_OK;
+  }
+  const int n = side_len(d.nx, d.ny, side);
+  *count = n;
+  if (global_edges)
+    for (int q = 0; q < n; ++q) global_edges[q] = global_edge(d, side_edge(d.nx, d.ny, side, q));
+  return MG_OK;
+}
+
+int mg_get_nccl_unique_id(uint8_t out[128]) {
+  if (!out) return MG_ERR_ARG;
+  std::string err;
+  return nccl_unique_id(out, err) == 0 ? MG_OK : MG_ERR_NCCL;
+}
+
+void* mg_loopback_create(int32_t nranks) { return nranks >= 1 ? loopback_create(nranks) : nullptr; }
+void mg_loopback_destroy(void* hub) { loopback_destroy(static_cast<LoopbackHub*>(hub)); }
 
 int mg_workspace_bytes(const void* ctx, size_t* bytes) {
   const Ctx* c = static_cast<const Ctx*>(ctx);
@@ -931,18 +1241,10 @@ int mg_restrict(void* ctx, int32_t level, const double* res, double* rc) {
   if (!c->setup_done) return fail(c, MG_ERR_STATE, "setup first");
   HostLevel* L = level_of(c, level);
   if (!L || L->kind == KIND_COARSEST) return fail(c, MG_ERR_ARG, "no coarser level");
-  HostLevel& C = *(L + 1);
-  if (L->kind == KIND_H) {
-    c->launches += launch_lc_restrict(L->d, res, nullptr, L->KIIinv, L->Pm, L->cbuf, false, true,
-                                      c->st);
-    c->launches += launch_restrict_edges(L->d, C.d, res, L->cbuf, rc, false, nullptr, nullptr,
-                                         c->st);
-  } else {
-    c->launches += launch_p_restrict(L->d, C.d, c->refdev.Jp, res, rc, false, nullptr, nullptr,
-                                     c->st);
-  }
+  const int li = (int)(L - &c->lev[0]);
+  restrict_level(c, li, res, nullptr, false, rc, false);
   CK(cudaGetLastError());
-  return MG_OK;
+  return c->comm_rc ? c->comm_rc : MG_OK;
 }
 
 int mg_prolong(void* ctx, int32_t level, const double* ec, double* e) {
@@ -951,13 +1253,10 @@ int mg_prolong(void* ctx, int32_t level, const double* ec, double* e) {
   if (!c->setup_done) return fail(c, MG_ERR_STATE, "setup first");
   HostLevel* L = level_of(c, level);
   if (!L || L->kind == KIND_COARSEST) return fail(c, MG_ERR_ARG, "no coarser level");
-  HostLevel& C = *(L + 1);
-  if (L->kind == KIND_H)
-    c->launches += launch_prolong_macro(L->d, C.d, ec, L->Pm, e, c->st);
-  else
-    c->launches += launch_p_prolong(L->d, c->refdev.Jp, ec, e, c->st);
+  const int li = (int)(L - &c->lev[0]);
+  prolong_level(c, li, ec, e);
   CK(cudaGetLastError());
-  return MG_OK;
+  return c->comm_rc ? c->comm_rc : MG_OK;
 }
 
 int mg_pcg_solve(void* ctx, const double* g, double* lambda, double rtol, int32_t maxit,
@@ -1157,6 +1456,7 @@ void mg_destroy(void* ctx) {
   Ctx* c = static_cast<Ctx*>(ctx);
   if (!c) return;
   drop_graphs(c);
+  delete c->comm;
   if (c->pinned) cudaFreeHost(c->pinned);
   delete c;
 }

@@ -33,7 +33,7 @@ class mg_quad_mesh(C.Structure):
 
 class mg_partition(C.Structure):
     _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("px", C.c_int32), ("py", C.c_int32),
-                ("nccl_id", C.c_void_p)]
+                ("nccl_id", C.c_void_p), ("gather_ne", C.c_int32), ("loopback", C.c_void_p)]
 
 
 class mg_smoother_cfg(C.Structure):
@@ -73,6 +73,14 @@ _SIGS = {
     "mg_last_launch_count": [_P, C.POINTER(C.c_int64)],
     "mg_total_launch_count": [_P, C.POINTER(C.c_int64)],
     "mg_set_use_graphs": [_P, C.c_int32],
+    "mg_partition_plan": [C.POINTER(mg_quad_mesh), C.c_int32, C.c_int32, C.POINTER(mg_partition),
+                          C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), _P],
+    "mg_partition_side_edges": [C.POINTER(mg_quad_mesh), C.c_int32, C.c_int32,
+                                C.POINTER(mg_partition), C.c_int32, C.c_int32, _P,
+                                C.POINTER(C.c_int32)],
+    "mg_get_nccl_unique_id": [_P],
+    "mg_loopback_create": [C.c_int32],
+    "mg_loopback_destroy": [_P],
     "mg_last_error": [_P],
     "mg_last_error_index": [_P],
     "mg_destroy": [_P],
@@ -97,6 +105,8 @@ def load_library(path: str = LIB_PATH):
     lib.mg_last_error.restype = C.c_char_p
     lib.mg_last_error_index.restype = C.c_int64
     lib.mg_destroy.restype = None
+    lib.mg_loopback_create.restype = C.c_void_p
+    lib.mg_loopback_destroy.restype = None
     _lib = lib
     return lib
 
@@ -142,15 +152,104 @@ class _Ordered:
         return False
 
 
+@dataclass
+class Partition:
+    """Element-block partition of the global mesh over px x py ranks (mg_partition).
+
+    nccl_id: the 128-byte id from nccl_unique_id() on rank 0 (NCCL, one process per
+    GPU); loopback: a LoopbackHub instead (virtual ranks in one process, tests)."""
+    rank: int
+    nranks: int
+    px: int
+    py: int
+    nccl_id: bytes | None = None
+    gather_ne: int = 0
+    loopback: "LoopbackHub | None" = None
+
+    def c(self):
+        self._id = None if self.nccl_id is None else C.create_string_buffer(bytes(self.nccl_id), 128)
+        return mg_partition(self.rank, self.nranks, self.px, self.py,
+                            None if self._id is None else C.cast(self._id, C.c_void_p),
+                            self.gather_ne, None if self.loopback is None else self.loopback.handle)
+
+    def block(self, nx: int, ny: int):
+        """(ox, oy, bx, by): this rank's element block of an nx x ny level."""
+        bx, by = nx // self.px, ny // self.py
+        return (self.rank % self.px) * bx, (self.rank // self.px) * by, bx, by
+
+
+class LoopbackHub:
+    """Communicator hub for `n` virtual ranks in this process on one GPU (tests)."""
+
+    def __init__(self, n: int):
+        self.lib = load_library()
+        self.handle = C.c_void_p(self.lib.mg_loopback_create(n))
+        self.n = n
+
+    def close(self):
+        if self.handle:
+            self.lib.mg_loopback_destroy(self.handle)
+            self.handle = None
+
+
+def nccl_unique_id() -> bytes:
+    lib = load_library()
+    buf = C.create_string_buffer(128)
+    rc = lib.mg_get_nccl_unique_id(C.cast(buf, C.c_void_p))
+    if rc != MG_OK:
+        raise MGError(f"mg_get_nccl_unique_id: {ERRORS.get(rc, rc)}")
+    return buf.raw
+
+
+def partition_plan(nx: int, ny: int, p: int, part: Partition, n_h_levels: int = 0):
+    """Host-only decomposition (no device work): dict(nlevels, gather_level, levels=[...]),
+    levels[k-1] = dict(nx, ny, ox, oy, gnx, gny, dmask, imask) of paper level k."""
+    lib = load_library()
+    mesh = mg_quad_mesh(nx, ny, 0.0, 0.0, 1.0 / nx)
+    info = np.zeros(8 * 64, dtype=np.int32)
+    nl, gl = C.c_int32(), C.c_int32()
+    pc = part.c()
+    rc = lib.mg_partition_plan(C.byref(mesh), p, n_h_levels, C.byref(pc), 64, C.byref(nl),
+                               C.byref(gl), C.c_void_p(info.ctypes.data))
+    if rc != MG_OK:
+        raise MGError(f"mg_partition_plan: {ERRORS.get(rc, rc)}")
+    keys = ("nx", "ny", "ox", "oy", "gnx", "gny", "dmask", "imask")
+    levels = [dict(zip(keys, info[8 * k:8 * k + 8].tolist())) for k in range(nl.value)]
+    return dict(nlevels=nl.value, gather_level=gl.value, levels=levels)
+
+
+def partition_side_edges(nx: int, ny: int, p: int, part: Partition, level: int, side: int,
+                         n_h_levels: int = 0) -> np.ndarray:
+    """Global edge ids of an interface side of a level's block, in halo-message order."""
+    lib = load_library()
+    mesh = mg_quad_mesh(nx, ny, 0.0, 0.0, 1.0 / nx)
+    pc = part.c()
+    cnt = C.c_int32()
+    rc = lib.mg_partition_side_edges(C.byref(mesh), p, n_h_levels, C.byref(pc), level, side, None,
+                                     C.byref(cnt))
+    if rc != MG_OK:
+        raise MGError(f"mg_partition_side_edges: {ERRORS.get(rc, rc)}")
+    out = np.zeros(cnt.value, dtype=np.int64)
+    if cnt.value:
+        lib.mg_partition_side_edges(C.byref(mesh), p, n_h_levels, C.byref(pc), level, side,
+                                    C.c_void_p(out.ctypes.data), C.byref(cnt))
+    return out
+
+
 class MGSolver:
-    """One context of the C ABI on a CUDA device (own stream unless given)."""
+    """One context of the C ABI on a CUDA device (own stream unless given).
+
+    partition: None (one GPU) or a Partition -- then nx, ny are the GLOBAL mesh and
+    every array argument is this rank's element block / its local edge numbering."""
 
     def __init__(self, nx: int, ny: int | None = None, p: int = 1, h: float | None = None,
-                 n_h_levels: int = 0, device="cuda", stream: torch.cuda.Stream | None = None):
+                 n_h_levels: int = 0, device="cuda", stream: torch.cuda.Stream | None = None,
+                 partition: Partition | None = None):
         if not torch.cuda.is_available():
             raise MGError("MGSolver needs a CUDA device (no CPU fallback)")
         self.lib = load_library()
         ny = nx if ny is None else ny
+        self.partition = partition
         self.device = torch.device(device)
         if self.device.index is None:
             self.device = torch.device("cuda", torch.cuda.current_device())
@@ -160,7 +259,9 @@ class MGSolver:
         self.nx, self.ny, self.p = nx, ny, p
         mesh = mg_quad_mesh(nx, ny, 0.0, 0.0, h if h is not None else 1.0 / nx)
         ctx = C.c_void_p()
-        rc = self.lib.mg_build_hierarchy(C.byref(mesh), p, n_h_levels, None,
+        self._pc = None if partition is None else partition.c()
+        rc = self.lib.mg_build_hierarchy(C.byref(mesh), p, n_h_levels,
+                                         None if self._pc is None else C.byref(self._pc),
                                          C.c_void_p(self.stream.cuda_stream), C.byref(ctx))
         if rc != MG_OK:
             raise MGError(f"mg_build_hierarchy failed: {ERRORS.get(rc, rc)}")

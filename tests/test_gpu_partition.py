@@ -1,0 +1,133 @@
+"""Partitioned (multi-GPU) path, on ONE GPU: N virtual ranks in
+this process (include/mgdtn.h `mg_partition.loopback`), each driven by its own
+host thread and stream, exchanging interface partial sums, all-reduced PCG
+scalars and the all-gathered coarse levels through the loopback communicator
+(device copies ordered by events; no kernel waits on another rank's kernel).
+The same library code path runs over NCCL with one process per GPU.
+
+Checked against the single-GPU context on the same global problem (which is
+itself parity-tested against the oracle):
+  apply on every level, V-cycle, assembled right-hand side: <= 1e-12 relative,
+  PCG: the same iteration count and lambda within 1e-10 relative,
+  every interface dof bitwise identical on the two ranks that hold it.
+"""
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+import torch
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    from paper_1811_09909_b200 import build
+    build.build()
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+# (config recipe, n, px, py, gather_ne): gather_ne small keeps several levels partitioned
+CASES = [(2, 32, 2, 1, 16), (2, 32, 2, 2, 0), (4, 32, 2, 2, 16), (3, 64, 1, 2, 64), (1, 16, 2, 2, 4)]
+
+
+def level_ids(plan, lev):
+    """global dof ids of a rank's local dofs on paper level `lev` (identity if replicated)."""
+    L = plan["levels"][lev - 1]
+    if L["imask"] == 0 and L["nx"] == L["gnx"] and L["ny"] == L["gny"]:
+        return None
+    return W.block_edge_ids_at(L["gnx"], L["ox"], L["oy"], L["nx"], L["ny"])
+
+
+def run_ranks(cfg, pr, px, py, gather_ne, x_glob, r_glob):
+    from paper_1811_09909_b200 import (LoopbackHub, MGSolver, Partition, partition_plan,
+                                       smoother_from_config)
+    n, p, N = cfg.n, cfg.p, px * py
+    hub = LoopbackHub(N)
+    dev = torch.device("cuda", 0)
+
+    def rank_main(rank):
+        torch.cuda.set_device(dev)
+        part = Partition(rank, N, px, py, gather_ne=gather_ne, loopback=hub)
+        plan = partition_plan(n, n, p, part)
+        s = MGSolver(n, p=p, partition=part)
+        assert s.nlevels == plan["nlevels"]
+        bp = W.block_problem(pr, px, py, rank)
+        s.setup(bp.K, bp.method, bp.tau, smoother_from_config(cfg))
+        g, lam_bc = s.assemble_rhs(bp.f_qp, bp.f_const, bp.gD_qp)
+        out = {"g": g.cpu().numpy(), "plan": plan}
+        for lev in range(s.nlevels, 0, -1):
+            k1 = s.level_info(lev)["p"] + 1
+            e = level_ids(plan, lev)
+            ids = np.arange(s.ndof(lev)) if e is None else W.dof_ids(e, k1 - 1)
+            out[("ids", lev)] = ids
+            out[("apply", lev)] = s.apply(lev, torch.from_numpy(x_glob[lev][ids])).cpu().numpy()
+        rl = r_glob[W.block_dof_ids(n, p, px, py, rank)]
+        out["vcycle"] = s.vcycle(torch.from_numpy(rl)).cpu().numpy()
+        lam, inf = s.pcg_solve(g, rtol=cfg.rtol, maxit=4000)
+        out["lam"] = lam.cpu().numpy()
+        out["info"] = inf
+        torch.cuda.synchronize()
+        return out
+
+    try:
+        with ThreadPoolExecutor(N) as ex:
+            res = list(ex.map(rank_main, range(N)))
+    finally:
+        hub.close()
+    return res
+
+
+@pytest.mark.parametrize("idx,n,px,py,gne", CASES, ids=[f"c{c[0]}n{c[1]}_{c[2]}x{c[3]}_g{c[4]}" for c in CASES])
+def test_partitioned_equals_single(idx, n, px, py, gne):
+    from paper_1811_09909_b200 import MGSolver, smoother_from_config
+    cfg = W.scaled_config(idx, n)
+    pr = W.make_problem(cfg)
+    # single-GPU reference run
+    s1 = MGSolver(n, p=cfg.p)
+    s1.setup(pr.K, pr.method, pr.tau, smoother_from_config(cfg))
+    g1, _ = s1.assemble_rhs(pr.f_qp, pr.f_const, pr.gD_qp)
+    x_glob = {lev: W.random_trace_vector(s1.ndof(lev), 5000 + lev) for lev in range(1, s1.nlevels + 1)}
+    ref = {lev: s1.apply(lev, torch.from_numpy(x_glob[lev])).cpu().numpy()
+           for lev in range(1, s1.nlevels + 1)}
+    r_glob = W.random_trace_vector(s1.ndof(), 6000)
+    z1 = s1.vcycle(torch.from_numpy(r_glob)).cpu().numpy()
+    lam1, info1 = s1.pcg_solve(g1, rtol=cfg.rtol, maxit=4000)
+    lam1 = lam1.cpu().numpy()
+    g1 = g1.cpu().numpy()
+    torch.cuda.synchronize()
+
+    res = run_ranks(cfg, pr, px, py, gne, x_glob, r_glob)
+    N = px * py
+    for rank, out in enumerate(res):
+        assert out["plan"]["gather_level"] >= 1
+        ids = W.block_dof_ids(n, cfg.p, px, py, rank)
+        assert rel(out["g"], g1[ids]) <= TOL, ("rhs", rank, rel(out["g"], g1[ids]))
+        for lev in range(1, s1.nlevels + 1):
+            gid = out[("ids", lev)]
+            loc = out[("apply", lev)]
+            assert rel(loc, ref[lev][gid]) <= TOL, ("apply", lev, rank, rel(loc, ref[lev][gid]))
+        assert rel(out["vcycle"], z1[ids]) <= TOL, ("vcycle", rank, rel(out["vcycle"], z1[ids]))
+        assert out["info"]["status"] == "converged"
+        assert out["info"]["iters"] == info1["iters"], (out["info"], info1)
+        assert rel(out["lam"], lam1[ids]) <= 1e-10, ("lambda", rank, rel(out["lam"], lam1[ids]))
+    # duplicated interface dofs: bitwise identical on the ranks that hold them
+    for key in ("lam", "vcycle", "g"):
+        seen = {}
+        for rank, out in enumerate(res):
+            ids = W.block_dof_ids(n, cfg.p, px, py, rank)
+            for gid, val in zip(ids.tolist(), out[key].tolist()):
+                if gid in seen:
+                    assert seen[gid] == val, (key, gid, seen[gid], val)
+                else:
+                    seen[gid] = val
+    assert N > 1

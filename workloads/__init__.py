@@ -246,3 +246,64 @@ def random_trace_vector(ndof: int, seed: int) -> np.ndarray:
 
 def trace_ndof(n: int, p: int) -> int:
     return 2 * n * (n + 1) * (p + 1)
+
+
+# ---------------------------------------------------------------- element-block partitions
+# (multi-GPU layout of include/mgdtn.h `mg_partition`: rank r = ry*px + rx holds the
+# global elements [rx*bx, (rx+1)*bx) x [ry*by, (ry+1)*by), bx = n/px, by = n/py, in
+# local element order jl*bx + il, and the edges of those elements in the local
+# numbering of a bx x by mesh.)
+
+def block_of(n: int, px: int, py: int, rank: int):
+    """(ox, oy, bx, by) of a rank's element block of an n x n mesh."""
+    bx, by = n // px, n // py
+    return (rank % px) * bx, (rank // px) * by, bx, by
+
+
+def block_edge_ids(n: int, px: int, py: int, rank: int) -> np.ndarray:
+    """Global edge id of every local edge of a rank's block (local edge order)."""
+    return block_edge_ids_at(n, *block_of(n, px, py, rank))
+
+
+def block_edge_ids_at(n: int, ox: int, oy: int, bx: int, by: int) -> np.ndarray:
+    """Global edge ids (n x n mesh) of the local edges of the block at (ox, oy), bx x by."""
+    jh, ih = np.divmod(np.arange(bx * (by + 1)), bx)
+    hid = (oy + jh) * n + (ox + ih)
+    jv, iv = np.divmod(np.arange((bx + 1) * by), bx + 1)
+    vid = n * (n + 1) + (oy + jv) * (n + 1) + (ox + iv)
+    return np.concatenate([hid, vid]).astype(np.int64)
+
+
+def block_dof_ids(n: int, p: int, px: int, py: int, rank: int) -> np.ndarray:
+    """Global trace-dof id of every local dof of a rank's block."""
+    return dof_ids(block_edge_ids(n, px, py, rank), p)
+
+
+def dof_ids(edges: np.ndarray, p: int) -> np.ndarray:
+    k1 = p + 1
+    return (edges[:, None] * k1 + np.arange(k1)[None, :]).reshape(-1)
+
+
+def block_problem(pr: Problem, px: int, py: int, rank: int) -> Problem:
+    """A rank's share of a problem: its elements' K / method / tau / f samples and
+    the g_D samples of its block's 2*bx + 2*by boundary edges (sides that are
+    partition interfaces get zeros; the library ignores them)."""
+    n = pr.cfg.n
+    ox, oy, bx, by = block_of(n, px, py, rank)
+    jj, ii = np.divmod(np.arange(bx * by), bx)
+    ge = (oy + jj) * n + (ox + ii)
+    f = None if pr.f_qp is None else np.ascontiguousarray(pr.f_qp[ge])
+    gD = None
+    if pr.gD_qp is not None:
+        nq = pr.gD_qp.shape[1]
+        gD = np.zeros((2 * bx + 2 * by, nq))
+        if oy == 0:
+            gD[:bx] = pr.gD_qp[ox:ox + bx]                                    # bottom
+        if oy + by == n:
+            gD[bx:2 * bx] = pr.gD_qp[n + ox:n + ox + bx]                      # top
+        if ox == 0:
+            gD[2 * bx:2 * bx + by] = pr.gD_qp[2 * n + oy:2 * n + oy + by]     # left
+        if ox + bx == n:
+            gD[2 * bx + by:] = pr.gD_qp[3 * n + oy:3 * n + oy + by]           # right
+    return Problem(pr.cfg, np.ascontiguousarray(pr.K[ge]), np.ascontiguousarray(pr.method[ge]),
+                   np.ascontiguousarray(pr.tau[ge]), f, pr.f_const, gD, pr.exact)
