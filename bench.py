@@ -165,27 +165,42 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, help="BASELINE.json config index (1-5)")
+    ap.add_argument("--config", type=int, default=0,
+                    help="BASELINE.json config index (1-5); default: 2 on one GPU (the headline "
+                         "config), 5 (the north star's scaling run, strong scaling) on N > 1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true")
     args = ap.parse_args()
+    _, world0, _ = _dist_env()
+    if args.config == 0:
+        args.config = 2 if world0 == 1 else 5
     cfg = W.CONFIGS[args.config]
     if args.impl == "reference":
         return reference_arm(args, cfg)
 
     import torch
     import torch.distributed as dist
-    from paper_1811_09909_b200 import MGSolver, smoother_from_config
+    from paper_1811_09909_b200 import MGSolver, Partition, nccl_unique_id, smoother_from_config
 
     rank, world, local = _dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    part = None
     if world > 1:
+        # one global problem sharded in element blocks over px x py ranks:
+        # NCCL halo sums of interface edges, all-reduced PCG scalars, gathered coarse levels
         dist.init_process_group("nccl", device_id=dev)
+        px = {2: 2, 4: 2, 8: 4, 16: 4}.get(world, world)
+        py = world // px
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        part = Partition(rank, world, px, py, nccl_id=obj[0])
 
-    # ---- inputs resident in HBM (weak scaling: every rank solves its own problem)
+    # ---- inputs resident in HBM (N > 1: this rank's element block of the one problem)
     pr = W.make_problem(cfg)
+    if part is not None:
+        pr = W.block_problem(pr, part.px, part.py, rank)
     K = torch.from_numpy(pr.K).to(dev)
     meth = torch.from_numpy(pr.method).to(dev)
     tau = torch.from_numpy(pr.tau).to(dev)
@@ -193,7 +208,7 @@ def main():
     gD = None if pr.gD_qp is None else torch.from_numpy(pr.gD_qp).to(dev)
     stream = torch.cuda.Stream(dev)
     with torch.cuda.stream(stream):
-        s = MGSolver(cfg.n, p=cfg.p, device=dev, stream=stream)
+        s = MGSolver(cfg.n, p=cfg.p, device=dev, stream=stream, partition=part)
     if args.no_graphs:
         s.use_graphs(False)
     sm = smoother_from_config(cfg)
@@ -234,7 +249,8 @@ def main():
             dist.barrier()
     ms_per_step = t_ms / args.steps
     info = st["info"]
-    value = world * cfg.trace_dofs / (ms_per_step * 1e-3)
+    # one global problem on all ranks (strong scaling) when partitioned
+    value = cfg.trace_dofs / (ms_per_step * 1e-3)
 
     # ---- phase breakdown + dominant-kernel roofline (fine-level apply, 2 colour passes)
     with torch.cuda.stream(stream):
@@ -256,7 +272,7 @@ def main():
         y = torch.empty_like(x)
         N = s.nlevels
         t_apply = timed(lambda: s.apply(N, x, y), 10)
-    ne = cfg.n * cfg.n
+    ne = cfg.n * cfg.n // world      # this rank's elements
     m = 4 * (cfg.p + 1)
     npk = m * (m + 1) // 2
     ndof = s.ndof()
@@ -269,9 +285,10 @@ def main():
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(cfg.name)
 
-    # ---- end to end through the C ABI with HOST buffers (h2d inputs, d2h solution)
+    # ---- end to end through the C ABI with HOST buffers (h2d inputs, d2h solution);
+    # collective on a partition (every rank solves its block), rank 0 reports
     e2e = None
-    if rank == 0:
+    if True:
         Kh = torch.from_numpy(pr.K).pin_memory()
         mh = torch.from_numpy(pr.method).pin_memory()
         th = torch.from_numpy(pr.tau).pin_memory()
@@ -284,9 +301,15 @@ def main():
             for _ in range(max(1, min(args.steps, 3))):
                 flush.fill_(2.0)
                 torch.cuda.synchronize(dev)
+                if world > 1:
+                    dist.barrier()
                 t0 = time.perf_counter()
                 s.solve_host(Kh, mh, th, fh, pr.f_const, gh, sm, cfg.rtol, 4000, out=out.numpy())
                 te.append(time.perf_counter() - t0)
+            if world > 1:   # the slowest rank's wall time
+                tt = torch.tensor([float(np.mean(te))], dtype=torch.float64, device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                te = [float(tt.item())]
         h2d = 8 * ne * 2 + ne + (0 if fh is None else 8 * fh.numel()) + (0 if gh is None else 8 * gh.numel())
         e2e = {"value": cfg.trace_dofs / float(np.mean(te)), "unit": "trace DoF/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * ndof)}
@@ -304,11 +327,13 @@ def main():
         line = {
             "metric": "fine trace DoFs/s in MG-PCG solve to 1e-10", "value": value, "unit": "trace DoF/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": cfg.name, "n": cfg.n, "p": cfg.p, "trace_dofs": cfg.trace_dofs,
                        "smoother": "chebyshev" if cfg.smoother else "block-jacobi", "nu": cfg.nu,
-                       "rtol": cfg.rtol, "parallelism": f"replicas{world}" if world > 1 else "1gpu",
+                       "rtol": cfg.rtol,
+                       "parallelism": f"elem-blocks{part.px}x{part.py}" if part else "1gpu",
                        "l2": "256 MiB flush between steps (outside the per-step event window)",
                        "step": "setup_dtn + assemble_rhs + pcg_solve"},
             "iters": info["iters"], "solve_status": info["status"], "relres": info["relres"],
