@@ -1,6 +1,8 @@
 // Setup kernels: batched element-local static condensation (H1), the
 // right-hand side, p-coarsening (H2), per-agglomerate Galerkin coarse DtN
 // (H3), edge-block diagonals (H4) and the coarsest dense factor (H5).
+#include <cstdlib>
+
 #include "bodies.cuh"
 
 namespace mgdtn {
@@ -42,12 +44,13 @@ __global__ void __launch_bounds__(32 * (2 * (P + 1))) k_local_dtn(LevelDev L, Re
                                                               const double* __restrict__ K,
                                                               const int8_t* __restrict__ method,
                                                               const double* __restrict__ tau,
-                                                              DevError* err) {
+                                                              DevError* err, int project) {
   using Sh = LocalShape<P>;
   constexpr int NV = Sh::NV, M = Sh::M, NPK = Sh::NPK, NW = M / 2;
   __shared__ double sAt[2][NV * M], sBk[2][NV * M];
   __shared__ double sW[M * M], sH[M * M];
   __shared__ double sc[NV][32];   // 1 / d_i per lane-element
+  __shared__ double srow[M][32];  // row sums S_T 1 per lane-element (projection)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int q = threadIdx.x; q < NV * M; q += blockDim.x) {
     sAt[0][q] = R.pAt[0][q];
@@ -113,6 +116,42 @@ __global__ void __launch_bounds__(32 * (2 * (P + 1))) k_local_dtn(LevelDev L, Re
           if (b >= a) dst[(int64_t)(base + b) * 32] = acc[b];
       }
     }
+    if (project) {
+      // S_T 1 = 0 exactly for the DtN map (constant traces: u = 0, q = lambda = c solve
+      // the local problem with zero flux).  The elimination
+      // leaves a rounding-level constant-mode error (amplified by the coarse Schur
+      // complements, R5); replace S by its nearest symmetric matrix with
+      // S 1 = 0, P S P with P = I - 1 1^T / m.
+      __syncthreads();   // every row of the chunk stored
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int a = half == 0 ? w : M - 1 - w;
+        double rs = 0.0;
+#pragma unroll
+        for (int b = 0; b < M; ++b) {
+          const int lo = a < b ? a : b, hi = a < b ? b : a;
+          rs += act ? dst[(int64_t)(lo * (2 * M - lo + 1) / 2 + (hi - lo)) * 32] : 0.0;
+        }
+        srow[a][lane] = rs;
+      }
+      __syncthreads();
+      double sig = 0.0;
+#pragma unroll
+      for (int b = 0; b < M; ++b) sig += srow[b][lane];
+      const double inv_m = 1.0 / M, c0 = sig * inv_m * inv_m;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int a = half == 0 ? w : M - 1 - w;
+        if (!act) continue;
+        const int base = a * (2 * M - a + 1) / 2 - a;
+#pragma unroll
+        for (int b = 0; b < M; ++b)
+          if (b >= a) {
+            double* q = dst + (int64_t)(base + b) * 32;
+            *q = (*q - (srow[a][lane] + srow[b][lane]) * inv_m) + c0;
+          }
+      }
+    }
   }
 }
 
@@ -120,11 +159,16 @@ int launch_local_dtn(const LevelDev& L, const RefDev& R, double h, const double*
                      const int8_t* method, const double* tau, DevError* err, cudaStream_t st) {
   const int64_t nct = 2 * (int64_t)L.nchunk;
   const int grid = (int)(nct < 148 * 8 ? nct : 148 * 8);
+  static int project = -1;   // MGDTN_DTN_PROJECT=0: no constant-mode projection (A/B)
+  if (project < 0) {
+    const char* e = std::getenv("MGDTN_DTN_PROJECT");
+    project = (e && std::atoi(e) == 0) ? 0 : 1;
+  }
   switch (L.p) {
-    case 1: k_local_dtn<1><<<grid, 32 * 4, 0, st>>>(L, R, h, K, method, tau, err); break;
-    case 2: k_local_dtn<2><<<grid, 32 * 6, 0, st>>>(L, R, h, K, method, tau, err); break;
-    case 3: k_local_dtn<3><<<grid, 32 * 8, 0, st>>>(L, R, h, K, method, tau, err); break;
-    default: k_local_dtn<4><<<grid, 32 * 10, 0, st>>>(L, R, h, K, method, tau, err); break;
+    case 1: k_local_dtn<1><<<grid, 32 * 4, 0, st>>>(L, R, h, K, method, tau, err, project); break;
+    case 2: k_local_dtn<2><<<grid, 32 * 6, 0, st>>>(L, R, h, K, method, tau, err, project); break;
+    case 3: k_local_dtn<3><<<grid, 32 * 8, 0, st>>>(L, R, h, K, method, tau, err, project); break;
+    default: k_local_dtn<4><<<grid, 32 * 10, 0, st>>>(L, R, h, K, method, tau, err, project); break;
   }
   return 1;
 }
