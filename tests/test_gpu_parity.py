@@ -63,7 +63,7 @@ class Case:
         return self.olev(level).free
 
 
-CASES = [(1, 8), (2, 16), (3, 16), (4, 16), (5, 16)]
+CASES = [(1, 8), (2, 16), (3, 16), (4, 16), (5, 16), (2, 64), (3, 64), (4, 64)]
 
 
 @pytest.fixture(scope="module", params=CASES, ids=[f"c{a}n{b}" for a, b in CASES])
