@@ -225,6 +225,18 @@ int mg_solve_host(void* ctx, const double* K_host, const int8_t* method_host,
 int mg_staging_bytes(const void* ctx, int32_t with_f, int32_t with_gD, size_t* bytes);
 int mg_bind_staging(void* ctx, void* dev_ptr, size_t bytes);
 
+/* Volume recovery (element by element):
+ * q_T from the element's full trace (free solution + Dirichlet values,
+ * lambda + lambda_bc of mg_assemble_rhs) and the same f as mg_assemble_rhs:
+ *   q_T = Q^-1 (R lambda_T + f_w)  (the local solve of Eqs. HDG / SIPG_H).
+ * lambda_full: device [ndof_N]; q_out: device [ne][(p+1)^2], GLL nodal coefficients
+ * of Q^p (node b*(p+1)+a, a along x), element-id order.  If q_exact_qp (device
+ * [ne][nq][nq], nq = p+4, the f_qp sampling grid) is given and l2_err (host) is
+ * not NULL, *l2_err = ||q_T - q_exact||_{L2(Omega)} by that quadrature (all ranks'
+ * elements on a partition).  Synchronises when l2_err is requested. */
+int mg_recover_volume(void* ctx, const double* lambda_full, const double* f_qp, double f_const,
+                      double* q_out, const double* q_exact_qp, double* l2_err);
+
 /* Introspection. */
 int mg_num_levels(const void* ctx, int32_t* nlevels);
 int mg_level_info(const void* ctx, int32_t level, int32_t* nx, int32_t* ny, int32_t* p,

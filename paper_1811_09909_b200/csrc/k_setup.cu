@@ -269,6 +269,97 @@ int launch_local_rhs(const LevelDev& L, const RefDev& R, double h, const double*
   return 2;
 }
 
+// ============================================================================
+// volume recovery ("the local volume unknowns
+// can be recovered in an element-by-element fashion completely independent of
+// each other").  With the local pencil (refelem.h), Q = T^-1 diag(d) T^-T and
+//   q_T = Q^-1 (R lambda_T + f_w) = T^T diag(1/d) (W lambda_T + f'),
+// W = t At + K Bk (rows w_i), f'_i = h^2 sum_q fqT[q,i] f_q, d_i = K lam_i + t mu_i
+// (the same factors the element DtN and the right-hand side use).  q_T: GLL nodal
+// coefficients [(p+1)^2] in element-id order.  With q_exact samples at the
+// (p+4)^2 Gauss points: per-block partial sums of h^2 sum_q w_q (q_T(x_q) - q_ex)^2.
+// ============================================================================
+template <int P>
+__global__ void __launch_bounds__(128) k_recover(LevelDev L, RefDev R, double h,
+                                                 const double* __restrict__ K,
+                                                 const int8_t* __restrict__ method,
+                                                 const double* __restrict__ tau,
+                                                 const double* __restrict__ lam,
+                                                 const double* __restrict__ f_qp, double f_const,
+                                                 double* q_out, const double* __restrict__ qex,
+                                                 double* partials) {
+  using Sh = LocalShape<P>;
+  constexpr int NV = Sh::NV, M = Sh::M, K1 = Sh::K1;
+  const int nq2 = R.nqf * R.nqf;
+  double err = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < L.ne;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e / L.nx), i = (int)(e - (int64_t)j * L.nx);
+    const double Kc = K[e], t = tau[e] * h;
+    const int meth = method[e] == 1 ? 1 : 0;
+    int64_t ed[4];
+    bool bd[4];
+    elem_edges(L.nx, L.ny, i, j, ed, bd, L.dmask);
+    double lt[M];
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+#pragma unroll
+      for (int a = 0; a < K1; ++a) lt[f * K1 + a] = lam[ed[f] * K1 + a];
+    double c[NV];
+    for (int v = 0; v < NV; ++v) {
+      double acc = 0.0;
+      for (int q = 0; q < nq2; ++q)
+        acc = fma(R.pfq[meth][q * NV + v], f_qp ? f_qp[e * nq2 + q] : f_const, acc);
+      acc *= h * h;
+#pragma unroll
+      for (int a = 0; a < M; ++a)
+        acc = fma(fma(t, R.pAt[meth][v * M + a], Kc * R.pBk[meth][v * M + a]), lt[a], acc);
+      c[v] = acc / fma(Kc, R.plam[meth][v], t * R.pmu[meth][v]);
+    }
+    double qv[NV];
+    for (int k = 0; k < NV; ++k) {
+      double acc = 0.0;
+      for (int v = 0; v < NV; ++v) acc = fma(R.pTt[meth][k * NV + v], c[v], acc);
+      qv[k] = acc;
+      q_out[e * NV + k] = acc;
+    }
+    if (qex) {
+      double s = 0.0;
+      for (int q = 0; q < nq2; ++q) {
+        double val = 0.0;
+        for (int k = 0; k < NV; ++k) val = fma(R.vq[q * NV + k], qv[k], val);
+        const double d = val - qex[e * nq2 + q];
+        s = fma(R.wq[q] * d, d, s);
+      }
+      err = fma(h * h, s, err);
+    }
+  }
+  if (qex) {
+    __shared__ double red[4];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) err += __shfl_xor_sync(0xffffffffu, err, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = err;
+    __syncthreads();
+    if (threadIdx.x == 0) partials[blockIdx.x] = (red[0] + red[1]) + (red[2] + red[3]);
+  }
+}
+
+int launch_recover(const LevelDev& L, const RefDev& R, double h, const double* K,
+                   const int8_t* method, const double* tau, const double* lam,
+                   const double* f_qp, double f_const, double* q_out, const double* qex_qp,
+                   double* partials, int* grid_out, cudaStream_t st) {
+  int64_t g = (L.ne + 127) / 128;
+  const int grid = (int)(g < 148 * 8 ? (g > 0 ? g : 1) : 148 * 8);
+  if (grid_out) *grid_out = grid;
+  switch (L.p) {
+    case 1: k_recover<1><<<grid, 128, 0, st>>>(L, R, h, K, method, tau, lam, f_qp, f_const, q_out, qex_qp, partials); break;
+    case 2: k_recover<2><<<grid, 128, 0, st>>>(L, R, h, K, method, tau, lam, f_qp, f_const, q_out, qex_qp, partials); break;
+    case 3: k_recover<3><<<grid, 128, 0, st>>>(L, R, h, K, method, tau, lam, f_qp, f_const, q_out, qex_qp, partials); break;
+    default: k_recover<4><<<grid, 128, 0, st>>>(L, R, h, K, method, tau, lam, f_qp, f_const, q_out, qex_qp, partials); break;
+  }
+  return 1;
+}
+
 // Dirichlet values: per-edge L2 projection of g_D onto P^p (reading Q4).
 __global__ void k_dirichlet(LevelDev L, RefDev R, const double* __restrict__ gD, double* lamD) {
   const int nb = 2 * L.nx + 2 * L.ny;

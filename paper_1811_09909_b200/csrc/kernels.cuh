@@ -198,6 +198,7 @@ struct RefDev {
   const double *G, *F, *P, *E, *W, *H, *LN, *Nl, *fq, *ew, *H1inv, *Jp;
   // pencil tables per method (refelem.h RefTables::Pencil): [0] HDG, [1] SIPG-H
   const double *plam[2], *pmu[2], *pAt[2], *pBk[2], *pfq[2];
+  const double *pTt[2], *vq, *wq;   // volume recovery (refelem.h)
 };
 
 // ---------------------------------------------------------------- programmatic dependent launch
@@ -258,6 +259,12 @@ int launch_local_rhs(const LevelDev& L, const RefDev& R, double h, const double*
                      cudaStream_t st);
 int launch_dirichlet(const LevelDev& L, const RefDev& R, const double* gD_qp, double* lamD,
                      cudaStream_t st);
+// volume recovery q_T from the full trace and, if qex_qp, the
+// per-block partial sums of ||q - q_exact||^2 over the elements (partials[grid])
+int launch_recover(const LevelDev& L, const RefDev& R, double h, const double* K,
+                   const int8_t* method, const double* tau, const double* lam,
+                   const double* f_qp, double f_const, double* q_out, const double* qex_qp,
+                   double* partials, int* grid_out, cudaStream_t st);
 int launch_p_coarsen(const LevelDev& F, const LevelDev& C, const double* Jp, cudaStream_t st);
 int launch_agglomerate(const LevelDev& F, const LevelDev& C, double* KIIinv, double* Pm,
                        DevError* err, cudaStream_t st);

@@ -309,7 +309,10 @@ static void bind_pointers(Ctx* c) {
     rd.pAt[k] = put(T.pen[k].At);
     rd.pBk[k] = put(T.pen[k].Bk);
     rd.pfq[k] = put(T.pen[k].fqT);
+    rd.pTt[k] = put(T.pen[k].Tt);
   }
+  rd.vq = put(T.vq);
+  rd.wq = put(T.wq);
 }
 
 // Levels from tail_start down run as ONE launch of k_coarse_tail (k_coarse.cu):
@@ -399,8 +402,11 @@ static int upload_static(Ctx* c) {
                         &T.Jp})
     all.insert(all.end(), v->begin(), v->end());
   for (int k = 0; k < 2; ++k)
-    for (const auto* v : {&T.pen[k].lam, &T.pen[k].mu, &T.pen[k].At, &T.pen[k].Bk, &T.pen[k].fqT})
+    for (const auto* v : {&T.pen[k].lam, &T.pen[k].mu, &T.pen[k].At, &T.pen[k].Bk, &T.pen[k].fqT,
+                          &T.pen[k].Tt})
       all.insert(all.end(), v->begin(), v->end());
+  all.insert(all.end(), T.vq.begin(), T.vq.end());
+  all.insert(all.end(), T.wq.begin(), T.wq.end());
   CK(cudaMemcpyAsync(c->ws + c->o_ref, all.data(), all.size() * sizeof(double),
                      cudaMemcpyHostToDevice, c->st));
   // coarsest free-dof maps
@@ -1051,7 +1057,8 @@ int mg_build_hierarchy(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
                    T.Jp.size();
   for (int k = 0; k < 2; ++k)
     c->ref_doubles += T.pen[k].lam.size() + T.pen[k].mu.size() + T.pen[k].At.size() +
-                      T.pen[k].Bk.size() + T.pen[k].fqT.size();
+                      T.pen[k].Bk.size() + T.pen[k].fqT.size() + T.pen[k].Tt.size();
+  c->ref_doubles += T.vq.size() + T.wq.size();
   int rc = build_levels(c, mesh, p, n_h_levels, part);
   if (rc != MG_OK) {
     delete c;
@@ -1349,6 +1356,25 @@ int mg_solve_host(void* ctx, const double* K_host, const int8_t* method_host,
   if (relres) *relres = rel;
   if (solve_status) *solve_status = stt;
   return MG_OK;
+}
+
+int mg_recover_volume(void* ctx, const double* lambda_full, const double* f_qp, double f_const,
+                      double* q_out, const double* q_exact_qp, double* l2_err) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !lambda_full || !q_out) return MG_ERR_ARG;
+  if (!c->setup_done) return fail(c, MG_ERR_STATE, "mg_setup_dtn must precede mg_recover_volume");
+  HostLevel& F = c->lev[0];
+  int grid = 0;
+  c->launches += launch_recover(F.d, c->refdev, F.h, c->Kc, c->methc, c->tauc, lambda_full, f_qp,
+                                f_const, q_out, q_exact_qp, c->part, &grid, c->st);
+  if (q_exact_qp && l2_err) {
+    reduce_scal(c, c->part, grid, c->sscal, 6, 0);   // sum over elements (and ranks)
+    CK(cudaMemcpyAsync(c->pinned, c->sscal + 6, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    *l2_err = std::sqrt(c->pinned[0]);
+  }
+  CK(cudaGetLastError());
+  return c->comm_rc ? c->comm_rc : MG_OK;
 }
 
 int mg_num_levels(const void* ctx, int32_t* nlevels) {

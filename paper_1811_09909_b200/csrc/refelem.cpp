@@ -248,6 +248,9 @@ static RefTables::Pencil make_pencil(const std::vector<double>& A, const std::ve
       P.At[i * m + a] = s1;
       P.Bk[i * m + a] = s2;
     }
+  P.Tt.assign(nv * nv, 0.0);
+  for (int i = 0; i < nv; ++i)
+    for (int k = 0; k < nv; ++k) P.Tt[k * nv + i] = T[i * nv + k];
   P.fqT.assign(nqf2 * nv, 0.0);
   for (int q = 0; q < nqf2; ++q)
     for (int i = 0; i < nv; ++i) {
@@ -378,6 +381,15 @@ RefTables build_ref_tables(int p) {
         for (int a = 0; a < k1; ++a)
           T.fq[(qy * T.nqf + qx) * nv + b * k1 + a] =
               wf[qy] * wf[qx] * lag(nd, a, xf[qx]) * lag(nd, b, xf[qy]);
+  T.vq.assign(T.nqf * T.nqf * nv, 0.0);
+  T.wq.assign(T.nqf * T.nqf, 0.0);
+  for (int qy = 0; qy < T.nqf; ++qy)
+    for (int qx = 0; qx < T.nqf; ++qx) {
+      T.wq[qy * T.nqf + qx] = wf[qy] * wf[qx];
+      for (int b = 0; b < k1; ++b)
+        for (int a = 0; a < k1; ++a)
+          T.vq[(qy * T.nqf + qx) * nv + b * k1 + a] = lag(nd, a, xf[qx]) * lag(nd, b, xf[qy]);
+    }
   T.ew.assign(T.nqf * k1, 0.0);
   for (int q = 0; q < T.nqf; ++q)
     for (int a = 0; a < k1; ++a) T.ew[q * k1 + a] = wf[q] * lag(nd, a, xf[q]);

@@ -27,6 +27,8 @@ struct RefTables {
   //   fw_i = h^2 * sum_{qy,qx} fq[qy,qx,i] * f(qy,qx)
   int nqf = 0;
   std::vector<double> fq;             // [nqf*nqf*nv] (weights folded in)
+  std::vector<double> vq;             // [nqf*nqf*nv] basis values at those points (no weights)
+  std::vector<double> wq;             // [nqf*nqf] tensor Gauss weights on the unit square
   // boundary-data projection: lambda = H1inv * (sum_q ew[q,a] g_q)
   std::vector<double> ew;             // [nqf*k1] (weights folded in)
   std::vector<double> H1inv;          // [k1*k1]
@@ -45,6 +47,7 @@ struct RefTables {
     std::vector<double> lam, mu;      // [nv]
     std::vector<double> At, Bk;       // [nv*m]
     std::vector<double> fqT;          // [nqf*nqf*nv]
+    std::vector<double> Tt;           // [nv*nv] T^T (volume recovery: q = T^T diag(1/d) (w lam + f'))
   };
   Pencil pen[2];                      // [0] HDG, [1] SIPG-H
 };

@@ -63,6 +63,7 @@ _SIGS = {
                       C.c_int32, _P, C.POINTER(C.c_int32), C.POINTER(C.c_double), C.POINTER(C.c_int32)],
     "mg_staging_bytes": [_P, C.c_int32, C.c_int32, C.POINTER(C.c_size_t)],
     "mg_bind_staging": [_P, _P, C.c_size_t],
+    "mg_recover_volume": [_P, _P, _P, C.c_double, _P, _P, C.POINTER(C.c_double)],
     "mg_num_levels": [_P, C.POINTER(C.c_int32)],
     "mg_level_info": [_P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                       C.POINTER(C.c_int32), C.POINTER(C.c_int64)],
@@ -418,6 +419,20 @@ class MGSolver:
                                          hp(gD_qp), C.byref(cfg), rtol, maxit, hp(out), C.byref(it),
                                          C.byref(rel), C.byref(st))
         return out, dict(iters=it.value, relres=rel.value, status=STATUS[st.value])
+
+    def recover_volume(self, lam_full, f_qp=None, f_const=0.0, q_exact_qp=None):
+        """q_T per element (GLL nodal [ne][(p+1)^2]) from the full trace; with q_exact
+        samples also the L2 error (mg_recover_volume)."""
+        lam_full = self._d(lam_full)
+        f = self._d(f_qp)
+        qe = self._d(q_exact_qp)
+        info = self.level_info(self.nlevels)
+        q = torch.empty((info["nx"] * info["ny"], (self.p + 1) ** 2), dtype=torch.float64,
+                        device=self.device)
+        err = C.c_double(float("nan"))
+        self._call("mg_recover_volume", _ptr(lam_full), _ptr(f), float(f_const), _ptr(q),
+                   _ptr(qe), C.byref(err) if qe is not None else None)
+        return q, (err.value if qe is not None else None)
 
     def element_dtn(self, level: int):
         info = self.level_info(level)
