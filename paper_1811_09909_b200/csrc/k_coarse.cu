@@ -159,25 +159,35 @@ __global__ void __launch_bounds__(TAIL_TPB, 1) k_tail_basis(const __grid_constan
   k_coarse_tail_t<true>(G, tfidx, nfb, Bt);
 }
 
-// e = B_tail r on the free dofs of the top tail level: one warp per row, lanes
-// stride the row (coalesced), fixed shuffle tree (deterministic)
-__global__ void __launch_bounds__(256) k_tail_dense(const int* __restrict__ tfidx, int nf,
-                                                    const double* __restrict__ Bt,
-                                                    const double* __restrict__ r, double* e) {
+// e = B_tail r on the free dofs of the top tail level: one CTA per row, each
+// thread a strided slice of the row (coalesced, one memory round trip), fixed
+// warp-shuffle + shared-memory tree (deterministic)
+constexpr int TD_THREADS = 256;
+__global__ void __launch_bounds__(TD_THREADS) k_tail_dense(const int* __restrict__ tfidx, int nf,
+                                                           const double* __restrict__ Bt,
+                                                           const double* __restrict__ r,
+                                                           double* e) {
+  __shared__ double red[TD_THREADS / 32];
   pdl_enter();
-  const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
-  if (warp >= nf) return;
-  const double* row = Bt + (int64_t)warp * nf;
+  const int row = blockIdx.x;
+  const double* b = Bt + (int64_t)row * nf;
   double acc = 0.0;
-  for (int j = lane; j < nf; j += 32) acc = fma(row[j], r[tfidx[j]], acc);
+  for (int j = threadIdx.x; j < nf; j += TD_THREADS) acc = fma(__ldg(b + j), __ldg(r + tfidx[j]), acc);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) e[tfidx[warp]] = acc;
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < TD_THREADS / 32; ++w) s += red[w];
+    e[tfidx[row]] = s;
+  }
 }
 
 int launch_tail_dense(const int* tfidx, int nf, const double* Bt, const double* r, double* e,
                       cudaStream_t st) {
-  launch_ex(k_tail_dense, (nf + 7) / 8, 256, 0, true, st, tfidx, nf, Bt, r, e);
+  launch_ex(k_tail_dense, nf, TD_THREADS, 0, true, st, tfidx, nf, Bt, r, e);
   return 1;
 }
 

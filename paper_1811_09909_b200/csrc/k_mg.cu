@@ -34,8 +34,58 @@ __global__ void k_smooth_first(LevelDev L, const double* __restrict__ r, double*
   smooth_first_body(L, r, e, d, GTID, GNT);
 }
 
+// the same step as a pass over the colour-1 elements (every free edge has exactly
+// one): D_e^-1 from the packed, chunk-interleaved Dc (coalesced, 40% fewer bytes
+// than the SoA blocks at p=4).  Single-GPU levels only (a partition-interface edge
+// may have no local colour-1 element).
+template <int K1>
+__global__ void k_smooth_first_dc(LevelDev L, const double* __restrict__ r, double* e, double* d) {
+  pdl_enter();
+  constexpr int NDE = K1 * (K1 + 1) / 2;
+  const double c2 = L.coef[1];
+  const unsigned nec = (unsigned)(L.ne >> 1);
+  // work item = (edge f of the colour-1 element at slot s), f-major: a warp covers 32
+  // consecutive slots of one local edge, so every Dc row load is 256 contiguous bytes
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < 4 * (int64_t)nec;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int f = (int)((unsigned)w / nec);
+    const int64_t s = (int64_t)((unsigned)w - (unsigned)f * nec);
+    int i, j;
+    slot_elem(L.nx, 1, s, i, j);
+    int64_t ed[4];
+    bool bd[4];
+    elem_edges(L.nx, L.ny, i, j, ed, bd, L.dmask);
+    if (bd[f]) continue;
+    const double* Dp = L.Dc + ((s >> 5) * L.ndi + f * NDE) * 32 + (s & 31);
+    double rv[K1];
+#pragma unroll
+    for (int a = 0; a < K1; ++a) rv[a] = __ldg(r + ed[f] * K1 + a);
+#pragma unroll
+    for (int a = 0; a < K1; ++a) {
+      double c = 0.0;
+#pragma unroll
+      for (int b = 0; b < K1; ++b) {
+        const int lo = a < b ? a : b, hi = a < b ? b : a;
+        c = fma(__ldg(Dp + (int64_t)(lo * (2 * K1 - lo + 1) / 2 + (hi - lo)) * 32), rv[b], c);
+      }
+      const double v = c2 * c;
+      e[ed[f] * K1 + a] = v;
+      if (L.smoother == 1) d[ed[f] * K1 + a] = v;
+    }
+  }
+}
+
 int launch_smooth_first(const LevelDev& L, const double* r, double* e, double* d,
                         cudaStream_t st) {
+  if (L.imask == 0 && L.Dc != nullptr) {
+    const int g = cap_grid(2 * L.ne, 128, 148 * 16);
+    switch (L.k1) {
+      case 2: launch_ex(k_smooth_first_dc<2>, g, 128, 0, true, st, L, r, e, d); return 1;
+      case 3: launch_ex(k_smooth_first_dc<3>, g, 128, 0, true, st, L, r, e, d); return 1;
+      case 4: launch_ex(k_smooth_first_dc<4>, g, 128, 0, true, st, L, r, e, d); return 1;
+      default: launch_ex(k_smooth_first_dc<5>, g, 128, 0, true, st, L, r, e, d); return 1;
+    }
+  }
   launch_ex(k_smooth_first, cap_grid(L.nedge, 128, 148 * 8), 128, 0, true, st, L, r, e, d);
   return 1;
 }
