@@ -140,6 +140,9 @@ typedef struct {
   double cheb_ratio;            /* lambda_min = lambda_max / ratio, default 30 */
   int32_t lmax_iters;           /* default 20 */
   double lmax_safety;           /* default 1.05 */
+  int32_t nu_doubling;          /* 1: nu steps on the finest level, x 2 per coarser level
+                                   (beta_0 = beta_1 = 2; block-Jacobi
+                                   only); 0: V(nu_pre, nu_post) on every level (configs) */
 } mg_smoother_cfg;
 
 /* Build the level structure (host only; no device work).  p in 1..4.
@@ -210,6 +213,20 @@ int mg_prolong(void* ctx, int32_t level, const double* ec, double* e);
  * MG_BREAKDOWN), resid_hist [maxit+1].  Synchronises the stream. */
 int mg_pcg_solve(void* ctx, const double* g, double* lambda, double rtol, int32_t maxit,
                  int32_t* iters, double* relres, int32_t* solve_status, double* resid_hist);
+
+/* The paper's own Krylov setting, host-driven loops of
+ * library kernels, lambda_0 = 0, stopping on the TRUE residual
+ * ||g - A lambda|| <= tol ||g||:
+ *   mg_mg_solve:    MG as a solver, lambda += B_N (g - A lambda)
+ *   mg_gmres_solve: full GMRES left-preconditioned by B_N,
+ *                   modified Gram-Schmidt; basis: caller-owned device scratch of
+ *                   (maxit + 1) * ndof_N doubles.
+ * resid_hist (host, may be NULL): [maxit + 1] relative residuals. */
+int mg_mg_solve(void* ctx, const double* g, double* lambda, double tol, int32_t maxit,
+                int32_t* iters, double* relres, int32_t* solve_status, double* resid_hist);
+int mg_gmres_solve(void* ctx, const double* g, double* lambda, double tol, int32_t maxit,
+                   double* basis, int32_t* iters, double* relres, int32_t* solve_status,
+                   double* resid_hist);
 
 /* The whole user call with HOST buffers: copy K/method/tau/f/g_D to the
  * device, setup, rhs, PCG, copy the full trace solution (free + Dirichlet)

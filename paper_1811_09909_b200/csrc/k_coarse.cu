@@ -91,11 +91,16 @@ __device__ __forceinline__ void k_coarse_tail_t(const TailParams& G,
   const TailParams& P = use_smem ? SP : G;
   const int nlev = P.nlev;
   // ---- down-sweep: pre-smoothing, residual, step 3 + restriction
+  // smoothing steps of tail level li (beta = 2 doubling per coarser level); the
+  // coefficient slot is clamped to MAX_NU-1 (block-Jacobi's are step-invariant)
+  auto nu_of = [&](int nu, int li) { return P.nu_doubling ? nu << li : nu; };
+  auto cs = [](int s) { return s < MAX_NU ? s : MAX_NU - 1; };
   for (int li = 0; li < nlev - 1; ++li) {
     const TailLevel& L = P.lev[li];
     const TailLevel& C = P.lev[li + 1];
+    const int nu_pre = nu_of(P.nu_pre, li);
     int s0 = 0;
-    if (P.nu_pre > 0) {
+    if (nu_pre > 0) {
       const bool first_done = li == 0 ? P.first_fused != 0 : true;
       if (!first_done) {
         smooth_first_body(L.d, L.r, L.e, L.dv, t0, nt);
@@ -106,10 +111,10 @@ __device__ __forceinline__ void k_coarse_tail_t(const TailParams& G,
       zero_body(L.e, L.d.ndof, t0, nt);
       sync();
     }
-    for (int s = s0; s < P.nu_pre; ++s) {
+    for (int s = s0; s < nu_pre; ++s) {
       apply_pass_body<1, AM_W0, false>(L.d, 0, L.e, L.w, nullptr, nullptr, 0, t0, nt);
       sync();
-      apply_pass_body<1, AM_SMOOTH, false>(L.d, 1, L.e, L.w, L.r, L.dv, s, t0, nt);
+      apply_pass_body<1, AM_SMOOTH, false>(L.d, 1, L.e, L.w, L.r, L.dv, cs(s), t0, nt);
       sync();
     }
     apply_pass_body<1, AM_W0, false>(L.d, 0, L.e, L.w, nullptr, nullptr, 0, t0, nt);
@@ -118,7 +123,7 @@ __device__ __forceinline__ void k_coarse_tail_t(const TailParams& G,
     sync();
     lc_restrict_body(L.d, L.w, L.e, L.KIIinv, L.Pm, L.cbuf, 1, 1, t0, nt);
     sync();
-    const int fuse = (li + 1 < nlev - 1) && P.nu_pre > 0;
+    const int fuse = (li + 1 < nlev - 1) && nu_of(P.nu_pre, li + 1) > 0;
     restrict_edges_body(L.d, C.d, L.w, L.cbuf, C.r, fuse, C.e, C.dv, t0, nt);
     sync();
   }
@@ -134,10 +139,10 @@ __device__ __forceinline__ void k_coarse_tail_t(const TailParams& G,
     const TailLevel& C = P.lev[li + 1];
     prolong_macro_body(L.d, C.d, C.e, L.Pm, L.e, t0, nt);
     sync();
-    for (int s = 0; s < P.nu_post; ++s) {
+    for (int s = 0; s < nu_of(P.nu_post, li); ++s) {
       apply_pass_body<1, AM_W0, false>(L.d, 0, L.e, L.w, nullptr, nullptr, 0, t0, nt);
       sync();
-      apply_pass_body<1, AM_SMOOTH, false>(L.d, 1, L.e, L.w, L.r, L.dv, s, t0, nt);
+      apply_pass_body<1, AM_SMOOTH, false>(L.d, 1, L.e, L.w, L.r, L.dv, cs(s), t0, nt);
       sync();
     }
   }

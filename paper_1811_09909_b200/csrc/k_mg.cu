@@ -475,4 +475,19 @@ int launch_add(double* dst, const double* src, int64_t n, cudaStream_t st) {
   return 1;
 }
 
+// z = a x + b y (host scalars; the host-driven Krylov drivers)
+__global__ void k_axpby(double a, const double* __restrict__ x, double b, const double* y,
+                        double* z, int64_t n) {
+  pdl_enter();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    z[i] = fma(a, x[i], b * y[i]);
+}
+
+int launch_axpby(double a, const double* x, double b, const double* y, double* z, int64_t n,
+                 cudaStream_t st) {
+  launch_ex(k_axpby, vec_grid(n), 256, 0, true, st, a, x, b, y, z, n);
+  return 1;
+}
+
 }  // namespace mgdtn

@@ -326,6 +326,8 @@ int launch_copy(double* dst, const double* src, int64_t n, cudaStream_t st);
 int launch_zero(double* dst, int64_t n, cudaStream_t st);
 int launch_copy_masked(const LevelDev& L, double* dst, const double* src, cudaStream_t st);
 int launch_add(double* dst, const double* src, int64_t n, cudaStream_t st);
+int launch_axpby(double a, const double* x, double b, const double* y, double* z, int64_t n,
+                 cudaStream_t st);   // z = a x + b y
 
 // ---------------------------------------------------------------- partitioned levels (k_part.cu)
 int itf_stride(const LevelDev& L);     // doubles per side in a halo buffer

@@ -517,8 +517,14 @@ static inline void apply_full(Ctx* c, const HostLevel& L, const double* x, doubl
 }
 
 static inline void smooth_step(Ctx* c, HostLevel& L, int step) {
-  apply_mode(c, L, AM_SMOOTH, L.e, L.w, L.r, L.dv, step, nullptr);
+  // coefficient slot clamped to MAX_NU-1: only block-Jacobi (step-invariant
+  // coefficients) may run more steps than that (beta-doubling)
+  apply_mode(c, L, AM_SMOOTH, L.e, L.w, L.r, L.dv, step < MAX_NU ? step : MAX_NU - 1, nullptr);
 }
+
+// smoothing steps on level li: V(nu, nu), times 2 per coarser level with the
+// paper's beta = 2 schedule
+static inline int nu_at(const Ctx* c, int nu, int li) { return c->sm.nu_doubling ? nu << li : nu; }
 
 static inline void residual(Ctx* c, HostLevel& L) {  // L.w = L.r - A L.e
   apply_mode(c, L, AM_RESID, L.e, L.w, L.r, nullptr, 0, nullptr);
@@ -591,8 +597,9 @@ static void vcycle_level(Ctx* c, int li, bool first_done) {
   }
   if (c->tail_vcycle && li == c->tail_start) {   // this level and every coarser one: one launch
     TailParams& T = c->tail;
-    T.nu_pre = c->sm.nu_pre;
-    T.nu_post = c->sm.nu_post;
+    T.nu_pre = nu_at(c, c->sm.nu_pre, li);
+    T.nu_post = nu_at(c, c->sm.nu_post, li);
+    T.nu_doubling = c->sm.nu_doubling;
     T.first_fused = first_done ? 1 : 0;
     for (int k = 0; k < T.nlev; ++k) T.lev[k].d = c->lev[c->tail_start + k].d;   // smoother kind
     c->launches += launch_coarse_tail(T, c->st);
@@ -602,7 +609,7 @@ static void vcycle_level(Ctx* c, int li, bool first_done) {
     c->launches += launch_coarse_solve(L.d, c->fidx, c->nf, c->A1inv, L.r, L.e, c->st);
     return;
   }
-  const int nu_pre = c->sm.nu_pre, nu_post = c->sm.nu_post;
+  const int nu_pre = nu_at(c, c->sm.nu_pre, li), nu_post = nu_at(c, c->sm.nu_post, li);
   int s0 = 0;
   if (nu_pre > 0) {
     if (!first_done) c->launches += launch_smooth_first(L.d, L.r, L.e, L.dv, c->st);
@@ -613,7 +620,7 @@ static void vcycle_level(Ctx* c, int li, bool first_done) {
   for (int s = s0; s < nu_pre; ++s) smooth_step(c, L, s);
   residual(c, L);  // L.w = r - A e1
   HostLevel& C = c->lev[li + 1];
-  const bool fuse = (li + 1 < nlev - 1) && nu_pre > 0 &&
+  const bool fuse = (li + 1 < nlev - 1) && nu_at(c, c->sm.nu_pre, li + 1) > 0 &&
                     !(c->tail_dense && li + 1 == c->tail_start) && !gathers(c, li);
   restrict_level(c, li, L.w, L.e, true, C.r, fuse);
   vcycle_level(c, li + 1, fuse);
@@ -702,8 +709,9 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
   }
   if (c->tail_dense) {
     TailParams& T = c->tail;
-    T.nu_pre = c->sm.nu_pre;
-    T.nu_post = c->sm.nu_post;
+    T.nu_pre = nu_at(c, c->sm.nu_pre, c->tail_start);
+    T.nu_post = nu_at(c, c->sm.nu_post, c->tail_start);
+    T.nu_doubling = c->sm.nu_doubling;
     T.first_fused = 0;
     for (int k = 0; k < T.nlev; ++k) T.lev[k].d = c->lev[c->tail_start + k].d;
     c->launches += launch_tail_basis(T, c->tfidx, c->nft, c->Bt, st);
@@ -896,6 +904,150 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
   if (status_out) *status_out = status;
   c->last_solve_launches = c->launches - l0;
   return MG_OK;
+}
+
+// ---------------------------------------------------------------- MG as a solver, GMRES
+// host-driven drivers of the paper's own Krylov setting (PAPER.md:937-939,
+// 1008-1018): every step is a library kernel; the host holds the scalars.
+static double gdot(Ctx* c, const double* a, const double* b) {
+  HostLevel& F = c->lev[0];
+  const int vg = vec_grid(F.d.ndof);
+  c->launches += launch_dot(a, b, F.d.ndof, c->part, vg, c->st, &F.d);
+  reduce_scal(c, c->part, vg, c->scal, 12, 0);
+  cudaMemcpyAsync(c->pinned, c->scal + 12, sizeof(double), cudaMemcpyDeviceToHost, c->st);
+  cudaStreamSynchronize(c->st);
+  return c->pinned[0];
+}
+
+// out = B_N v: one V-cycle of Algorithm 1 from e = 0
+static void precond(Ctx* c, const double* v, double* out) {
+  HostLevel& F = c->lev[0];
+  c->launches += launch_copy_masked(F.d, F.r, v, c->st);
+  vcycle_level(c, 0, false);
+  c->launches += launch_copy(out, F.e, F.d.ndof, c->st);
+}
+
+// lambda^{i+1} = lambda^i + B_N (g - A lambda^i), lambda^0 = 0,
+// until ||g - A lambda|| <= tol ||g||
+static int mgsolve_impl(Ctx* c, const double* g, double* x, double tol, int maxit, int* iters,
+                        double* relres, int* status, double* hist) {
+  HostLevel& F = c->lev[0];
+  const int64_t n = F.d.ndof;
+  double* gb = c->gbuf;   // masked g
+  double* r = c->pv;
+  c->launches += launch_copy_masked(F.d, gb, g, c->st);
+  c->launches += launch_zero(x, n, c->st);
+  c->launches += launch_copy(r, gb, n, c->st);
+  const double gn = std::sqrt(gdot(c, gb, gb));
+  int st = MG_MAXIT, it = 0;
+  double rel = gn > 0 ? 1.0 : 0.0;
+  if (hist) hist[0] = rel;
+  if (!(gn > 0)) st = MG_CONVERGED;
+  for (it = 1; it <= maxit && st != MG_CONVERGED; ++it) {
+    precond(c, r, c->ap);
+    c->launches += launch_add(x, c->ap, n, c->st);
+    apply_full(c, F, x, c->ap, nullptr);
+    c->launches += launch_axpby(1.0, gb, -1.0, c->ap, r, n, c->st);
+    rel = std::sqrt(gdot(c, r, r)) / gn;
+    if (hist) hist[it] = rel;
+    if (rel <= tol) {
+      st = MG_CONVERGED;
+      break;
+    }
+    if (!std::isfinite(rel) || rel > 1e6) {
+      st = MG_DIVERGED;
+      break;
+    }
+  }
+  if (it > maxit) it = maxit;
+  CK(cudaGetLastError());
+  *iters = gn > 0 ? it : 0;
+  *relres = rel;
+  *status = st;
+  return c->comm_rc ? c->comm_rc : MG_OK;
+}
+
+// Left-preconditioned full GMRES: Arnoldi on B_N A from
+// v_0 = B_N g / ||B_N g||, modified Gram-Schmidt, Givens least squares; stops on
+// the true residual ||g - A lambda_j|| <= tol ||g||.
+// V: caller-provided device basis [(maxit+1)][ndof].
+static int gmres_impl(Ctx* c, const double* g, double* x, double tol, int maxit, double* V,
+                      int* iters, double* relres, int* status, double* hist) {
+  HostLevel& F = c->lev[0];
+  const int64_t n = F.d.ndof;
+  double* gb = c->gbuf;
+  c->launches += launch_copy_masked(F.d, gb, g, c->st);
+  c->launches += launch_zero(x, n, c->st);
+  const double gn = std::sqrt(gdot(c, gb, gb));
+  *iters = 0;
+  *relres = 0.0;
+  *status = MG_CONVERGED;
+  if (hist) hist[0] = gn > 0 ? 1.0 : 0.0;
+  if (!(gn > 0)) return MG_OK;
+  auto Vj = [&](int j) { return V + (int64_t)j * n; };
+  precond(c, gb, Vj(0));
+  const double beta = std::sqrt(gdot(c, Vj(0), Vj(0)));
+  c->launches += launch_axpby(1.0 / beta, Vj(0), 0.0, Vj(0), Vj(0), n, c->st);
+  std::vector<double> H((size_t)(maxit + 1) * maxit, 0.0), cs(maxit), sn(maxit), rhs(maxit + 1, 0.0);
+  auto h = [&](int i, int j) -> double& { return H[(size_t)i * maxit + j]; };
+  rhs[0] = beta;
+  int st = MG_MAXIT, j = 0;
+  double rel = 1.0;
+  for (j = 0; j < maxit; ++j) {
+    apply_full(c, F, Vj(j), c->ap, nullptr);
+    precond(c, c->ap, Vj(j + 1));
+    for (int i = 0; i <= j; ++i) {   // modified Gram-Schmidt
+      h(i, j) = gdot(c, Vj(j + 1), Vj(i));
+      c->launches += launch_axpby(-h(i, j), Vj(i), 1.0, Vj(j + 1), Vj(j + 1), n, c->st);
+    }
+    const double hn = std::sqrt(gdot(c, Vj(j + 1), Vj(j + 1)));
+    h(j + 1, j) = hn;
+    if (hn > 0) c->launches += launch_axpby(1.0 / hn, Vj(j + 1), 0.0, Vj(j + 1), Vj(j + 1), n, c->st);
+    // least squares min || beta e1 - H y || by Givens rotations on a copy of column j
+    std::vector<double> col(j + 2);
+    for (int i = 0; i <= j + 1; ++i) col[i] = h(i, j);
+    for (int i = 0; i < j; ++i) {
+      const double t = cs[i] * col[i] + sn[i] * col[i + 1];
+      col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1];
+      col[i] = t;
+    }
+    const double rr = std::hypot(col[j], col[j + 1]);
+    cs[j] = rr > 0 ? col[j] / rr : 1.0;
+    sn[j] = rr > 0 ? col[j + 1] / rr : 0.0;
+    col[j] = rr;
+    col[j + 1] = 0.0;
+    for (int i = 0; i <= j; ++i) h(i, j) = col[i];   // R factor, column j
+    rhs[j + 1] = -sn[j] * rhs[j];
+    rhs[j] = cs[j] * rhs[j];
+    std::vector<double> y(j + 1);
+    for (int i = j; i >= 0; --i) {
+      double s = rhs[i];
+      for (int k = i + 1; k <= j; ++k) s -= h(i, k) * y[k];
+      y[i] = s / h(i, i);
+    }
+    // x = V y and the true residual
+    c->launches += launch_zero(x, n, c->st);
+    for (int i = 0; i <= j; ++i) c->launches += launch_axpby(y[i], Vj(i), 1.0, x, x, n, c->st);
+    apply_full(c, F, x, c->ap, nullptr);
+    c->launches += launch_axpby(1.0, gb, -1.0, c->ap, c->pv, n, c->st);
+    rel = std::sqrt(gdot(c, c->pv, c->pv)) / gn;
+    if (hist) hist[j + 1] = rel;
+    if (rel <= tol || hn == 0.0) {
+      st = MG_CONVERGED;
+      ++j;
+      break;
+    }
+    if (!std::isfinite(rel)) {
+      st = MG_BREAKDOWN;
+      ++j;
+      break;
+    }
+  }
+  CK(cudaGetLastError());
+  *iters = j > maxit ? maxit : j;
+  *relres = rel;
+  *status = st;
+  return c->comm_rc ? c->comm_rc : MG_OK;
 }
 
 static int rhs_impl(Ctx* c, const double* f_qp, double f_const, const double* gD_qp, double* g,
@@ -1179,7 +1331,10 @@ int mg_setup_dtn(void* ctx, const double* K, const int8_t* method, const double*
   if (!(sm.cheb_ratio > 1)) sm.cheb_ratio = 30.0;
   if (sm.lmax_iters <= 0) sm.lmax_iters = 20;
   if (!(sm.lmax_safety > 0)) sm.lmax_safety = 1.05;
-  if (sm.nu_pre != c->sm.nu_pre || sm.nu_post != c->sm.nu_post || sm.kind != c->sm.kind)
+  if (sm.nu_doubling && sm.kind != MG_SMOOTH_BLOCK_JACOBI)
+    return fail(c, MG_ERR_ARG, "nu_doubling needs the block-Jacobi smoother");
+  if (sm.nu_pre != c->sm.nu_pre || sm.nu_post != c->sm.nu_post || sm.kind != c->sm.kind ||
+      sm.nu_doubling != c->sm.nu_doubling)
     drop_graphs(c);
   c->sm = sm;
   c->setup_done = false;
@@ -1277,6 +1432,35 @@ int mg_pcg_solve(void* ctx, const double* g, double* lambda, double rtol, int32_
   if (iters) *iters = it;
   if (relres) *relres = rel;
   if (solve_status) *solve_status = stt;
+  return MG_OK;
+}
+
+int mg_mg_solve(void* ctx, const double* g, double* lambda, double tol, int32_t maxit,
+                int32_t* iters, double* relres, int32_t* solve_status, double* resid_hist) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !g || !lambda || maxit < 1 || !(tol > 0)) return MG_ERR_ARG;
+  if (!c->setup_done) return fail(c, MG_ERR_STATE, "setup first");
+  int it = 0, st = 0;
+  double rel = 0;
+  RC(mgsolve_impl(c, g, lambda, tol, maxit, &it, &rel, &st, resid_hist));
+  if (iters) *iters = it;
+  if (relres) *relres = rel;
+  if (solve_status) *solve_status = st;
+  return MG_OK;
+}
+
+int mg_gmres_solve(void* ctx, const double* g, double* lambda, double tol, int32_t maxit,
+                   double* basis, int32_t* iters, double* relres, int32_t* solve_status,
+                   double* resid_hist) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !g || !lambda || !basis || maxit < 1 || !(tol > 0)) return MG_ERR_ARG;
+  if (!c->setup_done) return fail(c, MG_ERR_STATE, "setup first");
+  int it = 0, st = 0;
+  double rel = 0;
+  RC(gmres_impl(c, g, lambda, tol, maxit, basis, &it, &rel, &st, resid_hist));
+  if (iters) *iters = it;
+  if (relres) *relres = rel;
+  if (solve_status) *solve_status = st;
   return MG_OK;
 }
 

@@ -39,7 +39,7 @@ class mg_partition(C.Structure):
 class mg_smoother_cfg(C.Structure):
     _fields_ = [("kind", C.c_int32), ("nu_pre", C.c_int32), ("nu_post", C.c_int32),
                 ("omega", C.c_double), ("cheb_ratio", C.c_double), ("lmax_iters", C.c_int32),
-                ("lmax_safety", C.c_double)]
+                ("lmax_safety", C.c_double), ("nu_doubling", C.c_int32)]
 
 
 # exported symbols and their argtypes (must match include/mgdtn.h)
@@ -61,6 +61,10 @@ _SIGS = {
                      C.POINTER(C.c_double), C.POINTER(C.c_int32), _P],
     "mg_solve_host": [_P, _P, _P, _P, _P, C.c_double, _P, C.POINTER(mg_smoother_cfg), C.c_double,
                       C.c_int32, _P, C.POINTER(C.c_int32), C.POINTER(C.c_double), C.POINTER(C.c_int32)],
+    "mg_mg_solve": [_P, _P, _P, C.c_double, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_double),
+                    C.POINTER(C.c_int32), _P],
+    "mg_gmres_solve": [_P, _P, _P, C.c_double, C.c_int32, _P, C.POINTER(C.c_int32),
+                       C.POINTER(C.c_double), C.POINTER(C.c_int32), _P],
     "mg_staging_bytes": [_P, C.c_int32, C.c_int32, C.POINTER(C.c_size_t)],
     "mg_bind_staging": [_P, _P, C.c_size_t],
     "mg_recover_volume": [_P, _P, _P, C.c_double, _P, _P, C.POINTER(C.c_double)],
@@ -129,10 +133,11 @@ class SmootherConfig:
     cheb_ratio: float = 30.0
     lmax_iters: int = 20
     lmax_safety: float = 1.05
+    nu_doubling: bool = False
 
     def c(self):
         return mg_smoother_cfg(self.kind, self.nu_pre, self.nu_post, self.omega, self.cheb_ratio,
-                               self.lmax_iters, self.lmax_safety)
+                               self.lmax_iters, self.lmax_safety, int(self.nu_doubling))
 
 
 class _Ordered:
@@ -380,6 +385,33 @@ class MGSolver:
         hp = hist.ctypes.data_as(C.c_void_p) if history else None
         self._call("mg_pcg_solve", _ptr(g), _ptr(lam), rtol, maxit, C.byref(it),
                                         C.byref(rel), C.byref(st), hp)
+        info = dict(iters=it.value, relres=rel.value, status=STATUS[st.value])
+        if history:
+            info["hist"] = hist[: it.value + 1]
+        return lam, info
+
+    def mg_solve(self, g, tol=1e-9, maxit=200, history=False):
+        """MG as a solver (mg_mg_solve)."""
+        g = self._d(g)
+        lam = self._vec()
+        it, rel, st = C.c_int32(), C.c_double(), C.c_int32()
+        hist = np.zeros(maxit + 1) if history else None
+        self._call("mg_mg_solve", _ptr(g), _ptr(lam), tol, maxit, C.byref(it), C.byref(rel),
+                   C.byref(st), hist.ctypes.data_as(C.c_void_p) if history else None)
+        info = dict(iters=it.value, relres=rel.value, status=STATUS[st.value])
+        if history:
+            info["hist"] = hist[: it.value + 1]
+        return lam, info
+
+    def gmres_solve(self, g, tol=1e-9, maxit=200, history=False):
+        """Left-preconditioned full GMRES (mg_gmres_solve)."""
+        g = self._d(g)
+        lam = self._vec()
+        basis = torch.empty((maxit + 1) * self.ndof(), dtype=torch.float64, device=self.device)
+        it, rel, st = C.c_int32(), C.c_double(), C.c_int32()
+        hist = np.zeros(maxit + 1) if history else None
+        self._call("mg_gmres_solve", _ptr(g), _ptr(lam), tol, maxit, _ptr(basis), C.byref(it),
+                   C.byref(rel), C.byref(st), hist.ctypes.data_as(C.c_void_p) if history else None)
         info = dict(iters=it.value, relres=rel.value, status=STATUS[st.value])
         if history:
             info["hist"] = hist[: it.value + 1]

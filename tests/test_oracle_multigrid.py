@@ -248,14 +248,8 @@ def _example1(n, p, tau_mode, step3=True):
     """Example I: q = x y exp(x^2 y^3), K = 1, strong
     Dirichlet data, MG (block-Jacobi, beta = 2 doubling, m_N = 3) as solver and
     as GMRES left preconditioner, tol 1e-9."""
-    X, Y = W.element_sample_coords(n, p)
-    e = np.exp(X ** 2 * Y ** 3)
-    f = -(e * (6 * X * Y ** 4 + 4 * X ** 3 * Y ** 7) + e * (12 * X ** 3 * Y ** 2 + 9 * X ** 5 * Y ** 5))
-    BX, BY = W.boundary_sample_coords(n, p)
-    gD = BX * BY * np.exp(BX ** 2 * BY ** 3)
-    ne = n * n
-    tau = np.full(ne, 1.0 if tau_mode == "1" else float(n))     # 1/h_min, h_min = 1/n
-    ts = assembly.TraceSystem(n, p, np.ones(ne), np.zeros(ne, np.int8), tau, f, 0.0, gD)
+    pr = W.example1_problem(n, p, tau_mode)
+    ts = assembly.TraceSystem(n, p, pr.K, pr.method, pr.tau, pr.f_qp, 0.0, pr.gD_qp)
     H = multigrid.Hierarchy(ts.A, n, p, smoother=0, nu_pre=3, nu_post=3, step3=step3,
                             nu_doubling=True)
     a = krylov.mg_solver(ts.A, H.vcycle, ts.g, 1e-9, 200)
