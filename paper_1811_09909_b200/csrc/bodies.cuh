@@ -38,13 +38,15 @@ __device__ __forceinline__ void gather_x(const double* x, const int64_t ed[4], c
 // itf: bit f set if edge f is a partition interface edge (multi-GPU): the
 // colour-1 pass stores only this rank's partial sum there (y = y_T) and the
 // interface epilogue (k_itf_epilogue) finishes it after the halo exchange.
-template <int K1, int MODE, bool NC = true>
+// FMASK: the edges (bits) this call handles (the two-warp apply splits them)
+template <int K1, int MODE, bool NC = true, int FMASK = 15>
 __device__ __forceinline__ void epi_load(const LevelDev& L, const int64_t ed[4], const bool bd[4],
                                          const double* y, const double* __restrict__ r,
                                          const double* d, double* t, double* dd, int itf = 0) {
   if (MODE == AM_W0) return;
 #pragma unroll
   for (int f = 0; f < 4; ++f) {
+    if (!((FMASK >> f) & 1)) continue;
     if ((itf >> f) & 1) {
 #pragma unroll
       for (int a = 0; a < K1; ++a) {
@@ -64,7 +66,7 @@ __device__ __forceinline__ void epi_load(const LevelDev& L, const int64_t ed[4],
   }
 }
 
-template <int K1, int MODE, bool DOT>
+template <int K1, int MODE, bool DOT, int FMASK = 15>
 __device__ __forceinline__ void epi_store(const LevelDev& L, const int64_t ed[4], const bool bd[4],
                                           const double* xv, const double* yv, const double* t,
                                           const double* dd, const double* x, double* y, double* d,
@@ -72,6 +74,7 @@ __device__ __forceinline__ void epi_store(const LevelDev& L, const int64_t ed[4]
                                           int itf = 0) {
 #pragma unroll
   for (int f = 0; f < 4; ++f) {
+    if (!((FMASK >> f) & 1)) continue;
     const int64_t base = ed[f] * K1;
     if (MODE != AM_W0 && ((itf >> f) & 1)) {   // partial sum only; finished after the halo
 #pragma unroll

@@ -184,6 +184,16 @@ __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, 
       t[a] = 0.0;
       dd[a] = 0.0;
     }
+    if (L.probe == 1) {   // measurement probe: the S_T stream alone (no gather, math, stores)
+      const int st = k % NST;
+      mbar_wait(&bars[st], (uint32_t)((k / NST) & 1));
+      __syncwarp();
+      if (lane == 0 && k + NST < nmine) {
+        fence_proxy_async();
+        issue(k + NST);
+      }
+      continue;
+    }
     if (act) epi_load<K1, MODE>(L, ed, bd, y, r, d, t, dd, itf);   // needed after the matvec only
     if (XPF) prefetch(k + 1);
     const int st = k % NST;
@@ -211,6 +221,152 @@ __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
     if (lane == 0) partials[blockIdx.x] = dot;
+  }
+}
+
+// ---------------------------------------------------------------- two-warp TMA apply
+// k_apply_tma with TWO warps per CTA sharing the chunk ring: warp w computes the
+// packed rows a in [A0*w, A0 + w*(M-A0)) of every element of the chunk (A0 splits the
+// npk entries in halves), so each warp issues half the FMA chain; the partial
+// sums of the other warp's two edges go through shared memory, and warp w runs
+// the epilogue of edges {2w, 2w+1}.  Same math, same per-entry FMA order within
+// each row; the two halves are added once (y = y_w0 + y_w1).
+template <int M>
+struct RowSplit {   // smallest A0 with sum_{a<A0} (M - a) >= npk / 2
+  static constexpr int NPK = M * (M + 1) / 2;
+  static constexpr int calc() {
+    int acc = 0;
+    for (int a = 0; a < M; ++a) {
+      acc += M - a;
+      if (2 * acc >= NPK) return a + 1;
+    }
+    return M;
+  }
+  static constexpr int A0 = calc();
+};
+
+template <int P, int MODE, bool DOT, int NST>
+__global__ void __launch_bounds__(64) k_apply_tma2(const LevelDev L, int colour, const double* x,
+                                                   double* y, const double* __restrict__ r,
+                                                   double* d, int step,
+                                                   double* __restrict__ partials, int early) {
+  using C = TmaCfg<P>;
+  constexpr int K1 = C::K1, M = C::M, NPK = C::NPK, A0 = RowSplit<M>::A0, HK = 2 * K1;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bars[NST];
+  __shared__ double xch[2][K1][32];   // one edge's partial sums handed to the other warp
+  __shared__ double dred[2];
+  double* stage_buf = reinterpret_cast<double*>(smem_raw);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t nec = L.ne >> 1;
+  const int nchunk = (int)((nec + 31) >> 5);
+  const double* Sbase = L.S + (int64_t)colour * L.nchunk * NPK * 32;
+  const uint64_t pol = evict_first_policy();
+  const int nmine = (int)blockIdx.x < nchunk ? (nchunk - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int k) {
+    const int c = (int)blockIdx.x + k * (int)gridDim.x;
+    const int s = k % NST;
+    mbar_expect_tx(&bars[s], C::CHUNK_BYTES);
+    tma_bulk_g2s(stage_buf + (size_t)s * NPK * 32, Sbase + (int64_t)c * NPK * 32, C::CHUNK_BYTES,
+                 &bars[s], pol);
+  };
+  if (early) {
+    if (threadIdx.x == 0)
+      for (int k = 0; k < NST && k < nmine; ++k) issue(k);
+    pdl_trigger();
+    pdl_wait();
+  } else {
+    pdl_wait();
+    if (threadIdx.x == 0)
+      for (int k = 0; k < NST && k < nmine; ++k) issue(k);
+    pdl_trigger();
+  }
+  double dot = 0.0;
+  for (int k = 0; k < nmine; ++k) {
+    const int c = (int)blockIdx.x + k * (int)gridDim.x;
+    const int64_t s = (int64_t)c * 32 + lane;
+    const bool act = s < nec;
+    int64_t ed[4] = {0, 0, 0, 0};
+    bool bd[4] = {true, true, true, true};
+    int itf = 0;
+    double xv[M], yv[M], t[M], dd[M];
+#pragma unroll
+    for (int a = 0; a < M; ++a) {
+      xv[a] = 0.0;
+      yv[a] = 0.0;
+      t[a] = 0.0;
+      dd[a] = 0.0;
+    }
+    if (act) {
+      int i, j;
+      slot_elem(L.nx, colour, s, i, j);
+      elem_edges(L.nx, L.ny, i, j, ed, bd, L.dmask);
+      itf = elem_itf(L.nx, L.ny, i, j, L.imask);
+      gather_x<K1>(x, ed, bd, xv);
+      if (wid == 0) epi_load<K1, MODE, true, 3>(L, ed, bd, y, r, d, t, dd, itf);
+      else epi_load<K1, MODE, true, 12>(L, ed, bd, y, r, d, t, dd, itf);
+    }
+    const int st = k % NST;
+    mbar_wait(&bars[st], (uint32_t)((k / NST) & 1));
+    const double* Sp = stage_buf + (size_t)st * NPK * 32 + lane;
+    if (wid == 0) {
+#pragma unroll
+      for (int a = 0; a < A0; ++a) {
+#pragma unroll
+        for (int b = a; b < M; ++b) {
+          const int kk = a * (2 * M - a + 1) / 2 + (b - a);
+          const double sv = Sp[kk * 32];
+          yv[a] = fma(sv, xv[b], yv[a]);
+          if (b != a) yv[b] = fma(sv, xv[a], yv[b]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int a = A0; a < M; ++a) {
+#pragma unroll
+        for (int b = a; b < M; ++b) {
+          const int kk = a * (2 * M - a + 1) / 2 + (b - a);
+          const double sv = Sp[kk * 32];
+          yv[a] = fma(sv, xv[b], yv[a]);
+          if (b != a) yv[b] = fma(sv, xv[a], yv[b]);
+        }
+      }
+    }
+    // hand the other warp's two edges over, one edge per round (warp 0 owns edges
+    // 0,1 = outputs [0,HK)); the first barrier also frees the stage for the refill
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+#pragma unroll
+      for (int q = 0; q < K1; ++q) xch[wid][q][lane] = yv[(wid == 0 ? HK : 0) + hr * K1 + q];
+      __syncthreads();
+      if (hr == 0 && threadIdx.x == 0 && k + NST < nmine) {
+        fence_proxy_async();
+        issue(k + NST);
+      }
+#pragma unroll
+      for (int q = 0; q < K1; ++q) {
+        const int o = (wid == 0 ? 0 : HK) + hr * K1 + q;
+        yv[o] = yv[o] + xch[wid ^ 1][q][lane];
+      }
+      __syncthreads();
+    }
+    if (act) {
+      if (wid == 0) epi_store<K1, MODE, DOT, 3>(L, ed, bd, xv, yv, t, dd, x, y, d, step, 0.0, 0.0, dot, itf);
+      else epi_store<K1, MODE, DOT, 12>(L, ed, bd, xv, yv, t, dd, x, y, d, step, 0.0, 0.0, dot, itf);
+    }
+  }
+  if (DOT) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if (lane == 0) dred[wid] = dot;
+    __syncthreads();
+    if (threadIdx.x == 0) partials[blockIdx.x] = dred[0] + dred[1];
   }
 }
 
@@ -553,16 +709,26 @@ __global__ void __launch_bounds__(32) k_apply_fused(const LevelDev L, const doub
     }
     if (!FLAGS && k == nmine0) {   // grid barrier between the colour passes
       __syncwarp();
-      if (lane == 0) {
+      if (lane == 0) {   // one poller per CTA (not 32): the flag's L2 line stays uncontended
         __threadfence();
         if (atomicAdd(L.sync + 1, 1u) == (unsigned)G - 1u) {
           L.sync[1] = 0u;
           __threadfence();
           st_release_u32(L.sync, gen);
         }
+        while (ld_acquire_u32(L.sync) != gen) __nanosleep(100);
       }
-      while (ld_acquire_u32(L.sync) != gen) __nanosleep(64);
       __syncwarp();
+    }
+    if (L.probe == 1) {   // measurement probe: the S_T stream alone
+      const int st = k % NST;
+      mbar_wait(&bars[st], (uint32_t)((k / NST) & 1));
+      __syncwarp();
+      if (lane == 0 && k + NST < nitems) {
+        fence_proxy_async();
+        issue(k + NST);
+      }
+      continue;
     }
     if (act) {
       int i, j;
@@ -810,10 +976,28 @@ static void launch_tma_x(const LevelDev& L, int colour, const double* x, double*
             step, partials, pdl ? 1 : 0);
 }
 
+static bool use_tma2() {   // MGDTN_TMA2=1: two warps per CTA (A/B; measured slower)
+  static int v = -1;
+  if (v < 0) v = env_int("MGDTN_TMA2", 0);
+  return v != 0;
+}
+
 template <int P, int MODE, bool DOT, int NST>
 static void launch_tma(const LevelDev& L, int colour, const double* x, double* y, const double* r,
                        double* d, int step, double* partials, int grid, bool pdl,
                        cudaStream_t st) {
+  if (use_tma2() && MODE != AM_SMOOTH && MODE != AM_DINV) {
+    const size_t smem = (size_t)NST * TmaCfg<P>::CHUNK_BYTES;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(k_apply_tma2<P, MODE, DOT, NST>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr_set = true;
+    }
+    launch_ex(k_apply_tma2<P, MODE, DOT, NST>, grid, 64, smem, pdl, st, L, colour, x, y, r, d,
+              step, partials, pdl ? 1 : 0);
+    return;
+  }
   if (use_xpf())
     launch_tma_x<P, MODE, DOT, NST, true>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
   else

@@ -47,6 +47,7 @@ struct LevelDev {
   int imask;               // sides that are partition interfaces (15 & ~dmask on a rank, or 0)
   int ox, oy, gnx, gny;    // this block's element offset in the global level and the global
                            // level's dims (0, 0, nx, ny on one GPU)
+  int probe;               // measurement probe (MGDTN_PROBE=1: the apply streams S_T only)
 };
 
 // global edge id of local edge e of a level block (power-iteration start vector)

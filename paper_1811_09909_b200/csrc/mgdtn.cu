@@ -124,6 +124,11 @@ static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 constexpr int HIST_CAP = 16384;   // device residual history; larger maxit -> host loop
 
 // ---------------------------------------------------------------- hierarchy
+static int env_or(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
 static void init_level(HostLevel& L, int nx, int ny, int p, double h, int kind) {
   LevelDev& d = L.d;
   d.nx = nx;
@@ -142,6 +147,7 @@ static void init_level(HostLevel& L, int nx, int ny, int p, double h, int kind) 
   d.oy = 0;
   d.gnx = nx;
   d.gny = ny;
+  d.probe = env_or("MGDTN_PROBE", 0);
   d.ndi = 4 * d.k1 * (d.k1 + 1) / 2;
   L.h = h;
   L.kind = kind;
@@ -321,10 +327,6 @@ static void bind_pointers(Ctx* c) {
 // single CTA over <= 16x16 levels beats the per-step launches; multi-CTA
 // clusters and larger tails lose to them).  MGDTN_TAIL_VCYCLE=0 /
 // MGDTN_TAIL_LMAX=0 keep the V-cycle / the Chebyshev power iteration on launches.
-static int env_or(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e ? std::atoi(e) : dflt;
-}
 
 static void plan_tail(Ctx* c) {
   const char* env = std::getenv("MGDTN_TAIL_NE");
