@@ -32,6 +32,17 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
   return pol;
 }
 
+// L2 policy of a level's operator stream: fraction `keep` evict_last (stays resident
+// across the many applies of a solve), the rest evict_first
+__device__ __forceinline__ uint64_t stream_policy(float keep) {
+  if (!(keep > 0.0f)) return evict_first_policy();
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;"
+               : "=l"(pol)
+               : "f"(keep > 1.0f ? 1.0f : keep));
+  return pol;
+}
+
 __device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
   double v;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
@@ -104,7 +115,7 @@ __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, 
   const int64_t nec = L.ne >> 1;
   const int nchunk = (int)((nec + 31) >> 5);
   const double* Sbase = L.S + (int64_t)colour * L.nchunk * NPK * 32;
-  const uint64_t pol = evict_first_policy();
+  const uint64_t pol = stream_policy(L.l2keep);
   // chunks of this CTA: c_k = blockIdx.x + k * gridDim.x
   const int nmine = (int)blockIdx.x < nchunk ? (nchunk - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   if (lane == 0) {
@@ -261,7 +272,7 @@ __global__ void __launch_bounds__(64) k_apply_tma2(const LevelDev L, int colour,
   const int64_t nec = L.ne >> 1;
   const int nchunk = (int)((nec + 31) >> 5);
   const double* Sbase = L.S + (int64_t)colour * L.nchunk * NPK * 32;
-  const uint64_t pol = evict_first_policy();
+  const uint64_t pol = stream_policy(L.l2keep);
   const int nmine = (int)blockIdx.x < nchunk ? (nchunk - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -411,7 +422,7 @@ __global__ void __launch_bounds__(32) k_apply_seg(const LevelDev L, int colour, 
   const int64_t nec = L.ne >> 1;
   const int nchunk = L.nchunk;
   const double* Sbase = L.S + (int64_t)colour * nchunk * NPK * 32;
-  const uint64_t pol = evict_first_policy();
+  const uint64_t pol = stream_policy(L.l2keep);
   const int G = (int)gridDim.x, b = (int)blockIdx.x;
   const int nmine = b < nchunk ? (nchunk - 1 - b) / G + 1 : 0;
   const int total = nmine * NS;
@@ -655,7 +666,7 @@ __global__ void __launch_bounds__(32) k_apply_fused(const LevelDev L, const doub
   const int64_t nec = L.ne >> 1;
   const int nchunk = L.nchunk;
   const int64_t nxh = L.nx >> 1;
-  const uint64_t pol = evict_first_policy();
+  const uint64_t pol = stream_policy(L.l2keep);
   const int G = (int)gridDim.x, b = (int)blockIdx.x;
   const int nmine0 = b < nchunk ? (nchunk - 1 - b) / G + 1 : 0;   // same count for colour 1
   const int nitems = 2 * nmine0;
@@ -807,7 +818,7 @@ __global__ void __launch_bounds__(128) k_apply_ldg(const LevelDev L, int colour,
   constexpr int NPK = M * (M + 1) / 2;
   const int64_t nec = L.ne >> 1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const uint64_t pol = evict_first_policy();
+  const uint64_t pol = stream_policy(L.l2keep);
   pdl_wait();
   pdl_trigger();
   double c1 = 0.0, c2 = 0.0;

@@ -48,6 +48,9 @@ struct LevelDev {
   int ox, oy, gnx, gny;    // this block's element offset in the global level and the global
                            // level's dims (0, 0, nx, ny on one GPU)
   int probe;               // measurement probe (MGDTN_PROBE=1: the apply streams S_T only)
+  float l2keep;            // fraction of this level's S_T / Dc stream loaded L2::evict_last
+                           // (kept resident across applies in the 126 MB L2); the rest
+                           // evict_first.  0: all evict_first
 };
 
 // global edge id of local edge e of a level block (power-iteration start vector)

@@ -148,6 +148,7 @@ static void init_level(HostLevel& L, int nx, int ny, int p, double h, int kind) 
   d.gnx = nx;
   d.gny = ny;
   d.probe = env_or("MGDTN_PROBE", 0);
+  d.l2keep = 0.0f;
   d.ndi = 4 * d.k1 * (d.k1 + 1) / 2;
   L.h = h;
   L.kind = kind;
@@ -363,6 +364,18 @@ static void plan_tail_dense(Ctx* c) {
   if (nf <= 0 || nf > 2048) return;
   c->nft = (int)nf;
   c->tail_dense = true;
+}
+
+// L2 residency of the finest operator (B200: 126 MB L2).  Every PCG iteration
+// streams the finest S_T ~5 times; MGDTN_L2KEEP_MB of it can be loaded evict_last
+// so it stays in L2 across applies (the rest streams evict_first).  Off by default:
+// at config 2 (110 MB S_T) 32 / 48 / 64 / 100 MB budgets changed the solve by
+// -1.2 / -0.3 / +2 / +3 % (profiles/r01_l2keep.jsonl).
+static void plan_l2(Ctx* c) {
+  const double budget = (double)env_or("MGDTN_L2KEEP_MB", 0) * 1048576.0;
+  LevelDev& d = c->lev[0].d;
+  const double bytes = (double)d.nchunk * 32 * 8 * (2.0 * d.npk);
+  d.l2keep = budget > 0 ? (float)std::min(1.0, budget / bytes) : 0.0f;
 }
 
 static void fill_tail(Ctx* c) {
@@ -1239,6 +1252,7 @@ int mg_build_hierarchy(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
   }
   plan_tail(c);
   plan_tail_dense(c);
+  plan_l2(c);
   layout(c);   // host only: no CUDA call until mg_bind_workspace
   *out_ctx = c;
   return MG_OK;
