@@ -46,10 +46,12 @@ def main():
                 flush.fill_(float(k))
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
+            torch.cuda.nvtx.range_push("probe")
             if a.op == "apply":
                 s.apply(lev, x, y)
             else:
                 s.smooth(lev, x, y, 1)
+            torch.cuda.nvtx.range_pop()
             e1.record(st)
             torch.cuda.synchronize()
             if k >= 3:
