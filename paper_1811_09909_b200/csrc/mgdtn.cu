@@ -27,7 +27,8 @@ struct HostLevel {
   int kind = KIND_COARSEST;
   double h = 0.0;
   size_t o_sync = 0, o_S = 0, o_Dinv = 0, o_Dc = 0, o_coef = 0, o_lam = 0, o_r = 0, o_e = 0, o_w = 0, o_d = 0;
-  size_t o_KIIinv = 0, o_Pm = 0, o_cbuf = 0;
+  size_t o_KIIinv = 0, o_Pm = 0, o_cbuf = 0, o_lpart = 0;
+  double* lpart = nullptr;   // per-level partial sums + 16 scalars (concurrent power iterations)
   double *KIIinv = nullptr, *Pm = nullptr, *cbuf = nullptr;
   double *r = nullptr, *e = nullptr, *w = nullptr, *dv = nullptr, *lam = nullptr;
 };
@@ -89,6 +90,11 @@ struct Ctx {
   HostLevel lgl;                   // this rank's block of level Lg (restriction / prolongation)
   size_t o_hs = 0, o_hr = 0, o_gall = 0, o_sden = 0, o_sall = 0, halo_doubles = 0;
   int comm_rc = 0;                 // first communicator failure (reported by the next sync point)
+  // setup: the levels' Chebyshev power iterations are independent and run on their
+  // own streams (fork / join with events on the ctx stream)
+  std::vector<cudaStream_t> side;
+  std::vector<cudaEvent_t> side_ev;
+  cudaEvent_t fork_ev = nullptr;
   double *hsend = nullptr, *hrecv = nullptr, *gall = nullptr, *sden = nullptr, *sall = nullptr;
 };
 
@@ -185,6 +191,7 @@ static void layout(Ctx* c) {
     L.o_Dinv = take((size_t)d.nedge * d.k1 * d.k1 * sizeof(double));
     L.o_Dc = take((size_t)d.nchunk * d.ndi * 32 * sizeof(double));
     L.o_coef = take(2 * MAX_NU * sizeof(double));
+    L.o_lpart = take((size_t)(c->npart + 16) * sizeof(double));
     L.o_lam = take(sizeof(double));
     L.o_r = take(d.ndof * sizeof(double));
     L.o_e = take(d.ndof * sizeof(double));
@@ -272,6 +279,7 @@ static void bind_pointers(Ctx* c) {
     L.d.Dinv = D(L.o_Dinv);
     L.d.Dc = D(L.o_Dc);
     L.d.coef = D(L.o_coef);
+    L.lpart = D(L.o_lpart);
     L.lam = D(L.o_lam);
     L.r = D(L.o_r);
     L.e = D(L.o_e);
@@ -672,6 +680,7 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
   }
   const int nlev = (int)c->lev.size();
   const int numax = MAX_NU;   // coefficients for any step count (mg_smooth may exceed nu)
+  std::vector<int> pow_levels;
   for (int li = 0; li < nlev - 1; ++li) {
     HostLevel& L = c->lev[li];
     L.d.smoother = c->sm.kind;
@@ -687,21 +696,50 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
       continue;
     }
     if (c->tail_lmax && li >= c->tail_start && c->tail_start >= 0) continue;   // k_tail_lmax below
-    // Chebyshev: lambda_max of D_B^-1 A_k by power iteration (Q11):
-    // v <- D^-1 A v in place (colour-1 epilogue AM_DINV), no per-step normalisation
-    c->launches += launch_pow_init(L.d, L.e, st);
+    pow_levels.push_back(li);
+  }
+  // Chebyshev: lambda_max of D_B^-1 A_k by power iteration (Q11), v <- D^-1 A v in
+  // place (colour-1 epilogue AM_DINV), no per-step normalisation.  The levels are
+  // independent: on one GPU each runs on its own stream with its own scratch
+  // (MGDTN_SETUP_STREAMS=0: in sequence on the ctx stream).
+  const bool fork = !partitioned(c) && pow_levels.size() > 1 && env_or("MGDTN_SETUP_STREAMS", 1) != 0;
+  if (fork) {
+    while (c->side.size() < pow_levels.size()) {
+      cudaStream_t sx;
+      cudaEvent_t ex;
+      CK(cudaStreamCreateWithFlags(&sx, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ex, cudaEventDisableTiming));
+      c->side.push_back(sx);
+      c->side_ev.push_back(ex);
+    }
+    if (!c->fork_ev) CK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(c->fork_ev, st));
+  }
+  for (size_t q = 0; q < pow_levels.size(); ++q) {
+    HostLevel& L = c->lev[pow_levels[q]];
+    double* part = fork ? L.lpart : c->part;
+    double* sc = fork ? L.lpart + c->npart : c->sscal;
+    if (fork) {
+      c->st = c->side[q];
+      CK(cudaStreamWaitEvent(c->st, c->fork_ev, 0));
+    }
+    c->launches += launch_pow_init(L.d, L.e, c->st);
     for (int it = 0; it < c->sm.lmax_iters; ++it) {
       const bool last = it + 1 == c->sm.lmax_iters;
-      apply_mode(c, L, AM_DINV, L.e, L.w, nullptr, nullptr, 0, last ? c->part : nullptr);
+      apply_mode(c, L, AM_DINV, L.e, L.w, nullptr, nullptr, 0, last ? part : nullptr);
     }
-    reduce_scal(c, c->part, apply_parts(L.d, AM_DINV), c->sscal, 7, 0);   // v.Dv
-    apply_full(c, L, L.e, L.w, c->part);
-    reduce_scal(c, c->part, apply_parts(L.d, AM_APPLY), c->sscal, 8, 0);  // v.Av
-    c->launches += launch_lmax_finish(c->sscal, c->sm.lmax_safety, c->sm.cheb_ratio, numax, L.lam,
-                                      L.d.coef, st);
+    reduce_scal(c, part, apply_parts(L.d, AM_DINV), sc, 7, 0);   // v.Dv
+    apply_full(c, L, L.e, L.w, part);
+    reduce_scal(c, part, apply_parts(L.d, AM_APPLY), sc, 8, 0);  // v.Av
+    c->launches += launch_lmax_finish(sc, c->sm.lmax_safety, c->sm.cheb_ratio, numax, L.lam,
+                                      L.d.coef, c->st);
+    if (fork) {
+      CK(cudaEventRecord(c->side_ev[q], c->st));
+      c->st = st;
+    }
   }
   if (c->sm.kind == MG_SMOOTH_CHEBYSHEV && c->tail_lmax && c->tail_start >= 0 &&
-      c->tail_start < nlev - 1) {
+      c->tail_start < nlev - 1) {   // (overlaps the forked power iterations)
     TailParams& T = c->tail;
     for (int k = 0; k < T.nlev; ++k) T.lev[k].d = c->lev[c->tail_start + k].d;
     c->launches += launch_tail_lmax(T, c->sm.lmax_iters, c->sm.lmax_safety, c->sm.cheb_ratio,
@@ -710,6 +748,21 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
   c->lev.back().d.smoother = c->sm.kind;
   c->launches += launch_coarse_assemble_factor(c->lev.back().d, c->fpos, c->nf, c->A1, c->A1inv,
                                                c->err, st);
+  // the tabulated tail needs only the tail levels (their coefficients come from
+  // k_tail_lmax / block-Jacobi on this stream): it also overlaps the forked iterations
+  auto tail_basis = [&]() {
+    TailParams& T = c->tail;
+    T.nu_pre = nu_at(c, c->sm.nu_pre, c->tail_start);
+    T.nu_post = nu_at(c, c->sm.nu_post, c->tail_start);
+    T.nu_doubling = c->sm.nu_doubling;
+    T.first_fused = 0;
+    for (int k = 0; k < T.nlev; ++k) T.lev[k].d = c->lev[c->tail_start + k].d;
+    c->launches += launch_tail_basis(T, c->tfidx, c->nft, c->Bt, st);
+  };
+  const bool basis_early = c->tail_dense && (c->tail_lmax || c->sm.kind == MG_SMOOTH_BLOCK_JACOBI);
+  if (basis_early) tail_basis();
+  if (fork)   // join
+    for (size_t q = 0; q < pow_levels.size(); ++q) CK(cudaStreamWaitEvent(st, c->side_ev[q], 0));
   CK(cudaGetLastError());
   // e / w / d vectors must hold 0 on dOmega: zero them once
   for (auto& L : c->lev) {
@@ -722,16 +775,8 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
     CK(cudaMemsetAsync(c->lgl.r, 0, c->lgl.d.ndof * sizeof(double), st));
     CK(cudaMemsetAsync(c->lgl.e, 0, c->lgl.d.ndof * sizeof(double), st));
   }
-  if (c->tail_dense) {
-    TailParams& T = c->tail;
-    T.nu_pre = nu_at(c, c->sm.nu_pre, c->tail_start);
-    T.nu_post = nu_at(c, c->sm.nu_post, c->tail_start);
-    T.nu_doubling = c->sm.nu_doubling;
-    T.first_fused = 0;
-    for (int k = 0; k < T.nlev; ++k) T.lev[k].d = c->lev[c->tail_start + k].d;
-    c->launches += launch_tail_basis(T, c->tfidx, c->nft, c->Bt, st);
-    CK(cudaGetLastError());
-  }
+  if (c->tail_dense && !basis_early) tail_basis();
+  CK(cudaGetLastError());
   RC(check_device_error(c));
   c->setup_done = true;
   return MG_OK;
@@ -1683,6 +1728,9 @@ void mg_destroy(void* ctx) {
   if (!c) return;
   drop_graphs(c);
   delete c->comm;
+  for (auto sx : c->side) cudaStreamDestroy(sx);
+  for (auto ex : c->side_ev) cudaEventDestroy(ex);
+  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->pinned) cudaFreeHost(c->pinned);
   delete c;
 }
