@@ -405,33 +405,71 @@ __device__ __forceinline__ double pk_get(const double* base, int m, int a, int b
   return base[(int64_t)pk_index(a, b, m) * 32];
 }
 
-__global__ void k_p_coarsen(LevelDev F, LevelDev C, const double* __restrict__ Jp) {
-  const int K1 = F.k1, m = F.m;
+// One thread per element; J_p is block diagonal (one [(p+1) x 2] block per edge),
+// so per row block f: T_f = S_{f,:} J_p (K1 x 8, from the packed rows of edge f),
+// then rows 2f, 2f+1 of J_p^T S J_p = J_f^T T_f.  Compile-time indices throughout.
+template <int P>
+__global__ void __launch_bounds__(128) k_p_coarsen(LevelDev F, LevelDev C,
+                                                   const double* __restrict__ Jp) {
+  constexpr int K1 = P + 1, M = 4 * K1;
+  double J[K1][2];
+#pragma unroll
+  for (int a = 0; a < K1; ++a) {
+    J[a][0] = Jp[a * 2];
+    J[a][1] = Jp[a * 2 + 1];
+  }
   const int64_t nec = F.ne >> 1;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < 2 * nec;
        t += (int64_t)gridDim.x * blockDim.x) {
-    int colour = (int)(t / nec);
-    int64_t s = t - colour * nec;
+    const int colour = (int)(t / nec);
+    const int64_t s = t - colour * nec;
     const double* src = F.S + s_offset(F.nchunk, F.npk, colour, s, 0);
     double* dst = C.S + s_offset(C.nchunk, C.npk, colour, s, 0);
-    for (int A = 0; A < 8; ++A)
-      for (int B = A; B < 8; ++B) {
-        int f = A >> 1, al = A & 1, g = B >> 1, be = B & 1;
-        double acc = 0.0;
-        for (int a = 0; a < K1; ++a) {
-          double inner = 0.0;
-          for (int b = 0; b < K1; ++b) inner += pk_get(src, m, f * K1 + a, g * K1 + b) * Jp[b * 2 + be];
-          acc += Jp[a * 2 + al] * inner;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      double T[K1][8];
+#pragma unroll
+      for (int a = 0; a < K1; ++a)
+#pragma unroll
+        for (int B = 0; B < 8; ++B) T[a][B] = 0.0;
+#pragma unroll
+      for (int a = 0; a < K1; ++a) {
+        const int r = f * K1 + a;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+#pragma unroll
+          for (int b = 0; b < K1; ++b) {
+            const int cidx = g * K1 + b;
+            const int lo = r < cidx ? r : cidx, hi = r < cidx ? cidx : r;
+            const double v = __ldg(src + (int64_t)(lo * (2 * M - lo + 1) / 2 + (hi - lo)) * 32);
+            T[a][2 * g] = fma(v, J[b][0], T[a][2 * g]);
+            T[a][2 * g + 1] = fma(v, J[b][1], T[a][2 * g + 1]);
+          }
         }
-        dst[(int64_t)pk_index(A, B, 8) * 32] = acc;
       }
+#pragma unroll
+      for (int al = 0; al < 2; ++al) {
+        const int A = 2 * f + al;
+#pragma unroll
+        for (int B = A; B < 8; ++B) {
+          double acc = 0.0;
+#pragma unroll
+          for (int a = 0; a < K1; ++a) acc = fma(J[a][al], T[a][B], acc);
+          dst[(int64_t)pk_index(A, B, 8) * 32] = acc;
+        }
+      }
+    }
   }
 }
 
 int launch_p_coarsen(const LevelDev& F, const LevelDev& C, const double* Jp, cudaStream_t st) {
   int64_t n = F.ne;
   int grid = (int)((n + 127) / 128 < 148 * 16 ? (n + 127) / 128 : 148 * 16);
-  k_p_coarsen<<<grid, 128, 0, st>>>(F, C, Jp);
+  switch (F.p) {
+    case 2: k_p_coarsen<2><<<grid, 128, 0, st>>>(F, C, Jp); break;
+    case 3: k_p_coarsen<3><<<grid, 128, 0, st>>>(F, C, Jp); break;
+    default: k_p_coarsen<4><<<grid, 128, 0, st>>>(F, C, Jp); break;
+  }
   return 1;
 }
 
