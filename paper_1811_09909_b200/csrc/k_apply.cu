@@ -1044,7 +1044,13 @@ static int fused_mode() {   // MGDTN_FUSED: 0 two launches (default), 1 grid bar
   if (v < 0) v = env_int("MGDTN_FUSED", 0);
   return v;
 }
-static bool use_fused() { return fused_mode() != 0 && apply_impl() == 2; }
+static bool use_fused() { return fused_mode() != 0 && apply_impl() != 1; }
+// mode 3: the grid-barrier variant on the P1 levels only (short, launch-bound passes)
+static bool fused_for(const LevelDev& L) {
+  const int m = fused_mode();
+  if (m == 3) return L.p == 1 && apply_impl() != 1;
+  return (m == 1 || m == 2) && apply_impl() == 2;
+}
 
 
 
@@ -1084,7 +1090,7 @@ static int fused_grid(const LevelDev& L) {
 }
 
 int apply2_grid(const LevelDev& L, int mode) {
-  if (!use_fused()) return apply_grid_mode(L, mode);
+  if (!fused_for(L) || L.sync == nullptr || L.imask != 0) return apply_grid_mode(L, mode);
   switch (L.p) {
     case 1: return fused_grid<1>(L);
     case 2: return fused_grid<2>(L);
@@ -1188,7 +1194,7 @@ int launch_apply(const LevelDev& L, int colour, int mode, const double* x, doubl
 
 int launch_apply2(const LevelDev& L, int mode, const double* x, double* y, const double* r,
                   double* d, int step, double* partials, bool pdl, cudaStream_t st) {
-  if (!use_fused() || L.sync == nullptr || L.imask != 0) {   // fused: single GPU only
+  if (!fused_for(L) || L.sync == nullptr || L.imask != 0) {   // fused: single GPU only
     int n = launch_apply(L, 0, AM_W0, x, y, nullptr, nullptr, 0, nullptr, pdl, st);
     return n + launch_apply(L, 1, mode, x, y, r, d, step, partials, pdl, st);
   }
