@@ -111,6 +111,8 @@ int mg_get_nccl_unique_id(uint8_t out[128]);
 /* Loopback communicator hub for nranks virtual ranks on one GPU (tests). */
 void* mg_loopback_create(int32_t nranks);
 void mg_loopback_destroy(void* hub);
+/* A virtual rank failed: every rank waiting in a loopback collective returns MG_ERR_NCCL. */
+void mg_loopback_abort(void* hub);
 
 /* Host-only partition plan (no device work; for checking the decomposition):
  * nlevels, the paper-numbered level of the first replicated level (0: none)

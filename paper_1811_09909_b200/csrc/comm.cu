@@ -142,18 +142,30 @@ struct LoopbackHub {
   std::vector<cudaEvent_t> ready, done;
   std::vector<double*> tmp;   // per-rank device scratch for all-reduce results
   std::vector<int> tmp_n;
-  void barrier() {
+  bool aborted = false;       // a rank failed: every barrier returns at once, ops report errors
+  bool barrier() {
     std::unique_lock<std::mutex> lk(m);
+    if (aborted) return false;
     const long long g = gen;
     if (++count == n) {
       count = 0;
       ++gen;
       cv.notify_all();
     } else {
-      cv.wait(lk, [&] { return gen != g; });
+      cv.wait(lk, [&] { return gen != g || aborted; });
     }
+    return !aborted;
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(m);
+    aborted = true;
+    cv.notify_all();
   }
 };
+
+void loopback_abort(LoopbackHub* h) {
+  if (h) h->abort();
+}
 
 LoopbackHub* loopback_create(int nranks) {
   LoopbackHub* h = new LoopbackHub();
@@ -199,6 +211,10 @@ __global__ void k_lb_sum(PtrList in, int nr, int n, double* out) {
 struct LoopbackComm : Comm {
   LoopbackHub* h = nullptr;
   int r = 0;
+  int fail_abort() {
+    err = "loopback: another rank aborted";
+    return -1;
+  }
   int rank() const override { return r; }
   int nranks() const override { return h->n; }
   // after every exchange: this rank's later work waits until every peer has
@@ -217,7 +233,7 @@ struct LoopbackComm : Comm {
     h->sendp[r] = send;
     h->stride[r] = stride;
     cudaEventRecord(h->ready[r], st);
-    h->barrier();
+    if (!h->barrier()) return fail_abort();
     for (int f = 0; f < 4; ++f) {
       const int q = nbr[f];
       if (q < 0 || count[f] == 0) continue;
@@ -227,7 +243,7 @@ struct LoopbackComm : Comm {
                       (size_t)count[f] * sizeof(double), cudaMemcpyDeviceToDevice, st);
     }
     cudaEventRecord(h->done[r], st);
-    h->barrier();
+    if (!h->barrier()) return fail_abort();
     wait_peers_done(st, false, nbr);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
   }
@@ -240,7 +256,7 @@ struct LoopbackComm : Comm {
     }
     h->sendp[r] = dev;
     cudaEventRecord(h->ready[r], st);
-    h->barrier();
+    if (!h->barrier()) return fail_abort();
     PtrList pl{};
     for (int q = 0; q < h->n; ++q) {
       pl.p[q] = h->sendp[q];
@@ -248,7 +264,7 @@ struct LoopbackComm : Comm {
     }
     k_lb_sum<<<1, 128, 0, st>>>(pl, h->n, n, h->tmp[r]);
     cudaEventRecord(h->done[r], st);
-    h->barrier();
+    if (!h->barrier()) return fail_abort();
     int none[4] = {-1, -1, -1, -1};
     wait_peers_done(st, true, none);
     cudaMemcpyAsync(dev, h->tmp[r], (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, st);
@@ -257,14 +273,14 @@ struct LoopbackComm : Comm {
   int allgather(const double* send, double* recv, size_t count, cudaStream_t st) override {
     h->sendp[r] = send;
     cudaEventRecord(h->ready[r], st);
-    h->barrier();
+    if (!h->barrier()) return fail_abort();
     for (int q = 0; q < h->n; ++q) {
       if (q != r) cudaStreamWaitEvent(st, h->ready[q], 0);
       cudaMemcpyAsync(recv + (size_t)q * count, h->sendp[q], count * sizeof(double),
                       cudaMemcpyDeviceToDevice, st);
     }
     cudaEventRecord(h->done[r], st);
-    h->barrier();
+    if (!h->barrier()) return fail_abort();
     int none[4] = {-1, -1, -1, -1};
     wait_peers_done(st, true, none);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;

@@ -45,6 +45,7 @@ int nccl_unique_id(uint8_t out[128], std::string& err);
 struct LoopbackHub;
 LoopbackHub* loopback_create(int nranks);
 void loopback_destroy(LoopbackHub* hub);
+void loopback_abort(LoopbackHub* hub);   // a rank failed: release every waiting rank
 Comm* make_loopback_comm(LoopbackHub* hub, int rank);
 
 }  // namespace mgdtn

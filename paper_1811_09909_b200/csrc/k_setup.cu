@@ -497,9 +497,13 @@ __constant__ int c_child_map[4][4] = {
 
 constexpr int AGG_WARPS = 4;
 
+// dense_out != nullptr: the coarse maps go to dense_out[M][8][8] (element-id order of
+// the coarse block; both triangles) instead of the packed chunk layout -- the gather
+// level's per-rank block, whose element count may be odd
 __global__ void __launch_bounds__(32 * AGG_WARPS) k_agglomerate(LevelDev F, LevelDev C,
                                                                 double* KIIinv, double* Pm,
-                                                                DevError* err) {
+                                                                DevError* err,
+                                                                double* dense_out) {
   __shared__ double smK[AGG_WARPS][16 * 16];
   __shared__ double smG[AGG_WARPS][8 * 16];
   __shared__ double smU[AGG_WARPS][8 * 16];
@@ -606,7 +610,16 @@ __global__ void __launch_bounds__(32 * AGG_WARPS) k_agglomerate(LevelDev F, Leve
     }
     __syncwarp();
     // S_c = Kr_CC + Kr_IC^T P_M, packed upper (36), into the coarse storage
-    {
+    if (dense_out) {
+      for (int kk = lane; kk < 36; kk += 32) {
+        int a, b;
+        pk_row_col(kk, 8, a, b);
+        double acc = Kr[(8 + a) * 16 + 8 + b];
+        for (int r = 0; r < 8; ++r) acc += Kr[r * 16 + 8 + a] * U[r * 16 + b];
+        dense_out[M * 64 + a * 8 + b] = acc;
+        dense_out[M * 64 + b * 8 + a] = acc;
+      }
+    } else {
       int colour;
       int64_t s;
       elem_slot(C.nx, I, J, colour, s);
@@ -624,11 +637,11 @@ __global__ void __launch_bounds__(32 * AGG_WARPS) k_agglomerate(LevelDev F, Leve
 }
 
 int launch_agglomerate(const LevelDev& F, const LevelDev& C, double* KIIinv, double* Pm,
-                       DevError* err, cudaStream_t st) {
+                       DevError* err, cudaStream_t st, double* dense_out) {
   int64_t nmac = (int64_t)(F.nx / 2) * (F.ny / 2);
   int64_t g = (nmac + AGG_WARPS - 1) / AGG_WARPS;
   int grid = (int)(g < 148 * 16 ? g : 148 * 16);
-  k_agglomerate<<<grid, 32 * AGG_WARPS, 0, st>>>(F, C, KIIinv, Pm, err);
+  k_agglomerate<<<grid, 32 * AGG_WARPS, 0, st>>>(F, C, KIIinv, Pm, err, dense_out);
   return 1;
 }
 

@@ -271,7 +271,7 @@ int launch_recover(const LevelDev& L, const RefDev& R, double h, const double* K
                    double* partials, int* grid_out, cudaStream_t st);
 int launch_p_coarsen(const LevelDev& F, const LevelDev& C, const double* Jp, cudaStream_t st);
 int launch_agglomerate(const LevelDev& F, const LevelDev& C, double* KIIinv, double* Pm,
-                       DevError* err, cudaStream_t st);
+                       DevError* err, cudaStream_t st, double* dense_out = nullptr);
 int launch_edge_blocks(const LevelDev& L, DevError* err, cudaStream_t st);
 int launch_dinv_pack(const LevelDev& L, cudaStream_t st);   // Dinv (SoA) -> Dc
 int launch_dense_to_packed(const LevelDev& L, const double* src, cudaStream_t st);

@@ -93,8 +93,7 @@ struct Ctx {
   // setup: the levels' Chebyshev power iterations are independent and run on their
   // own streams (fork / join with events on the ctx stream)
   std::vector<cudaStream_t> side;
-  std::vector<cudaEvent_t> side_ev;
-  cudaEvent_t fork_ev = nullptr;
+  std::vector<cudaEvent_t> side_ev, fork_evs;
   double *hsend = nullptr, *hrecv = nullptr, *gall = nullptr, *sden = nullptr, *sall = nullptr;
 };
 
@@ -216,8 +215,6 @@ static void layout(Ctx* c) {
   if (partitioned(c)) {
     HostLevel& G = c->lgl;
     const LevelDev& d = G.d;
-    G.o_sync = take((size_t)(2 + d.nchunk) * sizeof(unsigned));
-    G.o_S = take((size_t)2 * d.nchunk * d.npk * 32 * sizeof(double));
     G.o_r = take(d.ndof * sizeof(double));
     G.o_e = take(d.ndof * sizeof(double));
     size_t hd = 0;
@@ -259,9 +256,7 @@ static void bind_pointers(Ctx* c) {
     c->tfidx = reinterpret_cast<int*>(b + c->o_tfidx);
   }
   if (partitioned(c)) {
-    HostLevel& G = c->lgl;
-    G.d.sync = reinterpret_cast<unsigned*>(b + G.o_sync);
-    G.d.S = D(G.o_S);
+    HostLevel& G = c->lgl;   // vectors only (its coarse maps go straight to sden)
     G.r = D(G.o_r);
     G.e = D(G.o_e);
     c->hsend = D(c->o_hs);
@@ -661,67 +656,41 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
   CK(cudaMemcpyAsync(c->tauc, tau, ne * sizeof(double), cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(c->methc, method, ne * sizeof(int8_t), cudaMemcpyDeviceToDevice, st));
   c->launches += launch_local_dtn(F.d, c->refdev, F.h, c->Kc, c->methc, c->tauc, c->err, st);
-  for (size_t li = 0; li + 1 < c->lev.size(); ++li) {
-    HostLevel& L = c->lev[li];
-    HostLevel& C = c->lev[li + 1];
-    if (L.kind == KIND_P) {
-      c->launches += launch_p_coarsen(L.d, C.d, c->refdev.Jp, st);
-    } else if (gathers(c, (int)li)) {
-      // gather level: this rank's macros' coarse DtN maps, all-gathered into the
-      // replicated level (every rank then builds the coarser levels redundantly)
-      HostLevel& B = c->lgl;
-      c->launches += launch_agglomerate(L.d, B.d, L.KIIinv, L.Pm, c->err, st);
-      c->launches += launch_packed_to_dense(B.d, c->sden, st);
-      comm_fail(c, c->comm->allgather(c->sden, c->sall, (size_t)B.d.ne * 64, st));
-      c->launches += launch_gather_S(C.d, B.d.nx, B.d.ny, c->px, c->sall, st);
-    } else {
-      c->launches += launch_agglomerate(L.d, C.d, L.KIIinv, L.Pm, c->err, st);
-    }
-  }
   const int nlev = (int)c->lev.size();
   const int numax = MAX_NU;   // coefficients for any step count (mg_smooth may exceed nu)
-  std::vector<int> pow_levels;
-  for (int li = 0; li < nlev - 1; ++li) {
-    HostLevel& L = c->lev[li];
-    L.d.smoother = c->sm.kind;
-    c->launches += launch_edge_blocks(L.d, c->err, st);
-    if (L.d.imask) {   // interface edge blocks: D_e = D_own + D_remote, then inverted
-      c->launches += launch_eblk_pack(L.d, c->hsend, st);
-      halo_exchange(c, L.d, eblk_stride(L.d), L.d.k1 * L.d.k1);
-      c->launches += launch_eblk_finish(L.d, c->hrecv, c->err, st);
-    }
-    c->launches += launch_dinv_pack(L.d, st);
-    if (c->sm.kind == MG_SMOOTH_BLOCK_JACOBI) {
-      c->launches += launch_set_bj_coef(c->sm.omega, L.d.coef, st);
-      continue;
-    }
-    if (c->tail_lmax && li >= c->tail_start && c->tail_start >= 0) continue;   // k_tail_lmax below
-    pow_levels.push_back(li);
-  }
   // Chebyshev: lambda_max of D_B^-1 A_k by power iteration (Q11), v <- D^-1 A v in
-  // place (colour-1 epilogue AM_DINV), no per-step normalisation.  The levels are
-  // independent: on one GPU each runs on its own stream with its own scratch
-  // (MGDTN_SETUP_STREAMS=0: in sequence on the ctx stream).
-  const bool fork = !partitioned(c) && pow_levels.size() > 1 && env_or("MGDTN_SETUP_STREAMS", 1) != 0;
+  // place (colour-1 epilogue AM_DINV), no per-step normalisation.  A level's
+  // iteration needs only that level's operator and edge blocks: on one GPU it is
+  // forked onto its own stream (own scratch) as soon as they exist, so it overlaps
+  // the coarsening of the levels below (MGDTN_SETUP_STREAMS=0: in sequence).
+  const bool cheb = c->sm.kind == MG_SMOOTH_CHEBYSHEV;
+  const bool fork = cheb && !partitioned(c) && env_or("MGDTN_SETUP_STREAMS", 1) != 0;
+  auto is_pow = [&](int li) {
+    return cheb && li < nlev - 1 && !(c->tail_lmax && c->tail_start >= 0 && li >= c->tail_start);
+  };
+  int npow = 0;
+  for (int li = 0; li < nlev - 1; ++li) npow += is_pow(li) ? 1 : 0;
   if (fork) {
-    while (c->side.size() < pow_levels.size()) {
+    while ((int)c->side.size() < npow) {
       cudaStream_t sx;
-      cudaEvent_t ex;
+      cudaEvent_t ex, fx;
       CK(cudaStreamCreateWithFlags(&sx, cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&ex, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&fx, cudaEventDisableTiming));
       c->side.push_back(sx);
       c->side_ev.push_back(ex);
+      c->fork_evs.push_back(fx);
     }
-    if (!c->fork_ev) CK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
-    CK(cudaEventRecord(c->fork_ev, st));
   }
-  for (size_t q = 0; q < pow_levels.size(); ++q) {
-    HostLevel& L = c->lev[pow_levels[q]];
+  int q = 0;   // forked power iterations so far
+  auto power_iteration = [&](int li) -> int {
+    HostLevel& L = c->lev[li];
     double* part = fork ? L.lpart : c->part;
     double* sc = fork ? L.lpart + c->npart : c->sscal;
     if (fork) {
+      CK(cudaEventRecord(c->fork_evs[q], st));
       c->st = c->side[q];
-      CK(cudaStreamWaitEvent(c->st, c->fork_ev, 0));
+      CK(cudaStreamWaitEvent(c->st, c->fork_evs[q], 0));
     }
     c->launches += launch_pow_init(L.d, L.e, c->st);
     for (int it = 0; it < c->sm.lmax_iters; ++it) {
@@ -736,6 +705,39 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
     if (fork) {
       CK(cudaEventRecord(c->side_ev[q], c->st));
       c->st = st;
+    }
+    ++q;
+    return MG_OK;
+  };
+  for (int li = 0; li < nlev; ++li) {
+    HostLevel& L = c->lev[li];
+    // smoother setup of level li (its operator is complete on st)
+    if (li < nlev - 1) {
+      L.d.smoother = c->sm.kind;
+      c->launches += launch_edge_blocks(L.d, c->err, st);
+      if (L.d.imask) {   // interface edge blocks: D_e = D_own + D_remote, then inverted
+        c->launches += launch_eblk_pack(L.d, c->hsend, st);
+        halo_exchange(c, L.d, eblk_stride(L.d), L.d.k1 * L.d.k1);
+        c->launches += launch_eblk_finish(L.d, c->hrecv, c->err, st);
+      }
+      c->launches += launch_dinv_pack(L.d, st);
+      if (!cheb) c->launches += launch_set_bj_coef(c->sm.omega, L.d.coef, st);
+      if (is_pow(li)) RC(power_iteration(li));
+    }
+    if (li + 1 >= nlev) break;
+    // coarsening li -> li + 1
+    HostLevel& C = c->lev[li + 1];
+    if (L.kind == KIND_P) {
+      c->launches += launch_p_coarsen(L.d, C.d, c->refdev.Jp, st);
+    } else if (gathers(c, li)) {
+      // gather level: this rank's macros' coarse DtN maps, all-gathered into the
+      // replicated level (every rank then builds the coarser levels redundantly)
+      HostLevel& B = c->lgl;   // dense output: the block's element count may be odd
+      c->launches += launch_agglomerate(L.d, B.d, L.KIIinv, L.Pm, c->err, st, c->sden);
+      comm_fail(c, c->comm->allgather(c->sden, c->sall, (size_t)B.d.ne * 64, st));
+      c->launches += launch_gather_S(C.d, B.d.nx, B.d.ny, c->px, c->sall, st);
+    } else {
+      c->launches += launch_agglomerate(L.d, C.d, L.KIIinv, L.Pm, c->err, st);
     }
   }
   if (c->sm.kind == MG_SMOOTH_CHEBYSHEV && c->tail_lmax && c->tail_start >= 0 &&
@@ -762,7 +764,7 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
   const bool basis_early = c->tail_dense && (c->tail_lmax || c->sm.kind == MG_SMOOTH_BLOCK_JACOBI);
   if (basis_early) tail_basis();
   if (fork)   // join
-    for (size_t q = 0; q < pow_levels.size(); ++q) CK(cudaStreamWaitEvent(st, c->side_ev[q], 0));
+    for (int k = 0; k < q; ++k) CK(cudaStreamWaitEvent(st, c->side_ev[k], 0));
   CK(cudaGetLastError());
   // e / w / d vectors must hold 0 on dOmega: zero them once
   for (auto& L : c->lev) {
@@ -1352,6 +1354,7 @@ int mg_get_nccl_unique_id(uint8_t out[128]) {
 
 void* mg_loopback_create(int32_t nranks) { return nranks >= 1 ? loopback_create(nranks) : nullptr; }
 void mg_loopback_destroy(void* hub) { loopback_destroy(static_cast<LoopbackHub*>(hub)); }
+void mg_loopback_abort(void* hub) { loopback_abort(static_cast<LoopbackHub*>(hub)); }
 
 int mg_workspace_bytes(const void* ctx, size_t* bytes) {
   const Ctx* c = static_cast<const Ctx*>(ctx);
@@ -1730,7 +1733,7 @@ void mg_destroy(void* ctx) {
   delete c->comm;
   for (auto sx : c->side) cudaStreamDestroy(sx);
   for (auto ex : c->side_ev) cudaEventDestroy(ex);
-  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  for (auto ex : c->fork_evs) cudaEventDestroy(ex);
   if (c->pinned) cudaFreeHost(c->pinned);
   delete c;
 }

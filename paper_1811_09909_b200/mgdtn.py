@@ -86,6 +86,7 @@ _SIGS = {
     "mg_get_nccl_unique_id": [_P],
     "mg_loopback_create": [C.c_int32],
     "mg_loopback_destroy": [_P],
+    "mg_loopback_abort": [_P],
     "mg_last_error": [_P],
     "mg_last_error_index": [_P],
     "mg_destroy": [_P],
@@ -112,6 +113,7 @@ def load_library(path: str = LIB_PATH):
     lib.mg_destroy.restype = None
     lib.mg_loopback_create.restype = C.c_void_p
     lib.mg_loopback_destroy.restype = None
+    lib.mg_loopback_abort.restype = None
     _lib = lib
     return lib
 
@@ -191,6 +193,11 @@ class LoopbackHub:
         self.lib = load_library()
         self.handle = C.c_void_p(self.lib.mg_loopback_create(n))
         self.n = n
+
+    def abort(self):
+        """A rank failed: release the others from their collectives (they raise MGError)."""
+        if self.handle:
+            self.lib.mg_loopback_abort(self.handle)
 
     def close(self):
         if self.handle:

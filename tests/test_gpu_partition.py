@@ -37,7 +37,8 @@ def rel(a, b):
 
 
 # (config recipe, n, px, py, gather_ne): gather_ne small keeps several levels partitioned
-CASES = [(2, 32, 2, 1, 16), (2, 32, 2, 2, 0), (4, 32, 2, 2, 16), (3, 64, 1, 2, 64), (1, 16, 2, 2, 4)]
+CASES = [(2, 32, 2, 1, 16), (2, 32, 2, 2, 0), (4, 32, 2, 2, 16), (3, 64, 1, 2, 64), (1, 16, 2, 2, 4),
+         (2, 24, 2, 2, 0)]   # the last: odd (3 x 3) gather-level blocks
 
 
 def level_ids(plan, lev):
@@ -56,6 +57,13 @@ def run_ranks(cfg, pr, px, py, gather_ne, x_glob, r_glob):
     dev = torch.device("cuda", 0)
 
     def rank_main(rank):
+        try:
+            return rank_body(rank)
+        except Exception:
+            hub.abort()   # release the other ranks from their collectives
+            raise
+
+    def rank_body(rank):
         torch.cuda.set_device(dev)
         part = Partition(rank, N, px, py, gather_ne=gather_ne, loopback=hub)
         plan = partition_plan(n, n, p, part)
