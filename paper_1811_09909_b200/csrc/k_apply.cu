@@ -877,8 +877,20 @@ static int apply_impl() {
 }
 static bool use_ldg() { return apply_impl() == 1; }
 static bool mode_has_dinv(int mode) { return mode == AM_SMOOTH || mode == AM_DINV; }
-static bool use_seg(int mode) {
-  return apply_impl() == 3 || (apply_impl() == 0 && mode_has_dinv(mode));
+// MGDTN_SEG_PMASK: bit p set -> "auto" uses the segmented ring for EVERY pass at order p
+// (default bit 2: at p = 2 it beats the whole-chunk kernel for the plain passes too,
+// config 3 solve 4.37 -> 3.98 s; at p = 1, 3 and 4 it loses, profiles/r01_seg_pmask.jsonl)
+static int seg_pmask() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MGDTN_SEG_PMASK");
+    v = e ? std::atoi(e) : (1 << 2);
+  }
+  return v;
+}
+static bool use_seg(int mode, int p) {
+  return apply_impl() == 3 ||
+         (apply_impl() == 0 && (mode_has_dinv(mode) || ((seg_pmask() >> p) & 1)));
 }
 
 static int env_int(const char* name, int dflt) {
@@ -962,7 +974,7 @@ int apply_grid_mode(const LevelDev& L, int mode) {
     return (int)(g < gmax ? (g > 0 ? g : 1) : gmax);
   }
   const int64_t nchunk = (nec + 31) / 32;
-  if (use_seg(mode)) return balanced_grid(nchunk, (int64_t)num_sms() * seg_cps(L.p));
+  if (use_seg(mode, L.p)) return balanced_grid(nchunk, (int64_t)num_sms() * seg_cps(L.p));
   return balanced_grid(nchunk, 148 * tma_cps(L.p));
 }
 
@@ -1024,7 +1036,7 @@ static void launch_one(const LevelDev& L, int colour, const double* x, double* y
              partials, 0);
     return;
   }
-  if (use_seg(MODE)) {
+  if (use_seg(MODE, P)) {
     launch_seg<P, MODE, DOT>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
     return;
   }
