@@ -33,6 +33,7 @@ from .basis import gll_nodes
 
 BLOCK_JACOBI = 0
 CHEBYSHEV = 1
+LUSGS = 2       # symmetric block Gauss-Seidel on edge blocks, 4-colour order
 
 
 # --------------------------------------------------------------------------
@@ -160,6 +161,20 @@ class Level:
     def apply_D(self, v):
         k = self.k1
         return np.einsum("eab,eb->ea", self.D, v.reshape(-1, k)).reshape(-1)
+
+    # ---- 4-colour edge partition for LU-SGS (reading F3, DESIGN.md) ----
+    def colour_sets(self):
+        """[4] arrays of free-edge positions (into the free-edge list): colour 0/1 =
+        horizontal edges of even / odd rows j, colour 2/3 = vertical edges of even /
+        odd columns i.  An element's 4 edges have 4 different colours, so the edges
+        of one colour share no element: their blocks are mutually uncoupled."""
+        if getattr(self, "_colours", None) is None:
+            k = self.k1
+            edges = self.free[::k] // k
+            nh = self.n * (self.n + 1)
+            col = np.where(edges < nh, (edges // self.n) % 2, 2 + ((edges - nh) % (self.n + 1)) % 2)
+            self._colours = [np.nonzero(col == c)[0] for c in range(4)]
+        return self._colours
 
 
 def _block_inverse(A_II: sp.csr_matrix, blocks: np.ndarray) -> sp.csr_matrix:
@@ -299,6 +314,20 @@ class Hierarchy:
         if self.smoother == BLOCK_JACOBI:
             for _ in range(steps):
                 e = e + self.omega * L.apply_Dinv(r - A @ e)
+            return e
+        if self.smoother == LUSGS:
+            # LU-SGS (one forward and one backward Gauss-Seidel
+            # sweep) on edge blocks, in the 4-colour order: forward colours 0,1,2,3,
+            # backward 3,2,1,0; each colour's blocks update together (reading F3)
+            k = L.k1
+            sets = L.colour_sets()
+            for _ in range(steps):
+                for c in (0, 1, 2, 3, 3, 2, 1, 0):
+                    ed = sets[c]
+                    pos = (ed[:, None] * k + np.arange(k)[None, :]).reshape(-1)
+                    res = (r[pos] - A[pos] @ e).reshape(-1, k, 1)
+                    e = e.copy()
+                    e[pos] += self.omega * np.linalg.solve(L.D[ed], res).reshape(-1)
             return e
         # Chebyshev on D^-1 A over [b/ratio, b] (O8)
         b = L.lam_max

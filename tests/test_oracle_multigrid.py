@@ -301,3 +301,66 @@ def test_element_p_coarsening_sums_to_global_galerkin(p):
     assert np.abs(dense_e - glob.toarray()).max() <= 1e-12 * np.abs(dense_e).max()
     H = multigrid.Hierarchy(A[fr][:, fr], n, p, smoother=0)
     assert np.abs(H.levels[1].A.toarray() - dense_e).max() <= 1e-12 * np.abs(dense_e).max()
+
+
+# ------------------------------------------------ f3: LU-SGS in 4-colour order
+def _lusgs_hier(n, p):
+    ts = assembly.TraceSystem(n, p, np.ones(n * n), np.zeros(n * n, np.int8), np.ones(n * n), None, 1.0)
+    return ts, multigrid.Hierarchy(ts.A, n, p, smoother=multigrid.LUSGS, nu_pre=1, nu_post=1)
+
+
+@pytest.mark.parametrize("p", [1, 3])
+def test_lusgs_step_is_symmetric_block_gauss_seidel(p):
+    """One LU-SGS step equals the textbook symmetric block Gauss-Seidel on the
+    colour-ordered matrix, computed with dense solves of (D + L) and (D + U):
+    x_1/2 = x + (D+L)^-1 (r - A x), x_1 = x_1/2 + (D+U)^-1 (r - A x_1/2);
+    and the colour-diagonal blocks of A are exactly the edge blocks D (edges of
+    one colour share no element, PAPER.md:1061-1062 made parallel)."""
+    ts, H = _lusgs_hier(8, p)
+    L = H.levels[0]
+    k = L.k1
+    A = L.A.toarray()
+    sets = L.colour_sets()
+    order = np.concatenate([(ed[:, None] * k + np.arange(k)[None, :]).reshape(-1) for ed in sets])
+    Ap = A[np.ix_(order, order)]
+    sizes = [len(ed) * k for ed in sets]
+    cuts = np.cumsum([0] + sizes)
+    blk = np.zeros_like(Ap)
+    for c in range(4):
+        sl = slice(cuts[c], cuts[c + 1])
+        Acc = Ap[sl, sl]
+        Dcc = np.zeros_like(Acc)
+        for q, ed in enumerate(sets[c]):
+            Dcc[q * k:(q + 1) * k, q * k:(q + 1) * k] = L.D[ed]
+        assert np.array_equal(Acc, Dcc)
+        blk[sl, sl] = Acc
+    lower = np.tril(np.ones_like(Ap), -1) * 0
+    for c in range(4):
+        for c2 in range(c):
+            lower[cuts[c]:cuts[c + 1], cuts[c2]:cuts[c2 + 1]] = 1
+    DL = blk + Ap * lower
+    DU = blk + Ap * lower.T
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(len(order))
+    r = rng.standard_normal(len(order))
+    xh = x + np.linalg.solve(DL, r - Ap @ x)
+    x1 = xh + np.linalg.solve(DU, r - Ap @ xh)
+    inv = np.empty_like(order)
+    inv[order] = np.arange(len(order))
+    got = H.smooth(0, x[inv], r[inv], 1)
+    assert np.allclose(got, x1[inv], rtol=1e-12, atol=1e-12 * np.abs(x1).max())
+
+
+def test_lusgs_vcycle_symmetric_and_better_than_bj():
+    """The symmetric step keeps B_N symmetric (PCG-valid) and, as
+    in the paper's Example I tables (LU-SGS vs block-Jacobi),
+    needs fewer iterations than block-Jacobi at the same V(1,1)."""
+    ts, H = _lusgs_hier(16, 2)
+    rng = np.random.default_rng(6)
+    r1, r2 = rng.standard_normal((2, len(ts.free)))
+    a, b = H.vcycle(r1) @ r2, r1 @ H.vcycle(r2)
+    assert abs(a - b) <= 1e-12 * abs(a)
+    its = krylov.pcg(ts.A, H.vcycle, ts.g, rtol=1e-10)["iters"]
+    Hb = multigrid.Hierarchy(ts.A, 16, 2, smoother=multigrid.BLOCK_JACOBI, nu_pre=1, nu_post=1)
+    its_bj = krylov.pcg(ts.A, Hb.vcycle, ts.g, rtol=1e-10)["iters"]
+    assert its < its_bj, (its, its_bj)
