@@ -171,6 +171,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true")
+    ap.add_argument("--smoother", default="config", choices=["config", "bj", "cheb", "lusgs"],
+                    help="override the config's smoother (lusgs: SURVEY 8(f) f3)")
     args = ap.parse_args()
     _, world0, _ = _dist_env()
     if args.config == 0:
@@ -212,6 +214,8 @@ def main():
     if args.no_graphs:
         s.use_graphs(False)
     sm = smoother_from_config(cfg)
+    if args.smoother != "config":
+        sm.kind = {"bj": 0, "cheb": 1, "lusgs": 2}[args.smoother]
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     st = {}
 
@@ -333,7 +337,7 @@ def main():
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": cfg.name, "n": cfg.n, "p": cfg.p, "trace_dofs": cfg.trace_dofs,
-                       "smoother": "chebyshev" if cfg.smoother else "block-jacobi", "nu": cfg.nu,
+                       "smoother": ["block-jacobi", "chebyshev", "lu-sgs"][sm.kind], "nu": cfg.nu,
                        "rtol": cfg.rtol,
                        "parallelism": f"elem-blocks{part.px}x{part.py}" if part else "1gpu",
                        "l2": "256 MiB flush between steps (outside the per-step event window)",

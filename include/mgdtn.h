@@ -74,7 +74,11 @@ enum { MG_HDG = 0,      /* Eqs. HDG, HDG_flux */
 
 /* ---- smoothers ---- */
 enum { MG_SMOOTH_BLOCK_JACOBI = 0,  /* edge blocks, e += omega D_B^-1 (r - A e) */
-       MG_SMOOTH_CHEBYSHEV = 1 };   /* Chebyshev on D_B^-1 A over [lmax/ratio, lmax] */
+       MG_SMOOTH_CHEBYSHEV = 1,     /* Chebyshev on D_B^-1 A over [lmax/ratio, lmax] */
+       MG_SMOOTH_LUSGS = 2 };       /* LU-SGS on edge blocks: forward
+                                       block Gauss-Seidel over 4 edge colours (H even / odd
+                                       rows, V even / odd columns), then backward; one
+                                       "step" = both sweeps.  One GPU only. */
 
 /* Structured mesh of nx x ny squares of side h with lower-left corner (x0,y0).
  * nx and ny must be even and divisible by 2^(number of h-levels). */

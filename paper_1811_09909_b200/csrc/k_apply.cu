@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(32) k_apply_seg(const LevelDev L, int colour, 
                                                   double* __restrict__ partials, int early) {
   using C = SegCfg<P>;
   constexpr int K1 = C::K1, M = C::M, NPK = C::NPK, SEGR = C::SEGR, NSLOT = C::NSLOT;
-  constexpr bool HASD = (MODE == AM_SMOOTH || MODE == AM_DINV);   // D_e^-1 streamed too
+  constexpr bool HASD = (MODE == AM_SMOOTH || MODE == AM_DINV || MODE == AM_GSC);   // + D_e^-1
   constexpr int NS = C::NSEG_S + (HASD ? C::NSEG_D : 0);          // segments per chunk
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bars[NSLOT];
@@ -475,6 +475,8 @@ __global__ void __launch_bounds__(32) k_apply_seg(const LevelDev L, int colour, 
   if (MODE == AM_SMOOTH) {
     c1 = L.coef[2 * step];
     c2 = L.coef[2 * step + 1];
+  } else if (MODE == AM_GSC) {
+    c2 = L.coef[1];   // omega (block-Jacobi coefficients)
   }
   double dot = 0.0;
   for (int k = 0; k < nmine; ++k) {
@@ -492,13 +494,13 @@ __global__ void __launch_bounds__(32) k_apply_seg(const LevelDev L, int colour, 
       t[a] = 0.0;
       dd[a] = 0.0;
     }
+    int ei = 0, ej = 0;
     if (act) {   // every global read of the element, independent of the ring: overlaps the wait
-      int i, j;
-      slot_elem(L.nx, colour, s, i, j);
-      elem_edges(L.nx, L.ny, i, j, ed, bd, L.dmask);
-      itf = elem_itf(L.nx, L.ny, i, j, L.imask);
+      slot_elem(L.nx, colour, s, ei, ej);
+      elem_edges(L.nx, L.ny, ei, ej, ed, bd, L.dmask);
+      itf = elem_itf(L.nx, L.ny, ei, ej, L.imask);
       gather_x<K1>(x, ed, bd, xv);
-      epi_load<K1, MODE>(L, ed, bd, y, r, d, t, dd, itf);
+      epi_load<K1, MODE == AM_GSC ? AM_RESID : MODE>(L, ed, bd, y, r, d, t, dd, itf);
     }
     const int g0 = k * NS;
     const double* Sp = nullptr;
@@ -545,6 +547,7 @@ __global__ void __launch_bounds__(32) k_apply_seg(const LevelDev L, int colour, 
           for (int a = 0; a < K1; ++a) y[base + a] = yv[f * K1 + a];
           continue;
         }
+        if (MODE == AM_GSC && gs_colour(ei, ej, f) != step) continue;   // other colours: untouched
         double res[K1];
 #pragma unroll
         for (int a = 0; a < K1; ++a) {
@@ -563,6 +566,8 @@ __global__ void __launch_bounds__(32) k_apply_seg(const LevelDev L, int colour, 
           if (MODE == AM_DINV) {
             xo[base + a] = cc;
             if (DOT) dot = fma(cc, res[a], dot);
+          } else if (MODE == AM_GSC) {
+            xo[base + a] = fma(c2, cc, xv[f * K1 + a]);
           } else {
             double dn = c2 * cc;
             if (L.smoother == 1) {
@@ -876,7 +881,9 @@ static int apply_impl() {
   return v;
 }
 static bool use_ldg() { return apply_impl() == 1; }
-static bool mode_has_dinv(int mode) { return mode == AM_SMOOTH || mode == AM_DINV; }
+static bool mode_has_dinv(int mode) {
+  return mode == AM_SMOOTH || mode == AM_DINV || mode == AM_GSC;
+}
 // MGDTN_SEG_PMASK: bit p set -> "auto" uses the segmented ring for EVERY pass at order p
 // (default bit 2: at p = 2 it beats the whole-chunk kernel for the plain passes too,
 // config 3 solve 4.37 -> 3.98 s; at p = 1, 3 and 4 it loses, profiles/r01_seg_pmask.jsonl)
@@ -1031,6 +1038,10 @@ template <int P, int MODE, bool DOT>
 static void launch_one(const LevelDev& L, int colour, const double* x, double* y, const double* r,
                        double* d, int step, double* partials, int grid, bool pdl,
                        cudaStream_t st) {
+  if (MODE == AM_GSC) {   // colour sweeps exist in the segmented-ring kernel only
+    launch_seg<P, AM_GSC, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
+    return;
+  }
   if (use_ldg()) {
     launch_ex(k_apply_ldg<P, MODE, DOT>, grid, 128, 0, pdl, st, L, colour, x, y, r, d, step,
              partials, 0);
@@ -1102,7 +1113,8 @@ static int fused_grid(const LevelDev& L) {
 }
 
 int apply2_grid(const LevelDev& L, int mode) {
-  if (!fused_for(L) || L.sync == nullptr || L.imask != 0) return apply_grid_mode(L, mode);
+  if (!fused_for(L) || L.sync == nullptr || L.imask != 0 || mode == AM_GSC)
+    return apply_grid_mode(L, mode);
   switch (L.p) {
     case 1: return fused_grid<1>(L);
     case 2: return fused_grid<2>(L);
@@ -1185,6 +1197,9 @@ static void dispatch_apply(const LevelDev& L, int colour, int mode, const double
       else
         launch_one<P, AM_DINV, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
       break;
+    case AM_GSC:
+      launch_one<P, AM_GSC, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
+      break;
     default:
       launch_one<P, AM_SMOOTH, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
       break;
@@ -1206,7 +1221,7 @@ int launch_apply(const LevelDev& L, int colour, int mode, const double* x, doubl
 
 int launch_apply2(const LevelDev& L, int mode, const double* x, double* y, const double* r,
                   double* d, int step, double* partials, bool pdl, cudaStream_t st) {
-  if (!fused_for(L) || L.sync == nullptr || L.imask != 0) {   // fused: single GPU only
+  if (!fused_for(L) || L.sync == nullptr || L.imask != 0 || mode == AM_GSC) {   // fused: 1 GPU
     int n = launch_apply(L, 0, AM_W0, x, y, nullptr, nullptr, 0, nullptr, pdl, st);
     return n + launch_apply(L, 1, mode, x, y, r, d, step, partials, pdl, st);
   }

@@ -24,8 +24,17 @@ enum ApplyMode : int {
   AM_APPLY = 1,   // pass 1: y[e] += (S_T x_T)[e]  (+ optional dot x.y)
   AM_RESID = 2,   // pass 1: w[e] = r[e] - (w[e] + (S_T x_T)[e])
   AM_SMOOTH = 3,  // pass 1: d = c1 d + c2 Dinv (r - A x)_e ; x[e] += d  (in place)
-  AM_DINV = 4     // pass 1: y[e] = (A x)_e ; x[e] = Dinv (A x)_e (in place; power iteration)
+  AM_DINV = 4,    // pass 1: y[e] = (A x)_e ; x[e] = Dinv (A x)_e (in place; power iteration)
+  AM_GSC = 5      // pass 1, LU-SGS colour sweep: on edges of colour `step` only,
+                  // x[e] += omega Dinv (r - A x)_e (in place; segmented-ring kernel only)
 };
+
+// LU-SGS colour of local edge f of element (i,j): horizontal edges of even / odd
+// rows 0 / 1, vertical edges of even / odd columns 2 / 3 (an element's four edges
+// have four different colours, so one colour's edges share no element)
+__host__ __device__ __forceinline__ int gs_colour(int i, int j, int f) {
+  return f == 0 ? (j & 1) : f == 2 ? ((j + 1) & 1) : f == 3 ? 2 + (i & 1) : 2 + ((i + 1) & 1);
+}
 
 struct LevelDev {
   int nx, ny, p, k1, m, npk;

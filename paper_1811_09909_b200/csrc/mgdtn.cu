@@ -535,6 +535,13 @@ static inline void apply_full(Ctx* c, const HostLevel& L, const double* x, doubl
 }
 
 static inline void smooth_step(Ctx* c, HostLevel& L, int step) {
+  if (c->sm.kind == MG_SMOOTH_LUSGS) {
+    // one LU-SGS step: forward block Gauss-Seidel sweep over the
+    // four edge colours, then backward (oracle/multigrid.py)
+    static const int order[8] = {0, 1, 2, 3, 3, 2, 1, 0};
+    for (int q = 0; q < 8; ++q) apply_mode(c, L, AM_GSC, L.e, L.w, L.r, nullptr, order[q], nullptr);
+    return;
+  }
   // coefficient slot clamped to MAX_NU-1: only block-Jacobi (step-invariant
   // coefficients) may run more steps than that (beta-doubling)
   apply_mode(c, L, AM_SMOOTH, L.e, L.w, L.r, L.dv, step < MAX_NU ? step : MAX_NU - 1, nullptr);
@@ -609,11 +616,12 @@ static void prolong_level(Ctx* c, int li, const double* ec, double* e) {
 static void vcycle_level(Ctx* c, int li, bool first_done) {
   HostLevel& L = c->lev[li];
   const int nlev = (int)c->lev.size();
-  if (c->tail_dense && li == c->tail_start) {   // this level and every coarser one: e = B_tail r
+  const bool tail_ok = c->sm.kind != MG_SMOOTH_LUSGS;   // the tail kernels have no LU-SGS
+  if (tail_ok && c->tail_dense && li == c->tail_start) {   // this level and every coarser one: e = B_tail r
     c->launches += launch_tail_dense(c->tfidx, c->nft, c->Bt, L.r, L.e, c->st);
     return;
   }
-  if (c->tail_vcycle && li == c->tail_start) {   // this level and every coarser one: one launch
+  if (tail_ok && c->tail_vcycle && li == c->tail_start) {   // this level and every coarser one: one launch
     TailParams& T = c->tail;
     T.nu_pre = nu_at(c, c->sm.nu_pre, li);
     T.nu_post = nu_at(c, c->sm.nu_post, li);
@@ -629,7 +637,7 @@ static void vcycle_level(Ctx* c, int li, bool first_done) {
   }
   const int nu_pre = nu_at(c, c->sm.nu_pre, li), nu_post = nu_at(c, c->sm.nu_post, li);
   int s0 = 0;
-  if (nu_pre > 0) {
+  if (nu_pre > 0 && c->sm.kind != MG_SMOOTH_LUSGS) {
     if (!first_done) c->launches += launch_smooth_first(L.d, L.r, L.e, L.dv, c->st);
     s0 = 1;
   } else {
@@ -639,6 +647,7 @@ static void vcycle_level(Ctx* c, int li, bool first_done) {
   residual(c, L);  // L.w = r - A e1
   HostLevel& C = c->lev[li + 1];
   const bool fuse = (li + 1 < nlev - 1) && nu_at(c, c->sm.nu_pre, li + 1) > 0 &&
+                    c->sm.kind != MG_SMOOTH_LUSGS &&
                     !(c->tail_dense && li + 1 == c->tail_start) && !gathers(c, li);
   restrict_level(c, li, L.w, L.e, true, C.r, fuse);
   vcycle_level(c, li + 1, fuse);
@@ -761,7 +770,8 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
     for (int k = 0; k < T.nlev; ++k) T.lev[k].d = c->lev[c->tail_start + k].d;
     c->launches += launch_tail_basis(T, c->tfidx, c->nft, c->Bt, st);
   };
-  const bool basis_early = c->tail_dense && (c->tail_lmax || c->sm.kind == MG_SMOOTH_BLOCK_JACOBI);
+  const bool use_basis = c->tail_dense && c->sm.kind != MG_SMOOTH_LUSGS;
+  const bool basis_early = use_basis && (c->tail_lmax || c->sm.kind == MG_SMOOTH_BLOCK_JACOBI);
   if (basis_early) tail_basis();
   if (fork)   // join
     for (int k = 0; k < q; ++k) CK(cudaStreamWaitEvent(st, c->side_ev[k], 0));
@@ -777,7 +787,7 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
     CK(cudaMemsetAsync(c->lgl.r, 0, c->lgl.d.ndof * sizeof(double), st));
     CK(cudaMemsetAsync(c->lgl.e, 0, c->lgl.d.ndof * sizeof(double), st));
   }
-  if (c->tail_dense && !basis_early) tail_basis();
+  if (use_basis && !basis_early) tail_basis();
   CK(cudaGetLastError());
   RC(check_device_error(c));
   c->setup_done = true;
@@ -1387,16 +1397,19 @@ int mg_setup_dtn(void* ctx, const double* K, const int8_t* method, const double*
   if (!c->ws) return fail(c, MG_ERR_WORKSPACE, "no workspace bound");
   if (!K || !method || !tau || !smoother) return fail(c, MG_ERR_ARG, "NULL argument");
   mg_smoother_cfg sm = *smoother;
-  if (sm.kind != MG_SMOOTH_BLOCK_JACOBI && sm.kind != MG_SMOOTH_CHEBYSHEV)
+  if (sm.kind != MG_SMOOTH_BLOCK_JACOBI && sm.kind != MG_SMOOTH_CHEBYSHEV &&
+      sm.kind != MG_SMOOTH_LUSGS)
     return fail(c, MG_ERR_ARG, "unknown smoother kind");
+  if (sm.kind == MG_SMOOTH_LUSGS && partitioned(c))
+    return fail(c, MG_ERR_UNSUPPORTED, "LU-SGS on a partitioned context");
   if (sm.nu_pre < 0 || sm.nu_post < 0 || sm.nu_pre > MAX_NU || sm.nu_post > MAX_NU)
     return fail(c, MG_ERR_ARG, "nu out of range (0..8)");
   if (!(sm.omega > 0)) sm.omega = 1.0;
   if (!(sm.cheb_ratio > 1)) sm.cheb_ratio = 30.0;
   if (sm.lmax_iters <= 0) sm.lmax_iters = 20;
   if (!(sm.lmax_safety > 0)) sm.lmax_safety = 1.05;
-  if (sm.nu_doubling && sm.kind != MG_SMOOTH_BLOCK_JACOBI)
-    return fail(c, MG_ERR_ARG, "nu_doubling needs the block-Jacobi smoother");
+  if (sm.nu_doubling && sm.kind == MG_SMOOTH_CHEBYSHEV)
+    return fail(c, MG_ERR_ARG, "nu_doubling needs block-Jacobi or LU-SGS");
   if (sm.nu_pre != c->sm.nu_pre || sm.nu_post != c->sm.nu_post || sm.kind != c->sm.kind ||
       sm.nu_doubling != c->sm.nu_doubling)
     drop_graphs(c);

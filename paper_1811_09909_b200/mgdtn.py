@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libmgdtn.so")
 
 MG_OK = 0
 MG_HDG, MG_SIPG_H = 0, 1
-MG_SMOOTH_BLOCK_JACOBI, MG_SMOOTH_CHEBYSHEV = 0, 1
+MG_SMOOTH_BLOCK_JACOBI, MG_SMOOTH_CHEBYSHEV, MG_SMOOTH_LUSGS = 0, 1, 2
 STATUS = {0: "converged", 1: "maxit", 2: "diverged", 3: "breakdown"}
 ERRORS = {-1: "MG_ERR_ARG", -2: "MG_ERR_SHAPE", -3: "MG_ERR_SINGULAR_LOCAL", -4: "MG_ERR_NOT_SPD",
           -5: "MG_ERR_CUDA", -6: "MG_ERR_NCCL", -7: "MG_ERR_STATE", -8: "MG_ERR_WORKSPACE",
