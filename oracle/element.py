@@ -32,6 +32,9 @@ from .basis import gauss, gll_nodes, lagrange, lagrange_deriv
 
 HDG = 0
 SIPG_H = 1
+IIPG_H = 2      # s_f = 0  (Eq. IPG_H)
+NIPG_H = 3      # s_f = -1
+S_F = {SIPG_H: 1.0, IIPG_H: 0.0, NIPG_H: -1.0}
 
 # outward unit normals of the local edges {bottom, right, top, left}
 NORMALS = np.array([[0.0, -1.0], [1.0, 0.0], [0.0, 1.0], [-1.0, 0.0]])
@@ -154,29 +157,47 @@ def _local_systems_hdg(R: RefElement, K: np.ndarray, tau: np.ndarray, h: float):
     return Z, Y, Bf, tH
 
 
-def _local_systems_sipg(R: RefElement, K: np.ndarray, tau: np.ndarray, h: float):
-    """SIPG-H local system (Eq. SIPG_H, s_f = 1) per element.
+def _local_systems_ipdg(R: RefElement, K: np.ndarray, tau: np.ndarray, h: float,
+                        s_f: float = 1.0):
+    """Hybridized IPDG local system (Eq. IPG_H, PAPER.md:238-247) per element;
+    s_f = 1 SIPG-H (Eq. SIPG_H), 0 IIPG-H, -1 NIPG-H.
 
-    (K grad q, grad w) - <q - lambda, K grad w.n> - <K grad q.n, w>
+    (K grad q, grad w) - s_f <q - lambda, K grad w.n> - <K grad q.n, w>
         + <tau (q - lambda), w> = (f, w)
     flux (Eq. IPDG_flux): u_hat.n = -K grad q.n + tau (q - lambda).
+    With N_ij = <grad phi_j.n, phi_i>, Nl_(i,(f,a)) = <mu_a, grad phi_i.n_f>:
+    <K grad q.n, w_i> = K (N q)_i,  s_f <q, K grad w_i.n> = s_f K (N^T q)_i,
+    s_f <lambda, K grad w_i.n> = s_f K (Nl lambda)_i.
     Physical: L = Lhat, N = Nhat, Nl = Nlhat, F = h Fhat, E = h Ehat.
     """
     Kb = K[:, None, None]
     t = tau[:, None, None]
     L, N, Nl = R.L, R.N, R.Nl
     F, E, H = h * R.F, h * R.E, h * R.H
-    Z = Kb * (L - N.T - N) + t * F
-    Y = t * E - Kb * Nl
+    Z = Kb * (L - s_f * N.T - N) + t * F
+    Y = t * E - s_f * Kb * Nl
     Bf = -Kb * Nl.T + t * E.T
     tH = t * H
     return Z, Y, Bf, tH
 
 
+def _local_systems_sipg(R, K, tau, h):
+    return _local_systems_ipdg(R, K, tau, h, S_F[SIPG_H])
+
+
+def _builders():
+    """(method code, local-system builder) for every hybridized scheme."""
+    out = [(HDG, _local_systems_hdg)]
+    for code, sf in S_F.items():
+        out.append((code, lambda R, K, tau, h, sf=sf: _local_systems_ipdg(R, K, tau, h, sf)))
+    return out
+
+
 def element_dtn(p: int, K, method, tau, h: float, chunk: int = 2048):
     """Element DtN maps S_T [ne, m, m] (Schur complement of the local solve).
 
-    S_T = tau H - Bf Z^{-1} Y  (= -d flux_T / d lambda), per element.
+    S_T = tau H - Bf Z^{-1} Y  (= -d flux_T / d lambda), per element.  Row a
+    is the flux moment on local dof a; nonsymmetric for IIPG-H / NIPG-H.
     """
     R = ref(p)
     K = np.asarray(K, float)
@@ -184,7 +205,7 @@ def element_dtn(p: int, K, method, tau, h: float, chunk: int = 2048):
     method = np.asarray(method)
     ne = len(K)
     S = np.empty((ne, R.m, R.m))
-    for mcode, builder in ((HDG, _local_systems_hdg), (SIPG_H, _local_systems_sipg)):
+    for mcode, builder in _builders():
         idx = np.nonzero(method == mcode)[0]
         for s in range(0, len(idx), chunk):
             ids = idx[s:s + chunk]
@@ -214,7 +235,7 @@ def element_rhs(p: int, K, method, tau, h: float, f_qp=None, f_const=0.0,
         fw = load_vectors(p, h, f_qp)
     b = np.empty((ne, R.m))
     nv = R.nv
-    for mcode, builder in ((HDG, _local_systems_hdg), (SIPG_H, _local_systems_sipg)):
+    for mcode, builder in _builders():
         idx = np.nonzero(method == mcode)[0]
         for s in range(0, len(idx), chunk):
             ids = idx[s:s + chunk]
@@ -243,7 +264,7 @@ def recover_q(p: int, K, method, tau, h: float, lam_T, f_qp=None, f_const=0.0):
     else:
         fw = load_vectors(p, h, f_qp)
     q = np.empty((ne, nv))
-    for mcode, builder in ((HDG, _local_systems_hdg), (SIPG_H, _local_systems_sipg)):
+    for mcode, builder in _builders():
         idx = np.nonzero(method == mcode)[0]
         if len(idx) == 0:
             continue

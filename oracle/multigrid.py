@@ -256,7 +256,18 @@ class Hierarchy:
         self.levels = levels                 # levels[0] = finest (k = N)
         coarsest = levels[-1]
         self.A1_dense = coarsest.A.toarray()
-        self.A1_chol = None if all_free else sla.cho_factor(self.A1_dense, lower=True)
+        # A_N nonsymmetric (IIPG-H / NIPG-H elements): every level is (the
+        # Galerkin Q A I of a nonsymmetric A); B_1 = A_1^-1 by LU instead of Cholesky
+        dA = A_N - A_N.T
+        self.symmetric = (abs(dA).max() if dA.nnz else 0.0) <= 1e-13 * abs(A_N).max()
+        self.A1_chol = self.A1_lu = None
+        if not all_free:
+            if self.symmetric:
+                self.A1_chol = sla.cho_factor(self.A1_dense, lower=True)
+            else:
+                self.A1_lu = sla.lu_factor(self.A1_dense)
+        if smoother == CHEBYSHEV and not self.symmetric:
+            raise ValueError("Chebyshev needs a symmetric A (real spectrum of D^-1 A)")
         for L in levels[:-1]:
             L.build_edge_blocks()
             if smoother == CHEBYSHEV:
@@ -304,6 +315,8 @@ class Hierarchy:
         return e
 
     def coarse_solve(self, r):
+        if self.A1_lu is not None:
+            return sla.lu_solve(self.A1_lu, r)
         return sla.cho_solve(self.A1_chol, r)
 
     # ---- smoothers G_{k,m} ----

