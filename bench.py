@@ -173,6 +173,10 @@ def main():
     ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--smoother", default="config", choices=["config", "bj", "cheb", "lusgs"],
                     help="override the config's smoother (lusgs: SURVEY 8(f) f3)")
+    ap.add_argument("--scheme", default="config", choices=["config", "nipg", "iipg", "tiles"],
+                    help="SURVEY 8(f) f2: the config's recipe with IIPG-H / NIPG-H elements "
+                         "(workloads.nonsymmetric_problem), a MG_BUILD_NONSYMMETRIC context, "
+                         "block-Jacobi and left-preconditioned GMRES (one GPU)")
     args = ap.parse_args()
     _, world0, _ = _dist_env()
     if args.config == 0:
@@ -180,6 +184,9 @@ def main():
     cfg = W.CONFIGS[args.config]
     if args.impl == "reference":
         return reference_arm(args, cfg)
+    ns = args.scheme != "config"
+    if ns and world0 > 1:
+        ap.error("--scheme nipg / iipg / tiles runs on one GPU")
 
     import torch
     import torch.distributed as dist
@@ -200,7 +207,7 @@ def main():
         part = Partition(rank, world, px, py, nccl_id=obj[0])
 
     # ---- inputs resident in HBM (N > 1: this rank's element block of the one problem)
-    pr = W.make_problem(cfg)
+    pr = W.nonsymmetric_problem(cfg, args.scheme) if ns else W.make_problem(cfg)
     if part is not None:
         pr = W.block_problem(pr, part.px, part.py, rank)
     K = torch.from_numpy(pr.K).to(dev)
@@ -210,19 +217,26 @@ def main():
     gD = None if pr.gD_qp is None else torch.from_numpy(pr.gD_qp).to(dev)
     stream = torch.cuda.Stream(dev)
     with torch.cuda.stream(stream):
-        s = MGSolver(cfg.n, p=cfg.p, device=dev, stream=stream, partition=part)
+        s = MGSolver(cfg.n, p=cfg.p, device=dev, stream=stream, partition=part, nonsymmetric=ns)
     if args.no_graphs:
         s.use_graphs(False)
     sm = smoother_from_config(cfg)
     if args.smoother != "config":
         sm.kind = {"bj": 0, "cheb": 1, "lusgs": 2}[args.smoother]
+    if ns:
+        sm.kind = 0   # block-Jacobi: Chebyshev needs a real spectrum, PCG a symmetric A
+
+    def solve(g):
+        if ns:
+            return s.gmres_solve(g, tol=cfg.rtol, maxit=400)
+        return s.pcg_solve(g, rtol=cfg.rtol, maxit=4000)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     st = {}
 
     def step():
         s.setup(K, meth, tau, sm)
         g, lam_bc = s.assemble_rhs(fq, pr.f_const, gD)
-        lam, info = s.pcg_solve(g, rtol=cfg.rtol, maxit=4000)
+        lam, info = solve(g)
         st["info"] = info
         return lam
 
@@ -273,16 +287,16 @@ def main():
             return tot / reps
         t_setup = timed(lambda: s.setup(K, meth, tau, sm), 3)
         g, _ = s.assemble_rhs(fq, pr.f_const, gD)
-        t_solve = timed(lambda: s.pcg_solve(g, rtol=cfg.rtol, maxit=4000), 3)
+        t_solve = timed(lambda: solve(g), 3)
         x = torch.rand(s.ndof(), dtype=torch.float64, device=dev)
         y = torch.empty_like(x)
         N = s.nlevels
         t_apply = timed(lambda: s.apply(N, x, y), 20, warm=3)
     ne = cfg.n * cfg.n // world      # this rank's elements
     m = 4 * (cfg.p + 1)
-    npk = m * (m + 1) // 2
+    npk = m * m if ns else m * (m + 1) // 2
     ndof = s.ndof()
-    alg_bytes = ne * 8 * npk + 16 * ndof           # packed S_T + x read + y write
+    alg_bytes = ne * 8 * npk + 16 * ndof           # packed (ns: full) S_T + x + y
     peaks = _peaks()
     peak = peaks.get("hbm_gbs", 6650.0)
     achieved = alg_bytes / (t_apply * 1e-3) / 1e9
@@ -294,7 +308,37 @@ def main():
     # ---- end to end through the C ABI with HOST buffers (h2d inputs, d2h solution);
     # collective on a partition (every rank solves its block), rank 0 reports
     e2e = None
-    if True:
+    if ns:   # no mg_solve_host for GMRES: the same public calls with the copies in the region
+        Kh = torch.from_numpy(pr.K).pin_memory()
+        mh = torch.from_numpy(pr.method).pin_memory()
+        th = torch.from_numpy(pr.tau).pin_memory()
+        fh = None if pr.f_qp is None else torch.from_numpy(pr.f_qp).pin_memory()
+        gh = None if pr.gD_qp is None else torch.from_numpy(pr.gD_qp).pin_memory()
+        out = torch.empty(ndof, dtype=torch.float64).pin_memory()
+
+        def host_step():
+            Kd, md, td = (Kh.to(dev, non_blocking=True), mh.to(dev, non_blocking=True),
+                          th.to(dev, non_blocking=True))
+            fd = None if fh is None else fh.to(dev, non_blocking=True)
+            gd = None if gh is None else gh.to(dev, non_blocking=True)
+            s.setup(Kd, md, td, sm)
+            g2, lbc = s.assemble_rhs(fd, pr.f_const, gd)
+            lam2, _ = solve(g2)
+            out.copy_(lam2 + lbc, non_blocking=True)
+            torch.cuda.synchronize(dev)
+        with torch.cuda.stream(stream):
+            host_step()
+            te = []
+            for _ in range(max(1, min(args.steps, 3))):
+                flush.fill_(2.0)
+                torch.cuda.synchronize(dev)
+                t0 = time.perf_counter()
+                host_step()
+                te.append(time.perf_counter() - t0)
+        h2d = 8 * ne * 2 + ne + (0 if fh is None else 8 * fh.numel()) + (0 if gh is None else 8 * gh.numel())
+        e2e = {"value": cfg.trace_dofs / float(np.mean(te)), "unit": "trace DoF/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * ndof)}
+    else:
         Kh = torch.from_numpy(pr.K).pin_memory()
         mh = torch.from_numpy(pr.method).pin_memory()
         th = torch.from_numpy(pr.tau).pin_memory()
@@ -321,7 +365,7 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * ndof)}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not ns:
         ns = oracle_sample_n(cfg, 30.0)
         sc = W.scaled_config(cfg.index, ns) if ns != cfg.n else cfg
         t, its = run_oracle_step(sc)
@@ -331,24 +375,28 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": "fine trace DoFs/s in MG-PCG solve to 1e-10", "value": value, "unit": "trace DoF/s",
+            "metric": ("fine trace DoFs/s in MG-GMRES solve to 1e-10" if ns
+                       else "fine trace DoFs/s in MG-PCG solve to 1e-10"),
+            "value": value, "unit": "trace DoF/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": cfg.name, "n": cfg.n, "p": cfg.p, "trace_dofs": cfg.trace_dofs,
+            "config": {"workload": cfg.name + ("" if not ns else f"+{args.scheme}"),
+                       "n": cfg.n, "p": cfg.p, "trace_dofs": cfg.trace_dofs,
                        "smoother": ["block-jacobi", "chebyshev", "lu-sgs"][sm.kind], "nu": cfg.nu,
                        "rtol": cfg.rtol,
                        "parallelism": f"elem-blocks{part.px}x{part.py}" if part else "1gpu",
                        "l2": "256 MiB flush between steps (outside the per-step event window)",
-                       "step": "setup_dtn + assemble_rhs + pcg_solve"},
+                       "step": "setup_dtn + assemble_rhs + " + ("gmres_solve" if ns else "pcg_solve")},
             "iters": info["iters"], "solve_status": info["status"], "relres": info["relres"],
             "phases_ms": {"setup": t_setup, "solve": t_solve, "fine_apply": t_apply},
             "solve_only_dofs_per_s": cfg.trace_dofs / (t_solve * 1e-3),
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_apply<4,*> fine-level colour passes (mg_apply, both colours)",
+                         "kernel": ("k_apply_ldg<p,*,NS> full-storage" if ns else "k_apply<p,*>")
+                                   + " fine-level colour passes (mg_apply, both colours)",
                          "alg_bytes_per_apply": alg_bytes,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in peaks
                          else "fallback 6650 GB/s (B200_PROFILING.md)"},

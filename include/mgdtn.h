@@ -70,7 +70,19 @@ enum { MG_CONVERGED = 0, MG_MAXIT = 1, MG_DIVERGED = 2, MG_BREAKDOWN = 3 };
 
 /* ---- hybridized method per element ---- */
 enum { MG_HDG = 0,      /* Eqs. HDG, HDG_flux */
-       MG_SIPG_H = 1 }; /* Eq. SIPG_H, s_f = 1 */
+       MG_SIPG_H = 1,   /* Eq. SIPG_H, s_f = 1 */
+       MG_IIPG_H = 2,   /* Eq. IPG_H, s_f = 0: nonsymmetric */
+       MG_NIPG_H = 3 }; /* Eq. IPG_H, s_f = -1: nonsymmetric */
+
+/* ---- mg_build_hierarchy_ex flags ---- */
+enum { MG_BUILD_NONSYMMETRIC = 1 };  /* A may be nonsymmetric (MG_IIPG_H / MG_NIPG_H elements):
+                                        element maps stored full (m*m doubles instead of
+                                        m(m+1)/2), local / edge / macro / coarsest blocks by
+                                        LU, restriction by Eq. 3.5 (Q_{k-1} != I_k^T).
+                                        Accepts every method code.  Solvers: mg_mg_solve and
+                                        mg_gmres_solve (mg_pcg_solve / mg_solve_host return
+                                        MG_ERR_UNSUPPORTED: PCG needs a symmetric A).
+                                        Smoother: block-Jacobi only.  One GPU only. */
 
 /* ---- smoothers ---- */
 enum { MG_SMOOTH_BLOCK_JACOBI = 0,  /* edge blocks, e += omega D_B^-1 (r - A e) */
@@ -159,6 +171,11 @@ typedef struct {
  * collective (all ranks call it in the same order). */
 int mg_build_hierarchy(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
                        const mg_partition* part, void* cuda_stream, void** out_ctx);
+/* The same with flags (MG_BUILD_NONSYMMETRIC; 0 = mg_build_hierarchy).  A
+ * nonsymmetric build with a partition (nranks > 1) returns MG_ERR_UNSUPPORTED. */
+int mg_build_hierarchy_ex(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
+                          const mg_partition* part, int32_t flags, void* cuda_stream,
+                          void** out_ctx);
 
 /* Bytes of device workspace the ctx needs (256-byte aligned pointer). */
 int mg_workspace_bytes(const void* ctx, size_t* bytes);
@@ -173,7 +190,8 @@ int mg_bind_workspace(void* ctx, void* dev_ptr, size_t bytes);
  *   per 2x2 agglomerate: A_II^-1, P_M = -A_II^-1 A_IB J, coarse DtN (Eq. Akm1),
  *   edge-block diagonals D_e^-1, Chebyshev lambda_max, coarsest A_1^-1.
  * K[ne] > 0 (scalar permeability per element), method[ne] in {MG_HDG,
- * MG_SIPG_H}, tau[ne] > 0 (stabilisation of the element's own flux,
+ * MG_SIPG_H} (any of the four codes on a MG_BUILD_NONSYMMETRIC ctx; an IIPG-H /
+ * NIPG-H code on a symmetric ctx is MG_ERR_ARG), tau[ne] > 0 (stabilisation of the element's own flux,
  * Eq. HDG_flux / IPDG_flux), all device arrays in element-id order.
  * Errors: MG_ERR_NOT_SPD / MG_ERR_SINGULAR_LOCAL with the element index
  * (detected asynchronously; reported by the next synchronising call). */

@@ -4,10 +4,10 @@ steps in hand-written sm_100a CUDA kernels behind the C ABI include/mgdtn.h.
 
     from paper_1811_09909_b200 import MGSolver, SmootherConfig
 """
-from .mgdtn import (MG_HDG, MG_SIPG_H, MG_SMOOTH_BLOCK_JACOBI, MG_SMOOTH_CHEBYSHEV, LIB_PATH,
+from .mgdtn import (MG_HDG, MG_IIPG_H, MG_NIPG_H, MG_SIPG_H, MG_SMOOTH_BLOCK_JACOBI, MG_SMOOTH_CHEBYSHEV, LIB_PATH,
                     LoopbackHub, MGError, MGSolver, Partition, SmootherConfig, load_library,
                     nccl_unique_id, partition_plan, partition_side_edges, smoother_from_config)
 
 __all__ = ["MGSolver", "SmootherConfig", "MGError", "load_library", "LIB_PATH", "MG_HDG",
-           "MG_SIPG_H", "MG_SMOOTH_BLOCK_JACOBI", "MG_SMOOTH_CHEBYSHEV", "smoother_from_config",
+           "MG_SIPG_H", "MG_IIPG_H", "MG_NIPG_H", "MG_SMOOTH_BLOCK_JACOBI", "MG_SMOOTH_CHEBYSHEV", "smoother_from_config",
            "Partition", "LoopbackHub", "nccl_unique_id", "partition_plan", "partition_side_edges"]

@@ -810,8 +810,11 @@ __global__ void __launch_bounds__(32) k_apply_fused(const LevelDev L, const doub
   }
 }
 
-// ---------------------------------------------------------------- direct-load apply (A/B)
-template <int P, int MODE, bool DOT>
+// ---------------------------------------------------------------- direct-load apply
+// A/B variant of the packed apply, and THE apply of a nonsymmetric context (NS:
+// full row-major S_T, Eq. IPG_H with s_f != 1): thread per element, the 32 lanes
+// of a warp read one entry of 32 consecutive elements as one 256-byte segment.
+template <int P, int MODE, bool DOT, bool NS = false>
 __global__ void __launch_bounds__(128) k_apply_ldg(const LevelDev L, int colour,
                                                    const double* x, double* y,
                                                    const double* __restrict__ r, double* d,
@@ -820,7 +823,7 @@ __global__ void __launch_bounds__(128) k_apply_ldg(const LevelDev L, int colour,
   (void)early;
   constexpr int K1 = P + 1;
   constexpr int M = 4 * K1;
-  constexpr int NPK = M * (M + 1) / 2;
+  constexpr int NPK = NS ? M * M : M * (M + 1) / 2;
   const int64_t nec = L.ne >> 1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const uint64_t pol = stream_policy(L.l2keep);
@@ -845,14 +848,21 @@ __global__ void __launch_bounds__(128) k_apply_ldg(const LevelDev L, int colour,
 #pragma unroll
     for (int a = 0; a < M; ++a) yv[a] = 0.0;
     const double* Sp = L.S + ((((int64_t)colour * L.nchunk + (s >> 5)) * NPK) << 5) + (s & 31);
+    if (NS) {
 #pragma unroll
-    for (int a = 0; a < M; ++a) {
+      for (int a = 0; a < M; ++a)
 #pragma unroll
-      for (int b = a; b < M; ++b) {
-        const int kk = a * (2 * M - a + 1) / 2 + (b - a);
-        const double sv = ld_stream(Sp + (kk << 5), pol);
-        yv[a] = fma(sv, xv[b], yv[a]);
-        if (b != a) yv[b] = fma(sv, xv[a], yv[b]);
+        for (int b = 0; b < M; ++b) yv[a] = fma(ld_stream(Sp + ((a * M + b) << 5), pol), xv[b], yv[a]);
+    } else {
+#pragma unroll
+      for (int a = 0; a < M; ++a) {
+#pragma unroll
+        for (int b = a; b < M; ++b) {
+          const int kk = a * (2 * M - a + 1) / 2 + (b - a);
+          const double sv = ld_stream(Sp + (kk << 5), pol);
+          yv[a] = fma(sv, xv[b], yv[a]);
+          if (b != a) yv[b] = fma(sv, xv[a], yv[b]);
+        }
       }
     }
     epi_store<K1, MODE, DOT>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot, itf);
@@ -975,7 +985,7 @@ int apply_grid(const LevelDev& L) { return apply_grid_mode(L, AM_APPLY); }
 
 int apply_grid_mode(const LevelDev& L, int mode) {
   const int64_t nec = L.ne / 2;
-  if (use_ldg()) {
+  if (use_ldg() || L.ns) {
     int64_t g = (nec + 127) / 128;
     const int64_t gmax = 148 * 8;
     return (int)(g < gmax ? (g > 0 ? g : 1) : gmax);
@@ -1038,6 +1048,12 @@ template <int P, int MODE, bool DOT>
 static void launch_one(const LevelDev& L, int colour, const double* x, double* y, const double* r,
                        double* d, int step, double* partials, int grid, bool pdl,
                        cudaStream_t st) {
+  if (L.ns) {   // nonsymmetric context: full-storage apply (no LU-SGS / power iteration there)
+    if (MODE != AM_GSC && MODE != AM_DINV)
+      launch_ex(k_apply_ldg<P, MODE, DOT, true>, grid, 128, 0, pdl, st, L, colour, x, y, r, d,
+                step, partials, 0);
+    return;
+  }
   if (MODE == AM_GSC) {   // colour sweeps exist in the segmented-ring kernel only
     launch_seg<P, AM_GSC, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
     return;
@@ -1113,7 +1129,7 @@ static int fused_grid(const LevelDev& L) {
 }
 
 int apply2_grid(const LevelDev& L, int mode) {
-  if (!fused_for(L) || L.sync == nullptr || L.imask != 0 || mode == AM_GSC)
+  if (!fused_for(L) || L.sync == nullptr || L.imask != 0 || mode == AM_GSC || L.ns)
     return apply_grid_mode(L, mode);
   switch (L.p) {
     case 1: return fused_grid<1>(L);
@@ -1221,7 +1237,7 @@ int launch_apply(const LevelDev& L, int colour, int mode, const double* x, doubl
 
 int launch_apply2(const LevelDev& L, int mode, const double* x, double* y, const double* r,
                   double* d, int step, double* partials, bool pdl, cudaStream_t st) {
-  if (!fused_for(L) || L.sync == nullptr || L.imask != 0 || mode == AM_GSC) {   // fused: 1 GPU
+  if (!fused_for(L) || L.sync == nullptr || L.imask != 0 || mode == AM_GSC || L.ns) {   // fused: 1 GPU
     int n = launch_apply(L, 0, AM_W0, x, y, nullptr, nullptr, 0, nullptr, pdl, st);
     return n + launch_apply(L, 1, mode, x, y, r, d, step, partials, pdl, st);
   }

@@ -164,6 +164,7 @@ int launch_local_dtn(const LevelDev& L, const RefDev& R, double h, const double*
     const char* e = std::getenv("MGDTN_DTN_PROJECT");
     project = (e && std::atoi(e) == 0) ? 0 : 1;
   }
+  if (L.ns) return launch_local_dtn_ns(L, R, h, K, method, tau, err, project, st);
   switch (L.p) {
     case 1: k_local_dtn<1><<<grid, 32 * 4, 0, st>>>(L, R, h, K, method, tau, err, project); break;
     case 2: k_local_dtn<2><<<grid, 32 * 6, 0, st>>>(L, R, h, K, method, tau, err, project); break;
@@ -255,6 +256,7 @@ int launch_local_rhs(const LevelDev& L, const RefDev& R, double h, const double*
                      double f_const, const double* lamD, double* g, DevError* err,
                      cudaStream_t st) {
   (void)err;
+  if (L.ns) return launch_local_rhs_ns(L, R, h, K, method, tau, f_qp, f_const, lamD, g, st);
   int64_t gsz = (L.ne / 2 + 127) / 128;
   int grid = (int)(gsz < 148 * 16 ? gsz : 148 * 16);
   if (grid < 1) grid = 1;
@@ -348,6 +350,9 @@ int launch_recover(const LevelDev& L, const RefDev& R, double h, const double* K
                    const int8_t* method, const double* tau, const double* lam,
                    const double* f_qp, double f_const, double* q_out, const double* qex_qp,
                    double* partials, int* grid_out, cudaStream_t st) {
+  if (L.ns)
+    return launch_recover_ns(L, R, h, K, method, tau, lam, f_qp, f_const, q_out, qex_qp,
+                             partials, grid_out, st);
   int64_t g = (L.ne + 127) / 128;
   const int grid = (int)(g < 148 * 8 ? (g > 0 ? g : 1) : 148 * 8);
   if (grid_out) *grid_out = grid;
@@ -400,15 +405,16 @@ int launch_dirichlet(const LevelDev& L, const RefDev& R, const double* gD_qp, do
 // H2: p-coarsening S^(1)_T = J_p^T S_T J_p (Eq. ANm1), per
 // element, J_p = blockdiag over the 4 edges of [(1-s_a), s_a].
 // ============================================================================
-__device__ __forceinline__ double pk_get(const double* base, int m, int a, int b) {
-  if (a > b) { int t = a; a = b; b = t; }
-  return base[(int64_t)pk_index(a, b, m) * 32];
+__device__ __forceinline__ double s_get(const double* base, int m, int ns, int a, int b) {
+  return base[(int64_t)s_index(a, b, m, ns) * 32];
 }
 
 // One thread per element; J_p is block diagonal (one [(p+1) x 2] block per edge),
 // so per row block f: T_f = S_{f,:} J_p (K1 x 8, from the packed rows of edge f),
 // then rows 2f, 2f+1 of J_p^T S J_p = J_f^T T_f.  Compile-time indices throughout.
-template <int P>
+// NS: full row-major storage on both levels (nonsymmetric context): every entry of
+// J_p^T S_T J_p is formed (the symmetric path forms the upper triangle).
+template <int P, bool NS>
 __global__ void __launch_bounds__(128) k_p_coarsen(LevelDev F, LevelDev C,
                                                    const double* __restrict__ Jp) {
   constexpr int K1 = P + 1, M = 4 * K1;
@@ -441,7 +447,9 @@ __global__ void __launch_bounds__(128) k_p_coarsen(LevelDev F, LevelDev C,
           for (int b = 0; b < K1; ++b) {
             const int cidx = g * K1 + b;
             const int lo = r < cidx ? r : cidx, hi = r < cidx ? cidx : r;
-            const double v = __ldg(src + (int64_t)(lo * (2 * M - lo + 1) / 2 + (hi - lo)) * 32);
+            const double v =
+                NS ? __ldg(src + (int64_t)(r * M + cidx) * 32)
+                   : __ldg(src + (int64_t)(lo * (2 * M - lo + 1) / 2 + (hi - lo)) * 32);
             T[a][2 * g] = fma(v, J[b][0], T[a][2 * g]);
             T[a][2 * g + 1] = fma(v, J[b][1], T[a][2 * g + 1]);
           }
@@ -451,11 +459,11 @@ __global__ void __launch_bounds__(128) k_p_coarsen(LevelDev F, LevelDev C,
       for (int al = 0; al < 2; ++al) {
         const int A = 2 * f + al;
 #pragma unroll
-        for (int B = A; B < 8; ++B) {
+        for (int B = NS ? 0 : A; B < 8; ++B) {
           double acc = 0.0;
 #pragma unroll
           for (int a = 0; a < K1; ++a) acc = fma(J[a][al], T[a][B], acc);
-          dst[(int64_t)pk_index(A, B, 8) * 32] = acc;
+          dst[(int64_t)(NS ? A * 8 + B : pk_index(A, B, 8)) * 32] = acc;
         }
       }
     }
@@ -465,10 +473,18 @@ __global__ void __launch_bounds__(128) k_p_coarsen(LevelDev F, LevelDev C,
 int launch_p_coarsen(const LevelDev& F, const LevelDev& C, const double* Jp, cudaStream_t st) {
   int64_t n = F.ne;
   int grid = (int)((n + 127) / 128 < 148 * 16 ? (n + 127) / 128 : 148 * 16);
+  if (F.ns) {
+    switch (F.p) {
+      case 2: k_p_coarsen<2, true><<<grid, 128, 0, st>>>(F, C, Jp); break;
+      case 3: k_p_coarsen<3, true><<<grid, 128, 0, st>>>(F, C, Jp); break;
+      default: k_p_coarsen<4, true><<<grid, 128, 0, st>>>(F, C, Jp); break;
+    }
+    return 1;
+  }
   switch (F.p) {
-    case 2: k_p_coarsen<2><<<grid, 128, 0, st>>>(F, C, Jp); break;
-    case 3: k_p_coarsen<3><<<grid, 128, 0, st>>>(F, C, Jp); break;
-    default: k_p_coarsen<4><<<grid, 128, 0, st>>>(F, C, Jp); break;
+    case 2: k_p_coarsen<2, false><<<grid, 128, 0, st>>>(F, C, Jp); break;
+    case 3: k_p_coarsen<3, false><<<grid, 128, 0, st>>>(F, C, Jp); break;
+    default: k_p_coarsen<4, false><<<grid, 128, 0, st>>>(F, C, Jp); break;
   }
   return 1;
 }
@@ -500,10 +516,15 @@ constexpr int AGG_WARPS = 4;
 // dense_out != nullptr: the coarse maps go to dense_out[M][8][8] (element-id order of
 // the coarse block; both triangles) instead of the packed chunk layout -- the gather
 // level's per-rank block, whose element count may be odd
+// Nonsymmetric context (F.ns): A_II is inverted by Gauss-Jordan with partial
+// pivoting, S_c = Kr_CC + Kr_CI P_M is formed in full, and the restriction's macro
+// term of Eq. 3.5, Q_M = -J^T A_BI A_II^-1 = -Kr_CI A_II^-1 (not P_M^T when A is
+// nonsymmetric), is stored transposed in Rm (Rm[a*8 + c] = Q_M[c][a], the layout in
+// which the restriction reads P_M on a symmetric level).
 __global__ void __launch_bounds__(32 * AGG_WARPS) k_agglomerate(LevelDev F, LevelDev C,
                                                                 double* KIIinv, double* Pm,
                                                                 DevError* err,
-                                                                double* dense_out) {
+                                                                double* dense_out, double* Rm) {
   __shared__ double smK[AGG_WARPS][16 * 16];
   __shared__ double smG[AGG_WARPS][8 * 16];
   __shared__ double smU[AGG_WARPS][8 * 16];
@@ -525,11 +546,11 @@ __global__ void __launch_bounds__(32 * AGG_WARPS) k_agglomerate(LevelDev F, Leve
       int colour;
       int64_t s;
       elem_slot(F.nx, ci, cj, colour, s);
-      const double* src = F.S + s_offset(F.nchunk, 36, colour, s, 0);
+      const double* src = F.S + s_offset(F.nchunk, F.npk, colour, s, 0);
       // child S (dense 8x8) into Sc, G_c (8 x 16) into G
       for (int q = lane; q < 64; q += 32) {
         int a = q >> 3, b = q & 7;
-        Sc[q] = pk_get(src, 8, a, b);
+        Sc[q] = s_get(src, 8, F.ns, a, b);
       }
       for (int q = lane; q < 128; q += 32) G[q] = 0.0;
       __syncwarp();
@@ -563,6 +584,40 @@ __global__ void __launch_bounds__(32 * AGG_WARPS) k_agglomerate(LevelDev F, Leve
         Kr[q] += acc;
       }
       __syncwarp();
+    }
+    if (F.ns) {
+      // A_II^-1 (Gauss-Jordan, partial pivoting) into G[0..63]; scratch Sc
+      if (lane == 0) {
+        double Kii[64];
+        for (int q = 0; q < 64; ++q) Kii[q] = Kr[(q >> 3) * 16 + (q & 7)];
+        if (!gj_inverse(Kii, 8, G, Sc)) report_error(err, -3, M);
+      }
+      __syncwarp();
+      for (int q = lane; q < 64; q += 32) {
+        const int a = q >> 3, b = q & 7;
+        KIIinv[M * 64 + q] = G[q];
+        double pm = 0.0, qm = 0.0;
+        for (int r = 0; r < 8; ++r) {
+          pm = fma(-G[a * 8 + r], Kr[r * 16 + 8 + b], pm);          // P_M[a][b]
+          qm = fma(-Kr[(8 + b) * 16 + r], G[r * 8 + a], qm);        // Q_M[b][a]
+        }
+        Pm[M * 64 + q] = pm;
+        U[a * 16 + b] = pm;
+        Rm[M * 64 + q] = qm;
+      }
+      __syncwarp();
+      int colour;
+      int64_t s;
+      elem_slot(C.nx, I, J, colour, s);
+      double* dst = C.S + s_offset(C.nchunk, C.npk, colour, s, 0);
+      for (int q = lane; q < 64; q += 32) {
+        const int a = q >> 3, b = q & 7;
+        double acc = Kr[(8 + a) * 16 + 8 + b];
+        for (int r = 0; r < 8; ++r) acc = fma(Kr[(8 + a) * 16 + r], U[r * 16 + b], acc);
+        dst[(int64_t)q * 32] = acc;
+      }
+      __syncwarp();
+      continue;
     }
     // Cholesky of Kr_II (8x8, lower, in Sc)
     for (int q = lane; q < 64; q += 32) Sc[q] = Kr[(q >> 3) * 16 + (q & 7)];
@@ -637,11 +692,11 @@ __global__ void __launch_bounds__(32 * AGG_WARPS) k_agglomerate(LevelDev F, Leve
 }
 
 int launch_agglomerate(const LevelDev& F, const LevelDev& C, double* KIIinv, double* Pm,
-                       DevError* err, cudaStream_t st, double* dense_out) {
+                       DevError* err, cudaStream_t st, double* dense_out, double* Rm) {
   int64_t nmac = (int64_t)(F.nx / 2) * (F.ny / 2);
   int64_t g = (nmac + AGG_WARPS - 1) / AGG_WARPS;
   int grid = (int)(g < 148 * 16 ? g : 148 * 16);
-  k_agglomerate<<<grid, 32 * AGG_WARPS, 0, st>>>(F, C, KIIinv, Pm, err, dense_out);
+  k_agglomerate<<<grid, 32 * AGG_WARPS, 0, st>>>(F, C, KIIinv, Pm, err, dense_out, Rm);
   return 1;
 }
 
@@ -682,14 +737,20 @@ __global__ void k_edge_blocks(LevelDev L, DevError* err) {
       elem_slot(L.nx, ei[t], ej[t], colour, s);
       const double* src = L.S + s_offset(L.nchunk, L.npk, colour, s, 0);
       for (int a = 0; a < K1; ++a)
-        for (int b = 0; b < K1; ++b) D[a * K1 + b] += pk_get(src, m, ef[t] * K1 + a, ef[t] * K1 + b);
+        for (int b = 0; b < K1; ++b)
+          D[a * K1 + b] += s_get(src, m, L.ns, ef[t] * K1 + a, ef[t] * K1 + b);
     }
     if (side >= 0) {   // interface: this rank's partial block; inverted after the halo (k_part.cu)
       for (int q = 0; q < K1 * K1; ++q) out[q * sd] = D[q];
       continue;
     }
     double inv[MAX_K1 * MAX_K1];
-    if (!chol_inverse(D, K1, inv)) report_error(err, -4, e);
+    if (L.ns) {   // nonsymmetric block: Gauss-Jordan with partial pivoting
+      double scr[MAX_K1 * MAX_K1];
+      if (!gj_inverse(D, K1, inv, scr)) report_error(err, -3, e);
+    } else if (!chol_inverse(D, K1, inv)) {
+      report_error(err, -4, e);
+    }
     for (int q = 0; q < K1 * K1; ++q) out[q * sd] = inv[q];
   }
 }
@@ -741,7 +802,8 @@ __global__ void k_dense_to_packed(LevelDev L, const double* __restrict__ src) {
     double* dst = L.S + s_offset(L.nchunk, L.npk, colour, s, 0);
     const double* a0 = src + e * L.m * L.m;
     for (int a = 0; a < L.m; ++a)
-      for (int b = a; b < L.m; ++b) dst[(int64_t)pk_index(a, b, L.m) * 32] = a0[a * L.m + b];
+      for (int b = L.ns ? 0 : a; b < L.m; ++b)
+        dst[(int64_t)s_index(a, b, L.m, L.ns) * 32] = a0[a * L.m + b];
   }
 }
 __global__ void k_packed_to_dense(LevelDev L, double* __restrict__ dst) {
@@ -753,7 +815,7 @@ __global__ void k_packed_to_dense(LevelDev L, double* __restrict__ dst) {
     const double* src = L.S + s_offset(L.nchunk, L.npk, colour, s, 0);
     double* a0 = dst + e * L.m * L.m;
     for (int a = 0; a < L.m; ++a)
-      for (int b = 0; b < L.m; ++b) a0[a * L.m + b] = pk_get(src, L.m, a, b);
+      for (int b = 0; b < L.m; ++b) a0[a * L.m + b] = s_get(src, L.m, L.ns, a, b);
   }
 }
 int launch_dense_to_packed(const LevelDev& L, const double* src, cudaStream_t st) {
@@ -783,7 +845,7 @@ __global__ void k_gather_dense(LevelDev L, const int64_t* __restrict__ elems, in
     int colour;
     int64_t s;
     elem_slot(L.nx, (int)(e % L.nx), (int)(e / L.nx), colour, s);
-    dst[q] = pk_get(L.S + s_offset(L.nchunk, L.npk, colour, s, 0), m, a, b);
+    dst[q] = s_get(L.S + s_offset(L.nchunk, L.npk, colour, s, 0), m, L.ns, a, b);
   }
 }
 
@@ -819,10 +881,14 @@ __global__ void k_coarse_factor(LevelDev L, const int* __restrict__ fpos, int nf
         for (int a = 0; a < L.k1; ++a) gi[f * L.k1 + a] = fpos[ed[f] * L.k1 + a];
       for (int a = 0; a < L.m; ++a)
         for (int b = 0; b < L.m; ++b)
-          if (gi[a] >= 0 && gi[b] >= 0) A[gi[a] * nf + gi[b]] += pk_get(src, L.m, a, b);
+          if (gi[a] >= 0 && gi[b] >= 0) A[gi[a] * nf + gi[b]] += s_get(src, L.m, L.ns, a, b);
     }
   }
   __syncthreads();
+  if (L.ns) {   // nonsymmetric A_1: Gauss-Jordan with partial pivoting (A is the scratch)
+    if (tid == 0 && !gj_inverse(A, nf, Ainv, A)) report_error(err, -3, -2);
+    return;
+  }
   __shared__ int bad;
   if (tid == 0) bad = 0;
   __syncthreads();

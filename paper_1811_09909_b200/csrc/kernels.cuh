@@ -1,7 +1,9 @@
 // Device data layout, indexing helpers and kernel launchers (sm_100a, FP64).
 //
 // Element DtN maps of a level are stored packed-symmetric (upper triangle,
-// row-major, npk = m(m+1)/2 entries, m = 4(p+1)) and element-interleaved in
+// row-major, npk = m(m+1)/2 entries, m = 4(p+1)) -- or, in a context built for
+// the nonsymmetric schemes IIPG-H / NIPG-H (LevelDev::ns), in full row-major
+// storage (npk = m*m, entry kk = a*m + b) -- and element-interleaved in
 // chunks of 32 same-colour elements:
 //     S[((colour*nchunk + chunk)*npk + kk)*32 + lane]
 // so that one warp-wide load of entry kk of 32 consecutive elements is one
@@ -38,6 +40,7 @@ __host__ __device__ __forceinline__ int gs_colour(int i, int j, int f) {
 
 struct LevelDev {
   int nx, ny, p, k1, m, npk;
+  int ns;                  // 1: nonsymmetric operator (full S_T storage, LU factors; Eq. IPG_H)
   int64_t ne, nedge, ndof;
   int nchunk;              // chunks of 32 per colour
   double* S;               // interleaved packed DtN
@@ -87,6 +90,12 @@ __host__ __device__ __forceinline__ int64_t vedge(int nx, int ny, int i, int j) 
 }
 __host__ __device__ __forceinline__ int pk_index(int i, int j, int m) {  // i <= j
   return i * (2 * m - i + 1) / 2 + (j - i);
+}
+// storage index of entry (a, b) of an element map: packed upper triangle, or
+// row-major when the level is nonsymmetric
+__host__ __device__ __forceinline__ int s_index(int a, int b, int m, int ns) {
+  if (ns) return a * m + b;
+  return a <= b ? pk_index(a, b, m) : pk_index(b, a, m);
 }
 __host__ __device__ __forceinline__ int64_t s_offset(int nchunk, int npk, int colour, int64_t s,
                                                      int kk) {
@@ -205,10 +214,61 @@ __host__ __device__ __forceinline__ bool chol_inverse(const double* D, int K1, d
   return ok;
 }
 
+// explicit inverse of a general k x k block (row-major) by Gauss-Jordan elimination
+// with partial pivoting (the nonsymmetric schemes' edge / macro / coarsest blocks);
+// false if a pivot vanishes
+__host__ __device__ __forceinline__ bool gj_inverse(const double* D, int n, double* inv, double* A) {
+  // A: n*n scratch
+  for (int q = 0; q < n * n; ++q) {
+    A[q] = D[q];
+    inv[q] = (q / n == q % n) ? 1.0 : 0.0;
+  }
+  bool ok = true;
+  for (int k = 0; k < n; ++k) {
+    int piv = k;
+    double best = fabs(A[k * n + k]);
+    for (int r = k + 1; r < n; ++r)
+      if (fabs(A[r * n + k]) > best) {
+        best = fabs(A[r * n + k]);
+        piv = r;
+      }
+    if (!(best > 0.0)) {
+      ok = false;
+      A[k * n + k] = 1e-300;
+      piv = k;
+    }
+    if (piv != k)
+      for (int c = 0; c < n; ++c) {
+        double t = A[k * n + c];
+        A[k * n + c] = A[piv * n + c];
+        A[piv * n + c] = t;
+        t = inv[k * n + c];
+        inv[k * n + c] = inv[piv * n + c];
+        inv[piv * n + c] = t;
+      }
+    const double dinv = 1.0 / A[k * n + k];
+    for (int c = 0; c < n; ++c) {
+      A[k * n + c] *= dinv;
+      inv[k * n + c] *= dinv;
+    }
+    for (int r = 0; r < n; ++r) {
+      if (r == k) continue;
+      const double f = A[r * n + k];
+      if (f == 0.0) continue;
+      for (int c = 0; c < n; ++c) {
+        A[r * n + c] -= f * A[k * n + c];
+        inv[r * n + c] -= f * inv[k * n + c];
+      }
+    }
+  }
+  return ok;
+}
+
 // reference tables on the device (one set per p)
 struct RefDev {
   int p, k1, nv, m, nqf;
   const double *G, *F, *P, *E, *W, *H, *LN, *Nl, *fq, *ew, *H1inv, *Jp;
+  const double *Lv, *Nv;   // volume stiffness L and <grad phi_j.n, phi_i>_dT (IPDG with s_f != 1)
   // pencil tables per method (refelem.h RefTables::Pencil): [0] HDG, [1] SIPG-H
   const double *plam[2], *pmu[2], *pAt[2], *pBk[2], *pfq[2];
   const double *pTt[2], *vq, *wq;   // volume recovery (refelem.h)
@@ -279,8 +339,21 @@ int launch_recover(const LevelDev& L, const RefDev& R, double h, const double* K
                    const double* f_qp, double f_const, double* q_out, const double* qex_qp,
                    double* partials, int* grid_out, cudaStream_t st);
 int launch_p_coarsen(const LevelDev& F, const LevelDev& C, const double* Jp, cudaStream_t st);
+// Rm: the restriction's macro matrix of a nonsymmetric level (k_setup.cu), else unused
 int launch_agglomerate(const LevelDev& F, const LevelDev& C, double* KIIinv, double* Pm,
-                       DevError* err, cudaStream_t st, double* dense_out = nullptr);
+                       DevError* err, cudaStream_t st, double* dense_out = nullptr,
+                       double* Rm = nullptr);
+// nonsymmetric context (k_local_ns.cu): the same three element-local operations
+int launch_local_dtn_ns(const LevelDev& L, const RefDev& R, double h, const double* K,
+                        const int8_t* method, const double* tau, DevError* err, int project,
+                        cudaStream_t st);
+int launch_local_rhs_ns(const LevelDev& L, const RefDev& R, double h, const double* K,
+                        const int8_t* method, const double* tau, const double* f_qp,
+                        double f_const, const double* lamD, double* g, cudaStream_t st);
+int launch_recover_ns(const LevelDev& L, const RefDev& R, double h, const double* K,
+                      const int8_t* method, const double* tau, const double* lam,
+                      const double* f_qp, double f_const, double* q_out, const double* qex_qp,
+                      double* partials, int* grid_out, cudaStream_t st);
 int launch_edge_blocks(const LevelDev& L, DevError* err, cudaStream_t st);
 int launch_dinv_pack(const LevelDev& L, cudaStream_t st);   // Dinv (SoA) -> Dc
 int launch_dense_to_packed(const LevelDev& L, const double* src, cudaStream_t st);

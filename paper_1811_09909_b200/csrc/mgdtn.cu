@@ -27,15 +27,18 @@ struct HostLevel {
   int kind = KIND_COARSEST;
   double h = 0.0;
   size_t o_sync = 0, o_S = 0, o_Dinv = 0, o_Dc = 0, o_coef = 0, o_lam = 0, o_r = 0, o_e = 0, o_w = 0, o_d = 0;
-  size_t o_KIIinv = 0, o_Pm = 0, o_cbuf = 0, o_lpart = 0;
+  size_t o_KIIinv = 0, o_Pm = 0, o_Rm = 0, o_cbuf = 0, o_lpart = 0;
   double* lpart = nullptr;   // per-level partial sums + 16 scalars (concurrent power iterations)
   double *KIIinv = nullptr, *Pm = nullptr, *cbuf = nullptr;
+  double* Rm = nullptr;      // restriction's macro matrix: Pm (symmetric) or -J^T A_BI A_II^-1
+                             // transposed (nonsymmetric context, Eq. 3.5)
   double *r = nullptr, *e = nullptr, *w = nullptr, *dv = nullptr, *lam = nullptr;
 };
 
 struct Ctx {
   mg_quad_mesh mesh{};
   int p = 1;
+  bool ns = false;              // MG_BUILD_NONSYMMETRIC: full S_T storage, LU blocks, Eq. 3.5 restriction
   std::vector<HostLevel> lev;   // lev[0] = finest (paper's level N)
   cudaStream_t st = nullptr;
   RefTables ref;
@@ -200,6 +203,7 @@ static void layout(Ctx* c) {
       int64_t nmac = (int64_t)(d.nx / 2) * (d.ny / 2);
       L.o_KIIinv = take(nmac * 64 * sizeof(double));
       L.o_Pm = take(nmac * 64 * sizeof(double));
+      if (c->ns) L.o_Rm = take(nmac * 64 * sizeof(double));
       L.o_cbuf = take(nmac * 8 * sizeof(double));
     }
   }
@@ -272,7 +276,7 @@ static void bind_pointers(Ctx* c) {
     L.d.sync = reinterpret_cast<unsigned*>(b + L.o_sync);
     L.d.S = D(L.o_S);
     L.d.Dinv = D(L.o_Dinv);
-    L.d.Dc = D(L.o_Dc);
+    L.d.Dc = c->ns ? nullptr : D(L.o_Dc);   // packed-symmetric D_e^-1: symmetric levels only
     L.d.coef = D(L.o_coef);
     L.lpart = D(L.o_lpart);
     L.lam = D(L.o_lam);
@@ -283,6 +287,7 @@ static void bind_pointers(Ctx* c) {
     if (L.kind == KIND_H) {
       L.KIIinv = D(L.o_KIIinv);
       L.Pm = D(L.o_Pm);
+      L.Rm = c->ns ? D(L.o_Rm) : L.Pm;
       L.cbuf = D(L.o_cbuf);
     }
   }
@@ -323,6 +328,8 @@ static void bind_pointers(Ctx* c) {
   }
   rd.vq = put(T.vq);
   rd.wq = put(T.wq);
+  rd.Lv = put(T.L);
+  rd.Nv = put(T.N);
 }
 
 // Levels from tail_start down run as ONE launch of k_coarse_tail (k_coarse.cu):
@@ -339,7 +346,7 @@ static void plan_tail(Ctx* c) {
   c->tail_lmax = env_or("MGDTN_TAIL_LMAX", 1) == 1;
   const int nlev = (int)c->lev.size();
   c->tail_start = -1;
-  if (tail_ne <= 0) return;
+  if (tail_ne <= 0 || c->ns) return;   // the tail kernels read packed-symmetric maps
   for (int li = c->Lg > 0 ? c->Lg : 0; li < nlev; ++li) {   // replicated levels only
     const LevelDev& d = c->lev[li].d;
     if (d.p == 1 && d.ne <= tail_ne && nlev - li >= 2 && nlev - li <= MAX_TAIL &&
@@ -425,6 +432,8 @@ static int upload_static(Ctx* c) {
       all.insert(all.end(), v->begin(), v->end());
   all.insert(all.end(), T.vq.begin(), T.vq.end());
   all.insert(all.end(), T.wq.begin(), T.wq.end());
+  all.insert(all.end(), T.L.begin(), T.L.end());
+  all.insert(all.end(), T.N.begin(), T.N.end());
   CK(cudaMemcpyAsync(c->ws + c->o_ref, all.data(), all.size() * sizeof(double),
                      cudaMemcpyHostToDevice, c->st));
   // coarsest free-dof maps
@@ -475,7 +484,16 @@ static int check_device_error(Ctx* c) {
                   "(element / edge / macro; -2 = coarsest) reported",
                   h.index);
     case -1:
-      return fail(c, MG_ERR_ARG, "invalid K / tau / method at element", h.index);
+      return fail(c, MG_ERR_ARG,
+                  c->ns ? "invalid K / tau / method at element"
+                        : "invalid K / tau / method at element (IIPG-H / NIPG-H need a "
+                          "MG_BUILD_NONSYMMETRIC context)",
+                  h.index);
+    case -3:
+      return fail(c, MG_ERR_SINGULAR_LOCAL,
+                  "LU pivot vanished (local block, edge block, macro A_II or A_1); index "
+                  "(element / edge / macro; -2 = coarsest) reported",
+                  h.index);
     default:
       return fail(c, MG_ERR_SINGULAR_LOCAL, "device error", h.index);
   }
@@ -570,7 +588,7 @@ static void restrict_level(Ctx* c, int li, const double* res, double* e, bool do
   double* rcl = gat ? c->lgl.r : rc;
   if (gat) fuse = false;
   if (L.kind == KIND_H) {
-    c->launches += launch_lc_restrict(L.d, res, e, L.KIIinv, L.Pm, L.cbuf, do_lc, true, c->st);
+    c->launches += launch_lc_restrict(L.d, res, e, L.KIIinv, L.Rm, L.cbuf, do_lc, true, c->st);
     c->launches += launch_restrict_edges(L.d, C.d, res, L.cbuf, rcl, fuse, C.e, C.dv, c->st);
     if (C.d.imask) {
       c->launches += launch_restrict_halo_pack(C.d, L.cbuf, c->hsend, c->st);
@@ -729,7 +747,7 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
         halo_exchange(c, L.d, eblk_stride(L.d), L.d.k1 * L.d.k1);
         c->launches += launch_eblk_finish(L.d, c->hrecv, c->err, st);
       }
-      c->launches += launch_dinv_pack(L.d, st);
+      if (!c->ns) c->launches += launch_dinv_pack(L.d, st);
       if (!cheb) c->launches += launch_set_bj_coef(c->sm.omega, L.d.coef, st);
       if (is_pow(li)) RC(power_iteration(li));
     }
@@ -746,7 +764,8 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
       comm_fail(c, c->comm->allgather(c->sden, c->sall, (size_t)B.d.ne * 64, st));
       c->launches += launch_gather_S(C.d, B.d.nx, B.d.ny, c->px, c->sall, st);
     } else {
-      c->launches += launch_agglomerate(L.d, C.d, L.KIIinv, L.Pm, c->err, st);
+      c->launches += launch_agglomerate(L.d, C.d, L.KIIinv, L.Pm, c->err, st, nullptr,
+                                        c->ns ? L.Rm : nullptr);
     }
   }
   if (c->sm.kind == MG_SMOOTH_CHEBYSHEV && c->tail_lmax && c->tail_start >= 0 &&
@@ -1260,7 +1279,16 @@ extern "C" {
 
 int mg_build_hierarchy(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
                        const mg_partition* part, void* cuda_stream, void** out_ctx) {
+  return mg_build_hierarchy_ex(mesh, p, n_h_levels, part, 0, cuda_stream, out_ctx);
+}
+
+int mg_build_hierarchy_ex(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
+                          const mg_partition* part, int32_t flags, void* cuda_stream,
+                          void** out_ctx) {
   if (!mesh || !out_ctx) return MG_ERR_ARG;
+  if (flags & ~MG_BUILD_NONSYMMETRIC) return MG_ERR_ARG;
+  const bool ns = (flags & MG_BUILD_NONSYMMETRIC) != 0;
+  if (ns && part && part->nranks > 1) return MG_ERR_UNSUPPORTED;
   *out_ctx = nullptr;
   if (p < 1 || p > 4) return MG_ERR_ARG;
   const int nx = mesh->nx, ny = mesh->ny;
@@ -1282,11 +1310,16 @@ int mg_build_hierarchy(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_levels,
   for (int k = 0; k < 2; ++k)
     c->ref_doubles += T.pen[k].lam.size() + T.pen[k].mu.size() + T.pen[k].At.size() +
                       T.pen[k].Bk.size() + T.pen[k].fqT.size() + T.pen[k].Tt.size();
-  c->ref_doubles += T.vq.size() + T.wq.size();
+  c->ref_doubles += T.vq.size() + T.wq.size() + T.L.size() + T.N.size();
   int rc = build_levels(c, mesh, p, n_h_levels, part);
   if (rc != MG_OK) {
     delete c;
     return rc;
+  }
+  c->ns = ns;
+  for (auto& L : c->lev) {   // full element-map storage on every level
+    L.d.ns = ns ? 1 : 0;
+    if (ns) L.d.npk = L.d.m * L.d.m;
   }
   if (partitioned(c)) {   // the communicator: loopback hub (tests) or NCCL (one process per GPU)
     if (part->loopback) {
@@ -1402,6 +1435,9 @@ int mg_setup_dtn(void* ctx, const double* K, const int8_t* method, const double*
     return fail(c, MG_ERR_ARG, "unknown smoother kind");
   if (sm.kind == MG_SMOOTH_LUSGS && partitioned(c))
     return fail(c, MG_ERR_UNSUPPORTED, "LU-SGS on a partitioned context");
+  if (c->ns && sm.kind != MG_SMOOTH_BLOCK_JACOBI)
+    return fail(c, MG_ERR_UNSUPPORTED,
+                "nonsymmetric context: block-Jacobi only (Chebyshev needs a real spectrum)");
   if (sm.nu_pre < 0 || sm.nu_post < 0 || sm.nu_pre > MAX_NU || sm.nu_post > MAX_NU)
     return fail(c, MG_ERR_ARG, "nu out of range (0..8)");
   if (!(sm.omega > 0)) sm.omega = 1.0;
@@ -1503,6 +1539,9 @@ int mg_pcg_solve(void* ctx, const double* g, double* lambda, double rtol, int32_
   Ctx* c = static_cast<Ctx*>(ctx);
   if (!c || !g || !lambda || maxit < 1 || !(rtol > 0)) return MG_ERR_ARG;
   if (!c->setup_done) return fail(c, MG_ERR_STATE, "setup first");
+  if (c->ns)
+    return fail(c, MG_ERR_UNSUPPORTED,
+                "PCG needs a symmetric operator: use mg_gmres_solve / mg_mg_solve");
   int it = 0, stt = 0;
   double rel = 0;
   RC(pcg_impl(c, g, lambda, rtol, maxit, &it, &rel, &stt, resid_hist));
@@ -1572,6 +1611,7 @@ int mg_solve_host(void* ctx, const double* K_host, const int8_t* method_host,
                   int32_t* solve_status) {
   Ctx* c = static_cast<Ctx*>(ctx);
   if (!c || !K_host || !method_host || !tau_host || !lambda_host || !smoother) return MG_ERR_ARG;
+  if (c->ns) return fail(c, MG_ERR_UNSUPPORTED, "mg_solve_host runs PCG: symmetric contexts only");
   size_t need = 0;
   mg_staging_bytes(c, f_qp_host != nullptr, gD_qp_host != nullptr, &need);
   if (!c->stg || c->stg_bytes < need) return fail(c, MG_ERR_WORKSPACE, "staging not bound / too small");

@@ -370,6 +370,8 @@ RefTables build_ref_tables(int p) {
   for (int i = 0; i < nv; ++i)
     for (int j = 0; j < nv; ++j) T.LN[i * nv + j] = L[i * nv + j] - N[i * nv + j] - N[j * nv + i];
   T.Nl = Nl;
+  T.L = L;
+  T.N = N;
   // source / boundary-data quadrature on the p+4 Gauss sampling grid
   std::vector<double> xf, wf;
   T.nqf = p + 4;

@@ -23,6 +23,9 @@ struct RefTables {
   // SIPG-H: Q = K*LN + t*F, R = t*E - K*Nl, S0 = t*H, LN = L - N - N^T
   std::vector<double> LN;             // [nv*nv]
   std::vector<double> Nl;             // [nv*m]
+  // IPDG-H with general s_f (Eq. IPG_H): Q = K*(L - N - s_f N^T) + t*F, R = t*E - s_f K*Nl,
+  // flux rows (t*E - K*Nl)^T; L_ij = (grad phi_j, grad phi_i), N_ij = <grad phi_j.n, phi_i>_dT
+  std::vector<double> L, N;           // [nv*nv]
   // source quadrature on the input sampling grid (p+4 Gauss per direction):
   //   fw_i = h^2 * sum_{qy,qx} fq[qy,qx,i] * f(qy,qx)
   int nqf = 0;

@@ -18,7 +18,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmgdtn.so")
 
 MG_OK = 0
-MG_HDG, MG_SIPG_H = 0, 1
+MG_HDG, MG_SIPG_H, MG_IIPG_H, MG_NIPG_H = 0, 1, 2, 3
+MG_BUILD_NONSYMMETRIC = 1
 MG_SMOOTH_BLOCK_JACOBI, MG_SMOOTH_CHEBYSHEV, MG_SMOOTH_LUSGS = 0, 1, 2
 STATUS = {0: "converged", 1: "maxit", 2: "diverged", 3: "breakdown"}
 ERRORS = {-1: "MG_ERR_ARG", -2: "MG_ERR_SHAPE", -3: "MG_ERR_SINGULAR_LOCAL", -4: "MG_ERR_NOT_SPD",
@@ -47,6 +48,8 @@ _P = C.c_void_p
 _SIGS = {
     "mg_build_hierarchy": [C.POINTER(mg_quad_mesh), C.c_int32, C.c_int32, C.POINTER(mg_partition), _P,
                            C.POINTER(C.c_void_p)],
+    "mg_build_hierarchy_ex": [C.POINTER(mg_quad_mesh), C.c_int32, C.c_int32, C.POINTER(mg_partition),
+                              C.c_int32, _P, C.POINTER(C.c_void_p)],
     "mg_workspace_bytes": [_P, C.POINTER(C.c_size_t)],
     "mg_bind_workspace": [_P, _P, C.c_size_t],
     "mg_setup_dtn": [_P, _P, _P, _P, C.POINTER(mg_smoother_cfg)],
@@ -253,11 +256,13 @@ class MGSolver:
     """One context of the C ABI on a CUDA device (own stream unless given).
 
     partition: None (one GPU) or a Partition -- then nx, ny are the GLOBAL mesh and
-    every array argument is this rank's element block / its local edge numbering."""
+    every array argument is this rank's element block / its local edge numbering.
+    nonsymmetric: build with MG_BUILD_NONSYMMETRIC (IIPG-H / NIPG-H elements; full
+    element maps, LU blocks; solve with mg_solve / gmres_solve, block-Jacobi only)."""
 
     def __init__(self, nx: int, ny: int | None = None, p: int = 1, h: float | None = None,
                  n_h_levels: int = 0, device="cuda", stream: torch.cuda.Stream | None = None,
-                 partition: Partition | None = None):
+                 partition: Partition | None = None, nonsymmetric: bool = False):
         if not torch.cuda.is_available():
             raise MGError("MGSolver needs a CUDA device (no CPU fallback)")
         self.lib = load_library()
@@ -273,9 +278,11 @@ class MGSolver:
         mesh = mg_quad_mesh(nx, ny, 0.0, 0.0, h if h is not None else 1.0 / nx)
         ctx = C.c_void_p()
         self._pc = None if partition is None else partition.c()
-        rc = self.lib.mg_build_hierarchy(C.byref(mesh), p, n_h_levels,
-                                         None if self._pc is None else C.byref(self._pc),
-                                         C.c_void_p(self.stream.cuda_stream), C.byref(ctx))
+        self.nonsymmetric = bool(nonsymmetric)
+        rc = self.lib.mg_build_hierarchy_ex(C.byref(mesh), p, n_h_levels,
+                                            None if self._pc is None else C.byref(self._pc),
+                                            MG_BUILD_NONSYMMETRIC if nonsymmetric else 0,
+                                            C.c_void_p(self.stream.cuda_stream), C.byref(ctx))
         if rc != MG_OK:
             raise MGError(f"mg_build_hierarchy failed: {ERRORS.get(rc, rc)}")
         self.ctx = ctx

@@ -83,6 +83,28 @@ def test_level_counts_match_survey(lib):
         lib.mg_destroy(ctx)
 
 
+def test_nonsymmetric_build_host_only(lib):
+    """MG_BUILD_NONSYMMETRIC (IIPG-H / NIPG-H, Eq. IPG_H): full element maps (m*m
+    doubles, 400 at p=4 vs 210 packed), bad flags refused, no partition."""
+    import ctypes as C
+    from paper_1811_09909_b200.mgdtn import mg_partition, mg_quad_mesh
+    mesh = mg_quad_mesh(256, 256, 0.0, 0.0, 1.0 / 256)
+    sizes = []
+    for flags in (0, 1):
+        ctx = C.c_void_p()
+        assert lib.mg_build_hierarchy_ex(C.byref(mesh), 4, 0, None, flags, None, C.byref(ctx)) == 0
+        nb = C.c_size_t()
+        assert lib.mg_workspace_bytes(ctx, C.byref(nb)) == 0
+        sizes.append(nb.value)
+        lib.mg_destroy(ctx)
+    fine_packed, fine_full = 65536 * 210 * 8, 65536 * 400 * 8
+    assert sizes[1] - sizes[0] >= fine_full - fine_packed
+    ctx = C.c_void_p()
+    assert lib.mg_build_hierarchy_ex(C.byref(mesh), 4, 0, None, 2, None, C.byref(ctx)) == -1
+    part = mg_partition(0, 2, 2, 1, None, 0, None)
+    assert lib.mg_build_hierarchy_ex(C.byref(mesh), 4, 0, C.byref(part), 1, None, C.byref(ctx)) == -9
+
+
 def _imports(path):
     tree = ast.parse(open(path).read())
     for node in ast.walk(tree):

@@ -240,6 +240,29 @@ def make_problem(cfg: Config, with_f: bool = True) -> Problem:
                    None if gD is None else np.ascontiguousarray(gD), exact)
 
 
+def nonsymmetric_problem(cfg: Config, mix: str = "tiles") -> Problem:
+    """The config's recipe (K field, f, g_D) with the nonsymmetric IPDG-H schemes
+    (Eq. IPG_H) on its elements -- the SURVEY 8(f) f2 workload:
+      mix = "nipg" / "iipg": that scheme everywhere;
+      mix = "tiles": 8 x 8 tiles (at least 1 element) cycling HDG, SIPG-H, IIPG-H,
+                     NIPG-H by (I + 2 J) mod 4 (multinumerics).
+    tau = (p+1)(p+2) K_T / h on the IPDG-H elements (the kappa-scaled penalty of
+    PAPER.md:1700-1701, 1391-1392), the config's tau on HDG elements."""
+    pr = make_problem(cfg)
+    n, p = cfg.n, cfg.p
+    ne = n * n
+    if mix in ("nipg", "iipg"):
+        method = np.full(ne, NIPG_H if mix == "nipg" else IIPG_H, dtype=np.int8)
+    else:
+        tile = max(1, n // 8)
+        jj, ii = np.divmod(np.arange(ne), n)
+        method = np.array([HDG, SIPG_H, IIPG_H, NIPG_H], np.int8)[((ii // tile) + 2 * (jj // tile)) % 4]
+    tau = np.where(method == HDG, np.where(pr.method == HDG, pr.tau, 1.0),
+                   (p + 1) * (p + 2) * pr.K * n)
+    return Problem(cfg, pr.K, method, np.ascontiguousarray(tau), pr.f_qp, pr.f_const, pr.gD_qp,
+                   pr.exact)
+
+
 def random_trace_vector(ndof: int, seed: int) -> np.ndarray:
     """x ~ U[-1,1] on every dof (reading Q19); Dirichlet entries are ignored
     by both implementations."""
