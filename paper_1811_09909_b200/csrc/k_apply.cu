@@ -101,45 +101,70 @@ struct TmaCfg {
   static constexpr int CPS = P == 4 ? 2 : P == 3 ? 3 : P == 2 ? 4 : 6;
 };
 
+// tick != nullptr: dynamic chunk scheduling (MGDTN_GRID=dyn).  The CTA's first NST
+// chunks are static (blockIdx.x + k*gridDim.x, prefetched before the PDL wait); every
+// later chunk is a ticket tick[0]++ (+ NST*gridDim.x) taken when its stage frees up, so
+// the SMs that stream faster take more chunks.  Tickets are taken only after the PDL
+// wait (the previous launch on this level / colour, which used the same counter, has
+// then completed), and the last CTA to exit resets the counter for the next launch.
 template <int P, int MODE, bool DOT, int NST, bool XPF = true>
 __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, const double* x,
                                                   double* y, const double* __restrict__ r,
                                                   double* d, int step,
-                                                  double* __restrict__ partials, int early) {
+                                                  double* __restrict__ partials, int early,
+                                                  unsigned* tick) {
   using C = TmaCfg<P>;
   constexpr int K1 = C::K1, M = C::M, NPK = C::NPK;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bars[NST];
+  __shared__ int cid[NST];   // chunk in each stage (-1: none)
   double* stage_buf = reinterpret_cast<double*>(smem_raw);
   const int lane = threadIdx.x;
   const int64_t nec = L.ne >> 1;
   const int nchunk = (int)((nec + 31) >> 5);
   const double* Sbase = L.S + (int64_t)colour * L.nchunk * NPK * 32;
   const uint64_t pol = stream_policy(L.l2keep);
-  // chunks of this CTA: c_k = blockIdx.x + k * gridDim.x
-  const int nmine = (int)blockIdx.x < nchunk ? (nchunk - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  // static chunks of this CTA: c_k = blockIdx.x + k * gridDim.x
+  const int nmine_static =
+      (int)blockIdx.x < nchunk ? (nchunk - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int nmine = tick ? 0x7fffffff : nmine_static;   // dynamic: until a ticket runs out
   if (lane == 0) {
 #pragma unroll
-    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&bars[s], 1);
+      cid[s] = s < nmine_static ? (int)blockIdx.x + s * (int)gridDim.x : -1;
+    }
     fence_mbar_init();
   }
   __syncwarp();
-  auto issue = [&](int k) {   // lane 0: chunk k of this CTA into stage k % NST
-    const int c = (int)blockIdx.x + k * (int)gridDim.x;
+  auto chunk_of = [&](int k) -> int {   // chunk processed at position k (-1: done)
+    if (tick) return cid[k % NST];
+    return k < nmine_static ? (int)blockIdx.x + k * (int)gridDim.x : -1;
+  };
+  auto issue = [&](int k) {   // lane 0: chunk of position k into stage k % NST
     const int s = k % NST;
+    int c;
+    if (tick && k >= NST) {
+      const unsigned t = atomicAdd(tick, 1u) + (unsigned)(NST * gridDim.x);
+      c = t < (unsigned)nchunk ? (int)t : -1;
+      cid[s] = c;
+    } else {
+      c = chunk_of(k);
+    }
+    if (c < 0) return;
     mbar_expect_tx(&bars[s], C::CHUNK_BYTES);
     tma_bulk_g2s(stage_buf + (size_t)s * NPK * 32, Sbase + (int64_t)c * NPK * 32, C::CHUNK_BYTES,
                  &bars[s], pol);
   };
   if (early) {   // S_T is immutable during a solve: prefetch before the dependency wait
     if (lane == 0)
-      for (int k = 0; k < NST && k < nmine; ++k) issue(k);
+      for (int k = 0; k < NST && k < nmine_static; ++k) issue(k);
     pdl_trigger();
     pdl_wait();
   } else {
     pdl_wait();
     if (lane == 0)
-      for (int k = 0; k < NST && k < nmine; ++k) issue(k);
+      for (int k = 0; k < NST && k < nmine_static; ++k) issue(k);
     pdl_trigger();
   }
   double c1 = 0.0, c2 = 0.0;
@@ -158,8 +183,9 @@ __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, 
   auto prefetch = [&](int k) {
 #pragma unroll
     for (int a = 0; a < M; ++a) xn[a] = 0.0;
-    const int64_t s = ((int64_t)blockIdx.x + (int64_t)k * gridDim.x) * 32 + lane;
-    if (k < nmine && s < nec) {
+    const int ck = chunk_of(k);
+    const int64_t s = (int64_t)ck * 32 + lane;
+    if (ck >= 0 && s < nec) {
       int i, j;
       slot_elem(L.nx, colour, s, i, j);
       elem_edges(L.nx, L.ny, i, j, edn, bdn, L.dmask);
@@ -176,7 +202,8 @@ __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, 
   };
   prefetch(0);
   for (int k = 0; k < nmine; ++k) {
-    const int c = (int)blockIdx.x + k * (int)gridDim.x;
+    const int c = chunk_of(k);
+    if (c < 0) break;
     const int64_t s = (int64_t)c * 32 + lane;
     const bool act = s < nec;
     int64_t ed[4];
@@ -203,6 +230,7 @@ __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, 
         fence_proxy_async();
         issue(k + NST);
       }
+      __syncwarp();
       continue;
     }
     if (act) epi_load<K1, MODE>(L, ed, bd, y, r, d, t, dd, itf);   // needed after the matvec only
@@ -225,6 +253,7 @@ __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, 
       fence_proxy_async();
       issue(k + NST);
     }
+    __syncwarp();   // cid of position k + NST visible to the prefetch below
     if (act) epi_store<K1, MODE, DOT>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot, itf);
     if (!XPF) prefetch(k + 1);
   }
@@ -232,6 +261,13 @@ __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
     if (lane == 0) partials[blockIdx.x] = dot;
+  }
+  if (tick && lane == 0) {   // last CTA out resets the ticket counter for the next launch
+    __threadfence();
+    if (atomicAdd(tick + 1, 1u) == gridDim.x - 1u) {
+      atomicExch(tick, 0u);
+      atomicExch(tick + 1, 0u);
+    }
   }
 }
 
@@ -972,6 +1008,25 @@ static void launch_seg(const LevelDev& L, int colour, const double* x, double* y
             partials, pdl ? 1 : 0);
 }
 
+// MGDTN_GRID: how the whole-chunk TMA apply spreads a colour's chunks over its CTAs
+//   bal (default) -- balanced_grid: every CTA the same number of chunks
+//   full          -- 148 x CTAs-per-SM CTAs, chunk c to CTA c mod grid (per-SM balance
+//                    when the CTAs land round-robin on the SMs)
+//   dyn           -- full grid, first NST chunks static, then tickets (dynamic)
+static int grid_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MGDTN_GRID");
+    v = !e ? 0 : std::strcmp(e, "full") == 0 ? 1 : std::strcmp(e, "dyn") == 0 ? 2 : 0;
+  }
+  return v;
+}
+// the ticket counter pair of a level / colour (LevelDev::sync tail, mgdtn.cu layout)
+static unsigned* ticket_of(const LevelDev& L, int colour) {
+  if (grid_mode() != 2 || L.sync == nullptr) return nullptr;
+  return L.sync + 2 + L.nchunk + 2 * colour;
+}
+
 // grid of at most gmax persistent CTAs over n chunks with the work spread evenly:
 // k = ceil(n / gmax) chunks per CTA, ceil(n / k) CTAs (every CTA gets k or k-1)
 static int balanced_grid(int64_t n, int64_t gmax) {
@@ -992,6 +1047,10 @@ int apply_grid_mode(const LevelDev& L, int mode) {
   }
   const int64_t nchunk = (nec + 31) / 32;
   if (use_seg(mode, L.p)) return balanced_grid(nchunk, (int64_t)num_sms() * seg_cps(L.p));
+  if (grid_mode() != 0) {
+    const int64_t g = (int64_t)num_sms() * tma_cps(L.p);
+    return (int)(nchunk < g ? (nchunk > 0 ? nchunk : 1) : g);
+  }
   return balanced_grid(nchunk, 148 * tma_cps(L.p));
 }
 
@@ -1013,7 +1072,7 @@ static void launch_tma_x(const LevelDev& L, int colour, const double* x, double*
     attr_set = true;
   }
   launch_ex(k_apply_tma<P, MODE, DOT, NST, XPF>, grid, 32, smem, pdl, st, L, colour, x, y, r, d,
-            step, partials, pdl ? 1 : 0);
+            step, partials, pdl ? 1 : 0, ticket_of(L, colour));
 }
 
 static bool use_tma2() {   // MGDTN_TMA2=1: two warps per CTA (A/B; measured slower)

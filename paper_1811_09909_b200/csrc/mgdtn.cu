@@ -188,7 +188,7 @@ static void layout(Ctx* c) {
   c->o_meth = take(c->lev[0].d.ne * sizeof(int8_t));
   for (auto& L : c->lev) {
     const LevelDev& d = L.d;
-    L.o_sync = take((size_t)(2 + d.nchunk) * sizeof(unsigned));
+    L.o_sync = take((size_t)(2 + d.nchunk + 4) * sizeof(unsigned));   // + 2 ticket pairs
     L.o_S = take((size_t)2 * d.nchunk * d.npk * 32 * sizeof(double));
     L.o_Dinv = take((size_t)d.nedge * d.k1 * d.k1 * sizeof(double));
     L.o_Dc = take((size_t)d.nchunk * d.ndi * 32 * sizeof(double));
