@@ -490,4 +490,54 @@ int launch_axpby(double a, const double* x, double b, const double* y, double* z
   return 1;
 }
 
+// ---------------------------------------------------------------- GMRES helpers (gmres_impl)
+// modified Gram-Schmidt with device-resident coefficients: the Hessenberg column
+// never round-trips through the host inside an Arnoldi step.  The arithmetic is
+// the host-coefficient version's (k_axpby with b = 1, then (1/||v||) v).
+__global__ void k_axpy_dev(const double* __restrict__ coef, double sign,
+                           const double* __restrict__ x, double* y, int64_t n) {
+  pdl_enter();
+  const double a = sign * coef[0];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = fma(a, x[i], y[i]);
+}
+int launch_axpy_dev(const double* coef, double sign, const double* x, double* y, int64_t n,
+                    cudaStream_t st) {
+  launch_ex(k_axpy_dev, vec_grid(n), 256, 0, true, st, coef, sign, x, y, n);
+  return 1;
+}
+
+// v <- v / sqrt(ss[0]) (no-op when ss[0] <= 0: the Krylov space is exhausted)
+__global__ void k_scale_rsqrt(const double* __restrict__ ss, double* v, int64_t n) {
+  pdl_enter();
+  const double s = ss[0];
+  if (!(s > 0.0)) return;
+  const double a = 1.0 / sqrt(s);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = a * v[i];
+}
+int launch_scale_rsqrt(const double* ss, double* v, int64_t n, cudaStream_t st) {
+  launch_ex(k_scale_rsqrt, vec_grid(n), 256, 0, true, st, ss, v, n);
+  return 1;
+}
+
+// x = sum_{i < m} y[i] V[i*n ..] (in order i = 0, 1, ..: the sequential axpy's rounding)
+__global__ void k_combine(double* x, const double* __restrict__ V, int64_t n,
+                          const double* __restrict__ y, int m) {
+  pdl_enter();
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int i = 0; i < m; ++i) acc = fma(y[i], V[(int64_t)i * n + t], acc);
+    x[t] = acc;
+  }
+}
+int launch_combine(double* x, const double* V, int64_t n, const double* y, int m,
+                   cudaStream_t st) {
+  launch_ex(k_combine, vec_grid(n), 256, 0, true, st, x, V, n, y, m);
+  return 1;
+}
+
 }  // namespace mgdtn

@@ -412,6 +412,11 @@ int launch_copy(double* dst, const double* src, int64_t n, cudaStream_t st);
 int launch_zero(double* dst, int64_t n, cudaStream_t st);
 int launch_copy_masked(const LevelDev& L, double* dst, const double* src, cudaStream_t st);
 int launch_add(double* dst, const double* src, int64_t n, cudaStream_t st);
+int launch_axpy_dev(const double* coef, double sign, const double* x, double* y, int64_t n,
+                    cudaStream_t st);   // y += sign * coef[0] * x (device coefficient)
+int launch_scale_rsqrt(const double* ss, double* v, int64_t n, cudaStream_t st);
+int launch_combine(double* x, const double* V, int64_t n, const double* y, int m,
+                   cudaStream_t st);   // x = sum_i y[i] V_i
 int launch_axpby(double a, const double* x, double b, const double* y, double* z, int64_t n,
                  cudaStream_t st);   // z = a x + b y
 

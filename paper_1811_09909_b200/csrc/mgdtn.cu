@@ -69,6 +69,8 @@ struct Ctx {
   long long launches = 0, last_solve_launches = 0;
   double* pinned = nullptr;
   cudaGraphExec_t gS = nullptr;   // whole PCG solve: prologue + conditional WHILE loop
+  cudaGraphExec_t gV = nullptr;   // one V-cycle, fine L.r -> L.e (GMRES / MG-solver / mg_vcycle)
+  long long nV = 0;               // kernels in gV
   cudaGraphConditionalHandle cond = 0;
   long long nPro = 0, nBody = 0;  // kernels in the prologue / in one loop iteration
   bool use_graphs = true;
@@ -468,6 +470,8 @@ static int upload_static(Ctx* c) {
 static void drop_graphs(Ctx* c) {
   if (c->gS) cudaGraphExecDestroy(c->gS);
   c->gS = nullptr;
+  if (c->gV) cudaGraphExecDestroy(c->gV);
+  c->gV = nullptr;
 }
 
 static int check_device_error(Ctx* c) {
@@ -1010,11 +1014,42 @@ static double gdot(Ctx* c, const double* a, const double* b) {
   return c->pinned[0];
 }
 
+// F.e = B_N F.r: the V-cycle's fixed kernel sequence, replayed from a CUDA graph
+// captured on first use (one GPU, graphs on); eager launches otherwise
+static void run_vcycle(Ctx* c) {
+  if (!c->use_graphs || partitioned(c) || c->st == nullptr) {
+    vcycle_level(c, 0, false);
+    return;
+  }
+  if (!c->gV) {
+    cudaGraph_t g = nullptr;
+    const long long l0 = c->launches;
+    if (cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      vcycle_level(c, 0, false);
+      return;
+    }
+    vcycle_level(c, 0, false);
+    c->nV = c->launches - l0;
+    c->launches = l0;
+    if (cudaStreamEndCapture(c->st, &g) != cudaSuccess || !g ||
+        cudaGraphInstantiate(&c->gV, g, 0) != cudaSuccess) {
+      if (g) cudaGraphDestroy(g);
+      c->gV = nullptr;
+      cudaGetLastError();
+      vcycle_level(c, 0, false);
+      return;
+    }
+    cudaGraphDestroy(g);
+  }
+  cudaGraphLaunch(c->gV, c->st);
+  c->launches += c->nV;
+}
+
 // out = B_N v: one V-cycle of Algorithm 1 from e = 0
 static void precond(Ctx* c, const double* v, double* out) {
   HostLevel& F = c->lev[0];
   c->launches += launch_copy_masked(F.d, F.r, v, c->st);
-  vcycle_level(c, 0, false);
+  run_vcycle(c);
   c->launches += launch_copy(out, F.e, F.d.ndof, c->st);
 }
 
@@ -1084,16 +1119,41 @@ static int gmres_impl(Ctx* c, const double* g, double* x, double tol, int maxit,
   rhs[0] = beta;
   int st = MG_MAXIT, j = 0;
   double rel = 1.0;
+  // one GPU: the Hessenberg column stays on the device through the Gram-Schmidt
+  // sweep (k_axpy_dev / k_scale_rsqrt) and comes back with one copy per step;
+  // x = V y is one k_combine.  Partitioned: dots all-reduced through the host.
+  const bool dev_mgs = !partitioned(c) && maxit + 2 <= HIST_CAP / 2;
+  double* Hd = c->dhist;                  // column j of H (H[j+1][j] as ||w||^2)
+  double* yd = c->dhist + HIST_CAP / 2;   // least-squares coefficients
+  const int vg = vec_grid(n);
+  std::vector<double> hcol(maxit + 2);
   for (j = 0; j < maxit; ++j) {
     apply_full(c, F, Vj(j), c->ap, nullptr);
     precond(c, c->ap, Vj(j + 1));
-    for (int i = 0; i <= j; ++i) {   // modified Gram-Schmidt
-      h(i, j) = gdot(c, Vj(j + 1), Vj(i));
-      c->launches += launch_axpby(-h(i, j), Vj(i), 1.0, Vj(j + 1), Vj(j + 1), n, c->st);
+    double hn;
+    if (dev_mgs) {
+      for (int i = 0; i <= j; ++i) {   // modified Gram-Schmidt
+        c->launches += launch_dot(Vj(j + 1), Vj(i), n, c->part, vg, c->st, &F.d);
+        c->launches += launch_reduce(c->part, vg, Hd, i, 0, nullptr, c->st);
+        c->launches += launch_axpy_dev(Hd + i, -1.0, Vj(i), Vj(j + 1), n, c->st);
+      }
+      c->launches += launch_dot(Vj(j + 1), Vj(j + 1), n, c->part, vg, c->st, &F.d);
+      c->launches += launch_reduce(c->part, vg, Hd, j + 1, 0, nullptr, c->st);
+      c->launches += launch_scale_rsqrt(Hd + j + 1, Vj(j + 1), n, c->st);
+      CK(cudaMemcpyAsync(hcol.data(), Hd, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost,
+                         c->st));
+      CK(cudaStreamSynchronize(c->st));
+      for (int i = 0; i <= j; ++i) h(i, j) = hcol[i];
+      hn = std::sqrt(hcol[j + 1]);
+    } else {
+      for (int i = 0; i <= j; ++i) {   // modified Gram-Schmidt
+        h(i, j) = gdot(c, Vj(j + 1), Vj(i));
+        c->launches += launch_axpby(-h(i, j), Vj(i), 1.0, Vj(j + 1), Vj(j + 1), n, c->st);
+      }
+      hn = std::sqrt(gdot(c, Vj(j + 1), Vj(j + 1)));
+      if (hn > 0) c->launches += launch_axpby(1.0 / hn, Vj(j + 1), 0.0, Vj(j + 1), Vj(j + 1), n, c->st);
     }
-    const double hn = std::sqrt(gdot(c, Vj(j + 1), Vj(j + 1)));
     h(j + 1, j) = hn;
-    if (hn > 0) c->launches += launch_axpby(1.0 / hn, Vj(j + 1), 0.0, Vj(j + 1), Vj(j + 1), n, c->st);
     // least squares min || beta e1 - H y || by Givens rotations on a copy of column j
     std::vector<double> col(j + 2);
     for (int i = 0; i <= j + 1; ++i) col[i] = h(i, j);
@@ -1117,8 +1177,13 @@ static int gmres_impl(Ctx* c, const double* g, double* x, double tol, int maxit,
       y[i] = s / h(i, i);
     }
     // x = V y and the true residual
-    c->launches += launch_zero(x, n, c->st);
-    for (int i = 0; i <= j; ++i) c->launches += launch_axpby(y[i], Vj(i), 1.0, x, x, n, c->st);
+    if (dev_mgs) {
+      CK(cudaMemcpyAsync(yd, y.data(), (j + 1) * sizeof(double), cudaMemcpyHostToDevice, c->st));
+      c->launches += launch_combine(x, V, n, yd, j + 1, c->st);
+    } else {
+      c->launches += launch_zero(x, n, c->st);
+      for (int i = 0; i <= j; ++i) c->launches += launch_axpby(y[i], Vj(i), 1.0, x, x, n, c->st);
+    }
     apply_full(c, F, x, c->ap, nullptr);
     c->launches += launch_axpby(1.0, gb, -1.0, c->ap, c->pv, n, c->st);
     rel = std::sqrt(gdot(c, c->pv, c->pv)) / gn;
@@ -1479,7 +1544,7 @@ int mg_vcycle(void* ctx, const double* r, double* z) {
   if (!c->setup_done) return fail(c, MG_ERR_STATE, "setup first");
   HostLevel& F = c->lev[0];
   c->launches += launch_copy_masked(F.d, F.r, r, c->st);
-  vcycle_level(c, 0, false);
+  run_vcycle(c);
   c->launches += launch_copy(z, F.e, F.d.ndof, c->st);
   CK(cudaGetLastError());
   return MG_OK;
