@@ -428,28 +428,33 @@ __global__ void __launch_bounds__(64) k_apply_tma2(const LevelDev L, int colour,
 // whose in-flight bytes drop to one chunk while the other is being consumed
 // (ncu: k_apply_tma at config 2 stalls on the stage wait and reaches 44% of
 // DRAM peak).
-template <int P>
+// NSYM: a nonsymmetric context's full row-major maps (npk = m*m, Eq. IPG_H); the
+// epilogue then takes D_e^-1 from the SoA blocks (epi_store), not from the ring.
+template <int P, bool NSYM = false>
 struct SegCfg {
-  static constexpr int K1 = P + 1, M = 4 * K1, NPK = M * (M + 1) / 2;
+  static constexpr int K1 = P + 1, M = 4 * K1, NPK = NSYM ? M * M : M * (M + 1) / 2;
   static constexpr int NDE = K1 * (K1 + 1) / 2;   // packed D_e^-1 entries per edge
   static constexpr int NDI = 4 * NDE;             // per colour-1 element
-  static constexpr int SEGR = P == 4 ? 30 : P == 3 ? 17 : P == 2 ? 13 : 12;   // rows | NPK
+  static constexpr int SEGR = NSYM ? (P == 4 ? 25 : 16)
+                                   : (P == 4 ? 30 : P == 3 ? 17 : P == 2 ? 13 : 12);   // rows | NPK
   static constexpr int NSEG_S = NPK / SEGR;
   static constexpr int NSEG_D = (NDI + SEGR - 1) / SEGR;
   static constexpr int SEG_BYTES = SEGR * 32 * 8;
-  static constexpr int NSLOT = P == 4 ? 14 : P == 3 ? 16 : P == 2 ? 16 : 12;
+  static constexpr int NSLOT = NSYM ? (P == 4 ? 16 : P == 3 ? 16 : P == 2 ? 12 : 8)
+                                    : (P == 4 ? 14 : P == 3 ? 16 : P == 2 ? 16 : 12);
   static constexpr int CPS = P == 4 ? 2 : P == 3 ? 3 : P == 2 ? 4 : 6;
   static_assert(NPK % SEGR == 0, "segment rows must divide the packed matrix");
 };
 
-template <int P, int MODE, bool DOT>
+template <int P, int MODE, bool DOT, bool NSYM = false>
 __global__ void __launch_bounds__(32) k_apply_seg(const LevelDev L, int colour, const double* x,
                                                   double* y, const double* __restrict__ r,
                                                   double* d, int step,
                                                   double* __restrict__ partials, int early) {
-  using C = SegCfg<P>;
+  using C = SegCfg<P, NSYM>;
   constexpr int K1 = C::K1, M = C::M, NPK = C::NPK, SEGR = C::SEGR, NSLOT = C::NSLOT;
-  constexpr bool HASD = (MODE == AM_SMOOTH || MODE == AM_DINV || MODE == AM_GSC);   // + D_e^-1
+  constexpr bool HASD =
+      !NSYM && (MODE == AM_SMOOTH || MODE == AM_DINV || MODE == AM_GSC);   // + D_e^-1
   constexpr int NS = C::NSEG_S + (HASD ? C::NSEG_D : 0);          // segments per chunk
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bars[NSLOT];
@@ -540,22 +545,35 @@ __global__ void __launch_bounds__(32) k_apply_seg(const LevelDev L, int colour, 
     }
     const int g0 = k * NS;
     const double* Sp = nullptr;
+    if (NSYM) {
 #pragma unroll
-    for (int a = 0; a < M; ++a) {
+      for (int a = 0; a < M; ++a) {
 #pragma unroll
-      for (int bb = a; bb < M; ++bb) {
-        const int kk = a * (2 * M - a + 1) / 2 + (bb - a);
-        if (kk % SEGR == 0) Sp = wait_seg(g0 + kk / SEGR);
-        const double sv = Sp[(kk % SEGR) * 32];
-        yv[a] = fma(sv, xv[bb], yv[a]);
-        if (bb != a) yv[bb] = fma(sv, xv[a], yv[bb]);
-        if (kk % SEGR == SEGR - 1) release(g0 + kk / SEGR);
+        for (int bb = 0; bb < M; ++bb) {
+          const int kk = a * M + bb;
+          if (kk % SEGR == 0) Sp = wait_seg(g0 + kk / SEGR);
+          yv[a] = fma(Sp[(kk % SEGR) * 32], xv[bb], yv[a]);
+          if (kk % SEGR == SEGR - 1) release(g0 + kk / SEGR);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < M; ++a) {
+#pragma unroll
+        for (int bb = a; bb < M; ++bb) {
+          const int kk = a * (2 * M - a + 1) / 2 + (bb - a);
+          if (kk % SEGR == 0) Sp = wait_seg(g0 + kk / SEGR);
+          const double sv = Sp[(kk % SEGR) * 32];
+          yv[a] = fma(sv, xv[bb], yv[a]);
+          if (bb != a) yv[bb] = fma(sv, xv[a], yv[bb]);
+          if (kk % SEGR == SEGR - 1) release(g0 + kk / SEGR);
+        }
       }
     }
     if (!HASD) {
       if (act) epi_store<K1, MODE, DOT>(L, ed, bd, xv, yv, t, dd, x, y, d, step, c1, c2, dot, itf);
       continue;
-    }
+    } else {
     // smoothing / power-iteration epilogue with D_e^-1 from the ring (packed upper
     // triangle per edge, rows f*NDE + pk(a,b) of the colour-1 element's record)
     const double* Dp[C::NSEG_D];
@@ -617,6 +635,7 @@ __global__ void __launch_bounds__(32) k_apply_seg(const LevelDev L, int colour, 
     }
 #pragma unroll
     for (int q = 0; q < C::NSEG_D; ++q) release(g0 + C::NSEG_S + q);
+    }
   }
   if (DOT) {
 #pragma unroll
@@ -1027,6 +1046,38 @@ static unsigned* ticket_of(const LevelDev& L, int colour) {
   return L.sync + 2 + L.nchunk + 2 * colour;
 }
 
+// nonsymmetric context's apply: MGDTN_NS_APPLY = seg (default, full-storage segmented
+// ring) | ldg (thread per element, direct loads; A/B)
+static bool ns_use_ldg() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MGDTN_NS_APPLY");
+    v = (e && std::strcmp(e, "ldg") == 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+template <int P, int MODE, bool DOT>
+static int seg_ns_resident() {
+  static int v = 0;
+  if (v == 0) {
+    using C = SegCfg<P, true>;
+    const size_t smem = (size_t)C::NSLOT * C::SEG_BYTES;
+    cudaFuncSetAttribute(k_apply_seg<P, MODE, DOT, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_apply_seg<P, MODE, DOT, true>, 32, smem);
+    v = nb > 0 ? nb : 1;
+  }
+  return v;
+}
+static int seg_ns_cps(int p) {
+  const int c = p == 4 ? SegCfg<4, true>::CPS : p == 3 ? SegCfg<3, true>::CPS
+                : p == 2 ? SegCfg<2, true>::CPS : SegCfg<1, true>::CPS;
+  const int res = p == 4 ? seg_ns_resident<4, AM_W0, false>() : p == 3 ? seg_ns_resident<3, AM_W0, false>()
+                  : p == 2 ? seg_ns_resident<2, AM_W0, false>() : seg_ns_resident<1, AM_W0, false>();
+  return c < res ? c : res;
+}
+
 // grid of at most gmax persistent CTAs over n chunks with the work spread evenly:
 // k = ceil(n / gmax) chunks per CTA, ceil(n / k) CTAs (every CTA gets k or k-1)
 static int balanced_grid(int64_t n, int64_t gmax) {
@@ -1040,6 +1091,8 @@ int apply_grid(const LevelDev& L) { return apply_grid_mode(L, AM_APPLY); }
 
 int apply_grid_mode(const LevelDev& L, int mode) {
   const int64_t nec = L.ne / 2;
+  if (L.ns && !ns_use_ldg() && !use_ldg())
+    return balanced_grid((nec + 31) / 32, (int64_t)num_sms() * seg_ns_cps(L.p));
   if (use_ldg() || L.ns) {
     int64_t g = (nec + 127) / 128;
     const int64_t gmax = 148 * 8;
@@ -1108,9 +1161,16 @@ static void launch_one(const LevelDev& L, int colour, const double* x, double* y
                        double* d, int step, double* partials, int grid, bool pdl,
                        cudaStream_t st) {
   if (L.ns) {   // nonsymmetric context: full-storage apply (no LU-SGS / power iteration there)
-    if (MODE != AM_GSC && MODE != AM_DINV)
+    if (MODE == AM_GSC || MODE == AM_DINV) return;
+    if (ns_use_ldg() || use_ldg()) {
       launch_ex(k_apply_ldg<P, MODE, DOT, true>, grid, 128, 0, pdl, st, L, colour, x, y, r, d,
                 step, partials, 0);
+    } else {
+      using C = SegCfg<P, true>;
+      seg_ns_resident<P, MODE, DOT>();   // sets the dynamic smem attribute once
+      launch_ex(k_apply_seg<P, MODE, DOT, true>, grid, 32, (size_t)C::NSLOT * C::SEG_BYTES, pdl,
+                st, L, colour, x, y, r, d, step, partials, pdl ? 1 : 0);
+    }
     return;
   }
   if (MODE == AM_GSC) {   // colour sweeps exist in the segmented-ring kernel only
