@@ -160,6 +160,44 @@ def reference_arm(args, cfg):
     return 0
 
 
+def bytes_per_iteration(s, sm, ns=False, krylov="pcg"):
+    """Modelled algorithmic bytes of one solver iteration (SURVEY 8(d) "per PCG
+    iteration"): what the method must move, each operand once per use.
+      per apply on level l: S_T (packed m(m+1)/2 or, nonsymmetric, m^2 doubles per
+        element) + 16 B per trace dof (x read, y written);
+      per smoothing step: an apply + D_e^-1 (packed, k1(k1+1)/2 doubles per edge) +
+        r read and e read/written (24 B/dof; Chebyshev d read/written +16 B/dof);
+      per non-coarsest level and V-cycle: nu_pre + nu_post smoothing steps (the first
+        pre-step from e = 0 has no apply), one residual apply (+8 B/dof for r), the
+        transfers (restriction reads the residual, prolongation reads / writes e:
+        24 B/dof);
+      per Krylov iteration: one fine apply + ~6 fine vector passes (PCG x, r, p, z
+        updates and dots; GMRES: its Gram-Schmidt passes are counted at 2 per basis
+        vector by the caller's iteration count, approximated here by 6)."""
+    tot = 0
+    nl = s.nlevels
+    for level in range(nl, 1, -1):
+        li = s.level_info(level)
+        ne, p, ndof = li["nx"] * li["ny"], li["p"], li["ndof"]
+        m, k1 = 4 * (p + 1), p + 1
+        npk = m * m if ns else m * (m + 1) // 2
+        S = 8 * ne * npk
+        apply_b = S + 16 * ndof
+        nedge = ndof // k1
+        D = 8 * nedge * k1 * (k1 + 1) // 2
+        steps = sm.nu_pre + sm.nu_post
+        if getattr(sm, "nu_doubling", 0):
+            steps *= 2 ** (nl - level)
+        vec = 24 + (16 if sm.kind == 1 else 0)
+        tot += steps * (apply_b + D + vec * ndof) - (apply_b if sm.nu_pre > 0 else 0)
+        tot += apply_b + 8 * ndof + 24 * ndof
+    fine = s.level_info(nl)
+    m = 4 * (fine["p"] + 1)
+    npk = m * m if ns else m * (m + 1) // 2
+    tot += 8 * fine["nx"] * fine["ny"] * npk + 16 * fine["ndof"] + 6 * 8 * fine["ndof"]
+    return tot
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -300,6 +338,12 @@ def main():
     peaks = _peaks()
     peak = peaks.get("hbm_gbs", 6650.0)
     achieved = alg_bytes / (t_apply * 1e-3) / 1e9
+    bpi = bytes_per_iteration(s, sm, ns)
+    t_iter = t_solve / max(1, info["iters"])
+    solve_roof = {"bytes_per_iter": int(bpi), "ms_per_iter": t_iter,
+                  "achieved_gbs": bpi / (t_iter * 1e-3) / 1e9,
+                  "frac": bpi / (t_iter * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0),
+                  "model": "bench.bytes_per_iteration (SURVEY 8(d) per-iteration byte model)"}
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -400,6 +444,7 @@ def main():
                          "alg_bytes_per_apply": alg_bytes,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in peaks
                          else "fallback 6650 GB/s (B200_PROFILING.md)"},
+            "solve_roofline": solve_roof,
             "clocks": ck, "e2e": e2e, "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
