@@ -231,10 +231,12 @@ __device__ double cluster_sum(cg::cluster_group& cl, double v, double* part) {
 
 // Chebyshev lambda_max of D_B^-1 A_k (Q11) for every tail level except the
 // coarsest: power iteration v <- D^-1 A v (AM_DINV epilogue, in place), then
-// lambda = safety * v.Av / v.Dv and the Chebyshev coefficients.
+// lambda = safety * v.Av / v.Dv and the Chebyshev coefficients.  The levels'
+// iterations are independent: one cluster per level, all running concurrently,
+// each with its own reduction scratch part[li * cluster size ..].
 __global__ void __launch_bounds__(TAIL_TPB, 1)
     k_tail_lmax(const __grid_constant__ TailParams P, int iters, double safety, double ratio,
-                int nu_max, double* part) {
+                int nu_max, double* part_all) {
   cg::cluster_group cl = cg::this_cluster();
   const int64_t t0 = (int64_t)cl.block_rank() * TAIL_TPB + threadIdx.x;
   const int64_t nt = (int64_t)cl.num_blocks() * TAIL_TPB;
@@ -243,7 +245,10 @@ __global__ void __launch_bounds__(TAIL_TPB, 1)
     if (single) __syncthreads();
     else cl.sync();
   };
-  for (int li = 0; li < P.nlev - 1; ++li) {
+  {
+    const int li = (int)(blockIdx.x / cl.num_blocks());
+    if (li >= P.nlev - 1) return;
+    double* part = part_all + (int64_t)li * cl.num_blocks();
     const TailLevel& L = P.lev[li];
     pow_init_body(L.d, L.e, t0, nt);
     sync();
@@ -304,7 +309,7 @@ int launch_tail_lmax(const TailParams& P, int iters, double safety, double ratio
                      double* part, cudaStream_t st) {
   const int cs = tail_cluster_size();
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(cs);
+  cfg.gridDim = dim3(cs * (P.nlev > 1 ? P.nlev - 1 : 1));   // one cluster per level
   cfg.blockDim = dim3(TAIL_TPB);
   cfg.stream = st;
   cudaLaunchAttribute at[1];

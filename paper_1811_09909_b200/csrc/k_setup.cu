@@ -470,9 +470,82 @@ __global__ void __launch_bounds__(128) k_p_coarsen(LevelDev F, LevelDev C,
   }
 }
 
+// The same product with every stored entry of S_T loaded exactly once (210 loads per
+// element at p = 4 instead of 400): entry (a, b) of edge blocks (f, g) is scattered
+// straight into the coarse entries (2f + al, 2g + be) it feeds, accumulated in 36
+// (NS: 64) registers.  Loads are independent, so a thread keeps many in flight.
+template <int P, bool NS>
+__global__ void __launch_bounds__(128) k_p_coarsen_acc(LevelDev F, LevelDev C,
+                                                       const double* __restrict__ Jp) {
+  constexpr int K1 = P + 1, M = 4 * K1, NC = NS ? 64 : 36;
+  double J[K1][2];
+#pragma unroll
+  for (int a = 0; a < K1; ++a) {
+    J[a][0] = Jp[a * 2];
+    J[a][1] = Jp[a * 2 + 1];
+  }
+  const int64_t nec = F.ne >> 1;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < 2 * nec;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int colour = (int)(t / nec);
+    const int64_t s = t - colour * nec;
+    const double* src = F.S + s_offset(F.nchunk, F.npk, colour, s, 0);
+    double* dst = C.S + s_offset(C.nchunk, C.npk, colour, s, 0);
+    double acc[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) acc[q] = 0.0;
+#pragma unroll
+    for (int a = 0; a < M; ++a) {
+#pragma unroll
+      for (int b = NS ? 0 : a; b < M; ++b) {
+        const int f = a / K1, al = a % K1, g = b / K1, bl = b % K1;
+        const double v = __ldg(src + (int64_t)(NS ? a * M + b : pk_index(a, b, M)) * 32);
+#pragma unroll
+        for (int ca = 0; ca < 2; ++ca)
+#pragma unroll
+          for (int cb = 0; cb < 2; ++cb) {
+            const int A = 2 * f + ca, B = 2 * g + cb;
+            if (NS) {
+              acc[A * 8 + B] = fma(J[al][ca] * J[bl][cb], v, acc[A * 8 + B]);
+            } else if (f < g) {   // off-diagonal edge blocks: a < b always
+              acc[pk_index(A, B, 8)] = fma(J[al][ca] * J[bl][cb], v, acc[pk_index(A, B, 8)]);
+            } else if (A <= B) {  // same edge: the pair (a, b) and, if a != b, (b, a)
+              acc[pk_index(A, B, 8)] = fma(J[al][ca] * J[bl][cb], v, acc[pk_index(A, B, 8)]);
+              if (a != b)
+                acc[pk_index(A, B, 8)] = fma(J[bl][ca] * J[al][cb], v, acc[pk_index(A, B, 8)]);
+            }
+          }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NC; ++q) dst[(int64_t)q * 32] = acc[q];
+  }
+}
+
 int launch_p_coarsen(const LevelDev& F, const LevelDev& C, const double* Jp, cudaStream_t st) {
   int64_t n = F.ne;
   int grid = (int)((n + 127) / 128 < 148 * 16 ? (n + 127) / 128 : 148 * 16);
+  static int v = -1;   // MGDTN_PCOARSEN=1: the row-block kernel (A/B)
+  if (v < 0) {
+    const char* e = std::getenv("MGDTN_PCOARSEN");
+    v = e ? std::atoi(e) : 2;
+  }
+  if (v == 2) {
+    if (F.ns) {
+      switch (F.p) {
+        case 2: k_p_coarsen_acc<2, true><<<grid, 128, 0, st>>>(F, C, Jp); break;
+        case 3: k_p_coarsen_acc<3, true><<<grid, 128, 0, st>>>(F, C, Jp); break;
+        default: k_p_coarsen_acc<4, true><<<grid, 128, 0, st>>>(F, C, Jp); break;
+      }
+    } else {
+      switch (F.p) {
+        case 2: k_p_coarsen_acc<2, false><<<grid, 128, 0, st>>>(F, C, Jp); break;
+        case 3: k_p_coarsen_acc<3, false><<<grid, 128, 0, st>>>(F, C, Jp); break;
+        default: k_p_coarsen_acc<4, false><<<grid, 128, 0, st>>>(F, C, Jp); break;
+      }
+    }
+    return 1;
+  }
   if (F.ns) {
     switch (F.p) {
       case 2: k_p_coarsen<2, true><<<grid, 128, 0, st>>>(F, C, Jp); break;
@@ -619,49 +692,45 @@ __global__ void __launch_bounds__(32 * AGG_WARPS) k_agglomerate(LevelDev F, Leve
       __syncwarp();
       continue;
     }
-    // Cholesky of Kr_II (8x8, lower, in Sc)
-    for (int q = lane; q < 64; q += 32) Sc[q] = Kr[(q >> 3) * 16 + (q & 7)];
-    __syncwarp();
-    bool ok = true;
-    if (lane == 0) {
-      for (int jc = 0; jc < 8; ++jc) {
-        double d = Sc[jc * 8 + jc];
-        for (int k = 0; k < jc; ++k) d -= Sc[jc * 8 + k] * Sc[jc * 8 + k];
-        if (!(d > 0.0)) { ok = false; d = 1e-300; }
-        d = sqrt(d);
-        Sc[jc * 8 + jc] = d;
-        for (int i2 = jc + 1; i2 < 8; ++i2) {
-          double sacc = Sc[i2 * 8 + jc];
-          for (int k = 0; k < jc; ++k) sacc -= Sc[i2 * 8 + k] * Sc[jc * 8 + k];
-          Sc[i2 * 8 + jc] = sacc / d;
-        }
-      }
-      if (!ok) report_error(err, -4, M);
+    // A_II^-1 and A_II^-1 Kr_IC by Gauss-Jordan on [Kr_II | I | Kr_IC] (8 x 24, no
+    // pivoting: A_II is SPD), all lanes per elimination step: left 16 columns in G
+    // (row stride 16), right 8 in U (row stride 16).  Every lane reads its entries,
+    // the pivot row and the pivot column before any lane writes (one __syncwarp).
+    for (int q = lane; q < 128; q += 32) {
+      const int r = q >> 4, j = q & 15;
+      G[q] = j < 8 ? Kr[r * 16 + j] : (j - 8 == r ? 1.0 : 0.0);
+      U[q] = j < 8 ? Kr[r * 16 + 8 + j] : 0.0;
     }
     __syncwarp();
-    // columns: lanes 0..7 -> A_II^-1 e_col ; lanes 8..15 -> A_II^-1 Kr_IC[:, col]
-    if (lane < 16) {
-      double v[8];
-      for (int a = 0; a < 8; ++a)
-        v[a] = lane < 8 ? (a == lane ? 1.0 : 0.0) : Kr[a * 16 + 8 + (lane - 8)];
-      for (int a = 0; a < 8; ++a) {
-        double sacc = v[a];
-        for (int k = 0; k < a; ++k) sacc -= Sc[a * 8 + k] * v[k];
-        v[a] = sacc / Sc[a * 8 + a];
+    bool ok = true;
+    for (int k = 0; k < 8; ++k) {
+      const double piv = G[k * 16 + k];
+      if (!(piv > 0.0)) ok = false;
+      const double ipiv = piv > 0.0 ? 1.0 / piv : 0.0;
+      double nv[6];
+#pragma unroll
+      for (int u = 0; u < 6; ++u) {   // 192 entries, 6 per lane
+        const int q = lane + 32 * u, r = q / 24, j = q - (q / 24) * 24;
+        double* X = j < 16 ? G + r * 16 + j : U + r * 16 + (j - 16);
+        const double pk = (j < 16 ? G[k * 16 + j] : U[k * 16 + (j - 16)]) * ipiv;
+        nv[u] = r == k ? pk : fma(-G[r * 16 + k], pk, *X);
       }
-      for (int a = 7; a >= 0; --a) {
-        double sacc = v[a];
-        for (int k = a + 1; k < 8; ++k) sacc -= Sc[k * 8 + a] * v[k];
-        v[a] = sacc / Sc[a * 8 + a];
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < 6; ++u) {
+        const int q = lane + 32 * u, r = q / 24, j = q - (q / 24) * 24;
+        double* X = j < 16 ? G + r * 16 + j : U + r * 16 + (j - 16);
+        *X = nv[u];
       }
-      if (lane < 8) {
-        for (int a = 0; a < 8; ++a) KIIinv[M * 64 + a * 8 + lane] = v[a];
-      } else {
-        for (int a = 0; a < 8; ++a) {
-          Pm[M * 64 + a * 8 + (lane - 8)] = -v[a];
-          U[a * 16 + (lane - 8)] = -v[a];   // keep P_M for S_c
-        }
-      }
+      __syncwarp();
+    }
+    if (!ok && lane == 0) report_error(err, -4, M);
+    for (int q = lane; q < 64; q += 32) {
+      const int a = q >> 3, b = q & 7;
+      KIIinv[M * 64 + q] = G[a * 16 + 8 + b];
+      const double pm = -U[a * 16 + b];
+      Pm[M * 64 + q] = pm;
+      U[a * 16 + b] = pm;   // keep P_M for S_c
     }
     __syncwarp();
     // S_c = Kr_CC + Kr_IC^T P_M, packed upper (36), into the coarse storage
