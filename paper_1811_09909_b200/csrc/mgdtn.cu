@@ -71,6 +71,9 @@ struct Ctx {
   cudaGraphExec_t gS = nullptr;   // whole PCG solve: prologue + conditional WHILE loop
   cudaGraphExec_t gV = nullptr;   // one V-cycle, fine L.r -> L.e (GMRES / MG-solver / mg_vcycle)
   long long nV = 0;               // kernels in gV
+  cudaGraphExec_t gU = nullptr;   // the whole setup after the input copies (forked streams as
+  long long nU = 0;               // graph branches); captured for the smoother config gU_sm
+  mg_smoother_cfg gU_sm{};
   cudaGraphConditionalHandle cond = 0;
   long long nPro = 0, nBody = 0;  // kernels in the prologue / in one loop iteration
   bool use_graphs = true;
@@ -472,6 +475,8 @@ static void drop_graphs(Ctx* c) {
   c->gS = nullptr;
   if (c->gV) cudaGraphExecDestroy(c->gV);
   c->gV = nullptr;
+  if (c->gU) cudaGraphExecDestroy(c->gU);
+  c->gU = nullptr;
 }
 
 static int check_device_error(Ctx* c) {
@@ -678,14 +683,10 @@ static void vcycle_level(Ctx* c, int li, bool first_done) {
 }
 
 // ---------------------------------------------------------------- setup
-static int setup_impl(Ctx* c, const double* K, const int8_t* method, const double* tau) {
+// everything of mg_setup_dtn after the input copies (reads Kc / tauc / methc only), on c->st
+static int setup_body(Ctx* c) {
   cudaStream_t st = c->st;
-  CK(cudaMemsetAsync(c->err, 0, sizeof(DevError), st));
   HostLevel& F = c->lev[0];
-  const int64_t ne = F.d.ne;
-  CK(cudaMemcpyAsync(c->Kc, K, ne * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemcpyAsync(c->tauc, tau, ne * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemcpyAsync(c->methc, method, ne * sizeof(int8_t), cudaMemcpyDeviceToDevice, st));
   c->launches += launch_local_dtn(F.d, c->refdev, F.h, c->Kc, c->methc, c->tauc, c->err, st);
   const int nlev = (int)c->lev.size();
   const int numax = MAX_NU;   // coefficients for any step count (mg_smooth may exceed nu)
@@ -694,35 +695,27 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
   // iteration needs only that level's operator and edge blocks: on one GPU it is
   // forked onto its own stream (own scratch) as soon as they exist, so it overlaps
   // the coarsening of the levels below (MGDTN_SETUP_STREAMS=0: in sequence).
+  // A level's whole smoother setup (edge blocks, their packed copy, the coefficients or
+  // the Chebyshev power iteration) needs only that level's operator: on one GPU it is
+  // forked onto its own stream as soon as the operator exists, so the main stream goes
+  // straight on to the next coarsening (the critical path is then the coarsening chain
+  // and the tail).  Tail levels stay on the main stream (k_tail_lmax / k_tail_basis
+  // read their blocks).  MGDTN_SETUP_STREAMS=0: everything in sequence.
   const bool cheb = c->sm.kind == MG_SMOOTH_CHEBYSHEV;
-  const bool fork = cheb && !partitioned(c) && env_or("MGDTN_SETUP_STREAMS", 1) != 0;
+  const bool fork = !partitioned(c) && env_or("MGDTN_SETUP_STREAMS", 1) != 0;
+  auto in_tail = [&](int li) { return c->tail_start >= 0 && li >= c->tail_start; };
   auto is_pow = [&](int li) {
-    return cheb && li < nlev - 1 && !(c->tail_lmax && c->tail_start >= 0 && li >= c->tail_start);
+    return cheb && li < nlev - 1 && !(c->tail_lmax && in_tail(li));
   };
+  auto forked = [&](int li) { return fork && li < nlev - 1 && !in_tail(li); };
   int npow = 0;
-  for (int li = 0; li < nlev - 1; ++li) npow += is_pow(li) ? 1 : 0;
-  if (fork) {
-    while ((int)c->side.size() < npow) {
-      cudaStream_t sx;
-      cudaEvent_t ex, fx;
-      CK(cudaStreamCreateWithFlags(&sx, cudaStreamNonBlocking));
-      CK(cudaEventCreateWithFlags(&ex, cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&fx, cudaEventDisableTiming));
-      c->side.push_back(sx);
-      c->side_ev.push_back(ex);
-      c->fork_evs.push_back(fx);
-    }
-  }
-  int q = 0;   // forked power iterations so far
-  auto power_iteration = [&](int li) -> int {
+  for (int li = 0; li < nlev - 1; ++li) npow += forked(li) ? 1 : 0;
+  if (fork && (int)c->side.size() < npow) return fail(c, MG_ERR_STATE, "side streams missing");
+  int q = 0;   // forked levels so far
+  auto power_iteration = [&](int li) -> int {   // on c->st
     HostLevel& L = c->lev[li];
-    double* part = fork ? L.lpart : c->part;
-    double* sc = fork ? L.lpart + c->npart : c->sscal;
-    if (fork) {
-      CK(cudaEventRecord(c->fork_evs[q], st));
-      c->st = c->side[q];
-      CK(cudaStreamWaitEvent(c->st, c->fork_evs[q], 0));
-    }
+    double* part = forked(li) ? L.lpart : c->part;
+    double* sc = forked(li) ? L.lpart + c->npart : c->sscal;
     c->launches += launch_pow_init(L.d, L.e, c->st);
     for (int it = 0; it < c->sm.lmax_iters; ++it) {
       const bool last = it + 1 == c->sm.lmax_iters;
@@ -733,28 +726,37 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
     reduce_scal(c, part, apply_parts(L.d, AM_APPLY), sc, 8, 0);  // v.Av
     c->launches += launch_lmax_finish(sc, c->sm.lmax_safety, c->sm.cheb_ratio, numax, L.lam,
                                       L.d.coef, c->st);
-    if (fork) {
+    return MG_OK;
+  };
+  auto smoother_setup = [&](int li) -> int {   // level li's operator is complete on st
+    HostLevel& L = c->lev[li];
+    const bool fk = forked(li);
+    if (fk) {
+      CK(cudaEventRecord(c->fork_evs[q], st));
+      c->st = c->side[q];
+      CK(cudaStreamWaitEvent(c->st, c->fork_evs[q], 0));
+    }
+    L.d.smoother = c->sm.kind;
+    c->launches += launch_edge_blocks(L.d, c->err, c->st);
+    if (L.d.imask) {   // interface edge blocks: D_e = D_own + D_remote, then inverted
+      c->launches += launch_eblk_pack(L.d, c->hsend, c->st);
+      halo_exchange(c, L.d, eblk_stride(L.d), L.d.k1 * L.d.k1);
+      c->launches += launch_eblk_finish(L.d, c->hrecv, c->err, c->st);
+    }
+    if (!c->ns) c->launches += launch_dinv_pack(L.d, c->st);
+    if (!cheb) c->launches += launch_set_bj_coef(c->sm.omega, L.d.coef, c->st);
+    if (is_pow(li)) RC(power_iteration(li));
+    if (fk) {
       CK(cudaEventRecord(c->side_ev[q], c->st));
       c->st = st;
+      ++q;
     }
-    ++q;
     return MG_OK;
   };
   for (int li = 0; li < nlev; ++li) {
     HostLevel& L = c->lev[li];
     // smoother setup of level li (its operator is complete on st)
-    if (li < nlev - 1) {
-      L.d.smoother = c->sm.kind;
-      c->launches += launch_edge_blocks(L.d, c->err, st);
-      if (L.d.imask) {   // interface edge blocks: D_e = D_own + D_remote, then inverted
-        c->launches += launch_eblk_pack(L.d, c->hsend, st);
-        halo_exchange(c, L.d, eblk_stride(L.d), L.d.k1 * L.d.k1);
-        c->launches += launch_eblk_finish(L.d, c->hrecv, c->err, st);
-      }
-      if (!c->ns) c->launches += launch_dinv_pack(L.d, st);
-      if (!cheb) c->launches += launch_set_bj_coef(c->sm.omega, L.d.coef, st);
-      if (is_pow(li)) RC(power_iteration(li));
-    }
+    if (li < nlev - 1) RC(smoother_setup(li));
     if (li + 1 >= nlev) break;
     // coarsening li -> li + 1
     HostLevel& C = c->lev[li + 1];
@@ -812,6 +814,70 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
   }
   if (use_basis && !basis_early) tail_basis();
   CK(cudaGetLastError());
+  return MG_OK;
+}
+
+static bool same_smoother(const mg_smoother_cfg& a, const mg_smoother_cfg& b) {
+  return a.kind == b.kind && a.nu_pre == b.nu_pre && a.nu_post == b.nu_post &&
+         a.omega == b.omega && a.cheb_ratio == b.cheb_ratio && a.lmax_iters == b.lmax_iters &&
+         a.lmax_safety == b.lmax_safety && a.nu_doubling == b.nu_doubling;
+}
+
+// mg_setup_dtn: copy the element data, then the setup body -- replayed from a CUDA
+// graph on one GPU (its ~300 launches cost one graph launch of host time; the forked
+// smoother setups become parallel graph branches), eager otherwise
+static int setup_impl(Ctx* c, const double* K, const int8_t* method, const double* tau) {
+  cudaStream_t st = c->st;
+  CK(cudaMemsetAsync(c->err, 0, sizeof(DevError), st));
+  HostLevel& F = c->lev[0];
+  const int64_t ne = F.d.ne;
+  CK(cudaMemcpyAsync(c->Kc, K, ne * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(c->tauc, tau, ne * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(c->methc, method, ne * sizeof(int8_t), cudaMemcpyDeviceToDevice, st));
+  if (!partitioned(c)) {   // side streams of the forked smoother setups (created outside capture)
+    const int need = (int)c->lev.size();
+    while ((int)c->side.size() < need) {
+      cudaStream_t sx;
+      cudaEvent_t ex, fx;
+      CK(cudaStreamCreateWithFlags(&sx, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ex, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&fx, cudaEventDisableTiming));
+      c->side.push_back(sx);
+      c->side_ev.push_back(ex);
+      c->fork_evs.push_back(fx);
+    }
+  }
+  const bool graph = c->use_graphs && !partitioned(c) && st != nullptr &&
+                     env_or("MGDTN_SETUP_GRAPH", 1) != 0;
+  if (graph) {
+    if (c->gU && !same_smoother(c->gU_sm, c->sm)) {
+      cudaGraphExecDestroy(c->gU);
+      c->gU = nullptr;
+    }
+    if (!c->gU) {
+      const long long l0 = c->launches;
+      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      const int rc = setup_body(c);
+      c->st = st;
+      cudaGraph_t g = nullptr;
+      const cudaError_t e = cudaStreamEndCapture(st, &g);
+      c->nU = c->launches - l0;
+      c->launches = l0;
+      if (rc != MG_OK) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      CK(e);
+      const cudaError_t e2 = cudaGraphInstantiate(&c->gU, g, 0);
+      cudaGraphDestroy(g);
+      CK(e2);
+      c->gU_sm = c->sm;
+    }
+    CK(cudaGraphLaunch(c->gU, st));
+    c->launches += c->nU;
+  } else {
+    RC(setup_body(c));
+  }
   RC(check_device_error(c));
   c->setup_done = true;
   return MG_OK;
