@@ -21,6 +21,7 @@
 // loads), kept for A/B measurement (MGDTN_APPLY=ldg).
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "bodies.cuh"
 
@@ -930,6 +931,111 @@ __global__ void __launch_bounds__(128) k_apply_ldg(const LevelDev L, int colour,
     __syncthreads();
     if (threadIdx.x == 0) partials[blockIdx.x] = (red[0] + red[1]) + (red[2] + red[3]);
   }
+}
+
+// ---------------------------------------------------------------- LU-SGS colour sweep, edge rows only
+// One LU-SGS colour sweep (reading F3) needs (r - A x)_e on the
+// edges of ONE colour only, and every element has exactly one edge of each colour:
+// each element forms just the K1 rows of S_T x_T belonging to that edge (K1*M of
+// its m(m+1)/2 packed entries, 100 of 210 at p = 4) with plain coalesced loads (the
+// 32 lanes of a warp share the edge's local index within a mesh row).  Pass 0
+// (colour-0 elements) writes the partial sums y_e; pass 1 (colour-1 elements) adds
+// its own, x_e += omega D_e^-1 (r_e - y_e).  Each row is accumulated in increasing
+// column order, the order of the whole-matrix packed loop; D_e^-1 comes from the SoA
+// blocks (the masked apply reads their packed upper triangle), so the two agree to
+// rounding.  Measured slower than the TMA-streamed masked apply at config 2 (38.7 vs
+// 34.9 ms LU-SGS solve): off by default, MGDTN_GS=rows selects it.
+template <int P, int PASS>
+__global__ void __launch_bounds__(128) k_gs_rows(const LevelDev L, int gcol, double* x, double* y,
+                                                 const double* __restrict__ r) {
+  constexpr int K1 = P + 1, M = 4 * K1, NPK = M * (M + 1) / 2;
+  pdl_enter();
+  const int colour = PASS;
+  const int64_t nec = L.ne >> 1;
+  const uint64_t pol = stream_policy(L.l2keep);
+  const double om = L.coef[1];
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nec;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int i, j;
+    slot_elem(L.nx, colour, s, i, j);
+    int64_t ed[4];
+    bool bd[4];
+    elem_edges(L.nx, L.ny, i, j, ed, bd, L.dmask);
+    int fc = 0;
+#pragma unroll
+    for (int f = 1; f < 4; ++f)
+      if (gs_colour(i, j, f) == gcol) fc = f;
+    if (bd[fc]) continue;
+    double xv[M];
+    gather_x<K1>(x, ed, bd, xv);
+    const double* Sp = L.S + ((((int64_t)colour * L.nchunk + (s >> 5)) * NPK) << 5) + (s & 31);
+    double yv[K1];
+    auto rows = [&](auto F) {
+      constexpr int f = decltype(F)::value;
+#pragma unroll
+      for (int al = 0; al < K1; ++al) {
+        const int a = f * K1 + al;
+        double acc = 0.0;
+#pragma unroll
+        for (int b = 0; b < M; ++b) {
+          const int kk = b < a ? b * (2 * M - b + 1) / 2 + (a - b) : a * (2 * M - a + 1) / 2 + (b - a);
+          acc = fma(ld_stream(Sp + ((int64_t)kk << 5), pol), xv[b], acc);
+        }
+        yv[al] = acc;
+      }
+    };
+    switch (fc) {
+      case 0: rows(std::integral_constant<int, 0>{}); break;
+      case 1: rows(std::integral_constant<int, 1>{}); break;
+      case 2: rows(std::integral_constant<int, 2>{}); break;
+      default: rows(std::integral_constant<int, 3>{}); break;
+    }
+    const int64_t base = ed[fc] * K1;
+    if (PASS == 0) {
+#pragma unroll
+      for (int al = 0; al < K1; ++al) y[base + al] = yv[al];
+    } else {
+      double res[K1];
+#pragma unroll
+      for (int al = 0; al < K1; ++al) res[al] = (__ldg(r + base + al) - y[base + al]) - yv[al];
+      const double* Di = L.Dinv + ed[fc];
+#pragma unroll
+      for (int al = 0; al < K1; ++al) {
+        double c = 0.0;
+#pragma unroll
+        for (int b = 0; b < K1; ++b) c = fma(__ldg(Di + (al * K1 + b) * L.nedge), res[b], c);
+        x[base + al] = fma(om, c, xv[fc * K1 + al]);
+      }
+    }
+  }
+}
+
+static bool gs_full() {   // MGDTN_GS=rows: the edge-row sweep (A/B); default the masked apply
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MGDTN_GS");
+    v = (e && std::strcmp(e, "rows") == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+
+int launch_gs_sweep(const LevelDev& L, int gcol, double* x, double* y, const double* r,
+                    cudaStream_t st) {
+  if (gs_full() || L.ns || L.imask) return -1;   // caller uses the masked full apply
+  const int64_t nec = L.ne / 2;
+  int64_t g = (nec + 127) / 128;
+  const int grid = (int)(g < 148 * 8 ? (g > 0 ? g : 1) : 148 * 8);
+#define GS_LAUNCH(PP)                                                                     \
+  launch_ex(k_gs_rows<PP, 0>, grid, 128, 0, true, st, L, gcol, x, y, r);                 \
+  launch_ex(k_gs_rows<PP, 1>, grid, 128, 0, true, st, L, gcol, x, y, r);
+  switch (L.p) {
+    case 1: GS_LAUNCH(1) break;
+    case 2: GS_LAUNCH(2) break;
+    case 3: GS_LAUNCH(3) break;
+    default: GS_LAUNCH(4) break;
+  }
+#undef GS_LAUNCH
+  return 2;
 }
 
 // ---------------------------------------------------------------- host side

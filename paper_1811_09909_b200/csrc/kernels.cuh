@@ -323,6 +323,10 @@ int apply_grid_mode(const LevelDev& L, int mode);   // blocks of a colour pass i
 int launch_apply2(const LevelDev& L, int mode, const double* x, double* y, const double* r,
                   double* d, int step, double* partials, bool pdl, cudaStream_t st);
 int apply2_grid(const LevelDev& L, int mode);  // blocks of launch_apply2 (partials length)
+// one LU-SGS colour sweep of colour gcol from the edge rows only (k_apply.cu); -1 if not
+// applicable (then the colour-masked full apply AM_GSC is used)
+int launch_gs_sweep(const LevelDev& L, int gcol, double* x, double* y, const double* r,
+                    cudaStream_t st);
 
 int launch_local_dtn(const LevelDev& L, const RefDev& R, double h, const double* K,
                      const int8_t* method, const double* tau, DevError* err, cudaStream_t st);

@@ -566,7 +566,11 @@ static inline void smooth_step(Ctx* c, HostLevel& L, int step) {
     // one LU-SGS step: forward block Gauss-Seidel sweep over the
     // four edge colours, then backward (oracle/multigrid.py)
     static const int order[8] = {0, 1, 2, 3, 3, 2, 1, 0};
-    for (int q = 0; q < 8; ++q) apply_mode(c, L, AM_GSC, L.e, L.w, L.r, nullptr, order[q], nullptr);
+    for (int q = 0; q < 8; ++q) {
+      const int n = launch_gs_sweep(L.d, order[q], L.e, L.w, L.r, c->st);
+      if (n >= 0) c->launches += n;
+      else apply_mode(c, L, AM_GSC, L.e, L.w, L.r, nullptr, order[q], nullptr);
+    }
     return;
   }
   // coefficient slot clamped to MAX_NU-1: only block-Jacobi (step-invariant
