@@ -121,6 +121,24 @@ int launch_restrict_edges(const LevelDev& F, const LevelDev& C, const double* re
   return 1;
 }
 
+__global__ void k_lc_restrict_fused(LevelDev F, LevelDev C, const double* __restrict__ res,
+                                    double* e, const double* __restrict__ KIIinv,
+                                    const double* __restrict__ Rm, int do_lc, double* rc,
+                                    int fuse, double* ec, double* dc) {
+  pdl_enter();
+  lc_restrict_fused_body(F, C, res, e, KIIinv, Rm, do_lc, rc, fuse, ec, dc, GTID, GNT);
+}
+
+int launch_lc_restrict_fused(const LevelDev& F, const LevelDev& C, const double* res, double* e,
+                             const double* KIIinv, const double* Rm, bool do_lc, double* rc,
+                             bool fuse_first, double* ec, double* dc, cudaStream_t st) {
+  const int64_t nmac = (int64_t)(F.nx / 2) * (F.ny / 2);
+  const int64_t n = (do_lc ? 8 * nmac : 0) + C.nedge;
+  launch_ex(k_lc_restrict_fused, cap_grid(n, 128, 148 * 8), 128, 0, true, st, F, C, res, e,
+            KIIinv, Rm, do_lc ? 1 : 0, rc, fuse_first ? 1 : 0, ec, dc);
+  return 1;
+}
+
 __global__ void k_prolong_macro(LevelDev F, LevelDev C, const double* __restrict__ ec,
                                 const double* __restrict__ Pm, double* e) {
   pdl_enter();

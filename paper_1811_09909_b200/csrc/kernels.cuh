@@ -368,6 +368,10 @@ int launch_gather_dense(const LevelDev& L, const int64_t* elems, int64_t n, doub
 // MG transfer / smoothing kernels
 int launch_smooth_first(const LevelDev& L, const double* r, double* e, double* d,
                         cudaStream_t st);
+// step 3 + the whole h-restriction in one launch (one GPU; bodies.cuh lc_restrict_fused_body)
+int launch_lc_restrict_fused(const LevelDev& F, const LevelDev& C, const double* res, double* e,
+                             const double* KIIinv, const double* Rm, bool do_lc, double* rc,
+                             bool fuse_first, double* ec, double* dc, cudaStream_t st);
 int launch_lc_restrict(const LevelDev& F, const double* res, double* e, const double* KIIinv,
                        const double* Pm, double* cbuf, bool do_lc, bool do_restrict,
                        cudaStream_t st);

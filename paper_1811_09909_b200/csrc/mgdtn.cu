@@ -600,7 +600,14 @@ static void restrict_level(Ctx* c, int li, const double* res, double* e, bool do
   HostLevel& C = gat ? c->lgl : c->lev[li + 1];
   double* rcl = gat ? c->lgl.r : rc;
   if (gat) fuse = false;
-  if (L.kind == KIND_H) {
+  // MGDTN_RESTRICT_FUSED=1: step 3 + restriction as one launch (A/B; measured slower at
+  // configs 2 / 4: 7.05 vs 6.81 ms and 162 vs 156 ms solves -- the on-the-fly macro terms
+  // cost more latency per coarse edge than the saved launch)
+  static const bool rfused = env_or("MGDTN_RESTRICT_FUSED", 0) != 0;
+  if (L.kind == KIND_H && !partitioned(c) && rfused) {
+    c->launches += launch_lc_restrict_fused(L.d, C.d, res, e, L.KIIinv, L.Rm, do_lc, rcl, fuse,
+                                            C.e, C.dv, c->st);
+  } else if (L.kind == KIND_H) {
     c->launches += launch_lc_restrict(L.d, res, e, L.KIIinv, L.Rm, L.cbuf, do_lc, true, c->st);
     c->launches += launch_restrict_edges(L.d, C.d, res, L.cbuf, rcl, fuse, C.e, C.dv, c->st);
     if (C.d.imask) {
