@@ -410,11 +410,11 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not ns:
-        ns = oracle_sample_n(cfg, 30.0)
-        sc = W.scaled_config(cfg.index, ns) if ns != cfg.n else cfg
+        n_smp = oracle_sample_n(cfg, 30.0)
+        sc = W.scaled_config(cfg.index, n_smp) if n_smp != cfg.n else cfg
         t, its = run_oracle_step(sc)
         cpu = {"value": sc.trace_dofs / t, "unit": "trace DoF/s", "cores": cpu_threads(), "kind": "oracle",
-               "sample": f"one oracle setup+rhs+PCG solve of the config-{cfg.index} recipe at n={ns} "
+               "sample": f"one oracle setup+rhs+PCG solve of the config-{cfg.index} recipe at n={n_smp} "
                          f"({sc.trace_dofs} trace dofs, {its} iterations, {t:.1f} s)"}
 
     if rank == 0:
@@ -439,7 +439,7 @@ def main():
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": ("k_apply_ldg<p,*,NS> full-storage" if ns else "k_apply<p,*>")
+                         "kernel": ("k_apply_seg<p,*,*,NSYM> full-storage" if ns else "k_apply<p,*>")
                                    + " fine-level colour passes (mg_apply, both colours)",
                          "alg_bytes_per_apply": alg_bytes,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in peaks

@@ -136,3 +136,14 @@ def test_no_cpu_fallback_without_gpu():
     from paper_1811_09909_b200 import MGError, MGSolver
     with pytest.raises(MGError):
         MGSolver(8, p=1)
+
+
+def test_bench_flags_not_shadowed():
+    """bench.py main(): the nonsymmetric-scheme flag `ns` is assigned once (a later
+    reuse of the name once relabelled the default PCG line as GMRES)."""
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    tree = ast.parse(src)
+    main = next(n for n in tree.body if isinstance(n, ast.FunctionDef) and n.name == "main")
+    targets = [t.id for node in ast.walk(main) if isinstance(node, ast.Assign)
+               for t in node.targets if isinstance(t, ast.Name)]
+    assert targets.count("ns") == 1, targets.count("ns")
