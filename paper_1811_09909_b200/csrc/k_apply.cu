@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(32) k_apply_tma(const LevelDev L, int colour, 
   const int64_t nec = L.ne >> 1;
   const int nchunk = (int)((nec + 31) >> 5);
   const double* Sbase = L.S + (int64_t)colour * L.nchunk * NPK * 32;
-  const uint64_t pol = stream_policy(L.l2keep);
+  const uint64_t pol = stream_policy(colour == 0 && L.l2keep0 ? 1.0f : L.l2keep);
   // static chunks of this CTA: c_k = blockIdx.x + k * gridDim.x
   const int nmine_static =
       (int)blockIdx.x < nchunk ? (nchunk - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(64) k_apply_tma2(const LevelDev L, int colour,
   const int64_t nec = L.ne >> 1;
   const int nchunk = (int)((nec + 31) >> 5);
   const double* Sbase = L.S + (int64_t)colour * L.nchunk * NPK * 32;
-  const uint64_t pol = stream_policy(L.l2keep);
+  const uint64_t pol = stream_policy(colour == 0 && L.l2keep0 ? 1.0f : L.l2keep);
   const int nmine = (int)blockIdx.x < nchunk ? (nchunk - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(32) k_apply_seg(const LevelDev L, int colour, 
   const int64_t nec = L.ne >> 1;
   const int nchunk = L.nchunk;
   const double* Sbase = L.S + (int64_t)colour * nchunk * NPK * 32;
-  const uint64_t pol = stream_policy(L.l2keep);
+  const uint64_t pol = stream_policy(colour == 0 && L.l2keep0 ? 1.0f : L.l2keep);
   const int G = (int)gridDim.x, b = (int)blockIdx.x;
   const int nmine = b < nchunk ? (nchunk - 1 - b) / G + 1 : 0;
   const int total = nmine * NS;
@@ -882,7 +882,7 @@ __global__ void __launch_bounds__(128) k_apply_ldg(const LevelDev L, int colour,
   constexpr int NPK = NS ? M * M : M * (M + 1) / 2;
   const int64_t nec = L.ne >> 1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const uint64_t pol = stream_policy(L.l2keep);
+  const uint64_t pol = stream_policy(colour == 0 && L.l2keep0 ? 1.0f : L.l2keep);
   pdl_wait();
   pdl_trigger();
   double c1 = 0.0, c2 = 0.0;

@@ -60,6 +60,8 @@ struct LevelDev {
   int ox, oy, gnx, gny;    // this block's element offset in the global level and the global
                            // level's dims (0, 0, nx, ny on one GPU)
   int probe;               // measurement probe (MGDTN_PROBE=1: the apply streams S_T only)
+  int l2keep0;             // 1: the colour-0 half of S_T is loaded L2::evict_last (kept
+                           // resident across the solve's colour-0 passes), colour 1 evict_first
   float l2keep;            // fraction of this level's S_T / Dc stream loaded L2::evict_last
                            // (kept resident across applies in the 126 MB L2); the rest
                            // evict_first.  0: all evict_first

@@ -391,6 +391,18 @@ static void plan_l2(Ctx* c) {
   LevelDev& d = c->lev[0].d;
   const double bytes = (double)d.nchunk * 32 * 8 * (2.0 * d.npk);
   d.l2keep = budget > 0 ? (float)std::min(1.0, budget / bytes) : 0.0f;
+  // MGDTN_L2HALF_MB: keep the colour-0 halves of the finest levels resident, finest
+  // first, while they fit the budget.  Every colour-0 pass of a level (the W0 pass of
+  // each smoothing step, residual and PCG apply) then re-reads its half from L2.
+  double half_budget = (double)env_or("MGDTN_L2HALF_MB", 0) * 1048576.0;
+  for (auto& L : c->lev) {
+    L.d.l2keep0 = 0;
+    const double half = (double)L.d.nchunk * 32 * 8 * L.d.npk;
+    if (half_budget > 0 && half <= half_budget && !partitioned(c)) {
+      L.d.l2keep0 = 1;
+      half_budget -= half;
+    }
+  }
 }
 
 static void fill_tail(Ctx* c) {
