@@ -196,14 +196,120 @@ int launch_tail_dense(const int* tfidx, int nf, const double* Bt, const double* 
   return 1;
 }
 
-int launch_tail_basis(const TailParams& P, const int* tfidx, int nf, double* Bt, cudaStream_t st) {
-  const size_t smem = (size_t)P.smem_doubles * sizeof(double);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(k_tail_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
+// B_tail with NC columns per CTA: thread group g (TAIL_TPB / NC threads) runs the tail
+// V-cycle of column blockIdx.x * NC + g on its own shared-memory copy of the tail
+// vectors; the groups share every CTA barrier and the (L1-resident) level matrices.
+// The single-column kernel leaves 3/4 of its threads idle on the 16x16 top level
+// (128 elements per colour pass); NC = 4 fills them.  Same bodies, same order per
+// column as k_coarse_tail_t<true>.
+template <int NC>
+__global__ void __launch_bounds__(TAIL_TPB, 1)
+    k_tail_basis_mc(const __grid_constant__ TailParams P, const int* __restrict__ tfidx, int nfb,
+                    double* Bt) {
+  extern __shared__ __align__(16) double tail_smem[];
+  constexpr int NG = TAIL_TPB / NC;
+  const int g = threadIdx.x / NG, tg = threadIdx.x - g * NG;
+  const int col = blockIdx.x * NC + g;
+  const int nlev = P.nlev;
+  double* base = tail_smem + (int64_t)g * P.smem_doubles;
+  // per-level vector offsets of the k_coarse_tail_t shared-memory layout
+  double *vr[MAX_TAIL], *ve[MAX_TAIL], *vw[MAX_TAIL], *vd[MAX_TAIL], *vc[MAX_TAIL];
+  {
+    double* q = base;
+    for (int k = 0; k < nlev; ++k) {
+      const int64_t n = P.lev[k].d.ndof;
+      vr[k] = q; q += n;
+      ve[k] = q; q += n;
+      vw[k] = q; q += n;
+      vd[k] = q; q += n;
+      vc[k] = q;
+      if (k < nlev - 1) q += (int64_t)(P.lev[k].d.nx / 2) * (P.lev[k].d.ny / 2) * 8;
+    }
   }
-  k_tail_basis<<<nf, TAIL_TPB, smem, st>>>(P, tfidx, nf, Bt);
+  for (int64_t i = threadIdx.x; i < (int64_t)NC * P.smem_doubles; i += TAIL_TPB) tail_smem[i] = 0.0;
+  __syncthreads();
+  if (tg == 0 && col < nfb) vr[0][tfidx[col]] = 1.0;
+  __syncthreads();
+  auto nu_of = [&](int nu, int li) { return P.nu_doubling ? nu << li : nu; };
+  auto cs = [](int s) { return s < MAX_NU ? s : MAX_NU - 1; };
+  for (int li = 0; li < nlev - 1; ++li) {
+    const TailLevel& L = P.lev[li];
+    const TailLevel& C = P.lev[li + 1];
+    const int nu_pre = nu_of(P.nu_pre, li);
+    int s0 = 0;
+    if (nu_pre > 0) {
+      if (li == 0) {   // below the top level the restriction did the first step (fuse)
+        smooth_first_body(L.d, vr[li], ve[li], vd[li], tg, NG);
+        __syncthreads();
+      }
+      s0 = 1;
+    } else {
+      zero_body(ve[li], L.d.ndof, tg, NG);
+      __syncthreads();
+    }
+    for (int s = s0; s < nu_pre; ++s) {
+      apply_pass_body<1, AM_W0, false>(L.d, 0, ve[li], vw[li], nullptr, nullptr, 0, tg, NG);
+      __syncthreads();
+      apply_pass_body<1, AM_SMOOTH, false>(L.d, 1, ve[li], vw[li], vr[li], vd[li], cs(s), tg, NG);
+      __syncthreads();
+    }
+    apply_pass_body<1, AM_W0, false>(L.d, 0, ve[li], vw[li], nullptr, nullptr, 0, tg, NG);
+    __syncthreads();
+    apply_pass_body<1, AM_RESID, false>(L.d, 1, ve[li], vw[li], vr[li], nullptr, 0, tg, NG);
+    __syncthreads();
+    lc_restrict_body(L.d, vw[li], ve[li], L.KIIinv, L.Pm, vc[li], 1, 1, tg, NG);
+    __syncthreads();
+    const int fuse = (li + 1 < nlev - 1) && nu_of(P.nu_pre, li + 1) > 0;
+    restrict_edges_body(L.d, C.d, vw[li], vc[li], vr[li + 1], fuse, ve[li + 1], vd[li + 1], tg, NG);
+    __syncthreads();
+    (void)C;
+  }
+  coarse_solve_body(P.fidx, P.nf, P.A1inv, vr[nlev - 1], ve[nlev - 1], tg, NG);
+  __syncthreads();
+  for (int li = nlev - 2; li >= 0; --li) {
+    const TailLevel& L = P.lev[li];
+    const TailLevel& C = P.lev[li + 1];
+    prolong_macro_body(L.d, C.d, ve[li + 1], L.Pm, ve[li], tg, NG);
+    __syncthreads();
+    for (int s = 0; s < nu_of(P.nu_post, li); ++s) {
+      apply_pass_body<1, AM_W0, false>(L.d, 0, ve[li], vw[li], nullptr, nullptr, 0, tg, NG);
+      __syncthreads();
+      apply_pass_body<1, AM_SMOOTH, false>(L.d, 1, ve[li], vw[li], vr[li], vd[li], cs(s), tg, NG);
+      __syncthreads();
+    }
+  }
+  if (col < nfb)
+    for (int i = tg; i < nfb; i += NG) Bt[(int64_t)i * nfb + col] = ve[0][tfidx[i]];
+}
+
+int launch_tail_basis(const TailParams& P, const int* tfidx, int nf, double* Bt, cudaStream_t st) {
+  const size_t smem1 = (size_t)P.smem_doubles * sizeof(double);
+  static int mc = -1;   // MGDTN_TAIL_BASIS_NC: columns per CTA (1 = the single-column kernel)
+  if (mc < 0) {
+    const char* e = std::getenv("MGDTN_TAIL_BASIS_NC");
+    mc = e ? std::atoi(e) : 4;
+  }
+  int nc = mc;
+  while (nc > 1 && (size_t)nc * smem1 > 220 * 1024) nc /= 2;
+  if (nc >= 4 || nc == 2) {
+    const size_t smem = (size_t)nc * smem1;
+    auto kern = nc >= 4 ? k_tail_basis_mc<4> : k_tail_basis_mc<2>;
+    if (nc >= 4) nc = 4;
+    static size_t attr4 = 0, attr2 = 0;
+    size_t& attr = nc == 4 ? attr4 : attr2;
+    if (smem > attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = smem;
+    }
+    kern<<<(nf + nc - 1) / nc, TAIL_TPB, smem, st>>>(P, tfidx, nf, Bt);
+    return 1;
+  }
+  static size_t attr = 0;
+  if (smem1 > attr) {
+    cudaFuncSetAttribute(k_tail_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+    attr = smem1;
+  }
+  k_tail_basis<<<nf, TAIL_TPB, smem1, st>>>(P, tfidx, nf, Bt);
   return 1;
 }
 
