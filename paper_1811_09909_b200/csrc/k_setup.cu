@@ -96,24 +96,37 @@ __global__ void __launch_bounds__(32 * (2 * (P + 1))) k_local_dtn(LevelDev L, Re
     const double* At = sAt[meth];
     const double* Bk = sBk[meth];
     double* dst = L.S + (((int64_t)colour * L.nchunk + chunk) * NPK) * 32 + lane;
+    {
+      // the warp's two rows a1 < a2 in one sweep over (i, b): each w_ib (two shared
+      // loads) feeds both rows' FMAs (same arithmetic per entry as one row at a time)
+      const int a1 = w, a2 = M - 1 - w;
+      double acc1[M], acc2[M];
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const int a = half == 0 ? w : M - 1 - w;
-      double acc[M];
-#pragma unroll
-      for (int b = 0; b < M; ++b)
-        acc[b] = (meth == 0 ? Kc * sW[a * M + b] : 0.0) + t * sH[a * M + b];
+      for (int b = 0; b < M; ++b) {
+        acc1[b] = (meth == 0 ? Kc * sW[a1 * M + b] : 0.0) + t * sH[a1 * M + b];
+        acc2[b] = (meth == 0 ? Kc * sW[a2 * M + b] : 0.0) + t * sH[a2 * M + b];
+      }
       for (int i = 0; i < NV; ++i) {
-        const double wa = fma(t, At[i * M + a], Kc * Bk[i * M + a]) * sc[i][lane];
+        const double si = sc[i][lane];
+        const double wa1 = fma(t, At[i * M + a1], Kc * Bk[i * M + a1]) * si;
+        const double wa2 = fma(t, At[i * M + a2], Kc * Bk[i * M + a2]) * si;
 #pragma unroll
-        for (int b = 0; b < M; ++b)
-          if (b >= a) acc[b] = fma(-wa, fma(t, At[i * M + b], Kc * Bk[i * M + b]), acc[b]);
+        for (int b = 0; b < M; ++b) {
+          if (b >= a1) {
+            const double wib = fma(t, At[i * M + b], Kc * Bk[i * M + b]);
+            acc1[b] = fma(-wa1, wib, acc1[b]);
+            if (b >= a2) acc2[b] = fma(-wa2, wib, acc2[b]);
+          }
+        }
       }
       if (act) {
-        const int base = a * (2 * M - a + 1) / 2 - a;   // kk(a, b) = base + b
+        const int base1 = a1 * (2 * M - a1 + 1) / 2 - a1;   // kk(a, b) = base + b
+        const int base2 = a2 * (2 * M - a2 + 1) / 2 - a2;
 #pragma unroll
-        for (int b = 0; b < M; ++b)
-          if (b >= a) dst[(int64_t)(base + b) * 32] = acc[b];
+        for (int b = 0; b < M; ++b) {
+          if (b >= a1) dst[(int64_t)(base1 + b) * 32] = acc1[b];
+          if (b >= a2) dst[(int64_t)(base2 + b) * 32] = acc2[b];
+        }
       }
     }
     if (project) {
