@@ -947,9 +947,55 @@ int launch_gather_dense(const LevelDev& L, const int64_t* elems, int64_t n, doub
 __global__ void k_coarse_factor(LevelDev L, const int* __restrict__ fpos, int nf, double* A,
                                 double* Ainv, DevError* err) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  for (int q = tid; q < nf * nf; q += nt) A[q] = 0.0;
+  // small coarsest level (the 2x2 macro mesh: nf = 8, 4 elements): every thread owns
+  // entries of A and sums their contributions in the serial loop's order (elements,
+  // then a, then b), from a shared copy of the element-to-free-dof maps -- the same
+  // sums as the one-thread assembly below, without its chain of dependent global
+  // read-modify-writes
+  constexpr int SGI = 1024, SNF = 32;
+  __shared__ int sgi[SGI];
+  __shared__ double sA[SNF * SNF], sI[SNF * SNF];   // A and A^-1 of a small coarsest level
+  const bool par = nf <= SNF && L.ne * L.m <= SGI;
+  double* Aw = par ? sA : A;
+  double* Iw = par ? sI : Ainv;
+  if (par) {
+    for (int q = tid; q < L.ne * L.m; q += nt) {
+      const int64_t e = q / L.m;
+      const int a = q - (int)e * L.m;
+      const int i = (int)(e % L.nx), j = (int)(e / L.nx);
+      int64_t ed[4];
+      bool bd[4];
+      elem_edges(L.nx, L.ny, i, j, ed, bd, L.dmask);
+      sgi[q] = fpos[ed[a / L.k1] * L.k1 + a % L.k1];
+    }
+    __syncthreads();
+    for (int q = tid; q < nf * nf; q += nt) {
+      const int gr = q / nf, gc = q - gr * nf;
+      double acc = 0.0;
+      for (int64_t e = 0; e < L.ne; ++e) {
+        const int* gi = sgi + e * L.m;
+        const double* src = nullptr;
+        for (int a = 0; a < L.m; ++a) {
+          if (gi[a] != gr) continue;
+          for (int b = 0; b < L.m; ++b) {
+            if (gi[b] != gc) continue;
+            if (!src) {
+              int colour;
+              int64_t s;
+              elem_slot(L.nx, (int)(e % L.nx), (int)(e / L.nx), colour, s);
+              src = L.S + s_offset(L.nchunk, L.npk, colour, s, 0);
+            }
+            acc += s_get(src, L.m, L.ns, a, b);
+          }
+        }
+      }
+      Aw[q] = acc;
+    }
+  } else {
+    for (int q = tid; q < nf * nf; q += nt) A[q] = 0.0;
+  }
   __syncthreads();
-  if (tid == 0) {
+  if (!par && tid == 0) {
     for (int64_t e = 0; e < L.ne; ++e) {
       int i = (int)(e % L.nx), j = (int)(e / L.nx), colour;
       int64_t s;
@@ -968,7 +1014,13 @@ __global__ void k_coarse_factor(LevelDev L, const int* __restrict__ fpos, int nf
   }
   __syncthreads();
   if (L.ns) {   // nonsymmetric A_1: Gauss-Jordan with partial pivoting (A is the scratch)
-    if (tid == 0 && !gj_inverse(A, nf, Ainv, A)) report_error(err, -3, -2);
+    if (tid == 0 && !gj_inverse(Aw, nf, Iw, Aw)) report_error(err, -3, -2);
+    __syncthreads();
+    if (par)
+      for (int q = tid; q < nf * nf; q += nt) {
+        A[q] = sA[q];
+        Ainv[q] = sI[q];
+      }
     return;
   }
   __shared__ int bad;
@@ -976,18 +1028,18 @@ __global__ void k_coarse_factor(LevelDev L, const int* __restrict__ fpos, int nf
   __syncthreads();
   for (int jc = 0; jc < nf; ++jc) {
     if (tid == 0) {
-      double d = A[jc * nf + jc];
+      double d = Aw[jc * nf + jc];
       if (!(d > 0.0)) { bad = 1; d = 1e-300; }
-      A[jc * nf + jc] = sqrt(d);
+      Aw[jc * nf + jc] = sqrt(d);
     }
     __syncthreads();
-    const double dj = A[jc * nf + jc];
-    for (int i = jc + 1 + tid; i < nf; i += nt) A[i * nf + jc] /= dj;
+    const double dj = Aw[jc * nf + jc];
+    for (int i = jc + 1 + tid; i < nf; i += nt) Aw[i * nf + jc] /= dj;
     __syncthreads();
     const int r = nf - jc - 1;
     for (int q = tid; q < r * r; q += nt) {
       int ii = jc + 1 + q / r, cc = jc + 1 + q % r;
-      if (cc <= ii) A[ii * nf + cc] -= A[ii * nf + jc] * A[cc * nf + jc];
+      if (cc <= ii) Aw[ii * nf + cc] -= Aw[ii * nf + jc] * Aw[cc * nf + jc];
     }
     __syncthreads();
   }
@@ -996,13 +1048,20 @@ __global__ void k_coarse_factor(LevelDev L, const int* __restrict__ fpos, int nf
   for (int c = tid; c < nf; c += nt) {
     for (int a = 0; a < nf; ++a) {
       double s = (a == c) ? 1.0 : 0.0;
-      for (int k = 0; k < a; ++k) s -= A[a * nf + k] * Ainv[k * nf + c];
-      Ainv[a * nf + c] = s / A[a * nf + a];
+      for (int k = 0; k < a; ++k) s -= Aw[a * nf + k] * Iw[k * nf + c];
+      Iw[a * nf + c] = s / Aw[a * nf + a];
     }
     for (int a = nf - 1; a >= 0; --a) {
-      double s = Ainv[a * nf + c];
-      for (int k = a + 1; k < nf; ++k) s -= A[k * nf + a] * Ainv[k * nf + c];
-      Ainv[a * nf + c] = s / A[a * nf + a];
+      double s = Iw[a * nf + c];
+      for (int k = a + 1; k < nf; ++k) s -= Aw[k * nf + a] * Iw[k * nf + c];
+      Iw[a * nf + c] = s / Aw[a * nf + a];
+    }
+  }
+  if (par) {
+    __syncthreads();
+    for (int q = tid; q < nf * nf; q += nt) {
+      A[q] = sA[q];
+      Ainv[q] = sI[q];
     }
   }
 }
