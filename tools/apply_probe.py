@@ -27,14 +27,20 @@ def main():
     ap.add_argument("--op", default="apply", choices=["apply", "smooth"],
                     help="smooth: one fine smoothing step through mg_smooth (apply + D^-1 epilogue, "
                          "plus mg_smooth's two masked input copies and one output copy)")
+    ap.add_argument("--scheme", default="config", choices=["config", "nipg", "iipg", "tiles"],
+                    help="nonsymmetric context with IIPG-H / NIPG-H elements (full-storage apply)")
     a = ap.parse_args()
     cfg = W.CONFIGS[a.config] if not a.n else W.scaled_config(a.config, a.n)
-    pr = W.make_problem(cfg, with_f=False)
+    ns = a.scheme != "config"
+    pr = W.nonsymmetric_problem(cfg, a.scheme) if ns else W.make_problem(cfg, with_f=False)
     dev = torch.device("cuda", 0)
     st = torch.cuda.Stream(dev)
     with torch.cuda.stream(st):
-        s = MGSolver(cfg.n, p=cfg.p, device=dev, stream=st)
-        s.setup(pr.K, pr.method, pr.tau, smoother_from_config(cfg))
+        s = MGSolver(cfg.n, p=cfg.p, device=dev, stream=st, nonsymmetric=ns)
+        sm = smoother_from_config(cfg)
+        if ns:
+            sm.kind = 0
+        s.setup(pr.K, pr.method, pr.tau, sm)
         lev = a.level or s.nlevels
         nd = s.ndof(lev)
         x = torch.rand(nd, dtype=torch.float64, device=dev)
@@ -59,11 +65,12 @@ def main():
     info = s.level_info(lev)
     ne = info["nx"] * info["ny"]
     m = 4 * (info["p"] + 1)
-    alg = ne * 8 * m * (m + 1) // 2 + 16 * nd
+    alg = ne * 8 * (m * m if ns else m * (m + 1) // 2) + 16 * nd
     t = float(np.median(ts))
     print(json.dumps({"config": cfg.name, "level": lev, "p": info["p"], "ne": ne, "us_median": t,
                       "us_min": float(np.min(ts)), "alg_bytes": alg, "GBps": alg / t / 1e3,
-                      "apply": os.environ.get("MGDTN_APPLY", "tma"), "op": a.op}))
+                      "apply": os.environ.get("MGDTN_APPLY", "tma"), "op": a.op,
+                      "scheme": a.scheme}))
 
 
 if __name__ == "__main__":
