@@ -102,6 +102,10 @@ struct Ctx {
   // own streams (fork / join with events on the ctx stream)
   std::vector<cudaStream_t> side;
   std::vector<cudaEvent_t> side_ev, fork_evs;
+  // mg_solve_host: the source-term / boundary-data uploads run on their own stream,
+  // overlapped with mg_setup_dtn (which does not read them)
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t copy_ev0 = nullptr, copy_ev1 = nullptr;
   double *hsend = nullptr, *hrecv = nullptr, *gall = nullptr, *sden = nullptr, *sall = nullptr;
 };
 
@@ -1792,13 +1796,29 @@ int mg_solve_host(void* ctx, const double* K_host, const int8_t* method_host,
   CK(cudaMemcpyAsync(Kd, K_host, d.ne * sizeof(double), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(taud, tau_host, d.ne * sizeof(double), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(md, method_host, d.ne, cudaMemcpyHostToDevice, st));
+  // f / g_D samples (the bulk of the upload) on the copy stream, overlapped with the
+  // setup; it starts after everything already queued on st (staging reuse)
+  const bool side_copy = (fd || gDd) && st != nullptr;
+  if (side_copy) {
+    if (!c->copy_st) {
+      CK(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->copy_ev0, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->copy_ev1, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(c->copy_ev0, st));
+    CK(cudaStreamWaitEvent(c->copy_st, c->copy_ev0, 0));
+  }
+  cudaStream_t cst = side_copy ? c->copy_st : st;
   if (fd)
     CK(cudaMemcpyAsync(fd, f_qp_host, (size_t)d.ne * nq * nq * sizeof(double),
-                       cudaMemcpyHostToDevice, st));
+                       cudaMemcpyHostToDevice, cst));
   if (gDd)
     CK(cudaMemcpyAsync(gDd, gD_qp_host, (size_t)(2 * d.nx + 2 * d.ny) * nq * sizeof(double),
-                       cudaMemcpyHostToDevice, st));
-  RC(mg_setup_dtn(c, Kd, md, taud, smoother));
+                       cudaMemcpyHostToDevice, cst));
+  if (side_copy) CK(cudaEventRecord(c->copy_ev1, c->copy_st));
+  const int rs = mg_setup_dtn(c, Kd, md, taud, smoother);
+  if (side_copy) CK(cudaStreamWaitEvent(st, c->copy_ev1, 0));
+  RC(rs);
   RC(rhs_impl(c, fd, f_const, gDd, gd, nullptr));
   int it = 0, stt = 0;
   double rel = 0;
@@ -1941,6 +1961,9 @@ void mg_destroy(void* ctx) {
   for (auto sx : c->side) cudaStreamDestroy(sx);
   for (auto ex : c->side_ev) cudaEventDestroy(ex);
   for (auto ex : c->fork_evs) cudaEventDestroy(ex);
+  if (c->copy_st) cudaStreamDestroy(c->copy_st);
+  if (c->copy_ev0) cudaEventDestroy(c->copy_ev0);
+  if (c->copy_ev1) cudaEventDestroy(c->copy_ev1);
   if (c->pinned) cudaFreeHost(c->pinned);
   delete c;
 }
