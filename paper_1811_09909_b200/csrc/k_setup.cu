@@ -215,7 +215,20 @@ __global__ void __launch_bounds__(128) k_local_rhs(
     double fp[NV];
 #pragma unroll
     for (int a = 0; a < NV; ++a) fp[a] = 0.0;
-    for (int q = 0; q < nq2; ++q) {
+    // the element's (p+4)^2 samples, 8 loads in flight per thread (a chain of one
+    // dependent load per sample was the kernel's latency); same FMA order per fp[a]
+    constexpr int QB = 8;
+    int q = 0;
+    for (; q + QB <= nq2; q += QB) {
+      double fv[QB];
+#pragma unroll
+      for (int u = 0; u < QB; ++u) fv[u] = f_qp ? f_qp[e * nq2 + q + u] : f_const;
+#pragma unroll
+      for (int u = 0; u < QB; ++u)
+#pragma unroll
+        for (int a = 0; a < NV; ++a) fp[a] = fma(fqT[(q + u) * NV + a], fv[u], fp[a]);
+    }
+    for (; q < nq2; ++q) {
       const double fv = f_qp ? f_qp[e * nq2 + q] : f_const;
 #pragma unroll
       for (int a = 0; a < NV; ++a) fp[a] = fma(fqT[q * NV + a], fv, fp[a]);
