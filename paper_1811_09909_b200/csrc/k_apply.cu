@@ -933,6 +933,309 @@ __global__ void __launch_bounds__(128) k_apply_ldg(const LevelDev L, int colour,
   }
 }
 
+// ---------------------------------------------------------------- single-pass strip apply
+// y = A x (AM_APPLY, optional dot) or w = r - A e (AM_RESID) in ONE pass over S_T
+// (MGDTN_STRIP=1, one GPU, nx % 64 == 0, ny % R == 0).  A CTA (one warp) owns tiles of
+// 64 columns x R rows; for each row it streams the row's colour-0 chunk, then its
+// colour-1 chunk (32 elements each, the S_T chunk layout), through the same TMA ring as
+// k_apply_tma.  Lane l holds the elements of columns x0+2l (A) and x0+2l+1 (B), so every
+// edge inside the tile is completed in registers: the A|B edge in-lane, the edge left
+// of A with the B contribution of lane l-1 (shuffle), a bottom edge with the top
+// contribution carried from the previous row.  Tile-perimeter edges leave their two
+// partial sums (by the colour of the contributing element) in pc0 / pc1, finished by
+// k_strip_fixup.  Every sum is taken colour 0 first, as in the two-pass apply (colour 0
+// writes, colour 1 adds), so y is bit-identical to it (the dot's summation order differs).
+template <int P, int MODE, bool DOT, int RR>
+__global__ void __launch_bounds__(32) k_apply_strip(const LevelDev L, const double* x, double* y,
+                                                    const double* __restrict__ r,
+                                                    double* __restrict__ partials, int early) {
+  using C = TmaCfg<P>;
+  constexpr int K1 = C::K1, M = C::M, NPK = C::NPK, NST = 2, TW = 64;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bars[NST];
+  double* stage_buf = reinterpret_cast<double*>(smem_raw);
+  const int lane = threadIdx.x;
+  const int nx = L.nx, ny = L.ny, nxh = nx >> 1;
+  const int ntx = nx / TW, ntiles = ntx * (ny / RR);
+  const int nmine = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int npos = nmine * 2 * RR;
+  const uint64_t pol = stream_policy(L.l2keep);
+  if (lane == 0) {
+#pragma unroll
+    for (int st = 0; st < NST; ++st) mbar_init(&bars[st], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto issue = [&](int pos) {   // lane 0
+    const int tile = (int)blockIdx.x + (pos / (2 * RR)) * (int)gridDim.x;
+    const int kk = pos % (2 * RR);
+    const int x0 = (tile % ntx) * TW, y0 = (tile / ntx) * RR;
+    const int j = y0 + (kk >> 1), c = kk & 1;
+    const int64_t q = ((int64_t)j * nxh + (x0 >> 1)) >> 5;
+    const int st = pos % NST;
+    mbar_expect_tx(&bars[st], C::CHUNK_BYTES);
+    tma_bulk_g2s(stage_buf + (size_t)st * NPK * 32, L.S + (((int64_t)c * L.nchunk + q) * NPK) * 32,
+                 C::CHUNK_BYTES, &bars[st], pol);
+  };
+  if (early) {
+    if (lane == 0)
+      for (int pos = 0; pos < NST && pos < npos; ++pos) issue(pos);
+    pdl_trigger();
+    pdl_wait();
+  } else {
+    pdl_wait();
+    if (lane == 0)
+      for (int pos = 0; pos < NST && pos < npos; ++pos) issue(pos);
+    pdl_trigger();
+  }
+  double dot = 0.0;
+  // epilogue of a completed edge: c0 / c1 = the colour-0 / colour-1 element's part
+  auto finish = [&](int64_t g, const double* c0, const double* c1) {
+#pragma unroll
+    for (int a = 0; a < K1; ++a) {
+      double v;
+      if (MODE == AM_RESID) v = (__ldg(r + g * K1 + a) - c0[a]) - c1[a];
+      else v = c0[a] + c1[a];
+      y[g * K1 + a] = v;
+      if (DOT) dot = fma(x[g * K1 + a], v, dot);
+    }
+  };
+  auto zero = [&](int64_t g) {
+#pragma unroll
+    for (int a = 0; a < K1; ++a) y[g * K1 + a] = 0.0;
+  };
+  auto partial = [&](int64_t g, int colour, const double* v) {
+    double* dst = colour ? L.pc1 : L.pc0;
+#pragma unroll
+    for (int a = 0; a < K1; ++a) dst[g * K1 + a] = v[a];
+  };
+  // x of the element at position q (software pipeline: gathered one position ahead,
+  // so the gather's latency overlaps the previous matvec)
+  auto gather_at = [&](int q, double* xo) {
+    if (q >= npos) return;
+    const int tile = (int)blockIdx.x + (q / (2 * RR)) * (int)gridDim.x;
+    const int kk = q % (2 * RR);
+    const int j = (tile / ntx) * RR + (kk >> 1), c = kk & 1;
+    const int i = (tile % ntx) * TW + 2 * lane + ((c + j) & 1);
+    int64_t ed[4];
+    bool bd[4];
+    elem_edges(nx, ny, i, j, ed, bd, 15);
+    gather_x<K1>(x, ed, bd, xo);
+  };
+  double xn[M];
+  gather_at(0, xn);
+  int pos = 0;
+  for (int k = 0; k < nmine; ++k) {
+    const int tile = (int)blockIdx.x + k * (int)gridDim.x;
+    const int x0 = (tile % ntx) * TW, y0 = (tile / ntx) * RR;
+    const int cA = x0 + 2 * lane, cB = cA + 1;
+    double carA[K1], carB[K1];   // tops of the previous row's A / B elements
+    for (int rj = 0; rj < RR; ++rj) {
+      const int j = y0 + rj;
+      double A[M], B[M];   // edge contributions of the elements in columns cA / cB
+#pragma unroll
+      for (int c = 0; c < 2; ++c, ++pos) {
+        const int d = (c + j) & 1;   // colour c sits in column x0 + 2l + d
+        double xv[M], yv[M];
+#pragma unroll
+        for (int a = 0; a < M; ++a) xv[a] = xn[a];
+        gather_at(pos + 1, xn);
+        const int st = pos % NST;
+        mbar_wait(&bars[st], (uint32_t)((pos / NST) & 1));
+        const double* Sp = stage_buf + (size_t)st * NPK * 32 + lane;
+#pragma unroll
+        for (int a = 0; a < M; ++a) yv[a] = 0.0;
+#pragma unroll
+        for (int a = 0; a < M; ++a) {
+#pragma unroll
+          for (int b = a; b < M; ++b) {
+            const int kk = a * (2 * M - a + 1) / 2 + (b - a);
+            const double sv = Sp[kk * 32];
+            yv[a] = fma(sv, xv[b], yv[a]);
+            if (b != a) yv[b] = fma(sv, xv[a], yv[b]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0 && pos + NST < npos) {
+          fence_proxy_async();
+          issue(pos + NST);
+        }
+        if (d == 0) {
+#pragma unroll
+          for (int a = 0; a < M; ++a) A[a] = yv[a];
+        } else {
+#pragma unroll
+          for (int a = 0; a < M; ++a) B[a] = yv[a];
+        }
+      }
+      const int colA = j & 1, colB = colA ^ 1;   // colours of the A / B elements
+      // local edge f of an element: 0 bottom, 1 right, 2 top, 3 left (K1 values each)
+      // (1) A|B edge V(cB, j)
+      {
+        const int64_t g = vedge(nx, ny, cB, j);
+        if (colA == 0) finish(g, A + 1 * K1, B + 3 * K1);
+        else finish(g, B + 3 * K1, A + 1 * K1);
+      }
+      // (2) left edge of A, V(cA, j): B.right of lane l - 1
+      {
+        double lb[K1];
+#pragma unroll
+        for (int a = 0; a < K1; ++a) lb[a] = __shfl_up_sync(0xffffffffu, B[1 * K1 + a], 1);
+        const int64_t g = vedge(nx, ny, cA, j);
+        if (lane > 0) {
+          if (colA == 0) finish(g, A + 3 * K1, lb);
+          else finish(g, lb, A + 3 * K1);
+        } else if (x0 == 0) {
+          zero(g);
+        } else {
+          partial(g, colA, A + 3 * K1);
+        }
+      }
+      // (3) right edge of the strip, V(x0 + 64, j): lane 31's B.right
+      if (lane == 31) {
+        const int64_t g = vedge(nx, ny, cB + 1, j);
+        if (cB + 1 == nx) zero(g);
+        else partial(g, colB, B + 1 * K1);
+      }
+      // (4) bottoms H(cA, j), H(cB, j) with the carried tops of row j - 1
+      {
+        const int64_t gA = hedge(nx, cA, j), gB = hedge(nx, cB, j);
+        if (rj > 0) {
+          if (colA == 0) {
+            finish(gA, A + 0 * K1, carA);
+            finish(gB, carB, B + 0 * K1);
+          } else {
+            finish(gA, carA, A + 0 * K1);
+            finish(gB, B + 0 * K1, carB);
+          }
+        } else if (j == 0) {
+          zero(gA);
+          zero(gB);
+        } else {
+          partial(gA, colA, A + 0 * K1);
+          partial(gB, colB, B + 0 * K1);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < K1; ++a) {
+        carA[a] = A[2 * K1 + a];
+        carB[a] = B[2 * K1 + a];
+      }
+    }
+    // tops of the tile's last row, H(cA, y0 + R), H(cB, y0 + R)
+    {
+      const int jt = y0 + RR;
+      const int64_t gA = hedge(nx, cA, jt), gB = hedge(nx, cB, jt);
+      const int colA = (jt - 1) & 1;   // colour of the row-(jt-1) element in column cA
+      if (jt == ny) {
+        zero(gA);
+        zero(gB);
+      } else {
+        partial(gA, colA, carA);
+        partial(gB, colA ^ 1, carB);
+      }
+    }
+  }
+  if (DOT) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if (lane == 0) partials[blockIdx.x] = dot;
+  }
+}
+
+// perimeter edges of the strip tiles: horizontal tile boundaries j = R t (0 < j < ny),
+// vertical ones i = 64 t (0 < i < nx); y = c0 + c1 (AM_RESID: (r - c0) - c1)
+template <int MODE, bool DOT>
+__global__ void __launch_bounds__(256) k_strip_fixup(const LevelDev L, const double* x, double* y,
+                                                     const double* __restrict__ r,
+                                                     double* __restrict__ partials) {
+  pdl_enter();
+  const int nx = L.nx, ny = L.ny, R = L.strip_r, K1 = L.k1;
+  const int64_t nh = (int64_t)(ny / R - 1) * nx, nv = (int64_t)(nx / 64 - 1) * ny;
+  double dot = 0.0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nh + nv;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t g;
+    if (t < nh) {
+      const int jb = (int)(t / nx + 1) * R, i = (int)(t % nx);
+      g = hedge(nx, i, jb);
+    } else {
+      const int64_t u = t - nh;
+      const int ib = (int)(u / ny + 1) * 64, j = (int)(u % ny);
+      g = vedge(nx, ny, ib, j);
+    }
+    for (int a = 0; a < K1; ++a) {
+      const double c0 = L.pc0[g * K1 + a], c1 = L.pc1[g * K1 + a];
+      const double v = MODE == AM_RESID ? (__ldg(r + g * K1 + a) - c0) - c1 : c0 + c1;
+      y[g * K1 + a] = v;
+      if (DOT) dot = fma(x[g * K1 + a], v, dot);
+    }
+  }
+  if (DOT) {
+    __shared__ double red[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dot;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += red[w];
+      partials[blockIdx.x] = s;
+    }
+  }
+}
+
+static int strip_fixup_grid(const LevelDev& L) {
+  const int64_t n = (int64_t)(L.ny / L.strip_r - 1) * L.nx + (int64_t)(L.nx / 64 - 1) * L.ny;
+  const int64_t g = (n + 255) / 256;
+  return (int)(g < 148 ? (g > 0 ? g : 1) : 148);
+}
+static int strip_grid(const LevelDev& L) {
+  const int ntiles = (L.nx / 64) * (L.ny / L.strip_r);
+  const int g = 148 * 2;
+  return ntiles < g ? ntiles : g;
+}
+static bool strip_ok(const LevelDev& L, int mode) {
+  return L.strip_r > 0 && (mode == AM_APPLY || mode == AM_RESID) && L.pc0 && L.pc1 &&
+         !L.ns && L.imask == 0 && L.dmask == 15 && L.nx % 64 == 0 && L.ny % L.strip_r == 0 &&
+         L.ny / L.strip_r >= 1;
+}
+
+template <int P, int MODE, bool DOT>
+static void launch_strip_t(const LevelDev& L, const double* x, double* y, const double* r,
+                           double* partials, bool pdl, cudaStream_t st) {
+  const size_t smem = (size_t)2 * TmaCfg<P>::CHUNK_BYTES;
+  const int grid = strip_grid(L);
+  double* pf = partials ? partials + grid : nullptr;
+  switch (L.strip_r) {
+#define STRIP_CASE(RV)                                                                        \
+    case RV: {                                                                                \
+      static bool attr = false;                                                               \
+      if (!attr) {                                                                            \
+        cudaFuncSetAttribute(k_apply_strip<P, MODE, DOT, RV>,                                 \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
+        attr = true;                                                                          \
+      }                                                                                       \
+      launch_ex(k_apply_strip<P, MODE, DOT, RV>, grid, 32, smem, pdl, st, L, x, y, r,         \
+                partials, pdl ? 1 : 0);                                                       \
+      break;                                                                                  \
+    }
+    STRIP_CASE(2)
+    STRIP_CASE(4)
+    default: STRIP_CASE(8)
+#undef STRIP_CASE
+  }
+  launch_ex(k_strip_fixup<MODE, DOT>, strip_fixup_grid(L), 256, 0, true, st, L, x, y, r, pf);
+}
+
+template <int P>
+static void launch_strip_p(const LevelDev& L, int mode, const double* x, double* y,
+                           const double* r, double* partials, bool pdl, cudaStream_t st) {
+  if (mode == AM_RESID) launch_strip_t<P, AM_RESID, false>(L, x, y, r, nullptr, pdl, st);
+  else if (partials) launch_strip_t<P, AM_APPLY, true>(L, x, y, r, partials, pdl, st);
+  else launch_strip_t<P, AM_APPLY, false>(L, x, y, r, nullptr, pdl, st);
+}
+
 // ---------------------------------------------------------------- LU-SGS colour sweep, edge rows only
 // One LU-SGS colour sweep (reading F3) needs (r - A x)_e on the
 // edges of ONE colour only, and every element has exactly one edge of each colour:
@@ -1354,6 +1657,7 @@ static int fused_grid(const LevelDev& L) {
 }
 
 int apply2_grid(const LevelDev& L, int mode) {
+  if (strip_ok(L, mode)) return strip_grid(L) + strip_fixup_grid(L);
   if (!fused_for(L) || L.sync == nullptr || L.imask != 0 || mode == AM_GSC || L.ns)
     return apply_grid_mode(L, mode);
   switch (L.p) {
@@ -1462,6 +1766,15 @@ int launch_apply(const LevelDev& L, int colour, int mode, const double* x, doubl
 
 int launch_apply2(const LevelDev& L, int mode, const double* x, double* y, const double* r,
                   double* d, int step, double* partials, bool pdl, cudaStream_t st) {
+  if (strip_ok(L, mode)) {
+    switch (L.p) {
+      case 1: launch_strip_p<1>(L, mode, x, y, r, partials, pdl, st); break;
+      case 2: launch_strip_p<2>(L, mode, x, y, r, partials, pdl, st); break;
+      case 3: launch_strip_p<3>(L, mode, x, y, r, partials, pdl, st); break;
+      default: launch_strip_p<4>(L, mode, x, y, r, partials, pdl, st); break;
+    }
+    return 2;
+  }
   if (!fused_for(L) || L.sync == nullptr || L.imask != 0 || mode == AM_GSC || L.ns) {   // fused: 1 GPU
     int n = launch_apply(L, 0, AM_W0, x, y, nullptr, nullptr, 0, nullptr, pdl, st);
     return n + launch_apply(L, 1, mode, x, y, r, d, step, partials, pdl, st);

@@ -51,6 +51,9 @@ struct LevelDev {
                            // colour-1 element); streamed with S_T by the smoothing applies
   int ndi;                 // 4 * k1*(k1+1)/2
   double* coef;            // [2*MAX_NU] smoothing coefficients (c1_j, c2_j), device
+  double *pc0, *pc1;       // single-pass strip apply (MGDTN_STRIP): partial sums of the
+                           // tile-perimeter edges from their colour-0 / colour-1 element
+  int strip_r;             // rows per strip tile (0: strip apply off on this level)
   int smoother;            // 0 BJ, 1 Chebyshev (d vector used)
   unsigned* sync;          // fused apply: [0] generation, [1] CTA exit count,
                            // [2 + c] generation at which colour-0 chunk c was stored

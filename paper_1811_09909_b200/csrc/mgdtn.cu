@@ -27,6 +27,7 @@ struct HostLevel {
   int kind = KIND_COARSEST;
   double h = 0.0;
   size_t o_sync = 0, o_S = 0, o_Dinv = 0, o_Dc = 0, o_coef = 0, o_lam = 0, o_r = 0, o_e = 0, o_w = 0, o_d = 0;
+  size_t o_pc0 = 0, o_pc1 = 0;   // strip-apply perimeter partials (MGDTN_STRIP)
   size_t o_KIIinv = 0, o_Pm = 0, o_Rm = 0, o_cbuf = 0, o_lpart = 0;
   double* lpart = nullptr;   // per-level partial sums + 16 scalars (concurrent power iterations)
   double *KIIinv = nullptr, *Pm = nullptr, *cbuf = nullptr;
@@ -208,6 +209,10 @@ static void layout(Ctx* c) {
     L.o_e = take(d.ndof * sizeof(double));
     L.o_w = take(d.ndof * sizeof(double));
     L.o_d = take(d.ndof * sizeof(double));
+    if (L.d.strip_r > 0) {
+      L.o_pc0 = take(d.ndof * sizeof(double));
+      L.o_pc1 = take(d.ndof * sizeof(double));
+    }
     if (L.kind == KIND_H) {
       int64_t nmac = (int64_t)(d.nx / 2) * (d.ny / 2);
       L.o_KIIinv = take(nmac * 64 * sizeof(double));
@@ -286,6 +291,8 @@ static void bind_pointers(Ctx* c) {
     L.d.S = D(L.o_S);
     L.d.Dinv = D(L.o_Dinv);
     L.d.Dc = c->ns ? nullptr : D(L.o_Dc);   // packed-symmetric D_e^-1: symmetric levels only
+    L.d.pc0 = L.d.strip_r > 0 ? D(L.o_pc0) : nullptr;
+    L.d.pc1 = L.d.strip_r > 0 ? D(L.o_pc1) : nullptr;
     L.d.coef = D(L.o_coef);
     L.lpart = D(L.o_lpart);
     L.lam = D(L.o_lam);
@@ -1501,6 +1508,16 @@ int mg_build_hierarchy_ex(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_level
   plan_tail(c);
   plan_tail_dense(c);
   plan_l2(c);
+  {   // MGDTN_STRIP=R (2 / 4 / 8): single-pass strip apply on the levels it fits
+    const int R = env_or("MGDTN_STRIP", 0);
+    for (auto& L : c->lev) {
+      LevelDev& d = L.d;
+      d.strip_r = 0;
+      if ((R == 2 || R == 4 || R == 8) && !partitioned(c) && !c->ns && d.nx % 64 == 0 &&
+          d.ny % R == 0 && d.nx >= 128)
+        d.strip_r = R;
+    }
+  }
   layout(c);   // host only: no CUDA call until mg_bind_workspace
   *out_ctx = c;
   return MG_OK;
