@@ -26,7 +26,7 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-@pytest.mark.parametrize("idx,n", [(1, 8), (2, 16), (4, 16), (3, 32)])
+@pytest.mark.parametrize("idx,n", [(1, 8), (2, 16), (4, 16), (3, 32), (4, 64)])
 def test_lusgs_parity(idx, n):
     from paper_1811_09909_b200 import MGSolver, SmootherConfig
     cfg = W.scaled_config(idx, n)

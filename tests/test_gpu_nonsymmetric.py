@@ -63,7 +63,10 @@ class NSCase:
 
 
 CASES = [(1, 8, 1, "nipg"), (4, 16, 3, "tiles"), (2, 16, 4, "iipg"), (4, 16, 2, "nipg"),
-         (4, 64, 3, "tiles"), (2, 32, 4, "tiles")]
+         (4, 64, 3, "tiles"), (2, 32, 4, "tiles"), (2, 64, 2, "nipg")]
+# n <= 64 as in test_gpu_parity.py: at n = 128 the per-V-cycle gap reaches the FP64 floor of two
+# valid eliminations amplified through 7 Galerkin levels (3.1e-12 here, 1.8e-12 for config 2's
+# symmetric recipe), above the 1e-12 per-V-cycle gate
 
 
 @pytest.fixture(scope="module", params=CASES, ids=[f"c{a}n{b}p{c}{d}" for a, b, c, d in CASES])
