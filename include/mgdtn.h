@@ -19,8 +19,9 @@
  *     for the duration of the call, unless the name ends in _host.
  *   - All device work is issued on the ctx stream (mg_build_hierarchy's
  *     `cuda_stream`, a cudaStream_t or NULL = legacy default stream).
- *     mg_apply / mg_vcycle / mg_assemble_rhs / mg_setup_dtn are asynchronous;
- *     mg_pcg_solve and the *_host calls synchronise the stream.
+ *     mg_apply / mg_vcycle / mg_assemble_rhs are asynchronous; mg_setup_dtn
+ *     synchronises once at its end (to report local-solve errors); the solvers
+ *     and the *_host calls synchronise the stream.
  *   - The library allocates no device memory: everything lives in one
  *     caller-allocated workspace (mg_workspace_bytes / mg_bind_workspace)
  *     that must stay alive until mg_destroy.
@@ -193,8 +194,9 @@ int mg_bind_workspace(void* ctx, void* dev_ptr, size_t bytes);
  * MG_SIPG_H} (any of the four codes on a MG_BUILD_NONSYMMETRIC ctx; an IIPG-H /
  * NIPG-H code on a symmetric ctx is MG_ERR_ARG), tau[ne] > 0 (stabilisation of the element's own flux,
  * Eq. HDG_flux / IPDG_flux), all device arrays in element-id order.
- * Errors: MG_ERR_NOT_SPD / MG_ERR_SINGULAR_LOCAL with the element index
- * (detected asynchronously; reported by the next synchronising call). */
+ * Errors: MG_ERR_NOT_SPD / MG_ERR_SINGULAR_LOCAL (nonsymmetric context: a
+ * vanishing LU pivot) with the element / edge / macro index, MG_ERR_ARG for
+ * invalid K, tau or method (checked on the device; reported by this call). */
 int mg_setup_dtn(void* ctx, const double* K, const int8_t* method, const double* tau,
                  const mg_smoother_cfg* smoother);
 
