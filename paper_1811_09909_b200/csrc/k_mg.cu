@@ -304,6 +304,76 @@ __global__ void k_pcg_pupdate(double* p, const double* __restrict__ z,
     p[i] = fma(beta, p[i], z[i]);
 }
 
+// ---- PCG scalar reductions folded into their consumers (MGDTN_PCG_FUSED, one GPU):
+// every block sums the producer's partials in the same fixed order (so every block
+// holds the identical value) instead of a separate one-block k_reduce launch.
+// Slots: [6] rz of the current z (written by the p-update, read by the x/r update,
+// which copies it to [0] for the next beta); [0] rz of the previous z.
+__device__ __forceinline__ double sum_partials(const double* __restrict__ part, int n) {
+  __shared__ double bc;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  s = block_sum(s);
+  if (threadIdx.x == 0) bc = s;
+  __syncthreads();
+  const double v = bc;
+  __syncthreads();
+  return v;
+}
+
+__global__ void k_pcg_update_fused(double* x, double* r, const double* __restrict__ p,
+                                   const double* __restrict__ ap, double* scal, int64_t n,
+                                   const double* __restrict__ pap_part, int n_pap,
+                                   double* partials, OwnMask om) {
+  pdl_enter();
+  const double pAp = sum_partials(pap_part, n_pap);
+  const double rz = scal[6];
+  const double alpha = pAp > 0.0 ? rz / pAp : 0.0;   // pAp <= 0: breakdown (k_pcg_check)
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    scal[1] = pAp;
+    scal[3] = alpha;
+    scal[0] = rz;
+  }
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, ap[i], r[i]);
+    r[i] = ri;
+    if (counted(om, i)) s = fma(ri, ri, s);
+  }
+  s = block_sum(s);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+int launch_pcg_update_fused(double* x, double* r, const double* p, const double* ap, double* scal,
+                            int64_t n, const double* pap_part, int n_pap, double* partials,
+                            int grid, cudaStream_t st, const LevelDev* L) {
+  launch_ex(k_pcg_update_fused, grid, 256, 0, true, st, x, r, p, ap, scal, n, pap_part, n_pap,
+            partials, own_mask(L));
+  return 1;
+}
+
+__global__ void k_pcg_pupdate_fused(double* p, const double* __restrict__ z, double* scal,
+                                    int64_t n, const double* __restrict__ rz_part, int n_rz) {
+  pdl_enter();
+  const double rz = sum_partials(rz_part, n_rz);
+  const double beta = rz / scal[0];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    scal[6] = rz;
+    scal[4] = beta;
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
+}
+
+int launch_pcg_pupdate_fused(double* p, const double* z, double* scal, int64_t n,
+                             const double* rz_part, int n_rz, cudaStream_t st) {
+  launch_ex(k_pcg_pupdate_fused, vec_grid(n), 256, 0, true, st, p, z, scal, n, rz_part, n_rz);
+  return 1;
+}
+
 int launch_pcg_pupdate(double* p, const double* z, const double* scal, int64_t n,
                        cudaStream_t st) {
   launch_ex(k_pcg_pupdate, vec_grid(n), 256, 0, true, st, p, z, scal, n);

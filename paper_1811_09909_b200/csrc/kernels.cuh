@@ -425,6 +425,12 @@ int launch_copy(double* dst, const double* src, int64_t n, cudaStream_t st);
 int launch_zero(double* dst, int64_t n, cudaStream_t st);
 int launch_copy_masked(const LevelDev& L, double* dst, const double* src, cudaStream_t st);
 int launch_add(double* dst, const double* src, int64_t n, cudaStream_t st);
+// PCG updates with the scalar reductions folded in (k_mg.cu, MGDTN_PCG_FUSED)
+int launch_pcg_update_fused(double* x, double* r, const double* p, const double* ap, double* scal,
+                            int64_t n, const double* pap_part, int n_pap, double* partials,
+                            int grid, cudaStream_t st, const LevelDev* L);
+int launch_pcg_pupdate_fused(double* p, const double* z, double* scal, int64_t n,
+                             const double* rz_part, int n_rz, cudaStream_t st);
 int launch_axpy_dev(const double* coef, double sign, const double* x, double* y, int64_t n,
                     cudaStream_t st);   // y += sign * coef[0] * x (device coefficient)
 int launch_scale_rsqrt(const double* ss, double* v, int64_t n, cudaStream_t st);

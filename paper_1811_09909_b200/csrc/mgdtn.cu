@@ -919,9 +919,24 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
 
 // ---------------------------------------------------------------- PCG
 // scal: [0] rz, [1] pAp, [2] rr, [3] alpha, [4] beta, [5] gg
+// MGDTN_PCG_FUSED=1 (one GPU): alpha and beta are reduced inside the update kernels
+static bool pcg_fused(const Ctx* c) {
+  static const bool on = env_or("MGDTN_PCG_FUSED", 0) != 0;
+  return on && !partitioned(c);
+}
+static inline int rz_slot(const Ctx* c) { return pcg_fused(c) ? 6 : 0; }
+
 static void pcg_iter_A(Ctx* c) {  // Ap, alpha, x/r update, rr
   HostLevel& F = c->lev[0];
   const int vg = vec_grid(F.d.ndof);
+  if (pcg_fused(c)) {
+    apply_full(c, F, c->pv, c->ap, c->part);
+    double* rr_part = c->part + 1024;   // disjoint from the pAp partials being read
+    c->launches += launch_pcg_update_fused(c->x, F.r, c->pv, c->ap, c->scal, F.d.ndof, c->part,
+                                           apply_parts(F.d, AM_APPLY), rr_part, vg, c->st, &F.d);
+    reduce_scal(c, rr_part, vg, c->scal, 2, 0);
+    return;
+  }
   apply_full(c, F, c->pv, c->ap, c->part);
   reduce_scal(c, c->part, apply_parts(F.d, AM_APPLY), c->scal, 1, 1);
   c->launches += launch_pcg_update(c->x, F.r, c->pv, c->ap, c->scal, F.d.ndof, c->part, vg, c->st,
@@ -934,6 +949,10 @@ static void pcg_iter_B(Ctx* c) {  // z = B r, beta, p update
   const int vg = vec_grid(F.d.ndof);
   vcycle_level(c, 0, false);
   c->launches += launch_dot(F.r, F.e, F.d.ndof, c->part, vg, c->st, &F.d);
+  if (pcg_fused(c)) {
+    c->launches += launch_pcg_pupdate_fused(c->pv, F.e, c->scal, F.d.ndof, c->part, vg, c->st);
+    return;
+  }
   reduce_scal(c, c->part, vg, c->scal, 0, 2);
   c->launches += launch_pcg_pupdate(c->pv, F.e, c->scal, F.d.ndof, c->st);
 }
@@ -950,7 +969,7 @@ static void pcg_prologue(Ctx* c) {
   reduce_scal(c, c->part, vg, c->scal, 5, 0);
   vcycle_level(c, 0, false);
   c->launches += launch_dot(F.r, F.e, n, c->part, vg, c->st, &F.d);
-  reduce_scal(c, c->part, vg, c->scal, 0, 0);
+  reduce_scal(c, c->part, vg, c->scal, rz_slot(c), 0);
   c->launches += launch_copy(c->pv, F.e, n, c->st);
   pcg_iter_A(c);
   c->launches += launch_pcg_check(c->scal, c->ist, c->dhist, HIST_CAP, c->cond, c->st);
@@ -1065,7 +1084,7 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
   // z = B r ; rz = r.z ; p = z
   vcycle_level(c, 0, false);
   c->launches += launch_dot(F.r, F.e, n, c->part, vg, st, &F.d);
-  reduce_scal(c, c->part, vg, c->scal, 0, 0);
+  reduce_scal(c, c->part, vg, c->scal, rz_slot(c), 0);
   c->launches += launch_copy(c->pv, F.e, n, st);
   CK(cudaGetLastError());
   for (it = 1; it <= maxit; ++it) {
