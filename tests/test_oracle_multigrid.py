@@ -467,3 +467,48 @@ def test_nonsymmetric_gmres_equals_direct_solve(method):
     assert np.linalg.norm(res["x"] - x_ref) <= 1e-8 * np.linalg.norm(x_ref)
     with pytest.raises(ValueError):
         multigrid.Hierarchy(ts.A, n, p, smoother=1)
+
+
+@pytest.mark.parametrize("nu", [2, 3, 4])
+@pytest.mark.parametrize("level,lmax_scale", [(0, None), (1, None), (0, 1.4)])
+def test_chebyshev_error_propagator_closed_form(nu, level, lmax_scale):
+    """O8 pinned against the closed form of the Chebyshev iteration (PAPER.md:1054-1057;
+    the three-term recurrence is Saad, Iterative Methods, Alg. 12.1).  From e = 0 the
+    nu-step smoother's error propagator on A e = r is the residual polynomial
+
+        E_nu = p_nu(D^-1 A),  p_nu(lam) = T_nu((theta - lam)/delta) / T_nu(theta/delta),
+
+    theta = (b + a)/2, delta = (b - a)/2, [a, b] = [b/30, b].  D^-1 A is diagonalised by
+    the generalised symmetric eigenproblem A V = D V Lam (V^T D V = I), so the expected
+    propagator is V p_nu(Lam) V^T D.  The smoother is run on every unit residual of a
+    real hierarchy level (config-2 recipe, p = 2: the p-level and the first h-level),
+    E = I - M A with M r = smooth(0, r).  A wrong rho_0, rho_k update or 2 rho_k/delta
+    factor changes p_nu at every eigenvalue and fails this test.  lmax_scale overrides b
+    (an over-estimate of lambda_max, so the interval does not touch the spectrum's top)."""
+    import scipy.linalg as sla
+    from numpy.polynomial import chebyshev as C
+
+    ts, H = _hier(8, 2, smoother=1)
+    L = H.levels[level]
+    Ad = L.A.toarray()
+    n = Ad.shape[0]
+    k = L.k1
+    Dd = np.zeros_like(Ad)
+    for q in range(n // k):
+        Dd[q * k:(q + 1) * k, q * k:(q + 1) * k] = L.D[q]
+    lam, V = sla.eigh(Ad, Dd)
+    if lmax_scale is not None:
+        L.lam_max = lmax_scale * lam.max()
+    b = L.lam_max
+    a = b / 30.0
+    theta, delta = 0.5 * (b + a), 0.5 * (b - a)
+    Tnu = np.zeros(nu + 1)
+    Tnu[nu] = 1.0
+    pnu = C.chebval((theta - lam) / delta, Tnu) / C.chebval(theta / delta, Tnu)
+    E_exp = V @ np.diag(pnu) @ V.T @ Dd
+    M = np.stack([H.smooth(level, np.zeros(n), col, nu) for col in np.eye(n)], axis=1)
+    E = np.eye(n) - M @ Ad
+    assert np.abs(E - E_exp).max() <= 1e-12 * max(1.0, np.abs(E_exp).max())
+    # Chebyshev minimax bound on the interval: |p_nu| <= 1 / T_nu(theta / delta) there
+    inside = (lam >= a) & (lam <= b)
+    assert np.all(np.abs(pnu[inside]) <= 1.0 / C.chebval(theta / delta, Tnu) + 1e-14)

@@ -25,6 +25,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs (per-kernel profiling)")
+    ap.add_argument("--maxit", type=int, default=4000, help="PCG iteration cap (short per-iteration profiles)")
+    ap.add_argument("--warm", type=int, default=2)
     a = ap.parse_args()
     cfg = W.CONFIGS[a.config]
     pr = W.make_problem(cfg)
@@ -40,10 +42,10 @@ def main():
         s = MGSolver(cfg.n, p=cfg.p, device=dev, stream=st)
         if a.eager:
             s.use_graphs(False)
-        for _ in range(2):   # warm-up (graph capture, lazy attributes)
+        for _ in range(a.warm):   # warm-up (graph capture, lazy attributes)
             s.setup(K, meth, tau, sm)
             g, _ = s.assemble_rhs(fq, pr.f_const, gD)
-            s.pcg_solve(g, rtol=cfg.rtol, maxit=4000)
+            s.pcg_solve(g, rtol=cfg.rtol, maxit=a.maxit)
         torch.cuda.synchronize()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         torch.cuda.nvtx.range_push("mg")
@@ -57,7 +59,7 @@ def main():
         torch.cuda.nvtx.range_pop()
         ev[2].record(st)
         torch.cuda.nvtx.range_push("solve")
-        lam, info = s.pcg_solve(g, rtol=cfg.rtol, maxit=4000)
+        lam, info = s.pcg_solve(g, rtol=cfg.rtol, maxit=a.maxit)
         torch.cuda.nvtx.range_pop()
         ev[3].record(st)
         torch.cuda.nvtx.range_pop()
