@@ -22,7 +22,7 @@ SOURCES = ["k_apply.cu", "k_setup.cu", "k_local_ns.cu", "k_mg.cu", "k_coarse.cu"
 def _compile(src: str) -> str:
     out = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
     path = os.path.join(CSRC, src)
-    deps = [path] + [os.path.join(CSRC, h) for h in ("kernels.cuh", "bodies.cuh", "tail.h", "refelem.h", "comm.h")] + \
+    deps = [path] + [os.path.join(CSRC, h) for h in ("kernels.cuh", "bodies.cuh", "tail.h", "refelem.h", "comm.h", "d4.cuh")] + \
         [os.path.join(ROOT, "include", "mgdtn.h")]
     if os.path.exists(out) and all(os.path.getmtime(out) >= os.path.getmtime(d) for d in deps):
         return out

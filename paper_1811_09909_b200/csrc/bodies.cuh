@@ -329,99 +329,6 @@ __device__ __forceinline__ void restrict_edges_body(const LevelDev& F, const Lev
   }
 }
 
-// (Q_M res_I)[slot] of macro M (the cbuf entry of lc_restrict_body, same FMA order)
-__device__ __forceinline__ double macro_cb(const LevelDev& F, const double* __restrict__ res,
-                                           const double* __restrict__ Rm, int64_t M, int nxc,
-                                           int slot) {
-  const int J = (int)((uint64_t)M / (unsigned)nxc), I = (int)(M - (int64_t)J * nxc);
-  int64_t ie[4];
-  macro_interior_edges(F, I, J, ie);
-  const double* P = Rm + M * 64 + slot;
-  double acc = 0.0;
-#pragma unroll
-  for (int l = 0; l < 4; ++l) {
-    acc = fma(P[(2 * l) * 8], res[ie[l] * 2], acc);
-    acc = fma(P[(2 * l + 1) * 8], res[ie[l] * 2 + 1], acc);
-  }
-  return acc;
-}
-
-// step 3 and the whole restriction in ONE pass (one GPU): work items [0, n_lc) are the
-// local-correction rows of lc_restrict_body, the rest the coarse edges of
-// restrict_edges_body, whose macro terms are formed on the fly (each cbuf entry feeds
-// exactly one coarse edge, so nothing is computed twice).  Same arithmetic, same order.
-__device__ __forceinline__ void lc_restrict_fused_body(const LevelDev& F, const LevelDev& C,
-                                                       const double* __restrict__ res, double* e,
-                                                       const double* __restrict__ KIIinv,
-                                                       const double* __restrict__ Rm, int do_lc,
-                                                       double* rc, int fuse, double* ec,
-                                                       double* dc, int64_t t0, int64_t nt) {
-  const int nxc = C.nx, nyc = C.ny;
-  const int64_t nmac = (int64_t)nxc * nyc;
-  const int64_t n_lc = do_lc ? 8 * nmac : 0;
-  const int64_t nh = (int64_t)nxc * (nyc + 1);
-  const double c2 = fuse ? C.coef[1] : 0.0;
-  for (int64_t w = t0; w < n_lc + C.nedge; w += nt) {
-    if (w < n_lc) {
-      const int64_t M = w >> 3;
-      const int c = (int)(w & 7);
-      const int J = (int)((uint64_t)M / (unsigned)nxc), I = (int)M - J * nxc;
-      int64_t ie[4];
-      macro_interior_edges(F, I, J, ie);
-      const double* Ki = KIIinv + M * 64 + c * 8;
-      double acc = 0.0;
-#pragma unroll
-      for (int l = 0; l < 4; ++l) {
-        acc = fma(Ki[2 * l], res[ie[l] * 2], acc);
-        acc = fma(Ki[2 * l + 1], res[ie[l] * 2 + 1], acc);
-      }
-      e[ie[c >> 1] * 2 + (c & 1)] += acc;
-      continue;
-    }
-    const int64_t E = w - n_lc;
-    double v0 = 0.0, v1 = 0.0;
-    const bool bnd = edge_on_boundary(nxc, nyc, E);
-    if (E < nh) {
-      const int J = (int)((uint64_t)E / (unsigned)nxc), I = (int)E - J * nxc;
-      if (!bnd) {
-        const int64_t f0 = hedge(F.nx, 2 * I, 2 * J), f1 = hedge(F.nx, 2 * I + 1, 2 * J);
-        const double a0 = res[f0 * 2], a1 = res[f0 * 2 + 1], b0 = res[f1 * 2], b1 = res[f1 * 2 + 1];
-        v0 = a0 + 0.5 * a1 + 0.5 * b0;
-        v1 = 0.5 * a1 + 0.5 * b0 + b1;
-        const int64_t Mb = (int64_t)(J - 1) * nxc + I, Ma = (int64_t)J * nxc + I;
-        v0 += macro_cb(F, res, Rm, Mb, nxc, 4) + macro_cb(F, res, Rm, Ma, nxc, 0);
-        v1 += macro_cb(F, res, Rm, Mb, nxc, 5) + macro_cb(F, res, Rm, Ma, nxc, 1);
-      }
-    } else {
-      const int64_t rr = E - nh;
-      const int J = (int)((uint64_t)rr / (unsigned)(nxc + 1)), I = (int)rr - J * (nxc + 1);
-      if (!bnd) {
-        const int64_t f0 = vedge(F.nx, F.ny, 2 * I, 2 * J), f1 = vedge(F.nx, F.ny, 2 * I, 2 * J + 1);
-        const double a0 = res[f0 * 2], a1 = res[f0 * 2 + 1], b0 = res[f1 * 2], b1 = res[f1 * 2 + 1];
-        v0 = a0 + 0.5 * a1 + 0.5 * b0;
-        v1 = 0.5 * a1 + 0.5 * b0 + b1;
-        const int64_t Ml = (int64_t)J * nxc + (I - 1), Mr = (int64_t)J * nxc + I;
-        v0 += macro_cb(F, res, Rm, Ml, nxc, 2) + macro_cb(F, res, Rm, Mr, nxc, 6);
-        v1 += macro_cb(F, res, Rm, Ml, nxc, 3) + macro_cb(F, res, Rm, Mr, nxc, 7);
-      }
-    }
-    rc[E * 2] = v0;
-    rc[E * 2 + 1] = v1;
-    if (fuse && !bnd) {
-      const double* Di = C.Dinv + E;
-      const int64_t sd = C.nedge;
-      double e0 = c2 * (Di[0] * v0 + Di[sd] * v1);
-      double e1 = c2 * (Di[2 * sd] * v0 + Di[3 * sd] * v1);
-      ec[E * 2] = e0;
-      ec[E * 2 + 1] = e1;
-      if (C.smoother == 1) {
-        dc[E * 2] = e0;
-        dc[E * 2 + 1] = e1;
-      }
-    }
-  }
-}
-
 // prolongation (macro): e_I += P_M e_c(M); e_B += J e_c on the macro's bottom and
 // left macro-edges (every interior macro-edge is the bottom or left edge of
 // exactly one macro).  Work item = (macro M, t in 0..7): row t of P_M e_c, and

@@ -7,6 +7,7 @@
 #include <cstdlib>
 
 #include "bodies.cuh"
+#include "d4.cuh"
 
 namespace mgdtn {
 
@@ -75,8 +76,45 @@ __global__ void k_smooth_first_dc(LevelDev L, const double* __restrict__ r, doub
   }
 }
 
+// the same step on an orbit-stored level (R9): edge-parallel, D_e^-1 from its
+// centrosymmetric orbits Dso (SoA, coalesced), r / e / d as contiguous per-edge rows
+template <int P>
+__global__ void k_smooth_first_orb(LevelDev L, const double* __restrict__ r, double* e, double* d) {
+  pdl_enter();
+  using D = D4<P>;
+  constexpr int K1 = P + 1;
+  const double c2 = L.coef[1];
+  for (int64_t ed = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ed < L.nedge;
+       ed += (int64_t)gridDim.x * blockDim.x) {
+    if (edge_on_boundary(L.nx, L.ny, ed, L.dmask)) continue;
+    double dv[D::NCS], rv[K1];
+#pragma unroll
+    for (int o = 0; o < D::NCS; ++o) dv[o] = __ldg(L.Dso + (int64_t)o * L.nedge + ed);
+#pragma unroll
+    for (int a = 0; a < K1; ++a) rv[a] = __ldg(r + ed * K1 + a);
+#pragma unroll
+    for (int a = 0; a < K1; ++a) {
+      double c = 0.0;
+#pragma unroll
+      for (int b = 0; b < K1; ++b) c = fma(dv[D::cs(D::pe(a, b))], rv[b], c);
+      const double v = c2 * c;
+      e[ed * K1 + a] = v;
+      if (L.smoother == 1) d[ed * K1 + a] = v;
+    }
+  }
+}
+
 int launch_smooth_first(const LevelDev& L, const double* r, double* e, double* d,
                         cudaStream_t st) {
+  if (L.orb) {
+    const int g = cap_grid(L.nedge, 128, 148 * 16);
+    switch (L.k1) {
+      case 2: launch_ex(k_smooth_first_orb<1>, g, 128, 0, true, st, L, r, e, d); return 1;
+      case 3: launch_ex(k_smooth_first_orb<2>, g, 128, 0, true, st, L, r, e, d); return 1;
+      case 4: launch_ex(k_smooth_first_orb<3>, g, 128, 0, true, st, L, r, e, d); return 1;
+      default: launch_ex(k_smooth_first_orb<4>, g, 128, 0, true, st, L, r, e, d); return 1;
+    }
+  }
   if (L.imask == 0 && L.Dc != nullptr) {
     const int g = cap_grid(2 * L.ne, 128, 148 * 16);
     switch (L.k1) {
@@ -118,24 +156,6 @@ int launch_restrict_edges(const LevelDev& F, const LevelDev& C, const double* re
                           double* dc, cudaStream_t st) {
   launch_ex(k_restrict_edges, cap_grid(C.nedge, 128, 148 * 8), 128, 0, true, st, F, C, res, cbuf, rc,
                                                                     fuse_first, ec, dc);
-  return 1;
-}
-
-__global__ void k_lc_restrict_fused(LevelDev F, LevelDev C, const double* __restrict__ res,
-                                    double* e, const double* __restrict__ KIIinv,
-                                    const double* __restrict__ Rm, int do_lc, double* rc,
-                                    int fuse, double* ec, double* dc) {
-  pdl_enter();
-  lc_restrict_fused_body(F, C, res, e, KIIinv, Rm, do_lc, rc, fuse, ec, dc, GTID, GNT);
-}
-
-int launch_lc_restrict_fused(const LevelDev& F, const LevelDev& C, const double* res, double* e,
-                             const double* KIIinv, const double* Rm, bool do_lc, double* rc,
-                             bool fuse_first, double* ec, double* dc, cudaStream_t st) {
-  const int64_t nmac = (int64_t)(F.nx / 2) * (F.ny / 2);
-  const int64_t n = (do_lc ? 8 * nmac : 0) + C.nedge;
-  launch_ex(k_lc_restrict_fused, cap_grid(n, 128, 148 * 8), 128, 0, true, st, F, C, res, e,
-            KIIinv, Rm, do_lc ? 1 : 0, rc, fuse_first ? 1 : 0, ec, dc);
   return 1;
 }
 
@@ -302,76 +322,6 @@ __global__ void k_pcg_pupdate(double* p, const double* __restrict__ z,
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     p[i] = fma(beta, p[i], z[i]);
-}
-
-// ---- PCG scalar reductions folded into their consumers (MGDTN_PCG_FUSED, one GPU):
-// every block sums the producer's partials in the same fixed order (so every block
-// holds the identical value) instead of a separate one-block k_reduce launch.
-// Slots: [6] rz of the current z (written by the p-update, read by the x/r update,
-// which copies it to [0] for the next beta); [0] rz of the previous z.
-__device__ __forceinline__ double sum_partials(const double* __restrict__ part, int n) {
-  __shared__ double bc;
-  double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
-  s = block_sum(s);
-  if (threadIdx.x == 0) bc = s;
-  __syncthreads();
-  const double v = bc;
-  __syncthreads();
-  return v;
-}
-
-__global__ void k_pcg_update_fused(double* x, double* r, const double* __restrict__ p,
-                                   const double* __restrict__ ap, double* scal, int64_t n,
-                                   const double* __restrict__ pap_part, int n_pap,
-                                   double* partials, OwnMask om) {
-  pdl_enter();
-  const double pAp = sum_partials(pap_part, n_pap);
-  const double rz = scal[6];
-  const double alpha = pAp > 0.0 ? rz / pAp : 0.0;   // pAp <= 0: breakdown (k_pcg_check)
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    scal[1] = pAp;
-    scal[3] = alpha;
-    scal[0] = rz;
-  }
-  double s = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    x[i] = fma(alpha, p[i], x[i]);
-    const double ri = fma(-alpha, ap[i], r[i]);
-    r[i] = ri;
-    if (counted(om, i)) s = fma(ri, ri, s);
-  }
-  s = block_sum(s);
-  if (threadIdx.x == 0) partials[blockIdx.x] = s;
-}
-
-int launch_pcg_update_fused(double* x, double* r, const double* p, const double* ap, double* scal,
-                            int64_t n, const double* pap_part, int n_pap, double* partials,
-                            int grid, cudaStream_t st, const LevelDev* L) {
-  launch_ex(k_pcg_update_fused, grid, 256, 0, true, st, x, r, p, ap, scal, n, pap_part, n_pap,
-            partials, own_mask(L));
-  return 1;
-}
-
-__global__ void k_pcg_pupdate_fused(double* p, const double* __restrict__ z, double* scal,
-                                    int64_t n, const double* __restrict__ rz_part, int n_rz) {
-  pdl_enter();
-  const double rz = sum_partials(rz_part, n_rz);
-  const double beta = rz / scal[0];
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    scal[6] = rz;
-    scal[4] = beta;
-  }
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = fma(beta, p[i], z[i]);
-}
-
-int launch_pcg_pupdate_fused(double* p, const double* z, double* scal, int64_t n,
-                             const double* rz_part, int n_rz, cudaStream_t st) {
-  launch_ex(k_pcg_pupdate_fused, vec_grid(n), 256, 0, true, st, p, z, scal, n, rz_part, n_rz);
-  return 1;
 }
 
 int launch_pcg_pupdate(double* p, const double* z, const double* scal, int64_t n,

@@ -4,6 +4,7 @@
 #include <cstdlib>
 
 #include "bodies.cuh"
+#include "d4.cuh"
 
 namespace mgdtn {
 
@@ -441,66 +442,6 @@ __device__ __forceinline__ double s_get(const double* base, int m, int ns, int a
 // NS: full row-major storage on both levels (nonsymmetric context): every entry of
 // J_p^T S_T J_p is formed (the symmetric path forms the upper triangle).
 template <int P, bool NS>
-__global__ void __launch_bounds__(128) k_p_coarsen(LevelDev F, LevelDev C,
-                                                   const double* __restrict__ Jp) {
-  constexpr int K1 = P + 1, M = 4 * K1;
-  double J[K1][2];
-#pragma unroll
-  for (int a = 0; a < K1; ++a) {
-    J[a][0] = Jp[a * 2];
-    J[a][1] = Jp[a * 2 + 1];
-  }
-  const int64_t nec = F.ne >> 1;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < 2 * nec;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int colour = (int)(t / nec);
-    const int64_t s = t - colour * nec;
-    const double* src = F.S + s_offset(F.nchunk, F.npk, colour, s, 0);
-    double* dst = C.S + s_offset(C.nchunk, C.npk, colour, s, 0);
-#pragma unroll
-    for (int f = 0; f < 4; ++f) {
-      double T[K1][8];
-#pragma unroll
-      for (int a = 0; a < K1; ++a)
-#pragma unroll
-        for (int B = 0; B < 8; ++B) T[a][B] = 0.0;
-#pragma unroll
-      for (int a = 0; a < K1; ++a) {
-        const int r = f * K1 + a;
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-#pragma unroll
-          for (int b = 0; b < K1; ++b) {
-            const int cidx = g * K1 + b;
-            const int lo = r < cidx ? r : cidx, hi = r < cidx ? cidx : r;
-            const double v =
-                NS ? __ldg(src + (int64_t)(r * M + cidx) * 32)
-                   : __ldg(src + (int64_t)(lo * (2 * M - lo + 1) / 2 + (hi - lo)) * 32);
-            T[a][2 * g] = fma(v, J[b][0], T[a][2 * g]);
-            T[a][2 * g + 1] = fma(v, J[b][1], T[a][2 * g + 1]);
-          }
-        }
-      }
-#pragma unroll
-      for (int al = 0; al < 2; ++al) {
-        const int A = 2 * f + al;
-#pragma unroll
-        for (int B = NS ? 0 : A; B < 8; ++B) {
-          double acc = 0.0;
-#pragma unroll
-          for (int a = 0; a < K1; ++a) acc = fma(J[a][al], T[a][B], acc);
-          dst[(int64_t)(NS ? A * 8 + B : pk_index(A, B, 8)) * 32] = acc;
-        }
-      }
-    }
-  }
-}
-
-// The same product with every stored entry of S_T loaded exactly once (210 loads per
-// element at p = 4 instead of 400): entry (a, b) of edge blocks (f, g) is scattered
-// straight into the coarse entries (2f + al, 2g + be) it feeds, accumulated in 36
-// (NS: 64) registers.  Loads are independent, so a thread keeps many in flight.
-template <int P, bool NS>
 __global__ void __launch_bounds__(128) k_p_coarsen_acc(LevelDev F, LevelDev C,
                                                        const double* __restrict__ Jp) {
   constexpr int K1 = P + 1, M = 4 * K1, NC = NS ? 64 : 36;
@@ -551,39 +492,18 @@ __global__ void __launch_bounds__(128) k_p_coarsen_acc(LevelDev F, LevelDev C,
 int launch_p_coarsen(const LevelDev& F, const LevelDev& C, const double* Jp, cudaStream_t st) {
   int64_t n = F.ne;
   int grid = (int)((n + 127) / 128 < 148 * 16 ? (n + 127) / 128 : 148 * 16);
-  static int v = -1;   // MGDTN_PCOARSEN=1: the row-block kernel (A/B)
-  if (v < 0) {
-    const char* e = std::getenv("MGDTN_PCOARSEN");
-    v = e ? std::atoi(e) : 2;
-  }
-  if (v == 2) {
-    if (F.ns) {
-      switch (F.p) {
-        case 2: k_p_coarsen_acc<2, true><<<grid, 128, 0, st>>>(F, C, Jp); break;
-        case 3: k_p_coarsen_acc<3, true><<<grid, 128, 0, st>>>(F, C, Jp); break;
-        default: k_p_coarsen_acc<4, true><<<grid, 128, 0, st>>>(F, C, Jp); break;
-      }
-    } else {
-      switch (F.p) {
-        case 2: k_p_coarsen_acc<2, false><<<grid, 128, 0, st>>>(F, C, Jp); break;
-        case 3: k_p_coarsen_acc<3, false><<<grid, 128, 0, st>>>(F, C, Jp); break;
-        default: k_p_coarsen_acc<4, false><<<grid, 128, 0, st>>>(F, C, Jp); break;
-      }
-    }
-    return 1;
-  }
   if (F.ns) {
     switch (F.p) {
-      case 2: k_p_coarsen<2, true><<<grid, 128, 0, st>>>(F, C, Jp); break;
-      case 3: k_p_coarsen<3, true><<<grid, 128, 0, st>>>(F, C, Jp); break;
-      default: k_p_coarsen<4, true><<<grid, 128, 0, st>>>(F, C, Jp); break;
+      case 2: k_p_coarsen_acc<2, true><<<grid, 128, 0, st>>>(F, C, Jp); break;
+      case 3: k_p_coarsen_acc<3, true><<<grid, 128, 0, st>>>(F, C, Jp); break;
+      default: k_p_coarsen_acc<4, true><<<grid, 128, 0, st>>>(F, C, Jp); break;
     }
-    return 1;
-  }
-  switch (F.p) {
-    case 2: k_p_coarsen<2, false><<<grid, 128, 0, st>>>(F, C, Jp); break;
-    case 3: k_p_coarsen<3, false><<<grid, 128, 0, st>>>(F, C, Jp); break;
-    default: k_p_coarsen<4, false><<<grid, 128, 0, st>>>(F, C, Jp); break;
+  } else {
+    switch (F.p) {
+      case 2: k_p_coarsen_acc<2, false><<<grid, 128, 0, st>>>(F, C, Jp); break;
+      case 3: k_p_coarsen_acc<3, false><<<grid, 128, 0, st>>>(F, C, Jp); break;
+      default: k_p_coarsen_acc<4, false><<<grid, 128, 0, st>>>(F, C, Jp); break;
+    }
   }
   return 1;
 }
@@ -880,10 +800,115 @@ __global__ void k_dinv_pack(LevelDev L) {
         }
   }
 }
+// orbit level (R9): D_e^-1 is centrosymmetric (d4.cuh); each orbit of the upper
+// triangle is replaced by its mean (in place, both triangles), and the orbit values go
+// to the SoA Dso (edge-parallel kernels)
+template <int P>
+__global__ void k_dinv_orb(LevelDev L) {
+  using D = D4<P>;
+  constexpr int K1 = P + 1;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < L.nedge;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double* Di = L.Dinv + e;
+    double sum[D::NCS];
+#pragma unroll
+    for (int o = 0; o < D::NCS; ++o) sum[o] = 0.0;
+#pragma unroll
+    for (int a = 0; a < K1; ++a)
+#pragma unroll
+      for (int b = a; b < K1; ++b) sum[D::cs(D::pe(a, b))] += Di[(int64_t)(a * K1 + b) * L.nedge];
+    double v[D::NCS];
+#pragma unroll
+    for (int o = 0; o < D::NCS; ++o) {
+      v[o] = sum[o] / (double)D::ccnt(o);
+      L.Dso[(int64_t)o * L.nedge + e] = v[o];
+    }
+#pragma unroll
+    for (int a = 0; a < K1; ++a)
+#pragma unroll
+      for (int b = 0; b < K1; ++b) Di[(int64_t)(a * K1 + b) * L.nedge] = v[D::cs(D::pe(a, b))];
+  }
+}
+// Dso -> the colour-1 element-chunk records Dco streamed by k_apply_orb
+template <int P>
+__global__ void k_dinv_pack_orb(LevelDev L) {
+  using D = D4<P>;
+  const int64_t nec = L.ne >> 1;
+  const int64_t nslot = (int64_t)L.nchunk * 32;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nslot;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int64_t ed[4] = {0, 0, 0, 0};
+    bool bd[4] = {true, true, true, true};
+    if (s < nec) {
+      int i, j;
+      slot_elem(L.nx, 1, s, i, j);
+      elem_edges(L.nx, L.ny, i, j, ed, bd, L.dmask);
+    }
+    double* dst = L.Dco + (s >> 5) * 4 * D::NCS * 32 + (s & 31);
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+#pragma unroll
+      for (int o = 0; o < D::NCS; ++o)
+        dst[(f * D::NCS + o) * 32] = bd[f] ? 0.0 : L.Dso[(int64_t)o * L.nedge + ed[f]];
+  }
+}
+
 int launch_dinv_pack(const LevelDev& L, cudaStream_t st) {
   const int64_t n = (int64_t)L.nchunk * 32;
-  int grid = (int)((n + 127) / 128 < 1184 ? (n + 127) / 128 : 1184);
+  const int grid = (int)((n + 127) / 128 < 1184 ? (n + 127) / 128 : 1184);
+  if (L.orb) {
+    const int ge = (int)((L.nedge + 127) / 128 < 1184 ? (L.nedge + 127) / 128 : 1184);
+    switch (L.p) {
+      case 1: k_dinv_orb<1><<<ge, 128, 0, st>>>(L); k_dinv_pack_orb<1><<<grid, 128, 0, st>>>(L); break;
+      case 2: k_dinv_orb<2><<<ge, 128, 0, st>>>(L); k_dinv_pack_orb<2><<<grid, 128, 0, st>>>(L); break;
+      case 3: k_dinv_orb<3><<<ge, 128, 0, st>>>(L); k_dinv_pack_orb<3><<<grid, 128, 0, st>>>(L); break;
+      default: k_dinv_orb<4><<<ge, 128, 0, st>>>(L); k_dinv_pack_orb<4><<<grid, 128, 0, st>>>(L); break;
+    }
+    return 2;
+  }
   k_dinv_pack<<<grid, 128, 0, st>>>(L);
+  return 1;
+}
+
+// orbit storage (R9): every element map of the level is replaced by its D4 orbit
+// averages (mean over the packed entries of each orbit, in packed order), in place,
+// and the orbit values are written to the chunk records So
+template <int P>
+__global__ void k_orbit_pack(LevelDev L) {
+  using D = D4<P>;
+  constexpr int NPK = D::NPK, NORB = D::NORB;
+  const int64_t nslot = (int64_t)L.nchunk * 32;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < 2 * nslot;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int colour = q >= nslot ? 1 : 0;
+    const int64_t s = q - colour * nslot;
+    const int64_t rec = (int64_t)colour * L.nchunk + (s >> 5);
+    double* Sp = L.S + rec * NPK * 32 + (s & 31);
+    double sum[NORB];
+#pragma unroll
+    for (int o = 0; o < NORB; ++o) sum[o] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < NPK; ++kk) sum[D::orb(kk)] += Sp[kk * 32];
+    double* Op = L.So + rec * NORB * 32 + (s & 31);
+#pragma unroll
+    for (int o = 0; o < NORB; ++o) {
+      sum[o] = sum[o] / (double)D::cnt(o);
+      Op[o * 32] = sum[o];
+    }
+#pragma unroll
+    for (int kk = 0; kk < NPK; ++kk) Sp[kk * 32] = sum[D::orb(kk)];
+  }
+}
+int launch_orbit_pack(const LevelDev& L, cudaStream_t st) {
+  if (!L.orb) return 0;
+  const int64_t n = (int64_t)L.nchunk * 64;
+  const int grid = (int)((n + 127) / 128 < 2368 ? (n + 127) / 128 : 2368);
+  switch (L.p) {
+    case 1: k_orbit_pack<1><<<grid, 128, 0, st>>>(L); break;
+    case 2: k_orbit_pack<2><<<grid, 128, 0, st>>>(L); break;
+    case 3: k_orbit_pack<3><<<grid, 128, 0, st>>>(L); break;
+    default: k_orbit_pack<4><<<grid, 128, 0, st>>>(L); break;
+  }
   return 1;
 }
 

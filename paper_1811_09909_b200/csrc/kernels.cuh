@@ -51,23 +51,18 @@ struct LevelDev {
                            // colour-1 element); streamed with S_T by the smoothing applies
   int ndi;                 // 4 * k1*(k1+1)/2
   double* coef;            // [2*MAX_NU] smoothing coefficients (c1_j, c2_j), device
-  double *pc0, *pc1;       // single-pass strip apply (MGDTN_STRIP): partial sums of the
-                           // tile-perimeter edges from their colour-0 / colour-1 element
-  int strip_r;             // rows per strip tile (0: strip apply off on this level)
   int smoother;            // 0 BJ, 1 Chebyshev (d vector used)
-  unsigned* sync;          // fused apply: [0] generation, [1] CTA exit count,
-                           // [2 + c] generation at which colour-0 chunk c was stored
+  // D4-orbit storage (d4.cuh, reading R9): set on the levels whose element maps are all
+  // D4-invariant (the finest level and its p-coarsened P1 level, symmetric contexts)
+  int orb;                 // 1: the apply streams So / Dco (k_apply_orb)
+  double* So;              // [2][nchunk][NORB][32] orbit values of the element maps
+  double* Dco;             // [nchunk][4][NCS][32] D_e^-1 orbits, colour-1 element order
+  double* Dso;             // [NCS][nedge] D_e^-1 orbits, SoA (edge-parallel kernels)
   // partitioned levels (multi-GPU): local sides 0 bottom, 1 right, 2 top, 3 left
   int dmask;               // sides on the global boundary dOmega (Dirichlet); 15 on one GPU
   int imask;               // sides that are partition interfaces (15 & ~dmask on a rank, or 0)
   int ox, oy, gnx, gny;    // this block's element offset in the global level and the global
                            // level's dims (0, 0, nx, ny on one GPU)
-  int probe;               // measurement probe (MGDTN_PROBE=1: the apply streams S_T only)
-  int l2keep0;             // 1: the colour-0 half of S_T is loaded L2::evict_last (kept
-                           // resident across the solve's colour-0 passes), colour 1 evict_first
-  float l2keep;            // fraction of this level's S_T / Dc stream loaded L2::evict_last
-                           // (kept resident across applies in the 126 MB L2); the rest
-                           // evict_first.  0: all evict_first
 };
 
 // global edge id of local edge e of a level block (power-iteration start vector)
@@ -321,17 +316,10 @@ int launch_apply(const LevelDev& L, int colour, int mode, const double* x, doubl
                  cudaStream_t st);
 int apply_grid(const LevelDev& L);   // blocks of an AM_APPLY colour pass (partials length)
 int apply_grid_mode(const LevelDev& L, int mode);   // blocks of a colour pass in `mode`
-// whole apply (both colours) in ONE launch: colour-1 chunks wait only for the
-// colour-0 chunks they share edges with (per-chunk flags in L.sync), so the
-// two passes overlap instead of being separated by a launch boundary.
-// Falls back to two launch_apply calls when MGDTN_FUSED=0.
+// whole apply: the colour-0 pass (AM_W0) then the colour-1 pass in `mode`
 int launch_apply2(const LevelDev& L, int mode, const double* x, double* y, const double* r,
                   double* d, int step, double* partials, bool pdl, cudaStream_t st);
 int apply2_grid(const LevelDev& L, int mode);  // blocks of launch_apply2 (partials length)
-// one LU-SGS colour sweep of colour gcol from the edge rows only (k_apply.cu); -1 if not
-// applicable (then the colour-masked full apply AM_GSC is used)
-int launch_gs_sweep(const LevelDev& L, int gcol, double* x, double* y, const double* r,
-                    cudaStream_t st);
 
 int launch_local_dtn(const LevelDev& L, const RefDev& R, double h, const double* K,
                      const int8_t* method, const double* tau, DevError* err, cudaStream_t st);
@@ -364,7 +352,10 @@ int launch_recover_ns(const LevelDev& L, const RefDev& R, double h, const double
                       const double* f_qp, double f_const, double* q_out, const double* qex_qp,
                       double* partials, int* grid_out, cudaStream_t st);
 int launch_edge_blocks(const LevelDev& L, DevError* err, cudaStream_t st);
-int launch_dinv_pack(const LevelDev& L, cudaStream_t st);   // Dinv (SoA) -> Dc
+int launch_dinv_pack(const LevelDev& L, cudaStream_t st);   // Dinv (SoA) -> Dc (or Dso / Dco)
+// orbit storage of a D4-invariant level (R9): the packed maps are replaced by their orbit
+// averages (in place) and the orbit values written to So
+int launch_orbit_pack(const LevelDev& L, cudaStream_t st);
 int launch_dense_to_packed(const LevelDev& L, const double* src, cudaStream_t st);
 int launch_packed_to_dense(const LevelDev& L, double* dst, cudaStream_t st);
 int launch_gather_dense(const LevelDev& L, const int64_t* elems, int64_t n, double* dst,
@@ -373,10 +364,6 @@ int launch_gather_dense(const LevelDev& L, const int64_t* elems, int64_t n, doub
 // MG transfer / smoothing kernels
 int launch_smooth_first(const LevelDev& L, const double* r, double* e, double* d,
                         cudaStream_t st);
-// step 3 + the whole h-restriction in one launch (one GPU; bodies.cuh lc_restrict_fused_body)
-int launch_lc_restrict_fused(const LevelDev& F, const LevelDev& C, const double* res, double* e,
-                             const double* KIIinv, const double* Rm, bool do_lc, double* rc,
-                             bool fuse_first, double* ec, double* dc, cudaStream_t st);
 int launch_lc_restrict(const LevelDev& F, const double* res, double* e, const double* KIIinv,
                        const double* Pm, double* cbuf, bool do_lc, bool do_restrict,
                        cudaStream_t st);
@@ -425,12 +412,6 @@ int launch_copy(double* dst, const double* src, int64_t n, cudaStream_t st);
 int launch_zero(double* dst, int64_t n, cudaStream_t st);
 int launch_copy_masked(const LevelDev& L, double* dst, const double* src, cudaStream_t st);
 int launch_add(double* dst, const double* src, int64_t n, cudaStream_t st);
-// PCG updates with the scalar reductions folded in (k_mg.cu, MGDTN_PCG_FUSED)
-int launch_pcg_update_fused(double* x, double* r, const double* p, const double* ap, double* scal,
-                            int64_t n, const double* pap_part, int n_pap, double* partials,
-                            int grid, cudaStream_t st, const LevelDev* L);
-int launch_pcg_pupdate_fused(double* p, const double* z, double* scal, int64_t n,
-                             const double* rz_part, int n_rz, cudaStream_t st);
 int launch_axpy_dev(const double* coef, double sign, const double* x, double* y, int64_t n,
                     cudaStream_t st);   // y += sign * coef[0] * x (device coefficient)
 int launch_scale_rsqrt(const double* ss, double* v, int64_t n, cudaStream_t st);

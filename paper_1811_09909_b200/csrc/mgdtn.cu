@@ -14,6 +14,7 @@
 
 #include "../../include/mgdtn.h"
 #include "comm.h"
+#include "d4.cuh"
 #include "kernels.cuh"
 #include "refelem.h"
 #include "tail.h"
@@ -26,8 +27,8 @@ struct HostLevel {
   LevelDev d{};
   int kind = KIND_COARSEST;
   double h = 0.0;
-  size_t o_sync = 0, o_S = 0, o_Dinv = 0, o_Dc = 0, o_coef = 0, o_lam = 0, o_r = 0, o_e = 0, o_w = 0, o_d = 0;
-  size_t o_pc0 = 0, o_pc1 = 0;   // strip-apply perimeter partials (MGDTN_STRIP)
+  size_t o_S = 0, o_Dinv = 0, o_Dc = 0, o_coef = 0, o_lam = 0, o_r = 0, o_e = 0, o_w = 0, o_d = 0;
+  size_t o_So = 0, o_Dco = 0, o_Dso = 0;   // orbit storage (R9, d4.cuh)
   size_t o_KIIinv = 0, o_Pm = 0, o_Rm = 0, o_cbuf = 0, o_lpart = 0;
   double* lpart = nullptr;   // per-level partial sums + 16 scalars (concurrent power iterations)
   double *KIIinv = nullptr, *Pm = nullptr, *cbuf = nullptr;
@@ -165,8 +166,8 @@ static void init_level(HostLevel& L, int nx, int ny, int p, double h, int kind) 
   d.oy = 0;
   d.gnx = nx;
   d.gny = ny;
-  d.probe = env_or("MGDTN_PROBE", 0);
-  d.l2keep = 0.0f;
+  d.orb = 0;
+  d.So = d.Dco = d.Dso = nullptr;
   d.ndi = 4 * d.k1 * (d.k1 + 1) / 2;
   L.h = h;
   L.kind = kind;
@@ -181,7 +182,7 @@ static void layout(Ctx* c) {
   };
   c->o_err = take(sizeof(DevError));
   c->o_ref = take(c->ref_doubles * sizeof(double));
-  c->npart = 2 * 148 * 8 + 64;
+  c->npart = 4 * 148 * 16 + 64;   // >= any apply / vector grid (at most 16 CTAs per SM)
   c->o_part = take((size_t)c->npart * sizeof(double));
   c->o_scal = take(16 * sizeof(double));
   c->o_sscal = take(16 * sizeof(double));
@@ -198,10 +199,15 @@ static void layout(Ctx* c) {
   c->o_meth = take(c->lev[0].d.ne * sizeof(int8_t));
   for (auto& L : c->lev) {
     const LevelDev& d = L.d;
-    L.o_sync = take((size_t)(2 + d.nchunk + 4) * sizeof(unsigned));   // + 2 ticket pairs
     L.o_S = take((size_t)2 * d.nchunk * d.npk * 32 * sizeof(double));
     L.o_Dinv = take((size_t)d.nedge * d.k1 * d.k1 * sizeof(double));
-    L.o_Dc = take((size_t)d.nchunk * d.ndi * 32 * sizeof(double));
+    if (d.orb) {   // orbit records replace the packed colour-1 D_e^-1 stream
+      L.o_So = take((size_t)2 * d.nchunk * d4_norb(d.p) * 32 * sizeof(double));
+      L.o_Dco = take((size_t)d.nchunk * 4 * d4_ncs(d.p) * 32 * sizeof(double));
+      L.o_Dso = take((size_t)d.nedge * d4_ncs(d.p) * sizeof(double));
+    } else {
+      L.o_Dc = take((size_t)d.nchunk * d.ndi * 32 * sizeof(double));
+    }
     L.o_coef = take(2 * MAX_NU * sizeof(double));
     L.o_lpart = take((size_t)(c->npart + 16) * sizeof(double));
     L.o_lam = take(sizeof(double));
@@ -209,10 +215,6 @@ static void layout(Ctx* c) {
     L.o_e = take(d.ndof * sizeof(double));
     L.o_w = take(d.ndof * sizeof(double));
     L.o_d = take(d.ndof * sizeof(double));
-    if (L.d.strip_r > 0) {
-      L.o_pc0 = take(d.ndof * sizeof(double));
-      L.o_pc1 = take(d.ndof * sizeof(double));
-    }
     if (L.kind == KIND_H) {
       int64_t nmac = (int64_t)(d.nx / 2) * (d.ny / 2);
       L.o_KIIinv = take(nmac * 64 * sizeof(double));
@@ -287,12 +289,15 @@ static void bind_pointers(Ctx* c) {
   c->tauc = D(c->o_tau);
   c->methc = reinterpret_cast<int8_t*>(b + c->o_meth);
   for (auto& L : c->lev) {
-    L.d.sync = reinterpret_cast<unsigned*>(b + L.o_sync);
     L.d.S = D(L.o_S);
     L.d.Dinv = D(L.o_Dinv);
-    L.d.Dc = c->ns ? nullptr : D(L.o_Dc);   // packed-symmetric D_e^-1: symmetric levels only
-    L.d.pc0 = L.d.strip_r > 0 ? D(L.o_pc0) : nullptr;
-    L.d.pc1 = L.d.strip_r > 0 ? D(L.o_pc1) : nullptr;
+    // packed-symmetric D_e^-1 (symmetric packed levels) or the orbit records
+    L.d.Dc = (c->ns || L.d.orb) ? nullptr : D(L.o_Dc);
+    if (L.d.orb) {
+      L.d.So = D(L.o_So);
+      L.d.Dco = D(L.o_Dco);
+      L.d.Dso = D(L.o_Dso);
+    }
     L.d.coef = D(L.o_coef);
     L.lpart = D(L.o_lpart);
     L.lam = D(L.o_lam);
@@ -390,30 +395,6 @@ static void plan_tail_dense(Ctx* c) {
   if (nf <= 0 || nf > 2048) return;
   c->nft = (int)nf;
   c->tail_dense = true;
-}
-
-// L2 residency of the finest operator (B200: 126 MB L2).  Every PCG iteration
-// streams the finest S_T ~5 times; MGDTN_L2KEEP_MB of it can be loaded evict_last
-// so it stays in L2 across applies (the rest streams evict_first).  Off by default:
-// at config 2 (110 MB S_T) 32 / 48 / 64 / 100 MB budgets changed the solve by
-// -1.2 / -0.3 / +2 / +3 % (profiles/r01_l2keep.jsonl).
-static void plan_l2(Ctx* c) {
-  const double budget = (double)env_or("MGDTN_L2KEEP_MB", 0) * 1048576.0;
-  LevelDev& d = c->lev[0].d;
-  const double bytes = (double)d.nchunk * 32 * 8 * (2.0 * d.npk);
-  d.l2keep = budget > 0 ? (float)std::min(1.0, budget / bytes) : 0.0f;
-  // MGDTN_L2HALF_MB: keep the colour-0 halves of the finest levels resident, finest
-  // first, while they fit the budget.  Every colour-0 pass of a level (the W0 pass of
-  // each smoothing step, residual and PCG apply) then re-reads its half from L2.
-  double half_budget = (double)env_or("MGDTN_L2HALF_MB", 0) * 1048576.0;
-  for (auto& L : c->lev) {
-    L.d.l2keep0 = 0;
-    const double half = (double)L.d.nchunk * 32 * 8 * L.d.npk;
-    if (half_budget > 0 && half <= half_budget && !partitioned(c)) {
-      L.d.l2keep0 = 1;
-      half_budget -= half;
-    }
-  }
 }
 
 static void fill_tail(Ctx* c) {
@@ -589,11 +570,7 @@ static inline void smooth_step(Ctx* c, HostLevel& L, int step) {
     // one LU-SGS step: forward block Gauss-Seidel sweep over the
     // four edge colours, then backward (oracle/multigrid.py)
     static const int order[8] = {0, 1, 2, 3, 3, 2, 1, 0};
-    for (int q = 0; q < 8; ++q) {
-      const int n = launch_gs_sweep(L.d, order[q], L.e, L.w, L.r, c->st);
-      if (n >= 0) c->launches += n;
-      else apply_mode(c, L, AM_GSC, L.e, L.w, L.r, nullptr, order[q], nullptr);
-    }
+    for (int q = 0; q < 8; ++q) apply_mode(c, L, AM_GSC, L.e, L.w, L.r, nullptr, order[q], nullptr);
     return;
   }
   // coefficient slot clamped to MAX_NU-1: only block-Jacobi (step-invariant
@@ -623,14 +600,7 @@ static void restrict_level(Ctx* c, int li, const double* res, double* e, bool do
   HostLevel& C = gat ? c->lgl : c->lev[li + 1];
   double* rcl = gat ? c->lgl.r : rc;
   if (gat) fuse = false;
-  // MGDTN_RESTRICT_FUSED=1: step 3 + restriction as one launch (A/B; measured slower at
-  // configs 2 / 4: 7.05 vs 6.81 ms and 162 vs 156 ms solves -- the on-the-fly macro terms
-  // cost more latency per coarse edge than the saved launch)
-  static const bool rfused = env_or("MGDTN_RESTRICT_FUSED", 0) != 0;
-  if (L.kind == KIND_H && !partitioned(c) && rfused) {
-    c->launches += launch_lc_restrict_fused(L.d, C.d, res, e, L.KIIinv, L.Rm, do_lc, rcl, fuse,
-                                            C.e, C.dv, c->st);
-  } else if (L.kind == KIND_H) {
+  if (L.kind == KIND_H) {
     c->launches += launch_lc_restrict(L.d, res, e, L.KIIinv, L.Rm, L.cbuf, do_lc, true, c->st);
     c->launches += launch_restrict_edges(L.d, C.d, res, L.cbuf, rcl, fuse, C.e, C.dv, c->st);
     if (C.d.imask) {
@@ -789,6 +759,9 @@ static int setup_body(Ctx* c) {
   };
   for (int li = 0; li < nlev; ++li) {
     HostLevel& L = c->lev[li];
+    // orbit storage (R9): symmetrise the level's maps and write their orbit records
+    // before anything reads them
+    c->launches += launch_orbit_pack(L.d, st);
     // smoother setup of level li (its operator is complete on st)
     if (li < nlev - 1) RC(smoother_setup(li));
     if (li + 1 >= nlev) break;
@@ -919,24 +892,9 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
 
 // ---------------------------------------------------------------- PCG
 // scal: [0] rz, [1] pAp, [2] rr, [3] alpha, [4] beta, [5] gg
-// MGDTN_PCG_FUSED=1 (one GPU): alpha and beta are reduced inside the update kernels
-static bool pcg_fused(const Ctx* c) {
-  static const bool on = env_or("MGDTN_PCG_FUSED", 0) != 0;
-  return on && !partitioned(c);
-}
-static inline int rz_slot(const Ctx* c) { return pcg_fused(c) ? 6 : 0; }
-
 static void pcg_iter_A(Ctx* c) {  // Ap, alpha, x/r update, rr
   HostLevel& F = c->lev[0];
   const int vg = vec_grid(F.d.ndof);
-  if (pcg_fused(c)) {
-    apply_full(c, F, c->pv, c->ap, c->part);
-    double* rr_part = c->part + 1024;   // disjoint from the pAp partials being read
-    c->launches += launch_pcg_update_fused(c->x, F.r, c->pv, c->ap, c->scal, F.d.ndof, c->part,
-                                           apply_parts(F.d, AM_APPLY), rr_part, vg, c->st, &F.d);
-    reduce_scal(c, rr_part, vg, c->scal, 2, 0);
-    return;
-  }
   apply_full(c, F, c->pv, c->ap, c->part);
   reduce_scal(c, c->part, apply_parts(F.d, AM_APPLY), c->scal, 1, 1);
   c->launches += launch_pcg_update(c->x, F.r, c->pv, c->ap, c->scal, F.d.ndof, c->part, vg, c->st,
@@ -949,10 +907,6 @@ static void pcg_iter_B(Ctx* c) {  // z = B r, beta, p update
   const int vg = vec_grid(F.d.ndof);
   vcycle_level(c, 0, false);
   c->launches += launch_dot(F.r, F.e, F.d.ndof, c->part, vg, c->st, &F.d);
-  if (pcg_fused(c)) {
-    c->launches += launch_pcg_pupdate_fused(c->pv, F.e, c->scal, F.d.ndof, c->part, vg, c->st);
-    return;
-  }
   reduce_scal(c, c->part, vg, c->scal, 0, 2);
   c->launches += launch_pcg_pupdate(c->pv, F.e, c->scal, F.d.ndof, c->st);
 }
@@ -969,7 +923,7 @@ static void pcg_prologue(Ctx* c) {
   reduce_scal(c, c->part, vg, c->scal, 5, 0);
   vcycle_level(c, 0, false);
   c->launches += launch_dot(F.r, F.e, n, c->part, vg, c->st, &F.d);
-  reduce_scal(c, c->part, vg, c->scal, rz_slot(c), 0);
+  reduce_scal(c, c->part, vg, c->scal, 0, 0);
   c->launches += launch_copy(c->pv, F.e, n, c->st);
   pcg_iter_A(c);
   c->launches += launch_pcg_check(c->scal, c->ist, c->dhist, HIST_CAP, c->cond, c->st);
@@ -1084,7 +1038,7 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
   // z = B r ; rz = r.z ; p = z
   vcycle_level(c, 0, false);
   c->launches += launch_dot(F.r, F.e, n, c->part, vg, st, &F.d);
-  reduce_scal(c, c->part, vg, c->scal, rz_slot(c), 0);
+  reduce_scal(c, c->part, vg, c->scal, 0, 0);
   c->launches += launch_copy(c->pv, F.e, n, st);
   CK(cudaGetLastError());
   for (it = 1; it <= maxit; ++it) {
@@ -1526,16 +1480,11 @@ int mg_build_hierarchy_ex(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_level
   }
   plan_tail(c);
   plan_tail_dense(c);
-  plan_l2(c);
-  {   // MGDTN_STRIP=R (2 / 4 / 8): single-pass strip apply on the levels it fits
-    const int R = env_or("MGDTN_STRIP", 0);
-    for (auto& L : c->lev) {
-      LevelDev& d = L.d;
-      d.strip_r = 0;
-      if ((R == 2 || R == 4 || R == 8) && !partitioned(c) && !c->ns && d.nx % 64 == 0 &&
-          d.ny % R == 0 && d.nx >= 128)
-        d.strip_r = R;
-    }
+  // orbit storage (R9, d4.cuh): the finest level and its p-coarsened P1 level hold
+  // D4-invariant element maps (uniform squares, scalar K per element)
+  if (!c->ns) {
+    c->lev[0].d.orb = 1;
+    if (c->lev[0].kind == KIND_P) c->lev[1].d.orb = 1;
   }
   layout(c);   // host only: no CUDA call until mg_bind_workspace
   *out_ctx = c;
@@ -1939,6 +1888,7 @@ int mg_debug_set_element_dtn(void* ctx, int32_t level, const double* src) {
   HostLevel* L = level_of(c, level);
   if (!L) return MG_ERR_ARG;
   c->launches += launch_dense_to_packed(L->d, src, c->st);
+  c->launches += launch_orbit_pack(L->d, c->st);
   CK(cudaGetLastError());
   // the apply kernels prefetch S_T before their dependency wait (PDL): make the
   // new S_T complete before any later launch

@@ -28,7 +28,7 @@ from oracle import assembly, krylov, multigrid  # noqa: E402
 EPS = np.finfo(np.float64).eps
 
 
-def main(idx):
+def main(idx, which=("rhs", "operator")):
     cfg = W.CONFIGS[idx]
     pr = W.make_problem(cfg)
     gold = json.load(open(os.path.join(ROOT, "tests", "golden", f"fullsize_oracle_c{idx}.json")))
@@ -50,7 +50,11 @@ def main(idx):
 
     # (a) rhs at rounding level
     g2 = ts.g * (1.0 + EPS * rng.uniform(-1, 1, ts.g.shape))
-    run("rhs (1 + eps u)", ts.A, g2)
+    if "rhs" in which:
+        run("rhs (1 + eps u)", ts.A, g2)
+    if "operator" not in which:
+        print(json.dumps(out))
+        return
     # (b) symmetric entrywise perturbation of the assembled operator at rounding level
     A = ts.A.tocoo()
     u = rng.uniform(-1, 1, A.nnz)
@@ -65,4 +69,4 @@ def main(idx):
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]))
+    main(int(sys.argv[1]), tuple(sys.argv[2].split(",")) if len(sys.argv) > 2 else ("rhs", "operator"))
