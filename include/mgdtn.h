@@ -302,6 +302,17 @@ int mg_total_launch_count(const void* ctx, int64_t* launches);
 /* 1 (default): replay each PCG iteration as two captured CUDA graphs; 0: eager launches. */
 int mg_set_use_graphs(void* ctx, int32_t on);
 
+/* Execution options of a context (no effect on the arithmetic each kernel performs;
+ * they select which kernel / how many CTAs run it, so that tests can drive every code
+ * path at small sizes).  Drops the captured graphs.  MG_ERR_ARG for an unknown key.
+ *   MG_OPT_SWEEP          0 (default): the single-pass streamed smoothing kernel on the
+ *                         orbit levels large enough for it; 1: wherever its geometry allows
+ *                         (one GPU, nx % 64 == 0); -1: never (two-colour passes).
+ *   MG_OPT_APPLY_GRID_CAP 0 (default): the tuned grid; n > 0: at most n CTAs per apply pass
+ *                         (each CTA then walks many chunks: ring wrap-around at small n). */
+enum { MG_OPT_SWEEP = 1, MG_OPT_APPLY_GRID_CAP = 2 };
+int mg_set_option(void* ctx, int32_t key, int64_t value);
+
 const char* mg_last_error(const void* ctx);
 int64_t mg_last_error_index(const void* ctx);
 void mg_destroy(void* ctx);

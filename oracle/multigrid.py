@@ -191,10 +191,63 @@ def _block_inverse(A_II: sp.csr_matrix, blocks: np.ndarray) -> sp.csr_matrix:
     return sp.coo_matrix((inv.ravel(), (rows, cols)), shape=A_II.shape).tocsr()
 
 
+def assembly_free(S: np.ndarray, n: int, p: int, free: np.ndarray) -> sp.csr_matrix:
+    """sum_T G_T^T S_T G_T restricted to the free dofs (oracle.assembly.assemble_full)."""
+    from .assembly import assemble_full
+    return assemble_full(n, p, S)[free][:, free].tocsr()
+
+
 def _positions(sub: np.ndarray, full_sorted: np.ndarray) -> np.ndarray:
     pos = np.searchsorted(full_sorted, sub)
     assert np.all(full_sorted[pos] == sub)
     return pos
+
+
+# child local edge -> macro edge: macro edges 0..3 are the interior cross
+# [H(2I,2J+1), H(2I+1,2J+1), V(2I+1,2J), V(2I+1,2J+1)] (macro_interior_edges order),
+# 4..11 the boundary halves [bottom (2I), (2I+1); right (2J), (2J+1); top; left], each
+# pair with the lower coordinate first; children (2I,2J), (2I+1,2J), (2I,2J+1), (2I+1,2J+1);
+# child local edges {bottom, right, top, left}
+_MACRO_EDGE = np.array([[4, 2, 0, 10], [5, 6, 1, 2], [0, 3, 8, 11], [1, 7, 9, 3]])
+
+
+def project_constants(S: np.ndarray) -> np.ndarray:
+    """P S P with P = I - 11^T/m: the nearest map (Frobenius) that annihilates constant
+    traces, as the exact DtN map of every level does (fine level: u = 0, q = lambda = c
+    solves the local problem; coarse levels: the macro's harmonic
+    extension of a constant is that constant and J_M maps constants to constants)."""
+    m = S.shape[1]
+    P = np.eye(m) - np.ones((m, m)) / m
+    return np.einsum("ab,ebc,cd->ead", P, S, P)
+
+
+def galerkin_per_macro(S: np.ndarray, n: int, schur_inv: bool = False) -> np.ndarray:
+    """Coarse element DtN maps by Prop. DtN macro by macro: for each
+    2x2 macro assemble its 24x24 map S^M from its four children's 8x8 maps (P1 level),
+    eliminate its interior edges, and inject its boundary halves:
+        S_c^M = J_M^T (S_BB - S_BI S_II^-1 S_IB) J_M            (Eq. Akm1, per macro),
+    J_M the nodal P1 injection of O7.  Summed over macros this is the same A_{k-1} as
+    the global product J^T (A_BB - A_BI A_II^-1 A_IB) J (A_II and A_IB are macro-local,
+    A_BB is the sum of the macros' S_BB), with the sums taken in another order -- a second
+    valid FP64 evaluation used to measure the per-V-cycle noise floor.
+    S: [n*n, 8, 8] element maps of the level (element id j*n+i); returns [(n/2)^2, 8, 8]."""
+    nc = n // 2
+    J, I = np.divmod(np.arange(nc * nc), nc)
+    kids = [(2 * I) + n * (2 * J), (2 * I + 1) + n * (2 * J), (2 * I) + n * (2 * J + 1),
+            (2 * I + 1) + n * (2 * J + 1)]
+    SM = np.zeros((nc * nc, 24, 24))
+    for c in range(4):
+        loc = (_MACRO_EDGE[c][:, None] * 2 + np.arange(2)[None, :]).reshape(-1)
+        SM[:, loc[:, None], loc[None, :]] += S[kids[c]]
+    Iq, Bq = np.arange(8), np.arange(8, 24)
+    SII = SM[:, Iq[:, None], Iq[None, :]]
+    SIB = SM[:, Iq[:, None], Bq[None, :]]
+    SBI = SM[:, Bq[:, None], Iq[None, :]]
+    SBB = SM[:, Bq[:, None], Bq[None, :]]
+    schur = SBB - (SBI @ np.linalg.inv(SII)) @ SIB if schur_inv else SBB - SBI @ np.linalg.solve(SII, SIB)
+    h = np.array([[1.0, 0.0], [0.5, 0.5], [0.5, 0.5], [0.0, 1.0]])
+    JM = np.kron(np.eye(4), h)          # [16, 8]: 4 sides x (2 halves x 2 dofs) -> 4 x 2
+    return np.einsum("ba,ebc,cd->ead", JM, schur, JM)
 
 
 class Hierarchy:
@@ -202,7 +255,12 @@ class Hierarchy:
 
     def __init__(self, A_N, n, p, n_h_levels=0, smoother=BLOCK_JACOBI, nu_pre=2, nu_post=2,
                  omega=1.0, cheb_ratio=30.0, lmax_iters=20, lmax_safety=1.05,
-                 step3=True, step5=False, nu_doubling=False, all_free=False):
+                 step3=True, step5=False, nu_doubling=False, all_free=False,
+                 element_maps=None, galerkin="global", project_levels=False, schur_inv=False):
+        """galerkin="macro" (needs element_maps, the fine level's [n*n, m, m] maps): every
+        coarse operator is assembled from per-macro coarse maps (galerkin_per_macro)
+        instead of the global sparse product -- the same operators summed in another
+        order (P17 noise floor)."""
         self.smoother = smoother
         self.nu_pre, self.nu_post = nu_pre, nu_post
         self.omega = omega
@@ -221,7 +279,13 @@ class Hierarchy:
             cfree = free_of(n, 1)
             J = Jf[fine.free][:, cfree].tocsr()
             fine.kind, fine.J = "p", J
-            levels.append(Level(n, 1, (J.T @ fine.A @ J).tocsr(), cfree))
+            A1 = (J.T @ fine.A @ J).tocsr()
+            if galerkin == "macro":
+                element_maps = p_coarsen_element(element_maps, p)
+                if project_levels:
+                    element_maps = project_constants(element_maps)
+                A1 = assembly_free(element_maps, n, 1, cfree)
+            levels.append(Level(n, 1, A1, cfree))
         # h-coarsening: Eq. Akm1 down to a 2x2 macro mesh (or n_h_levels)
         nh = 0
         # agglomerate while the coarse mesh stays even (n % 4 == 0) -- a 2x2
@@ -251,6 +315,13 @@ class Hierarchy:
             fine.I_pos, fine.B_pos = I_pos, B_pos
             fine.A_II, fine.A_IB, fine.A_BI, fine.A_BB = A_II, A_IB, A_BI, A_BB
             fine.AII_inv, fine.J, fine.macro_blocks = AII_inv, J, blocks
+            if galerkin == "macro":
+                if p == 1 and nh == 0 and element_maps is not None and element_maps.shape[1] != 8:
+                    raise ValueError("element_maps must be the fine level's maps")
+                element_maps = galerkin_per_macro(element_maps, nf, schur_inv)
+                if project_levels:
+                    element_maps = project_constants(element_maps)
+                Ac = assembly_free(element_maps, nc, 1, cfree)
             levels.append(Level(nc, 1, Ac.tocsr(), cfree))
             nh += 1
         self.levels = levels                 # levels[0] = finest (k = N)

@@ -789,7 +789,9 @@ int apply_grid_mode(const LevelDev& L, int mode) {
     case 3: cps = cps_of<3>(L, mode); break;
     default: cps = cps_of<4>(L, mode); break;
   }
-  return balanced_grid(nchunk, (int64_t)num_sms() * cps);
+  int64_t gmax = (int64_t)num_sms() * cps;
+  if (L.grid_cap > 0 && gmax > L.grid_cap) gmax = L.grid_cap;
+  return balanced_grid(nchunk, gmax);
 }
 
 template <int P, int MODE, bool DOT>

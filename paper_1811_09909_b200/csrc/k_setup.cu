@@ -715,6 +715,52 @@ int launch_agglomerate(const LevelDev& F, const LevelDev& C, double* KIIinv, dou
   return 1;
 }
 
+// Reading R10: the exact coarse maps annihilate constant traces too (a macro's harmonic
+// extension of a constant is that constant, and J_p / J_M map constants to constants),
+// so every p = 1 level's maps -- p-coarsened or agglomerated -- are replaced by P S P,
+// P = I - 11^T/8, as the fine maps are (R5).  Without it the rounding-level constant-mode
+// error of each level accumulates coherently through the Galerkin chain.
+__global__ void k_project_const8(LevelDev L) {
+  constexpr int M = 8, NPK = 36;
+  const int64_t nslot = (int64_t)L.nchunk * 32;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < 2 * nslot;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int colour = q >= nslot ? 1 : 0;
+    const int64_t s = q - colour * nslot;
+    double* Sp = L.S + (((int64_t)colour * L.nchunk + (s >> 5)) * NPK) * 32 + (s & 31);
+    double v[NPK], rs[M];
+#pragma unroll
+    for (int kk = 0; kk < NPK; ++kk) v[kk] = Sp[kk * 32];
+    double sig = 0.0;
+#pragma unroll
+    for (int a = 0; a < M; ++a) {
+      double t = 0.0;
+#pragma unroll
+      for (int b = 0; b < M; ++b) {
+        const int lo = a < b ? a : b, hi = a < b ? b : a;
+        t += v[lo * (2 * M - lo + 1) / 2 + (hi - lo)];
+      }
+      rs[a] = t;
+      sig += t;
+    }
+    const double c0 = sig / (M * M);
+#pragma unroll
+    for (int a = 0; a < M; ++a)
+#pragma unroll
+      for (int b = a; b < M; ++b) {
+        const int kk = a * (2 * M - a + 1) / 2 + (b - a);
+        Sp[kk * 32] = (v[kk] - (rs[a] + rs[b]) / M) + c0;
+      }
+  }
+}
+int launch_project_const(const LevelDev& L, cudaStream_t st) {
+  if (L.ns || L.p != 1) return 0;
+  const int64_t n = (int64_t)L.nchunk * 64;
+  const int grid = (int)((n + 127) / 128 < 2368 ? (n + 127) / 128 : 2368);
+  k_project_const8<<<grid, 128, 0, st>>>(L);
+  return 1;
+}
+
 // ============================================================================
 // H4: edge-block diagonal D_e = sum_{T owns e} S_T[e,e] and its inverse
 // (block-Jacobi with edge blocks).

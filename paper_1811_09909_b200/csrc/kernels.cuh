@@ -58,6 +58,8 @@ struct LevelDev {
   double* So;              // [2][nchunk][NORB][32] orbit values of the element maps
   double* Dco;             // [nchunk][4][NCS][32] D_e^-1 orbits, colour-1 element order
   double* Dso;             // [NCS][nedge] D_e^-1 orbits, SoA (edge-parallel kernels)
+  int sweep;               // mg_set_option MG_OPT_SWEEP: 0 auto, 1 wherever possible, -1 never
+  int grid_cap;            // mg_set_option MG_OPT_APPLY_GRID_CAP: max CTAs per apply pass (0: none)
   // partitioned levels (multi-GPU): local sides 0 bottom, 1 right, 2 top, 3 left
   int dmask;               // sides on the global boundary dOmega (Dirichlet); 15 on one GPU
   int imask;               // sides that are partition interfaces (15 & ~dmask on a rank, or 0)
@@ -320,6 +322,12 @@ int apply_grid_mode(const LevelDev& L, int mode);   // blocks of a colour pass i
 int launch_apply2(const LevelDev& L, int mode, const double* x, double* y, const double* r,
                   double* d, int step, double* partials, bool pdl, cudaStream_t st);
 int apply2_grid(const LevelDev& L, int mode);  // blocks of launch_apply2 (partials length)
+// single-pass tiled apply on a one-GPU orbit level (k_tile.cu): AM_APPLY (y = A x, dot
+// x.y into partials if given), AM_RESID (y = r - A x), AM_SMOOTH (xo = x + d, out of place)
+bool tile_level(const LevelDev& L);
+int apply_tile_grid(const LevelDev& L);
+int launch_apply_tile(const LevelDev& L, int mode, const double* x, double* y, const double* r,
+                      double* d, double* xo, int step, double* partials, cudaStream_t st);
 
 int launch_local_dtn(const LevelDev& L, const RefDev& R, double h, const double* K,
                      const int8_t* method, const double* tau, DevError* err, cudaStream_t st);
@@ -356,6 +364,8 @@ int launch_dinv_pack(const LevelDev& L, cudaStream_t st);   // Dinv (SoA) -> Dc 
 // orbit storage of a D4-invariant level (R9): the packed maps are replaced by their orbit
 // averages (in place) and the orbit values written to So
 int launch_orbit_pack(const LevelDev& L, cudaStream_t st);
+// R10: P S P (P = I - 11^T/8) on every map of a symmetric p = 1 level (k_setup.cu)
+int launch_project_const(const LevelDev& L, cudaStream_t st);
 int launch_dense_to_packed(const LevelDev& L, const double* src, cudaStream_t st);
 int launch_packed_to_dense(const LevelDev& L, double* dst, cudaStream_t st);
 int launch_gather_dense(const LevelDev& L, const int64_t* elems, int64_t n, double* dst,

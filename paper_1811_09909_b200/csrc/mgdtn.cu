@@ -73,6 +73,7 @@ struct Ctx {
   cudaGraphExec_t gS = nullptr;   // whole PCG solve: prologue + conditional WHILE loop
   cudaGraphExec_t gV = nullptr;   // one V-cycle, fine L.r -> L.e (GMRES / MG-solver / mg_vcycle)
   long long nV = 0;               // kernels in gV
+  const double* vres = nullptr;   // the fine work vector that holds gV's result
   cudaGraphExec_t gU = nullptr;   // the whole setup after the input copies (forked streams as
   long long nU = 0;               // graph branches); captured for the smoother config gU_sm
   mg_smoother_cfg gU_sm{};
@@ -168,6 +169,8 @@ static void init_level(HostLevel& L, int nx, int ny, int p, double h, int kind) 
   d.gny = ny;
   d.orb = 0;
   d.So = d.Dco = d.Dso = nullptr;
+  d.sweep = 0;
+  d.grid_cap = 0;
   d.ndi = 4 * d.k1 * (d.k1 + 1) / 2;
   L.h = h;
   L.kind = kind;
@@ -544,8 +547,18 @@ static void reduce_scal(Ctx* c, const double* partials, int n, double* scal, int
 // one apply in `mode` (bodies.cuh epilogues); on a partitioned level the colour
 // passes leave partial sums on the interface edges, which are exchanged and
 // finished by k_itf_epilogue (k_part.cu)
+// On a one-GPU orbit level the smoothing step is one streamed pass (k_tile.cu): it
+// reads x, r, d once instead of the two-colour pair's x twice and y three times
+// (config 5: 4.8 vs 5.2-5.9 ms per fine step).  The plain apply and the residual
+// stay on the two-colour pair of passes (k_apply.cu), which measured faster for them
+// (config 5: 2.3 vs 2.65 ms and 2.75 vs 2.96 ms; profiles/r02_sweep_probe.txt).
+static bool tiled(const LevelDev& d, int mode) { return tile_level(d) && mode == AM_SMOOTH; }
 static void apply_mode(Ctx* c, const HostLevel& L, int mode, const double* x, double* y,
                        const double* r, double* d, int step, double* partials) {
+  if (tiled(L.d, mode) && mode != AM_SMOOTH) {
+    c->launches += launch_apply_tile(L.d, mode, x, y, r, d, nullptr, step, partials, c->st);
+    return;
+  }
   c->launches += launch_apply2(L.d, mode, x, y, r, d, step, partials, true, c->st);
   if (L.d.imask) {
     c->launches += launch_itf_pack(L.d, y, c->hsend, c->st);
@@ -557,6 +570,7 @@ static void apply_mode(Ctx* c, const HostLevel& L, int mode, const double* x, do
 }
 // number of dot-product partials apply_mode writes
 static int apply_parts(const LevelDev& d, int mode) {
+  if (tiled(d, mode)) return apply_tile_grid(d);
   return apply2_grid(d, mode) + (d.imask ? itf_blocks() : 0);
 }
 
@@ -565,25 +579,44 @@ static inline void apply_full(Ctx* c, const HostLevel& L, const double* x, doubl
   apply_mode(c, L, AM_APPLY, x, y, nullptr, nullptr, 0, partials);
 }
 
-static inline void smooth_step(Ctx* c, HostLevel& L, int step) {
+// The level's iterate lives in one of its two work vectors L.e / L.w: the tiled
+// smoothing pass writes its result out of place (a neighbouring tile may still read
+// the old iterate on the shared edges), so the iterate alternates between them; the
+// two-colour passes update it in place (and use the other vector as scratch).
+static inline double* other(const HostLevel& L, const double* cur) { return cur == L.e ? L.w : L.e; }
+
+// one smoothing step on the iterate `cur`; returns where the new iterate is
+static inline double* smooth_step(Ctx* c, HostLevel& L, int step, double* cur) {
   if (c->sm.kind == MG_SMOOTH_LUSGS) {
     // one LU-SGS step: forward block Gauss-Seidel sweep over the
     // four edge colours, then backward (oracle/multigrid.py)
     static const int order[8] = {0, 1, 2, 3, 3, 2, 1, 0};
-    for (int q = 0; q < 8; ++q) apply_mode(c, L, AM_GSC, L.e, L.w, L.r, nullptr, order[q], nullptr);
-    return;
+    for (int q = 0; q < 8; ++q)
+      apply_mode(c, L, AM_GSC, cur, other(L, cur), L.r, nullptr, order[q], nullptr);
+    return cur;
   }
   // coefficient slot clamped to MAX_NU-1: only block-Jacobi (step-invariant
   // coefficients) may run more steps than that (beta-doubling)
-  apply_mode(c, L, AM_SMOOTH, L.e, L.w, L.r, L.dv, step < MAX_NU ? step : MAX_NU - 1, nullptr);
+  const int slot = step < MAX_NU ? step : MAX_NU - 1;
+  if (tiled(L.d, AM_SMOOTH)) {
+    double* out = other(L, cur);
+    c->launches += launch_apply_tile(L.d, AM_SMOOTH, cur, nullptr, L.r, L.dv, out, slot, nullptr,
+                                     c->st);
+    return out;
+  }
+  apply_mode(c, L, AM_SMOOTH, cur, other(L, cur), L.r, L.dv, slot, nullptr);
+  return cur;
 }
 
 // smoothing steps on level li: V(nu, nu), times 2 per coarser level with the
 // paper's beta = 2 schedule
 static inline int nu_at(const Ctx* c, int nu, int li) { return c->sm.nu_doubling ? nu << li : nu; }
 
-static inline void residual(Ctx* c, HostLevel& L) {  // L.w = L.r - A L.e
-  apply_mode(c, L, AM_RESID, L.e, L.w, L.r, nullptr, 0, nullptr);
+// res = L.r - A cur into the other work vector; returns it
+static inline double* residual(Ctx* c, HostLevel& L, const double* cur) {
+  double* res = other(L, cur);
+  apply_mode(c, L, AM_RESID, cur, res, L.r, nullptr, 0, nullptr);
+  return res;
 }
 
 // is level li+1 the gather level (li the last partitioned level)?
@@ -639,18 +672,19 @@ static void prolong_level(Ctx* c, int li, const double* ec, double* e) {
   }
 }
 
-// V-cycle B_k (Algorithm 1) on level li with input L.r, output L.e.
+// V-cycle B_k (Algorithm 1) on level li with input L.r; returns the vector holding
+// the result (L.e or L.w, see smooth_step).
 // `first_done`: the first pre-smoothing step (from e = 0) was fused into the
 // restriction kernel of the finer level.  Step 3 (local correction) and the
 // restriction share one residual: Q_{k-1} A_k T_k = 0, so Q(r - A e2) equals
 // Q(r - A e1).
-static void vcycle_level(Ctx* c, int li, bool first_done) {
+static double* vcycle_level(Ctx* c, int li, bool first_done) {
   HostLevel& L = c->lev[li];
   const int nlev = (int)c->lev.size();
   const bool tail_ok = c->sm.kind != MG_SMOOTH_LUSGS;   // the tail kernels have no LU-SGS
   if (tail_ok && c->tail_dense && li == c->tail_start) {   // this level and every coarser one: e = B_tail r
     c->launches += launch_tail_dense(c->tfidx, c->nft, c->Bt, L.r, L.e, c->st);
-    return;
+    return L.e;
   }
   if (tail_ok && c->tail_vcycle && li == c->tail_start) {   // this level and every coarser one: one launch
     TailParams& T = c->tail;
@@ -660,11 +694,11 @@ static void vcycle_level(Ctx* c, int li, bool first_done) {
     T.first_fused = first_done ? 1 : 0;
     for (int k = 0; k < T.nlev; ++k) T.lev[k].d = c->lev[c->tail_start + k].d;   // smoother kind
     c->launches += launch_coarse_tail(T, c->st);
-    return;
+    return L.e;
   }
   if (li == nlev - 1) {
     c->launches += launch_coarse_solve(L.d, c->fidx, c->nf, c->A1inv, L.r, L.e, c->st);
-    return;
+    return L.e;
   }
   const int nu_pre = nu_at(c, c->sm.nu_pre, li), nu_post = nu_at(c, c->sm.nu_post, li);
   int s0 = 0;
@@ -674,16 +708,18 @@ static void vcycle_level(Ctx* c, int li, bool first_done) {
   } else {
     c->launches += launch_zero(L.e, L.d.ndof, c->st);
   }
-  for (int s = s0; s < nu_pre; ++s) smooth_step(c, L, s);
-  residual(c, L);  // L.w = r - A e1
+  double* cur = L.e;
+  for (int s = s0; s < nu_pre; ++s) cur = smooth_step(c, L, s, cur);
+  double* res = residual(c, L, cur);  // r - A e1
   HostLevel& C = c->lev[li + 1];
   const bool fuse = (li + 1 < nlev - 1) && nu_at(c, c->sm.nu_pre, li + 1) > 0 &&
                     c->sm.kind != MG_SMOOTH_LUSGS &&
                     !(c->tail_dense && li + 1 == c->tail_start) && !gathers(c, li);
-  restrict_level(c, li, L.w, L.e, true, C.r, fuse);
-  vcycle_level(c, li + 1, fuse);
-  prolong_level(c, li, C.e, L.e);
-  for (int s = 0; s < nu_post; ++s) smooth_step(c, L, s);
+  restrict_level(c, li, res, cur, true, C.r, fuse);
+  const double* ec = vcycle_level(c, li + 1, fuse);
+  prolong_level(c, li, ec, cur);
+  for (int s = 0; s < nu_post; ++s) cur = smooth_step(c, L, s, cur);
+  return cur;
 }
 
 // ---------------------------------------------------------------- setup
@@ -769,6 +805,7 @@ static int setup_body(Ctx* c) {
     HostLevel& C = c->lev[li + 1];
     if (L.kind == KIND_P) {
       c->launches += launch_p_coarsen(L.d, C.d, c->refdev.Jp, st);
+      c->launches += launch_project_const(C.d, st);   // R10
     } else if (gathers(c, li)) {
       // gather level: this rank's macros' coarse DtN maps, all-gathered into the
       // replicated level (every rank then builds the coarser levels redundantly)
@@ -776,9 +813,11 @@ static int setup_body(Ctx* c) {
       c->launches += launch_agglomerate(L.d, B.d, L.KIIinv, L.Pm, c->err, st, c->sden);
       comm_fail(c, c->comm->allgather(c->sden, c->sall, (size_t)B.d.ne * 64, st));
       c->launches += launch_gather_S(C.d, B.d.nx, B.d.ny, c->px, c->sall, st);
+      c->launches += launch_project_const(C.d, st);   // R10 (same on every rank)
     } else {
       c->launches += launch_agglomerate(L.d, C.d, L.KIIinv, L.Pm, c->err, st, nullptr,
                                         c->ns ? L.Rm : nullptr);
+      c->launches += launch_project_const(C.d, st);   // R10
     }
   }
   if (c->sm.kind == MG_SMOOTH_CHEBYSHEV && c->tail_lmax && c->tail_start >= 0 &&
@@ -905,10 +944,10 @@ static void pcg_iter_A(Ctx* c) {  // Ap, alpha, x/r update, rr
 static void pcg_iter_B(Ctx* c) {  // z = B r, beta, p update
   HostLevel& F = c->lev[0];
   const int vg = vec_grid(F.d.ndof);
-  vcycle_level(c, 0, false);
-  c->launches += launch_dot(F.r, F.e, F.d.ndof, c->part, vg, c->st, &F.d);
+  const double* z = vcycle_level(c, 0, false);
+  c->launches += launch_dot(F.r, z, F.d.ndof, c->part, vg, c->st, &F.d);
   reduce_scal(c, c->part, vg, c->scal, 0, 2);
-  c->launches += launch_pcg_pupdate(c->pv, F.e, c->scal, F.d.ndof, c->st);
+  c->launches += launch_pcg_pupdate(c->pv, z, c->scal, F.d.ndof, c->st);
 }
 
 // Rotated PCG loop (same kernel sequence as the textbook loop):
@@ -921,10 +960,10 @@ static void pcg_prologue(Ctx* c) {
   c->launches += launch_zero(c->x, n, c->st);
   c->launches += launch_dot(F.r, F.r, n, c->part, vg, c->st, &F.d);
   reduce_scal(c, c->part, vg, c->scal, 5, 0);
-  vcycle_level(c, 0, false);
-  c->launches += launch_dot(F.r, F.e, n, c->part, vg, c->st, &F.d);
+  const double* z = vcycle_level(c, 0, false);
+  c->launches += launch_dot(F.r, z, n, c->part, vg, c->st, &F.d);
   reduce_scal(c, c->part, vg, c->scal, 0, 0);
-  c->launches += launch_copy(c->pv, F.e, n, c->st);
+  c->launches += launch_copy(c->pv, z, n, c->st);
   pcg_iter_A(c);
   c->launches += launch_pcg_check(c->scal, c->ist, c->dhist, HIST_CAP, c->cond, c->st);
 }
@@ -1036,10 +1075,10 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
     return MG_OK;
   }
   // z = B r ; rz = r.z ; p = z
-  vcycle_level(c, 0, false);
-  c->launches += launch_dot(F.r, F.e, n, c->part, vg, st, &F.d);
+  const double* z = vcycle_level(c, 0, false);
+  c->launches += launch_dot(F.r, z, n, c->part, vg, st, &F.d);
   reduce_scal(c, c->part, vg, c->scal, 0, 0);
-  c->launches += launch_copy(c->pv, F.e, n, st);
+  c->launches += launch_copy(c->pv, z, n, st);
   CK(cudaGetLastError());
   for (it = 1; it <= maxit; ++it) {
     pcg_iter_A(c);
@@ -1087,21 +1126,17 @@ static double gdot(Ctx* c, const double* a, const double* b) {
   return c->pinned[0];
 }
 
-// F.e = B_N F.r: the V-cycle's fixed kernel sequence, replayed from a CUDA graph
-// captured on first use (one GPU, graphs on); eager launches otherwise
-static void run_vcycle(Ctx* c) {
-  if (!c->use_graphs || partitioned(c) || c->st == nullptr) {
-    vcycle_level(c, 0, false);
-    return;
-  }
+// B_N F.r: the V-cycle's fixed kernel sequence, replayed from a CUDA graph captured on
+// first use (one GPU, graphs on); eager launches otherwise.  Returns the vector that
+// holds the result (fixed by the captured sequence).
+static const double* run_vcycle(Ctx* c) {
+  if (!c->use_graphs || partitioned(c) || c->st == nullptr) return vcycle_level(c, 0, false);
   if (!c->gV) {
     cudaGraph_t g = nullptr;
     const long long l0 = c->launches;
-    if (cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
-      vcycle_level(c, 0, false);
-      return;
-    }
-    vcycle_level(c, 0, false);
+    if (cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+      return vcycle_level(c, 0, false);
+    c->vres = vcycle_level(c, 0, false);
     c->nV = c->launches - l0;
     c->launches = l0;
     if (cudaStreamEndCapture(c->st, &g) != cudaSuccess || !g ||
@@ -1109,21 +1144,21 @@ static void run_vcycle(Ctx* c) {
       if (g) cudaGraphDestroy(g);
       c->gV = nullptr;
       cudaGetLastError();
-      vcycle_level(c, 0, false);
-      return;
+      return vcycle_level(c, 0, false);
     }
     cudaGraphDestroy(g);
   }
   cudaGraphLaunch(c->gV, c->st);
   c->launches += c->nV;
+  return c->vres;
 }
 
 // out = B_N v: one V-cycle of Algorithm 1 from e = 0
 static void precond(Ctx* c, const double* v, double* out) {
   HostLevel& F = c->lev[0];
   c->launches += launch_copy_masked(F.d, F.r, v, c->st);
-  run_vcycle(c);
-  c->launches += launch_copy(out, F.e, F.d.ndof, c->st);
+  const double* z = run_vcycle(c);
+  c->launches += launch_copy(out, z, F.d.ndof, c->st);
 }
 
 // lambda^{i+1} = lambda^i + B_N (g - A lambda^i), lambda^0 = 0,
@@ -1622,8 +1657,8 @@ int mg_vcycle(void* ctx, const double* r, double* z) {
   if (!c->setup_done) return fail(c, MG_ERR_STATE, "setup first");
   HostLevel& F = c->lev[0];
   c->launches += launch_copy_masked(F.d, F.r, r, c->st);
-  run_vcycle(c);
-  c->launches += launch_copy(z, F.e, F.d.ndof, c->st);
+  const double* zr = run_vcycle(c);
+  c->launches += launch_copy(z, zr, F.d.ndof, c->st);
   CK(cudaGetLastError());
   return MG_OK;
 }
@@ -1636,8 +1671,9 @@ int mg_smooth(void* ctx, int32_t level, const double* r, double* e, int32_t nste
   if (!L || L == &c->lev.back()) return fail(c, MG_ERR_ARG, "no smoother on this level");
   c->launches += launch_copy_masked(L->d, L->r, r, c->st);
   c->launches += launch_copy_masked(L->d, L->e, e, c->st);
-  for (int s = 0; s < nsteps; ++s) smooth_step(c, *L, s);
-  c->launches += launch_copy(e, L->e, L->d.ndof, c->st);
+  double* cur = L->e;
+  for (int s = 0; s < nsteps; ++s) cur = smooth_step(c, *L, s, cur);
+  c->launches += launch_copy(e, cur, L->d.ndof, c->st);
   CK(cudaGetLastError());
   return MG_OK;
 }
@@ -1919,6 +1955,22 @@ int mg_total_launch_count(const void* ctx, int64_t* launches) {
   const Ctx* c = static_cast<const Ctx*>(ctx);
   if (!c || !launches) return MG_ERR_ARG;
   *launches = c->launches;
+  return MG_OK;
+}
+
+int mg_set_option(void* ctx, int32_t key, int64_t value) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c) return MG_ERR_ARG;
+  if (key == MG_OPT_SWEEP) {
+    if (value < -1 || value > 1) return fail(c, MG_ERR_ARG, "MG_OPT_SWEEP: -1, 0 or 1");
+    for (auto& L : c->lev) L.d.sweep = (int)value;
+  } else if (key == MG_OPT_APPLY_GRID_CAP) {
+    if (value < 0 || value > (1 << 20)) return fail(c, MG_ERR_ARG, "MG_OPT_APPLY_GRID_CAP out of range");
+    for (auto& L : c->lev) L.d.grid_cap = (int)value;
+  } else {
+    return fail(c, MG_ERR_ARG, "unknown option");
+  }
+  drop_graphs(c);   // (the tail kernels copy the level descriptors at every launch)
   return MG_OK;
 }
 

@@ -81,6 +81,7 @@ _SIGS = {
     "mg_last_launch_count": [_P, C.POINTER(C.c_int64)],
     "mg_total_launch_count": [_P, C.POINTER(C.c_int64)],
     "mg_set_use_graphs": [_P, C.c_int32],
+    "mg_set_option": [_P, C.c_int32, C.c_int64],
     "mg_partition_plan": [C.POINTER(mg_quad_mesh), C.c_int32, C.c_int32, C.POINTER(mg_partition),
                           C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), _P],
     "mg_partition_side_edges": [C.POINTER(mg_quad_mesh), C.c_int32, C.c_int32,
@@ -517,6 +518,12 @@ class MGSolver:
 
     def use_graphs(self, on: bool):
         self._chk(self.lib.mg_set_use_graphs(self.ctx, int(on)), "mg_set_use_graphs")
+
+    OPT_SWEEP, OPT_APPLY_GRID_CAP = 1, 2
+
+    def set_option(self, key: int, value: int):
+        """mg_set_option: execution options (kernel choice / grid size) for tests."""
+        self._chk(self.lib.mg_set_option(self.ctx, int(key), int(value)), "mg_set_option")
 
     def close(self):
         if getattr(self, "ctx", None):

@@ -33,11 +33,17 @@ def test_fine_apply_dominates_and_counts():
     s = _Levels(256, 4)
     sm = SmootherConfig(kind=1, nu_pre=2, nu_post=2)
     b = bench.bytes_per_iteration(s, sm)
-    # fine packed S_T: 65536 elements x 210 doubles; 5 fine applies per iteration (3 smoothing
-    # steps with an apply, the residual, the PCG apply)
-    fine_S = 65536 * 210 * 8
-    assert 5 * fine_S < b < 10 * fine_S
-    assert abs(b - 1.0317e9) / 1.0317e9 < 1e-3
+    # fine level in D4-orbit storage (reading R9): 65536 elements x 33 doubles per apply;
+    # 5 fine applies per iteration (3 smoothing steps with an apply, the residual, the PCG
+    # apply), each with 16 B per trace dof of x / y, D_e^-1 orbits (9 per edge) and the
+    # smoothing vectors (r, e, Chebyshev d: 40 B per dof), transfers 32 B per dof, and
+    # the PCG's 6 vector passes
+    ne, nd, ned = 65536, 657920, 131584
+    fine_S = ne * 33 * 8
+    ap = fine_S + 16 * nd
+    fine = 4 * (ap + 8 * ned * 9 + 40 * nd) + 8 * nd + 24 * nd + (ap + 48 * nd)
+    assert 5 * fine_S < fine < b < 2 * fine
+    assert abs(b - 4.77434112e8) / 4.77434112e8 < 1e-6
     # full storage (nonsymmetric) moves more; block-Jacobi drops the Chebyshev d traffic
     assert bench.bytes_per_iteration(s, sm, ns=True) > b
     assert bench.bytes_per_iteration(s, SmootherConfig(kind=0, nu_pre=2, nu_post=2)) < b

@@ -33,7 +33,8 @@ def rel(a, b):
 class Case:
     """One problem set up identically on both sides."""
 
-    def __init__(self, cfg_index, n, p=None, smoother=None, nu=None):
+    def __init__(self, cfg_index, n, p=None, smoother=None, nu=None, proj=False):
+        from oracle_proj import project_maps
         from paper_1811_09909_b200 import MGSolver, SmootherConfig
         c = W.scaled_config(cfg_index, n) if W.CONFIGS[cfg_index].n != n else W.CONFIGS[cfg_index]
         if p is not None:
@@ -46,7 +47,19 @@ class Case:
         pr = W.make_problem(c)
         self.pr = pr
         self.ts = assembly.TraceSystem(c.n, c.p, pr.K, pr.method, pr.tau, pr.f_qp, pr.f_const, pr.gD_qp)
-        self.H = multigrid.Hierarchy(self.ts.A, c.n, c.p, smoother=c.smoother, nu_pre=c.nu, nu_post=c.nu)
+        self.proj = proj
+        if proj:   # the oracle on its maps projected by readings R5 / R9 (tests/oracle_proj.py)
+            ts = self.ts
+            ts.S = project_maps(ts.S, c.p)
+            ts.A_full = assembly.assemble_full(c.n, c.p, ts.S)
+            ts.A = ts.A_full[ts.free][:, ts.free].tocsr()
+            g_full = assembly.assemble_vector(c.n, c.p, ts.b)
+            ts.g = g_full[ts.free] - ts.A_full[ts.free][:, ts.dir] @ ts.lam_D[ts.dir]
+        # proj: readings R5 / R9 on the fine maps and R10 (constants annihilated) on every
+        # coarse level's maps, built macro by macro (Prop. DtN) as the GPU builds them
+        extra = dict(element_maps=self.ts.S, galerkin="macro", project_levels=True) if proj else {}
+        self.H = multigrid.Hierarchy(self.ts.A, c.n, c.p, smoother=c.smoother, nu_pre=c.nu,
+                                     nu_post=c.nu, **extra)
         self.gpu = MGSolver(c.n, p=c.p)
         self.sm = SmootherConfig(kind=c.smoother, nu_pre=c.nu, nu_post=c.nu)
         self.gpu.setup(pr.K, pr.method, pr.tau, self.sm)
@@ -63,12 +76,23 @@ class Case:
         return self.olev(level).free
 
 
-CASES = [(1, 8), (2, 16), (3, 16), (4, 16), (5, 16), (2, 64), (3, 64), (4, 64)]
+# (config, n, compare against the projected oracle): up to n = 64 against the oracle
+# as it stands; from n = 128 on (and the config-5 recipe at 64), the oracle's
+# constant-mode rounding, accumulated coherently through its Galerkin chain, moves a
+# V-cycle by more than the gate (2e-11 at config 2, n = 128: DESIGN.md 2b), so there the
+# reference is the oracle under the same readings as the GPU -- R5 / R9 on the fine maps
+# (tests/oracle_proj.py) and R10 on every coarse level (oracle/multigrid.py,
+# galerkin="macro", project_levels=True), whose two evaluation orders agree to ~5e-15
+CASES = [(1, 8, False), (2, 16, False), (3, 16, False), (4, 16, False), (5, 16, False),
+         (2, 64, False), (3, 64, False), (4, 64, False), (5, 64, False), (5, 64, True),
+         (2, 128, True), (5, 128, True), (2, 256, True)]
 
 
-@pytest.fixture(scope="module", params=CASES, ids=[f"c{a}n{b}" for a, b in CASES])
+@pytest.fixture(scope="module", params=CASES,
+                ids=[f"c{a}n{b}" + ("proj" if c else "") for a, b, c in CASES])
 def case(request):
-    return Case(*request.param)
+    a, b, c = request.param
+    return Case(a, b, proj=c)
 
 
 def test_element_dtn_parity(case):
@@ -151,6 +175,48 @@ def test_vcycle_parity(case):
     assert np.all(z[bd] == 0.0)
 
 
+EXEC_PATHS = [("sweep", 1, 1), ("grid_cap", 2, 1), ("grid_cap", 2, 3)]
+
+
+@pytest.mark.parametrize("path", EXEC_PATHS, ids=[f"{a}{c}" for a, _, c in EXEC_PATHS])
+def test_exec_paths_parity(case, path):
+    """The same operators through the other kernel paths (mg_set_option): the
+    single-pass streamed smoothing kernel forced onto the small orbit levels
+    (MG_OPT_SWEEP = 1, nx % 64 == 0), and apply grids capped at 1 or 3 CTAs, so every
+    CTA walks many chunks and the TMA / segment rings wrap around (MG_OPT_APPLY_GRID_CAP)."""
+    name, key, val = path
+    if name == "sweep" and case.cfg.n % 64:
+        pytest.skip("the streamed kernel needs nx % 64 == 0")
+    if case.cfg.n > 128:
+        pytest.skip("exec-path sweep at n <= 128")
+    gpu = case.gpu
+    gpu.set_option(key, val)
+    try:
+        for level in range(case.N, 0, -1):
+            L = case.olev(level)
+            x = case.vec(level, case.cfg.seed_vec + level)
+            y = gpu.apply(level, torch.from_numpy(x)).cpu().numpy()
+            assert rel(y[L.free], L.A @ x[L.free]) <= TOL_OP, (level, "apply")
+            if level > 1:
+                r = case.vec(level, 100 + level)
+                e0 = case.vec(level, 200 + level)
+                for steps in (1, 2, 3):
+                    e = gpu.smooth(level, torch.from_numpy(r), torch.from_numpy(e0), steps).cpu().numpy()
+                    eo = case.H.smooth(case.N - level, e0[L.free], r[L.free], steps)
+                    assert rel(e[L.free], eo) <= TOL_OP, (level, steps, "smooth")
+        r = case.vec(case.N, 600)
+        z = gpu.vcycle(torch.from_numpy(r)).cpu().numpy()
+        assert rel(z[case.ts.free], case.H.vcycle(r[case.ts.free])) <= TOL_OP
+        pr = case.pr
+        g, lam_bc = gpu.assemble_rhs(pr.f_qp, pr.f_const, pr.gD_qp)
+        lam, info = gpu.pcg_solve(g, rtol=case.cfg.rtol, maxit=2000)
+        res = krylov.pcg(case.ts.A, case.H.vcycle, case.ts.g, rtol=case.cfg.rtol, maxit=2000)
+        assert abs(info["iters"] - res["iters"]) <= 1
+        assert rel((lam + lam_bc).cpu().numpy(), case.ts.to_full(res["x"])) <= TOL_SOL
+    finally:
+        gpu.set_option(key, 0)
+
+
 def test_rhs_parity(case):
     pr = case.pr
     g, lam_bc = case.gpu.assemble_rhs(pr.f_qp, pr.f_const, pr.gD_qp)
@@ -175,8 +241,16 @@ def test_pcg_parity(case):
     # drift of the recursive residual (the stopping test, reading Q16) that the oracle's
     # own PCG shows at this conditioning (c3n64: oracle 2.75e-10 at rtol 1e-10)
     fr = case.ts.free
-    true_rel = np.linalg.norm(case.ts.g - case.ts.A @ lam.cpu().numpy()[fr]) / np.linalg.norm(case.ts.g)
-    assert true_rel <= max(3 * case.cfg.rtol, 2 * res["true_relres"]), (true_rel, res["true_relres"])
+    lf = lam.cpu().numpy()[fr]
+    true_rel = np.linalg.norm(case.ts.g - case.ts.A @ lf) / np.linalg.norm(case.ts.g)
+    # finite-precision CG: ||g - A x_k - r_k|| <= eps O(k) ||A|| max_j ||x_j|| (Greenbaum,
+    # "Iterative methods for solving linear systems", ch. 7.3), ||A||_2 <= ||A||_1 (symmetric)
+    import scipy.sparse.linalg as spla
+    m = 4 * (case.cfg.p + 1)
+    gap = info["iters"] * np.finfo(float).eps * 4 * m * spla.norm(case.ts.A, 1) * \
+        np.linalg.norm(lf) / np.linalg.norm(case.ts.g)
+    assert true_rel <= max(3 * case.cfg.rtol, 2 * res["true_relres"], case.cfg.rtol + gap), \
+        (true_rel, res["true_relres"], gap)
 
 
 def test_pcg_eager_equals_graph_replay(case):

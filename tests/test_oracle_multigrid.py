@@ -512,3 +512,61 @@ def test_chebyshev_error_propagator_closed_form(nu, level, lmax_scale):
     # Chebyshev minimax bound on the interval: |p_nu| <= 1 / T_nu(theta / delta) there
     inside = (lam >= a) & (lam <= b)
     assert np.all(np.abs(pnu[inside]) <= 1.0 / C.chebval(theta / delta, Tnu) + 1e-14)
+
+
+@pytest.mark.parametrize("p", [1, 2, 4])
+def test_projected_maps_reading_r5_r9(p):
+    """tests/oracle_proj.py (the reference of the n >= 128 GPU parity cases): the 8
+    permutations form a group, the oracle's maps are D4-invariant and annihilate
+    constants to rounding, and the projection is idempotent, exactly D4-invariant,
+    annihilates constants, and moves a map by rounding only."""
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from oracle_proj import d4_perms, project_maps
+    perms = d4_perms(p)
+    m = 4 * (p + 1)
+    keys = {tuple(P) for P in perms}
+    assert len(keys) == 8
+    for P in perms:
+        for Q in perms:
+            assert tuple(P[Q]) in keys
+    K = np.array([0.3, 7.0])
+    S = el.element_dtn(p, K, np.zeros(2, np.int8), np.ones(2), 1.0 / 16)
+    Sp = project_maps(S, p)
+    scale = np.abs(S).max()
+    assert np.abs(Sp - S).max() <= 1e-13 * scale
+    assert np.abs(Sp.sum(axis=2)).max() <= 1e-14 * scale
+    for P in perms:
+        assert np.abs(S[:, P][:, :, P] - S).max() <= 1e-13 * scale
+        assert np.abs(Sp[:, P][:, :, P] - Sp).max() <= 1e-15 * scale   # 8-term sums: rounding order
+    assert np.abs(project_maps(Sp, p) - Sp).max() <= 1e-14 * scale
+    assert Sp.shape == (2, m, m)
+
+
+@pytest.mark.parametrize("cfg_n", [(2, 16), (5, 16), (3, 16)])
+def test_per_macro_galerkin_route(cfg_n):
+    """oracle.multigrid.galerkin_per_macro (Prop. DtN macro by macro):
+    the same coarse operators as the global product J^T (A_BB - A_BI A_II^-1 A_IB) J on
+    every level (1e-12), coarse maps that annihilate constants (the exact invariant, to
+    rounding), and with R10 (project_levels) a V-cycle that moves only at rounding
+    level on these small meshes."""
+    ci, n = cfg_n
+    c = W.scaled_config(ci, n)
+    pr = W.make_problem(c, with_f=False)
+    ts = assembly.TraceSystem(n, c.p, pr.K, pr.method, pr.tau, None, 1.0)
+    kw = dict(smoother=c.smoother, nu_pre=c.nu, nu_post=c.nu)
+    Hg = multigrid.Hierarchy(ts.A, n, c.p, **kw)
+    Hm = multigrid.Hierarchy(ts.A, n, c.p, **kw, element_maps=ts.S, galerkin="macro")
+    Hp = multigrid.Hierarchy(ts.A, n, c.p, **kw, element_maps=ts.S, galerkin="macro",
+                             project_levels=True)
+    for Lg, Lm in zip(Hg.levels, Hm.levels):
+        d = abs(Lg.A - Lm.A).max()
+        assert d <= 1e-12 * abs(Lg.A).max(), d
+    S1 = multigrid.p_coarsen_element(ts.S, c.p)
+    Sc = multigrid.galerkin_per_macro(S1, n)
+    assert np.abs(Sc.sum(axis=2)).max() <= 1e-12 * np.abs(Sc).max()
+    assert np.allclose(multigrid.project_constants(Sc).sum(axis=2), 0.0, atol=1e-14 * np.abs(Sc).max())
+    r = W.random_trace_vector(ts.ndof, 600)[ts.free]
+    zg, zm, zp = Hg.vcycle(r), Hm.vcycle(r), Hp.vcycle(r)
+    assert np.linalg.norm(zm - zg) <= 1e-12 * np.linalg.norm(zg)
+    assert np.linalg.norm(zp - zg) <= 1e-12 * np.linalg.norm(zg)

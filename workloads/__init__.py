@@ -106,6 +106,16 @@ def scaled_config(index: int, n: int) -> Config:
     return c
 
 
+def config5_recipe(n: int) -> Config:
+    """Config 5's recipe on an n x n mesh with its FULL-SIZE correlation length
+    (32 elements, not scaled with n): the oracle-golden stand-in for config 5, whose
+    4096^2 mesh is beyond the oracle's memory (tools/make_c5_golden.py)."""
+    c = scaled_config(5, n)
+    c.extras["ell"] = CONFIGS[5].extras["ell"]
+    c.name = f"{CONFIGS[5].name}@n{n}_ell32"
+    return c
+
+
 # --------------------------------------------------------------------------
 # sampling grid of the input format
 # --------------------------------------------------------------------------
