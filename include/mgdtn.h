@@ -309,8 +309,11 @@ int mg_set_use_graphs(void* ctx, int32_t on);
  *                         orbit levels large enough for it; 1: wherever its geometry allows
  *                         (one GPU, nx % 64 == 0); -1: never (two-colour passes).
  *   MG_OPT_APPLY_GRID_CAP 0 (default): the tuned grid; n > 0: at most n CTAs per apply pass
- *                         (each CTA then walks many chunks: ring wrap-around at small n). */
-enum { MG_OPT_SWEEP = 1, MG_OPT_APPLY_GRID_CAP = 2 };
+ *                         (each CTA then walks many chunks: ring wrap-around at small n).
+ *   MG_OPT_COMM_TIMEOUT_MS partitioned contexts: every host wait polls NCCL's asynchronous
+ *                         error state and gives up after this many ms (default 300000),
+ *                         aborting the communicator and returning MG_ERR_NCCL. */
+enum { MG_OPT_SWEEP = 1, MG_OPT_APPLY_GRID_CAP = 2, MG_OPT_COMM_TIMEOUT_MS = 3 };
 int mg_set_option(void* ctx, int32_t key, int64_t value);
 
 const char* mg_last_error(const void* ctx);

@@ -3,8 +3,10 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <condition_variable>
 #include <cstring>
+#include <thread>
 #include <mutex>
 #include <vector>
 
@@ -26,6 +28,8 @@ struct NcclApi {
   decltype(&ncclAllReduce) allReduce = nullptr;
   decltype(&ncclAllGather) allGather = nullptr;
   decltype(&ncclGetErrorString) errStr = nullptr;
+  decltype(&ncclCommGetAsyncError) asyncError = nullptr;   // optional
+  decltype(&ncclCommAbort) abort = nullptr;                // optional
 };
 
 NcclApi& nccl_api() {
@@ -48,6 +52,8 @@ NcclApi& nccl_api() {
   LOAD(allReduce, "ncclAllReduce");
   LOAD(allGather, "ncclAllGather");
   LOAD(errStr, "ncclGetErrorString");
+  LOAD(asyncError, "ncclCommGetAsyncError");
+  LOAD(abort, "ncclCommAbort");
 #undef LOAD
   api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.groupStart &&
            api.groupEnd && api.send && api.recv && api.allReduce && api.allGather && api.errStr;
@@ -88,6 +94,45 @@ struct NcclComm : Comm {
   }
   int allgather(const double* send, double* recv, size_t cnt, cudaStream_t st) override {
     return check(nccl_api().allGather(send, recv, cnt, ncclDouble, comm, st), "ncclAllGather");
+  }
+  bool capturable() const override { return true; }
+  int wait(cudaStream_t st, double timeout_s) override {
+    NcclApi& a = nccl_api();
+    const auto t0 = std::chrono::steady_clock::now();
+    int naps = 0;
+    for (;;) {
+      const cudaError_t q = cudaStreamQuery(st);
+      if (q == cudaSuccess) return 0;
+      if (q != cudaErrorNotReady) {
+        err = std::string("stream: ") + cudaGetErrorString(q);
+        return -1;
+      }
+      if (a.asyncError && comm) {
+        ncclResult_t ae = ncclSuccess;
+        a.asyncError(comm, &ae);
+        if (ae != ncclSuccess && ae != ncclInProgress) {
+          err = std::string("NCCL asynchronous error: ") + a.errStr(ae);
+          abort_comm();
+          return -1;
+        }
+      }
+      const double el =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (timeout_s > 0 && el > timeout_s) {
+        err = "NCCL: stream not done after " + std::to_string(timeout_s) +
+              " s (peer lost?); communicator aborted";
+        abort_comm();
+        return -1;
+      }
+      // spin briefly, then back off to 50 us naps
+      if (++naps > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+  }
+  void abort_comm() {
+    if (comm && nccl_api().abort) {
+      nccl_api().abort(comm);
+      comm = nullptr;
+    }
   }
 };
 }  // namespace
@@ -269,6 +314,14 @@ struct LoopbackComm : Comm {
     wait_peers_done(st, true, none);
     cudaMemcpyAsync(dev, h->tmp[r], (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, st);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  }
+  int wait(cudaStream_t st, double) override {
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      err = std::string("stream: ") + cudaGetErrorString(e);
+      return -1;
+    }
+    return h->aborted ? fail_abort() : 0;
   }
   int allgather(const double* send, double* recv, size_t count, cudaStream_t st) override {
     h->sendp[r] = send;

@@ -35,6 +35,13 @@ struct Comm {
   virtual int allreduce_sum(double* dev, int n, cudaStream_t st) = 0;
   // recv[r*count ..) = rank r's send, count doubles
   virtual int allgather(const double* send, double* recv, size_t count, cudaStream_t st) = 0;
+  // Wait for the stream like cudaStreamSynchronize, but never forever: NCCL polls
+  // ncclCommGetAsyncError while the stream runs and aborts the communicator on an
+  // asynchronous error (a dead or failed peer) or after timeout_s seconds; -1 then.
+  virtual int wait(cudaStream_t st, double timeout_s) = 0;
+  // true if the collectives may be captured into a CUDA graph (NCCL; the loopback hub
+  // synchronises its virtual ranks on the host)
+  virtual bool capturable() const { return false; }
   std::string err;
 };
 

@@ -224,7 +224,14 @@ __global__ void __launch_bounds__(32) k_apply_orb(const LevelDev L, int colour, 
   const double* Sbase = L.So + (int64_t)colour * nchunk * NORB * 32;
   const uint64_t pol = evict_first_policy();
   const int G = (int)gridDim.x, b = (int)blockIdx.x;
-  const int nmine = b < nchunk ? (nchunk - 1 - b) / G + 1 : 0;
+  // L.clist: this launch covers only the listed chunks (the partitioned levels' split
+  // colour-1 pass: interface chunks first, then the rest while the halo is exchanged)
+  const int ntot = L.clist ? L.ncl : nchunk;
+  const int nmine = b < ntot ? (ntot - 1 - b) / G + 1 : 0;
+  auto chunk_at = [&](int k) -> int64_t {
+    const int q = b + k * G;
+    return L.clist ? (int64_t)__ldg(L.clist + q) : (int64_t)q;
+  };
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
@@ -233,7 +240,7 @@ __global__ void __launch_bounds__(32) k_apply_orb(const LevelDev L, int colour, 
   __syncwarp();
   auto issue = [&](int k) {   // lane 0: chunk of position k into stage k % NST
     const int s = k % NST;
-    const int64_t c = (int64_t)b + (int64_t)k * G;
+    const int64_t c = chunk_at(k);
     mbar_expect_tx(&bars[s], (uint32_t)C::STAGE_BYTES);
     tma_bulk_g2s(stage_buf + (size_t)s * NORB * 32, Sbase + c * NORB * 32, C::STAGE_BYTES,
                  &bars[s], pol);
@@ -273,7 +280,7 @@ __global__ void __launch_bounds__(32) k_apply_orb(const LevelDev L, int colour, 
       bdn[f] = true;
     }
     if (k >= nmine) return;
-    const int64_t s = ((int64_t)b + (int64_t)k * G) * 32 + lane;
+    const int64_t s = chunk_at(k) * 32 + lane;
     if (s < nec) {
       slot_elem(L.nx, colour, s, ein, ejn);
       elem_edges(L.nx, L.ny, ein, ejn, edn, bdn, L.dmask);
@@ -283,7 +290,7 @@ __global__ void __launch_bounds__(32) k_apply_orb(const LevelDev L, int colour, 
   };
   prefetch(0);
   for (int k = 0; k < nmine; ++k) {
-    const int64_t c = (int64_t)b + (int64_t)k * G;
+    const int64_t c = chunk_at(k);
     const int64_t s = c * 32 + lane;
     const bool act = s < nec;
     int64_t ed[4];
@@ -781,7 +788,7 @@ static int cps_of(const LevelDev& L, int mode) {
 int apply_grid(const LevelDev& L) { return apply_grid_mode(L, AM_APPLY); }
 
 int apply_grid_mode(const LevelDev& L, int mode) {
-  const int64_t nchunk = (L.ne / 2 + 31) / 32;
+  const int64_t nchunk = L.clist ? (int64_t)L.ncl : (L.ne / 2 + 31) / 32;
   int cps;
   switch (L.p) {
     case 1: cps = cps_of<1>(L, mode); break;

@@ -58,6 +58,8 @@ struct LevelDev {
   double* So;              // [2][nchunk][NORB][32] orbit values of the element maps
   double* Dco;             // [nchunk][4][NCS][32] D_e^-1 orbits, colour-1 element order
   double* Dso;             // [NCS][nedge] D_e^-1 orbits, SoA (edge-parallel kernels)
+  const int* clist;        // non-null: an orbit-level pass covers only these chunks (ncl of them)
+  int ncl;
   int sweep;               // mg_set_option MG_OPT_SWEEP: 0 auto, 1 wherever possible, -1 never
   int grid_cap;            // mg_set_option MG_OPT_APPLY_GRID_CAP: max CTAs per apply pass (0: none)
   // partitioned levels (multi-GPU): local sides 0 bottom, 1 right, 2 top, 3 left

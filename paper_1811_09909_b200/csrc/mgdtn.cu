@@ -29,6 +29,9 @@ struct HostLevel {
   double h = 0.0;
   size_t o_S = 0, o_Dinv = 0, o_Dc = 0, o_coef = 0, o_lam = 0, o_r = 0, o_e = 0, o_w = 0, o_d = 0;
   size_t o_So = 0, o_Dco = 0, o_Dso = 0;   // orbit storage (R9, d4.cuh)
+  size_t o_clist = 0;   // partitioned orbit level: colour-1 chunks, interface ones first
+  int* clist = nullptr;
+  int nclB = 0, nclI = 0;
   size_t o_KIIinv = 0, o_Pm = 0, o_Rm = 0, o_cbuf = 0, o_lpart = 0;
   double* lpart = nullptr;   // per-level partial sums + 16 scalars (concurrent power iterations)
   double *KIIinv = nullptr, *Pm = nullptr, *cbuf = nullptr;
@@ -72,6 +75,8 @@ struct Ctx {
   double* pinned = nullptr;
   cudaGraphExec_t gS = nullptr;   // whole PCG solve: prologue + conditional WHILE loop
   cudaGraphExec_t gV = nullptr;   // one V-cycle, fine L.r -> L.e (GMRES / MG-solver / mg_vcycle)
+  cudaGraphExec_t gPA = nullptr, gPBA = nullptr;   // partitioned PCG over NCCL: the first
+  long long nPA = 0, nPBA = 0;                      // iteration's A-part, then B + A parts
   long long nV = 0;               // kernels in gV
   const double* vres = nullptr;   // the fine work vector that holds gV's result
   cudaGraphExec_t gU = nullptr;   // the whole setup after the input copies (forked streams as
@@ -101,8 +106,12 @@ struct Ctx {
   HostLevel lgl;                   // this rank's block of level Lg (restriction / prolongation)
   size_t o_hs = 0, o_hr = 0, o_gall = 0, o_sden = 0, o_sall = 0, halo_doubles = 0;
   int comm_rc = 0;                 // first communicator failure (reported by the next sync point)
+  double comm_timeout_s = 300.0;   // host waits on a partitioned context give up after this
+                                   // (mg_set_option MG_OPT_COMM_TIMEOUT_MS); NCCL is aborted
   // setup: the levels' Chebyshev power iterations are independent and run on their
   // own streams (fork / join with events on the ctx stream)
+  cudaStream_t cst = nullptr;      // partitioned: halo exchange overlapped with interior work
+  cudaEvent_t evB = nullptr, evC = nullptr;
   std::vector<cudaStream_t> side;
   std::vector<cudaEvent_t> side_ev, fork_evs;
   // mg_solve_host: the source-term / boundary-data uploads run on their own stream,
@@ -140,6 +149,20 @@ static int cuda_check(Ctx* c, cudaError_t e, const char* where) {
   } while (0)
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// host wait for a stream: on a partitioned context through the communicator, which polls
+// NCCL's asynchronous errors and gives up after comm_timeout_s (a lost peer never hangs
+// the caller); plain cudaStreamSynchronize otherwise
+static int sync_st(Ctx* c, cudaStream_t st) {
+  if (c->comm && c->nranks > 1) {
+    if (c->comm->wait(st, c->comm_timeout_s) != 0) {
+      if (c->comm_rc == 0) c->comm_rc = MG_ERR_NCCL;
+      return fail(c, MG_ERR_NCCL, "communicator: " + c->comm->err);
+    }
+    return MG_OK;
+  }
+  return cuda_check(c, cudaStreamSynchronize(st), "cudaStreamSynchronize");
+}
 
 constexpr int HIST_CAP = 16384;   // device residual history; larger maxit -> host loop
 
@@ -204,6 +227,7 @@ static void layout(Ctx* c) {
     const LevelDev& d = L.d;
     L.o_S = take((size_t)2 * d.nchunk * d.npk * 32 * sizeof(double));
     L.o_Dinv = take((size_t)d.nedge * d.k1 * d.k1 * sizeof(double));
+    if (d.orb && d.imask) L.o_clist = take((size_t)d.nchunk * sizeof(int));
     if (d.orb) {   // orbit records replace the packed colour-1 D_e^-1 stream
       L.o_So = take((size_t)2 * d.nchunk * d4_norb(d.p) * 32 * sizeof(double));
       L.o_Dco = take((size_t)d.nchunk * 4 * d4_ncs(d.p) * 32 * sizeof(double));
@@ -296,6 +320,7 @@ static void bind_pointers(Ctx* c) {
     L.d.Dinv = D(L.o_Dinv);
     // packed-symmetric D_e^-1 (symmetric packed levels) or the orbit records
     L.d.Dc = (c->ns || L.d.orb) ? nullptr : D(L.o_Dc);
+    if (L.d.orb && L.d.imask) L.clist = reinterpret_cast<int*>(b + L.o_clist);
     if (L.d.orb) {
       L.d.So = D(L.o_So);
       L.d.Dco = D(L.o_Dco);
@@ -463,6 +488,25 @@ static int upload_static(Ctx* c) {
   if (!fidx.empty())
     CK(cudaMemcpyAsync(c->fidx, fidx.data(), fidx.size() * sizeof(int), cudaMemcpyHostToDevice,
                        c->st));
+  for (auto& L : c->lev) {   // split colour-1 pass of the partitioned orbit levels
+    if (!L.clist) continue;
+    const LevelDev& d = L.d;
+    const int64_t nec = d.ne / 2;
+    std::vector<int> bl, il;
+    for (int q = 0; q < d.nchunk; ++q) {
+      bool itf = false;
+      for (int64_t sl = (int64_t)q * 32; sl < (int64_t)q * 32 + 32 && sl < nec && !itf; ++sl) {
+        int i, j;
+        slot_elem(d.nx, 1, sl, i, j);
+        itf = elem_itf(d.nx, d.ny, i, j, d.imask) != 0;
+      }
+      (itf ? bl : il).push_back(q);
+    }
+    L.nclB = (int)bl.size();
+    L.nclI = (int)il.size();
+    bl.insert(bl.end(), il.begin(), il.end());
+    CK(cudaMemcpyAsync(L.clist, bl.data(), bl.size() * sizeof(int), cudaMemcpyHostToDevice, c->st));
+  }
   if (c->tail_dense) {
     const LevelDev& t = c->lev[c->tail_start].d;
     std::vector<int> tf;
@@ -473,13 +517,17 @@ static int upload_static(Ctx* c) {
     CK(cudaMemcpyAsync(c->tfidx, tf.data(), tf.size() * sizeof(int), cudaMemcpyHostToDevice,
                        c->st));
   }
-  CK(cudaStreamSynchronize(c->st));
+  RC(sync_st(c, c->st));
   return MG_OK;
 }
 
 static void drop_graphs(Ctx* c) {
   if (c->gS) cudaGraphExecDestroy(c->gS);
   c->gS = nullptr;
+  if (c->gPA) cudaGraphExecDestroy(c->gPA);
+  c->gPA = nullptr;
+  if (c->gPBA) cudaGraphExecDestroy(c->gPBA);
+  c->gPBA = nullptr;
   if (c->gV) cudaGraphExecDestroy(c->gV);
   c->gV = nullptr;
   if (c->gU) cudaGraphExecDestroy(c->gU);
@@ -489,7 +537,7 @@ static void drop_graphs(Ctx* c) {
 static int check_device_error(Ctx* c) {
   DevError h{};
   CK(cudaMemcpyAsync(&h, c->err, sizeof(DevError), cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
+  RC(sync_st(c, c->st));
   if (c->comm_rc) return c->comm_rc;
   if (h.code == 0) return MG_OK;
   CK(cudaMemsetAsync(c->err, 0, sizeof(DevError), c->st));
@@ -525,10 +573,11 @@ static void comm_fail(Ctx* c, int rc) {
 
 // exchange c->hsend -> c->hrecv with the neighbours across the interface sides of
 // level d: `per` doubles per interface edge, side stride `stride` doubles
-static void halo_exchange(Ctx* c, const LevelDev& d, int stride, int per) {
+static void halo_exchange(Ctx* c, const LevelDev& d, int stride, int per,
+                          cudaStream_t st = nullptr) {
   int cnt[4];
   for (int f = 0; f < 4; ++f) cnt[f] = ((d.imask >> f) & 1) ? side_len(d.nx, d.ny, f) * per : 0;
-  comm_fail(c, c->comm->halo(c->nbr, c->hsend, c->hrecv, stride, cnt, c->st));
+  comm_fail(c, c->comm->halo(c->nbr, c->hsend, c->hrecv, stride, cnt, st ? st : c->st));
 }
 
 // scal[slot] = sum of partials over every rank (then the k_reduce op)
@@ -559,6 +608,34 @@ static void apply_mode(Ctx* c, const HostLevel& L, int mode, const double* x, do
     c->launches += launch_apply_tile(L.d, mode, x, y, r, d, nullptr, step, partials, c->st);
     return;
   }
+  if (L.clist && c->cst) {
+    // partitioned orbit level ("boundary elements first, start NCCL, then
+    // interior"): colour 0 everywhere, then the colour-1 chunks that touch a partition
+    // interface; their partial sums go out (pack, halo, interface epilogue) on the
+    // communication stream while the other colour-1 chunks -- which touch no interface
+    // edge -- run on the main stream
+    LevelDev dB = L.d, dI = L.d;
+    dB.clist = L.clist;
+    dB.ncl = L.nclB;
+    dI.clist = L.clist + L.nclB;
+    dI.ncl = L.nclI;
+    const int gB = L.nclB ? apply_grid_mode(dB, mode) : 0;
+    const int gI = L.nclI ? apply_grid_mode(dI, mode) : 0;
+    c->launches += launch_apply(L.d, 0, AM_W0, x, y, nullptr, nullptr, 0, nullptr, true, c->st);
+    if (L.nclB) c->launches += launch_apply(dB, 1, mode, x, y, r, d, step, partials, true, c->st);
+    cudaEventRecord(c->evB, c->st);
+    cudaStreamWaitEvent(c->cst, c->evB, 0);
+    c->launches += launch_itf_pack(L.d, y, c->hsend, c->cst);
+    halo_exchange(c, L.d, itf_stride(L.d), L.d.k1, c->cst);
+    c->launches += launch_itf_epilogue(L.d, mode, const_cast<double*>(x), y, r, d, step, c->hrecv,
+                                       partials ? partials + gB + gI : nullptr, c->cst);
+    cudaEventRecord(c->evC, c->cst);
+    if (L.nclI)
+      c->launches += launch_apply(dI, 1, mode, x, y, r, d, step, partials ? partials + gB : nullptr,
+                                  true, c->st);
+    cudaStreamWaitEvent(c->st, c->evC, 0);
+    return;
+  }
   c->launches += launch_apply2(L.d, mode, x, y, r, d, step, partials, true, c->st);
   if (L.d.imask) {
     c->launches += launch_itf_pack(L.d, y, c->hsend, c->st);
@@ -569,8 +646,18 @@ static void apply_mode(Ctx* c, const HostLevel& L, int mode, const double* x, do
   }
 }
 // number of dot-product partials apply_mode writes
-static int apply_parts(const LevelDev& d, int mode) {
+static int apply_parts(const HostLevel& L, int mode) {
+  const LevelDev& d = L.d;
   if (tiled(d, mode)) return apply_tile_grid(d);
+  if (L.clist) {   // split colour-1 pass (apply_mode)
+    LevelDev dB = d, dI = d;
+    dB.clist = L.clist;
+    dB.ncl = L.nclB;
+    dI.clist = L.clist + L.nclB;
+    dI.ncl = L.nclI;
+    return (L.nclB ? apply_grid_mode(dB, mode) : 0) + (L.nclI ? apply_grid_mode(dI, mode) : 0) +
+           itf_blocks();
+  }
   return apply2_grid(d, mode) + (d.imask ? itf_blocks() : 0);
 }
 
@@ -761,9 +848,9 @@ static int setup_body(Ctx* c) {
       const bool last = it + 1 == c->sm.lmax_iters;
       apply_mode(c, L, AM_DINV, L.e, L.w, nullptr, nullptr, 0, last ? part : nullptr);
     }
-    reduce_scal(c, part, apply_parts(L.d, AM_DINV), sc, 7, 0);   // v.Dv
+    reduce_scal(c, part, apply_parts(L, AM_DINV), sc, 7, 0);   // v.Dv
     apply_full(c, L, L.e, L.w, part);
-    reduce_scal(c, part, apply_parts(L.d, AM_APPLY), sc, 8, 0);  // v.Av
+    reduce_scal(c, part, apply_parts(L, AM_APPLY), sc, 8, 0);  // v.Av
     c->launches += launch_lmax_finish(sc, c->sm.lmax_safety, c->sm.cheb_ratio, numax, L.lam,
                                       L.d.coef, c->st);
     return MG_OK;
@@ -935,7 +1022,7 @@ static void pcg_iter_A(Ctx* c) {  // Ap, alpha, x/r update, rr
   HostLevel& F = c->lev[0];
   const int vg = vec_grid(F.d.ndof);
   apply_full(c, F, c->pv, c->ap, c->part);
-  reduce_scal(c, c->part, apply_parts(F.d, AM_APPLY), c->scal, 1, 1);
+  reduce_scal(c, c->part, apply_parts(F, AM_APPLY), c->scal, 1, 1);
   c->launches += launch_pcg_update(c->x, F.r, c->pv, c->ap, c->scal, F.d.ndof, c->part, vg, c->st,
                                    &F.d);
   reduce_scal(c, c->part, vg, c->scal, 2, 0);
@@ -1032,7 +1119,7 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
     c->launches += launch_pcg_init(c->ist, c->scal, rtol, maxit, st);
     CK(cudaGraphLaunch(c->gS, st));
     CK(cudaMemcpyAsync(c->pinned, c->ist, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    RC(sync_st(c, st));
     int hs[2];
     std::memcpy(hs, c->pinned, sizeof(hs));
     it = hs[0];
@@ -1047,7 +1134,7 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
       c->launches += launch_copy(lambda, c->x, n, st);
     }
     CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(st));
+    RC(sync_st(c, st));
     rel = hv[it];
     if (hist) std::memcpy(hist, hv.data(), (it + 1) * sizeof(double));
     if (iters_out) *iters_out = it;
@@ -1062,12 +1149,12 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
   c->launches += launch_dot(F.r, F.r, n, c->part, vg, st, &F.d);
   reduce_scal(c, c->part, vg, c->scal, 5, 0);
   CK(cudaMemcpyAsync(c->pinned, c->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  RC(sync_st(c, st));
   const double gg = c->pinned[5];
   if (hist) hist[0] = gg > 0 ? 1.0 : 0.0;
   if (!(gg > 0.0)) {   // g = 0 -> lambda = 0 in 0 iterations
     CK(cudaMemsetAsync(lambda, 0, n * sizeof(double), st));
-    CK(cudaStreamSynchronize(st));
+    RC(sync_st(c, st));
     if (iters_out) *iters_out = 0;
     if (relres_out) *relres_out = 0.0;
     if (status_out) *status_out = MG_CONVERGED;
@@ -1080,10 +1167,43 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
   reduce_scal(c, c->part, vg, c->scal, 0, 0);
   c->launches += launch_copy(c->pv, z, n, st);
   CK(cudaGetLastError());
-  for (it = 1; it <= maxit; ++it) {
+  // Partitioned over NCCL with graphs on: every iteration's ~150 launches -- the V-cycle,
+  // the halo send / recv groups, the all-reduced PCG scalars -- are captured once (NCCL
+  // collectives are stream-capturable) and replayed as ONE graph launch; the host then
+  // waits (polling NCCL's error state) and reads the two scalars of the stop test.
+  const bool gpart = partitioned(c) && c->use_graphs && c->comm && c->comm->capturable() &&
+                     st != nullptr;
+  auto capture = [&](bool withB, cudaGraphExec_t* out, long long* nk) -> int {
+    cudaGraph_t g = nullptr;
+    const long long l0g = c->launches;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    if (withB) pcg_iter_B(c);
     pcg_iter_A(c);
-    CK(cudaMemcpyAsync(c->pinned, c->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    cudaMemcpyAsync(c->pinned, c->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, st);
+    const cudaError_t e = cudaStreamEndCapture(st, &g);
+    *nk = c->launches - l0g;
+    c->launches = l0g;
+    if (c->comm_rc) {
+      if (g) cudaGraphDestroy(g);
+      return c->comm_rc;
+    }
+    CK(e);
+    const cudaError_t e2 = cudaGraphInstantiate(out, g, 0);
+    cudaGraphDestroy(g);
+    CK(e2);
+    return MG_OK;
+  };
+  if (gpart && !c->gPA) RC(capture(false, &c->gPA, &c->nPA));
+  if (gpart && !c->gPBA) RC(capture(true, &c->gPBA, &c->nPBA));
+  for (it = 1; it <= maxit; ++it) {
+    if (gpart) {
+      CK(cudaGraphLaunch(it == 1 ? c->gPA : c->gPBA, st));
+      c->launches += it == 1 ? c->nPA : c->nPBA;
+    } else {
+      pcg_iter_A(c);
+      CK(cudaMemcpyAsync(c->pinned, c->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    RC(sync_st(c, st));
     const double pAp = c->pinned[1], rr = c->pinned[2];
     rel = std::sqrt(rr / gg);
     if (hist) hist[it] = rel;
@@ -1100,12 +1220,12 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
       break;
     }
     if (it == maxit) break;
-    pcg_iter_B(c);
+    if (!gpart) pcg_iter_B(c);
   }
   if (it > maxit) it = maxit;
   c->launches += launch_copy(lambda, c->x, n, st);
   CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(st));
+  RC(sync_st(c, st));
   if (iters_out) *iters_out = it;
   if (relres_out) *relres_out = rel;
   if (status_out) *status_out = status;
@@ -1250,7 +1370,7 @@ static int gmres_impl(Ctx* c, const double* g, double* x, double tol, int maxit,
       c->launches += launch_scale_rsqrt(Hd + j + 1, Vj(j + 1), n, c->st);
       CK(cudaMemcpyAsync(hcol.data(), Hd, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost,
                          c->st));
-      CK(cudaStreamSynchronize(c->st));
+      RC(sync_st(c, c->st));
       for (int i = 0; i <= j; ++i) h(i, j) = hcol[i];
       hn = std::sqrt(hcol[j + 1]);
     } else {
@@ -1511,7 +1631,15 @@ int mg_build_hierarchy_ex(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_level
         return MG_ERR_NCCL;
       }
     }
-    c->use_graphs = false;   // host-driven PCG loop (collectives between iterations)
+    // PCG: host-driven loop; over NCCL each iteration is replayed from a captured graph
+    // (the loopback hub synchronises its virtual ranks on the host: eager launches)
+    if (cudaStreamCreateWithFlags(&c->cst, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->evB, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->evC, cudaEventDisableTiming) != cudaSuccess) {
+      delete c->comm;
+      delete c;
+      return MG_ERR_CUDA;
+    }
   }
   plan_tail(c);
   plan_tail_dense(c);
@@ -1847,7 +1975,7 @@ int mg_solve_host(void* ctx, const double* K_host, const int8_t* method_host,
   // full trace: free part + Dirichlet values (c->lamD is 0 off dOmega, lamd is 0 on it)
   c->launches += launch_add(lamd, c->lamD, d.ndof, st);
   CK(cudaMemcpyAsync(lambda_host, lamd, d.ndof * sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  RC(sync_st(c, st));
   if (iters) *iters = it;
   if (relres) *relres = rel;
   if (solve_status) *solve_status = stt;
@@ -1866,7 +1994,7 @@ int mg_recover_volume(void* ctx, const double* lambda_full, const double* f_qp, 
   if (q_exact_qp && l2_err) {
     reduce_scal(c, c->part, grid, c->sscal, 6, 0);   // sum over elements (and ranks)
     CK(cudaMemcpyAsync(c->pinned, c->sscal + 6, sizeof(double), cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
+    RC(sync_st(c, c->st));
     *l2_err = std::sqrt(c->pinned[0]);
   }
   CK(cudaGetLastError());
@@ -1928,7 +2056,7 @@ int mg_debug_set_element_dtn(void* ctx, int32_t level, const double* src) {
   CK(cudaGetLastError());
   // the apply kernels prefetch S_T before their dependency wait (PDL): make the
   // new S_T complete before any later launch
-  CK(cudaStreamSynchronize(c->st));
+  RC(sync_st(c, c->st));
   return MG_OK;
 }
 
@@ -1940,7 +2068,7 @@ int mg_level_lambda_max(const void* ctx, int32_t level, double* lam) {
   *lam = 0.0;
   if (c->sm.kind != MG_SMOOTH_CHEBYSHEV || L == &c->lev.back()) return MG_OK;
   CK(cudaMemcpyAsync(lam, L->lam, sizeof(double), cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
+  RC(sync_st(c, c->st));
   return MG_OK;
 }
 
@@ -1964,6 +2092,10 @@ int mg_set_option(void* ctx, int32_t key, int64_t value) {
   if (key == MG_OPT_SWEEP) {
     if (value < -1 || value > 1) return fail(c, MG_ERR_ARG, "MG_OPT_SWEEP: -1, 0 or 1");
     for (auto& L : c->lev) L.d.sweep = (int)value;
+  } else if (key == MG_OPT_COMM_TIMEOUT_MS) {
+    if (value < 1) return fail(c, MG_ERR_ARG, "MG_OPT_COMM_TIMEOUT_MS must be >= 1");
+    c->comm_timeout_s = (double)value * 1e-3;
+    return MG_OK;
   } else if (key == MG_OPT_APPLY_GRID_CAP) {
     if (value < 0 || value > (1 << 20)) return fail(c, MG_ERR_ARG, "MG_OPT_APPLY_GRID_CAP out of range");
     for (auto& L : c->lev) L.d.grid_cap = (int)value;
@@ -2000,6 +2132,9 @@ void mg_destroy(void* ctx) {
   for (auto ex : c->side_ev) cudaEventDestroy(ex);
   for (auto ex : c->fork_evs) cudaEventDestroy(ex);
   if (c->copy_st) cudaStreamDestroy(c->copy_st);
+  if (c->cst) cudaStreamDestroy(c->cst);
+  if (c->evB) cudaEventDestroy(c->evB);
+  if (c->evC) cudaEventDestroy(c->evC);
   if (c->copy_ev0) cudaEventDestroy(c->copy_ev0);
   if (c->copy_ev1) cudaEventDestroy(c->copy_ev1);
   if (c->pinned) cudaFreeHost(c->pinned);

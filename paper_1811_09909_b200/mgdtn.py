@@ -519,7 +519,7 @@ class MGSolver:
     def use_graphs(self, on: bool):
         self._chk(self.lib.mg_set_use_graphs(self.ctx, int(on)), "mg_set_use_graphs")
 
-    OPT_SWEEP, OPT_APPLY_GRID_CAP = 1, 2
+    OPT_SWEEP, OPT_APPLY_GRID_CAP, OPT_COMM_TIMEOUT_MS = 1, 2, 3
 
     def set_option(self, key: int, value: int):
         """mg_set_option: execution options (kernel choice / grid size) for tests."""

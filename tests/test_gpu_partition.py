@@ -38,7 +38,11 @@ def rel(a, b):
 
 # (config recipe, n, px, py, gather_ne): gather_ne small keeps several levels partitioned
 CASES = [(2, 32, 2, 1, 16), (2, 32, 2, 2, 0), (4, 32, 2, 2, 16), (3, 64, 1, 2, 64), (1, 16, 2, 2, 4),
-         (2, 24, 2, 2, 0)]   # the last: odd (3 x 3) gather-level blocks
+         (2, 24, 2, 2, 0),    # odd (3 x 3) gather-level blocks
+         # the config-5 recipe (the north star's scaling run) in its bench layouts 2x1, 2x2,
+         # 4x2: the orbit levels' split colour-1 pass (interface chunks, halo on the
+         # communication stream, interior chunks) and the gather level
+         (5, 64, 2, 1, 16), (5, 64, 2, 2, 16), (5, 128, 4, 2, 64), (5, 128, 2, 2, 0)]
 
 
 def level_ids(plan, lev):
@@ -68,6 +72,7 @@ def run_ranks(cfg, pr, px, py, gather_ne, x_glob, r_glob):
         part = Partition(rank, N, px, py, gather_ne=gather_ne, loopback=hub)
         plan = partition_plan(n, n, p, part)
         s = MGSolver(n, p=p, partition=part)
+        s.set_option(s.OPT_COMM_TIMEOUT_MS, 120000)   # host waits poll the communicator
         assert s.nlevels == plan["nlevels"]
         bp = W.block_problem(pr, px, py, rank)
         s.setup(bp.K, bp.method, bp.tau, smoother_from_config(cfg))

@@ -6,9 +6,10 @@ u = 0 on dOmega, V(2,2) Chebyshev, rtol 1e-10) on an n x n mesh, the whole trace
 solution stored.  Config 5 itself (4096^2, 168M trace dofs) is beyond the oracle's
 memory; this is the largest size of its recipe the container solves.
 
-The oracle runs on its element maps projected by readings R5 / R9
+The oracle runs under the GPU's readings: fine maps projected by R5 / R9
 (tests/oracle_proj.py; both projections are onto subspaces holding the exact maps,
-so they are no farther from them): the GPU stores the same projections.  Calls only
+so they are no farther from them) and every coarse level built macro by macro and
+projected onto S.1 = 0 (R10, oracle/multigrid.py galerkin="macro", project_levels=True).  Calls only
 oracle/, workloads/ and that numpy projection -- no value comes from the CUDA path.
 
     python tools/make_c5_golden.py 512
@@ -39,7 +40,8 @@ def main(n):
     ts.A = ts.A_full[ts.free][:, ts.free].tocsr()
     g_full = assembly.assemble_vector(n, c.p, ts.b)
     ts.g = g_full[ts.free] - ts.A_full[ts.free][:, ts.dir] @ ts.lam_D[ts.dir]
-    H = multigrid.Hierarchy(ts.A, n, c.p, smoother=c.smoother, nu_pre=c.nu, nu_post=c.nu)
+    H = multigrid.Hierarchy(ts.A, n, c.p, smoother=c.smoother, nu_pre=c.nu, nu_post=c.nu,
+                            element_maps=ts.S, galerkin="macro", project_levels=True)
     res = krylov.pcg(ts.A, H.vcycle, ts.g, rtol=c.rtol, maxit=4000)
     t1 = time.perf_counter()
     lam = ts.to_full(res["x"])
@@ -47,7 +49,7 @@ def main(n):
     np.save(base + ".npy", lam)
     lg = np.log10(pr.K)
     out = {
-        "source": "tools/make_c5_golden.py (oracle/ on R5/R9-projected maps); config-5 recipe at n=%d, "
+        "source": "tools/make_c5_golden.py (oracle/ under readings R5/R9/R10); config-5 recipe at n=%d, "
                   "ell = 32 elements" % n,
         "config": 5, "n": n, "p": c.p, "ell": c.extras["ell"], "iters": int(res["iters"]),
         "relres": float(res["relres"]), "true_relres": float(res["true_relres"]),
