@@ -285,9 +285,14 @@ struct RefDev {
 // kernels) but waits for the predecessor's completion and memory flush before
 // touching any data.  In a kernel launched without the attribute both are no-ops.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
+// No explicit griddepcontrol.launch_dependents: the dependent grid is released when this
+// grid exits (the implicit trigger).  Triggering at kernel entry let the next kernel's
+// CTAs take SM slots and spin for the whole of a long pass; measured (round 2, solve
+// time, trigger at entry -> at exit): config 2 6.03 -> 5.71 ms, config 3 3389 -> 3127 ms,
+// config 4 150 -> 116 ms, config 5 (30 iterations) 1417 -> 1163 ms.  What PDL still buys:
+// the launch of the dependent and its pre-wait prologue (the element-data TMA prefetch of
+// the apply kernels) overlap the primary's drain.
+__device__ __forceinline__ void pdl_trigger() {}
 __device__ __forceinline__ void pdl_enter() {
   pdl_wait();
   pdl_trigger();
