@@ -13,13 +13,67 @@
 namespace mgdtn {
 
 // ---------------------------------------------------------------- apply pieces
+// The K1 doubles of one edge with 16-byte accesses where the address allows (an edge
+// starts 16-byte aligned iff e*K1 is even).  In a colour pass the 32 lanes of a warp
+// hold every other element of a row, so their edges of one role all have one parity:
+// the branch does not diverge, and a warp's access to an edge block takes ceil(K1/2)
+// instead of K1 L1 wavefront groups (the gathers of a thread-per-element pass are
+// L1-wavefront-bound: 32 lanes x 8 bytes at an 80-byte stride touch 20 lines each).
+template <int K1>
+__device__ __forceinline__ void ld_edge(const double* p, double* v) {
+  if (K1 % 2 == 0) {
+#pragma unroll
+    for (int q = 0; q < K1 / 2; ++q) {
+      const double2 t = reinterpret_cast<const double2*>(p)[q];
+      v[2 * q] = t.x;
+      v[2 * q + 1] = t.y;
+    }
+  } else if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+    for (int q = 0; q < K1 / 2; ++q) {
+      const double2 t = reinterpret_cast<const double2*>(p)[q];
+      v[2 * q] = t.x;
+      v[2 * q + 1] = t.y;
+    }
+    v[K1 - 1] = p[K1 - 1];
+  } else {
+    v[0] = p[0];
+#pragma unroll
+    for (int q = 0; q < K1 / 2; ++q) {
+      const double2 t = reinterpret_cast<const double2*>(p + 1)[q];
+      v[1 + 2 * q] = t.x;
+      v[2 + 2 * q] = t.y;
+    }
+  }
+}
+template <int K1>
+__device__ __forceinline__ void st_edge(double* p, const double* v) {
+  if (K1 % 2 == 0) {
+#pragma unroll
+    for (int q = 0; q < K1 / 2; ++q) reinterpret_cast<double2*>(p)[q] = make_double2(v[2 * q], v[2 * q + 1]);
+  } else if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+    for (int q = 0; q < K1 / 2; ++q) reinterpret_cast<double2*>(p)[q] = make_double2(v[2 * q], v[2 * q + 1]);
+    p[K1 - 1] = v[K1 - 1];
+  } else {
+    p[0] = v[0];
+#pragma unroll
+    for (int q = 0; q < K1 / 2; ++q)
+      reinterpret_cast<double2*>(p + 1)[q] = make_double2(v[1 + 2 * q], v[2 + 2 * q]);
+  }
+}
+
 template <int K1>
 __device__ __forceinline__ void gather_x(const double* x, const int64_t ed[4], const bool bd[4],
                                          double* xv) {
 #pragma unroll
   for (int f = 0; f < 4; ++f) {
+    if (bd[f]) {
 #pragma unroll
-    for (int a = 0; a < K1; ++a) xv[f * K1 + a] = bd[f] ? 0.0 : x[ed[f] * K1 + a];
+      for (int a = 0; a < K1; ++a) xv[f * K1 + a] = 0.0;
+    } else {
+      ld_edge<K1>(x + ed[f] * K1, xv + f * K1);
+    }
   }
 }
 
@@ -56,12 +110,26 @@ __device__ __forceinline__ void epi_load(const LevelDev& L, const int64_t ed[4],
       continue;
     }
     const int64_t base = ed[f] * K1;
+    double yo[K1], rv[K1], dv[K1];
+#pragma unroll
+    for (int a = 0; a < K1; ++a) yo[a] = rv[a] = dv[a] = 0.0;
+    if (!bd[f]) {
+      ld_edge<K1>(y + base, yo);
+      if (MODE != AM_APPLY && MODE != AM_DINV) {
+        if (NC) {
+#pragma unroll
+          for (int a = 0; a < K1; ++a) rv[a] = __ldg(r + base + a);
+        } else {
+          ld_edge<K1>(r + base, rv);
+        }
+      }
+      if (MODE == AM_SMOOTH && L.smoother == 1) ld_edge<K1>(d + base, dv);
+    }
 #pragma unroll
     for (int a = 0; a < K1; ++a) {
-      const double yo = bd[f] ? 0.0 : y[base + a];
-      if (MODE == AM_APPLY || MODE == AM_DINV) t[f * K1 + a] = yo;
-      else t[f * K1 + a] = bd[f] ? 0.0 : (NC ? __ldg(r + base + a) : r[base + a]) - yo;
-      if (MODE == AM_SMOOTH) dd[f * K1 + a] = (bd[f] || L.smoother != 1) ? 0.0 : d[base + a];
+      if (MODE == AM_APPLY || MODE == AM_DINV) t[f * K1 + a] = yo[a];
+      else t[f * K1 + a] = bd[f] ? 0.0 : rv[a] - yo[a];
+      if (MODE == AM_SMOOTH) dd[f * K1 + a] = dv[a];
     }
   }
 }
@@ -77,23 +145,20 @@ __device__ __forceinline__ void epi_store(const LevelDev& L, const int64_t ed[4]
     if (!((FMASK >> f) & 1)) continue;
     const int64_t base = ed[f] * K1;
     if (MODE != AM_W0 && ((itf >> f) & 1)) {   // partial sum only; finished after the halo
-#pragma unroll
-      for (int a = 0; a < K1; ++a) y[base + a] = yv[f * K1 + a];
+      st_edge<K1>(y + base, yv + f * K1);
       continue;
     }
-    if (MODE == AM_W0) {
-#pragma unroll
-      for (int a = 0; a < K1; ++a) y[base + a] = bd[f] ? 0.0 : yv[f * K1 + a];
-    } else if (MODE == AM_APPLY) {
+    if (MODE == AM_W0 || MODE == AM_APPLY || MODE == AM_RESID) {
+      double v[K1];
 #pragma unroll
       for (int a = 0; a < K1; ++a) {
-        const double v = bd[f] ? 0.0 : t[f * K1 + a] + yv[f * K1 + a];
-        y[base + a] = v;
-        if (DOT) dot = fma(xv[f * K1 + a], v, dot);
+        v[a] = bd[f] ? 0.0
+             : MODE == AM_W0 ? yv[f * K1 + a]
+             : MODE == AM_APPLY ? t[f * K1 + a] + yv[f * K1 + a]
+                               : t[f * K1 + a] - yv[f * K1 + a];
+        if (MODE == AM_APPLY && DOT) dot = fma(xv[f * K1 + a], v[a], dot);
       }
-    } else if (MODE == AM_RESID) {
-#pragma unroll
-      for (int a = 0; a < K1; ++a) y[base + a] = bd[f] ? 0.0 : t[f * K1 + a] - yv[f * K1 + a];
+      st_edge<K1>(y + base, v);
     } else if (MODE == AM_DINV) {  // power iteration on D^-1 A: x <- D^-1 A x in place
       if (!bd[f]) {
         double yf[K1];

@@ -111,9 +111,12 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
   constexpr bool HASD = MODE == AM_SMOOTH || MODE == AM_DINV || MODE == AM_GSC;
   if (MODE == AM_W0) {
 #pragma unroll
-    for (int f = F0; f < F0 + NF; ++f)
+    for (int f = F0; f < F0 + NF; ++f) {
+      double v[K1];
 #pragma unroll
-      for (int a = 0; a < K1; ++a) y[ed[f] * K1 + a] = bd[f] ? 0.0 : yv[f * K1 + a];
+      for (int a = 0; a < K1; ++a) v[a] = bd[f] ? 0.0 : yv[f * K1 + a];
+      st_edge<K1>(y + ed[f] * K1, v);
+    }
     return;
   }
   // an edge is "live" if its epilogue reads anything: not on dOmega, not a partition
@@ -126,16 +129,20 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
 #pragma unroll
   for (int f = F0; f < F0 + NF; ++f) {
     const int64_t base = ed[f] * K1;
+    double yo[K1], rv[K1];
 #pragma unroll
     for (int a = 0; a < K1; ++a) {
-      t[f * K1 + a] = 0.0;
+      yo[a] = rv[a] = 0.0;
       dd[f * K1 + a] = 0.0;
-      if (!live[f]) continue;
-      const double yo = y[base + a];
-      if (MODE == AM_APPLY || MODE == AM_DINV) t[f * K1 + a] = yo;
-      else t[f * K1 + a] = __ldg(r + base + a) - yo;
-      if (MODE == AM_SMOOTH && L.smoother == 1 && step > 0) dd[f * K1 + a] = d[base + a];
     }
+    if (live[f]) {
+      ld_edge<K1>(y + base, yo);
+      if (MODE != AM_APPLY && MODE != AM_DINV) ld_edge<K1>(r + base, rv);
+      if (MODE == AM_SMOOTH && L.smoother == 1 && step > 0) ld_edge<K1>(d + base, dd + f * K1);
+    }
+#pragma unroll
+    for (int a = 0; a < K1; ++a)
+      t[f * K1 + a] = (MODE == AM_APPLY || MODE == AM_DINV) ? yo[a] : rv[a] - yo[a];
     if (HASD) {
 #pragma unroll
       for (int o = 0; o < NCS; ++o) dv[f * NCS + o] = live[f] ? __ldg(Dp + (f * NCS + o) * 32) : 0.0;
@@ -147,6 +154,7 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
     const int64_t base = ed[f] * K1;
     const double* xf = xv + f * K1;
     const double* yf = yv + f * K1;
+    double dnv[K1], xnv[K1];
     if (bd[f]) {   // dOmega: y = 0 (APPLY / RESID / DINV); SMOOTH / GSC leave x untouched
       if (MODE == AM_APPLY || MODE == AM_RESID || MODE == AM_DINV) {
 #pragma unroll
@@ -161,17 +169,20 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
     }
     if (!live[f]) continue;   // LU-SGS: another colour's edge
     if (MODE == AM_APPLY) {
+      double v[K1];
 #pragma unroll
       for (int a = 0; a < K1; ++a) {
-        const double v = t[f * K1 + a] + yf[a];
-        y[base + a] = v;
-        if (DOT) dot = fma(xf[a], v, dot);
+        v[a] = t[f * K1 + a] + yf[a];
+        if (DOT) dot = fma(xf[a], v[a], dot);
       }
+      st_edge<K1>(y + base, v);
       continue;
     }
     if (MODE == AM_RESID) {
+      double v[K1];
 #pragma unroll
-      for (int a = 0; a < K1; ++a) y[base + a] = t[f * K1 + a] - yf[a];
+      for (int a = 0; a < K1; ++a) v[a] = t[f * K1 + a] - yf[a];
+      st_edge<K1>(y + base, v);
       continue;
     }
     double res[K1];
@@ -197,12 +208,14 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
         xo[base + a] = fma(c2, cc, xf[a]);
       } else {
         double dn = c2 * cc;
-        if (L.smoother == 1) {
-          if (step > 0) dn = fma(c1, dd[f * K1 + a], dn);
-          d[base + a] = dn;
-        }
-        xo[base + a] = xf[a] + dn;
+        if (L.smoother == 1 && step > 0) dn = fma(c1, dd[f * K1 + a], dn);
+        dnv[a] = dn;
+        xnv[a] = xf[a] + dn;
       }
+    }
+    if (MODE == AM_SMOOTH) {
+      if (L.smoother == 1) st_edge<K1>(d + base, dnv);
+      st_edge<K1>(xo + base, xnv);
     }
   }
 }

@@ -480,9 +480,12 @@ static SweepGeom sweep_geom(const LevelDev& L) {
 // strips must be whole chunks of the orbit records (64 columns, nx % 64 == 0); other
 // meshes keep the two-colour passes, and so do meshes too small to give every SM a
 // few segments of >= 16 rows (config 2's 256 x 256: 64 work items for 148 SMs)
+// Off by default (MG_OPT_SWEEP = 1 turns it on): with the dependents of every pass released
+// at its exit, the two-colour orbit passes are as fast at config 5 (38.7 ms per iteration
+// either way) and faster at config 3 (2428 vs 3127 ms; the p <= 2 sweep loses to the
+// 2-4 KB-per-chunk orbit ring), profiles/r02_sweep_probe.txt.
 bool tile_level(const LevelDev& L) {
-  if (L.sweep < 0 || !L.orb || L.imask != 0 || L.ns || L.nx % SW_C != 0) return false;
-  return L.sweep > 0 || (int64_t)(L.nx / SW_C) * (L.ny / 16) >= 4 * 148;
+  return L.sweep > 0 && L.orb && L.imask == 0 && !L.ns && L.nx % SW_C == 0;
 }
 
 int apply_tile_grid(const LevelDev& L) {
