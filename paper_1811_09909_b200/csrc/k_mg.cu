@@ -79,35 +79,53 @@ __global__ void k_smooth_first_dc(LevelDev L, const double* __restrict__ r, doub
 // the same step on an orbit-stored level (R9): edge-parallel, D_e^-1 from its
 // centrosymmetric orbits Dso (SoA, coalesced), r / e / d as contiguous per-edge rows
 template <int P>
-__global__ void k_smooth_first_orb(LevelDev L, const double* __restrict__ r, double* e, double* d) {
+__global__ void __launch_bounds__(128) k_smooth_first_orb(LevelDev L, const double* __restrict__ r,
+                                                         double* e, double* d) {
   pdl_enter();
   using D = D4<P>;
-  constexpr int K1 = P + 1;
+  constexpr int K1 = P + 1, EB = 128;
+  // 128 edges per block: r staged through shared memory (coalesced loads / stores)
+  __shared__ double sr[EB * K1];
   const double c2 = L.coef[1];
-  for (int64_t ed = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ed < L.nedge;
-       ed += (int64_t)gridDim.x * blockDim.x) {
-    if (edge_on_boundary(L.nx, L.ny, ed, L.dmask)) continue;
-    double dv[D::NCS], rv[K1];
+  const int t = threadIdx.x;
+  for (int64_t e0 = (int64_t)blockIdx.x * EB; e0 < L.nedge; e0 += (int64_t)gridDim.x * EB) {
+    const int ne = (int)(L.nedge - e0 < EB ? L.nedge - e0 : EB);
+    const int64_t off = e0 * K1;
+    for (int q = t; q < ne * K1; q += EB) sr[q] = __ldg(r + off + q);
+    __syncthreads();
+    double ev[K1];
 #pragma unroll
-    for (int o = 0; o < D::NCS; ++o) dv[o] = __ldg(L.Dso + (int64_t)o * L.nedge + ed);
+    for (int a = 0; a < K1; ++a) ev[a] = 0.0;
+    if (t < ne && !edge_on_boundary(L.nx, L.ny, e0 + t, L.dmask)) {
+      double dv[D::NCS];
 #pragma unroll
-    for (int a = 0; a < K1; ++a) rv[a] = __ldg(r + ed * K1 + a);
+      for (int o = 0; o < D::NCS; ++o) dv[o] = __ldg(L.Dso + (int64_t)o * L.nedge + e0 + t);
 #pragma unroll
-    for (int a = 0; a < K1; ++a) {
-      double c = 0.0;
+      for (int a = 0; a < K1; ++a) {
+        double c = 0.0;
 #pragma unroll
-      for (int b = 0; b < K1; ++b) c = fma(dv[D::cs(D::pe(a, b))], rv[b], c);
-      const double v = c2 * c;
-      e[ed * K1 + a] = v;
-      if (L.smoother == 1) d[ed * K1 + a] = v;
+        for (int b = 0; b < K1; ++b) c = fma(dv[D::cs(D::pe(a, b))], sr[t * K1 + b], c);
+        ev[a] = c2 * c;
+      }
     }
+    // (each thread reads and rewrites only its own edge's row of sr)
+    if (t < ne) {
+#pragma unroll
+      for (int a = 0; a < K1; ++a) sr[t * K1 + a] = ev[a];
+    }
+    __syncthreads();
+    for (int q = t; q < ne * K1; q += EB) {
+      e[off + q] = sr[q];
+      if (L.smoother == 1) d[off + q] = sr[q];
+    }
+    __syncthreads();
   }
 }
 
 int launch_smooth_first(const LevelDev& L, const double* r, double* e, double* d,
                         cudaStream_t st) {
   if (L.orb) {
-    const int g = cap_grid(L.nedge, 128, 148 * 16);
+    const int g = cap_grid(L.nedge, 128, 148 * 8);
     switch (L.k1) {
       case 2: launch_ex(k_smooth_first_orb<1>, g, 128, 0, true, st, L, r, e, d); return 1;
       case 3: launch_ex(k_smooth_first_orb<2>, g, 128, 0, true, st, L, r, e, d); return 1;
@@ -295,6 +313,94 @@ int launch_pcg_update(double* x, double* r, const double* p, const double* ap,
                       const double* scal, int64_t n, double* partials, int grid,
                       cudaStream_t st, const LevelDev* L) {
   launch_ex(k_pcg_update, grid, 256, 0, true, st, x, r, p, ap, scal, n, partials, own_mask(L));
+  return 1;
+}
+
+// The PCG update fused with the next V-cycle's first smoothing step (reading R2: from
+// e = 0 the first step needs no apply, e = c2 D_e^-1 r): thread per fine edge, x += alpha p,
+// r -= alpha Ap, ||r||^2 partials, and on the orbit level e = c2 D_e^-1 r (d = e for
+// Chebyshev) from the centrosymmetric D_e^-1 orbits -- r is not read a second time by a
+// separate first-step kernel.  After the last iteration the e / d it wrote are unused.
+template <int P>
+__global__ void __launch_bounds__(128) k_pcg_update_sf(LevelDev L, double* x, double* r,
+                                                      const double* __restrict__ p,
+                                                      const double* __restrict__ ap,
+                                                      const double* __restrict__ scal,
+                                                      double* partials, OwnMask om, double* e,
+                                                      double* d) {
+  pdl_enter();
+  using D = D4<P>;
+  constexpr int K1 = P + 1, EB = 128;
+  // a block's 128 edges are 128*K1 contiguous doubles of every vector: staged through
+  // shared memory so that global loads and stores are fully coalesced (a thread's own
+  // edge block sits K1 doubles after its neighbour's)
+  __shared__ double sx[EB * K1], sr[EB * K1], sp[EB * K1], sa[EB * K1];
+  const double alpha = scal[3];
+  const double c2 = L.coef[1];
+  const int t = threadIdx.x;
+  double s = 0.0;
+  for (int64_t e0 = (int64_t)blockIdx.x * EB; e0 < L.nedge; e0 += (int64_t)gridDim.x * EB) {
+    const int ne = (int)(L.nedge - e0 < EB ? L.nedge - e0 : EB);
+    const int64_t off = e0 * K1;
+    for (int q = t; q < ne * K1; q += EB) {
+      sx[q] = x[off + q];
+      sr[q] = r[off + q];
+      sp[q] = p[off + q];
+      sa[q] = ap[off + q];
+    }
+    __syncthreads();
+    if (t < ne) {
+      const int64_t ed = e0 + t;
+      const bool cnt = counted(om, ed * K1);
+      double rv[K1];
+#pragma unroll
+      for (int a = 0; a < K1; ++a) {
+        sx[t * K1 + a] = fma(alpha, sp[t * K1 + a], sx[t * K1 + a]);
+        rv[a] = fma(-alpha, sa[t * K1 + a], sr[t * K1 + a]);
+        sr[t * K1 + a] = rv[a];
+        if (cnt) s = fma(rv[a], rv[a], s);
+      }
+      double ev[K1];
+#pragma unroll
+      for (int a = 0; a < K1; ++a) ev[a] = 0.0;
+      if (!edge_on_boundary(L.nx, L.ny, ed, L.dmask)) {
+        double dv[D::NCS];
+#pragma unroll
+        for (int o = 0; o < D::NCS; ++o) dv[o] = __ldg(L.Dso + (int64_t)o * L.nedge + ed);
+#pragma unroll
+        for (int a = 0; a < K1; ++a) {
+          double c = 0.0;
+#pragma unroll
+          for (int b = 0; b < K1; ++b) c = fma(dv[D::cs(D::pe(a, b))], rv[b], c);
+          ev[a] = c2 * c;
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < K1; ++a) sp[t * K1 + a] = ev[a];   // e (and d = e)
+    }
+    __syncthreads();
+    for (int q = t; q < ne * K1; q += EB) {
+      x[off + q] = sx[q];
+      r[off + q] = sr[q];
+      e[off + q] = sp[q];
+      if (L.smoother == 1) d[off + q] = sp[q];
+    }
+    __syncthreads();
+  }
+  s = block_sum(s);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+int launch_pcg_update_sf(const LevelDev& L, double* x, double* r, const double* p,
+                         const double* ap, const double* scal, double* partials, int grid,
+                         double* e, double* d, cudaStream_t st) {
+  const int threads = 128;
+  switch (L.p) {
+    case 1: launch_ex(k_pcg_update_sf<1>, grid, threads, 0, true, st, L, x, r, p, ap, scal, partials, own_mask(&L), e, d); break;
+    case 2: launch_ex(k_pcg_update_sf<2>, grid, threads, 0, true, st, L, x, r, p, ap, scal, partials, own_mask(&L), e, d); break;
+    case 3: launch_ex(k_pcg_update_sf<3>, grid, threads, 0, true, st, L, x, r, p, ap, scal, partials, own_mask(&L), e, d); break;
+    default: launch_ex(k_pcg_update_sf<4>, grid, threads, 0, true, st, L, x, r, p, ap, scal, partials, own_mask(&L), e, d); break;
+  }
   return 1;
 }
 

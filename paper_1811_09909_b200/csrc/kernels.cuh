@@ -414,6 +414,11 @@ int launch_pcg_update(double* x, double* r, const double* p, const double* ap,
                       cudaStream_t st, const LevelDev* L = nullptr);
 int launch_pcg_pupdate(double* p, const double* z, const double* scal, int64_t n,
                        cudaStream_t st);
+// the update fused with the next V-cycle's first smoothing step on an orbit fine level
+// (e = c2 D_e^-1 r, d = e); partials[grid] of ||r||^2
+int launch_pcg_update_sf(const LevelDev& L, double* x, double* r, const double* p,
+                         const double* ap, const double* scal, double* partials, int grid,
+                         double* e, double* d, cudaStream_t st);
 int launch_pcg_init(int* istate, double* scal, double rtol, int maxit, cudaStream_t st);
 int launch_pcg_check(const double* scal, int* istate, double* hist, int hist_cap,
                      cudaGraphConditionalHandle h, cudaStream_t st);

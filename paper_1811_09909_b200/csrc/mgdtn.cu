@@ -1018,11 +1018,28 @@ static int setup_impl(Ctx* c, const double* K, const int8_t* method, const doubl
 
 // ---------------------------------------------------------------- PCG
 // scal: [0] rz, [1] pAp, [2] rr, [3] alpha, [4] beta, [5] gg
+// the fine level's first pre-smoothing step folded into the PCG update (k_pcg_update_sf):
+// orbit fine level (D_e^-1 orbits), a pre-smoothing step, not LU-SGS, and the fine level
+// runs the launch-per-step V-cycle (not the tabulated / single-launch tail)
+static bool pcg_sf(const Ctx* c) {
+  const HostLevel& F = c->lev[0];
+  return F.d.orb && c->sm.kind != MG_SMOOTH_LUSGS && c->sm.nu_pre > 0 && c->tail_start != 0 &&
+         c->lev.size() > 1;
+}
+
 static void pcg_iter_A(Ctx* c) {  // Ap, alpha, x/r update, rr
   HostLevel& F = c->lev[0];
   const int vg = vec_grid(F.d.ndof);
   apply_full(c, F, c->pv, c->ap, c->part);
   reduce_scal(c, c->part, apply_parts(F, AM_APPLY), c->scal, 1, 1);
+  if (pcg_sf(c)) {
+    const int64_t nb = (F.d.nedge + 127) / 128;
+    const int g = (int)(nb < 148 * 8 ? nb : 148 * 8);
+    c->launches += launch_pcg_update_sf(F.d, c->x, F.r, c->pv, c->ap, c->scal, c->part, g, F.e,
+                                        F.dv, c->st);
+    reduce_scal(c, c->part, g, c->scal, 2, 0);
+    return;
+  }
   c->launches += launch_pcg_update(c->x, F.r, c->pv, c->ap, c->scal, F.d.ndof, c->part, vg, c->st,
                                    &F.d);
   reduce_scal(c, c->part, vg, c->scal, 2, 0);
@@ -1031,7 +1048,7 @@ static void pcg_iter_A(Ctx* c) {  // Ap, alpha, x/r update, rr
 static void pcg_iter_B(Ctx* c) {  // z = B r, beta, p update
   HostLevel& F = c->lev[0];
   const int vg = vec_grid(F.d.ndof);
-  const double* z = vcycle_level(c, 0, false);
+  const double* z = vcycle_level(c, 0, pcg_sf(c));   // first step done by the update
   c->launches += launch_dot(F.r, z, F.d.ndof, c->part, vg, c->st, &F.d);
   reduce_scal(c, c->part, vg, c->scal, 0, 2);
   c->launches += launch_pcg_pupdate(c->pv, z, c->scal, F.d.ndof, c->st);
