@@ -111,7 +111,11 @@ def cpu_threads():
 # measured oracle wall time (s) of one setup + rhs + PCG solve of a config's recipe at
 # sub-mesh n (tools/c5_scaling_study.py, profiles/r02_c5_oracle_study.jsonl); the config-5
 # recipe's iteration count grows with n (32 / 114 / 217 at n = 16 / 32 / 64)
-ORACLE_SECONDS = {5: {16: 0.3, 32: 2.1, 64: 11.5, 128: 150.0}}
+# (8-core container, 2 BLAS threads; the box host measured 2-3x faster): the heterogeneous
+# recipes' iteration counts grow with n, so the config-2 scaling estimate does not hold there
+ORACLE_SECONDS = {3: {32: 1.5, 64: 8.8, 128: 54.0},
+                  4: {64: 3.0, 128: 13.5, 256: 69.9},
+                  5: {16: 0.3, 32: 2.1, 64: 11.5, 128: 150.0}}
 
 
 def oracle_sample_n(cfg, budget_s: float) -> int:

@@ -302,6 +302,16 @@ int mg_total_launch_count(const void* ctx, int64_t* launches);
 /* 1 (default): replay each PCG iteration as two captured CUDA graphs; 0: eager launches. */
 int mg_set_use_graphs(void* ctx, int32_t on);
 
+/* Debug / invariant mode: checks a set-up hierarchy on the device and fills
+ * report[4] (host): [0] max over every level's element maps of ||S_T 1||_inf / max|S_T| (the
+ * exact DtN maps annihilate constants; readings R5 / R10 make it rounding-
+ * level), [1] the number of NaN / Inf entries in the maps, edge-block inverses, orbit records
+ * and the coarsest inverse, [2] the relative L2 difference between the two-colour apply and
+ * an independent atomicAdd scatter apply on the finest level (-1: not run, partitioned or
+ * nonsymmetric contexts), [3] 0.  MG_ERR_STATE (with mg_last_error) if [0] > 1e-12, [1] > 0
+ * or [2] > 1e-13; synchronises the stream. */
+int mg_check_invariants(void* ctx, double* report);
+
 /* Execution options of a context (no effect on the arithmetic each kernel performs;
  * they select which kernel / how many CTAs run it, so that tests can drive every code
  * path at small sizes).  Drops the captured graphs.  MG_ERR_ARG for an unknown key.

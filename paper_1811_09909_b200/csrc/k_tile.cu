@@ -31,7 +31,9 @@
 
 namespace mgdtn {
 
-constexpr int SW_C = 64, SW_R = 2, SW_T = 2 * SW_C * SW_R, SW_W = SW_C + 4;   // staged row width
+// one element row of a 64-column strip per step; 4 threads per element (one per edge's
+// row block of the element map); 2 CTAs per SM
+constexpr int SW_C = 64, SW_R = 1, SW_T = 4 * SW_C * SW_R, SW_W = SW_C + 4;   // staged row width
 
 __device__ __forceinline__ uint32_t sw_smem(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -73,11 +75,11 @@ struct SweepCfg {
   static constexpr int DD = SMO ? 2 * SW_R * ROW : 0;       // d (Chebyshev)
   static constexpr int DS = SMO ? NCS * 2 * SW_R * SW_W : 0;   // [o][row][edge] D_e^-1 orbits
   static constexpr int STAGE = XH + XV + SS + SH + RR + DD + DS;
-  static constexpr int Y = 2 * OWN * K1;                    // lo / hi contributions
-  static constexpr int CARRY = 2 * SW_C * K1;               // top-edge contributions, 2 steps
-  static constexpr int budget = (216 * 1024) / 8 - Y - CARRY;
+  static constexpr int Y = 2 * OWN * K1;                    // lo / hi contributions (x2: by step)
+  static constexpr int CARRY = 3 * SW_C * K1;               // top-edge contributions, 3 steps
+  static constexpr int budget = (108 * 1024) / 8 - 2 * Y - CARRY;   // 2 CTAs per SM
   static constexpr int NS = budget / STAGE >= 4 ? 4 : budget / STAGE >= 3 ? 3 : 2;
-  static constexpr int DOUBLES = NS * STAGE + Y + CARRY;
+  static constexpr int DOUBLES = NS * STAGE + 2 * Y + CARRY;
   static constexpr int BYTES = DOUBLES * 8;
 };
 
@@ -85,8 +87,19 @@ struct SweepGeom {
   int nstrip, nseg, seg;   // strips of SW_C columns, segments of `seg` rows (multiple of SW_R)
 };
 
+// Warp-specialised: warp NCW (the producer) walks the CTA's steps ahead of the
+// consumers and fills the NS-stage ring -- bulk copies of the contiguous rows (one
+// lane per copy) plus 8-byte cp.async of the left halo element's orbit values, all
+// completing on the stage's "full" mbarrier -- after the consumers have released the
+// stage on its "empty" mbarrier.  The NCW consumer warps only wait for data: per step
+// they form the element contributions, meet at one named barrier, and finish the owned
+// edges.  The contribution slots are double-buffered and the row carry triple-buffered
+// by step, so one barrier per step orders everything (a warp passes the barrier of
+// step k only when every warp has finished the epilogue of step k-1).
+constexpr int SW_NCW = SW_T / 32;   // consumer warps
+
 template <int P, int MODE, bool DOT>
-__global__ void __launch_bounds__(SW_T, 1)
+__global__ void __launch_bounds__(SW_T + 32, 2)
     k_apply_sweep(const LevelDev L, SweepGeom G, const double* __restrict__ x, double* y,
                   const double* __restrict__ r, double* d, double* xo, int step,
                   double* __restrict__ partials) {
@@ -95,18 +108,19 @@ __global__ void __launch_bounds__(SW_T, 1)
   constexpr int K1 = P + 1, M = 4 * K1, NORB = D::NORB, NCS = D::NCS, NS = C::NS;
   constexpr int OWN = C::OWN, ROW = C::ROW;
   extern __shared__ __align__(128) double sm[];
-  double* Ylo = sm + NS * C::STAGE;   // [OWN][K1]: H (rr, c) at rr*SW_C + c, V at SW_R*SW_C + ...
-  double* Yhi = Ylo + OWN * K1;
-  double* carry = Yhi + OWN * K1;     // [2][SW_C][K1]
-  __shared__ __align__(8) uint64_t bars[NS];
-  __shared__ double red[SW_T / 32];
-  const int tid = threadIdx.x;
+  double* Ybuf = sm + NS * C::STAGE;    // [2][lo | hi][OWN][K1]
+  double* carry = Ybuf + 2 * C::Y;      // [3][SW_C][K1]
+  __shared__ __align__(8) uint64_t full[NS], empty[NS];
+  __shared__ double red[SW_NCW];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nx = L.nx, ny = L.ny;
   const int64_t nh = (int64_t)nx * (ny + 1);
   const int nwork = G.nstrip * G.nseg;
   if (tid == 0) {
-    for (int q = 0; q < NS; ++q)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sw_smem(&bars[q])));
+    for (int q = 0; q < NS; ++q) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 33;" ::"r"(sw_smem(&full[q])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sw_smem(&empty[q])), "r"(SW_NCW));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -118,8 +132,7 @@ __global__ void __launch_bounds__(SW_T, 1)
   }
   const bool cheb_d = MODE == AM_SMOOTH && L.smoother == 1 && step > 0;
   double dot = 0.0;
-  uint32_t phase = 0;   // parity bits of the stage barriers (bit q: stage q)
-  int gstep = 0;        // steps of this CTA so far (step k of a work item uses stage (gstep+k) % NS)
+  int g = 0;   // global step counter of this CTA: stage g % NS, phase (g / NS) & 1
   for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
     const int i0 = (w % G.nstrip) * SW_C, jb = (w / G.nstrip) * G.seg;
     const int je = min(ny, jb + G.seg);
@@ -127,121 +140,116 @@ __global__ void __launch_bounds__(SW_T, 1)
     const int nsteps = (je - j00 + SW_R - 1) / SW_R;
     const int lo_i = i0 > 0 ? i0 - 1 : 0;     // first staged column
     const int hi_i = min(i0 + SW_C + 1, nx + 1);
-    const int g0 = gstep;
-    // Copy idx of step k (0 bytes: none).  Order: x H rows, x V rows, orbit chunk
-    // records, r rows, d rows, D_e^-1 orbit rows.
-    auto copy_desc = [&](int k, int idx, double*& dst, const double*& src) -> uint32_t {
-      double* st = sm + ((g0 + k) % NS) * C::STAGE;
-      const int j0 = j00 + k * SW_R;
-      const bool pro = jb > 0 && k == 0;
-      if (idx <= SW_R) {   // x, horizontal rows j0 .. j0 + SW_R
-        const int rr = idx;
-        if (j0 + rr > ny) return 0;
-        const int64_t e0 = (int64_t)(j0 + rr) * nx + lo_i;
-        dst = st + rr * ROW;
-        src = x + (e0 & ~(int64_t)1) * K1;
-        return sw_bytes(e0, i0 + SW_C - lo_i, K1);
-      }
-      idx -= SW_R + 1;
-      if (idx < SW_R) {    // x, vertical rows
-        const int rr = idx;
-        if (j0 + rr >= ny) return 0;
-        const int64_t e0 = nh + (int64_t)(j0 + rr) * (nx + 1) + lo_i;
-        dst = st + C::XH + rr * ROW;
-        src = x + (e0 & ~(int64_t)1) * K1;
-        return sw_bytes(e0, hi_i - lo_i, K1);
-      }
-      idx -= SW_R;
-      if (idx < 2 * SW_R) {   // the strip row's chunk record of each colour
-        const int rr = idx >> 1, cl = idx & 1;
-        if (j0 + rr >= ny) return 0;
-        const int64_t q = ((int64_t)(j0 + rr) * (nx >> 1) + (i0 >> 1)) >> 5;
-        dst = st + C::XH + C::XV + (rr * 2 + cl) * NORB * 32;
-        src = L.So + ((int64_t)cl * L.nchunk + q) * NORB * 32;
-        return NORB * 256;
-      }
-      idx -= 2 * SW_R;
-      if (!C::R || pro) return 0;
-      const int nvec = C::SMO ? (cheb_d ? 2 + NCS : 1 + NCS) : 1;   // r, [d], D orbits
-      if (idx >= nvec * 2 * SW_R) return 0;
-      const int vq = idx / (2 * SW_R), row = idx % (2 * SW_R), hv = row / SW_R, rr = row % SW_R;
-      if (j0 + rr >= je) return 0;
-      const int64_t e0 = hv == 0 ? (int64_t)(j0 + rr) * nx + i0 : nh + (int64_t)(j0 + rr) * (nx + 1) + i0;
-      double* RR = st + C::XH + C::XV + C::SS + C::SH;
-      if (vq == 0) {
-        dst = RR + row * ROW;
-        src = r + (e0 & ~(int64_t)1) * K1;
-        return sw_bytes(e0, SW_C, K1);
-      }
-      if (C::SMO && cheb_d && vq == 1) {
-        dst = RR + C::RR + row * ROW;
-        src = d + (e0 & ~(int64_t)1) * K1;
-        return sw_bytes(e0, SW_C, K1);
-      }
-      const int o = vq - (cheb_d ? 2 : 1);
-      const int64_t f0 = (int64_t)o * L.nedge + e0;
-      dst = RR + C::RR + C::DD + (o * 2 * SW_R + row) * SW_W;
-      src = L.Dso + (f0 & ~(int64_t)1);
-      return sw_bytes(f0, SW_C, 1);
-    };
-    constexpr int NCOPY = (SW_R + 1) + SW_R + 2 * SW_R + (C::SMO ? (2 + NCS) : C::R ? 1 : 0) * 2 * SW_R;
-    // warp 0: one copy per lane; every lane registers its bytes with expect_tx, then
-    // lane 0 arrives, then the copies go out (no complete_tx can precede an expect_tx)
-    auto issue = [&](int k) {
-      if (k >= nsteps) return;
-      uint64_t* bar = &bars[(g0 + k) % NS];
-      const int lane = tid & 31;
-      double* dst[(NCOPY + 31) / 32];
-      const double* src[(NCOPY + 31) / 32];
-      uint32_t nb[(NCOPY + 31) / 32];
+    if (warp == SW_NCW) {
+      // ================================================================ producer
+      for (int k = 0; k < nsteps; ++k, ++g) {
+        const int sidx = g % NS;
+        if (g >= NS) sw_wait(&empty[sidx], ((g / NS) - 1) & 1);
+        double* st = sm + sidx * C::STAGE;
+        const int j0 = j00 + k * SW_R;
+        const bool pro = jb > 0 && k == 0;
+        // copy idx -> (dst, src, bytes); order: x H rows, x V rows, chunk records, r, d, D
+        auto copy_desc = [&](int idx, double*& dst, const double*& src) -> uint32_t {
+          if (idx <= SW_R) {
+            const int rr = idx;
+            if (j0 + rr > ny) return 0;
+            const int64_t e0 = (int64_t)(j0 + rr) * nx + lo_i;
+            dst = st + rr * ROW;
+            src = x + (e0 & ~(int64_t)1) * K1;
+            return sw_bytes(e0, i0 + SW_C - lo_i, K1);
+          }
+          idx -= SW_R + 1;
+          if (idx < SW_R) {
+            const int rr = idx;
+            if (j0 + rr >= ny) return 0;
+            const int64_t e0 = nh + (int64_t)(j0 + rr) * (nx + 1) + lo_i;
+            dst = st + C::XH + rr * ROW;
+            src = x + (e0 & ~(int64_t)1) * K1;
+            return sw_bytes(e0, hi_i - lo_i, K1);
+          }
+          idx -= SW_R;
+          if (idx < 2 * SW_R) {
+            const int rr = idx >> 1, cl = idx & 1;
+            if (j0 + rr >= ny) return 0;
+            const int64_t q = ((int64_t)(j0 + rr) * (nx >> 1) + (i0 >> 1)) >> 5;
+            dst = st + C::XH + C::XV + (rr * 2 + cl) * NORB * 32;
+            src = L.So + ((int64_t)cl * L.nchunk + q) * NORB * 32;
+            return NORB * 256;
+          }
+          idx -= 2 * SW_R;
+          if (!C::R || pro) return 0;
+          const int nvec = C::SMO ? (cheb_d ? 2 + NCS : 1 + NCS) : 1;
+          if (idx >= nvec * 2 * SW_R) return 0;
+          const int vq = idx / (2 * SW_R), row = idx % (2 * SW_R), hv = row / SW_R, rr = row % SW_R;
+          if (j0 + rr >= je) return 0;
+          const int64_t e0 = hv == 0 ? (int64_t)(j0 + rr) * nx + i0 : nh + (int64_t)(j0 + rr) * (nx + 1) + i0;
+          double* RR = st + C::XH + C::XV + C::SS + C::SH;
+          if (vq == 0) {
+            dst = RR + row * ROW;
+            src = r + (e0 & ~(int64_t)1) * K1;
+            return sw_bytes(e0, SW_C, K1);
+          }
+          if (C::SMO && cheb_d && vq == 1) {
+            dst = RR + C::RR + row * ROW;
+            src = d + (e0 & ~(int64_t)1) * K1;
+            return sw_bytes(e0, SW_C, K1);
+          }
+          const int o = vq - (cheb_d ? 2 : 1);
+          const int64_t f0 = (int64_t)o * L.nedge + e0;
+          dst = RR + C::RR + C::DD + (o * 2 * SW_R + row) * SW_W;
+          src = L.Dso + (f0 & ~(int64_t)1);
+          return sw_bytes(f0, SW_C, 1);
+        };
+        constexpr int NCOPY = (SW_R + 1) + SW_R + 2 * SW_R + (C::SMO ? (2 + NCS) : C::R ? 1 : 0) * 2 * SW_R;
+        constexpr int NU = (NCOPY + 31) / 32;
+        double* dsts[NU];
+        const double* srcs[NU];
+        uint32_t nb[NU];
+        uint32_t mine = 0;
 #pragma unroll
-      for (int u = 0; u < (NCOPY + 31) / 32; ++u) {
-        nb[u] = 0;
-        if (lane + 32 * u < NCOPY) nb[u] = copy_desc(k, lane + 32 * u, dst[u], src[u]);
-        if (nb[u]) asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(sw_smem(bar)),
-                                "r"(nb[u])
-                                : "memory");
-      }
-      __syncwarp();
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sw_smem(bar)) : "memory");
-      __syncwarp();
-#pragma unroll
-      for (int u = 0; u < (NCOPY + 31) / 32; ++u)
-        if (nb[u]) sw_bulk(dst[u], src[u], nb[u], bar);
-    };
-    // every thread: the left halo elements' orbit values (8-byte cp.async, one group
-    // per step); thread 0: the bulk copies
-    auto issue_all = [&](int k) {
-      if (k < nsteps && i0 > 0 && tid < SW_R * NORB) {
-        const int rr = tid / NORB, o = tid - rr * NORB, j = j00 + k * SW_R + rr;
-        double* dst = sm + ((g0 + k) % NS) * C::STAGE + C::XH + C::XV + C::SS + tid;
-        const double* src = L.So;
-        const bool v = j < je;
-        if (v) {
-          int colour;
-          int64_t s;
-          elem_slot(nx, i0 - 1, j, colour, s);
-          src = L.So + ((((int64_t)colour * L.nchunk + (s >> 5)) * NORB + o) << 5) + (s & 31);
+        for (int u = 0; u < NU; ++u) {
+          nb[u] = 0;
+          if (lane + 32 * u < NCOPY) nb[u] = copy_desc(lane + 32 * u, dsts[u], srcs[u]);
+          mine += nb[u];
         }
-        const uint32_t da = sw_smem(dst);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(da), "l"(src),
-                     "r"(v ? 8 : 0)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sw_smem(&full[sidx])),
+                       "r"(mine)
+                       : "memory");
+        __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+        for (int u = 0; u < NU; ++u)
+          if (nb[u]) sw_bulk(dsts[u], srcs[u], nb[u], &full[sidx]);
+        // the left halo element's orbit values (scattered: 8-byte cp.async)
+        if (!pro && i0 > 0) {
+          for (int q = lane; q < SW_R * NORB; q += 32) {
+            const int rr = q / NORB, o = q - rr * NORB, j = j0 + rr;
+            const bool v = j < je;
+            const double* src = L.So;
+            if (v) {
+              int colour;
+              int64_t s;
+              elem_slot(nx, i0 - 1, j, colour, s);
+              src = L.So + ((((int64_t)colour * L.nchunk + (s >> 5)) * NORB + o) << 5) + (s & 31);
+            }
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                             sw_smem(st + C::XH + C::XV + C::SS + q)),
+                         "l"(src), "r"(v ? 8 : 0)
+                         : "memory");
+          }
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(sw_smem(&full[sidx]))
                      : "memory");
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      if (tid < 32) issue(k);
-    };
-    __syncthreads();   // the previous work item's readers of the ring are done
-    if (tid < 32) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    for (int k = 0; k < NS - 1; ++k) issue_all(k);
-#pragma unroll 1
-    for (int k = 0; k < nsteps; ++k) {
-      issue_all(k + NS - 1);
-      const int sidx = (g0 + k) % NS;
-      asm volatile("cp.async.wait_group %0;" ::"n"(NS - 1) : "memory");
-      sw_wait(&bars[sidx], (phase >> sidx) & 1u);
-      phase ^= 1u << sidx;
-      __syncthreads();   // the halo values of every thread are visible
+      continue;
+    }
+    // ================================================================ consumers
+    for (int k = 0; k < nsteps; ++k, ++g) {
+      const int sidx = g % NS;
+      sw_wait(&full[sidx], (g / NS) & 1);
       const double* st = sm + sidx * C::STAGE;
       const double* XH = st;
       const double* XV = XH + C::XH;
@@ -252,29 +260,26 @@ __global__ void __launch_bounds__(SW_T, 1)
       const double* DS = DD + C::DD;
       const int j0 = j00 + k * SW_R;
       const bool pro = jb > 0 && k == 0;
-      const double* cold = carry + (k & 1) * SW_C * K1;
-      double* cnew = carry + ((k + 1) & 1) * SW_C * K1;
-      // staged edge position of H(i, j0+rr) / V(i, j0+rr): i - i0 + hoff / voff[rr]
+      double* Ylo = Ybuf + (g & 1) * C::Y;
+      double* Yhi = Ylo + OWN * K1;
+      const double* cold = carry + (g % 3) * SW_C * K1;
+      double* cnew = carry + ((g + 1) % 3) * SW_C * K1;
+      // staged edge position of H(i, j0) / V(i, j0): i - i0 + hoff / voff
       const int hoff = (int)((lo_i + (int64_t)j0 * nx) & 1) + (i0 - lo_i);   // nx even: every row
-      int voff[SW_R];
-#pragma unroll
-      for (int rr = 0; rr < SW_R; ++rr)
-        voff[rr] = (int)((nh + (int64_t)(j0 + rr) * (nx + 1) + lo_i) & 1) + (i0 - lo_i);
-      // ---- elements: two threads per element, each forming the rows of two of its
-      // edges (h = 0: bottom, right; h = 1: top, left): y_f = S_T[f, :] x_T.  A warp
-      // holds 32 elements of one colour of a row, so its orbit reads are one
-      // conflict-free 256-byte row of the chunk record.
+      const int voff = (int)((nh + (int64_t)j0 * (nx + 1) + lo_i) & 1) + (i0 - lo_i);
+      // ---- elements: four threads per element, thread f forming the row block of edge f,
+      // y_f = S_T[f, :] x_T.  A warp holds one edge role of the 32 elements of one colour
+      // of the row, so its orbit reads are one conflict-free 256-byte row of the record.
       {
-        const int h = tid / (SW_T / 2), ew = tid % (SW_T / 2);
-        const int rr = ew / SW_C, col = (ew % SW_C) / 32, l = ew % 32;
-        const int j = j0 + rr;
-        const int cc = 2 * l + ((col + j) & 1), i = i0 + cc;
+        const int f = warp >> 1, col = warp & 1;
+        const int j = j0;
+        const int cc = 2 * lane + ((col + j) & 1), i = i0 + cc;
         if (j < je) {
           double xv[M];
-          const double* xb = XH + rr * ROW + (cc + hoff) * K1;         // H(i, j)
-          const double* xt = XH + (rr + 1) * ROW + (cc + hoff) * K1;   // H(i, j+1)
-          const double* xl = XV + rr * ROW + (cc + voff[rr]) * K1;     // V(i, j)
-          const double* xr = xl + K1;                                  // V(i+1, j)
+          const double* xb = XH + (cc + hoff) * K1;         // H(i, j)
+          const double* xt = XH + ROW + (cc + hoff) * K1;   // H(i, j+1)
+          const double* xl = XV + (cc + voff) * K1;         // V(i, j)
+          const double* xr = xl + K1;                       // V(i+1, j)
           const bool mb = j == 0, mt = j + 1 == ny, ml = i == 0, mr = i + 1 == nx;   // dOmega
 #pragma unroll
           for (int a = 0; a < K1; ++a) {
@@ -283,51 +288,41 @@ __global__ void __launch_bounds__(SW_T, 1)
             xv[2 * K1 + a] = mt ? 0.0 : xt[a];
             xv[3 * K1 + a] = ml ? 0.0 : xl[a];
           }
-          const double* Sp = SS + (rr * 2 + col) * NORB * 32 + l;
-          double yv[2 * K1];
-          const int hq = (rr * SW_C + cc) * K1, vq = ((SW_R + rr) * SW_C + cc) * K1;
-          if (h == 0) {
+          const double* Sp = SS + col * NORB * 32 + lane;
+          double yv[K1];
+#define SW_ROWS(FF)                                                                   \
+  _Pragma("unroll") for (int a = 0; a < K1; ++a) {                                    \
+    double acc = 0.0;                                                                 \
+    _Pragma("unroll") for (int b = 0; b < M; ++b)                                     \
+        acc = fma(Sp[D::orb(D::pk((FF) * K1 + a, b)) * 32], xv[b], acc);              \
+    yv[a] = acc;                                                                      \
+  }
+          if (f == 0) { SW_ROWS(0) } else if (f == 1) { SW_ROWS(1) }
+          else if (f == 2) { SW_ROWS(2) } else { SW_ROWS(3) }
+#undef SW_ROWS
+          if (f == 2) {   // top edge: the next step's bottom row (carry)
 #pragma unroll
-            for (int q = 0; q < 2 * K1; ++q) {
-              double acc = 0.0;
+            for (int a = 0; a < K1; ++a) cnew[cc * K1 + a] = yv[a];
+          } else if (!pro) {
+            double* dst = f == 0 ? Yhi + cc * K1                                  // bottom edge
+                        : f == 3 ? Yhi + (SW_C + cc) * K1                         // left edge
+                        : (cc + 1 < SW_C ? Ylo + (SW_C + cc + 1) * K1 : nullptr);  // right edge
+            if (dst) {
 #pragma unroll
-              for (int b = 0; b < M; ++b) acc = fma(Sp[D::orb(D::pk(q, b)) * 32], xv[b], acc);
-              yv[q] = acc;
-            }
-            if (!pro) {
-#pragma unroll
-              for (int a = 0; a < K1; ++a) {
-                Yhi[hq + a] = yv[a];                                           // bottom edge
-                if (cc + 1 < SW_C) Ylo[vq + K1 + a] = yv[K1 + a];             // right edge, inside
-              }
-            }
-          } else {
-#pragma unroll
-            for (int q = 0; q < 2 * K1; ++q) {
-              double acc = 0.0;
-#pragma unroll
-              for (int b = 0; b < M; ++b)
-                acc = fma(Sp[D::orb(D::pk(2 * K1 + q, b)) * 32], xv[b], acc);
-              yv[q] = acc;
-            }
-#pragma unroll
-            for (int a = 0; a < K1; ++a) {
-              if (rr + 1 < SW_R) Ylo[hq + SW_C * K1 + a] = yv[a];   // top edge, next row
-              else cnew[cc * K1 + a] = yv[a];                       // top edge, next step
-              if (!pro) Yhi[vq + a] = yv[K1 + a];                   // left edge
+              for (int a = 0; a < K1; ++a) dst[a] = yv[a];
             }
           }
         }
-        // the left neighbour strip's element (i0-1, j): row block of its right edge,
+        // the left neighbour strip's element (i0-1, j0): row block of its right edge,
         // one thread per row (orbit values staged in SH)
-        if (!pro && i0 > 0 && tid < SW_R * K1 && j0 + tid / K1 < je) {
-          const int hr = tid / K1, a = tid % K1, jh = j0 + hr, ih = i0 - 1;
+        if (!pro && i0 > 0 && tid < K1 && j0 < je) {
+          const int a = tid, ih = i0 - 1;
           double xv[M];
-          const double* xb = XH + hr * ROW + (hoff - 1) * K1;
-          const double* xt = XH + (hr + 1) * ROW + (hoff - 1) * K1;
-          const double* xl = XV + hr * ROW + (voff[hr] - 1) * K1;
+          const double* xb = XH + (hoff - 1) * K1;
+          const double* xt = XH + ROW + (hoff - 1) * K1;
+          const double* xl = XV + (voff - 1) * K1;
           const double* xr = xl + K1;
-          const bool mb = jh == 0, mt = jh + 1 == ny, ml = ih == 0;
+          const bool mb = j0 == 0, mt = j0 + 1 == ny, ml = ih == 0;
 #pragma unroll
           for (int q = 0; q < K1; ++q) {
             xv[0 * K1 + q] = mb ? 0.0 : xb[q];
@@ -335,28 +330,26 @@ __global__ void __launch_bounds__(SW_T, 1)
             xv[2 * K1 + q] = mt ? 0.0 : xt[q];
             xv[3 * K1 + q] = ml ? 0.0 : xl[q];
           }
-          const double* Sh = SH + hr * NORB;
           double acc = 0.0;
 #pragma unroll
           for (int b = 0; b < M; ++b) {
-            // row K1 + a of the packed map: orbit of (K1 + a, b), a runtime a
             int o = 0;
 #pragma unroll
             for (int q = 0; q < K1; ++q)
               if (q == a) o = D::orb(D::pk(K1 + q, b));
-            acc = fma(Sh[o], xv[b], acc);
+            acc = fma(SH[o], xv[b], acc);
           }
-          Ylo[((SW_R + hr) * SW_C) * K1 + a] = acc;
+          Ylo[SW_C * K1 + a] = acc;
         }
       }
-      __syncthreads();
+      asm volatile("bar.sync 1, %0;" ::"n"(SW_T) : "memory");   // consumers only
       // ---- owned edges (thread per edge): y_e = lo + hi, then the epilogue
       if (!pro) {
         for (int q = tid; q < OWN + SW_R + SW_C; q += SW_T) {
           int64_t e;
           bool bnd;
           const double* xs = nullptr;
-          int ro = 0, dro = 0;   // staged positions in the r / d rows and the D rows
+          int ro = 0;   // staged position in the r / d rows and the D rows
           double yy[K1];
           if (q >= OWN) {   // the mesh's right / top boundary edges next to this step
             const int u = q - OWN;
@@ -369,52 +362,48 @@ __global__ void __launch_bounds__(SW_T, 1)
             }
             bnd = true;
           } else {
-            const int hv = q / (SW_R * SW_C), rr = (q / SW_C) % SW_R, cc = q % SW_C;
-            const int i = i0 + cc, j = j0 + rr;
+            const int hv = q / SW_C, cc = q % SW_C;
+            const int i = i0 + cc, j = j0;
             if (j >= je) continue;
             int64_t e0;
             if (hv == 0) {
               e0 = (int64_t)j * nx + i0;
-              e = e0 + cc;
               bnd = j == 0;
-              xs = XH + rr * ROW + (cc + hoff) * K1;
+              xs = XH + (cc + hoff) * K1;
             } else {
               e0 = nh + (int64_t)j * (nx + 1) + i0;
-              e = e0 + cc;
               bnd = i == 0;
-              xs = XV + rr * ROW + (cc + voff[rr]) * K1;
+              xs = XV + (cc + voff) * K1;
             }
-            const int sh = cc + (int)(e0 & 1);   // r / d rows start at e0 & ~1
-            ro = (hv * SW_R + rr) * SW_W + sh;
-            dro = (hv * SW_R + rr) * SW_W + sh;   // D rows: o*nedge is even, same parity
+            e = e0 + cc;
+            ro = hv * SW_W + cc + (int)(e0 & 1);   // rows start at e0 & ~1 (D rows: same parity)
             if (!bnd) {
-              const double* lo = (hv == 0 && rr == 0) ? cold + cc * K1 : Ylo + q * K1;
+              const double* lo = hv == 0 ? cold + cc * K1 : Ylo + q * K1;
 #pragma unroll
               for (int a = 0; a < K1; ++a) yy[a] = lo[a] + Yhi[q * K1 + a];
             }
           }
           const int64_t base = e * K1;
+          double out[K1];
           if (bnd) {   // dOmega: y = 0; the smoothed iterate keeps 0 there
-            if (MODE == AM_SMOOTH) {
 #pragma unroll
-              for (int a = 0; a < K1; ++a) xo[base + a] = 0.0;
-            } else {
-#pragma unroll
-              for (int a = 0; a < K1; ++a) y[base + a] = 0.0;
-            }
+            for (int a = 0; a < K1; ++a) out[a] = 0.0;
+            st_edge<K1>((MODE == AM_SMOOTH ? xo : y) + base, out);
             continue;
           }
           if (MODE == AM_APPLY) {
 #pragma unroll
             for (int a = 0; a < K1; ++a) {
-              y[base + a] = yy[a];
+              out[a] = yy[a];
               if (DOT) dot = fma(xs[a], yy[a], dot);
             }
+            st_edge<K1>(y + base, out);
           } else if (MODE == AM_RESID) {
 #pragma unroll
-            for (int a = 0; a < K1; ++a) y[base + a] = RR[ro * K1 + a] - yy[a];
+            for (int a = 0; a < K1; ++a) out[a] = RR[ro * K1 + a] - yy[a];
+            st_edge<K1>(y + base, out);
           } else {   // AM_SMOOTH: res = r - A x, dn = c2 D^-1 res (+ c1 d), d = dn, xo = x + dn
-            double res[K1];
+            double res[K1], dn[K1];
 #pragma unroll
             for (int a = 0; a < K1; ++a) res[a] = RR[ro * K1 + a] - yy[a];
 #pragma unroll
@@ -422,30 +411,29 @@ __global__ void __launch_bounds__(SW_T, 1)
               double cc2 = 0.0;
 #pragma unroll
               for (int b = 0; b < K1; ++b)
-                cc2 = fma(DS[D::cs(D::pe(a, b)) * 2 * SW_R * SW_W + dro], res[b], cc2);
-              double dn = c2 * cc2;
-              if (L.smoother == 1) {
-                if (step > 0) dn = fma(c1, DD[ro * K1 + a], dn);
-                d[base + a] = dn;
-              }
-              xo[base + a] = xs[a] + dn;
+                cc2 = fma(DS[D::cs(D::pe(a, b)) * 2 * SW_R * SW_W + ro], res[b], cc2);
+              dn[a] = c2 * cc2;
+              if (L.smoother == 1 && step > 0) dn[a] = fma(c1, DD[ro * K1 + a], dn[a]);
+              out[a] = xs[a] + dn[a];
             }
+            if (L.smoother == 1) st_edge<K1>(d + base, dn);
+            st_edge<K1>(xo + base, out);
           }
         }
       }
-      __syncthreads();   // stage sidx and Ylo / Yhi / carry are free again
-      if (tid < 32) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sw_smem(&empty[sidx])) : "memory");
     }
-    gstep += nsteps;
   }
-  if (DOT) {
+  if (DOT && warp < SW_NCW) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-    if ((tid & 31) == 0) red[tid >> 5] = dot;
-    __syncthreads();
+    if (lane == 0) red[warp] = dot;
+    asm volatile("bar.sync 1, %0;" ::"n"(SW_T) : "memory");
     if (tid == 0) {
       double s = 0.0;
-      for (int w = 0; w < SW_T / 32; ++w) s += red[w];
+      for (int q = 0; q < SW_NCW; ++q) s += red[q];
       partials[blockIdx.x] = s;
     }
   }
@@ -467,7 +455,7 @@ static int sweep_sms() {
 static SweepGeom sweep_geom(const LevelDev& L) {
   SweepGeom g;
   g.nstrip = (L.nx + SW_C - 1) / SW_C;
-  const int want = 4 * sweep_sms();
+  const int want = 8 * sweep_sms();
   int seg = (int)(((int64_t)L.ny * g.nstrip + want - 1) / want);
   seg = ((seg + SW_R - 1) / SW_R) * SW_R;
   if (seg < 8 * SW_R) seg = 8 * SW_R;
@@ -492,7 +480,7 @@ int apply_tile_grid(const LevelDev& L) {
   const SweepGeom g = sweep_geom(L);
   int n = g.nstrip * g.nseg;
   if (L.grid_cap > 0 && n > L.grid_cap) n = L.grid_cap;
-  return n < sweep_sms() ? n : sweep_sms();
+  return n < 2 * sweep_sms() ? n : 2 * sweep_sms();   // 2 resident CTAs per SM
 }
 
 template <int P, int MODE, bool DOT>
@@ -505,7 +493,7 @@ static void launch_sweep_t(const LevelDev& L, const double* x, double* y, const 
                          C::BYTES);
     attr = true;
   }
-  launch_ex(k_apply_sweep<P, MODE, DOT>, apply_tile_grid(L), SW_T, (size_t)C::BYTES, true, st, L,
+  launch_ex(k_apply_sweep<P, MODE, DOT>, apply_tile_grid(L), SW_T + 32, (size_t)C::BYTES, true, st, L,
             sweep_geom(L), x, y, r, d, xo, step, partials);
 }
 

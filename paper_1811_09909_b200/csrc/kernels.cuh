@@ -371,6 +371,11 @@ int launch_dinv_pack(const LevelDev& L, cudaStream_t st);   // Dinv (SoA) -> Dc 
 // orbit storage of a D4-invariant level (R9): the packed maps are replaced by their orbit
 // averages (in place) and the orbit values written to So
 int launch_orbit_pack(const LevelDev& L, cudaStream_t st);
+// invariant checks (k_debug.cu, mg_check_invariants): out[0] = max ||S_T 1|| / max|S_T|,
+// out[1] += non-finite entries; an atomicAdd scatter apply (y zero on entry)
+int launch_check_maps(const LevelDev& L, double* out, cudaStream_t st);
+int launch_check_finite(const double* v, int64_t n, double* out, cudaStream_t st);
+int launch_apply_atomic(const LevelDev& L, const double* x, double* y, cudaStream_t st);
 // R10: P S P (P = I - 11^T/8) on every map of a symmetric p = 1 level (k_setup.cu)
 int launch_project_const(const LevelDev& L, cudaStream_t st);
 int launch_dense_to_packed(const LevelDev& L, const double* src, cudaStream_t st);

@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/mgdtn.h"
 #include "comm.h"
 #include "d4.cuh"
@@ -122,6 +124,24 @@ struct Ctx {
 };
 
 static bool partitioned(const Ctx* c) { return c->nranks > 1; }
+
+// NVTX ranges (nsys / ncu --nvtx): the setup, every level of a V-cycle (its smoothing,
+// residual and transfers) and every PCG iteration of the host-driven loops.  Host-side
+// markers: inside a captured graph they mark the capture, and the replays run unmarked.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+struct LevelNames {
+  char buf[64][24];
+  LevelNames() {
+    for (int k = 0; k < 64; ++k) std::snprintf(buf[k], sizeof(buf[k]), "mg/vcycle/li%d", k);
+  }
+};
+static const char* level_range_name(int li) {
+  static const LevelNames names;   // thread-safe initialisation (virtual ranks are threads)
+  return names.buf[li < 0 ? 0 : li > 63 ? 63 : li];
+}
 
 static int fail(Ctx* c, int code, const std::string& msg, long long idx = -1) {
   if (c) {
@@ -766,6 +786,7 @@ static void prolong_level(Ctx* c, int li, const double* ec, double* e) {
 // restriction share one residual: Q_{k-1} A_k T_k = 0, so Q(r - A e2) equals
 // Q(r - A e1).
 static double* vcycle_level(Ctx* c, int li, bool first_done) {
+  NvtxRange nv(level_range_name(li));
   HostLevel& L = c->lev[li];
   const int nlev = (int)c->lev.size();
   const bool tail_ok = c->sm.kind != MG_SMOOTH_LUSGS;   // the tail kernels have no LU-SGS
@@ -960,6 +981,7 @@ static bool same_smoother(const mg_smoother_cfg& a, const mg_smoother_cfg& b) {
 // graph on one GPU (its ~300 launches cost one graph launch of host time; the forked
 // smoother setups become parallel graph branches), eager otherwise
 static int setup_impl(Ctx* c, const double* K, const int8_t* method, const double* tau) {
+  NvtxRange nv("mg/setup");
   cudaStream_t st = c->st;
   CK(cudaMemsetAsync(c->err, 0, sizeof(DevError), st));
   HostLevel& F = c->lev[0];
@@ -1213,6 +1235,7 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
   if (gpart && !c->gPA) RC(capture(false, &c->gPA, &c->nPA));
   if (gpart && !c->gPBA) RC(capture(true, &c->gPBA, &c->nPBA));
   for (it = 1; it <= maxit; ++it) {
+    NvtxRange nv_it("mg/pcg/iteration");
     if (gpart) {
       CK(cudaGraphLaunch(it == 1 ? c->gPA : c->gPBA, st));
       c->launches += it == 1 ? c->nPA : c->nPBA;
@@ -2100,6 +2123,59 @@ int mg_total_launch_count(const void* ctx, int64_t* launches) {
   const Ctx* c = static_cast<const Ctx*>(ctx);
   if (!c || !launches) return MG_ERR_ARG;
   *launches = c->launches;
+  return MG_OK;
+}
+
+int mg_check_invariants(void* ctx, double* report) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !report) return MG_ERR_ARG;
+  if (!c->setup_done) return fail(c, MG_ERR_STATE, "setup first");
+  cudaStream_t st = c->st;
+  double* out = c->part;   // [0] worst constant-mode ratio, [1] non-finite count
+  CK(cudaMemsetAsync(out, 0, 2 * sizeof(double), st));
+  const int nlev = (int)c->lev.size();
+  for (int li = 0; li < nlev; ++li) {
+    const HostLevel& L = c->lev[li];
+    c->launches += launch_check_maps(L.d, out, st);
+    if (li < nlev - 1)
+      c->launches += launch_check_finite(L.d.Dinv, L.d.nedge * L.d.k1 * L.d.k1, out, st);
+    if (L.d.orb) {
+      c->launches += launch_check_finite(L.d.So, (int64_t)2 * L.d.nchunk * d4_norb(L.d.p) * 32, out, st);
+      c->launches += launch_check_finite(L.d.Dso, L.d.nedge * d4_ncs(L.d.p), out, st);
+    }
+  }
+  c->launches += launch_check_finite(c->A1inv, (int64_t)c->nf * c->nf, out, st);
+  CK(cudaMemcpyAsync(c->pinned, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  RC(sync_st(c, st));
+  report[0] = c->pinned[0];
+  report[1] = c->pinned[1];
+  report[2] = -1.0;
+  report[3] = 0.0;
+  // the two-colour apply against an atomic scatter on the finest level (one GPU)
+  if (!partitioned(c) && !c->ns) {
+    HostLevel& F = c->lev[0];
+    const int64_t n = F.d.ndof;
+    const int vg = vec_grid(n);
+    c->launches += launch_pow_init(F.d, c->pv, st);   // deterministic v_i = 1 + (i mod 7)/7
+    apply_full(c, F, c->pv, c->ap, nullptr);
+    CK(cudaMemsetAsync(F.w, 0, n * sizeof(double), st));
+    c->launches += launch_apply_atomic(F.d, c->pv, F.w, st);
+    c->launches += launch_axpby(1.0, F.w, -1.0, c->ap, F.w, n, st);   // w = atomic - coloured
+    c->launches += launch_dot(F.w, F.w, n, c->part, vg, st);
+    c->launches += launch_reduce(c->part, vg, c->sscal, 10, 0, nullptr, st);
+    c->launches += launch_dot(c->ap, c->ap, n, c->part, vg, st);
+    c->launches += launch_reduce(c->part, vg, c->sscal, 11, 0, nullptr, st);
+    CK(cudaMemsetAsync(F.w, 0, n * sizeof(double), st));   // the work vector holds 0 on dOmega
+    CK(cudaMemcpyAsync(c->pinned, c->sscal + 10, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    RC(sync_st(c, st));
+    report[2] = c->pinned[1] > 0 ? std::sqrt(c->pinned[0] / c->pinned[1]) : 0.0;
+  }
+  CK(cudaGetLastError());
+  if (report[1] > 0) return fail(c, MG_ERR_STATE, "invariants: non-finite entries in the hierarchy");
+  if (report[0] > 1e-12)
+    return fail(c, MG_ERR_STATE, "invariants: an element map does not annihilate constants");
+  if (report[2] > 1e-13)
+    return fail(c, MG_ERR_STATE, "invariants: coloured apply differs from the atomic scatter");
   return MG_OK;
 }
 

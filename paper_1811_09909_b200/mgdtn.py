@@ -82,6 +82,7 @@ _SIGS = {
     "mg_total_launch_count": [_P, C.POINTER(C.c_int64)],
     "mg_set_use_graphs": [_P, C.c_int32],
     "mg_set_option": [_P, C.c_int32, C.c_int64],
+    "mg_check_invariants": [_P, _P],
     "mg_partition_plan": [C.POINTER(mg_quad_mesh), C.c_int32, C.c_int32, C.POINTER(mg_partition),
                           C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), _P],
     "mg_partition_side_edges": [C.POINTER(mg_quad_mesh), C.c_int32, C.c_int32,
@@ -520,6 +521,13 @@ class MGSolver:
         self._chk(self.lib.mg_set_use_graphs(self.ctx, int(on)), "mg_set_use_graphs")
 
     OPT_SWEEP, OPT_APPLY_GRID_CAP, OPT_COMM_TIMEOUT_MS = 1, 2, 3
+
+    def check_invariants(self):
+        """mg_check_invariants: dict(const_mode, nonfinite, atomic_apply_diff); raises MGError
+        if an invariant fails."""
+        rep = (C.c_double * 4)()
+        self._call("mg_check_invariants", rep)
+        return dict(const_mode=rep[0], nonfinite=rep[1], atomic_apply_diff=rep[2])
 
     def set_option(self, key: int, value: int):
         """mg_set_option: execution options (kernel choice / grid size) for tests."""

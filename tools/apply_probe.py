@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--op", default="apply", choices=["apply", "smooth"],
                     help="smooth: one fine smoothing step through mg_smooth (apply + D^-1 epilogue, "
                          "plus mg_smooth's two masked input copies and one output copy)")
+    ap.add_argument("--sweep", type=int, default=0, help="mg_set_option MG_OPT_SWEEP")
+    ap.add_argument("--steps", type=int, default=1, help="smoothing steps per probe (--op smooth)")
     ap.add_argument("--scheme", default="config", choices=["config", "nipg", "iipg", "tiles"],
                     help="nonsymmetric context with IIPG-H / NIPG-H elements (full-storage apply)")
     a = ap.parse_args()
@@ -41,6 +43,8 @@ def main():
         if ns:
             sm.kind = 0
         s.setup(pr.K, pr.method, pr.tau, sm)
+        if a.sweep:
+            s.set_option(s.OPT_SWEEP, a.sweep)
         lev = a.level or s.nlevels
         nd = s.ndof(lev)
         x = torch.rand(nd, dtype=torch.float64, device=dev)
@@ -56,7 +60,7 @@ def main():
             if a.op == "apply":
                 s.apply(lev, x, y)
             else:
-                s.smooth(lev, x, y, 1)
+                s.smooth(lev, x, y, a.steps)
             torch.cuda.nvtx.range_pop()
             e1.record(st)
             torch.cuda.synchronize()

@@ -14,6 +14,11 @@ and reports the relative L2 difference of each against base.  A GPU / oracle gap
 or below the 'ulp' floor is the oracle's own rounding, not a GPU error.
 
     python tools/vcycle_floor.py 2:64,2:128,2:256,5:64,5:128 > profiles/r02_vcycle_floor.jsonl
+
+The last three columns compare evaluation orders of the hierarchy itself: global vs per-macro
+Galerkin product (both FP64, same maps), per-macro without vs with reading R10, and R10 with
+the Schur complement by solve vs explicit inverse -- the reproducibility of a V-cycle with
+and without the per-level constant-mode projection.
 """
 import json
 import os
@@ -57,6 +62,24 @@ def main(spec):
         for label in ("ulp", "proj"):
             out[f"apply_{label}"] = rel(res[label][0], res["base"][0])
             out[f"vcycle_{label}"] = rel(res[label][1], res["base"][1])
+        # two valid FP64 evaluation orders of the same hierarchy on the projected maps:
+        # the global sparse Galerkin product vs macro by macro (Prop. DtN), each without and
+        # with R10 (every coarse level projected onto S.1 = 0), and R10 with the Schur
+        # complement through an explicit inverse instead of a solve
+        Sp = project_maps(ts.S, c.p)
+        A = assembly.assemble_full(n, c.p, Sp)[ts.free][:, ts.free].tocsr()
+        kw = dict(smoother=c.smoother, nu_pre=c.nu, nu_post=c.nu)
+        z = {
+            "global": multigrid.Hierarchy(A, n, c.p, **kw).vcycle(r),
+            "macro": multigrid.Hierarchy(A, n, c.p, **kw, element_maps=Sp, galerkin="macro").vcycle(r),
+            "macro_r10": multigrid.Hierarchy(A, n, c.p, **kw, element_maps=Sp, galerkin="macro",
+                                             project_levels=True).vcycle(r),
+            "macro_r10_inv": multigrid.Hierarchy(A, n, c.p, **kw, element_maps=Sp, galerkin="macro",
+                                                 project_levels=True, schur_inv=True).vcycle(r),
+        }
+        out["vcycle_global_vs_macro"] = rel(z["macro"], z["global"])
+        out["vcycle_macro_vs_macro_r10"] = rel(z["macro_r10"], z["macro"])
+        out["vcycle_r10_solve_vs_inv"] = rel(z["macro_r10_inv"], z["macro_r10"])
         print(json.dumps(out), flush=True)
 
 
