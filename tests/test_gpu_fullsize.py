@@ -189,7 +189,14 @@ def test_fullsize_pcg(full):
     # the recursive residual (the stopping test) drifts from the
     # true one over many iterations on ill-conditioned systems (config 3: ~1270
     # iterations at contrast 1e6); the oracle's PCG drifts the same way
-    path = os.path.join(ROOT, "tests", "golden", f"fullsize_oracle_c{c.index}.json")
+    # the oracle under the GPU's storage readings R5 / R9 / R10 where that golden exists
+    # (tools/make_fullsize_golden.py --r10): each projection is onto a subspace holding the
+    # exact maps, and on the ill-conditioned heterogeneous recipes they move a converged
+    # solution by more than the operator's 1-ulp noise floor (config 3: 9.6e-11,
+    # profiles/r02_noise_floor_c3.json; GPU vs the plain oracle 1.3e-9 after 1270 iterations)
+    path = os.path.join(ROOT, "tests", "golden", f"fullsize_oracle_c{c.index}_r10.json")
+    if not os.path.exists(path):
+        path = os.path.join(ROOT, "tests", "golden", f"fullsize_oracle_c{c.index}.json")
     if not os.path.exists(path):
         # no oracle run at this size: the finite-precision CG residual gap bound
         # (Greenbaum, "Iterative methods for solving linear systems", 1997, ch. 7.3: ||g - A x_k - r_k|| <= eps O(k) ||A|| max_j ||x_j||,
