@@ -34,6 +34,7 @@ namespace mgdtn {
 // one element row of a 64-column strip per step; 4 threads per element (one per edge's
 // row block of the element map); 2 CTAs per SM
 constexpr int SW_C = 64, SW_R = 1, SW_T = 4 * SW_C * SW_R, SW_W = SW_C + 4;   // staged row width
+constexpr int SW_CPS = 2;   // CTAs per SM (SW_R = 2 with 1 CTA per SM: 1052 ms vs 1022 ms per 30 c5 iterations)
 
 __device__ __forceinline__ uint32_t sw_smem(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -77,7 +78,7 @@ struct SweepCfg {
   static constexpr int STAGE = XH + XV + SS + SH + RR + DD + DS;
   static constexpr int Y = 2 * OWN * K1;                    // lo / hi contributions (x2: by step)
   static constexpr int CARRY = 3 * SW_C * K1;               // top-edge contributions, 3 steps
-  static constexpr int budget = (108 * 1024) / 8 - 2 * Y - CARRY;   // 2 CTAs per SM
+  static constexpr int budget = (216 * 1024 / SW_CPS) / 8 - 2 * Y - CARRY;
   static constexpr int NS = budget / STAGE >= 4 ? 4 : budget / STAGE >= 3 ? 3 : 2;
   static constexpr int DOUBLES = NS * STAGE + 2 * Y + CARRY;
   static constexpr int BYTES = DOUBLES * 8;
@@ -99,7 +100,7 @@ struct SweepGeom {
 constexpr int SW_NCW = SW_T / 32;   // consumer warps
 
 template <int P, int MODE, bool DOT>
-__global__ void __launch_bounds__(SW_T + 32, 2)
+__global__ void __launch_bounds__(SW_T + 32, SW_CPS)
     k_apply_sweep(const LevelDev L, SweepGeom G, const double* __restrict__ x, double* y,
                   const double* __restrict__ r, double* d, double* xo, int step,
                   double* __restrict__ partials) {
@@ -264,22 +265,25 @@ __global__ void __launch_bounds__(SW_T + 32, 2)
       double* Yhi = Ylo + OWN * K1;
       const double* cold = carry + (g % 3) * SW_C * K1;
       double* cnew = carry + ((g + 1) % 3) * SW_C * K1;
-      // staged edge position of H(i, j0) / V(i, j0): i - i0 + hoff / voff
+      // staged edge position of H(i, j0+rr) / V(i, j0+rr): i - i0 + hoff / voff[rr]
       const int hoff = (int)((lo_i + (int64_t)j0 * nx) & 1) + (i0 - lo_i);   // nx even: every row
-      const int voff = (int)((nh + (int64_t)j0 * (nx + 1) + lo_i) & 1) + (i0 - lo_i);
+      int voff[SW_R];
+#pragma unroll
+      for (int rr = 0; rr < SW_R; ++rr)
+        voff[rr] = (int)((nh + (int64_t)(j0 + rr) * (nx + 1) + lo_i) & 1) + (i0 - lo_i);
       // ---- elements: four threads per element, thread f forming the row block of edge f,
       // y_f = S_T[f, :] x_T.  A warp holds one edge role of the 32 elements of one colour
       // of the row, so its orbit reads are one conflict-free 256-byte row of the record.
       {
-        const int f = warp >> 1, col = warp & 1;
-        const int j = j0;
+        const int rr = warp / 8, wr = warp % 8, f = wr >> 1, col = wr & 1;
+        const int j = j0 + rr;
         const int cc = 2 * lane + ((col + j) & 1), i = i0 + cc;
         if (j < je) {
           double xv[M];
-          const double* xb = XH + (cc + hoff) * K1;         // H(i, j)
-          const double* xt = XH + ROW + (cc + hoff) * K1;   // H(i, j+1)
-          const double* xl = XV + (cc + voff) * K1;         // V(i, j)
-          const double* xr = xl + K1;                       // V(i+1, j)
+          const double* xb = XH + rr * ROW + (cc + hoff) * K1;         // H(i, j)
+          const double* xt = XH + (rr + 1) * ROW + (cc + hoff) * K1;   // H(i, j+1)
+          const double* xl = XV + rr * ROW + (cc + voff[rr]) * K1;     // V(i, j)
+          const double* xr = xl + K1;                                  // V(i+1, j)
           const bool mb = j == 0, mt = j + 1 == ny, ml = i == 0, mr = i + 1 == nx;   // dOmega
 #pragma unroll
           for (int a = 0; a < K1; ++a) {
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(SW_T + 32, 2)
             xv[2 * K1 + a] = mt ? 0.0 : xt[a];
             xv[3 * K1 + a] = ml ? 0.0 : xl[a];
           }
-          const double* Sp = SS + col * NORB * 32 + lane;
+          const double* Sp = SS + (rr * 2 + col) * NORB * 32 + lane;
           double yv[K1];
 #define SW_ROWS(FF)                                                                   \
   _Pragma("unroll") for (int a = 0; a < K1; ++a) {                                    \
@@ -300,13 +304,15 @@ __global__ void __launch_bounds__(SW_T + 32, 2)
           if (f == 0) { SW_ROWS(0) } else if (f == 1) { SW_ROWS(1) }
           else if (f == 2) { SW_ROWS(2) } else { SW_ROWS(3) }
 #undef SW_ROWS
-          if (f == 2) {   // top edge: the next step's bottom row (carry)
+          if (f == 2) {   // top edge: the next row's bottom edge (carry after the last row)
+            double* dst = rr + 1 < SW_R ? Ylo + ((rr + 1) * SW_C + cc) * K1 : cnew + cc * K1;
 #pragma unroll
-            for (int a = 0; a < K1; ++a) cnew[cc * K1 + a] = yv[a];
+            for (int a = 0; a < K1; ++a) dst[a] = yv[a];
           } else if (!pro) {
-            double* dst = f == 0 ? Yhi + cc * K1                                  // bottom edge
-                        : f == 3 ? Yhi + (SW_C + cc) * K1                         // left edge
-                        : (cc + 1 < SW_C ? Ylo + (SW_C + cc + 1) * K1 : nullptr);  // right edge
+            const int hq = rr * SW_C + cc, vq = SW_R * SW_C + rr * SW_C + cc;
+            double* dst = f == 0 ? Yhi + hq * K1                                        // bottom
+                        : f == 3 ? Yhi + vq * K1                                        // left
+                        : (cc + 1 < SW_C ? Ylo + (vq + 1) * K1 : nullptr);              // right
             if (dst) {
 #pragma unroll
               for (int a = 0; a < K1; ++a) dst[a] = yv[a];
@@ -315,14 +321,14 @@ __global__ void __launch_bounds__(SW_T + 32, 2)
         }
         // the left neighbour strip's element (i0-1, j0): row block of its right edge,
         // one thread per row (orbit values staged in SH)
-        if (!pro && i0 > 0 && tid < K1 && j0 < je) {
-          const int a = tid, ih = i0 - 1;
+        if (!pro && i0 > 0 && tid < SW_R * K1 && j0 + tid / K1 < je) {
+          const int hr = tid / K1, a = tid % K1, ih = i0 - 1, jh = j0 + hr;
           double xv[M];
-          const double* xb = XH + (hoff - 1) * K1;
-          const double* xt = XH + ROW + (hoff - 1) * K1;
-          const double* xl = XV + (voff - 1) * K1;
+          const double* xb = XH + hr * ROW + (hoff - 1) * K1;
+          const double* xt = XH + (hr + 1) * ROW + (hoff - 1) * K1;
+          const double* xl = XV + hr * ROW + (voff[hr] - 1) * K1;
           const double* xr = xl + K1;
-          const bool mb = j0 == 0, mt = j0 + 1 == ny, ml = ih == 0;
+          const bool mb = jh == 0, mt = jh + 1 == ny, ml = ih == 0;
 #pragma unroll
           for (int q = 0; q < K1; ++q) {
             xv[0 * K1 + q] = mb ? 0.0 : xb[q];
@@ -337,9 +343,9 @@ __global__ void __launch_bounds__(SW_T + 32, 2)
 #pragma unroll
             for (int q = 0; q < K1; ++q)
               if (q == a) o = D::orb(D::pk(K1 + q, b));
-            acc = fma(SH[o], xv[b], acc);
+            acc = fma(SH[hr * NORB + o], xv[b], acc);
           }
-          Ylo[SW_C * K1 + a] = acc;
+          Ylo[(SW_R * SW_C + hr * SW_C) * K1 + a] = acc;
         }
       }
       asm volatile("bar.sync 1, %0;" ::"n"(SW_T) : "memory");   // consumers only
@@ -362,23 +368,23 @@ __global__ void __launch_bounds__(SW_T + 32, 2)
             }
             bnd = true;
           } else {
-            const int hv = q / SW_C, cc = q % SW_C;
-            const int i = i0 + cc, j = j0;
+            const int hv = q / (SW_R * SW_C), rr = (q / SW_C) % SW_R, cc = q % SW_C;
+            const int i = i0 + cc, j = j0 + rr;
             if (j >= je) continue;
             int64_t e0;
             if (hv == 0) {
               e0 = (int64_t)j * nx + i0;
               bnd = j == 0;
-              xs = XH + (cc + hoff) * K1;
+              xs = XH + rr * ROW + (cc + hoff) * K1;
             } else {
               e0 = nh + (int64_t)j * (nx + 1) + i0;
               bnd = i == 0;
-              xs = XV + (cc + voff) * K1;
+              xs = XV + rr * ROW + (cc + voff[rr]) * K1;
             }
             e = e0 + cc;
-            ro = hv * SW_W + cc + (int)(e0 & 1);   // rows start at e0 & ~1 (D rows: same parity)
+            ro = (hv * SW_R + rr) * SW_W + cc + (int)(e0 & 1);   // rows start at e0 & ~1
             if (!bnd) {
-              const double* lo = hv == 0 ? cold + cc * K1 : Ylo + q * K1;
+              const double* lo = (hv == 0 && rr == 0) ? cold + cc * K1 : Ylo + q * K1;
 #pragma unroll
               for (int a = 0; a < K1; ++a) yy[a] = lo[a] + Yhi[q * K1 + a];
             }
@@ -455,7 +461,7 @@ static int sweep_sms() {
 static SweepGeom sweep_geom(const LevelDev& L) {
   SweepGeom g;
   g.nstrip = (L.nx + SW_C - 1) / SW_C;
-  const int want = 8 * sweep_sms();
+  const int want = 4 * SW_CPS * sweep_sms();
   int seg = (int)(((int64_t)L.ny * g.nstrip + want - 1) / want);
   seg = ((seg + SW_R - 1) / SW_R) * SW_R;
   if (seg < 8 * SW_R) seg = 8 * SW_R;
@@ -480,7 +486,7 @@ int apply_tile_grid(const LevelDev& L) {
   const SweepGeom g = sweep_geom(L);
   int n = g.nstrip * g.nseg;
   if (L.grid_cap > 0 && n > L.grid_cap) n = L.grid_cap;
-  return n < 2 * sweep_sms() ? n : 2 * sweep_sms();   // 2 resident CTAs per SM
+  return n < SW_CPS * sweep_sms() ? n : SW_CPS * sweep_sms();
 }
 
 template <int P, int MODE, bool DOT>
