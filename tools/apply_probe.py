@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--op", default="apply", choices=["apply", "smooth"],
                     help="smooth: one fine smoothing step through mg_smooth (apply + D^-1 epilogue, "
                          "plus mg_smooth's two masked input copies and one output copy)")
+    ap.add_argument("--opt", action="append", default=[], help="KEY=VALUE for mg_set_option (repeatable)")
     ap.add_argument("--sweep", type=int, default=0, help="mg_set_option MG_OPT_SWEEP")
     ap.add_argument("--steps", type=int, default=1, help="smoothing steps per probe (--op smooth)")
     ap.add_argument("--scheme", default="config", choices=["config", "nipg", "iipg", "tiles"],
@@ -45,6 +46,9 @@ def main():
         s.setup(pr.K, pr.method, pr.tau, sm)
         if a.sweep:
             s.set_option(s.OPT_SWEEP, a.sweep)
+        for kv in a.opt:
+            k, v = kv.split("=")
+            s.set_option(int(k), int(v))
         lev = a.level or s.nlevels
         nd = s.ndof(lev)
         x = torch.rand(nd, dtype=torch.float64, device=dev)

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs (per-kernel profiling)")
     ap.add_argument("--maxit", type=int, default=4000, help="PCG iteration cap (short per-iteration profiles)")
     ap.add_argument("--warm", type=int, default=2)
+    ap.add_argument("--opt", action="append", default=[], help="KEY=VALUE for mg_set_option (repeatable)")
     ap.add_argument("--sweep", type=int, default=0, help="mg_set_option MG_OPT_SWEEP (-1 off, 0 auto, 1 force)")
     a = ap.parse_args()
     cfg = W.CONFIGS[a.config]
@@ -45,6 +46,9 @@ def main():
             s.use_graphs(False)
         if a.sweep:
             s.set_option(s.OPT_SWEEP, a.sweep)
+        for kv in a.opt:
+            k, v = kv.split("=")
+            s.set_option(int(k), int(v))
         for _ in range(a.warm):   # warm-up (graph capture, lazy attributes)
             s.setup(K, meth, tau, sm)
             g, _ = s.assemble_rhs(fq, pr.f_const, gD)
