@@ -125,7 +125,10 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
 #pragma unroll
   for (int f = F0; f < F0 + NF; ++f)
     live[f] = !bd[f] && !((itf >> f) & 1) && (MODE != AM_GSC || ((gsm >> f) & 1));
-  double t[M], dd[M], dv[HASD ? 4 * NCS : 1];
+  // SMOOTH + DOT (the PCG's last fine smoothing step): dot += x_new . r over the
+  // pass's edges, r kept from the load phase
+  constexpr bool SDOT = DOT && MODE == AM_SMOOTH;
+  double t[M], dd[M], dv[HASD ? 4 * NCS : 1], rk[SDOT ? M : 1];
 #pragma unroll
   for (int f = F0; f < F0 + NF; ++f) {
     const int64_t base = ed[f] * K1;
@@ -139,6 +142,10 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
       ld_edge<K1>(y + base, yo);
       if (MODE != AM_APPLY && MODE != AM_DINV) ld_edge<K1>(r + base, rv);
       if (MODE == AM_SMOOTH && L.smoother == 1 && step > 0) ld_edge<K1>(d + base, dd + f * K1);
+    }
+    if (SDOT) {
+#pragma unroll
+      for (int a = 0; a < K1; ++a) rk[f * K1 + a] = rv[a];
     }
 #pragma unroll
     for (int a = 0; a < K1; ++a)
@@ -211,6 +218,7 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
         if (L.smoother == 1 && step > 0) dn = fma(c1, dd[f * K1 + a], dn);
         dnv[a] = dn;
         xnv[a] = xf[a] + dn;
+        if (SDOT) dot = fma(xnv[a], rk[f * K1 + a], dot);
       }
     }
     if (MODE == AM_SMOOTH) {
@@ -872,7 +880,14 @@ static void dispatch_apply(const LevelDev& L, int colour, int mode, const double
       launch_one<P, AM_GSC, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
       break;
     default:
-      launch_one<P, AM_SMOOTH, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
+      if (partials && L.orb) {   // (only the orbit kernel has the SMOOTH + DOT epilogue)
+        orb_resident<P, AM_SMOOTH, true>();
+        launch_ex(k_apply_orb<P, AM_SMOOTH, true>, grid, 32,
+                  (size_t)OrbCfg<P>::NST * OrbCfg<P>::STAGE_BYTES, pdl, st, L, colour, x, y, r, d,
+                  step, partials, pdl ? 1 : 0);
+      } else {
+        launch_one<P, AM_SMOOTH, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
+      }
       break;
   }
 }

@@ -177,16 +177,76 @@ int launch_restrict_edges(const LevelDev& F, const LevelDev& C, const double* re
   return 1;
 }
 
-__global__ void k_prolong_macro(LevelDev F, LevelDev C, const double* __restrict__ ec,
-                                const double* __restrict__ Pm, double* e) {
+// Prolongation e += I_k e_c (Eqs. 3.3 / 3.4, bodies.cuh prolong_macro_body) gathered per fine edge (one thread per fine edge, one 16-byte
+// read-modify-write of its two dofs, consecutive threads on consecutive edges): a
+// macro-interior edge ie[k] takes rows 2k, 2k+1 of P_M e_c(M); an edge on a macro-edge
+// takes its half of J e_c (f0: (c0, cm), f1: (cm, c1)).  Every fine dof gets the one
+// term prolong_macro_body adds to it, in the same arithmetic, and the top / right
+// interface macro-edges are covered too (no k_prolong_itf).
+__global__ void __launch_bounds__(128) k_prolong_edges(LevelDev F, LevelDev C,
+                                                       const double* __restrict__ ec,
+                                                       const double* __restrict__ Pm, double* e) {
   pdl_enter();
-  prolong_macro_body(F, C, ec, Pm, e, GTID, GNT);
+  const int nx = F.nx, nxc = C.nx, nyc = C.ny;
+  const int64_t nhF = (int64_t)nx * (F.ny + 1);
+  for (int64_t E = GTID; E < F.nedge; E += GNT) {
+    int I, J, k = -1, half = 0;
+    int64_t cE = 0;
+    if (E < nhF) {
+      const int j = (int)((unsigned)E / (unsigned)nx), i = (int)E - j * nx;
+      I = i >> 1;
+      J = j >> 1;
+      if (j & 1) k = i & 1;                       // ie[0] / ie[1]
+      else { cE = hedge(nxc, I, J); half = i & 1; }
+    } else {
+      const int64_t r = E - nhF;
+      const int j = (int)((unsigned)r / (unsigned)(nx + 1)), i = (int)r - j * (nx + 1);
+      I = i >> 1;
+      J = j >> 1;
+      if (i & 1) k = 2 + (j & 1);                 // ie[2] / ie[3]
+      else { cE = vedge(nxc, nyc, I, J); half = j & 1; }
+    }
+    double2 v;
+    if (k >= 0) {
+      int64_t ce[4];
+      bool cb[4];
+      elem_edges(nxc, nyc, I, J, ce, cb, C.dmask);
+      double c[8];
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        const double2 t = cb[f] ? make_double2(0.0, 0.0) : reinterpret_cast<const double2*>(ec)[ce[f]];
+        c[2 * f] = t.x;
+        c[2 * f + 1] = t.y;
+      }
+      const double2* P = reinterpret_cast<const double2*>(Pm + ((int64_t)J * nxc + I) * 64 + k * 16);
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2 p0 = __ldg(P + q), p1 = __ldg(P + 4 + q);
+        a0 = fma(p0.x, c[2 * q], a0);
+        a0 = fma(p0.y, c[2 * q + 1], a0);
+        a1 = fma(p1.x, c[2 * q], a1);
+        a1 = fma(p1.y, c[2 * q + 1], a1);
+      }
+      v = make_double2(a0, a1);
+    } else {
+      if (edge_on_boundary(nxc, nyc, cE, C.dmask)) continue;
+      const double2 t = reinterpret_cast<const double2*>(ec)[cE];
+      const double cm = 0.5 * (t.x + t.y);
+      v = half ? make_double2(cm, t.y) : make_double2(t.x, cm);
+    }
+    double2* ep = reinterpret_cast<double2*>(e) + E;
+    double2 o = *ep;
+    o.x += v.x;
+    o.y += v.y;
+    *ep = o;
+  }
 }
 
+// (agglomerated levels are P1: two dofs per edge on both sides)
 int launch_prolong_macro(const LevelDev& F, const LevelDev& C, const double* ec,
                          const double* Pm, double* e, cudaStream_t st) {
-  int64_t nmac = (int64_t)C.nx * C.ny;
-  launch_ex(k_prolong_macro, cap_grid(8 * nmac, 128, 148 * 8), 128, 0, true, st, F, C, ec, Pm, e);
+  launch_ex(k_prolong_edges, cap_grid(F.nedge, 128, 148 * 16), 128, 0, true, st, F, C, ec, Pm, e);
   return 1;
 }
 
@@ -211,10 +271,46 @@ __global__ void k_p_prolong(LevelDev F, const double* __restrict__ Jp,
   p_prolong_body(F, Jp, ec, e, GTID, GNT);
 }
 
+// the same per edge with the fine rows staged through shared memory (128 edges per
+// block, coalesced loads and stores)
+template <int K1>
+__global__ void __launch_bounds__(128) k_p_prolong_st(LevelDev F, const double* __restrict__ Jp,
+                                                      const double* __restrict__ ec, double* e) {
+  pdl_enter();
+  constexpr int EB = 128;
+  __shared__ double se[EB * K1];
+  double j0[K1], j1[K1];
+#pragma unroll
+  for (int a = 0; a < K1; ++a) {
+    j0[a] = __ldg(Jp + a * 2);
+    j1[a] = __ldg(Jp + a * 2 + 1);
+  }
+  const int t = threadIdx.x;
+  for (int64_t e0 = (int64_t)blockIdx.x * EB; e0 < F.nedge; e0 += (int64_t)gridDim.x * EB) {
+    const int ne = (int)(F.nedge - e0 < EB ? F.nedge - e0 : EB);
+    const int64_t off = e0 * K1;
+    for (int q = t; q < ne * K1; q += EB) se[q] = e[off + q];
+    __syncthreads();
+    if (t < ne && !edge_on_boundary(F.nx, F.ny, e0 + t, F.dmask)) {
+      const double2 c = reinterpret_cast<const double2*>(ec)[e0 + t];
+#pragma unroll
+      for (int a = 0; a < K1; ++a) se[t * K1 + a] += fma(j0[a], c.x, j1[a] * c.y);
+    }
+    __syncthreads();
+    for (int q = t; q < ne * K1; q += EB) e[off + q] = se[q];
+    __syncthreads();
+  }
+}
+
 int launch_p_prolong(const LevelDev& F, const double* Jp, const double* ec, double* e,
                      cudaStream_t st) {
-  launch_ex(k_p_prolong, cap_grid(F.nedge, 128, 148 * 8), 128, 0, true, st, F, Jp, ec, e);
-  return 1;
+  const int g = cap_grid(F.nedge, 128, 148 * 8);
+  switch (F.k1) {
+    case 3: launch_ex(k_p_prolong_st<3>, g, 128, 0, true, st, F, Jp, ec, e); return 1;
+    case 4: launch_ex(k_p_prolong_st<4>, g, 128, 0, true, st, F, Jp, ec, e); return 1;
+    case 5: launch_ex(k_p_prolong_st<5>, g, 128, 0, true, st, F, Jp, ec, e); return 1;
+    default: launch_ex(k_p_prolong, g, 128, 0, true, st, F, Jp, ec, e); return 1;
+  }
 }
 
 // ---------------------------------------------------------------- reductions

@@ -247,41 +247,6 @@ int launch_restrict_halo_finish(const LevelDev& C, double* rc, const double* sen
   return 1;
 }
 
-// ---------------------------------------------------------------- prolongation on top / right interfaces
-// prolong_macro_body updates the bottom and left macro-edges of every macro; an
-// interface macro-edge on the local top / right side is the top / right edge of
-// a local macro and the bottom / left edge of a remote one, so it is done here
-// (both ranks hold the same e_c there, so both fine copies get the same J e_c).
-__global__ void k_prolong_itf(LevelDev F, LevelDev C, const double* __restrict__ ec, double* e) {
-  pdl_enter();
-  const int64_t n = itf_edges(C);
-  for (int64_t w = GTID; w < n; w += GNT) {
-    int f, q;
-    itf_item(C, w, f, q);
-    if (f != 1 && f != 2) continue;
-    const int64_t E = side_edge(C.nx, C.ny, f, q);
-    const double c0 = ec[E * 2], c1 = ec[E * 2 + 1], cm = 0.5 * (c0 + c1);
-    int64_t f0, f1;
-    if (f == 2) {
-      f0 = hedge(F.nx, 2 * q, F.ny);
-      f1 = hedge(F.nx, 2 * q + 1, F.ny);
-    } else {
-      f0 = vedge(F.nx, F.ny, F.nx, 2 * q);
-      f1 = vedge(F.nx, F.ny, F.nx, 2 * q + 1);
-    }
-    e[f0 * 2] += c0;
-    e[f0 * 2 + 1] += cm;
-    e[f1 * 2] += cm;
-    e[f1 * 2 + 1] += c1;
-  }
-}
-
-int launch_prolong_itf(const LevelDev& F, const LevelDev& C, const double* ec, double* e,
-                       cudaStream_t st) {
-  launch_ex(k_prolong_itf, grid_for(itf_edges(C), 128, 148), 128, 0, true, st, F, C, ec, e);
-  return 1;
-}
-
 // ---------------------------------------------------------------- edge blocks on interfaces
 // k_edge_blocks leaves this rank's partial D_e (not inverted) in Dinv on the
 // interface edges; pack it, and after the exchange invert D_own + D_remote.

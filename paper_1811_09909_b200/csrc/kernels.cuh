@@ -461,8 +461,6 @@ int launch_restrict_halo_pack(const LevelDev& C, const double* cbuf, double* sen
 int launch_restrict_halo_finish(const LevelDev& C, double* rc, const double* send,
                                 const double* recv, bool fuse, double* ec, double* dc,
                                 cudaStream_t st);
-int launch_prolong_itf(const LevelDev& F, const LevelDev& C, const double* ec, double* e,
-                       cudaStream_t st);
 int launch_eblk_pack(const LevelDev& L, double* send, cudaStream_t st);
 int launch_eblk_finish(const LevelDev& L, const double* recv, DevError* err, cudaStream_t st);
 int launch_gather_vec(const LevelDev& G, int bx, int by, int px, int py, int64_t ndof_loc,

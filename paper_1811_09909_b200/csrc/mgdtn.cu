@@ -87,6 +87,7 @@ struct Ctx {
   cudaGraphConditionalHandle cond = 0;
   long long nPro = 0, nBody = 0;  // kernels in the prologue / in one loop iteration
   bool use_graphs = true;
+  bool dot_fold = false;   // pcg_iter_B: the fine post-smoothing pass writes r.z partials
   int tail_start = -1;            // first level run by k_coarse_tail (-1: none)
   bool tail_vcycle = true;        // V-cycle levels >= tail_start through k_coarse_tail
   bool tail_lmax = true;          // their Chebyshev power iterations through k_tail_lmax
@@ -616,11 +617,10 @@ static void reduce_scal(Ctx* c, const double* partials, int n, double* scal, int
 // one apply in `mode` (bodies.cuh epilogues); on a partitioned level the colour
 // passes leave partial sums on the interface edges, which are exchanged and
 // finished by k_itf_epilogue (k_part.cu)
-// On a one-GPU orbit level the smoothing step is one streamed pass (k_tile.cu): it
-// reads x, r, d once instead of the two-colour pair's x twice and y three times
-// (config 5: 4.8 vs 5.2-5.9 ms per fine step).  The plain apply and the residual
-// stay on the two-colour pair of passes (k_apply.cu), which measured faster for them
-// (config 5: 2.3 vs 2.65 ms and 2.75 vs 2.96 ms; profiles/r02_sweep_probe.txt).
+// MG_OPT_SWEEP = 1 runs the smoothing step of a one-GPU orbit level as one streamed
+// pass (k_tile.cu): it reads x, r, d once instead of the two-colour pair's x twice and
+// y three times, but measured slower than the pair (profiles/r02_sweep_probe.txt), so
+// it is off by default.
 static bool tiled(const LevelDev& d, int mode) { return tile_level(d) && mode == AM_SMOOTH; }
 static void apply_mode(Ctx* c, const HostLevel& L, int mode, const double* x, double* y,
                        const double* r, double* d, int step, double* partials) {
@@ -692,8 +692,11 @@ static inline void apply_full(Ctx* c, const HostLevel& L, const double* x, doubl
 // two-colour passes update it in place (and use the other vector as scratch).
 static inline double* other(const HostLevel& L, const double* cur) { return cur == L.e ? L.w : L.e; }
 
-// one smoothing step on the iterate `cur`; returns where the new iterate is
-static inline double* smooth_step(Ctx* c, HostLevel& L, int step, double* cur) {
+// one smoothing step on the iterate `cur`; returns where the new iterate is.  With
+// `partials` (two-colour orbit level, pcg_dot_fold): the colour-1 pass also writes the
+// per-CTA partial sums of x_new . L.r
+static inline double* smooth_step(Ctx* c, HostLevel& L, int step, double* cur,
+                                  double* partials = nullptr) {
   if (c->sm.kind == MG_SMOOTH_LUSGS) {
     // one LU-SGS step: forward block Gauss-Seidel sweep over the
     // four edge colours, then backward (oracle/multigrid.py)
@@ -711,7 +714,7 @@ static inline double* smooth_step(Ctx* c, HostLevel& L, int step, double* cur) {
                                      c->st);
     return out;
   }
-  apply_mode(c, L, AM_SMOOTH, cur, other(L, cur), L.r, L.dv, slot, nullptr);
+  apply_mode(c, L, AM_SMOOTH, cur, other(L, cur), L.r, L.dv, slot, partials);
   return cur;
 }
 
@@ -772,8 +775,7 @@ static void prolong_level(Ctx* c, int li, const double* ec, double* e) {
     ecl = c->lgl.e;
   }
   if (L.kind == KIND_H) {
-    c->launches += launch_prolong_macro(L.d, C.d, ecl, L.Pm, e, c->st);
-    if (C.d.imask) c->launches += launch_prolong_itf(L.d, C.d, ecl, e, c->st);
+    c->launches += launch_prolong_macro(L.d, C.d, ecl, L.Pm, e, c->st);   // (interface edges included)
   } else {
     c->launches += launch_p_prolong(L.d, c->refdev.Jp, ecl, e, c->st);
   }
@@ -826,7 +828,8 @@ static double* vcycle_level(Ctx* c, int li, bool first_done) {
   restrict_level(c, li, res, cur, true, C.r, fuse);
   const double* ec = vcycle_level(c, li + 1, fuse);
   prolong_level(c, li, ec, cur);
-  for (int s = 0; s < nu_post; ++s) cur = smooth_step(c, L, s, cur);
+  for (int s = 0; s < nu_post; ++s)
+    cur = smooth_step(c, L, s, cur, li == 0 && c->dot_fold && s == nu_post - 1 ? c->part : nullptr);
   return cur;
 }
 
@@ -1067,12 +1070,27 @@ static void pcg_iter_A(Ctx* c) {  // Ap, alpha, x/r update, rr
   reduce_scal(c, c->part, vg, c->scal, 2, 0);
 }
 
+// r.z folded into the V-cycle's last fine smoothing pass (its colour-1 epilogue visits
+// every interior edge once; dOmega rows of r and z are 0): a one-GPU two-colour orbit
+// fine level with a post-smoothing step that the launch-per-step V-cycle runs
+static bool pcg_dot_fold(const Ctx* c) {
+  const HostLevel& F = c->lev[0];
+  return pcg_sf(c) && !partitioned(c) && F.d.imask == 0 && !F.clist && c->sm.nu_post > 0 &&
+         !tiled(F.d, AM_SMOOTH);
+}
+
 static void pcg_iter_B(Ctx* c) {  // z = B r, beta, p update
   HostLevel& F = c->lev[0];
   const int vg = vec_grid(F.d.ndof);
+  c->dot_fold = pcg_dot_fold(c);
   const double* z = vcycle_level(c, 0, pcg_sf(c));   // first step done by the update
-  c->launches += launch_dot(F.r, z, F.d.ndof, c->part, vg, c->st, &F.d);
-  reduce_scal(c, c->part, vg, c->scal, 0, 2);
+  if (c->dot_fold) {
+    reduce_scal(c, c->part, apply_grid_mode(F.d, AM_SMOOTH), c->scal, 0, 2);
+  } else {
+    c->launches += launch_dot(F.r, z, F.d.ndof, c->part, vg, c->st, &F.d);
+    reduce_scal(c, c->part, vg, c->scal, 0, 2);
+  }
+  c->dot_fold = false;
   c->launches += launch_pcg_pupdate(c->pv, z, c->scal, F.d.ndof, c->st);
 }
 
