@@ -322,8 +322,13 @@ int mg_check_invariants(void* ctx, double* report);
  *                         (each CTA then walks many chunks: ring wrap-around at small n).
  *   MG_OPT_COMM_TIMEOUT_MS partitioned contexts: every host wait polls NCCL's asynchronous
  *                         error state and gives up after this many ms (default 300000),
- *                         aborting the communicator and returning MG_ERR_NCCL. */
-enum { MG_OPT_SWEEP = 1, MG_OPT_APPLY_GRID_CAP = 2, MG_OPT_COMM_TIMEOUT_MS = 3 };
+ *                         aborting the communicator and returning MG_ERR_NCCL.
+ *   MG_OPT_GATHER_NE      packed P1 levels (one-GPU or replicated) with at most this many
+ *                         elements run the apply / residual / smoothing step as one
+ *                         gather-form pass (default 65536; 0: never).  Bitwise the same
+ *                         results as the pair of colour passes. */
+enum { MG_OPT_SWEEP = 1, MG_OPT_APPLY_GRID_CAP = 2, MG_OPT_COMM_TIMEOUT_MS = 3,
+       MG_OPT_GATHER_NE = 4 };
 int mg_set_option(void* ctx, int32_t key, int64_t value);
 
 const char* mg_last_error(const void* ctx);

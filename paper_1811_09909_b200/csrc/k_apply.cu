@@ -907,6 +907,131 @@ int launch_apply(const LevelDev& L, int colour, int mode, const double* x, doubl
 
 int apply2_grid(const LevelDev& L, int mode) { return apply_grid_mode(L, mode); }
 
+// ---------------------------------------------------------------- gather-form apply (small P1 levels)
+// One pass, thread per edge: an interior edge's output is the sum of the two rows of
+// S_T x_T that belong to it, one from each adjacent element, so no two threads write
+// the same value and the colour-0 / colour-1 pair of passes (two dependent launches)
+// becomes one.  Each row is accumulated in increasing column order from 0 and the two
+// rows are combined in the colour-0-then-colour-1 order of the pair of passes (APPLY:
+// y0 + y1; RESID / SMOOTH: (r - y0) - y1), so the results are bitwise those of the pair.
+// The smoothing update is written out of place (xo): the pair updates x in place only
+// because a colour-1 element owns its edges, which a per-edge thread does not.
+// Packed symmetric P1 maps (the agglomerated levels), one-GPU / replicated levels
+// (every domain-side edge on dOmega).
+template <int MODE>
+__global__ void __launch_bounds__(128) k_apply_gather(const LevelDev L, const double* x, double* y,
+                                                      const double* __restrict__ r, double* d,
+                                                      double* xo, int step) {
+  pdl_enter();
+  constexpr int K1 = 2, M = 8;
+  const int nx = L.nx, ny = L.ny;
+  const int64_t nh = (int64_t)nx * (ny + 1);
+  double c1 = 0.0, c2 = 0.0;
+  if (MODE == AM_SMOOTH) {
+    c1 = L.coef[2 * step];
+    c2 = L.coef[2 * step + 1];
+  }
+  for (int64_t E = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; E < L.nedge;
+       E += (int64_t)gridDim.x * blockDim.x) {
+    int i, j;
+    bool bnd;
+    int ti[2], tj[2], tf[2];   // the two adjacent elements and this edge's side in each
+    if (E < nh) {
+      j = (int)((unsigned)E / (unsigned)nx);
+      i = (int)E - j * nx;
+      bnd = j == 0 || j == ny;
+      ti[0] = i; tj[0] = j - 1; tf[0] = 2;   // below: its top edge
+      ti[1] = i; tj[1] = j;     tf[1] = 0;   // above: its bottom edge
+    } else {
+      const int64_t q = E - nh;
+      j = (int)((unsigned)q / (unsigned)(nx + 1));
+      i = (int)q - j * (nx + 1);
+      bnd = i == 0 || i == nx;
+      ti[0] = i - 1; tj[0] = j; tf[0] = 1;   // left: its right edge
+      ti[1] = i;     tj[1] = j; tf[1] = 3;   // right: its left edge
+    }
+    const double2 xe = reinterpret_cast<const double2*>(x)[E];
+    if (bnd) {   // dOmega: y = 0 (APPLY / RESID); the smoothed iterate keeps x
+      if (MODE == AM_SMOOTH) reinterpret_cast<double2*>(xo)[E] = xe;
+      else reinterpret_cast<double2*>(y)[E] = make_double2(0.0, 0.0);
+      continue;
+    }
+    double yc[2][K1];   // [colour][row]
+    int64_t s1 = 0;     // colour-1 slot and its side of this edge (D_e^-1 record)
+    int f1 = 0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      int colour;
+      int64_t s;
+      elem_slot(nx, ti[k], tj[k], colour, s);
+      if (colour) {
+        s1 = s;
+        f1 = tf[k];
+      }
+      int64_t ed[4];
+      bool bd[4];
+      elem_edges(nx, ny, ti[k], tj[k], ed, bd, L.dmask);
+      double xv[M];
+      gather_x<K1>(x, ed, bd, xv);
+      const double* Sp = L.S + s_offset(L.nchunk, L.npk, colour, s, 0);
+#pragma unroll
+      for (int a = 0; a < K1; ++a) {
+        const int ra = tf[k] * K1 + a;
+        double acc = 0.0;
+#pragma unroll
+        for (int b = 0; b < M; ++b) acc = fma(__ldg(Sp + (int64_t)s_index(ra, b, M, 0) * 32), xv[b], acc);
+        yc[colour][a] = acc;
+      }
+    }
+    if (MODE == AM_APPLY) {
+      reinterpret_cast<double2*>(y)[E] = make_double2(yc[0][0] + yc[1][0], yc[0][1] + yc[1][1]);
+      continue;
+    }
+    const double2 rv = __ldg(reinterpret_cast<const double2*>(r) + E);
+    const double res0 = (rv.x - yc[0][0]) - yc[1][0], res1 = (rv.y - yc[0][1]) - yc[1][1];
+    if (MODE == AM_RESID) {
+      reinterpret_cast<double2*>(y)[E] = make_double2(res0, res1);
+      continue;
+    }
+    // D_e^-1 as the pair's colour-1 pass reads it: the packed upper triangle of the
+    // colour-1 element's record (LevelDev::Dc; rows f*3 + {00, 01, 11})
+    const double* Dr = L.Dc + ((s1 >> 5) * 12 + f1 * 3) * 32 + (s1 & 31);
+    const double D00 = __ldg(Dr), D01 = __ldg(Dr + 32), D11 = __ldg(Dr + 64);
+    double dd[2] = {0.0, 0.0};
+    if (L.smoother == 1 && step > 0) {
+      const double2 t = reinterpret_cast<const double2*>(d)[E];
+      dd[0] = t.x;
+      dd[1] = t.y;
+    }
+    double dn[2];
+    dn[0] = c2 * fma(D01, res1, fma(D00, res0, 0.0));
+    dn[1] = c2 * fma(D11, res1, fma(D01, res0, 0.0));
+    if (L.smoother == 1 && step > 0) {
+      dn[0] = fma(c1, dd[0], dn[0]);
+      dn[1] = fma(c1, dd[1], dn[1]);
+    }
+    if (L.smoother == 1) reinterpret_cast<double2*>(d)[E] = make_double2(dn[0], dn[1]);
+    reinterpret_cast<double2*>(xo)[E] = make_double2(xe.x + dn[0], xe.y + dn[1]);
+  }
+}
+
+bool gather_level(const LevelDev& L) {
+  return L.gather && !L.orb && !L.ns && L.p == 1 && L.imask == 0 && L.dmask == 15 && L.Dc;
+}
+
+int launch_apply_gather(const LevelDev& L, int mode, const double* x, double* y, const double* r,
+                        double* d, double* xo, int step, cudaStream_t st) {
+  const int64_t nb = (L.nedge + 127) / 128, cap = (int64_t)num_sms() * 16;
+  const int g = (int)(nb < 1 ? 1 : nb < cap ? nb : cap);
+  switch (mode) {
+    case AM_APPLY: launch_ex(k_apply_gather<AM_APPLY>, g, 128, 0, true, st, L, x, y, r, d, xo, step); break;
+    case AM_RESID: launch_ex(k_apply_gather<AM_RESID>, g, 128, 0, true, st, L, x, y, r, d, xo, step); break;
+    case AM_SMOOTH: launch_ex(k_apply_gather<AM_SMOOTH>, g, 128, 0, true, st, L, x, y, r, d, xo, step); break;
+    default: return -1;
+  }
+  return 1;
+}
+
 int launch_apply2(const LevelDev& L, int mode, const double* x, double* y, const double* r,
                   double* d, int step, double* partials, bool pdl, cudaStream_t st) {
   int n = launch_apply(L, 0, AM_W0, x, y, nullptr, nullptr, 0, nullptr, pdl, st);

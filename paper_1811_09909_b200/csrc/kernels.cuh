@@ -61,6 +61,7 @@ struct LevelDev {
   const int* clist;        // non-null: an orbit-level pass covers only these chunks (ncl of them)
   int ncl;
   int sweep;               // mg_set_option MG_OPT_SWEEP: 0 auto, 1 wherever possible, -1 never
+  int gather;              // one-pass gather-form apply (k_apply_gather; plan_gather)
   int grid_cap;            // mg_set_option MG_OPT_APPLY_GRID_CAP: max CTAs per apply pass (0: none)
   // partitioned levels (multi-GPU): local sides 0 bottom, 1 right, 2 top, 3 left
   int dmask;               // sides on the global boundary dOmega (Dirichlet); 15 on one GPU
@@ -332,6 +333,9 @@ int apply2_grid(const LevelDev& L, int mode);  // blocks of launch_apply2 (parti
 // single-pass tiled apply on a one-GPU orbit level (k_tile.cu): AM_APPLY (y = A x, dot
 // x.y into partials if given), AM_RESID (y = r - A x), AM_SMOOTH (xo = x + d, out of place)
 bool tile_level(const LevelDev& L);
+bool gather_level(const LevelDev& L);
+int launch_apply_gather(const LevelDev& L, int mode, const double* x, double* y, const double* r,
+                        double* d, double* xo, int step, cudaStream_t st);
 int apply_tile_grid(const LevelDev& L);
 int launch_apply_tile(const LevelDev& L, int mode, const double* x, double* y, const double* r,
                       double* d, double* xo, int step, double* partials, cudaStream_t st);

@@ -87,7 +87,8 @@ struct Ctx {
   cudaGraphConditionalHandle cond = 0;
   long long nPro = 0, nBody = 0;  // kernels in the prologue / in one loop iteration
   bool use_graphs = true;
-  bool dot_fold = false;   // pcg_iter_B: the fine post-smoothing pass writes r.z partials
+  bool dot_fold = false;
+  long long gather_ne = 1LL << 16;   // MG_OPT_GATHER_NE   // pcg_iter_B: the fine post-smoothing pass writes r.z partials
   int tail_start = -1;            // first level run by k_coarse_tail (-1: none)
   bool tail_vcycle = true;        // V-cycle levels >= tail_start through k_coarse_tail
   bool tail_lmax = true;          // their Chebyshev power iterations through k_tail_lmax
@@ -214,6 +215,7 @@ static void init_level(HostLevel& L, int nx, int ny, int p, double h, int kind) 
   d.orb = 0;
   d.So = d.Dco = d.Dso = nullptr;
   d.sweep = 0;
+  d.gather = 0;
   d.grid_cap = 0;
   d.ndi = 4 * d.k1 * (d.k1 + 1) / 2;
   L.h = h;
@@ -408,6 +410,16 @@ static void bind_pointers(Ctx* c) {
 // single CTA over <= 16x16 levels beats the per-step launches; multi-CTA
 // clusters and larger tails lose to them).  MGDTN_TAIL_VCYCLE=0 /
 // MGDTN_TAIL_LMAX=0 keep the V-cycle / the Chebyshev power iteration on launches.
+
+// gather-form apply (k_apply_gather) on the packed P1 levels with at most gather_ne
+// elements (MG_OPT_GATHER_NE), one-GPU or replicated
+static void plan_gather(Ctx* c) {
+  for (auto& L : c->lev) {
+    LevelDev& d = L.d;
+    d.gather = (!c->ns && !d.orb && d.p == 1 && d.imask == 0 && d.dmask == 15 &&
+                d.ne <= c->gather_ne) ? 1 : 0;
+  }
+}
 
 static void plan_tail(Ctx* c) {
   const char* env = std::getenv("MGDTN_TAIL_NE");
@@ -622,10 +634,19 @@ static void reduce_scal(Ctx* c, const double* partials, int n, double* scal, int
 // y three times, but measured slower than the pair (profiles/r02_sweep_probe.txt), so
 // it is off by default.
 static bool tiled(const LevelDev& d, int mode) { return tile_level(d) && mode == AM_SMOOTH; }
+// small P1 levels: one gather-form pass per apply / residual / smoothing step
+// (k_apply_gather) instead of the pair of colour passes
+static bool gathered(const LevelDev& d, int mode) {
+  return gather_level(d) && (mode == AM_APPLY || mode == AM_RESID || mode == AM_SMOOTH);
+}
 static void apply_mode(Ctx* c, const HostLevel& L, int mode, const double* x, double* y,
                        const double* r, double* d, int step, double* partials) {
   if (tiled(L.d, mode) && mode != AM_SMOOTH) {
     c->launches += launch_apply_tile(L.d, mode, x, y, r, d, nullptr, step, partials, c->st);
+    return;
+  }
+  if (gathered(L.d, mode) && !partials && mode != AM_SMOOTH) {
+    c->launches += launch_apply_gather(L.d, mode, x, y, r, d, nullptr, step, c->st);
     return;
   }
   if (L.clist && c->cst) {
@@ -712,6 +733,11 @@ static inline double* smooth_step(Ctx* c, HostLevel& L, int step, double* cur,
     double* out = other(L, cur);
     c->launches += launch_apply_tile(L.d, AM_SMOOTH, cur, nullptr, L.r, L.dv, out, slot, nullptr,
                                      c->st);
+    return out;
+  }
+  if (gathered(L.d, AM_SMOOTH) && !partials) {
+    double* out = other(L, cur);
+    c->launches += launch_apply_gather(L.d, AM_SMOOTH, cur, nullptr, L.r, L.dv, out, slot, c->st);
     return out;
   }
   apply_mode(c, L, AM_SMOOTH, cur, other(L, cur), L.r, L.dv, slot, partials);
@@ -1701,6 +1727,7 @@ int mg_build_hierarchy_ex(const mg_quad_mesh* mesh, int32_t p, int32_t n_h_level
   }
   plan_tail(c);
   plan_tail_dense(c);
+  plan_gather(c);
   // orbit storage (R9, d4.cuh): the finest level and its p-coarsened P1 level hold
   // D4-invariant element maps (uniform squares, scalar K per element)
   if (!c->ns) {
@@ -2207,6 +2234,10 @@ int mg_set_option(void* ctx, int32_t key, int64_t value) {
     if (value < 1) return fail(c, MG_ERR_ARG, "MG_OPT_COMM_TIMEOUT_MS must be >= 1");
     c->comm_timeout_s = (double)value * 1e-3;
     return MG_OK;
+  } else if (key == MG_OPT_GATHER_NE) {
+    if (value < 0) return fail(c, MG_ERR_ARG, "MG_OPT_GATHER_NE must be >= 0");
+    c->gather_ne = value;
+    plan_gather(c);
   } else if (key == MG_OPT_APPLY_GRID_CAP) {
     if (value < 0 || value > (1 << 20)) return fail(c, MG_ERR_ARG, "MG_OPT_APPLY_GRID_CAP out of range");
     for (auto& L : c->lev) L.d.grid_cap = (int)value;

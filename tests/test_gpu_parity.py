@@ -217,6 +217,43 @@ def test_exec_paths_parity(case, path):
         gpu.set_option(key, 0)
 
 
+def test_gather_apply_bitwise(case):
+    """The one-pass gather-form apply (k_apply_gather, MG_OPT_GATHER_NE) against the pair
+    of colour passes on every packed P1 level: apply, 1-3 smoothing steps and the whole
+    V-cycle agree bit for bit (same row sums in the same order, same combination order),
+    and the gather-form V-cycle matches the oracle."""
+    if case.cfg.n > 256:
+        pytest.skip("bitwise gather check at n <= 256")
+    gpu = case.gpu
+    big = 1 << 40
+
+    def run():
+        out = []
+        for level in range(case.N, 0, -1):
+            x = case.vec(level, case.cfg.seed_vec + level)
+            out.append(gpu.apply(level, torch.from_numpy(x)).cpu().numpy())
+            if level > 1:
+                r = case.vec(level, 100 + level)
+                e0 = case.vec(level, 200 + level)
+                for steps in (1, 2, 3):
+                    out.append(gpu.smooth(level, torch.from_numpy(r), torch.from_numpy(e0), steps).cpu().numpy())
+        out.append(gpu.vcycle(torch.from_numpy(case.vec(case.N, 600))).cpu().numpy())
+        return out
+
+    try:
+        gpu.set_option(gpu.OPT_GATHER_NE, 0)
+        pair = run()
+        gpu.set_option(gpu.OPT_GATHER_NE, big)
+        gath = run()
+    finally:
+        gpu.set_option(gpu.OPT_GATHER_NE, 1 << 16)
+    assert len(pair) == len(gath)
+    for k, (a, b) in enumerate(zip(pair, gath)):
+        assert np.array_equal(a, b), (k, np.max(np.abs(a - b)))
+    r = case.vec(case.N, 600)
+    assert rel(gath[-1][case.ts.free], case.H.vcycle(r[case.ts.free])) <= TOL_OP
+
+
 def test_rhs_parity(case):
     pr = case.pr
     g, lam_bc = case.gpu.assemble_rhs(pr.f_qp, pr.f_const, pr.gD_qp)
