@@ -105,7 +105,7 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
                                              const double* xv, const double* yv, const double* x,
                                              double* y, const double* __restrict__ r, double* d,
                                              const double* __restrict__ Dp, int step, double c1,
-                                             double c2, double& dot) {
+                                             double c2, double& dot, const PRArgs& pr) {
   using D = D4<P>;
   constexpr int K1 = P + 1, M = 4 * K1, NCS = D::NCS;
   constexpr bool HASD = MODE == AM_SMOOTH || MODE == AM_DINV || MODE == AM_GSC;
@@ -125,10 +125,7 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
 #pragma unroll
   for (int f = F0; f < F0 + NF; ++f)
     live[f] = !bd[f] && !((itf >> f) & 1) && (MODE != AM_GSC || ((gsm >> f) & 1));
-  // SMOOTH + DOT (the PCG's last fine smoothing step): dot += x_new . r over the
-  // pass's edges, r kept from the load phase
-  constexpr bool SDOT = DOT && MODE == AM_SMOOTH;
-  double t[M], dd[M], dv[HASD ? 4 * NCS : 1], rk[SDOT ? M : 1];
+  double t[M], dd[M], dv[HASD ? 4 * NCS : 1];
 #pragma unroll
   for (int f = F0; f < F0 + NF; ++f) {
     const int64_t base = ed[f] * K1;
@@ -142,10 +139,6 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
       ld_edge<K1>(y + base, yo);
       if (MODE != AM_APPLY && MODE != AM_DINV) ld_edge<K1>(r + base, rv);
       if (MODE == AM_SMOOTH && L.smoother == 1 && step > 0) ld_edge<K1>(d + base, dd + f * K1);
-    }
-    if (SDOT) {
-#pragma unroll
-      for (int a = 0; a < K1; ++a) rk[f * K1 + a] = rv[a];
     }
 #pragma unroll
     for (int a = 0; a < K1; ++a)
@@ -192,6 +185,27 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
       st_edge<K1>(y + base, v);
       continue;
     }
+    if (MODE == AM_RESPR) {   // p_restrict_body's arithmetic on this edge's residual
+      double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+      for (int a = 0; a < K1; ++a) {
+        const double rs = t[f * K1 + a] - yf[a];
+        v0 = fma(__ldg(pr.Jp + a * 2), rs, v0);
+        v1 = fma(__ldg(pr.Jp + a * 2 + 1), rs, v1);
+      }
+      const int64_t E = ed[f];
+      reinterpret_cast<double2*>(pr.rc)[E] = make_double2(v0, v1);
+      if (pr.fuse) {
+        const double* Di = pr.Dinv + E;
+        const int64_t sd = pr.nedge;
+        const double c2c = __ldg(pr.coef + 1);
+        double e0 = c2c * (__ldg(Di) * v0 + __ldg(Di + sd) * v1);
+        double e1 = c2c * (__ldg(Di + 2 * sd) * v0 + __ldg(Di + 3 * sd) * v1);
+        reinterpret_cast<double2*>(pr.ec)[E] = make_double2(e0, e1);
+        if (pr.smoother == 1) reinterpret_cast<double2*>(pr.dc)[E] = make_double2(e0, e1);
+      }
+      continue;
+    }
     double res[K1];
 #pragma unroll
     for (int a = 0; a < K1; ++a) {
@@ -218,7 +232,6 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
         if (L.smoother == 1 && step > 0) dn = fma(c1, dd[f * K1 + a], dn);
         dnv[a] = dn;
         xnv[a] = xf[a] + dn;
-        if (SDOT) dot = fma(xnv[a], rk[f * K1 + a], dot);
       }
     }
     if (MODE == AM_SMOOTH) {
@@ -232,7 +245,8 @@ template <int P, int MODE, bool DOT>
 __global__ void __launch_bounds__(32) k_apply_orb(const LevelDev L, int colour, const double* x,
                                                   double* y, const double* __restrict__ r,
                                                   double* d, int step,
-                                                  double* __restrict__ partials, int early) {
+                                                  double* __restrict__ partials, int early,
+                                                  const PRArgs pr) {
   using D = D4<P>;
   using C = OrbCfg<P>;
   constexpr int K1 = P + 1, M = 4 * K1, NORB = D::NORB, NCS = D::NCS, NST = C::NST;
@@ -354,10 +368,10 @@ __global__ void __launch_bounds__(32) k_apply_orb(const LevelDev L, int colour, 
       }
       const double* Dp = L.Dco + c * 4 * NCS * 32 + lane;
       if (MODE == AM_SMOOTH || MODE == AM_GSC) {   // two edges at a time (registers)
-        orb_epilogue<P, MODE, DOT, 0, 2>(L, ed, bd, itf, gsm, xv, yv, x, y, r, d, Dp, step, c1, c2, dot);
-        orb_epilogue<P, MODE, DOT, 2, 2>(L, ed, bd, itf, gsm, xv, yv, x, y, r, d, Dp, step, c1, c2, dot);
+        orb_epilogue<P, MODE, DOT, 0, 2>(L, ed, bd, itf, gsm, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr);
+        orb_epilogue<P, MODE, DOT, 2, 2>(L, ed, bd, itf, gsm, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr);
       } else {
-        orb_epilogue<P, MODE, DOT>(L, ed, bd, itf, gsm, xv, yv, x, y, r, d, Dp, step, c1, c2, dot);
+        orb_epilogue<P, MODE, DOT>(L, ed, bd, itf, gsm, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr);
       }
     }
   }
@@ -838,7 +852,7 @@ static void launch_one(const LevelDev& L, int colour, const double* x, double* y
   if (L.orb) {
     orb_resident<P, MODE, DOT>();
     launch_ex(k_apply_orb<P, MODE, DOT>, grid, 32, (size_t)OrbCfg<P>::NST * OrbCfg<P>::STAGE_BYTES,
-              pdl, st, L, colour, x, y, r, d, step, partials, early);
+              pdl, st, L, colour, x, y, r, d, step, partials, early, PRArgs{});
     return;
   }
   if (MODE == AM_GSC || use_seg(MODE, P)) {
@@ -880,14 +894,7 @@ static void dispatch_apply(const LevelDev& L, int colour, int mode, const double
       launch_one<P, AM_GSC, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
       break;
     default:
-      if (partials && L.orb) {   // (only the orbit kernel has the SMOOTH + DOT epilogue)
-        orb_resident<P, AM_SMOOTH, true>();
-        launch_ex(k_apply_orb<P, AM_SMOOTH, true>, grid, 32,
-                  (size_t)OrbCfg<P>::NST * OrbCfg<P>::STAGE_BYTES, pdl, st, L, colour, x, y, r, d,
-                  step, partials, pdl ? 1 : 0);
-      } else {
-        launch_one<P, AM_SMOOTH, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
-      }
+      launch_one<P, AM_SMOOTH, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
       break;
   }
 }
@@ -906,6 +913,32 @@ int launch_apply(const LevelDev& L, int colour, int mode, const double* x, doubl
 }
 
 int apply2_grid(const LevelDev& L, int mode) { return apply_grid_mode(L, mode); }
+
+// residual + p-restriction (AM_RESPR): colour-0 pass, then the colour-1 pass whose
+// epilogue restricts each edge's residual instead of storing it
+template <int P>
+static void launch_respr(const LevelDev& F, const double* x, double* y, const double* r,
+                         const PRArgs& pr, cudaStream_t st) {
+  const int grid = apply_grid_mode(F, AM_RESID);
+  orb_resident<P, AM_RESPR, false>();
+  launch_ex(k_apply_orb<P, AM_RESPR, false>, grid, 32,
+            (size_t)OrbCfg<P>::NST * OrbCfg<P>::STAGE_BYTES, true, st, F, 1, x, y, r,
+            (double*)nullptr, 0, (double*)nullptr, 1, pr);
+}
+
+int launch_resid_prestrict(const LevelDev& F, const LevelDev& C, const double* Jp, const double* x,
+                           double* y, const double* r, double* rc, bool fuse, double* ec,
+                           double* dc, cudaStream_t st) {
+  if (!F.orb || F.imask || F.p < 2) return -1;
+  PRArgs pr{Jp, rc, ec, dc, C.Dinv, C.coef, C.nedge, fuse ? 1 : 0, C.smoother};
+  int n = launch_apply(F, 0, AM_W0, x, y, nullptr, nullptr, 0, nullptr, true, st);
+  switch (F.p) {
+    case 2: launch_respr<2>(F, x, y, r, pr, st); break;
+    case 3: launch_respr<3>(F, x, y, r, pr, st); break;
+    default: launch_respr<4>(F, x, y, r, pr, st); break;
+  }
+  return n + 1;
+}
 
 // ---------------------------------------------------------------- gather-form apply (small P1 levels)
 // One pass, thread per edge: an interior edge's output is the sum of the two rows of

@@ -27,8 +27,23 @@ enum ApplyMode : int {
   AM_RESID = 2,   // pass 1: w[e] = r[e] - (w[e] + (S_T x_T)[e])
   AM_SMOOTH = 3,  // pass 1: d = c1 d + c2 Dinv (r - A x)_e ; x[e] += d  (in place)
   AM_DINV = 4,    // pass 1: y[e] = (A x)_e ; x[e] = Dinv (A x)_e (in place; power iteration)
-  AM_GSC = 5      // pass 1, LU-SGS colour sweep: on edges of colour `step` only,
+  AM_GSC = 5,     // pass 1, LU-SGS colour sweep: on edges of colour `step` only,
                   // x[e] += omega Dinv (r - A x)_e (in place; segmented-ring kernel only)
+  AM_RESPR = 6    // pass 1 (orbit levels): res_e = r - A x, then the p-restriction
+                  // rc_e = J_p^T res_e (+ the coarse level's first smoothing step); res
+                  // itself is not stored (PRArgs)
+};
+
+// AM_RESPR: the p-coarse level's restriction target (bodies.cuh p_restrict_body)
+struct PRArgs {
+  const double* Jp;     // K1 x 2 (row a: the two P1 coefficients of dof a)
+  double* rc;           // coarse residual (2 per edge)
+  double* ec;           // fuse: coarse first smoothing step e = c2 D^-1 rc
+  double* dc;           // fuse, Chebyshev: its direction d = e
+  const double* Dinv;   // coarse D_e^-1 (SoA, stride nedge)
+  const double* coef;   // coarse smoothing coefficients (coef[1] = c2 of step 0)
+  int64_t nedge;
+  int fuse, smoother;
 };
 
 // LU-SGS colour of local edge f of element (i,j): horizontal edges of even / odd
@@ -330,6 +345,11 @@ int apply_grid_mode(const LevelDev& L, int mode);   // blocks of a colour pass i
 int launch_apply2(const LevelDev& L, int mode, const double* x, double* y, const double* r,
                   double* d, int step, double* partials, bool pdl, cudaStream_t st);
 int apply2_grid(const LevelDev& L, int mode);  // blocks of launch_apply2 (partials length)
+// residual + p-restriction in the pair of colour passes of an orbit level (AM_RESPR);
+// y is scratch for the colour-0 partial sums
+int launch_resid_prestrict(const LevelDev& F, const LevelDev& C, const double* Jp, const double* x,
+                           double* y, const double* r, double* rc, bool fuse, double* ec,
+                           double* dc, cudaStream_t st);
 // single-pass tiled apply on a one-GPU orbit level (k_tile.cu): AM_APPLY (y = A x, dot
 // x.y into partials if given), AM_RESID (y = r - A x), AM_SMOOTH (xo = x + d, out of place)
 bool tile_level(const LevelDev& L);

@@ -87,8 +87,7 @@ struct Ctx {
   cudaGraphConditionalHandle cond = 0;
   long long nPro = 0, nBody = 0;  // kernels in the prologue / in one loop iteration
   bool use_graphs = true;
-  bool dot_fold = false;
-  long long gather_ne = 1LL << 16;   // MG_OPT_GATHER_NE   // pcg_iter_B: the fine post-smoothing pass writes r.z partials
+  long long gather_ne = 1LL << 16;   // MG_OPT_GATHER_NE
   int tail_start = -1;            // first level run by k_coarse_tail (-1: none)
   bool tail_vcycle = true;        // V-cycle levels >= tail_start through k_coarse_tail
   bool tail_lmax = true;          // their Chebyshev power iterations through k_tail_lmax
@@ -713,11 +712,8 @@ static inline void apply_full(Ctx* c, const HostLevel& L, const double* x, doubl
 // two-colour passes update it in place (and use the other vector as scratch).
 static inline double* other(const HostLevel& L, const double* cur) { return cur == L.e ? L.w : L.e; }
 
-// one smoothing step on the iterate `cur`; returns where the new iterate is.  With
-// `partials` (two-colour orbit level, pcg_dot_fold): the colour-1 pass also writes the
-// per-CTA partial sums of x_new . L.r
-static inline double* smooth_step(Ctx* c, HostLevel& L, int step, double* cur,
-                                  double* partials = nullptr) {
+// one smoothing step on the iterate `cur`; returns where the new iterate is
+static inline double* smooth_step(Ctx* c, HostLevel& L, int step, double* cur) {
   if (c->sm.kind == MG_SMOOTH_LUSGS) {
     // one LU-SGS step: forward block Gauss-Seidel sweep over the
     // four edge colours, then backward (oracle/multigrid.py)
@@ -735,12 +731,12 @@ static inline double* smooth_step(Ctx* c, HostLevel& L, int step, double* cur,
                                      c->st);
     return out;
   }
-  if (gathered(L.d, AM_SMOOTH) && !partials) {
+  if (gathered(L.d, AM_SMOOTH)) {
     double* out = other(L, cur);
     c->launches += launch_apply_gather(L.d, AM_SMOOTH, cur, nullptr, L.r, L.dv, out, slot, c->st);
     return out;
   }
-  apply_mode(c, L, AM_SMOOTH, cur, other(L, cur), L.r, L.dv, slot, partials);
+  apply_mode(c, L, AM_SMOOTH, cur, other(L, cur), L.r, L.dv, slot, nullptr);
   return cur;
 }
 
@@ -846,16 +842,23 @@ static double* vcycle_level(Ctx* c, int li, bool first_done) {
   }
   double* cur = L.e;
   for (int s = s0; s < nu_pre; ++s) cur = smooth_step(c, L, s, cur);
-  double* res = residual(c, L, cur);  // r - A e1
   HostLevel& C = c->lev[li + 1];
   const bool fuse = (li + 1 < nlev - 1) && nu_at(c, c->sm.nu_pre, li + 1) > 0 &&
                     c->sm.kind != MG_SMOOTH_LUSGS &&
                     !(c->tail_dense && li + 1 == c->tail_start) && !gathers(c, li);
-  restrict_level(c, li, res, cur, true, C.r, fuse);
+  if (L.kind == KIND_P && L.d.orb && L.d.imask == 0 && !L.clist && !gathers(c, li) &&
+      !partitioned(c)) {
+    // residual and p-restriction in one pair of passes: the colour-1 epilogue restricts
+    // each edge's residual r - A e1 (Eq. 3.6 with the P1 injection J_p) instead of storing it
+    c->launches += launch_resid_prestrict(L.d, C.d, c->refdev.Jp, cur, other(L, cur), L.r, C.r, fuse,
+                                          C.e, C.dv, c->st);
+  } else {
+    double* res = residual(c, L, cur);  // r - A e1
+    restrict_level(c, li, res, cur, true, C.r, fuse);
+  }
   const double* ec = vcycle_level(c, li + 1, fuse);
   prolong_level(c, li, ec, cur);
-  for (int s = 0; s < nu_post; ++s)
-    cur = smooth_step(c, L, s, cur, li == 0 && c->dot_fold && s == nu_post - 1 ? c->part : nullptr);
+  for (int s = 0; s < nu_post; ++s) cur = smooth_step(c, L, s, cur);
   return cur;
 }
 
@@ -1096,27 +1099,15 @@ static void pcg_iter_A(Ctx* c) {  // Ap, alpha, x/r update, rr
   reduce_scal(c, c->part, vg, c->scal, 2, 0);
 }
 
-// r.z folded into the V-cycle's last fine smoothing pass (its colour-1 epilogue visits
-// every interior edge once; dOmega rows of r and z are 0): a one-GPU two-colour orbit
-// fine level with a post-smoothing step that the launch-per-step V-cycle runs
-static bool pcg_dot_fold(const Ctx* c) {
-  const HostLevel& F = c->lev[0];
-  return pcg_sf(c) && !partitioned(c) && F.d.imask == 0 && !F.clist && c->sm.nu_post > 0 &&
-         !tiled(F.d, AM_SMOOTH);
-}
-
+// (r.z stays a separate k_dot pass: folding it into the last fine smoothing pass
+// (SMOOTH + DOT epilogue) cost that pass 0.53 ms against k_dot's 0.38 ms at config 5,
+// register pressure; profiles/r02_c5_iteration_launches.txt)
 static void pcg_iter_B(Ctx* c) {  // z = B r, beta, p update
   HostLevel& F = c->lev[0];
   const int vg = vec_grid(F.d.ndof);
-  c->dot_fold = pcg_dot_fold(c);
   const double* z = vcycle_level(c, 0, pcg_sf(c));   // first step done by the update
-  if (c->dot_fold) {
-    reduce_scal(c, c->part, apply_grid_mode(F.d, AM_SMOOTH), c->scal, 0, 2);
-  } else {
-    c->launches += launch_dot(F.r, z, F.d.ndof, c->part, vg, c->st, &F.d);
-    reduce_scal(c, c->part, vg, c->scal, 0, 2);
-  }
-  c->dot_fold = false;
+  c->launches += launch_dot(F.r, z, F.d.ndof, c->part, vg, c->st, &F.d);
+  reduce_scal(c, c->part, vg, c->scal, 0, 2);
   c->launches += launch_pcg_pupdate(c->pv, z, c->scal, F.d.ndof, c->st);
 }
 
