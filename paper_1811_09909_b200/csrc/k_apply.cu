@@ -382,6 +382,147 @@ __global__ void __launch_bounds__(32) k_apply_orb(const LevelDev L, int colour, 
   }
 }
 
+// Two-warp variant of the colour-1 smoothing pass (k_apply_orb2): both warps of a CTA work on the
+// same chunk, warp w computing the rows of edges 2w, 2w+1 (each row summed over all
+// columns in increasing order, i.e. bitwise the rows of the symmetric loop above) and
+// running the epilogue of those two edges.  Half the accumulators and half the epilogue
+// per thread (228 instead of 255 registers; still 8 warps per SM), and the two warps'
+// epilogue loads overlap each other's row sums (the one-warp pass sits at 2 warps per
+// scheduler, 87 % of cycles with no eligible warp; profiles/r02_orb2.txt).
+template <int P, int MODE, bool DOT, int W>
+__device__ __forceinline__ void orb2_rows(const double* Sp, const double* xv, double* yv) {
+  using D = D4<P>;
+  constexpr int K1 = P + 1, M = 4 * K1;
+#pragma unroll
+  for (int a = 2 * W * K1; a < 2 * W * K1 + 2 * K1; ++a) {
+    double acc = 0.0;
+#pragma unroll
+    for (int b = 0; b < M; ++b) {
+      const int lo = a < b ? a : b, hi = a < b ? b : a;
+      acc = fma(Sp[D::orb(D::pk(lo, hi)) * 32], xv[b], acc);
+    }
+    yv[a] = acc;
+  }
+}
+
+#ifndef ORB2_MINB
+#define ORB2_MINB 4
+#endif
+template <int P, int MODE, bool DOT>
+__global__ void __launch_bounds__(64, ORB2_MINB) k_apply_orb2(const LevelDev L, int colour, const double* x,
+                                                   double* y, const double* __restrict__ r,
+                                                   double* d, int step,
+                                                   double* __restrict__ partials, int early,
+                                                   const PRArgs pr) {
+  using D = D4<P>;
+  using C = OrbCfg<P>;
+  constexpr int K1 = P + 1, M = 4 * K1, NORB = D::NORB, NCS = D::NCS, NST = C::NST;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bars[NST];
+  __shared__ double dsum[2];
+  double* stage_buf = reinterpret_cast<double*>(smem_raw);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t nec = L.ne >> 1;
+  const int nchunk = L.nchunk;
+  const double* Sbase = L.So + (int64_t)colour * nchunk * NORB * 32;
+  const uint64_t pol = evict_first_policy();
+  const int G = (int)gridDim.x, b = (int)blockIdx.x;
+  const int nmine = b < nchunk ? (nchunk - 1 - b) / G + 1 : 0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int k) {   // thread 0: chunk b + k*G into stage k % NST
+    const int s = k % NST;
+    const int64_t c = b + (int64_t)k * G;
+    mbar_expect_tx(&bars[s], (uint32_t)C::STAGE_BYTES);
+    tma_bulk_g2s(stage_buf + (size_t)s * NORB * 32, Sbase + c * NORB * 32, C::STAGE_BYTES,
+                 &bars[s], pol);
+  };
+  if (early) {
+    if (threadIdx.x == 0)
+      for (int k = 0; k < NST && k < nmine; ++k) issue(k);
+    pdl_trigger();
+    pdl_wait();
+  } else {
+    pdl_wait();
+    if (threadIdx.x == 0)
+      for (int k = 0; k < NST && k < nmine; ++k) issue(k);
+    pdl_trigger();
+  }
+  double c1 = 0.0, c2 = 0.0;
+  if (MODE == AM_SMOOTH) {
+    c1 = L.coef[2 * step];
+    c2 = L.coef[2 * step + 1];
+  }
+  double dot = 0.0;
+  int64_t edn[4] = {0, 0, 0, 0};
+  bool bdn[4] = {true, true, true, true};
+  double xn[M];
+  auto prefetch = [&](int k) {
+#pragma unroll
+    for (int a = 0; a < M; ++a) xn[a] = 0.0;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      edn[f] = 0;
+      bdn[f] = true;
+    }
+    if (k >= nmine) return;
+    const int64_t s = (b + (int64_t)k * G) * 32 + lane;
+    if (s < nec) {
+      int ei, ej;
+      slot_elem(L.nx, colour, s, ei, ej);
+      elem_edges(L.nx, L.ny, ei, ej, edn, bdn, L.dmask);
+      gather_x<K1>(x, edn, bdn, xn);
+    }
+  };
+  prefetch(0);
+  for (int k = 0; k < nmine; ++k) {
+    const int64_t c = b + (int64_t)k * G;
+    const bool act = c * 32 + lane < nec;
+    int64_t ed[4];
+    bool bd[4];
+    double xv[M], yv[M];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      ed[f] = edn[f];
+      bd[f] = bdn[f];
+    }
+#pragma unroll
+    for (int a = 0; a < M; ++a) {
+      xv[a] = xn[a];
+      yv[a] = 0.0;
+    }
+    prefetch(k + 1);
+    const int st = k % NST;
+    mbar_wait(&bars[st], (uint32_t)((k / NST) & 1));
+    const double* Sp = stage_buf + (size_t)st * NORB * 32 + lane;
+    if (w == 0) orb2_rows<P, MODE, DOT, 0>(Sp, xv, yv);
+    else orb2_rows<P, MODE, DOT, 1>(Sp, xv, yv);
+    __syncthreads();   // both warps are done with stage st
+    if (threadIdx.x == 0 && k + NST < nmine) {
+      fence_proxy_async();
+      issue(k + NST);
+    }
+    if (act) {
+      const double* Dp = L.Dco + c * 4 * NCS * 32 + lane;
+      if (w == 0)
+        orb_epilogue<P, MODE, DOT, 0, 2>(L, ed, bd, 0, 0, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr);
+      else
+        orb_epilogue<P, MODE, DOT, 2, 2>(L, ed, bd, 0, 0, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr);
+    }
+  }
+  if (DOT) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if (lane == 0) dsum[w] = dot;
+    __syncthreads();
+    if (threadIdx.x == 0) partials[blockIdx.x] = dsum[0] + dsum[1];
+  }
+}
+
 // ---------------------------------------------------------------- whole-chunk TMA apply (packed levels)
 template <int P>
 struct TmaCfg {
@@ -800,10 +941,30 @@ static int balanced_grid(int64_t n, int64_t gmax) {
   return (int)((n + k - 1) / k);
 }
 
+// two-warp colour-1 smoothing pass (k_apply_orb2): one-GPU orbit levels at p = 4.
+// Config 5: 2.32-2.62 vs 2.48-2.89 ms per pass, solve 883 vs 902 ms / 30 iterations; the
+// other colour-1 modes (APPLY + DOT 1.53 vs 1.24 ms, RESPR 2.46 vs 2.14 ms) and p = 3
+// (config 4: 95.9 vs 94.4 ms) measured slower (profiles/r02_orb2.txt)
+static bool orb2_on(const LevelDev& L, int mode) {
+  return L.orb && L.p == 4 && !L.imask && !L.clist && mode == AM_SMOOTH;
+}
+template <int P, int MODE, bool DOT>
+static int orb2_resident() {
+  static int v = 0;
+  if (v == 0) v = resident(k_apply_orb2<P, MODE, DOT>, (size_t)OrbCfg<P>::NST * OrbCfg<P>::STAGE_BYTES);
+  return v;
+}
+template <int P>
+static int orb2_cps(int) {
+  if constexpr (P != 4) return 1;
+  else return orb2_resident<P, AM_SMOOTH, false>();
+}
+
 // CTAs per SM of a pass: the configured count, capped by what is resident
 template <int P>
 static int cps_of(const LevelDev& L, int mode) {
   const bool hd = mode_has_dinv(mode);
+  if (orb2_on(L, mode)) return orb2_cps<P>(mode);
   if (L.orb) {
     const int res = hd ? orb_resident<P, AM_SMOOTH, false>() : orb_resident<P, AM_APPLY, true>();
     return OrbCfg<P>::CPS < res ? OrbCfg<P>::CPS : res;
@@ -850,6 +1011,15 @@ static void launch_one(const LevelDev& L, int colour, const double* x, double* y
     return;
   }
   if (L.orb) {
+    if constexpr (P == 4 && MODE == AM_SMOOTH && !DOT) {
+      if (colour == 1 && orb2_on(L, MODE)) {
+        orb2_resident<P, MODE, DOT>();
+        launch_ex(k_apply_orb2<P, MODE, DOT>, grid, 64,
+                  (size_t)OrbCfg<P>::NST * OrbCfg<P>::STAGE_BYTES, pdl, st, L, colour, x, y, r, d,
+                  step, partials, early, PRArgs{});
+        return;
+      }
+    }
     orb_resident<P, MODE, DOT>();
     launch_ex(k_apply_orb<P, MODE, DOT>, grid, 32, (size_t)OrbCfg<P>::NST * OrbCfg<P>::STAGE_BYTES,
               pdl, st, L, colour, x, y, r, d, step, partials, early, PRArgs{});
@@ -919,7 +1089,7 @@ int apply2_grid(const LevelDev& L, int mode) { return apply_grid_mode(L, mode); 
 template <int P>
 static void launch_respr(const LevelDev& F, const double* x, double* y, const double* r,
                          const PRArgs& pr, cudaStream_t st) {
-  const int grid = apply_grid_mode(F, AM_RESID);
+  const int grid = apply_grid_mode(F, AM_RESPR);
   orb_resident<P, AM_RESPR, false>();
   launch_ex(k_apply_orb<P, AM_RESPR, false>, grid, 32,
             (size_t)OrbCfg<P>::NST * OrbCfg<P>::STAGE_BYTES, true, st, F, 1, x, y, r,
