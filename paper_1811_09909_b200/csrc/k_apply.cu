@@ -196,11 +196,16 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
       const int64_t E = ed[f];
       reinterpret_cast<double2*>(pr.rc)[E] = make_double2(v0, v1);
       if (pr.fuse) {
-        const double* Di = pr.Dinv + E;
+        // the coarse P1 orbit level's D_e^-1 (k_dinv_orb: its full SoA blocks hold exactly
+        // these centrosymmetric orbit values, so this is p_restrict_body's arithmetic)
+        using D1 = D4<1>;
+        const double* Do = pr.Dso + E;
         const int64_t sd = pr.nedge;
         const double c2c = __ldg(pr.coef + 1);
-        double e0 = c2c * (__ldg(Di) * v0 + __ldg(Di + sd) * v1);
-        double e1 = c2c * (__ldg(Di + 2 * sd) * v0 + __ldg(Di + 3 * sd) * v1);
+        const double q00 = __ldg(Do + D1::cs(D1::pe(0, 0)) * sd), q01 = __ldg(Do + D1::cs(D1::pe(0, 1)) * sd);
+        const double q10 = __ldg(Do + D1::cs(D1::pe(1, 0)) * sd), q11 = __ldg(Do + D1::cs(D1::pe(1, 1)) * sd);
+        double e0 = c2c * (q00 * v0 + q01 * v1);
+        double e1 = c2c * (q10 * v0 + q11 * v1);
         reinterpret_cast<double2*>(pr.ec)[E] = make_double2(e0, e1);
         if (pr.smoother == 1) reinterpret_cast<double2*>(pr.dc)[E] = make_double2(e0, e1);
       }
@@ -1100,7 +1105,8 @@ int launch_resid_prestrict(const LevelDev& F, const LevelDev& C, const double* J
                            double* y, const double* r, double* rc, bool fuse, double* ec,
                            double* dc, cudaStream_t st) {
   if (!F.orb || F.imask || F.p < 2) return -1;
-  PRArgs pr{Jp, rc, ec, dc, C.Dinv, C.coef, C.nedge, fuse ? 1 : 0, C.smoother};
+  if (!C.orb || C.p != 1 || !C.Dso) return -1;
+  PRArgs pr{Jp, rc, ec, dc, C.Dso, C.coef, C.nedge, fuse ? 1 : 0, C.smoother};
   int n = launch_apply(F, 0, AM_W0, x, y, nullptr, nullptr, 0, nullptr, true, st);
   switch (F.p) {
     case 2: launch_respr<2>(F, x, y, r, pr, st); break;

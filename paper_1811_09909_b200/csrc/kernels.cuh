@@ -40,7 +40,7 @@ struct PRArgs {
   double* rc;           // coarse residual (2 per edge)
   double* ec;           // fuse: coarse first smoothing step e = c2 D^-1 rc
   double* dc;           // fuse, Chebyshev: its direction d = e
-  const double* Dinv;   // coarse D_e^-1 (SoA, stride nedge)
+  const double* Dso;    // coarse P1 orbit level's D_e^-1 orbits (SoA, stride nedge)
   const double* coef;   // coarse smoothing coefficients (coef[1] = c2 of step 0)
   int64_t nedge;
   int fuse, smoother;

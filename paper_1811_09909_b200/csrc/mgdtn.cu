@@ -847,7 +847,7 @@ static double* vcycle_level(Ctx* c, int li, bool first_done) {
                     c->sm.kind != MG_SMOOTH_LUSGS &&
                     !(c->tail_dense && li + 1 == c->tail_start) && !gathers(c, li);
   if (L.kind == KIND_P && L.d.orb && L.d.imask == 0 && !L.clist && !gathers(c, li) &&
-      !partitioned(c)) {
+      !partitioned(c) && C.d.orb && C.d.p == 1) {
     // residual and p-restriction in one pair of passes: the colour-1 epilogue restricts
     // each edge's residual r - A e1 (Eq. 3.6 with the P1 injection J_p) instead of storing it
     c->launches += launch_resid_prestrict(L.d, C.d, c->refdev.Jp, cur, other(L, cur), L.r, C.r, fuse,
