@@ -109,13 +109,15 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
   using D = D4<P>;
   constexpr int K1 = P + 1, M = 4 * K1, NCS = D::NCS;
   constexpr bool HASD = MODE == AM_SMOOTH || MODE == AM_DINV || MODE == AM_GSC;
-  if (MODE == AM_W0) {
+  if (MODE == AM_W0 || MODE == AM_W0P) {
 #pragma unroll
     for (int f = F0; f < F0 + NF; ++f) {
       double v[K1];
 #pragma unroll
       for (int a = 0; a < K1; ++a) v[a] = bd[f] ? 0.0 : yv[f * K1 + a];
       st_edge<K1>(y + ed[f] * K1, v);
+      // W0P: the prolonged iterate goes back to x (dOmega rows stay untouched)
+      if (MODE == AM_W0P && !bd[f]) st_edge<K1>(const_cast<double*>(x) + ed[f] * K1, xv + f * K1);
     }
     return;
   }
@@ -326,6 +328,16 @@ __global__ void __launch_bounds__(32) k_apply_orb(const LevelDev L, int colour, 
       elem_edges(L.nx, L.ny, ein, ejn, edn, bdn, L.dmask);
       itfn = elem_itf(L.nx, L.ny, ein, ejn, L.imask);
       gather_x<K1>(x, edn, bdn, xn);
+      if (MODE == AM_W0P) {   // x_e + J_p ec_e (p_prolong_body's arithmetic)
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          if (bdn[f]) continue;
+          const double2 cc = __ldg(reinterpret_cast<const double2*>(pr.ec) + edn[f]);
+#pragma unroll
+          for (int a = 0; a < K1; ++a)
+            xn[f * K1 + a] += fma(__ldg(pr.Jp + a * 2), cc.x, __ldg(pr.Jp + a * 2 + 1) * cc.y);
+        }
+      }
     }
   };
   prefetch(0);
@@ -1088,6 +1100,30 @@ int launch_apply(const LevelDev& L, int colour, int mode, const double* x, doubl
 }
 
 int apply2_grid(const LevelDev& L, int mode) { return apply_grid_mode(L, mode); }
+
+template <int P>
+static void launch_w0p(const LevelDev& F, const double* x, double* y, const PRArgs& pr,
+                       cudaStream_t st) {
+  const int grid = apply_grid_mode(F, AM_W0);
+  orb_resident<P, AM_W0P, false>();
+  launch_ex(k_apply_orb<P, AM_W0P, false>, grid, 32,
+            (size_t)OrbCfg<P>::NST * OrbCfg<P>::STAGE_BYTES, true, st, F, 0, x, y,
+            (const double*)nullptr, (double*)nullptr, 0, (double*)nullptr, 1, pr);
+}
+
+int launch_w0_prolong(const LevelDev& F, const double* Jp, const double* ec, double* x, double* y,
+                      cudaStream_t st) {
+  if (!F.orb || F.imask || F.p < 2) return -1;
+  PRArgs pr{};
+  pr.Jp = Jp;
+  pr.ec = const_cast<double*>(ec);
+  switch (F.p) {
+    case 2: launch_w0p<2>(F, x, y, pr, st); break;
+    case 3: launch_w0p<3>(F, x, y, pr, st); break;
+    default: launch_w0p<4>(F, x, y, pr, st); break;
+  }
+  return 1;
+}
 
 // residual + p-restriction (AM_RESPR): colour-0 pass, then the colour-1 pass whose
 // epilogue restricts each edge's residual instead of storing it

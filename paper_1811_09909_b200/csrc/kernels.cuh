@@ -29,9 +29,11 @@ enum ApplyMode : int {
   AM_DINV = 4,    // pass 1: y[e] = (A x)_e ; x[e] = Dinv (A x)_e (in place; power iteration)
   AM_GSC = 5,     // pass 1, LU-SGS colour sweep: on edges of colour `step` only,
                   // x[e] += omega Dinv (r - A x)_e (in place; segmented-ring kernel only)
-  AM_RESPR = 6    // pass 1 (orbit levels): res_e = r - A x, then the p-restriction
+  AM_RESPR = 6,   // pass 1 (orbit levels): res_e = r - A x, then the p-restriction
                   // rc_e = J_p^T res_e (+ the coarse level's first smoothing step); res
                   // itself is not stored (PRArgs)
+  AM_W0P = 7      // pass 0 (orbit levels) with the p-prolongation folded in: x_e += J_p ec_e
+                  // on the element's edges as they are gathered, stored back, then y = S x
 };
 
 // AM_RESPR: the p-coarse level's restriction target (bodies.cuh p_restrict_body)
@@ -347,6 +349,11 @@ int launch_apply2(const LevelDev& L, int mode, const double* x, double* y, const
 int apply2_grid(const LevelDev& L, int mode);  // blocks of launch_apply2 (partials length)
 // residual + p-restriction in the pair of colour passes of an orbit level (AM_RESPR);
 // y is scratch for the colour-0 partial sums
+// colour-0 pass with the p-prolongation x += J_p ec folded in (AM_W0P): afterwards x
+// holds the prolonged iterate on every edge (each edge has one colour-0 element) and y
+// the colour-0 partial sums of A x, as after p_prolong + the colour-0 pass
+int launch_w0_prolong(const LevelDev& F, const double* Jp, const double* ec, double* x, double* y,
+                      cudaStream_t st);
 int launch_resid_prestrict(const LevelDev& F, const LevelDev& C, const double* Jp, const double* x,
                            double* y, const double* r, double* rc, bool fuse, double* ec,
                            double* dc, cudaStream_t st);

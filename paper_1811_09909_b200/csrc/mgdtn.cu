@@ -857,8 +857,19 @@ static double* vcycle_level(Ctx* c, int li, bool first_done) {
     restrict_level(c, li, res, cur, true, C.r, fuse);
   }
   const double* ec = vcycle_level(c, li + 1, fuse);
-  prolong_level(c, li, ec, cur);
-  for (int s = 0; s < nu_post; ++s) cur = smooth_step(c, L, s, cur);
+  int s1 = 0;
+  if (nu_post > 0 && L.kind == KIND_P && L.d.orb && L.d.imask == 0 && !L.clist &&
+      !gathers(c, li) && !partitioned(c) && c->sm.kind != MG_SMOOTH_LUSGS &&
+      !tiled(L.d, AM_SMOOTH)) {
+    // the p-prolongation folded into the first post-smoothing step's colour-0 pass
+    c->launches += launch_w0_prolong(L.d, c->refdev.Jp, ec, cur, other(L, cur), c->st);
+    c->launches += launch_apply(L.d, 1, AM_SMOOTH, cur, other(L, cur), L.r, L.dv, 0, nullptr, true,
+                                c->st);
+    s1 = 1;
+  } else {
+    prolong_level(c, li, ec, cur);
+  }
+  for (int s = s1; s < nu_post; ++s) cur = smooth_step(c, L, s, cur);
   return cur;
 }
 
