@@ -109,15 +109,17 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
   using D = D4<P>;
   constexpr int K1 = P + 1, M = 4 * K1, NCS = D::NCS;
   constexpr bool HASD = MODE == AM_SMOOTH || MODE == AM_DINV || MODE == AM_GSC;
-  if (MODE == AM_W0 || MODE == AM_W0P) {
+  if (MODE == AM_W0 || MODE == AM_W0P || MODE == AM_W0U) {
 #pragma unroll
     for (int f = F0; f < F0 + NF; ++f) {
       double v[K1];
 #pragma unroll
       for (int a = 0; a < K1; ++a) v[a] = bd[f] ? 0.0 : yv[f * K1 + a];
       st_edge<K1>(y + ed[f] * K1, v);
-      // W0P: the prolonged iterate goes back to x (dOmega rows stay untouched)
-      if (MODE == AM_W0P && !bd[f]) st_edge<K1>(const_cast<double*>(x) + ed[f] * K1, xv + f * K1);
+      // W0P / W0U: the prolonged iterate / new direction goes back to x (dOmega rows stay
+      // untouched)
+      if ((MODE == AM_W0P || MODE == AM_W0U) && !bd[f])
+        st_edge<K1>(const_cast<double*>(x) + ed[f] * K1, xv + f * K1);
     }
     return;
   }
@@ -305,6 +307,7 @@ __global__ void __launch_bounds__(32) k_apply_orb(const LevelDev L, int colour, 
   } else if (MODE == AM_GSC) {
     c2 = L.coef[1];   // omega (block-Jacobi coefficients)
   }
+  const double beta = MODE == AM_W0U ? pr.coef[4] : 0.0;   // (after the dependency wait)
   double dot = 0.0;
   // software pipeline: the x gather of chunk k+1 is issued before the matvec of chunk k
   // (x of a same-colour element is never written by another same-colour element)
@@ -336,6 +339,16 @@ __global__ void __launch_bounds__(32) k_apply_orb(const LevelDev L, int colour, 
 #pragma unroll
           for (int a = 0; a < K1; ++a)
             xn[f * K1 + a] += fma(__ldg(pr.Jp + a * 2), cc.x, __ldg(pr.Jp + a * 2 + 1) * cc.y);
+        }
+      }
+      if (MODE == AM_W0U) {   // p_e = z_e + beta p_e (k_pcg_pupdate's arithmetic)
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          if (bdn[f]) continue;
+          double zv[K1];
+          ld_edge<K1>(pr.ec + edn[f] * K1, zv);
+#pragma unroll
+          for (int a = 0; a < K1; ++a) xn[f * K1 + a] = fma(beta, xn[f * K1 + a], zv[a]);
         }
       }
     }
@@ -1121,6 +1134,31 @@ int launch_w0_prolong(const LevelDev& F, const double* Jp, const double* ec, dou
     case 2: launch_w0p<2>(F, x, y, pr, st); break;
     case 3: launch_w0p<3>(F, x, y, pr, st); break;
     default: launch_w0p<4>(F, x, y, pr, st); break;
+  }
+  return 1;
+}
+
+template <int P>
+static void launch_w0u(const LevelDev& F, const double* x, double* y, const PRArgs& pr,
+                       cudaStream_t st) {
+  const int grid = apply_grid_mode(F, AM_W0);
+  orb_resident<P, AM_W0U, false>();
+  launch_ex(k_apply_orb<P, AM_W0U, false>, grid, 32,
+            (size_t)OrbCfg<P>::NST * OrbCfg<P>::STAGE_BYTES, true, st, F, 0, x, y,
+            (const double*)nullptr, (double*)nullptr, 0, (double*)nullptr, 1, pr);
+}
+
+int launch_w0_update(const LevelDev& F, const double* z, const double* scal, double* p, double* y,
+                     cudaStream_t st) {
+  if (!F.orb || F.imask || F.clist) return -1;
+  PRArgs pr{};
+  pr.ec = const_cast<double*>(z);
+  pr.coef = scal;
+  switch (F.p) {
+    case 1: launch_w0u<1>(F, p, y, pr, st); break;
+    case 2: launch_w0u<2>(F, p, y, pr, st); break;
+    case 3: launch_w0u<3>(F, p, y, pr, st); break;
+    default: launch_w0u<4>(F, p, y, pr, st); break;
   }
   return 1;
 }

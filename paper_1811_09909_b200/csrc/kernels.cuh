@@ -32,8 +32,11 @@ enum ApplyMode : int {
   AM_RESPR = 6,   // pass 1 (orbit levels): res_e = r - A x, then the p-restriction
                   // rc_e = J_p^T res_e (+ the coarse level's first smoothing step); res
                   // itself is not stored (PRArgs)
-  AM_W0P = 7      // pass 0 (orbit levels) with the p-prolongation folded in: x_e += J_p ec_e
+  AM_W0P = 7,     // pass 0 (orbit levels) with the p-prolongation folded in: x_e += J_p ec_e
                   // on the element's edges as they are gathered, stored back, then y = S x
+  AM_W0U = 8      // pass 0 (orbit fine level, PCG) with the direction update folded in:
+                  // p_e = z_e + beta p_e (k_pcg_pupdate's arithmetic; z = PRArgs::ec,
+                  // beta = PRArgs::coef[4]) as the edges are gathered, stored back, y = S p
 };
 
 // AM_RESPR: the p-coarse level's restriction target (bodies.cuh p_restrict_body)
@@ -354,6 +357,11 @@ int apply2_grid(const LevelDev& L, int mode);  // blocks of launch_apply2 (parti
 // the colour-0 partial sums of A x, as after p_prolong + the colour-0 pass
 int launch_w0_prolong(const LevelDev& F, const double* Jp, const double* ec, double* x, double* y,
                       cudaStream_t st);
+// colour-0 pass of the PCG apply with p = z + beta p folded in (AM_W0U; scal[4] = beta):
+// afterwards p holds the new direction on every edge and y the colour-0 partial sums of
+// A p, as after k_pcg_pupdate + the colour-0 pass; -1 if F is not a one-GPU orbit level
+int launch_w0_update(const LevelDev& F, const double* z, const double* scal, double* p, double* y,
+                     cudaStream_t st);
 int launch_resid_prestrict(const LevelDev& F, const LevelDev& C, const double* Jp, const double* x,
                            double* y, const double* r, double* rc, bool fuse, double* ec,
                            double* dc, cudaStream_t st);

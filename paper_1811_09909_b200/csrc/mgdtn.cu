@@ -120,6 +120,8 @@ struct Ctx {
   // mg_solve_host: the source-term / boundary-data uploads run on their own stream,
   // overlapped with mg_setup_dtn (which does not read them)
   cudaStream_t copy_st = nullptr;
+  bool pu_pending = false;          // pcg_iter_B left p = z + beta p to the next apply (AM_W0U)
+  const double* zp = nullptr;       // its z
   cudaEvent_t copy_ev0 = nullptr, copy_ev1 = nullptr;
   double *hsend = nullptr, *hrecv = nullptr, *gall = nullptr, *sden = nullptr, *sall = nullptr;
 };
@@ -1092,10 +1094,26 @@ static bool pcg_sf(const Ctx* c) {
          c->lev.size() > 1;
 }
 
+// the direction update p = z + beta p folded into the colour-0 pass of the next PCG apply
+// (AM_W0U): one-GPU orbit fine level whose apply is the pair of colour passes.  Config 5:
+// removes k_pcg_pupdate (0.77 ms, 4.0 GB) for a heavier colour-0 pass
+static bool pcg_w0u(const Ctx* c) {
+  const HostLevel& F = c->lev[0];
+  return F.d.orb && !F.d.imask && !F.clist && !partitioned(c) && !tiled(F.d, AM_APPLY) &&
+         !gathered(F.d, AM_APPLY) && env_or("MGDTN_W0U", 1) != 0;
+}
+
 static void pcg_iter_A(Ctx* c) {  // Ap, alpha, x/r update, rr
   HostLevel& F = c->lev[0];
   const int vg = vec_grid(F.d.ndof);
-  apply_full(c, F, c->pv, c->ap, c->part);
+  if (c->pu_pending) {   // p = z + beta p in the colour-0 pass, then the colour-1 pass
+    c->pu_pending = false;
+    c->launches += launch_w0_update(F.d, c->zp, c->scal, c->pv, c->ap, c->st);
+    c->launches += launch_apply(F.d, 1, AM_APPLY, c->pv, c->ap, nullptr, nullptr, 0, c->part, true,
+                                c->st);
+  } else {
+    apply_full(c, F, c->pv, c->ap, c->part);
+  }
   reduce_scal(c, c->part, apply_parts(F, AM_APPLY), c->scal, 1, 1);
   if (pcg_sf(c)) {
     const int64_t nb = (F.d.nedge + 127) / 128;
@@ -1119,6 +1137,11 @@ static void pcg_iter_B(Ctx* c) {  // z = B r, beta, p update
   const double* z = vcycle_level(c, 0, pcg_sf(c));   // first step done by the update
   c->launches += launch_dot(F.r, z, F.d.ndof, c->part, vg, c->st, &F.d);
   reduce_scal(c, c->part, vg, c->scal, 0, 2);
+  if (pcg_w0u(c)) {   // done by the next pcg_iter_A's colour-0 pass
+    c->pu_pending = true;
+    c->zp = z;
+    return;
+  }
   c->launches += launch_pcg_pupdate(c->pv, z, c->scal, F.d.ndof, c->st);
 }
 
@@ -1196,6 +1219,7 @@ static int pcg_impl(Ctx* c, const double* g, double* lambda, double rtol, int ma
   const int vg = vec_grid(n);
   const long long l0 = c->launches;
   if (c->st == nullptr) c->use_graphs = false;   // legacy stream cannot be captured
+  c->pu_pending = false;
   c->launches += launch_copy_masked(F.d, F.r, g, st);
   int status = MG_MAXIT, it = 0;
   double rel = 0.0;

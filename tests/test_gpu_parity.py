@@ -254,6 +254,28 @@ def test_gather_apply_bitwise(case):
     assert rel(gath[-1][case.ts.free], case.H.vcycle(r[case.ts.free])) <= TOL_OP
 
 
+def test_pcg_direction_fold_bitwise(case):
+    """The PCG direction update p = z + beta p folded into the colour-0 pass of the next
+    apply (AM_W0U, orbit fine level) against the separate k_pcg_pupdate pass: the same
+    fma per entry in the same order, so the whole solve agrees bit for bit."""
+    import os
+    gpu = case.gpu
+    pr = case.pr
+    g, _ = gpu.assemble_rhs(pr.f_qp, pr.f_const, pr.gD_qp)
+    out = {}
+    try:
+        for v in ("0", "1"):
+            os.environ["MGDTN_W0U"] = v
+            gpu.set_option(gpu.OPT_GATHER_NE, 1 << 16)   # (drops the captured solve graph)
+            lam, info = gpu.pcg_solve(g, rtol=case.cfg.rtol, maxit=2000)
+            out[v] = (lam.cpu().numpy(), info["iters"])
+    finally:
+        os.environ.pop("MGDTN_W0U", None)
+        gpu.set_option(gpu.OPT_GATHER_NE, 1 << 16)
+    assert out["0"][1] == out["1"][1]
+    assert np.array_equal(out["0"][0], out["1"][0])
+
+
 def test_rhs_parity(case):
     pr = case.pr
     g, lam_bc = case.gpu.assemble_rhs(pr.f_qp, pr.f_const, pr.gD_qp)

@@ -116,6 +116,17 @@ def config5_recipe(n: int) -> Config:
     return c
 
 
+def config3_recipe(n: int) -> Config:
+    """Config 3's recipe on an n x n mesh with its FULL-SIZE correlation length (16
+    elements, not scaled with n; std 1.5, clipped to a contrast of 1e6): the oracle-golden
+    stand-in for config 3 under the GPU's readings, whose full-size oracle solve (1270
+    PCG iterations on 6.3M dofs) takes the oracle ~4 h (tools/make_recipe_golden.py)."""
+    c = scaled_config(3, n)
+    c.extras["ell"] = CONFIGS[3].extras["ell"]
+    c.name = f"{CONFIGS[3].name}@n{n}_ell16"
+    return c
+
+
 # --------------------------------------------------------------------------
 # sampling grid of the input format
 # --------------------------------------------------------------------------
