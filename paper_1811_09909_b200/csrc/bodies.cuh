@@ -315,10 +315,17 @@ __device__ __forceinline__ void lc_restrict_body(const LevelDev& F, const double
       rI[2 * l + 1] = res[ie[l] * 2 + 1];
     }
     if (do_lc) {
-      const double* Ki = KIIinv + M * 64 + c * 8;
       double acc = 0.0;
+      if (F.ns) {   // full 8 x 8 (nonsymmetric A_II)
+        const double* Ki = KIIinv + M * 64 + c * 8;
 #pragma unroll
-      for (int b = 0; b < 8; ++b) acc = fma(Ki[b], rI[b], acc);
+        for (int b = 0; b < 8; ++b) acc = fma(Ki[b], rI[b], acc);
+      } else {      // packed upper triangle of the symmetric inverse
+        const double* Ki = KIIinv + M * 36;
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+          acc = fma(Ki[c <= b ? pk_index(c, b, 8) : pk_index(b, c, 8)], rI[b], acc);
+      }
       e[ie[c >> 1] * 2 + (c & 1)] += acc;
     }
     if (do_restrict) {

@@ -673,7 +673,9 @@ __global__ void __launch_bounds__(32 * AGG_WARPS) k_agglomerate(LevelDev F, Leve
     if (!ok && lane == 0) report_error(err, -4, M);
     for (int q = lane; q < 64; q += 32) {
       const int a = q >> 3, b = q & 7;
-      KIIinv[M * 64 + q] = G[a * 16 + 8 + b];
+      // symmetric A_II: its inverse as the packed upper triangle (36 of 64 doubles; the
+      // local correction's dominant stream at the 4096^2 P1 level, lc_restrict_body)
+      if (a <= b) KIIinv[M * 36 + pk_index(a, b, 8)] = G[a * 16 + 8 + b];
       const double pm = -U[a * 16 + b];
       Pm[M * 64 + q] = pm;
       U[a * 16 + b] = pm;   // keep P_M for S_c

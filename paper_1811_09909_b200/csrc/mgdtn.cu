@@ -268,7 +268,8 @@ static void layout(Ctx* c) {
     L.o_d = take(d.ndof * sizeof(double));
     if (L.kind == KIND_H) {
       int64_t nmac = (int64_t)(d.nx / 2) * (d.ny / 2);
-      L.o_KIIinv = take(nmac * 64 * sizeof(double));
+      // A_II^-1: packed upper triangle (36) in symmetric contexts, full 8 x 8 otherwise
+      L.o_KIIinv = take(nmac * (c->ns ? 64 : 36) * sizeof(double));
       L.o_Pm = take(nmac * 64 * sizeof(double));
       if (c->ns) L.o_Rm = take(nmac * 64 * sizeof(double));
       L.o_cbuf = take(nmac * 8 * sizeof(double));
