@@ -105,7 +105,8 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
                                              const double* xv, const double* yv, const double* x,
                                              double* y, const double* __restrict__ r, double* d,
                                              const double* __restrict__ Dp, int step, double c1,
-                                             double c2, double& dot, const PRArgs& pr) {
+                                             double c2, double& dot, const PRArgs& pr,
+                                             const double* din = nullptr) {
   using D = D4<P>;
   constexpr int K1 = P + 1, M = 4 * K1, NCS = D::NCS;
   constexpr bool HASD = MODE == AM_SMOOTH || MODE == AM_DINV || MODE == AM_GSC;
@@ -142,7 +143,9 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
     if (live[f]) {
       ld_edge<K1>(y + base, yo);
       if (MODE != AM_APPLY && MODE != AM_DINV) ld_edge<K1>(r + base, rv);
-      if (MODE == AM_SMOOTH && L.smoother == 1 && step > 0) ld_edge<K1>(d + base, dd + f * K1);
+      // (din: d read from x, STEP_D_FROM_X)
+      if (MODE == AM_SMOOTH && L.smoother == 1 && step > 0)
+        ld_edge<K1>((din ? din : d) + base, dd + f * K1);
     }
 #pragma unroll
     for (int a = 0; a < K1; ++a)
@@ -211,7 +214,7 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
         double e0 = c2c * (q00 * v0 + q01 * v1);
         double e1 = c2c * (q10 * v0 + q11 * v1);
         reinterpret_cast<double2*>(pr.ec)[E] = make_double2(e0, e1);
-        if (pr.smoother == 1) reinterpret_cast<double2*>(pr.dc)[E] = make_double2(e0, e1);
+        if (pr.smoother == 1 && pr.dc) reinterpret_cast<double2*>(pr.dc)[E] = make_double2(e0, e1);
       }
       continue;
     }
@@ -300,6 +303,8 @@ __global__ void __launch_bounds__(32) k_apply_orb(const LevelDev L, int colour, 
       for (int k = 0; k < NST && k < nmine; ++k) issue(k);
     pdl_trigger();
   }
+  const double* din = (step & STEP_D_FROM_X) ? x : nullptr;
+  step &= STEP_D_FROM_X - 1;
   double c1 = 0.0, c2 = 0.0;
   if (MODE == AM_SMOOTH) {
     c1 = L.coef[2 * step];
@@ -398,8 +403,8 @@ __global__ void __launch_bounds__(32) k_apply_orb(const LevelDev L, int colour, 
       }
       const double* Dp = L.Dco + c * 4 * NCS * 32 + lane;
       if (MODE == AM_SMOOTH || MODE == AM_GSC) {   // two edges at a time (registers)
-        orb_epilogue<P, MODE, DOT, 0, 2>(L, ed, bd, itf, gsm, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr);
-        orb_epilogue<P, MODE, DOT, 2, 2>(L, ed, bd, itf, gsm, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr);
+        orb_epilogue<P, MODE, DOT, 0, 2>(L, ed, bd, itf, gsm, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr, din);
+        orb_epilogue<P, MODE, DOT, 2, 2>(L, ed, bd, itf, gsm, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr, din);
       } else {
         orb_epilogue<P, MODE, DOT>(L, ed, bd, itf, gsm, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr);
       }
@@ -482,6 +487,8 @@ __global__ void __launch_bounds__(64, ORB2_MINB) k_apply_orb2(const LevelDev L, 
       for (int k = 0; k < NST && k < nmine; ++k) issue(k);
     pdl_trigger();
   }
+  const double* din = (step & STEP_D_FROM_X) ? x : nullptr;
+  step &= STEP_D_FROM_X - 1;
   double c1 = 0.0, c2 = 0.0;
   if (MODE == AM_SMOOTH) {
     c1 = L.coef[2 * step];
@@ -539,9 +546,9 @@ __global__ void __launch_bounds__(64, ORB2_MINB) k_apply_orb2(const LevelDev L, 
     if (act) {
       const double* Dp = L.Dco + c * 4 * NCS * 32 + lane;
       if (w == 0)
-        orb_epilogue<P, MODE, DOT, 0, 2>(L, ed, bd, 0, 0, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr);
+        orb_epilogue<P, MODE, DOT, 0, 2>(L, ed, bd, 0, 0, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr, din);
       else
-        orb_epilogue<P, MODE, DOT, 2, 2>(L, ed, bd, 0, 0, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr);
+        orb_epilogue<P, MODE, DOT, 2, 2>(L, ed, bd, 0, 0, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr, din);
     }
   }
   if (DOT) {

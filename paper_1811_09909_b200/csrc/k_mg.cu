@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(128) k_pcg_update_sf(LevelDev L, double* x, do
       x[off + q] = sx[q];
       r[off + q] = sr[q];
       e[off + q] = sp[q];
-      if (L.smoother == 1) d[off + q] = sp[q];
+      if (L.smoother == 1 && d) d[off + q] = sp[q];   // (d null: read from e, STEP_D_FROM_X)
     }
     __syncthreads();
   }

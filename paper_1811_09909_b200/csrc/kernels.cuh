@@ -39,6 +39,12 @@ enum ApplyMode : int {
                   // beta = PRArgs::coef[4]) as the edges are gathered, stored back, y = S p
 };
 
+// Flag in the `step` argument of the orbit-level smoothing passes (k_apply_orb / orb2,
+// AM_SMOOTH): Chebyshev step 1 after a first step from e = 0, whose direction d_0 equals
+// the iterate x_1 bit for bit (0 + d_0 = d_0): d is read from x (no second stream; the
+// first step then need not store d at all).
+constexpr int STEP_D_FROM_X = 1 << 8;
+
 // AM_RESPR: the p-coarse level's restriction target (bodies.cuh p_restrict_body)
 struct PRArgs {
   const double* Jp;     // K1 x 2 (row a: the two P1 coefficients of dof a)

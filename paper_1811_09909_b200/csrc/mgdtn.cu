@@ -715,8 +715,19 @@ static inline void apply_full(Ctx* c, const HostLevel& L, const double* x, doubl
 // two-colour passes update it in place (and use the other vector as scratch).
 static inline double* other(const HostLevel& L, const double* cur) { return cur == L.e ? L.w : L.e; }
 
+// Chebyshev step 1 after a first step from e = 0 reads its direction d_0 from the iterate
+// x_1 (equal bit for bit; STEP_D_FROM_X), so the first step need not store d: one-GPU
+// orbit levels run by the launch-per-step V-cycle through the pair of colour passes.
+// Config 5: one fewer vector write (first step) and read (step 1) on the two 4096^2 levels.
+static bool dfx_ok(const Ctx* c, int li) {
+  const HostLevel& L = c->lev[li];
+  return c->sm.kind == MG_SMOOTH_CHEBYSHEV && L.d.orb && !L.d.imask && !L.clist && !partitioned(c) &&
+         !tiled(L.d, AM_SMOOTH) && !gathered(L.d, AM_SMOOTH) &&
+         (c->tail_start < 0 || li < c->tail_start) && env_or("MGDTN_DFX", 1) != 0;
+}
+
 // one smoothing step on the iterate `cur`; returns where the new iterate is
-static inline double* smooth_step(Ctx* c, HostLevel& L, int step, double* cur) {
+static inline double* smooth_step(Ctx* c, HostLevel& L, int step, double* cur, bool dfx = false) {
   if (c->sm.kind == MG_SMOOTH_LUSGS) {
     // one LU-SGS step: forward block Gauss-Seidel sweep over the
     // four edge colours, then backward (oracle/multigrid.py)
@@ -739,7 +750,8 @@ static inline double* smooth_step(Ctx* c, HostLevel& L, int step, double* cur) {
     c->launches += launch_apply_gather(L.d, AM_SMOOTH, cur, nullptr, L.r, L.dv, out, slot, c->st);
     return out;
   }
-  apply_mode(c, L, AM_SMOOTH, cur, other(L, cur), L.r, L.dv, slot, nullptr);
+  apply_mode(c, L, AM_SMOOTH, cur, other(L, cur), L.r, L.dv, dfx ? slot | STEP_D_FROM_X : slot,
+             nullptr);
   return cur;
 }
 
@@ -844,7 +856,7 @@ static double* vcycle_level(Ctx* c, int li, bool first_done) {
     c->launches += launch_zero(L.e, L.d.ndof, c->st);
   }
   double* cur = L.e;
-  for (int s = s0; s < nu_pre; ++s) cur = smooth_step(c, L, s, cur);
+  for (int s = s0; s < nu_pre; ++s) cur = smooth_step(c, L, s, cur, s == 1 && s0 == 1 && dfx_ok(c, li));
   HostLevel& C = c->lev[li + 1];
   const bool fuse = (li + 1 < nlev - 1) && nu_at(c, c->sm.nu_pre, li + 1) > 0 &&
                     c->sm.kind != MG_SMOOTH_LUSGS &&
@@ -854,7 +866,7 @@ static double* vcycle_level(Ctx* c, int li, bool first_done) {
     // residual and p-restriction in one pair of passes: the colour-1 epilogue restricts
     // each edge's residual r - A e1 (Eq. 3.6 with the P1 injection J_p) instead of storing it
     c->launches += launch_resid_prestrict(L.d, C.d, c->refdev.Jp, cur, other(L, cur), L.r, C.r, fuse,
-                                          C.e, C.dv, c->st);
+                                          C.e, dfx_ok(c, li + 1) ? nullptr : C.dv, c->st);
   } else {
     double* res = residual(c, L, cur);  // r - A e1
     restrict_level(c, li, res, cur, true, C.r, fuse);
@@ -1120,7 +1132,7 @@ static void pcg_iter_A(Ctx* c) {  // Ap, alpha, x/r update, rr
     const int64_t nb = (F.d.nedge + 127) / 128;
     const int g = (int)(nb < 148 * 8 ? nb : 148 * 8);
     c->launches += launch_pcg_update_sf(F.d, c->x, F.r, c->pv, c->ap, c->scal, c->part, g, F.e,
-                                        F.dv, c->st);
+                                        dfx_ok(c, 0) ? nullptr : F.dv, c->st);
     reduce_scal(c, c->part, g, c->scal, 2, 0);
     return;
   }

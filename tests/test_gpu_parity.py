@@ -254,26 +254,33 @@ def test_gather_apply_bitwise(case):
     assert rel(gath[-1][case.ts.free], case.H.vcycle(r[case.ts.free])) <= TOL_OP
 
 
-def test_pcg_direction_fold_bitwise(case):
-    """The PCG direction update p = z + beta p folded into the colour-0 pass of the next
-    apply (AM_W0U, orbit fine level) against the separate k_pcg_pupdate pass: the same
-    fma per entry in the same order, so the whole solve agrees bit for bit."""
+@pytest.mark.parametrize("knob", ["MGDTN_W0U", "MGDTN_DFX"])
+def test_pcg_fold_bitwise(case, knob):
+    """Two bitwise-neutral rearrangements of the PCG / V-cycle on the orbit levels against
+    the plain sequence, over a whole solve and one V-cycle:
+    MGDTN_W0U -- the direction update p = z + beta p folded into the colour-0 pass of the
+    next apply (AM_W0U) instead of the k_pcg_pupdate pass (the same fma per entry);
+    MGDTN_DFX -- Chebyshev step 1 after a first step from e = 0 reads d_0 from the iterate
+    x_1 = 0 + d_0 (STEP_D_FROM_X) and the first step stores no d."""
     import os
     gpu = case.gpu
     pr = case.pr
     g, _ = gpu.assemble_rhs(pr.f_qp, pr.f_const, pr.gD_qp)
+    r = torch.from_numpy(case.vec(case.N, 600))
     out = {}
     try:
         for v in ("0", "1"):
-            os.environ["MGDTN_W0U"] = v
-            gpu.set_option(gpu.OPT_GATHER_NE, 1 << 16)   # (drops the captured solve graph)
+            os.environ[knob] = v
+            gpu.set_option(gpu.OPT_GATHER_NE, 1 << 16)   # (drops the captured graphs)
             lam, info = gpu.pcg_solve(g, rtol=case.cfg.rtol, maxit=2000)
-            out[v] = (lam.cpu().numpy(), info["iters"])
+            z = gpu.vcycle(r).cpu().numpy()
+            out[v] = (lam.cpu().numpy(), info["iters"], z)
     finally:
-        os.environ.pop("MGDTN_W0U", None)
+        os.environ.pop(knob, None)
         gpu.set_option(gpu.OPT_GATHER_NE, 1 << 16)
     assert out["0"][1] == out["1"][1]
     assert np.array_equal(out["0"][0], out["1"][0])
+    assert np.array_equal(out["0"][2], out["1"][2])
 
 
 def test_rhs_parity(case):
