@@ -106,7 +106,7 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
                                              double* y, const double* __restrict__ r, double* d,
                                              const double* __restrict__ Dp, int step, double c1,
                                              double c2, double& dot, const PRArgs& pr,
-                                             const double* din = nullptr) {
+                                             const double* din = nullptr, bool dst = true) {
   using D = D4<P>;
   constexpr int K1 = P + 1, M = 4 * K1, NCS = D::NCS;
   constexpr bool HASD = MODE == AM_SMOOTH || MODE == AM_DINV || MODE == AM_GSC;
@@ -247,7 +247,7 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
       }
     }
     if (MODE == AM_SMOOTH) {
-      if (L.smoother == 1) st_edge<K1>(d + base, dnv);
+      if (L.smoother == 1 && dst) st_edge<K1>(d + base, dnv);
       st_edge<K1>(xo + base, xnv);
     }
   }
@@ -304,6 +304,7 @@ __global__ void __launch_bounds__(32) k_apply_orb(const LevelDev L, int colour, 
     pdl_trigger();
   }
   const double* din = (step & STEP_D_FROM_X) ? x : nullptr;
+  const bool dst = !(step & STEP_NO_D_STORE);
   step &= STEP_D_FROM_X - 1;
   double c1 = 0.0, c2 = 0.0;
   if (MODE == AM_SMOOTH) {
@@ -403,8 +404,8 @@ __global__ void __launch_bounds__(32) k_apply_orb(const LevelDev L, int colour, 
       }
       const double* Dp = L.Dco + c * 4 * NCS * 32 + lane;
       if (MODE == AM_SMOOTH || MODE == AM_GSC) {   // two edges at a time (registers)
-        orb_epilogue<P, MODE, DOT, 0, 2>(L, ed, bd, itf, gsm, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr, din);
-        orb_epilogue<P, MODE, DOT, 2, 2>(L, ed, bd, itf, gsm, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr, din);
+        orb_epilogue<P, MODE, DOT, 0, 2>(L, ed, bd, itf, gsm, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr, din, dst);
+        orb_epilogue<P, MODE, DOT, 2, 2>(L, ed, bd, itf, gsm, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr, din, dst);
       } else {
         orb_epilogue<P, MODE, DOT>(L, ed, bd, itf, gsm, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr);
       }
@@ -488,6 +489,7 @@ __global__ void __launch_bounds__(64, ORB2_MINB) k_apply_orb2(const LevelDev L, 
     pdl_trigger();
   }
   const double* din = (step & STEP_D_FROM_X) ? x : nullptr;
+  const bool dst = !(step & STEP_NO_D_STORE);
   step &= STEP_D_FROM_X - 1;
   double c1 = 0.0, c2 = 0.0;
   if (MODE == AM_SMOOTH) {
@@ -546,9 +548,9 @@ __global__ void __launch_bounds__(64, ORB2_MINB) k_apply_orb2(const LevelDev L, 
     if (act) {
       const double* Dp = L.Dco + c * 4 * NCS * 32 + lane;
       if (w == 0)
-        orb_epilogue<P, MODE, DOT, 0, 2>(L, ed, bd, 0, 0, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr, din);
+        orb_epilogue<P, MODE, DOT, 0, 2>(L, ed, bd, 0, 0, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr, din, dst);
       else
-        orb_epilogue<P, MODE, DOT, 2, 2>(L, ed, bd, 0, 0, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr, din);
+        orb_epilogue<P, MODE, DOT, 2, 2>(L, ed, bd, 0, 0, xv, yv, x, y, r, d, Dp, step, c1, c2, dot, pr, din, dst);
     }
   }
   if (DOT) {

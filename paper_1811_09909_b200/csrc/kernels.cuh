@@ -44,6 +44,10 @@ enum ApplyMode : int {
 // the iterate x_1 bit for bit (0 + d_0 = d_0): d is read from x (no second stream; the
 // first step then need not store d at all).
 constexpr int STEP_D_FROM_X = 1 << 8;
+// ... and the last Chebyshev step of a pre- or post-smoothing sweep: its direction is never
+// read (the next step of the V-cycle is a restriction, or the V-cycle ends, and every sweep
+// starts with a step 0 that reads no d), so it is not stored.
+constexpr int STEP_NO_D_STORE = 1 << 9;
 
 // AM_RESPR: the p-coarse level's restriction target (bodies.cuh p_restrict_body)
 struct PRArgs {

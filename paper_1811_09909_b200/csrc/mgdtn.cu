@@ -727,7 +727,8 @@ static bool dfx_ok(const Ctx* c, int li) {
 }
 
 // one smoothing step on the iterate `cur`; returns where the new iterate is
-static inline double* smooth_step(Ctx* c, HostLevel& L, int step, double* cur, bool dfx = false) {
+static inline double* smooth_step(Ctx* c, HostLevel& L, int step, double* cur, bool dfx = false,
+                                  bool nod = false) {
   if (c->sm.kind == MG_SMOOTH_LUSGS) {
     // one LU-SGS step: forward block Gauss-Seidel sweep over the
     // four edge colours, then backward (oracle/multigrid.py)
@@ -750,8 +751,8 @@ static inline double* smooth_step(Ctx* c, HostLevel& L, int step, double* cur, b
     c->launches += launch_apply_gather(L.d, AM_SMOOTH, cur, nullptr, L.r, L.dv, out, slot, c->st);
     return out;
   }
-  apply_mode(c, L, AM_SMOOTH, cur, other(L, cur), L.r, L.dv, dfx ? slot | STEP_D_FROM_X : slot,
-             nullptr);
+  apply_mode(c, L, AM_SMOOTH, cur, other(L, cur), L.r, L.dv,
+             slot | (dfx ? STEP_D_FROM_X : 0) | (nod ? STEP_NO_D_STORE : 0), nullptr);
   return cur;
 }
 
@@ -856,7 +857,9 @@ static double* vcycle_level(Ctx* c, int li, bool first_done) {
     c->launches += launch_zero(L.e, L.d.ndof, c->st);
   }
   double* cur = L.e;
-  for (int s = s0; s < nu_pre; ++s) cur = smooth_step(c, L, s, cur, s == 1 && s0 == 1 && dfx_ok(c, li));
+  const bool dok = dfx_ok(c, li);
+  for (int s = s0; s < nu_pre; ++s)
+    cur = smooth_step(c, L, s, cur, s == 1 && s0 == 1 && dok, s == nu_pre - 1 && dok);
   HostLevel& C = c->lev[li + 1];
   const bool fuse = (li + 1 < nlev - 1) && nu_at(c, c->sm.nu_pre, li + 1) > 0 &&
                     c->sm.kind != MG_SMOOTH_LUSGS &&
@@ -884,7 +887,7 @@ static double* vcycle_level(Ctx* c, int li, bool first_done) {
   } else {
     prolong_level(c, li, ec, cur);
   }
-  for (int s = s1; s < nu_post; ++s) cur = smooth_step(c, L, s, cur);
+  for (int s = s1; s < nu_post; ++s) cur = smooth_step(c, L, s, cur, false, s == nu_post - 1 && dok);
   return cur;
 }
 
