@@ -130,7 +130,8 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
 #pragma unroll
   for (int f = F0; f < F0 + NF; ++f)
     live[f] = !bd[f] && !((itf >> f) & 1) && (MODE != AM_GSC || ((gsm >> f) & 1));
-  double t[M], dd[M], dv[HASD ? 4 * NCS : 1];
+  constexpr bool RZ = MODE == AM_SMOOTH && DOT;   // r . x_new: r kept past the load phase
+  double t[M], dd[M], dv[HASD ? 4 * NCS : 1], rk[RZ ? M : 1];
 #pragma unroll
   for (int f = F0; f < F0 + NF; ++f) {
     const int64_t base = ed[f] * K1;
@@ -148,8 +149,10 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
         ld_edge<K1>((din ? din : d) + base, dd + f * K1);
     }
 #pragma unroll
-    for (int a = 0; a < K1; ++a)
+    for (int a = 0; a < K1; ++a) {
       t[f * K1 + a] = (MODE == AM_APPLY || MODE == AM_DINV) ? yo[a] : rv[a] - yo[a];
+      if (RZ) rk[RZ ? f * K1 + a : 0] = rv[a];
+    }
     if (HASD) {
 #pragma unroll
       for (int o = 0; o < NCS; ++o) dv[f * NCS + o] = live[f] ? __ldg(Dp + (f * NCS + o) * 32) : 0.0;
@@ -244,6 +247,7 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
         if (L.smoother == 1 && step > 0) dn = fma(c1, dd[f * K1 + a], dn);
         dnv[a] = dn;
         xnv[a] = xf[a] + dn;
+        if (RZ) dot = fma(rk[RZ ? f * K1 + a : 0], xnv[a], dot);   // r . x_new
       }
     }
     if (MODE == AM_SMOOTH) {
@@ -1040,6 +1044,24 @@ template <int P, int MODE, bool DOT>
 static void launch_one(const LevelDev& L, int colour, const double* x, double* y, const double* r,
                        double* d, int step, double* partials, int grid, bool pdl,
                        cudaStream_t st) {
+  if constexpr (MODE == AM_SMOOTH && DOT) {
+    // r . x_new of a smoothing pass (the PCG's r.z in the V-cycle's last fine step): one-GPU
+    // orbit levels only (k_apply_orb2 at p = 4, k_apply_orb otherwise)
+    const int early = pdl ? 1 : 0;
+    if (!L.orb || L.ns || colour != 1) return;
+    if constexpr (P == 4) {
+      if (orb2_on(L, MODE)) {
+        orb2_resident<P, MODE, DOT>();
+        launch_ex(k_apply_orb2<P, MODE, DOT>, grid, 64,
+                  (size_t)OrbCfg<P>::NST * OrbCfg<P>::STAGE_BYTES, pdl, st, L, colour, x, y, r, d,
+                  step, partials, early, PRArgs{});
+        return;
+      }
+    }
+    orb_resident<P, MODE, DOT>();
+    launch_ex(k_apply_orb<P, MODE, DOT>, grid, 32, (size_t)OrbCfg<P>::NST * OrbCfg<P>::STAGE_BYTES,
+              pdl, st, L, colour, x, y, r, d, step, partials, early, PRArgs{});
+  } else {
   const int early = pdl ? 1 : 0;
   if (L.ns) {   // nonsymmetric context: full-storage apply (no LU-SGS / power iteration there)
     if (MODE == AM_GSC || MODE == AM_DINV) return;
@@ -1050,7 +1072,7 @@ static void launch_one(const LevelDev& L, int colour, const double* x, double* y
     return;
   }
   if (L.orb) {
-    if constexpr (P == 4 && MODE == AM_SMOOTH && !DOT) {
+    if constexpr (P == 4 && MODE == AM_SMOOTH) {
       if (colour == 1 && orb2_on(L, MODE)) {
         orb2_resident<P, MODE, DOT>();
         launch_ex(k_apply_orb2<P, MODE, DOT>, grid, 64,
@@ -1074,6 +1096,7 @@ static void launch_one(const LevelDev& L, int colour, const double* x, double* y
   launch_ex(k_apply_tma<P, MODE, DOT, TmaCfg<P>::NST>, grid, 32,
             (size_t)TmaCfg<P>::NST * TmaCfg<P>::CHUNK_BYTES, pdl, st, L, colour, x, y, r, d, step,
             partials, early);
+  }
 }
 
 template <int P>
@@ -1103,7 +1126,10 @@ static void dispatch_apply(const LevelDev& L, int colour, int mode, const double
       launch_one<P, AM_GSC, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
       break;
     default:
-      launch_one<P, AM_SMOOTH, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
+      if (partials && L.orb)   // (r . x_new: the PCG's r.z in the V-cycle's last fine step)
+        launch_one<P, AM_SMOOTH, true>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
+      else
+        launch_one<P, AM_SMOOTH, false>(L, colour, x, y, r, d, step, partials, grid, pdl, st);
       break;
   }
 }

@@ -728,7 +728,7 @@ static bool dfx_ok(const Ctx* c, int li) {
 
 // one smoothing step on the iterate `cur`; returns where the new iterate is
 static inline double* smooth_step(Ctx* c, HostLevel& L, int step, double* cur, bool dfx = false,
-                                  bool nod = false) {
+                                  bool nod = false, double* zpart = nullptr) {
   if (c->sm.kind == MG_SMOOTH_LUSGS) {
     // one LU-SGS step: forward block Gauss-Seidel sweep over the
     // four edge colours, then backward (oracle/multigrid.py)
@@ -752,7 +752,7 @@ static inline double* smooth_step(Ctx* c, HostLevel& L, int step, double* cur, b
     return out;
   }
   apply_mode(c, L, AM_SMOOTH, cur, other(L, cur), L.r, L.dv,
-             slot | (dfx ? STEP_D_FROM_X : 0) | (nod ? STEP_NO_D_STORE : 0), nullptr);
+             slot | (dfx ? STEP_D_FROM_X : 0) | (nod ? STEP_NO_D_STORE : 0), zpart);
   return cur;
 }
 
@@ -825,7 +825,9 @@ static void prolong_level(Ctx* c, int li, const double* ec, double* e) {
 // restriction kernel of the finer level.  Step 3 (local correction) and the
 // restriction share one residual: Q_{k-1} A_k T_k = 0, so Q(r - A e2) equals
 // Q(r - A e1).
-static double* vcycle_level(Ctx* c, int li, bool first_done) {
+// `zpart` (fine level, pcg_zdot): the last post-smoothing step also leaves the partial sums
+// of r . z (z = its new iterate) in zpart
+static double* vcycle_level(Ctx* c, int li, bool first_done, double* zpart = nullptr) {
   NvtxRange nv(level_range_name(li));
   HostLevel& L = c->lev[li];
   const int nlev = (int)c->lev.size();
@@ -887,7 +889,8 @@ static double* vcycle_level(Ctx* c, int li, bool first_done) {
   } else {
     prolong_level(c, li, ec, cur);
   }
-  for (int s = s1; s < nu_post; ++s) cur = smooth_step(c, L, s, cur, false, s == nu_post - 1 && dok);
+  for (int s = s1; s < nu_post; ++s)
+    cur = smooth_step(c, L, s, cur, false, s == nu_post - 1 && dok, s == nu_post - 1 ? zpart : nullptr);
   return cur;
 }
 
@@ -1147,12 +1150,28 @@ static void pcg_iter_A(Ctx* c) {  // Ap, alpha, x/r update, rr
 // (r.z stays a separate k_dot pass: folding it into the last fine smoothing pass
 // (SMOOTH + DOT epilogue) cost that pass 0.53 ms against k_dot's 0.38 ms at config 5,
 // register pressure; profiles/r02_c5_iteration_launches.txt)
+// r.z folded into the V-cycle's last fine smoothing step (its colour-1 epilogue holds r_e
+// and the new iterate z_e of every free edge it owns): one-GPU orbit fine level run by the
+// launch-per-step V-cycle, a last post-smoothing step through the pair of colour passes
+static bool pcg_zdot(const Ctx* c) {
+  const HostLevel& F = c->lev[0];
+  return F.d.orb && !F.d.imask && !F.clist && !partitioned(c) && !tiled(F.d, AM_SMOOTH) &&
+         !gathered(F.d, AM_SMOOTH) && c->sm.kind != MG_SMOOTH_LUSGS && c->sm.nu_post >= 2 &&
+         c->tail_start != 0 && !c->sm.nu_doubling && env_or("MGDTN_ZDOT", 1) != 0;
+}
+
 static void pcg_iter_B(Ctx* c) {  // z = B r, beta, p update
   HostLevel& F = c->lev[0];
   const int vg = vec_grid(F.d.ndof);
-  const double* z = vcycle_level(c, 0, pcg_sf(c));   // first step done by the update
-  c->launches += launch_dot(F.r, z, F.d.ndof, c->part, vg, c->st, &F.d);
-  reduce_scal(c, c->part, vg, c->scal, 0, 2);
+  const double* z;
+  if (pcg_zdot(c)) {
+    z = vcycle_level(c, 0, pcg_sf(c), c->part);
+    reduce_scal(c, c->part, apply_parts(F, AM_SMOOTH), c->scal, 0, 2);
+  } else {
+    z = vcycle_level(c, 0, pcg_sf(c));   // first step done by the update
+    c->launches += launch_dot(F.r, z, F.d.ndof, c->part, vg, c->st, &F.d);
+    reduce_scal(c, c->part, vg, c->scal, 0, 2);
+  }
   if (pcg_w0u(c)) {   // done by the next pcg_iter_A's colour-0 pass
     c->pu_pending = true;
     c->zp = z;

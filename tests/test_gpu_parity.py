@@ -283,6 +283,28 @@ def test_pcg_fold_bitwise(case, knob):
     assert np.array_equal(out["0"][2], out["1"][2])
 
 
+def test_pcg_zdot_fold(case):
+    """MGDTN_ZDOT: the PCG's r.z accumulated in the colour-1 epilogue of the V-cycle's last
+    fine smoothing step (orbit fine level) instead of a k_dot pass -- the same products
+    summed in another order: the same iteration count and the solution to 1e-12."""
+    import os
+    gpu = case.gpu
+    pr = case.pr
+    g, _ = gpu.assemble_rhs(pr.f_qp, pr.f_const, pr.gD_qp)
+    out = {}
+    try:
+        for v in ("0", "1"):
+            os.environ["MGDTN_ZDOT"] = v
+            gpu.set_option(gpu.OPT_GATHER_NE, 1 << 16)   # (drops the captured graphs)
+            lam, info = gpu.pcg_solve(g, rtol=case.cfg.rtol, maxit=2000)
+            out[v] = (lam.cpu().numpy(), info["iters"])
+    finally:
+        os.environ.pop("MGDTN_ZDOT", None)
+        gpu.set_option(gpu.OPT_GATHER_NE, 1 << 16)
+    assert abs(out["0"][1] - out["1"][1]) <= 1
+    assert rel(out["1"][0], out["0"][0]) <= 1e-12
+
+
 def test_rhs_parity(case):
     pr = case.pr
     g, lam_bc = case.gpu.assemble_rhs(pr.f_qp, pr.f_const, pr.gD_qp)
