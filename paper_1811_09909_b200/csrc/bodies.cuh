@@ -290,6 +290,64 @@ __device__ __forceinline__ void macro_interior_edges(const LevelDev& F, int I, i
   ie[3] = vedge(F.nx, F.ny, 2 * I + 1, 2 * J + 1);
 }
 
+// h-prolongation term (I_k ec)_E of fine P1 edge E (Eqs. 3.3 / 3.4): an edge inside a 2x2
+// macro gets its two rows of P_M ec_M (P_M = -A_II^-1 A_IB J), an edge on a macro side the
+// linear interpolation J of its coarse edge's two values (skip: that coarse edge is on
+// dOmega, no dofs).  k_prolong_edges and the folded colour-0 pass (AM_W0H) share it.
+__device__ __forceinline__ double2 prolong_edge_term(int nx, int ny, int nxc, int nyc, int cdmask,
+                                                     const double* __restrict__ ec,
+                                                     const double* __restrict__ Pm, int64_t E,
+                                                     bool& skip) {
+  const int64_t nhF = (int64_t)nx * (ny + 1);
+  int I, J, k = -1, half = 0;
+  int64_t cE = 0;
+  skip = false;
+  if (E < nhF) {
+    const int j = (int)((unsigned)E / (unsigned)nx), i = (int)E - j * nx;
+    I = i >> 1;
+    J = j >> 1;
+    if (j & 1) k = i & 1;                       // ie[0] / ie[1]
+    else { cE = hedge(nxc, I, J); half = i & 1; }
+  } else {
+    const int64_t r = E - nhF;
+    const int j = (int)((unsigned)r / (unsigned)(nx + 1)), i = (int)r - j * (nx + 1);
+    I = i >> 1;
+    J = j >> 1;
+    if (i & 1) k = 2 + (j & 1);                 // ie[2] / ie[3]
+    else { cE = vedge(nxc, nyc, I, J); half = j & 1; }
+  }
+  if (k >= 0) {
+    int64_t ce[4];
+    bool cb[4];
+    elem_edges(nxc, nyc, I, J, ce, cb, cdmask);
+    double c[8];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const double2 t = cb[f] ? make_double2(0.0, 0.0) : reinterpret_cast<const double2*>(ec)[ce[f]];
+      c[2 * f] = t.x;
+      c[2 * f + 1] = t.y;
+    }
+    const double2* P = reinterpret_cast<const double2*>(Pm + ((int64_t)J * nxc + I) * 64 + k * 16);
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double2 p0 = __ldg(P + q), p1 = __ldg(P + 4 + q);
+      a0 = fma(p0.x, c[2 * q], a0);
+      a0 = fma(p0.y, c[2 * q + 1], a0);
+      a1 = fma(p1.x, c[2 * q], a1);
+      a1 = fma(p1.y, c[2 * q + 1], a1);
+    }
+    return make_double2(a0, a1);
+  }
+  if (edge_on_boundary(nxc, nyc, cE, cdmask)) {
+    skip = true;
+    return make_double2(0.0, 0.0);
+  }
+  const double2 t = reinterpret_cast<const double2*>(ec)[cE];
+  const double cm = 0.5 * (t.x + t.y);
+  return half ? make_double2(cm, t.y) : make_double2(t.x, cm);
+}
+
 // step 3 (e_I += A_II^-1 res_I per macro) and the macro part of Q_{k-1}
 // (cbuf = P_M^T res_I per macro).  Work item = (macro M, row c): 8 threads per
 // macro, each one output row, so the 2 x 64 matrix loads of a macro are spread

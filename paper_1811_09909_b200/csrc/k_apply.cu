@@ -110,7 +110,7 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
   using D = D4<P>;
   constexpr int K1 = P + 1, M = 4 * K1, NCS = D::NCS;
   constexpr bool HASD = MODE == AM_SMOOTH || MODE == AM_DINV || MODE == AM_GSC;
-  if (MODE == AM_W0 || MODE == AM_W0P || MODE == AM_W0U) {
+  if (MODE == AM_W0 || MODE == AM_W0P || MODE == AM_W0U || MODE == AM_W0H) {
 #pragma unroll
     for (int f = F0; f < F0 + NF; ++f) {
       double v[K1];
@@ -119,7 +119,7 @@ __device__ __forceinline__ void orb_epilogue(const LevelDev& L, const int64_t ed
       st_edge<K1>(y + ed[f] * K1, v);
       // W0P / W0U: the prolonged iterate / new direction goes back to x (dOmega rows stay
       // untouched)
-      if ((MODE == AM_W0P || MODE == AM_W0U) && !bd[f])
+      if ((MODE == AM_W0P || MODE == AM_W0U || MODE == AM_W0H) && !bd[f])
         st_edge<K1>(const_cast<double*>(x) + ed[f] * K1, xv + f * K1);
     }
     return;
@@ -349,6 +349,18 @@ __global__ void __launch_bounds__(32) k_apply_orb(const LevelDev L, int colour, 
 #pragma unroll
           for (int a = 0; a < K1; ++a)
             xn[f * K1 + a] += fma(__ldg(pr.Jp + a * 2), cc.x, __ldg(pr.Jp + a * 2 + 1) * cc.y);
+        }
+      }
+      if (MODE == AM_W0H) {   // x_e + (I_k ec)_e (k_prolong_edges' arithmetic)
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          if (bdn[f]) continue;
+          bool skip;
+          const double2 v = prolong_edge_term(L.nx, L.ny, L.nx >> 1, L.ny >> 1, L.dmask, pr.ec,
+                                              pr.Jp, edn[f], skip);
+          if (skip) continue;
+          xn[f * K1] += v.x;
+          xn[f * K1 + 1] += v.y;
         }
       }
       if (MODE == AM_W0U) {   // p_e = z_e + beta p_e (k_pcg_pupdate's arithmetic)
@@ -1181,6 +1193,20 @@ static void launch_w0u(const LevelDev& F, const double* x, double* y, const PRAr
   launch_ex(k_apply_orb<P, AM_W0U, false>, grid, 32,
             (size_t)OrbCfg<P>::NST * OrbCfg<P>::STAGE_BYTES, true, st, F, 0, x, y,
             (const double*)nullptr, (double*)nullptr, 0, (double*)nullptr, 1, pr);
+}
+
+int launch_w0_hprolong(const LevelDev& F, const double* ec, const double* Pm, double* x, double* y,
+                       cudaStream_t st) {
+  if (!F.orb || F.imask || F.clist || F.p != 1 || (F.nx & 1) || (F.ny & 1)) return -1;
+  PRArgs pr{};
+  pr.ec = const_cast<double*>(ec);
+  pr.Jp = Pm;
+  const int grid = apply_grid_mode(F, AM_W0);
+  orb_resident<1, AM_W0H, false>();
+  launch_ex(k_apply_orb<1, AM_W0H, false>, grid, 32,
+            (size_t)OrbCfg<1>::NST * OrbCfg<1>::STAGE_BYTES, true, st, F, 0, x, y,
+            (const double*)nullptr, (double*)nullptr, 0, (double*)nullptr, 1, pr);
+  return 1;
 }
 
 int launch_w0_update(const LevelDev& F, const double* z, const double* scal, double* p, double* y,

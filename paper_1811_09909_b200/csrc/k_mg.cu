@@ -188,53 +188,10 @@ __global__ void __launch_bounds__(128) k_prolong_edges(LevelDev F, LevelDev C,
                                                        const double* __restrict__ Pm, double* e) {
   pdl_enter();
   const int nx = F.nx, nxc = C.nx, nyc = C.ny;
-  const int64_t nhF = (int64_t)nx * (F.ny + 1);
   for (int64_t E = GTID; E < F.nedge; E += GNT) {
-    int I, J, k = -1, half = 0;
-    int64_t cE = 0;
-    if (E < nhF) {
-      const int j = (int)((unsigned)E / (unsigned)nx), i = (int)E - j * nx;
-      I = i >> 1;
-      J = j >> 1;
-      if (j & 1) k = i & 1;                       // ie[0] / ie[1]
-      else { cE = hedge(nxc, I, J); half = i & 1; }
-    } else {
-      const int64_t r = E - nhF;
-      const int j = (int)((unsigned)r / (unsigned)(nx + 1)), i = (int)r - j * (nx + 1);
-      I = i >> 1;
-      J = j >> 1;
-      if (i & 1) k = 2 + (j & 1);                 // ie[2] / ie[3]
-      else { cE = vedge(nxc, nyc, I, J); half = j & 1; }
-    }
-    double2 v;
-    if (k >= 0) {
-      int64_t ce[4];
-      bool cb[4];
-      elem_edges(nxc, nyc, I, J, ce, cb, C.dmask);
-      double c[8];
-#pragma unroll
-      for (int f = 0; f < 4; ++f) {
-        const double2 t = cb[f] ? make_double2(0.0, 0.0) : reinterpret_cast<const double2*>(ec)[ce[f]];
-        c[2 * f] = t.x;
-        c[2 * f + 1] = t.y;
-      }
-      const double2* P = reinterpret_cast<const double2*>(Pm + ((int64_t)J * nxc + I) * 64 + k * 16);
-      double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double2 p0 = __ldg(P + q), p1 = __ldg(P + 4 + q);
-        a0 = fma(p0.x, c[2 * q], a0);
-        a0 = fma(p0.y, c[2 * q + 1], a0);
-        a1 = fma(p1.x, c[2 * q], a1);
-        a1 = fma(p1.y, c[2 * q + 1], a1);
-      }
-      v = make_double2(a0, a1);
-    } else {
-      if (edge_on_boundary(nxc, nyc, cE, C.dmask)) continue;
-      const double2 t = reinterpret_cast<const double2*>(ec)[cE];
-      const double cm = 0.5 * (t.x + t.y);
-      v = half ? make_double2(cm, t.y) : make_double2(t.x, cm);
-    }
+    bool skip;
+    const double2 v = prolong_edge_term(nx, F.ny, nxc, nyc, C.dmask, ec, Pm, E, skip);
+    if (skip) continue;
     double2* ep = reinterpret_cast<double2*>(e) + E;
     double2 o = *ep;
     o.x += v.x;

@@ -34,9 +34,12 @@ enum ApplyMode : int {
                   // itself is not stored (PRArgs)
   AM_W0P = 7,     // pass 0 (orbit levels) with the p-prolongation folded in: x_e += J_p ec_e
                   // on the element's edges as they are gathered, stored back, then y = S x
-  AM_W0U = 8      // pass 0 (orbit fine level, PCG) with the direction update folded in:
+  AM_W0U = 8,     // pass 0 (orbit fine level, PCG) with the direction update folded in:
                   // p_e = z_e + beta p_e (k_pcg_pupdate's arithmetic; z = PRArgs::ec,
                   // beta = PRArgs::coef[4]) as the edges are gathered, stored back, y = S p
+  AM_W0H = 9      // pass 0 (P1 orbit level, one GPU) with the h-prolongation folded in:
+                  // x_e += (I_k ec)_e (prolong_edge_term; ec = PRArgs::ec, P_M = PRArgs::Jp)
+                  // as the edges are gathered, stored back, then y = S x
 };
 
 // Flag in the `step` argument of the orbit-level smoothing passes (k_apply_orb / orb2,
@@ -372,6 +375,11 @@ int launch_w0_prolong(const LevelDev& F, const double* Jp, const double* ec, dou
 // A p, as after k_pcg_pupdate + the colour-0 pass; -1 if F is not a one-GPU orbit level
 int launch_w0_update(const LevelDev& F, const double* z, const double* scal, double* p, double* y,
                      cudaStream_t st);
+// colour-0 pass with the h-prolongation e += I_k ec folded in (AM_W0H): afterwards x holds
+// the prolonged iterate on every edge and y the colour-0 partial sums, as after
+// k_prolong_edges + the colour-0 pass; -1 unless F is a one-GPU P1 orbit level
+int launch_w0_hprolong(const LevelDev& F, const double* ec, const double* Pm, double* x, double* y,
+                       cudaStream_t st);
 int launch_resid_prestrict(const LevelDev& F, const LevelDev& C, const double* Jp, const double* x,
                            double* y, const double* r, double* rc, bool fuse, double* ec,
                            double* dc, cudaStream_t st);

@@ -883,8 +883,17 @@ static double* vcycle_level(Ctx* c, int li, bool first_done, double* zpart = nul
       !tiled(L.d, AM_SMOOTH)) {
     // the p-prolongation folded into the first post-smoothing step's colour-0 pass
     c->launches += launch_w0_prolong(L.d, c->refdev.Jp, ec, cur, other(L, cur), c->st);
-    c->launches += launch_apply(L.d, 1, AM_SMOOTH, cur, other(L, cur), L.r, L.dv, 0, nullptr, true,
-                                c->st);
+    c->launches += launch_apply(L.d, 1, AM_SMOOTH, cur, other(L, cur), L.r, L.dv,
+                                nu_post == 1 && dok ? STEP_NO_D_STORE : 0, nullptr, true, c->st);
+    s1 = 1;
+  } else if (nu_post > 0 && L.kind == KIND_H && L.d.orb && L.d.p == 1 && L.d.imask == 0 &&
+             !L.clist && !gathers(c, li) && !partitioned(c) && c->sm.kind != MG_SMOOTH_LUSGS &&
+             !tiled(L.d, AM_SMOOTH) && !gathered(L.d, AM_SMOOTH) && env_or("MGDTN_W0H", 1) != 0) {
+    // the h-prolongation (Eqs. 3.3 / 3.4) folded into the first post-smoothing step's
+    // colour-0 pass of the P1 orbit level (AM_W0H; config 5: the 4096^2 P1 level)
+    c->launches += launch_w0_hprolong(L.d, ec, L.Pm, cur, other(L, cur), c->st);
+    c->launches += launch_apply(L.d, 1, AM_SMOOTH, cur, other(L, cur), L.r, L.dv,
+                                nu_post == 1 && dok ? STEP_NO_D_STORE : 0, nullptr, true, c->st);
     s1 = 1;
   } else {
     prolong_level(c, li, ec, cur);

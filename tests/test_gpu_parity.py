@@ -254,14 +254,16 @@ def test_gather_apply_bitwise(case):
     assert rel(gath[-1][case.ts.free], case.H.vcycle(r[case.ts.free])) <= TOL_OP
 
 
-@pytest.mark.parametrize("knob", ["MGDTN_W0U", "MGDTN_DFX"])
+@pytest.mark.parametrize("knob", ["MGDTN_W0U", "MGDTN_DFX", "MGDTN_W0H"])
 def test_pcg_fold_bitwise(case, knob):
     """Two bitwise-neutral rearrangements of the PCG / V-cycle on the orbit levels against
     the plain sequence, over a whole solve and one V-cycle:
     MGDTN_W0U -- the direction update p = z + beta p folded into the colour-0 pass of the
     next apply (AM_W0U) instead of the k_pcg_pupdate pass (the same fma per entry);
     MGDTN_DFX -- Chebyshev step 1 after a first step from e = 0 reads d_0 from the iterate
-    x_1 = 0 + d_0 (STEP_D_FROM_X) and the first step stores no d."""
+    x_1 = 0 + d_0 (STEP_D_FROM_X) and the first step stores no d;
+    MGDTN_W0H -- the h-prolongation of the P1 orbit level folded into its first
+    post-smoothing step's colour-0 pass (AM_W0H) instead of k_prolong_edges."""
     import os
     gpu = case.gpu
     pr = case.pr
