@@ -326,9 +326,14 @@ int mg_check_invariants(void* ctx, double* report);
  *   MG_OPT_GATHER_NE      packed P1 levels (one-GPU or replicated) with at most this many
  *                         elements run the apply / residual / smoothing step as one
  *                         gather-form pass (default 65536; 0: never).  Bitwise the same
- *                         results as the pair of colour passes. */
+ *                         results as the pair of colour passes.
+ *   MG_OPT_KEEP_FINE_MAPS 1: mg_setup_dtn keeps the finest level's element maps as
+ *                         mg_debug_set_element_dtn wrote them (no local solves) and builds
+ *                         the rest of the hierarchy from them -- a test hook that runs the
+ *                         whole setup and solve on another implementation's element maps;
+ *                         0 (default): mg_setup_dtn computes them. */
 enum { MG_OPT_SWEEP = 1, MG_OPT_APPLY_GRID_CAP = 2, MG_OPT_COMM_TIMEOUT_MS = 3,
-       MG_OPT_GATHER_NE = 4 };
+       MG_OPT_GATHER_NE = 4, MG_OPT_KEEP_FINE_MAPS = 5 };
 int mg_set_option(void* ctx, int32_t key, int64_t value);
 
 const char* mg_last_error(const void* ctx);

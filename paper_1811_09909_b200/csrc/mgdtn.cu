@@ -92,6 +92,7 @@ struct Ctx {
   bool tail_vcycle = true;        // V-cycle levels >= tail_start through k_coarse_tail
   bool tail_lmax = true;          // their Chebyshev power iterations through k_tail_lmax
   bool tail_dense = false;        // B_tail as an explicit matrix (k_tail_basis / k_tail_dense)
+  bool keep_fine_maps = false;    // MG_OPT_KEEP_FINE_MAPS: setup keeps the finest level's maps
   int nft = 0;                    // free dofs of the top tail level
   size_t o_Bt = 0, o_tfidx = 0;
   double* Bt = nullptr;
@@ -908,7 +909,9 @@ static double* vcycle_level(Ctx* c, int li, bool first_done, double* zpart = nul
 static int setup_body(Ctx* c) {
   cudaStream_t st = c->st;
   HostLevel& F = c->lev[0];
-  c->launches += launch_local_dtn(F.d, c->refdev, F.h, c->Kc, c->methc, c->tauc, c->err, st);
+  // (MG_OPT_KEEP_FINE_MAPS: the maps mg_debug_set_element_dtn wrote stay; test hook)
+  if (!c->keep_fine_maps)
+    c->launches += launch_local_dtn(F.d, c->refdev, F.h, c->Kc, c->methc, c->tauc, c->err, st);
   const int nlev = (int)c->lev.size();
   const int numax = MAX_NU;   // coefficients for any step count (mg_smooth may exceed nu)
   // Chebyshev: lambda_max of D_B^-1 A_k by power iteration (Q11), v <- D^-1 A v in
@@ -2308,6 +2311,9 @@ int mg_set_option(void* ctx, int32_t key, int64_t value) {
     if (value < 0) return fail(c, MG_ERR_ARG, "MG_OPT_GATHER_NE must be >= 0");
     c->gather_ne = value;
     plan_gather(c);
+  } else if (key == MG_OPT_KEEP_FINE_MAPS) {
+    if (value < 0 || value > 1) return fail(c, MG_ERR_ARG, "MG_OPT_KEEP_FINE_MAPS: 0 or 1");
+    c->keep_fine_maps = value != 0;
   } else if (key == MG_OPT_APPLY_GRID_CAP) {
     if (value < 0 || value > (1 << 20)) return fail(c, MG_ERR_ARG, "MG_OPT_APPLY_GRID_CAP out of range");
     for (auto& L : c->lev) L.d.grid_cap = (int)value;

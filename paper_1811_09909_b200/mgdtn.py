@@ -520,7 +520,7 @@ class MGSolver:
     def use_graphs(self, on: bool):
         self._chk(self.lib.mg_set_use_graphs(self.ctx, int(on)), "mg_set_use_graphs")
 
-    OPT_SWEEP, OPT_APPLY_GRID_CAP, OPT_COMM_TIMEOUT_MS, OPT_GATHER_NE = 1, 2, 3, 4
+    OPT_SWEEP, OPT_APPLY_GRID_CAP, OPT_COMM_TIMEOUT_MS, OPT_GATHER_NE, OPT_KEEP_FINE_MAPS = 1, 2, 3, 4, 5
 
     def check_invariants(self):
         """mg_check_invariants: dict(const_mode, nonfinite, atomic_apply_diff); raises MGError
