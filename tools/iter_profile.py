@@ -1,7 +1,10 @@
 #!/usr/bin/env python3
 """Per-launch table of one PCG iteration from an ncu --csv launch list with
-gpu__time_duration.sum (+ optional dram__bytes_read/write.sum): the launches
-between the 1st and 2nd k_pcg_pupdate (one whole iteration of the eager solve)."""
+gpu__time_duration.sum (+ optional dram__bytes_read/write.sum): the launches after the
+1st and up to the 2nd launch of the marker kernel (default k_pcg_update_sf, once per
+iteration of the eager solve).
+
+    python tools/iter_profile.py launches.csv [threshold_us] [marker]"""
 import collections
 import csv
 import sys
@@ -31,19 +34,20 @@ def load(path):
     return list(by.values())
 
 
-def main(path, thresh=50.0):
+def main(path, thresh=50.0, marker="k_pcg_update_sf"):
     L = load(path)
-    idx = [i for i, d in enumerate(L) if "k_pcg_pupdate" in d["name"]]
+    idx = [i for i, d in enumerate(L) if marker in d["name"]]
     a, b = idx[0], idx[1]
     tot = tb = 0.0
     for d in L[a + 1:b + 1]:
         tot += d["t"]
         tb += d["b"]
         if d["t"] >= thresh:
-            bw = d["b"] / d["t"] / 1e3 if d["t"] > 0 else 0
+            bw = d["b"] / d["t"] / 1e6 if d["t"] > 0 else 0
             print(f"{d['t']:9.1f} us {d['b'] / 1e9:7.3f} GB {bw:5.2f} TB/s  {d['name'][:44]:44s} {d['grid']}")
-    print(f"iteration: {tot / 1e3:.3f} ms, {tb / 1e9:.2f} GB DRAM, {tb / tot / 1e3:.2f} TB/s")
+    print(f"iteration: {tot / 1e3:.3f} ms, {tb / 1e9:.2f} GB DRAM, {tb / tot / 1e6:.2f} TB/s")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], float(sys.argv[2]) if len(sys.argv) > 2 else 50.0)
+    main(sys.argv[1], float(sys.argv[2]) if len(sys.argv) > 2 else 50.0,
+         sys.argv[3] if len(sys.argv) > 3 else "k_pcg_update_sf")
