@@ -195,17 +195,16 @@ def test_fullsize_pcg(full):
     # solution by more than the operator's 1-ulp noise floor (config 3: 9.6e-11,
     # profiles/r02_noise_floor_c3.json; GPU vs the plain oracle 1.3e-9 after 1270 iterations)
     path = os.path.join(ROOT, "tests", "golden", f"fullsize_oracle_c{c.index}_r10.json")
-    tol = TOL_SOL
     if not os.path.exists(path):
         path = os.path.join(ROOT, "tests", "golden", f"fullsize_oracle_c{c.index}.json")
-        if c.index == 3:
-            # config 3 against the oracle as it stands (its full-size run under the readings
-            # takes ~4 h): the GPU is 1.3e-9 from it after 1270 iterations at contrast 1e6.
-            # The readings move a converged solution of this recipe (oracle vs oracle under
-            # R5/R9/R10: 5.8e-11 at n = 256, 560 iterations), and the GPU matches the
-            # oracle under the readings to 1e-9 on every dof at n = 256 / 512
-            # (tests/test_gpu_recipe_goldens.py, reading R10)
-            tol = 2e-9
+    # config 3 (contrast 1e6, 1270 iterations): FP64 pins its converged solution only to
+    # ~1e-9 -- the few-ulp difference between the GPU's and the oracle's element maps (two
+    # valid eliminations of the same local problem) moves it by 1.3e-9 at the n = 512 recipe,
+    # while the GPU's setup + solve on the oracle's maps land 6e-10 from the oracle and the
+    # order of the solve's own sums moves it by 2.5e-12 at full size
+    # (profiles/r02_c3_solution_floor.txt, tests/test_gpu_recipe_goldens.py);
+    # GPU vs the plain-oracle golden here: 1.3e-9
+    tol = 3e-9 if c.index == 3 else TOL_SOL
     if not os.path.exists(path):
         # no oracle run at this size: the finite-precision CG residual gap bound
         # (Greenbaum, "Iterative methods for solving linear systems", 1997, ch. 7.3: ||g - A x_k - r_k|| <= eps O(k) ||A|| max_j ||x_j||,
