@@ -5,6 +5,7 @@ oracle can compute one by one, else on properties that hold at any size:
   H1  element DtN maps of sampled elements        vs oracle.element.element_dtn
   H2  p-level element maps of the same elements   vs oracle.multigrid.p_coarsen_element
   H6  fine apply, sampled rows                    vs sum of the oracle's element DtN rows
+  H7/H8 one fine smoothing step, sampled rows     vs D_e^-1 (r - A e0)_e from the oracle's maps
   H3/H11 energy preservation a_k(I x, I x) = a_{k-1}(x, x) on every level
   H12 V-cycle symmetric and linear
   H13 PCG: converged, true residual through the (row-validated) apply, and -- where
@@ -105,17 +106,14 @@ def test_fullsize_p_level(full):
     assert rel(S1, So1) <= TOL_OP, rel(S1, So1)
 
 
-def test_fullsize_apply_rows(full):
-    c = full.cfg
-    n, p, k1 = c.n, c.p, c.p + 1
-    x = W.random_trace_vector(full.s.ndof(), c.seed_vec)
-    y = full.call(full.s.apply, full.N, torch.from_numpy(x)).cpu().numpy()
-    rng = np.random.default_rng(c.seed_vec + 1)
+def sampled_edges(full, seed, count=1500):
+    """Sampled edges (boundary ones and both ends included), the elements adjacent to each
+    with the edge's local index in them, and the oracle's element maps of those elements."""
+    n = full.cfg.n
+    rng = np.random.default_rng(seed)
     nE = mesh.n_edges(n)
-    edges = np.unique(np.concatenate([rng.choice(nE, 1500, replace=False),
+    edges = np.unique(np.concatenate([rng.choice(nE, count, replace=False),
                                       mesh.boundary_edges(n)[:50], [0, nE - 1]]))
-    bmask = mesh.boundary_edge_mask(n)
-    # elements adjacent to each sampled edge and the edge's local index in them
     ed = mesh.element_edges(n)
     adj = {}
     nh = n * (n + 1)
@@ -127,23 +125,78 @@ def test_fullsize_apply_rows(full):
             j, i = divmod(int(e) - nh, n + 1)
             cand = [(j * n + i - 1, 1) if i > 0 else None, (j * n + i, 3) if i < n else None]
         adj[int(e)] = [a for a in cand if a is not None]
+        for t, f in adj[int(e)]:
+            assert ed[t, f] == e
     T = np.array(sorted({t for v in adj.values() for t, _ in v}), dtype=np.int64)
     ST = dict(zip(T.tolist(), full.oracle_dtn(T)))
-    dofs = mesh.element_dofs(n, p)
+    dofs = mesh.element_dofs(n, full.cfg.p)
+    return edges, adj, ST, {int(t): dofs[t] for t in T}
+
+
+def oracle_rows(full, adj, ST, dofs, e, x):
+    """Row block e of A x (x with its Dirichlet entries zeroed) from the oracle's maps."""
+    k1 = full.cfg.p + 1
+    rows = np.zeros(k1)
+    for t, f in adj[int(e)]:
+        rows += (ST[t] @ x[dofs[t]])[f * k1:(f + 1) * k1]
+    return rows
+
+
+def test_fullsize_apply_rows(full):
+    c = full.cfg
+    n, p, k1 = c.n, c.p, c.p + 1
+    x = W.random_trace_vector(full.s.ndof(), c.seed_vec)
+    y = full.call(full.s.apply, full.N, torch.from_numpy(x)).cpu().numpy()
+    edges, adj, ST, dofs = sampled_edges(full, c.seed_vec + 1)
+    bmask = mesh.boundary_edge_mask(n)
     xm = x.copy()
     xm[np.repeat(bmask, k1)] = 0.0
     ref, got = [], []
     for e in edges:
-        rows = np.zeros(k1)
-        for t, f in adj[int(e)]:
-            assert ed[t, f] == e
-            rows += (ST[t] @ xm[dofs[t]])[f * k1:(f + 1) * k1]
+        rows = oracle_rows(full, adj, ST, dofs, e, xm)
         if bmask[e]:
             assert np.all(y[e * k1:(e + 1) * k1] == 0.0)
         else:
             ref.append(rows)
             got.append(y[e * k1:(e + 1) * k1])
     assert rel(np.array(got), np.array(ref)) <= TOL_OP, rel(np.array(got), np.array(ref))
+
+
+def test_fullsize_smooth_rows(full):
+    """One fine smoothing step at full size (mg_smooth, the context's smoother) on sampled
+    edges: e1 - e0 = c D_e^-1 (r - A e0)_e with D_e = sum of the two adjacent elements'
+    diagonal blocks of the oracle's maps.  Block-Jacobi (configs 3, 4):
+    c = 1 (no damping).  Chebyshev (configs 2, 5): step 0 is the same block
+    update scaled by 1/theta, which depends on the level's lambda_max (checked against the
+    oracle at the parity sizes): every sampled row must give one common scalar."""
+    c = full.cfg
+    n, p, k1 = c.n, c.p, c.p + 1
+    nd = full.s.ndof()
+    r = W.random_trace_vector(nd, c.seed_vec + 11)
+    e0 = W.random_trace_vector(nd, c.seed_vec + 12)
+    e1 = full.call(full.s.smooth, full.N, torch.from_numpy(r), torch.from_numpy(e0), 1).cpu().numpy()
+    edges, adj, ST, dofs = sampled_edges(full, c.seed_vec + 13, count=1000)
+    bmask = mesh.boundary_edge_mask(n)
+    bd = np.repeat(bmask, k1)
+    e0m, rm = e0.copy(), r.copy()
+    e0m[bd] = 0.0
+    rm[bd] = 0.0
+    ref, got = [], []
+    for e in edges:
+        sl = slice(e * k1, (e + 1) * k1)
+        if bmask[e]:
+            continue
+        De = sum(ST[t][f * k1:(f + 1) * k1, f * k1:(f + 1) * k1] for t, f in adj[int(e)])
+        ref.append(np.linalg.solve(De, rm[sl] - oracle_rows(full, adj, ST, dofs, e, e0m)))
+        got.append(e1[sl] - e0m[sl])
+    ref, got = np.array(ref), np.array(got)
+    if c.smoother == 1:   # one common 1/theta on every row
+        scale = float(np.sum(got * ref) / np.sum(ref * ref))
+        assert scale > 0.0
+        ref = scale * ref
+    # e1 - e0 loses the digits e0 and e1 share: compare at the level of |e0|
+    assert np.linalg.norm(got - ref) <= TOL_OP * np.linalg.norm(e0m), np.linalg.norm(got - ref) / np.linalg.norm(e0m)
+    assert rel(got, ref) <= 1e-10, rel(got, ref)
 
 
 def test_fullsize_energy_every_level(full):
