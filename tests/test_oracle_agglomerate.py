@@ -1,0 +1,112 @@
+"""Pins of the seed-point agglomeration oracle (oracle/agglomerate.py,
+PAPER.md:491-498; readings A1-A3 in DESIGN.md section 3) against what does not
+depend on it: scipy's graph shortest paths (brute force), the closed-form
+Voronoi cells of a strip, the closed-form quadtree of a 2^m x 2^m grid, and
+the invariants every correct agglomeration has."""
+import numpy as np
+import pytest
+from scipy.sparse import coo_matrix
+from scipy.sparse.csgraph import connected_components, shortest_path
+
+from oracle import agglomerate as A
+from workloads.unstructured import holed_quad_mesh, structured_quad_mesh
+
+
+def _graph(ne, edge_elem):
+    m = edge_elem[edge_elem[:, 1] >= 0]
+    return coo_matrix((np.ones(len(m)), (m[:, 0], m[:, 1])), shape=(ne, ne)).tocsr()
+
+
+@pytest.mark.parametrize("n,sx,sy,seed", [(12, 2, 2, 1), (20, 3, 2, 2), (24, 4, 2, 3001)])
+def test_level1_is_graph_voronoi_by_scipy_shortest_paths(n, sx, sy, seed):
+    """A1 against an independent library routine: unweighted all-source
+    shortest paths from scipy, then argmin over (distance, seed index)."""
+    m = holed_quad_mesh(n, holes=3, sx=sx, sy=sy, seed=seed)
+    D = shortest_path(_graph(m.ne, m.edge_elem), directed=False, unweighted=True,
+                      indices=m.seeds)                      # [nseed, ne]
+    assert np.isfinite(D).all()
+    want = np.lexsort((np.arange(len(m.seeds))[:, None].repeat(m.ne, 1), D), axis=0)[0]
+    got = A.seed_agglomerate(m.ne, m.edge_elem, m.seeds)
+    np.testing.assert_array_equal(got, want)
+
+
+def test_level1_on_a_strip_is_nearest_seed_with_ties_to_the_lower_index():
+    """1 x L strip: the dual graph is a path, d(t, s) = |t - s| (closed form)."""
+    L = 23
+    edge_elem = np.array([[t, t + 1] for t in range(L - 1)] + [[t, -1] for t in range(L)],
+                         dtype=np.int32)
+    seeds = [17, 3, 10, 20]
+    got = A.seed_agglomerate(L, edge_elem, seeds)
+    for t in range(L):
+        d = [abs(t - s) for s in seeds]
+        want = min(range(len(seeds)), key=lambda k: (d[k], k))
+        assert got[t] == want
+    seeds = [8, 2]                    # t = 5: d = 3 to both -> seed 0 (lower index)
+    got = A.seed_agglomerate(L, edge_elem, seeds)
+    assert got[5] == 0 and got[4] == 1 and got[6] == 0
+
+
+@pytest.mark.parametrize("m", [2, 3, 4])
+def test_quadrisection_of_a_square_grid_is_the_quadtree(m):
+    """A2 closed form: one seed on a 2^m x 2^m grid without jitter; level k
+    (k >= 2) id of element (i, j) = sum over the quadtree digits, east = x bit,
+    north = y bit, most significant first.  A transposed key or swapped child
+    digits breaks it."""
+    n = 1 << m
+    mesh = structured_quad_mesh(n, seeds=(5,))
+    labels, skel = A.agglomerate_levels(mesh.ne, mesh.edge_elem, mesh.cx, mesh.cy, mesh.seeds,
+                                        nlev=m + 3)
+    # element numbering of the structured mesh: row by row
+    i = np.arange(mesh.ne) % n
+    j = np.arange(mesh.ne) // n
+    assert (labels[0] == 0).all()
+    for k in range(2, m + 2):
+        want = np.zeros(mesh.ne, dtype=np.int64)
+        for lvl in range(1, k):
+            shift = m - lvl
+            want = 4 * want + 2 * ((i >> shift) & 1) + ((j >> shift) & 1)
+        np.testing.assert_array_equal(labels[k - 1], want)
+    # one element per agglomerate at level m+1: the next split keeps it in child 0
+    np.testing.assert_array_equal(labels[m + 1], 4 * labels[m])
+    # level m+1 skeleton = every edge; level 1 skeleton = the boundary of the box
+    assert skel[m].all()
+    np.testing.assert_array_equal(skel[0], (mesh.edge_elem[:, 1] < 0).astype(np.uint8))
+
+
+def test_split_sizes_connectivity_and_nested_skeletons():
+    m = holed_quad_mesh(40, holes=6, sx=3, sy=2, seed=7)
+    labels, skel = A.agglomerate_levels(m.ne, m.edge_elem, m.cx, m.cy, m.seeds, nlev=5)
+    G = _graph(m.ne, m.edge_elem)
+    # level-1 cells are connected (graph Voronoi cells with a consistent tie rule)
+    for g in np.unique(labels[0]):
+        idx = np.flatnonzero(labels[0] == g)
+        nc, _ = connected_components(G[idx][:, idx], directed=False)
+        assert nc == 1
+    for k in range(labels.shape[0] - 1):
+        par, ch = labels[k], labels[k + 1]
+        np.testing.assert_array_equal(ch // 4, par)          # children refine parents
+        for g in np.unique(par):
+            msz = int((par == g).sum())
+            h = [(msz + 1) // 2, msz // 2]
+            want = sorted([(h[0] + 1) // 2, h[0] // 2, (h[1] + 1) // 2, h[1] // 2])
+            got = sorted(int((ch == 4 * g + q).sum()) for q in range(4))
+            assert got == want
+        assert (skel[k] <= skel[k + 1]).all()                 # M_{k-1} inside M_{k,B}
+    assert skel[:, m.edge_elem[:, 1] < 0].all()
+
+
+def test_west_half_lies_left_of_east_half():
+    """A2: every west element precedes every east element of its parent in (cx, cy, id)."""
+    m = holed_quad_mesh(32, holes=4, sx=2, sy=2, seed=11)
+    labels, _ = A.agglomerate_levels(m.ne, m.edge_elem, m.cx, m.cy, m.seeds, nlev=3)
+    for g in np.unique(labels[0]):
+        idx = np.flatnonzero(labels[0] == g)
+        east = (labels[1][idx] // 2) % 2
+        kx = [(m.cx[t], m.cy[t], t) for t in idx]
+        assert max(k for k, e in zip(kx, east) if e == 0) < min(k for k, e in zip(kx, east) if e == 1)
+
+
+def test_unreachable_element_raises():
+    edge_elem = np.array([[0, 1], [2, -1], [0, -1], [1, -1]], dtype=np.int32)
+    with pytest.raises(ValueError):
+        A.seed_agglomerate(3, edge_elem, [0])
