@@ -336,6 +336,36 @@ enum { MG_OPT_SWEEP = 1, MG_OPT_APPLY_GRID_CAP = 2, MG_OPT_COMM_TIMEOUT_MS = 3,
        MG_OPT_GATHER_NE = 4, MG_OPT_KEEP_FINE_MAPS = 5 };
 int mg_set_option(void* ctx, int32_t key, int64_t value);
 
+/* ---- Seed-point agglomeration of an unstructured quad mesh ----
+ * PAPER.md:491-498 (section 3.1.2): N levels, N_T1 seed points; the fine
+ * elements (level N) are agglomerated around the seeds into N_T1 level-1
+ * macro-elements, then every level-k macro-element is divided into four
+ * approximately equal ones to form level k+1, k = 1 .. N-2.  PAPER.md:485-487:
+ * the level-(k-1) traces live on the boundary edges of the level-k agglomerates.
+ * Readings (A1-A3): level 1 = graph Voronoi cells of the
+ * seeds on the element dual graph (hop distance, ties to the lower seed index);
+ * the four-way split = west / east halves by rank under (cx, cy, id), the first
+ * ceil(m/2) west, then south / north by rank under (cy, cx, id) inside each half,
+ * child id 4*parent + 2*east + north; an edge is on the level-k skeleton iff it
+ * is on the domain boundary or its two elements differ in level-k label.
+ *   ne, nedge      elements and edges of the fine mesh (ne < 2^31)
+ *   edge_elem      DEVICE int32 [nedge][2]: the two elements of the edge,
+ *                  [e][1] = -1 on the domain boundary
+ *   cx, cy         DEVICE float64 [ne]: element centroids (the split's keys)
+ *   seeds          DEVICE int32 [nseed]: seed elements (duplicates: lower index wins)
+ *   nlev           N >= 2; outputs levels 1 .. N-1 (nseed * 4^(N-2) < 2^31)
+ *   labels         DEVICE int32 [(nlev-1)][ne] (caller-owned): row k-1 = level-k id
+ *   skel           DEVICE uint8 [(nlev-1)][nedge] (caller-owned): row k-1 = level-k skeleton
+ *   stream         cudaStream_t (NULL: legacy default); returns after it synchronises.
+ * Scratch (keys, member lists) is allocated with cudaMallocAsync on `stream`
+ * and freed before return: a setup-time call, once per mesh.  Errors: MG_ERR_ARG
+ * (NULL pointer, sizes, a seed or edge element id out of range), MG_ERR_SHAPE with
+ * *bad_index = the lowest element no seed reaches (disconnected mesh),
+ * MG_ERR_CUDA.  bad_index may be NULL; it is -1 unless MG_ERR_SHAPE. */
+int mg_agglomerate_seeds(int64_t ne, int64_t nedge, const int32_t* edge_elem, const double* cx,
+                         const double* cy, int32_t nseed, const int32_t* seeds, int32_t nlev,
+                         int32_t* labels, uint8_t* skel, void* stream, int64_t* bad_index);
+
 const char* mg_last_error(const void* ctx);
 int64_t mg_last_error_index(const void* ctx);
 void mg_destroy(void* ctx);

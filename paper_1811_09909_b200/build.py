@@ -16,7 +16,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
 
-SOURCES = ["k_apply.cu", "k_tile.cu", "k_debug.cu", "k_setup.cu", "k_local_ns.cu", "k_mg.cu", "k_coarse.cu", "k_part.cu", "comm.cu", "mgdtn.cu", "refelem.cpp"]
+SOURCES = ["k_apply.cu", "k_tile.cu", "k_debug.cu", "k_setup.cu", "k_local_ns.cu", "k_mg.cu", "k_coarse.cu", "k_part.cu", "comm.cu", "k_agglo.cu", "mgdtn.cu", "refelem.cpp"]
 
 
 def _compile(src: str) -> str:

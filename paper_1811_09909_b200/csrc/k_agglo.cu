@@ -1,0 +1,272 @@
+// Seed-point agglomeration of an unstructured quad mesh (SURVEY.md 8(f) f4,
+// PAPER.md:491-498, section 3.1.2; readings A1-A3 in DESIGN.md section 3):
+//   level 1      graph Voronoi cells of the seeds on the element dual graph,
+//                ties to the lower seed index (A1): a level-synchronous
+//                multi-source BFS whose per-element key (hop << 32 | seed) is
+//                lowered with atomicMin, one launch per BFS layer;
+//   level k + 1  every level-k agglomerate split in four (A2): west / east
+//                halves by rank under (cx, cy, id), then south / north by rank
+//                under (cy, cx, id) inside each half.  The ranks are counted
+//                per element over the agglomerate's member list (one thread per
+//                list position, so a warp mostly walks one member list and its
+//                loads are broadcasts); the member lists come from a counting
+//                sort (count, one-CTA exclusive scan, scatter);
+//   skeleton     an edge is on the level-k skeleton iff it is on the domain
+//                boundary or its two elements carry different labels (A3).
+// Integer output only: the comparisons are exact, so the labels are bit-equal
+// to any implementation of the same readings (tests/test_gpu_agglomerate.py).
+// This is setup-time work (once per mesh), not part of the solve.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "mgdtn.h"
+
+namespace {
+
+constexpr unsigned long long KEY_NONE = ~0ull;
+
+// keys reset; an edge naming an element outside [0, ne) (or no first element) is an error
+__global__ void k_seed_init(unsigned long long* key, int64_t ne, const int32_t* edge_elem,
+                            int64_t nedge, int* err) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < ne) key[t] = KEY_NONE;
+  if (t < nedge) {
+    const int32_t a = edge_elem[2 * t], b = edge_elem[2 * t + 1];
+    if (a < 0 || a >= ne || b < -1 || b >= ne) atomicExch(err, 1);
+  }
+}
+
+__global__ void k_seed_set(unsigned long long* key, int64_t ne, const int32_t* seeds, int nseed,
+                           int* err) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nseed) return;
+  const int32_t s = seeds[k];
+  if (s < 0 || s >= ne) {
+    atomicExch(err, 1);
+    return;
+  }
+  atomicMin(key + s, (unsigned long long)(uint32_t)k);   // hop 0; duplicate seeds: lower index
+}
+
+// one BFS layer: every element at hop d offers (d + 1, its seed) to its neighbours
+__global__ void k_bfs_layer(unsigned long long* key, const int32_t* __restrict__ edge_elem,
+                            int64_t nedge, uint32_t d, int* changed) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nedge) return;
+  const int32_t a = edge_elem[2 * e], b = edge_elem[2 * e + 1];
+  if (b < 0) return;
+  const unsigned long long ka = key[a], kb = key[b];
+  const unsigned long long nxt = (unsigned long long)(d + 1) << 32;
+  if (ka != KEY_NONE && (uint32_t)(ka >> 32) == d) {
+    const unsigned long long c = nxt | (ka & 0xffffffffull);
+    if (c < kb) {
+      atomicMin(key + b, c);
+      *changed = 1;
+    }
+  }
+  if (kb != KEY_NONE && (uint32_t)(kb >> 32) == d) {
+    const unsigned long long c = nxt | (kb & 0xffffffffull);
+    if (c < ka) {
+      atomicMin(key + a, c);
+      *changed = 1;
+    }
+  }
+}
+
+__global__ void k_label1(const unsigned long long* key, int64_t ne, int32_t* lab,
+                         unsigned long long* bad) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ne) return;
+  const unsigned long long k = key[t];
+  if (k == KEY_NONE) {
+    atomicMin(bad, (unsigned long long)t);
+    lab[t] = -1;
+  } else {
+    lab[t] = (int32_t)(k & 0xffffffffull);
+  }
+}
+
+__global__ void k_count(const int32_t* lab, int64_t ne, int32_t* cnt) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < ne) atomicAdd(cnt + lab[t], 1);
+}
+
+// exclusive scan of cnt[0..G) into off[0..G) by one CTA (setup-time, G <= ne)
+__global__ void k_scan(const int32_t* cnt, int64_t G, int64_t* off) {
+  __shared__ int64_t part[1024];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t per = (G + nt - 1) / nt, lo = tid * per, hi = lo + per < G ? lo + per : G;
+  int64_t s = 0;
+  for (int64_t g = lo; g < hi; ++g) s += cnt[g];
+  part[tid] = s;
+  __syncthreads();
+  if (tid == 0) {
+    int64_t run = 0;
+    for (int i = 0; i < nt; ++i) {
+      const int64_t v = part[i];
+      part[i] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  s = part[tid];
+  for (int64_t g = lo; g < hi; ++g) {
+    off[g] = s;
+    s += cnt[g];
+  }
+}
+
+__global__ void k_scatter(const int32_t* lab, int64_t ne, const int64_t* off, int32_t* cur,
+                          int32_t* list) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ne) return;
+  const int32_t g = lab[t];
+  list[off[g] + atomicAdd(cur + g, 1)] = (int32_t)t;
+}
+
+// (u0, u1, u) < (t0, t1, t) lexicographically
+__device__ __forceinline__ bool lex_less(double u0, double u1, int32_t u, double t0, double t1,
+                                         int32_t t) {
+  return u0 < t0 || (u0 == t0 && (u1 < t1 || (u1 == t1 && u < t)));
+}
+
+// west / east half (A2): rank of list[i] under (cx, cy, id) among its agglomerate
+__global__ void k_half(const int32_t* __restrict__ list, int64_t ne, const int32_t* __restrict__ lab,
+                       const int64_t* __restrict__ off, const int32_t* __restrict__ cnt,
+                       const double* __restrict__ cx, const double* __restrict__ cy,
+                       uint8_t* east) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ne) return;
+  const int32_t t = list[i], g = lab[t];
+  const double t0 = cx[t], t1 = cy[t];
+  const int64_t o = off[g];
+  const int32_t m = cnt[g];
+  int32_t rank = 0;
+  for (int32_t j = 0; j < m; ++j) {
+    const int32_t u = list[o + j];
+    rank += lex_less(cx[u], cy[u], u, t0, t1, t);
+  }
+  east[t] = rank >= (m + 1) / 2;
+}
+
+// south / north quarter (A2): rank under (cy, cx, id) among the same half
+__global__ void k_quarter(const int32_t* __restrict__ list, int64_t ne,
+                          const int32_t* __restrict__ lab, const int64_t* __restrict__ off,
+                          const int32_t* __restrict__ cnt, const double* __restrict__ cx,
+                          const double* __restrict__ cy, const uint8_t* __restrict__ east,
+                          int32_t* nlab) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ne) return;
+  const int32_t t = list[i], g = lab[t];
+  const double t0 = cy[t], t1 = cx[t];
+  const uint8_t h = east[t];
+  const int64_t o = off[g];
+  const int32_t m = cnt[g];
+  int32_t rank = 0, hm = 0;
+  for (int32_t j = 0; j < m; ++j) {
+    const int32_t u = list[o + j];
+    if (east[u] != h) continue;
+    ++hm;
+    rank += lex_less(cy[u], cx[u], u, t0, t1, t);
+  }
+  nlab[t] = 4 * g + 2 * h + (rank >= (hm + 1) / 2);
+}
+
+__global__ void k_skeleton(const int32_t* __restrict__ edge_elem, int64_t nedge,
+                           const int32_t* __restrict__ lab, uint8_t* skel) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nedge) return;
+  const int32_t a = edge_elem[2 * e], b = edge_elem[2 * e + 1];
+  skel[e] = b < 0 || lab[a] != lab[b];
+}
+
+inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t > 0 ? (n + t - 1) / t : 1); }
+
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void*> p;
+  template <class T>
+  T* get(size_t n) {
+    void* q = nullptr;
+    if (cudaMallocAsync(&q, n * sizeof(T) + 16, st) != cudaSuccess) return nullptr;
+    p.push_back(q);
+    return (T*)q;
+  }
+  ~Scratch() {
+    for (void* q : p) cudaFreeAsync(q, st);
+  }
+};
+
+}  // namespace
+
+extern "C" int mg_agglomerate_seeds(int64_t ne, int64_t nedge, const int32_t* edge_elem,
+                                    const double* cx, const double* cy, int32_t nseed,
+                                    const int32_t* seeds, int32_t nlev, int32_t* labels,
+                                    uint8_t* skel, void* stream, int64_t* bad_index) {
+  if (bad_index) *bad_index = -1;
+  if (ne <= 0 || ne > INT32_MAX || nedge <= 0 || nseed <= 0 || nlev < 2 || !edge_elem || !cx ||
+      !cy || !seeds || !labels || !skel)
+    return MG_ERR_ARG;
+  // level k has nseed * 4^(k-1) ids; keep the last one within int32
+  long double G = nseed;
+  for (int k = 2; k < nlev; ++k) G *= 4;
+  if (G > (long double)INT32_MAX) return MG_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = MG_OK;
+  {
+    Scratch S{st, {}};
+    unsigned long long* key = S.get<unsigned long long>(ne);
+    unsigned long long* bad = S.get<unsigned long long>(1);
+    int* flags = S.get<int>(2);   // [0] seed error, [1] BFS changed
+    int32_t* cnt = S.get<int32_t>((size_t)G);
+    int32_t* cur = S.get<int32_t>((size_t)G);
+    int64_t* off = S.get<int64_t>((size_t)G);
+    int32_t* list = S.get<int32_t>(ne);
+    uint8_t* east = S.get<uint8_t>(ne);
+    if (!key || !bad || !flags || !cnt || !cur || !off || !list || !east) return MG_ERR_CUDA;
+    int hflags[2] = {0, 0};
+    cudaMemsetAsync(flags, 0, 2 * sizeof(int), st);
+    cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st);
+    k_seed_init<<<nblk(ne > nedge ? ne : nedge), 256, 0, st>>>(key, ne, edge_elem, nedge, flags);
+    k_seed_set<<<nblk(nseed), 256, 0, st>>>(key, ne, seeds, nseed, flags);
+    cudaMemcpyAsync(hflags, flags, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return MG_ERR_CUDA;
+    if (hflags[0]) return MG_ERR_ARG;   // seed or edge element id out of range
+    // BFS layers in batches of 16 between host checks (extra layers are no-ops)
+    for (uint32_t d = 0;; d += 16) {
+      cudaMemsetAsync(flags + 1, 0, sizeof(int), st);
+      for (uint32_t q = 0; q < 16; ++q)
+        k_bfs_layer<<<nblk(nedge), 256, 0, st>>>(key, edge_elem, nedge, d + q, flags + 1);
+      cudaMemcpyAsync(hflags, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st);
+      if (cudaStreamSynchronize(st) != cudaSuccess) return MG_ERR_CUDA;
+      if (!hflags[1]) break;
+    }
+    k_label1<<<nblk(ne), 256, 0, st>>>(key, ne, labels, bad);
+    k_skeleton<<<nblk(nedge), 256, 0, st>>>(edge_elem, nedge, labels, skel);
+    unsigned long long hbad = 0;
+    cudaMemcpyAsync(&hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return MG_ERR_CUDA;
+    if (hbad != KEY_NONE) {   // an element no seed reaches
+      if (bad_index) *bad_index = (int64_t)hbad;
+      return MG_ERR_SHAPE;
+    }
+    int64_t Gk = nseed;
+    for (int k = 1; k + 1 < nlev; ++k, Gk *= 4) {
+      const int32_t* lab = labels + (size_t)(k - 1) * ne;
+      int32_t* nlab = labels + (size_t)k * ne;
+      cudaMemsetAsync(cnt, 0, (size_t)Gk * sizeof(int32_t), st);
+      cudaMemsetAsync(cur, 0, (size_t)Gk * sizeof(int32_t), st);
+      k_count<<<nblk(ne), 256, 0, st>>>(lab, ne, cnt);
+      k_scan<<<1, 1024, 0, st>>>(cnt, Gk, off);
+      k_scatter<<<nblk(ne), 256, 0, st>>>(lab, ne, off, cur, list);
+      k_half<<<nblk(ne), 256, 0, st>>>(list, ne, lab, off, cnt, cx, cy, east);
+      k_quarter<<<nblk(ne), 256, 0, st>>>(list, ne, lab, off, cnt, cx, cy, east, nlab);
+      k_skeleton<<<nblk(nedge), 256, 0, st>>>(edge_elem, nedge, nlab, skel + (size_t)k * nedge);
+    }
+    if (cudaGetLastError() != cudaSuccess) rc = MG_ERR_CUDA;
+  }
+  if (cudaStreamSynchronize(st) != cudaSuccess) rc = MG_ERR_CUDA;
+  return rc;
+}

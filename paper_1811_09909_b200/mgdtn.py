@@ -92,6 +92,8 @@ _SIGS = {
     "mg_loopback_create": [C.c_int32],
     "mg_loopback_destroy": [_P],
     "mg_loopback_abort": [_P],
+    "mg_agglomerate_seeds": [C.c_int64, C.c_int64, _P, _P, _P, C.c_int32, _P, C.c_int32, _P, _P, _P,
+                             C.POINTER(C.c_int64)],
     "mg_last_error": [_P],
     "mg_last_error_index": [_P],
     "mg_destroy": [_P],
@@ -217,6 +219,30 @@ def nccl_unique_id() -> bytes:
     if rc != MG_OK:
         raise MGError(f"mg_get_nccl_unique_id: {ERRORS.get(rc, rc)}")
     return buf.raw
+
+
+def agglomerate_seeds(edge_elem, cx, cy, seeds, nlev: int, stream=None):
+    """Seed-point agglomeration (mg_agglomerate_seeds): device
+    tensors in (edge_elem int32 [nedge, 2], cx / cy float64 [ne], seeds int32),
+    device tensors out: labels int32 [nlev-1, ne], skeleton uint8 [nlev-1, nedge]."""
+    import torch
+    lib = load_library()
+    ne, nedge = int(cx.numel()), int(edge_elem.shape[0])
+    for t, dt in ((edge_elem, torch.int32), (cx, torch.float64), (cy, torch.float64),
+                  (seeds, torch.int32)):
+        if not t.is_cuda or t.dtype != dt or not t.is_contiguous():
+            raise MGError(f"agglomerate_seeds: expected a contiguous CUDA {dt} tensor")
+    dev = cx.device
+    labels = torch.empty((max(nlev - 1, 1), ne), dtype=torch.int32, device=dev)
+    skel = torch.empty((max(nlev - 1, 1), nedge), dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream(dev) if stream is None else stream
+    bad = C.c_int64(-1)
+    rc = lib.mg_agglomerate_seeds(ne, nedge, _ptr(edge_elem), _ptr(cx), _ptr(cy), int(seeds.numel()),
+                                  _ptr(seeds), int(nlev), _ptr(labels), _ptr(skel),
+                                  C.c_void_p(st.cuda_stream), C.byref(bad))
+    if rc != 0:
+        raise MGError(f"mg_agglomerate_seeds: {ERRORS.get(rc, rc)} (element {bad.value})")
+    return labels, skel
 
 
 def partition_plan(nx: int, ny: int, p: int, part: Partition, n_h_levels: int = 0):
