@@ -26,6 +26,11 @@ The paper calls its procedure "ad hoc" and does not fix the rules; readings
   A3  an edge is on the level-k skeleton iff it lies on the domain boundary or
       its two elements have different level-k labels (k = 1..N-1); every edge
       is on the level-N (fine) skeleton.
+  A4  PAPER.md:355-356: "each e in E_k is the intersection of two
+      macro-elements in T_k": the level-k macro-edges are the non-empty sets
+      {fine edges between agglomerates a < b} and {fine edges of agglomerate a
+      on the domain boundary} (pair (-1, a)), numbered by the lexicographic
+      order of their pairs; a fine edge off the level-k skeleton gets -1.
 """
 from __future__ import annotations
 
@@ -98,6 +103,22 @@ def skeleton(labels: np.ndarray, edge_elem: np.ndarray) -> np.ndarray:
     inner = b >= 0
     out[inner] = (labels[a[inner]] != labels[b[inner]]).astype(np.uint8)
     return out
+
+
+def macro_edges(labels: np.ndarray, edge_elem: np.ndarray):
+    """Level macro-edge id of every fine edge (-1 off the skeleton) and the
+    number of macro-edges (reading A4)."""
+    pairs = []
+    for a, b in edge_elem.tolist():
+        if b < 0:
+            pairs.append((-1, int(labels[a])))
+        elif labels[a] != labels[b]:
+            la, lb = int(labels[a]), int(labels[b])
+            pairs.append((min(la, lb), max(la, lb)))
+        else:
+            pairs.append(None)
+    ids = {q: k for k, q in enumerate(sorted({q for q in pairs if q is not None}))}
+    return np.array([-1 if q is None else ids[q] for q in pairs], dtype=np.int32), len(ids)
 
 
 def agglomerate_levels(ne, edge_elem, cx, cy, seeds, nlev: int):

@@ -110,3 +110,27 @@ def test_unreachable_element_raises():
     edge_elem = np.array([[0, 1], [2, -1], [0, -1], [1, -1]], dtype=np.int32)
     with pytest.raises(ValueError):
         A.seed_agglomerate(3, edge_elem, [0])
+
+
+def test_macro_edges_of_the_quadtree_closed_form():
+    """A4 on the 2^m grid with one seed: level 2 (four quadrants) has 4 interior
+    macro-edges (W-E pairs (0,2), (1,3), S-N pairs (0,1), (2,3)) and 4 boundary
+    ones; every macro-edge of level k is a union of level-(k+1) macro-edges."""
+    n = 8
+    mesh = structured_quad_mesh(n)
+    labels, skel = A.agglomerate_levels(mesh.ne, mesh.edge_elem, mesh.cx, mesh.cy, mesh.seeds, 4)
+    me, nme = A.macro_edges(labels[1], mesh.edge_elem)
+    assert nme == 8
+    np.testing.assert_array_equal(me >= 0, skel[1].astype(bool))
+    a, b = mesh.edge_elem[:, 0], mesh.edge_elem[:, 1]
+    pairs = sorted({(-1, int(labels[1][x])) if y < 0 else tuple(sorted((int(labels[1][x]), int(labels[1][y]))))
+                    for x, y in zip(a, b) if y < 0 or labels[1][x] != labels[1][y]})
+    assert pairs == [(-1, 0), (-1, 1), (-1, 2), (-1, 3), (0, 1), (0, 2), (1, 3), (2, 3)]
+    for q in range(nme):      # a quadrant's share of dOmega: two sides; an interface: one
+        assert (me == q).sum() == (n if pairs[q][0] < 0 else n // 2)
+    me3, _ = A.macro_edges(labels[2], mesh.edge_elem)
+    for q in range(nme):                           # nesting: children's macro-edges tile it
+        sub = np.unique(me3[me == q])
+        assert (sub >= 0).all()
+        for r in sub:
+            assert (me[me3 == r] == q).all()
