@@ -356,6 +356,12 @@ int mg_set_option(void* ctx, int32_t key, int64_t value);
  *   nlev           N >= 2; outputs levels 1 .. N-1 (nseed * 4^(N-2) < 2^31)
  *   labels         DEVICE int32 [(nlev-1)][ne] (caller-owned): row k-1 = level-k id
  *   skel           DEVICE uint8 [(nlev-1)][nedge] (caller-owned): row k-1 = level-k skeleton
+ *   medge          DEVICE int32 [(nlev-1)][nedge] or NULL: row k-1 = the fine edge's level-k
+ *                  macro-edge id, -1 off the skeleton (reading A4: a
+ *                  macro-edge is the intersection of two agglomerates, or an agglomerate's
+ *                  share of the domain boundary = pair (-1, a); ids in lexicographic
+ *                  order of the pairs (lo, hi))
+ *   nmedge         HOST int64 [nlev-1] (required with medge): macro-edges per level
  *   stream         cudaStream_t (NULL: legacy default); returns after it synchronises.
  * Scratch (keys, member lists) is allocated with cudaMallocAsync on `stream`
  * and freed before return: a setup-time call, once per mesh.  Errors: MG_ERR_ARG
@@ -364,7 +370,8 @@ int mg_set_option(void* ctx, int32_t key, int64_t value);
  * MG_ERR_CUDA.  bad_index may be NULL; it is -1 unless MG_ERR_SHAPE. */
 int mg_agglomerate_seeds(int64_t ne, int64_t nedge, const int32_t* edge_elem, const double* cx,
                          const double* cy, int32_t nseed, const int32_t* seeds, int32_t nlev,
-                         int32_t* labels, uint8_t* skel, void* stream, int64_t* bad_index);
+                         int32_t* labels, uint8_t* skel, int32_t* medge, int64_t* nmedge,
+                         void* stream, int64_t* bad_index);
 
 const char* mg_last_error(const void* ctx);
 int64_t mg_last_error_index(const void* ctx);

@@ -182,6 +182,89 @@ __global__ void k_skeleton(const int32_t* __restrict__ edge_elem, int64_t nedge,
   skel[e] = b < 0 || lab[a] != lab[b];
 }
 
+// ---- level macro-edges (reading A4): the fine skeleton edges grouped by their pair
+// (lo, hi) of agglomerates (lo = -1 on the domain boundary), numbered in lexicographic
+// pair order.  Bucketed by lo (counting sort); inside a bucket the distinct hi values are
+// found and ranked by comparison (a bucket is about one agglomerate's perimeter).
+__device__ __forceinline__ bool edge_pair(const int32_t* __restrict__ edge_elem,
+                                          const int32_t* __restrict__ lab, int64_t e, int32_t& lo,
+                                          int32_t& hi) {
+  const int32_t a = edge_elem[2 * e], b = edge_elem[2 * e + 1];
+  if (b < 0) {
+    lo = -1;
+    hi = lab[a];
+    return true;
+  }
+  const int32_t la = lab[a], lb = lab[b];
+  lo = la < lb ? la : lb;
+  hi = la < lb ? lb : la;
+  return la != lb;
+}
+
+__global__ void k_me_count(const int32_t* edge_elem, int64_t nedge, const int32_t* lab,
+                           int32_t* cnt) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nedge) return;
+  int32_t lo, hi;
+  if (edge_pair(edge_elem, lab, e, lo, hi)) atomicAdd(cnt + lo + 1, 1);
+}
+
+__global__ void k_me_scatter(const int32_t* edge_elem, int64_t nedge, const int32_t* lab,
+                             const int64_t* off, int32_t* cur, int32_t* elist) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nedge) return;
+  int32_t lo, hi;
+  if (edge_pair(edge_elem, lab, e, lo, hi)) elist[off[lo + 1] + atomicAdd(cur + lo + 1, 1)] = (int32_t)e;
+}
+
+// first[e] = e is the lowest-numbered edge of its pair; dcnt[bucket] counts the pairs
+__global__ void k_me_first(const int32_t* __restrict__ edge_elem, int64_t nsk,
+                           const int32_t* __restrict__ lab, const int32_t* __restrict__ elist,
+                           const int64_t* __restrict__ off, const int32_t* __restrict__ cnt,
+                           uint8_t* first, int32_t* dcnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nsk) return;
+  const int32_t e = elist[i];
+  int32_t lo, hi;
+  edge_pair(edge_elem, lab, e, lo, hi);
+  const int64_t o = off[lo + 1];
+  const int32_t m = cnt[lo + 1];
+  bool f = true;
+  for (int32_t j = 0; j < m && f; ++j) {
+    const int32_t u = elist[o + j];
+    int32_t ul, uh;
+    edge_pair(edge_elem, lab, u, ul, uh);
+    if (uh == hi && u < e) f = false;
+  }
+  first[e] = f;
+  if (f) atomicAdd(dcnt + lo + 1, 1);
+}
+
+__global__ void k_me_rank(const int32_t* __restrict__ edge_elem, int64_t nedge,
+                          const int32_t* __restrict__ lab, const int32_t* __restrict__ elist,
+                          const int64_t* __restrict__ off, const int32_t* __restrict__ cnt,
+                          const uint8_t* __restrict__ first, const int64_t* __restrict__ doff,
+                          int32_t* medge) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nedge) return;
+  int32_t lo, hi;
+  if (!edge_pair(edge_elem, lab, e, lo, hi)) {
+    medge[e] = -1;
+    return;
+  }
+  const int64_t o = off[lo + 1];
+  const int32_t m = cnt[lo + 1];
+  int32_t rank = 0;
+  for (int32_t j = 0; j < m; ++j) {
+    const int32_t u = elist[o + j];
+    if (!first[u]) continue;
+    int32_t ul, uh;
+    edge_pair(edge_elem, lab, u, ul, uh);
+    rank += uh < hi;
+  }
+  medge[e] = (int32_t)(doff[lo + 1] + rank);
+}
+
 inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t > 0 ? (n + t - 1) / t : 1); }
 
 struct Scratch {
@@ -204,10 +287,11 @@ struct Scratch {
 extern "C" int mg_agglomerate_seeds(int64_t ne, int64_t nedge, const int32_t* edge_elem,
                                     const double* cx, const double* cy, int32_t nseed,
                                     const int32_t* seeds, int32_t nlev, int32_t* labels,
-                                    uint8_t* skel, void* stream, int64_t* bad_index) {
+                                    uint8_t* skel, int32_t* medge, int64_t* nmedge,
+                                    void* stream, int64_t* bad_index) {
   if (bad_index) *bad_index = -1;
   if (ne <= 0 || ne > INT32_MAX || nedge <= 0 || nseed <= 0 || nlev < 2 || !edge_elem || !cx ||
-      !cy || !seeds || !labels || !skel)
+      !cy || !seeds || !labels || !skel || (medge && !nmedge))
     return MG_ERR_ARG;
   // level k has nseed * 4^(k-1) ids; keep the last one within int32
   long double G = nseed;
@@ -220,12 +304,16 @@ extern "C" int mg_agglomerate_seeds(int64_t ne, int64_t nedge, const int32_t* ed
     unsigned long long* key = S.get<unsigned long long>(ne);
     unsigned long long* bad = S.get<unsigned long long>(1);
     int* flags = S.get<int>(2);   // [0] seed error, [1] BFS changed
-    int32_t* cnt = S.get<int32_t>((size_t)G);
-    int32_t* cur = S.get<int32_t>((size_t)G);
-    int64_t* off = S.get<int64_t>((size_t)G);
-    int32_t* list = S.get<int32_t>(ne);
-    uint8_t* east = S.get<uint8_t>(ne);
-    if (!key || !bad || !flags || !cnt || !cur || !off || !list || !east) return MG_ERR_CUDA;
+    // counting-sort buffers: G agglomerates (splits) or G + 1 pair buckets (macro-edges)
+    int32_t* cnt = S.get<int32_t>((size_t)G + 1);
+    int32_t* cur = S.get<int32_t>((size_t)G + 1);
+    int64_t* off = S.get<int64_t>((size_t)G + 1);
+    int32_t* dcnt = S.get<int32_t>((size_t)G + 1);
+    int64_t* doff = S.get<int64_t>((size_t)G + 1);
+    int32_t* list = S.get<int32_t>(ne > nedge ? ne : nedge);
+    uint8_t* east = S.get<uint8_t>(ne > nedge ? ne : nedge);
+    if (!key || !bad || !flags || !cnt || !cur || !off || !dcnt || !doff || !list || !east)
+      return MG_ERR_CUDA;
     int hflags[2] = {0, 0};
     cudaMemsetAsync(flags, 0, 2 * sizeof(int), st);
     cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st);
@@ -253,8 +341,33 @@ extern "C" int mg_agglomerate_seeds(int64_t ne, int64_t nedge, const int32_t* ed
       return MG_ERR_SHAPE;
     }
     int64_t Gk = nseed;
-    for (int k = 1; k + 1 < nlev; ++k, Gk *= 4) {
+    for (int k = 1; k < nlev; ++k, Gk *= 4) {
       const int32_t* lab = labels + (size_t)(k - 1) * ne;
+      if (medge) {   // level-k macro-edges (A4); `east` doubles as the first-of-pair flags
+        int32_t* me = medge + (size_t)(k - 1) * nedge;
+        const int64_t B = Gk + 1;
+        cudaMemsetAsync(cnt, 0, (size_t)B * sizeof(int32_t), st);
+        cudaMemsetAsync(cur, 0, (size_t)B * sizeof(int32_t), st);
+        cudaMemsetAsync(dcnt, 0, (size_t)B * sizeof(int32_t), st);
+        k_me_count<<<nblk(nedge), 256, 0, st>>>(edge_elem, nedge, lab, cnt);
+        k_scan<<<1, 1024, 0, st>>>(cnt, B, off);
+        k_me_scatter<<<nblk(nedge), 256, 0, st>>>(edge_elem, nedge, lab, off, cur, list);
+        int64_t hoff = 0;
+        int32_t hcnt = 0;
+        cudaMemcpyAsync(&hoff, off + Gk, sizeof(hoff), cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(&hcnt, cnt + Gk, sizeof(hcnt), cudaMemcpyDeviceToHost, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) return MG_ERR_CUDA;
+        const int64_t nsk = hoff + hcnt;   // skeleton edges of level k
+        k_me_first<<<nblk(nsk), 256, 0, st>>>(edge_elem, nsk, lab, list, off, cnt, east, dcnt);
+        k_scan<<<1, 1024, 0, st>>>(dcnt, B, doff);
+        k_me_rank<<<nblk(nedge), 256, 0, st>>>(edge_elem, nedge, lab, list, off, cnt, east, doff, me);
+        int32_t hd = 0;
+        cudaMemcpyAsync(&hoff, doff + Gk, sizeof(hoff), cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(&hd, dcnt + Gk, sizeof(hd), cudaMemcpyDeviceToHost, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) return MG_ERR_CUDA;
+        nmedge[k - 1] = hoff + hd;
+      }
+      if (k + 1 == nlev) break;
       int32_t* nlab = labels + (size_t)k * ne;
       cudaMemsetAsync(cnt, 0, (size_t)Gk * sizeof(int32_t), st);
       cudaMemsetAsync(cur, 0, (size_t)Gk * sizeof(int32_t), st);

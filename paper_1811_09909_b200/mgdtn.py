@@ -93,7 +93,7 @@ _SIGS = {
     "mg_loopback_destroy": [_P],
     "mg_loopback_abort": [_P],
     "mg_agglomerate_seeds": [C.c_int64, C.c_int64, _P, _P, _P, C.c_int32, _P, C.c_int32, _P, _P, _P,
-                             C.POINTER(C.c_int64)],
+                             _P, _P, C.POINTER(C.c_int64)],
     "mg_last_error": [_P],
     "mg_last_error_index": [_P],
     "mg_destroy": [_P],
@@ -224,7 +224,8 @@ def nccl_unique_id() -> bytes:
 def agglomerate_seeds(edge_elem, cx, cy, seeds, nlev: int, stream=None):
     """Seed-point agglomeration (mg_agglomerate_seeds): device
     tensors in (edge_elem int32 [nedge, 2], cx / cy float64 [ne], seeds int32),
-    device tensors out: labels int32 [nlev-1, ne], skeleton uint8 [nlev-1, nedge]."""
+    device tensors out: labels int32 [nlev-1, ne], skeleton uint8 [nlev-1, nedge],
+    macro-edge ids int32 [nlev-1, nedge]; and the macro-edge count per level (list)."""
     import torch
     lib = load_library()
     ne, nedge = int(cx.numel()), int(edge_elem.shape[0])
@@ -235,14 +236,16 @@ def agglomerate_seeds(edge_elem, cx, cy, seeds, nlev: int, stream=None):
     dev = cx.device
     labels = torch.empty((max(nlev - 1, 1), ne), dtype=torch.int32, device=dev)
     skel = torch.empty((max(nlev - 1, 1), nedge), dtype=torch.uint8, device=dev)
+    medge = torch.empty((max(nlev - 1, 1), nedge), dtype=torch.int32, device=dev)
+    nme = (C.c_int64 * max(nlev - 1, 1))()
     st = torch.cuda.current_stream(dev) if stream is None else stream
     bad = C.c_int64(-1)
     rc = lib.mg_agglomerate_seeds(ne, nedge, _ptr(edge_elem), _ptr(cx), _ptr(cy), int(seeds.numel()),
-                                  _ptr(seeds), int(nlev), _ptr(labels), _ptr(skel),
-                                  C.c_void_p(st.cuda_stream), C.byref(bad))
+                                  _ptr(seeds), int(nlev), _ptr(labels), _ptr(skel), _ptr(medge),
+                                  C.cast(nme, C.c_void_p), C.c_void_p(st.cuda_stream), C.byref(bad))
     if rc != 0:
         raise MGError(f"mg_agglomerate_seeds: {ERRORS.get(rc, rc)} (element {bad.value})")
-    return labels, skel
+    return labels, skel, medge, list(nme)[:nlev - 1]
 
 
 def partition_plan(nx: int, ny: int, p: int, part: Partition, n_h_levels: int = 0):

@@ -3,7 +3,7 @@ quad mesh (mg_agglomerate_seeds; readings A1-A3) against
 oracle/agglomerate.py, bit for bit (integer output): level labels and level
 skeletons on holed, jittered meshes (the Example II stand-in, DESIGN.md
 section 4), a 2^m grid, a strip, and the edge cases (one seed, every element a
-seed, duplicate seeds, levels past one element per agglomerate, a disconnected
+seed, duplicate seeds, macro-edges (A4), levels past one element per agglomerate, a disconnected
 mesh, bad ids)."""
 import numpy as np
 import pytest
@@ -26,17 +26,21 @@ def _built():
 def _gpu(m: QuadMesh, nlev: int):
     from paper_1811_09909_b200 import agglomerate_seeds
     d = torch.device("cuda:0")
-    lab, sk = agglomerate_seeds(torch.from_numpy(m.edge_elem).to(d).contiguous(),
+    lab, sk, me, nme = agglomerate_seeds(torch.from_numpy(m.edge_elem).to(d).contiguous(),
                                 torch.from_numpy(m.cx).to(d), torch.from_numpy(m.cy).to(d),
                                 torch.from_numpy(m.seeds).to(d), nlev)
-    return lab.cpu().numpy(), sk.cpu().numpy()
+    return lab.cpu().numpy(), sk.cpu().numpy(), me.cpu().numpy(), nme
 
 
 def _check(m: QuadMesh, nlev: int):
     want_l, want_s = A.agglomerate_levels(m.ne, m.edge_elem, m.cx, m.cy, m.seeds, nlev)
-    got_l, got_s = _gpu(m, nlev)
+    got_l, got_s, got_me, got_n = _gpu(m, nlev)
     np.testing.assert_array_equal(got_l, want_l)
     np.testing.assert_array_equal(got_s, want_s)
+    for k in range(nlev - 1):
+        want_me, want_n = A.macro_edges(want_l[k], m.edge_elem)
+        np.testing.assert_array_equal(got_me[k], want_me)
+        assert got_n[k] == want_n
 
 
 # (n, holes, sx, sy, seed, nlev): Example II's setting is N = 7 levels from 7 or 4 seeds
