@@ -6,11 +6,11 @@
 //                lowered with atomicMin, one launch per BFS layer;
 //   level k + 1  every level-k agglomerate split in four (A2): west / east
 //                halves by rank under (cx, cy, id), then south / north by rank
-//                under (cy, cx, id) inside each half.  The ranks are counted
-//                per element over the agglomerate's member list (one thread per
-//                list position, so a warp mostly walks one member list and its
-//                loads are broadcasts); the member lists come from a counting
-//                sort (count, one-CTA exclusive scan, scatter);
+//                under (cy, cx, id) inside each half.  The ranks come from
+//                stable LSD radix sorts of the element ids (CUB, least
+//                significant key first, the agglomerate label last): an
+//                element's rank is its sorted position minus its agglomerate's
+//                offset (count + one-CTA exclusive scan);
 //   skeleton     an edge is on the level-k skeleton iff it is on the domain
 //                boundary or its two elements carry different labels (A3).
 // Integer output only: the comparisons are exact, so the labels are bit-equal
@@ -20,6 +20,8 @@
 
 #include <cstdint>
 #include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
 
 #include "mgdtn.h"
 
@@ -118,60 +120,55 @@ __global__ void k_scan(const int32_t* cnt, int64_t G, int64_t* off) {
   }
 }
 
-__global__ void k_scatter(const int32_t* lab, int64_t ne, const int64_t* off, int32_t* cur,
-                          int32_t* list) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= ne) return;
-  const int32_t g = lab[t];
-  list[off[g] + atomicAdd(cur + g, 1)] = (int32_t)t;
+// ---- four-way split (A2) by stable LSD sorts: the element ids start in id order, then
+// are stably sorted by the least significant key first, so after the sort by the
+// agglomerate label they are in (label, key1, key2, id) order and an element's rank in
+// its agglomerate is its position minus the agglomerate's offset.
+__global__ void k_iota(int32_t* perm, int64_t ne) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < ne) perm[i] = (int32_t)i;
 }
 
-// (u0, u1, u) < (t0, t1, t) lexicographically
-__device__ __forceinline__ bool lex_less(double u0, double u1, int32_t u, double t0, double t1,
-                                         int32_t t) {
-  return u0 < t0 || (u0 == t0 && (u1 < t1 || (u1 == t1 && u < t)));
+// sort key of position i: v[perm[i]], -0.0 folded into +0.0 (the radix order of the bit
+// patterns then equals the order of operator<; NaN is rejected up front)
+__global__ void k_gather_d(const int32_t* __restrict__ perm, const double* __restrict__ v,
+                           int64_t ne, double* key) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ne) return;
+  const double x = v[perm[i]];
+  key[i] = x == 0.0 ? 0.0 : x;
 }
 
-// west / east half (A2): rank of list[i] under (cx, cy, id) among its agglomerate
-__global__ void k_half(const int32_t* __restrict__ list, int64_t ne, const int32_t* __restrict__ lab,
+__global__ void k_gather_i(const int32_t* __restrict__ perm, const int32_t* __restrict__ v,
+                           int64_t ne, int32_t* key) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < ne) key[i] = v[perm[i]];
+}
+
+// west / east half: the first ceil(m/2) of an agglomerate in (cx, cy, id) order are west;
+// sub = 2 * label + east keys the second split
+__global__ void k_half(const int32_t* __restrict__ perm, int64_t ne, const int32_t* __restrict__ lab,
                        const int64_t* __restrict__ off, const int32_t* __restrict__ cnt,
-                       const double* __restrict__ cx, const double* __restrict__ cy,
-                       uint8_t* east) {
+                       int32_t* sub) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ne) return;
-  const int32_t t = list[i], g = lab[t];
-  const double t0 = cx[t], t1 = cy[t];
-  const int64_t o = off[g];
-  const int32_t m = cnt[g];
-  int32_t rank = 0;
-  for (int32_t j = 0; j < m; ++j) {
-    const int32_t u = list[o + j];
-    rank += lex_less(cx[u], cy[u], u, t0, t1, t);
-  }
-  east[t] = rank >= (m + 1) / 2;
+  const int32_t t = perm[i], g = lab[t];
+  sub[t] = 2 * g + (i - off[g] >= (cnt[g] + 1) / 2);
 }
 
-// south / north quarter (A2): rank under (cy, cx, id) among the same half
-__global__ void k_quarter(const int32_t* __restrict__ list, int64_t ne,
-                          const int32_t* __restrict__ lab, const int64_t* __restrict__ off,
-                          const int32_t* __restrict__ cnt, const double* __restrict__ cx,
-                          const double* __restrict__ cy, const uint8_t* __restrict__ east,
-                          int32_t* nlab) {
+// south / north quarter: the first ceil(h/2) of a half in (cy, cx, id) order are south
+__global__ void k_quarter(const int32_t* __restrict__ perm, int64_t ne,
+                          const int32_t* __restrict__ sub, const int64_t* __restrict__ off,
+                          const int32_t* __restrict__ cnt, int32_t* nlab) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ne) return;
-  const int32_t t = list[i], g = lab[t];
-  const double t0 = cy[t], t1 = cx[t];
-  const uint8_t h = east[t];
-  const int64_t o = off[g];
-  const int32_t m = cnt[g];
-  int32_t rank = 0, hm = 0;
-  for (int32_t j = 0; j < m; ++j) {
-    const int32_t u = list[o + j];
-    if (east[u] != h) continue;
-    ++hm;
-    rank += lex_less(cy[u], cx[u], u, t0, t1, t);
-  }
-  nlab[t] = 4 * g + 2 * h + (rank >= (hm + 1) / 2);
+  const int32_t t = perm[i], h = sub[t];
+  nlab[t] = 2 * h + (i - off[h] >= (cnt[h] + 1) / 2);
+}
+
+__global__ void k_check_keys(const double* cx, const double* cy, int64_t ne, int* err) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < ne && (cx[t] != cx[t] || cy[t] != cy[t])) atomicExch(err, 1);
 }
 
 __global__ void k_skeleton(const int32_t* __restrict__ edge_elem, int64_t nedge,
@@ -184,8 +181,10 @@ __global__ void k_skeleton(const int32_t* __restrict__ edge_elem, int64_t nedge,
 
 // ---- level macro-edges (reading A4): the fine skeleton edges grouped by their pair
 // (lo, hi) of agglomerates (lo = -1 on the domain boundary), numbered in lexicographic
-// pair order.  Bucketed by lo (counting sort); inside a bucket the distinct hi values are
-// found and ranked by comparison (a bucket is about one agglomerate's perimeter).
+// pair order.  Counting-sorted into 2G buckets: bucket a < G holds agglomerate a's share
+// of the domain boundary (the single pair (-1, a)), bucket G + lo the interior edges of
+// pairs (lo, *); inside a bucket (at most about one agglomerate's perimeter) the distinct
+// hi values are found and ranked by comparison.  Bucket order = lexicographic pair order.
 __device__ __forceinline__ bool edge_pair(const int32_t* __restrict__ edge_elem,
                                           const int32_t* __restrict__ lab, int64_t e, int32_t& lo,
                                           int32_t& hi) {
@@ -201,34 +200,41 @@ __device__ __forceinline__ bool edge_pair(const int32_t* __restrict__ edge_elem,
   return la != lb;
 }
 
-__global__ void k_me_count(const int32_t* edge_elem, int64_t nedge, const int32_t* lab,
+__device__ __forceinline__ int64_t bucket_of(int32_t lo, int32_t hi, int64_t G) {
+  return lo < 0 ? hi : G + lo;
+}
+
+__global__ void k_me_count(const int32_t* edge_elem, int64_t nedge, const int32_t* lab, int64_t G,
                            int32_t* cnt) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nedge) return;
   int32_t lo, hi;
-  if (edge_pair(edge_elem, lab, e, lo, hi)) atomicAdd(cnt + lo + 1, 1);
+  if (edge_pair(edge_elem, lab, e, lo, hi)) atomicAdd(cnt + bucket_of(lo, hi, G), 1);
 }
 
-__global__ void k_me_scatter(const int32_t* edge_elem, int64_t nedge, const int32_t* lab,
+__global__ void k_me_scatter(const int32_t* edge_elem, int64_t nedge, const int32_t* lab, int64_t G,
                              const int64_t* off, int32_t* cur, int32_t* elist) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nedge) return;
   int32_t lo, hi;
-  if (edge_pair(edge_elem, lab, e, lo, hi)) elist[off[lo + 1] + atomicAdd(cur + lo + 1, 1)] = (int32_t)e;
+  if (edge_pair(edge_elem, lab, e, lo, hi)) {
+    const int64_t q = bucket_of(lo, hi, G);
+    elist[off[q] + atomicAdd(cur + q, 1)] = (int32_t)e;
+  }
 }
 
 // first[e] = e is the lowest-numbered edge of its pair; dcnt[bucket] counts the pairs
 __global__ void k_me_first(const int32_t* __restrict__ edge_elem, int64_t nsk,
-                           const int32_t* __restrict__ lab, const int32_t* __restrict__ elist,
-                           const int64_t* __restrict__ off, const int32_t* __restrict__ cnt,
-                           uint8_t* first, int32_t* dcnt) {
+                           const int32_t* __restrict__ lab, int64_t G,
+                           const int32_t* __restrict__ elist, const int64_t* __restrict__ off,
+                           const int32_t* __restrict__ cnt, uint8_t* first, int32_t* dcnt) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nsk) return;
   const int32_t e = elist[i];
   int32_t lo, hi;
   edge_pair(edge_elem, lab, e, lo, hi);
-  const int64_t o = off[lo + 1];
-  const int32_t m = cnt[lo + 1];
+  const int64_t q = bucket_of(lo, hi, G), o = off[q];
+  const int32_t m = cnt[q];
   bool f = true;
   for (int32_t j = 0; j < m && f; ++j) {
     const int32_t u = elist[o + j];
@@ -237,14 +243,14 @@ __global__ void k_me_first(const int32_t* __restrict__ edge_elem, int64_t nsk,
     if (uh == hi && u < e) f = false;
   }
   first[e] = f;
-  if (f) atomicAdd(dcnt + lo + 1, 1);
+  if (f) atomicAdd(dcnt + q, 1);
 }
 
 __global__ void k_me_rank(const int32_t* __restrict__ edge_elem, int64_t nedge,
-                          const int32_t* __restrict__ lab, const int32_t* __restrict__ elist,
-                          const int64_t* __restrict__ off, const int32_t* __restrict__ cnt,
-                          const uint8_t* __restrict__ first, const int64_t* __restrict__ doff,
-                          int32_t* medge) {
+                          const int32_t* __restrict__ lab, int64_t G,
+                          const int32_t* __restrict__ elist, const int64_t* __restrict__ off,
+                          const int32_t* __restrict__ cnt, const uint8_t* __restrict__ first,
+                          const int64_t* __restrict__ doff, int32_t* medge) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nedge) return;
   int32_t lo, hi;
@@ -252,8 +258,8 @@ __global__ void k_me_rank(const int32_t* __restrict__ edge_elem, int64_t nedge,
     medge[e] = -1;
     return;
   }
-  const int64_t o = off[lo + 1];
-  const int32_t m = cnt[lo + 1];
+  const int64_t q = bucket_of(lo, hi, G), o = off[q];
+  const int32_t m = cnt[q];
   int32_t rank = 0;
   for (int32_t j = 0; j < m; ++j) {
     const int32_t u = elist[o + j];
@@ -262,7 +268,7 @@ __global__ void k_me_rank(const int32_t* __restrict__ edge_elem, int64_t nedge,
     edge_pair(edge_elem, lab, u, ul, uh);
     rank += uh < hi;
   }
-  medge[e] = (int32_t)(doff[lo + 1] + rank);
+  medge[e] = (int32_t)(doff[q] + rank);
 }
 
 inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t > 0 ? (n + t - 1) / t : 1); }
@@ -304,21 +310,52 @@ extern "C" int mg_agglomerate_seeds(int64_t ne, int64_t nedge, const int32_t* ed
     unsigned long long* key = S.get<unsigned long long>(ne);
     unsigned long long* bad = S.get<unsigned long long>(1);
     int* flags = S.get<int>(2);   // [0] seed error, [1] BFS changed
-    // counting-sort buffers: G agglomerates (splits) or G + 1 pair buckets (macro-edges)
-    int32_t* cnt = S.get<int32_t>((size_t)G + 1);
-    int32_t* cur = S.get<int32_t>((size_t)G + 1);
-    int64_t* off = S.get<int64_t>((size_t)G + 1);
-    int32_t* dcnt = S.get<int32_t>((size_t)G + 1);
-    int64_t* doff = S.get<int64_t>((size_t)G + 1);
+    // counting-sort buffers: G agglomerates (splits) or 2G pair buckets (macro-edges)
+    int32_t* cnt = S.get<int32_t>(2 * (size_t)G);
+    int32_t* cur = S.get<int32_t>(2 * (size_t)G);
+    int64_t* off = S.get<int64_t>(2 * (size_t)G);
+    int32_t* dcnt = S.get<int32_t>(2 * (size_t)G);
+    int64_t* doff = S.get<int64_t>(2 * (size_t)G);
     int32_t* list = S.get<int32_t>(ne > nedge ? ne : nedge);
     uint8_t* east = S.get<uint8_t>(ne > nedge ? ne : nedge);
-    if (!key || !bad || !flags || !cnt || !cur || !off || !dcnt || !doff || !list || !east)
+    // split sorts: permutation / key double buffers and CUB's temporary storage
+    int32_t* permA = S.get<int32_t>(ne);
+    int32_t* permB = S.get<int32_t>(ne);
+    double* dkA = S.get<double>(ne);
+    double* dkB = S.get<double>(ne);
+    int32_t* ikA = S.get<int32_t>(ne);
+    int32_t* ikB = S.get<int32_t>(ne);
+    int32_t* sub = S.get<int32_t>(ne);
+    size_t tb_d = 0, tb_i = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb_d, dkA, dkB, permA, permB, (int)ne, 0, 64, st);
+    cub::DeviceRadixSort::SortPairs(nullptr, tb_i, ikA, ikB, permA, permB, (int)ne, 0, 32, st);
+    const size_t tbytes = tb_d > tb_i ? tb_d : tb_i;
+    void* temp = S.get<unsigned char>(tbytes);
+    if (!key || !bad || !flags || !cnt || !cur || !off || !dcnt || !doff || !list || !east ||
+        !permA || !permB || !dkA || !dkB || !ikA || !ikB || !sub || !temp)
       return MG_ERR_CUDA;
+    int32_t* perm = permA;   // current permutation (the other buffer receives each sort)
+    auto other = [&](int32_t* q) { return q == permA ? permB : permA; };
+    auto sort_by_d = [&](const double* v) {   // stable sort of perm by v[perm[i]]
+      k_gather_d<<<nblk(ne), 256, 0, st>>>(perm, v, ne, dkA);
+      size_t tb = tbytes;
+      cub::DeviceRadixSort::SortPairs(temp, tb, dkA, dkB, perm, other(perm), (int)ne, 0, 64, st);
+      perm = other(perm);
+    };
+    auto sort_by_i = [&](const int32_t* v, int64_t bound) {   // keys in [0, bound)
+      int bits = 1;
+      while (bits < 31 && ((int64_t)1 << bits) < bound) ++bits;
+      k_gather_i<<<nblk(ne), 256, 0, st>>>(perm, v, ne, ikA);
+      size_t tb = tbytes;
+      cub::DeviceRadixSort::SortPairs(temp, tb, ikA, ikB, perm, other(perm), (int)ne, 0, bits, st);
+      perm = other(perm);
+    };
     int hflags[2] = {0, 0};
     cudaMemsetAsync(flags, 0, 2 * sizeof(int), st);
     cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st);
     k_seed_init<<<nblk(ne > nedge ? ne : nedge), 256, 0, st>>>(key, ne, edge_elem, nedge, flags);
     k_seed_set<<<nblk(nseed), 256, 0, st>>>(key, ne, seeds, nseed, flags);
+    k_check_keys<<<nblk(ne), 256, 0, st>>>(cx, cy, ne, flags);
     cudaMemcpyAsync(hflags, flags, sizeof(int), cudaMemcpyDeviceToHost, st);
     if (cudaStreamSynchronize(st) != cudaSuccess) return MG_ERR_CUDA;
     if (hflags[0]) return MG_ERR_ARG;   // seed or edge element id out of range
@@ -345,37 +382,49 @@ extern "C" int mg_agglomerate_seeds(int64_t ne, int64_t nedge, const int32_t* ed
       const int32_t* lab = labels + (size_t)(k - 1) * ne;
       if (medge) {   // level-k macro-edges (A4); `east` doubles as the first-of-pair flags
         int32_t* me = medge + (size_t)(k - 1) * nedge;
-        const int64_t B = Gk + 1;
+        const int64_t B = 2 * Gk;
         cudaMemsetAsync(cnt, 0, (size_t)B * sizeof(int32_t), st);
         cudaMemsetAsync(cur, 0, (size_t)B * sizeof(int32_t), st);
         cudaMemsetAsync(dcnt, 0, (size_t)B * sizeof(int32_t), st);
-        k_me_count<<<nblk(nedge), 256, 0, st>>>(edge_elem, nedge, lab, cnt);
+        k_me_count<<<nblk(nedge), 256, 0, st>>>(edge_elem, nedge, lab, Gk, cnt);
         k_scan<<<1, 1024, 0, st>>>(cnt, B, off);
-        k_me_scatter<<<nblk(nedge), 256, 0, st>>>(edge_elem, nedge, lab, off, cur, list);
+        k_me_scatter<<<nblk(nedge), 256, 0, st>>>(edge_elem, nedge, lab, Gk, off, cur, list);
         int64_t hoff = 0;
         int32_t hcnt = 0;
-        cudaMemcpyAsync(&hoff, off + Gk, sizeof(hoff), cudaMemcpyDeviceToHost, st);
-        cudaMemcpyAsync(&hcnt, cnt + Gk, sizeof(hcnt), cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(&hoff, off + B - 1, sizeof(hoff), cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(&hcnt, cnt + B - 1, sizeof(hcnt), cudaMemcpyDeviceToHost, st);
         if (cudaStreamSynchronize(st) != cudaSuccess) return MG_ERR_CUDA;
         const int64_t nsk = hoff + hcnt;   // skeleton edges of level k
-        k_me_first<<<nblk(nsk), 256, 0, st>>>(edge_elem, nsk, lab, list, off, cnt, east, dcnt);
+        k_me_first<<<nblk(nsk), 256, 0, st>>>(edge_elem, nsk, lab, Gk, list, off, cnt, east, dcnt);
         k_scan<<<1, 1024, 0, st>>>(dcnt, B, doff);
-        k_me_rank<<<nblk(nedge), 256, 0, st>>>(edge_elem, nedge, lab, list, off, cnt, east, doff, me);
+        k_me_rank<<<nblk(nedge), 256, 0, st>>>(edge_elem, nedge, lab, Gk, list, off, cnt, east, doff,
+                                                me);
         int32_t hd = 0;
-        cudaMemcpyAsync(&hoff, doff + Gk, sizeof(hoff), cudaMemcpyDeviceToHost, st);
-        cudaMemcpyAsync(&hd, dcnt + Gk, sizeof(hd), cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(&hoff, doff + B - 1, sizeof(hoff), cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(&hd, dcnt + B - 1, sizeof(hd), cudaMemcpyDeviceToHost, st);
         if (cudaStreamSynchronize(st) != cudaSuccess) return MG_ERR_CUDA;
         nmedge[k - 1] = hoff + hd;
       }
       if (k + 1 == nlev) break;
       int32_t* nlab = labels + (size_t)k * ne;
+      // west / east: order (label, cx, cy, id)
       cudaMemsetAsync(cnt, 0, (size_t)Gk * sizeof(int32_t), st);
-      cudaMemsetAsync(cur, 0, (size_t)Gk * sizeof(int32_t), st);
       k_count<<<nblk(ne), 256, 0, st>>>(lab, ne, cnt);
       k_scan<<<1, 1024, 0, st>>>(cnt, Gk, off);
-      k_scatter<<<nblk(ne), 256, 0, st>>>(lab, ne, off, cur, list);
-      k_half<<<nblk(ne), 256, 0, st>>>(list, ne, lab, off, cnt, cx, cy, east);
-      k_quarter<<<nblk(ne), 256, 0, st>>>(list, ne, lab, off, cnt, cx, cy, east, nlab);
+      k_iota<<<nblk(ne), 256, 0, st>>>(perm, ne);
+      sort_by_d(cy);
+      sort_by_d(cx);
+      sort_by_i(lab, Gk);
+      k_half<<<nblk(ne), 256, 0, st>>>(perm, ne, lab, off, cnt, sub);
+      // south / north: order (2 label + east, cy, cx, id)
+      cudaMemsetAsync(cnt, 0, (size_t)(2 * Gk) * sizeof(int32_t), st);
+      k_count<<<nblk(ne), 256, 0, st>>>(sub, ne, cnt);
+      k_scan<<<1, 1024, 0, st>>>(cnt, 2 * Gk, off);
+      k_iota<<<nblk(ne), 256, 0, st>>>(perm, ne);
+      sort_by_d(cx);
+      sort_by_d(cy);
+      sort_by_i(sub, 2 * Gk);
+      k_quarter<<<nblk(ne), 256, 0, st>>>(perm, ne, sub, off, cnt, nlab);
       k_skeleton<<<nblk(nedge), 256, 0, st>>>(edge_elem, nedge, nlab, skel + (size_t)k * nedge);
     }
     if (cudaGetLastError() != cudaSuccess) rc = MG_ERR_CUDA;

@@ -150,3 +150,21 @@ def test_bench_flags_not_shadowed():
     targets = [t.id for node in ast.walk(main) if isinstance(node, ast.Assign)
                for t in node.targets if isinstance(t, ast.Name)]
     assert targets.count("ns") == 1, targets.count("ns")
+
+
+def test_agglomerate_seeds_rejects_bad_arguments_on_the_host(lib):
+    """mg_agglomerate_seeds validates sizes / pointers before touching the device."""
+    import ctypes as C
+    bad = C.c_int64(7)
+    dummy = C.c_void_p(16)
+    assert lib.mg_agglomerate_seeds(0, 4, dummy, dummy, dummy, 1, dummy, 3, dummy, dummy, None,
+                                    None, None, C.byref(bad)) == -1
+    assert bad.value == -1
+    assert lib.mg_agglomerate_seeds(4, 4, dummy, dummy, dummy, 1, dummy, 1, dummy, dummy, None,
+                                    None, None, None) == -1          # nlev < 2
+    assert lib.mg_agglomerate_seeds(4, 4, None, dummy, dummy, 1, dummy, 3, dummy, dummy, None,
+                                    None, None, None) == -1          # NULL edge_elem
+    assert lib.mg_agglomerate_seeds(4, 4, dummy, dummy, dummy, 1, dummy, 3, dummy, dummy, dummy,
+                                    None, None, None) == -1          # medge without nmedge
+    assert lib.mg_agglomerate_seeds(4, 4, dummy, dummy, dummy, 1 << 20, dummy, 8, dummy, dummy,
+                                    None, None, None, None) == -1    # ids beyond int32
