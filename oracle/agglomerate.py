@@ -31,9 +31,19 @@ The paper calls its procedure "ad hoc" and does not fix the rules; readings
       {fine edges between agglomerates a < b} and {fine edges of agglomerate a
       on the domain boundary} (pair (-1, a)), numbered by the lexicographic
       order of their pairs; a fine edge off the level-k skeleton gets -1.
+  A5  PAPER.md:360-372 (remark: macro-elements of no standard shape need "a
+      parameterization of each macro-edge to define M_k"): a macro-edge whose
+      fine edges form one simple open path is parameterised by arc length,
+      s in [0, 1], from the end vertex that is least in (vx, vy, vertex id);
+      s at a vertex = (sum of the lengths of the path's edges before it, added
+      in path order) / (the path's total length, added in path order), edge
+      length = sqrt(dx*dx + dy*dy).  A macro-edge that is not one open path
+      (a closed loop, several pieces, a vertex shared by more than two of its
+      edges) has no such parameterisation: its edges get s = -1.
 """
 from __future__ import annotations
 
+import math
 from collections import deque
 
 import numpy as np
@@ -119,6 +129,51 @@ def macro_edges(labels: np.ndarray, edge_elem: np.ndarray):
             pairs.append(None)
     ids = {q: k for k, q in enumerate(sorted({q for q in pairs if q is not None}))}
     return np.array([-1 if q is None else ids[q] for q in pairs], dtype=np.int32), len(ids)
+
+
+def macro_edge_params(medge: np.ndarray, nmedge: int, edge_vert: np.ndarray, vx, vy):
+    """s at each end vertex of every fine edge, [nedge, 2] (reading A5; -1 where the
+    edge is off the skeleton or its macro-edge is not one open path)."""
+    out = -np.ones((len(medge), 2))
+    members = [[] for _ in range(nmedge)]
+    for e, q in enumerate(medge.tolist()):
+        if q >= 0:
+            members[q].append(e)
+    for q, es in enumerate(members):
+        inc = {}                                  # vertex -> incident edges of q
+        for e in es:
+            for v in edge_vert[e].tolist():
+                inc.setdefault(v, []).append(e)
+        ends = [v for v, l in inc.items() if len(l) == 1]
+        if any(len(l) > 2 for l in inc.values()) or len(ends) != 2:
+            continue
+        v = min(ends, key=lambda w: (vx[w], vy[w], w))
+        path = []                                 # (edge, entry vertex, exit vertex)
+        e = inc[v][0]
+        while True:
+            a, b = edge_vert[e].tolist()
+            w = b if a == v else a
+            path.append((e, v, w))
+            nxt = [f for f in inc[w] if f != e]
+            if not nxt:
+                break
+            v, e = w, nxt[0]
+        if len(path) != len(es):                  # several pieces
+            continue
+        lengths = []
+        for e, a, b in path:
+            dx, dy = vx[b] - vx[a], vy[b] - vy[a]
+            lengths.append(math.sqrt(dx * dx + dy * dy))
+        total = 0.0
+        for ln in lengths:
+            total += ln
+        cum = 0.0
+        for (e, a, b), ln in zip(path, lengths):
+            s0, cum = cum / total, cum + ln
+            s1 = cum / total
+            out[e, 0 if edge_vert[e][0] == a else 1] = s0
+            out[e, 0 if edge_vert[e][0] == b else 1] = s1
+    return out
 
 
 def agglomerate_levels(ne, edge_elem, cx, cy, seeds, nlev: int):

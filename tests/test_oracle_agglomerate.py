@@ -134,3 +134,107 @@ def test_macro_edges_of_the_quadtree_closed_form():
         assert (sub >= 0).all()
         for r in sub:
             assert (me[me3 == r] == q).all()
+
+
+def _params(mesh, labels, k):
+    me, nme = A.macro_edges(labels[k], mesh.edge_elem)
+    return me, nme, A.macro_edge_params(me, nme, mesh.edge_vert, mesh.vx, mesh.vy)
+
+
+def test_macro_edge_parameter_of_the_quadtree_closed_form():
+    """A5 on the unjittered 8 x 8 grid (one seed), level 2: each interior macro-edge is
+    a straight 4-edge segment, s = distance to its start end / its length (exact in
+    binary here); each quadrant's share of dOmega is an L of 8 edges from the end least
+    in (x, y): s = arc length / 1."""
+    n = 8
+    mesh = structured_quad_mesh(n)
+    labels, _ = A.agglomerate_levels(mesh.ne, mesh.edge_elem, mesh.cx, mesh.cy, mesh.seeds, 3)
+    me, nme, P = _params(mesh, labels, 1)
+    assert (P[me >= 0] >= 0).all()
+    X, Y = mesh.vx, mesh.vy
+    for q in range(nme):
+        es = np.flatnonzero(me == q)
+        verts = np.unique(mesh.edge_vert[es])
+        deg = {v: int((mesh.edge_vert[es] == v).sum()) for v in verts}
+        ends = sorted([v for v in verts if deg[v] == 1], key=lambda v: (X[v], Y[v], v))
+        start, stop = ends
+        corner = [v for v in verts if X[v] == 0.0 and Y[v] == 0.0 or X[v] == 1.0 and Y[v] == 0.0
+                  or X[v] == 0.0 and Y[v] == 1.0 or X[v] == 1.0 and Y[v] == 1.0]
+        for e in es:
+            for c in range(2):
+                v = mesh.edge_vert[e, c]
+                if corner and len(es) == n:       # L-shaped boundary share (through a box corner)
+                    cv = corner[0]
+                    on_start_side = X[v] == X[cv] if X[start] == X[cv] else Y[v] == Y[cv]
+                    d1 = lambda u, w: abs(X[u] - X[w]) + abs(Y[u] - Y[w])
+                    want = d1(v, start) if on_start_side else d1(start, cv) + d1(v, cv)
+                else:                              # straight segment
+                    want = (abs(X[v] - X[start]) + abs(Y[v] - Y[start])) / \
+                        (abs(X[stop] - X[start]) + abs(Y[stop] - Y[start]))
+                assert P[e, c] == want, (q, e, c, P[e, c], want)
+
+
+def test_macro_edge_parameter_invariants_on_holed_meshes():
+    """A5 on jittered holed meshes: a parameterised macro-edge's s runs from 0 to 1,
+    agrees bit for bit at every vertex its edges share, and each edge's s-increment
+    is positive; a macro-edge is unparameterised exactly when it is not one open path
+    (checked by scipy connected components and vertex degrees)."""
+    mesh = holed_quad_mesh(48, holes=6, sx=3, sy=2, seed=21)
+    labels, _ = A.agglomerate_levels(mesh.ne, mesh.edge_elem, mesh.cx, mesh.cy, mesh.seeds, 5)
+    for k in range(4):
+        me, nme, P = _params(mesh, labels, k)
+        assert (P[me < 0] == -1).all()
+        for q in range(nme):
+            es = np.flatnonzero(me == q)
+            ev = mesh.edge_vert[es]
+            verts, inv = np.unique(ev, return_inverse=True)
+            inv = inv.reshape(-1, 2)
+            deg = np.bincount(inv.ravel(), minlength=len(verts))
+            g = coo_matrix((np.ones(len(es)), (inv[:, 0], inv[:, 1])), shape=(len(verts),) * 2)
+            ncomp, _ = connected_components(g, directed=False)
+            is_path = ncomp == 1 and deg.max() <= 2 and (deg == 1).sum() == 2
+            if not is_path:
+                assert (P[es] == -1).all()
+                continue
+            assert (P[es] >= 0).all() and (P[es] <= 1).all()
+            sv = {}
+            for e in es:
+                for c in range(2):
+                    v = mesh.edge_vert[e, c]
+                    assert sv.setdefault(v, P[e, c]) == P[e, c]
+                assert P[e, 0] != P[e, 1]
+            s_end = sorted(sv[v] for v, d in zip(verts, deg) if d == 1)
+            assert s_end == [0.0, 1.0]
+
+
+def test_macro_edge_around_a_hole_is_not_a_path():
+    """One agglomerate holding a hole: its dOmega share is the outer loop plus the
+    hole's loop -- not one open path, so it has no parameterisation (-1)."""
+    mesh = holed_quad_mesh(16, holes=1, sx=1, sy=1, seed=5)
+    labels, _ = A.agglomerate_levels(mesh.ne, mesh.edge_elem, mesh.cx, mesh.cy, mesh.seeds, 2)
+    me, nme, P = _params(mesh, labels, 0)
+    assert nme == 1 and (P == -1).all()
+
+
+def test_macro_edge_parameter_is_arc_length_on_a_graded_line():
+    """A5 with non-uniform fine edges: x graded as x^2 (no jitter); the horizontal level-2
+    macro-edges on y = 1/2 are straight, so s = (x - x_start) / (x_stop - x_start)
+    (to rounding).  A wrong length formula (e.g. a dropped sqrt) fails it."""
+    mesh = structured_quad_mesh(8)
+    mesh.vx = mesh.vx ** 2
+    labels, _ = A.agglomerate_levels(mesh.ne, mesh.edge_elem, mesh.cx, mesh.cy, mesh.seeds, 3)
+    me, nme, P = _params(mesh, labels, 1)
+    X, Y = mesh.vx, mesh.vy
+    checked = 0
+    for q in range(nme):
+        es = np.flatnonzero(me == q)
+        verts = np.unique(mesh.edge_vert[es])
+        if not (Y[verts] == 0.5).all():
+            continue
+        x0, x1 = X[verts].min(), X[verts].max()
+        for e in es:
+            for c in range(2):
+                v = mesh.edge_vert[e, c]
+                assert abs(P[e, c] - (X[v] - x0) / (x1 - x0)) <= 4e-16
+                checked += 1
+    assert checked == 2 * 8

@@ -14,7 +14,10 @@ each point of a regular sx x sy lattice over the box).
 Mesh description (shared with include/mgdtn.h, `mg_agglomerate_seeds`):
   ne elements, centroids cx[ne], cy[ne] (float64);
   nedge edges, edge_elem[nedge][2] (int32): the two elements sharing the edge,
-  edge_elem[e][1] = -1 on the domain boundary (holes included).
+  edge_elem[e][1] = -1 on the domain boundary (holes included); for the
+  macro-edge parameterisation (`mg_macro_edge_params`) also edge_vert[nedge][2]
+  (int32) the edge's end vertices and vx, vy[nvert] (float64) the vertex
+  coordinates (grid vertex (a, b) has id b*(n+1)+a; unused ones included).
 """
 from __future__ import annotations
 
@@ -30,6 +33,9 @@ class QuadMesh:
     cy: np.ndarray          # [ne] float64
     edge_elem: np.ndarray   # [nedge, 2] int32, second -1 on the boundary
     seeds: np.ndarray       # [nseed] int32 element ids
+    edge_vert: np.ndarray = None   # [nedge, 2] int32 vertex ids of the edge's endpoints
+    vx: np.ndarray = None          # [nvert] float64 vertex coordinates
+    vy: np.ndarray = None
 
     @property
     def nedge(self) -> int:
@@ -85,6 +91,8 @@ def holed_quad_mesh(n: int, holes: int = 8, jitter: float = 0.3, sx: int = 4, sy
             else:
                 edges[key][1] = k
     edge_elem = np.array([edges[key] for key in order], dtype=np.int32).reshape(-1, 2)
+    edge_vert = np.array([[a[1] * (n + 1) + a[0], b[1] * (n + 1) + b[0]] for a, b in order],
+                         dtype=np.int32).reshape(-1, 2)
     seeds = []
     for b in range(sy):
         for a in range(sx):
@@ -92,7 +100,8 @@ def holed_quad_mesh(n: int, holes: int = 8, jitter: float = 0.3, sx: int = 4, sy
             s = int(np.argmin((cx - px) ** 2 + (cy - py) ** 2))
             if s not in seeds:
                 seeds.append(s)
-    return QuadMesh(ne, cx, cy, edge_elem, np.array(seeds, dtype=np.int32))
+    return QuadMesh(ne, cx, cy, edge_elem, np.array(seeds, dtype=np.int32), edge_vert,
+                    vx.reshape(-1).copy(), vy.reshape(-1).copy())
 
 
 def structured_quad_mesh(n: int, seeds=(0,)) -> QuadMesh:
