@@ -373,6 +373,26 @@ int mg_agglomerate_seeds(int64_t ne, int64_t nedge, const int32_t* edge_elem, co
                          int32_t* labels, uint8_t* skel, int32_t* medge, int64_t* nmedge,
                          void* stream, int64_t* bad_index);
 
+/* Arc-length parameterisation of one level's macro-edges (
+ * macro-elements of no standard shape need "a parameterization
+ * of each macro-edge to define M_k"; reading A5).  A macro-edge
+ * whose fine edges form one simple open path gets s in [0, 1] at every vertex: the
+ * lengths sqrt(dx*dx + dy*dy) of the path's edges before the vertex, added in path
+ * order from the end vertex least in (vx, vy, vertex id), divided by the path's
+ * length (added in the same order).  Any other macro-edge (a closed loop, several
+ * pieces, a vertex shared by more than two of its edges) gets s = -1, as do the
+ * fine edges off the level's skeleton.
+ *   medge          DEVICE int32 [nedge]: one level's macro-edge ids (a row of
+ *                  mg_agglomerate_seeds' medge), -1 off the skeleton, < nmedge
+ *   edge_vert      DEVICE int32 [nedge][2]: the fine edge's end vertices, < nvert
+ *   vx, vy         DEVICE float64 [nvert]: vertex coordinates
+ *   s              DEVICE float64 [nedge][2] (caller-owned): s at edge_vert[e][0], [1]
+ *   stream         cudaStream_t; returns after it synchronises.  Scratch: cudaMallocAsync.
+ * Errors: MG_ERR_ARG (NULL, sizes, a vertex or macro-edge id out of range), MG_ERR_CUDA. */
+int mg_macro_edge_params(int64_t nedge, const int32_t* medge, int64_t nmedge,
+                         const int32_t* edge_vert, int64_t nvert, const double* vx,
+                         const double* vy, double* s, void* stream);
+
 const char* mg_last_error(const void* ctx);
 int64_t mg_last_error_index(const void* ctx);
 void mg_destroy(void* ctx);

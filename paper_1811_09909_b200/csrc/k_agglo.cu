@@ -432,3 +432,155 @@ extern "C" int mg_agglomerate_seeds(int64_t ne, int64_t nedge, const int32_t* ed
   if (cudaStreamSynchronize(st) != cudaSuccess) rc = MG_ERR_CUDA;
   return rc;
 }
+
+// ---- macro-edge arc-length parameterisation (reading A5) ----
+// Every fine-edge end of a macro-edge becomes a record keyed (macro-edge, vertex); after
+// a radix sort the records of one vertex are adjacent, so each end learns its partner:
+// the other edge of the same macro-edge at that vertex (-1: a path end, -2: a vertex
+// shared by more than two of its edges).  One thread per fine edge then walks its path:
+// to both ends (path check: no branch, no loop, one piece = the macro-edge's size), then
+// from the start end (least in (vx, vy, id)) forward, summing the edge lengths in path
+// order twice (total, then up to itself), the same additions in the same order as a
+// sequential sweep.  O(L) per edge for a path of L edges (setup-time).
+namespace {
+
+constexpr unsigned long long REC_NONE = ~0ull;
+
+__global__ void k_ep_records(const int32_t* __restrict__ medge, const int32_t* __restrict__ ev,
+                             int64_t nedge, int64_t nmedge, int64_t nvert, unsigned long long* key,
+                             int32_t* val, int32_t* size, int* err) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= 2 * nedge) return;
+  const int64_t e = r >> 1;
+  int32_t q = medge[e];
+  const int32_t v = ev[r];
+  if (v < 0 || v >= nvert || q >= nmedge) {
+    atomicExch(err, 1);
+    q = -1;
+  }
+  key[r] = q >= 0 && v >= 0 && v < nvert
+               ? ((unsigned long long)(uint32_t)q << 32) | (uint32_t)v : REC_NONE;
+  val[r] = (int32_t)r;
+  if (q >= 0 && (r & 1) == 0) atomicAdd(size + q, 1);
+}
+
+__global__ void k_ep_partner(const unsigned long long* __restrict__ key,
+                             const int32_t* __restrict__ val, int64_t nrec, int32_t* partner) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrec) return;
+  const unsigned long long k = key[i];
+  if (k == REC_NONE) return;
+  int64_t lo = i, hi = i + 1;
+  while (lo > 0 && key[lo - 1] == k) --lo;
+  while (hi < nrec && key[hi] == k) ++hi;
+  const int64_t deg = hi - lo;
+  partner[val[i]] = deg == 1 ? -1 : deg == 2 ? val[i == lo ? lo + 1 : lo] : -2;
+}
+
+__device__ __forceinline__ double edge_len(const double* vx, const double* vy, int32_t a,
+                                           int32_t b) {
+  const double dx = vx[b] - vx[a], dy = vy[b] - vy[a];
+  return sqrt(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));   // no FMA contraction
+}
+
+__global__ void k_ep_param(const int32_t* __restrict__ medge, const int32_t* __restrict__ ev,
+                           int64_t nedge, const int32_t* __restrict__ partner,
+                           const int32_t* __restrict__ size, const double* __restrict__ vx,
+                           const double* __restrict__ vy, double* s) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nedge) return;
+  s[2 * e] = s[2 * e + 1] = -1.0;
+  const int32_t q = medge[e];
+  if (q < 0) return;
+  const int32_t m = size[q];
+  // walk to the end beyond side c0 of e; returns the end record (edge << 1 | side) or -1
+  auto walk_end = [&](int c0, int32_t& steps) -> int64_t {
+    int64_t f = e;
+    int c = c0;
+    steps = 0;
+    for (;;) {
+      const int32_t p = partner[2 * f + c];
+      if (p == -1) return (f << 1) | c;
+      if (p == -2) return -1;
+      f = p >> 1;
+      c = 1 - (p & 1);
+      if (f == e || ++steps >= m) return -1;   // a loop, or longer than the macro-edge
+    }
+  };
+  int32_t s0 = 0, s1 = 0;
+  const int64_t A = walk_end(0, s0), B = walk_end(1, s1);
+  if (A < 0 || B < 0 || s0 + s1 + 1 != m) return;   // not one open path
+  const int32_t va = ev[A], vb = ev[B];
+  const bool a_first = vx[va] < vx[vb] || (vx[va] == vx[vb] && (vy[va] < vy[vb] ||
+                                                                 (vy[va] == vy[vb] && va < vb)));
+  const int64_t S = a_first ? A : B;   // start record: the path enters there
+  double total = 0.0;
+  {
+    int64_t f = S >> 1;
+    int c = (int)(S & 1);
+    for (;;) {
+      total += edge_len(vx, vy, ev[2 * f + c], ev[2 * f + 1 - c]);
+      const int32_t p = partner[2 * f + 1 - c];
+      if (p == -1) break;
+      f = p >> 1;
+      c = p & 1;
+    }
+  }
+  double cum = 0.0;
+  int64_t f = S >> 1;
+  int c = (int)(S & 1);
+  for (;;) {
+    const double ln = edge_len(vx, vy, ev[2 * f + c], ev[2 * f + 1 - c]);
+    if (f == e) {
+      s[2 * e + c] = cum / total;
+      s[2 * e + 1 - c] = (cum + ln) / total;
+      return;
+    }
+    cum += ln;
+    const int32_t p = partner[2 * f + 1 - c];
+    f = p >> 1;
+    c = p & 1;
+  }
+}
+
+}  // namespace
+
+extern "C" int mg_macro_edge_params(int64_t nedge, const int32_t* medge, int64_t nmedge,
+                                    const int32_t* edge_vert, int64_t nvert, const double* vx,
+                                    const double* vy, double* s, void* stream) {
+  if (nedge <= 0 || nedge > INT32_MAX / 2 || nmedge < 0 || nmedge > INT32_MAX || nvert <= 0 ||
+      nvert > INT32_MAX || !medge || !edge_vert || !vx || !vy || !s)
+    return MG_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nrec = 2 * nedge;
+  int rc = MG_OK;
+  {
+    Scratch S{st, {}};
+    unsigned long long* kA = S.get<unsigned long long>(nrec);
+    unsigned long long* kB = S.get<unsigned long long>(nrec);
+    int32_t* vA = S.get<int32_t>(nrec);
+    int32_t* vB = S.get<int32_t>(nrec);
+    int32_t* partner = S.get<int32_t>(nrec);
+    int32_t* size = S.get<int32_t>(nmedge + 1);
+    int* err = S.get<int>(1);
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, kA, kB, vA, vB, (int)nrec, 0, 64, st);
+    void* temp = S.get<unsigned char>(tb);
+    if (!kA || !kB || !vA || !vB || !partner || !size || !err || !temp) return MG_ERR_CUDA;
+    cudaMemsetAsync(size, 0, (size_t)(nmedge + 1) * sizeof(int32_t), st);
+    cudaMemsetAsync(err, 0, sizeof(int), st);
+    k_ep_records<<<nblk(nrec), 256, 0, st>>>(medge, edge_vert, nedge, nmedge, nvert, kA, vA, size,
+                                             err);
+    int herr = 0;
+    cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return MG_ERR_CUDA;
+    if (herr) return MG_ERR_ARG;   // a vertex or macro-edge id out of range
+    size_t tb2 = tb;
+    cub::DeviceRadixSort::SortPairs(temp, tb2, kA, kB, vA, vB, (int)nrec, 0, 64, st);
+    k_ep_partner<<<nblk(nrec), 256, 0, st>>>(kB, vB, nrec, partner);
+    k_ep_param<<<nblk(nedge), 256, 0, st>>>(medge, edge_vert, nedge, partner, size, vx, vy, s);
+    if (cudaGetLastError() != cudaSuccess) rc = MG_ERR_CUDA;
+  }
+  if (cudaStreamSynchronize(st) != cudaSuccess) rc = MG_ERR_CUDA;
+  return rc;
+}

@@ -94,6 +94,7 @@ _SIGS = {
     "mg_loopback_abort": [_P],
     "mg_agglomerate_seeds": [C.c_int64, C.c_int64, _P, _P, _P, C.c_int32, _P, C.c_int32, _P, _P, _P,
                              _P, _P, C.POINTER(C.c_int64)],
+    "mg_macro_edge_params": [C.c_int64, _P, C.c_int64, _P, C.c_int64, _P, _P, _P, _P],
     "mg_last_error": [_P],
     "mg_last_error_index": [_P],
     "mg_destroy": [_P],
@@ -246,6 +247,26 @@ def agglomerate_seeds(edge_elem, cx, cy, seeds, nlev: int, stream=None):
     if rc != 0:
         raise MGError(f"mg_agglomerate_seeds: {ERRORS.get(rc, rc)} (element {bad.value})")
     return labels, skel, medge, list(nme)[:nlev - 1]
+
+
+def macro_edge_params(medge, nmedge: int, edge_vert, vx, vy, stream=None):
+    """Arc-length parameter of one level's macro-edges (mg_macro_edge_params, reading
+    A5): device tensors in (medge int32 [nedge], edge_vert int32 [nedge, 2], vx / vy
+    float64 [nvert]); device float64 [nedge, 2] out (-1 where not parameterised)."""
+    import torch
+    lib = load_library()
+    for t, dt in ((medge, torch.int32), (edge_vert, torch.int32), (vx, torch.float64),
+                  (vy, torch.float64)):
+        if not t.is_cuda or t.dtype != dt or not t.is_contiguous():
+            raise MGError(f"macro_edge_params: expected a contiguous CUDA {dt} tensor")
+    nedge = int(medge.numel())
+    s = torch.empty((nedge, 2), dtype=torch.float64, device=medge.device)
+    st = torch.cuda.current_stream(medge.device) if stream is None else stream
+    rc = lib.mg_macro_edge_params(nedge, _ptr(medge), int(nmedge), _ptr(edge_vert), int(vx.numel()),
+                                  _ptr(vx), _ptr(vy), _ptr(s), C.c_void_p(st.cuda_stream))
+    if rc != 0:
+        raise MGError(f"mg_macro_edge_params: {ERRORS.get(rc, rc)}")
+    return s
 
 
 def partition_plan(nx: int, ny: int, p: int, part: Partition, n_h_levels: int = 0):

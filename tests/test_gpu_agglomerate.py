@@ -3,7 +3,7 @@ quad mesh (mg_agglomerate_seeds; readings A1-A3) against
 oracle/agglomerate.py, bit for bit (integer output): level labels and level
 skeletons on holed, jittered meshes (the Example II stand-in, DESIGN.md
 section 4), a 2^m grid, a strip, and the edge cases (one seed, every element a
-seed, duplicate seeds, macro-edges (A4), levels past one element per agglomerate, a disconnected
+seed, duplicate seeds, macro-edges (A4) and their arc-length parameters (A5), levels past one element per agglomerate, a disconnected
 mesh, bad ids)."""
 import numpy as np
 import pytest
@@ -32,7 +32,7 @@ def _gpu(m: QuadMesh, nlev: int):
     return lab.cpu().numpy(), sk.cpu().numpy(), me.cpu().numpy(), nme
 
 
-def _check(m: QuadMesh, nlev: int):
+def _check(m: QuadMesh, nlev: int, params: bool = True):
     want_l, want_s = A.agglomerate_levels(m.ne, m.edge_elem, m.cx, m.cy, m.seeds, nlev)
     got_l, got_s, got_me, got_n = _gpu(m, nlev)
     np.testing.assert_array_equal(got_l, want_l)
@@ -41,6 +41,19 @@ def _check(m: QuadMesh, nlev: int):
         want_me, want_n = A.macro_edges(want_l[k], m.edge_elem)
         np.testing.assert_array_equal(got_me[k], want_me)
         assert got_n[k] == want_n
+        if params and m.edge_vert is not None:
+            # A5: the same additions in the same order on both sides -> bit for bit
+            want_p = A.macro_edge_params(want_me, want_n, m.edge_vert, m.vx, m.vy)
+            np.testing.assert_array_equal(_gpu_params(m, got_me[k], got_n[k]), want_p)
+
+
+def _gpu_params(m: QuadMesh, me: np.ndarray, nme: int):
+    from paper_1811_09909_b200 import macro_edge_params
+    d = torch.device("cuda:0")
+    s = macro_edge_params(torch.from_numpy(me).to(d).contiguous(), nme,
+                          torch.from_numpy(m.edge_vert).to(d).contiguous(),
+                          torch.from_numpy(m.vx).to(d), torch.from_numpy(m.vy).to(d))
+    return s.cpu().numpy()
 
 
 # (n, holes, sx, sy, seed, nlev): Example II's setting is N = 7 levels from 7 or 4 seeds
@@ -56,7 +69,24 @@ def test_agglomeration_parity(n, holes, sx, sy, seed, nlev):
 
 def test_agglomeration_parity_large():
     """~250k elements (many BFS layer batches, 31k-element agglomerates at level 1)."""
-    _check(holed_quad_mesh(512, holes=12, sx=4, sy=2, seed=9), 7)
+    _check(holed_quad_mesh(512, holes=12, sx=4, sy=2, seed=9), 7, params=False)
+    m = holed_quad_mesh(256, holes=10, sx=4, sy=2, seed=9)
+    _check(m, 6)
+
+
+def test_macro_edge_params_graded_line_and_bad_ids():
+    from paper_1811_09909_b200 import MGError
+    m = structured_quad_mesh(16)
+    m.vx = m.vx ** 2
+    _check(m, 4)
+    lab, _ = A.agglomerate_levels(m.ne, m.edge_elem, m.cx, m.cy, m.seeds, 3)
+    me, nme = A.macro_edges(lab[1], m.edge_elem)
+    with pytest.raises(MGError, match="MG_ERR_ARG"):
+        _gpu_params(m, me, nme - 1)                     # an id >= nmedge
+    ev = m.edge_vert.copy()
+    ev[0, 0] = len(m.vx)
+    with pytest.raises(MGError, match="MG_ERR_ARG"):
+        _gpu_params(QuadMesh(m.ne, m.cx, m.cy, m.edge_elem, m.seeds, ev, m.vx, m.vy), me, nme)
 
 
 def test_quadtree_grid_and_levels_past_one_element():
