@@ -176,6 +176,19 @@ def macro_edge_params(medge: np.ndarray, nmedge: int, edge_vert: np.ndarray, vx,
     return out
 
 
+def macro_edge_transfer(s: np.ndarray, p: int) -> np.ndarray:
+    """J_e [nedge, p+1, p+1] (reading A6): row a = fine node, column j = macro-edge basis."""
+    from oracle.basis import gll_nodes, lagrange
+    t = gll_nodes(p)
+    J = np.zeros((len(s), p + 1, p + 1))
+    for e in range(len(s)):
+        s0, s1 = s[e]
+        if s0 < 0:
+            continue
+        J[e] = lagrange(t, s0 + (s1 - s0) * t)
+    return J
+
+
 def agglomerate_levels(ne, edge_elem, cx, cy, seeds, nlev: int):
     """Labels and skeleton flags of levels k = 1 .. nlev-1 (row k-1 each)."""
     if nlev < 2:

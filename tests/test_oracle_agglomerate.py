@@ -238,3 +238,31 @@ def test_macro_edge_parameter_is_arc_length_on_a_graded_line():
                 assert abs(P[e, c] - (X[v] - x0) / (x1 - x0)) <= 4e-16
                 checked += 1
     assert checked == 2 * 8
+
+
+@pytest.mark.parametrize("p", [1, 2, 4])
+def test_macro_edge_transfer_reproduces_polynomials_in_arc_length(p):
+    """A6: J is the P^p interpolation in s -- rows sum to 1, and the macro-edge
+    coefficients q(t_j) of a degree-p polynomial q give q(s) at every fine node,
+    s = s0 + (s1 - s0) xi_a (p = 1: the closed form [[1 - s0, s0], [1 - s1, s1]]);
+    unparameterised edges get zero blocks."""
+    from oracle.basis import gll_nodes
+    mesh = holed_quad_mesh(32, holes=4, sx=2, sy=2, seed=13)
+    labels, _ = A.agglomerate_levels(mesh.ne, mesh.edge_elem, mesh.cx, mesh.cy, mesh.seeds, 4)
+    me, nme, P = _params(mesh, labels, 2)
+    J = A.macro_edge_transfer(P, p)
+    t = gll_nodes(p)
+    rng = np.random.default_rng(p)
+    coef = rng.standard_normal(p + 1)
+    q = lambda x: np.polyval(coef, x)
+    on = P[:, 0] >= 0
+    assert on.sum() > 100 and (J[~on] == 0).all()
+    np.testing.assert_allclose(J[on].sum(axis=2), 1.0, atol=1e-13)
+    for e in np.flatnonzero(on):
+        sa = P[e, 0] + (P[e, 1] - P[e, 0]) * t
+        np.testing.assert_allclose(J[e] @ q(t), q(sa), atol=1e-12)
+    # p = 1 closed form: J_e = [[1 - s0, s0], [1 - s1, s1]]
+    if p == 1:
+        e = np.flatnonzero(on)[0]
+        np.testing.assert_allclose(J[e], [[1 - P[e, 0], P[e, 0]], [1 - P[e, 1], P[e, 1]]],
+                                   atol=1e-15)
