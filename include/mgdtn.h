@@ -393,6 +393,18 @@ int mg_macro_edge_params(int64_t nedge, const int32_t* medge, int64_t nmedge,
                          const int32_t* edge_vert, int64_t nvert, const double* vx,
                          const double* vy, double* s, void* stream);
 
+/* P^p transfer blocks of the parameterised macro-edges (reading A6,
+ * DESIGN.md section 3): the level's trace space on a macro-edge is P^p in its arc
+ * length s with the GLL nodal basis on [0, 1]; fine node a of fine edge e (GLL node
+ * t_a from edge_vert[e][0] to [1]) sits at s = s0 + (s1 - s0) t_a, so the injection
+ * M_{k-1} -> M_k on that edge is J_e[a][j] = l_j(s).
+ *   s      DEVICE float64 [nedge][2]: mg_macro_edge_params' output (s0 < 0: zero block)
+ *   p      1 .. 7
+ *   J      DEVICE float64 [nedge][p+1][p+1] (caller-owned), row a, column j
+ *   stream cudaStream_t; returns after it synchronises.
+ * Errors: MG_ERR_ARG (NULL, sizes, p), MG_ERR_CUDA. */
+int mg_macro_edge_transfer(int64_t nedge, const double* s, int32_t p, double* J, void* stream);
+
 const char* mg_last_error(const void* ctx);
 int64_t mg_last_error_index(const void* ctx);
 void mg_destroy(void* ctx);

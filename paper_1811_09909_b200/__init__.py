@@ -6,8 +6,8 @@ steps in hand-written sm_100a CUDA kernels behind the C ABI include/mgdtn.h.
 """
 from .mgdtn import (MG_HDG, MG_IIPG_H, MG_NIPG_H, MG_SIPG_H, MG_SMOOTH_BLOCK_JACOBI, MG_SMOOTH_CHEBYSHEV, LIB_PATH,
                     LoopbackHub, MGError, MGSolver, Partition, SmootherConfig, load_library,
-                    nccl_unique_id, partition_plan, agglomerate_seeds, macro_edge_params, partition_side_edges, smoother_from_config)
+                    nccl_unique_id, partition_plan, agglomerate_seeds, macro_edge_params, macro_edge_transfer, partition_side_edges, smoother_from_config)
 
 __all__ = ["MGSolver", "SmootherConfig", "MGError", "load_library", "LIB_PATH", "MG_HDG",
            "MG_SIPG_H", "MG_IIPG_H", "MG_NIPG_H", "MG_SMOOTH_BLOCK_JACOBI", "MG_SMOOTH_CHEBYSHEV", "smoother_from_config",
-           "Partition", "LoopbackHub", "nccl_unique_id", "partition_plan", "partition_side_edges", "agglomerate_seeds", "macro_edge_params"]
+           "Partition", "LoopbackHub", "nccl_unique_id", "partition_plan", "partition_side_edges", "agglomerate_seeds", "macro_edge_params", "macro_edge_transfer"]

@@ -24,6 +24,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include "mgdtn.h"
+#include "refelem.h"
 
 namespace {
 
@@ -583,4 +584,46 @@ extern "C" int mg_macro_edge_params(int64_t nedge, const int32_t* medge, int64_t
   }
   if (cudaStreamSynchronize(st) != cudaSuccess) rc = MG_ERR_CUDA;
   return rc;
+}
+
+// ---- P^p transfer blocks of the parameterised macro-edges (reading A6) ----
+// Fine node a of edge e sits at s = s0 + (s1 - s0) t_a on its macro-edge; the block row
+// is the macro-edge's GLL Lagrange basis there, l_j(s) = prod_{m != j} (s - t_m) /
+// (t_j - t_m) in increasing m (the injection M_{k-1} -> M_k).
+namespace {
+
+struct Gll {
+  double t[8];
+};
+
+__global__ void k_me_transfer(const double* __restrict__ s, int64_t nedge, int p, Gll g,
+                              double* J) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nedge) return;
+  const int k1 = p + 1;
+  const double s0 = s[2 * e], s1 = s[2 * e + 1];
+  double* Je = J + e * k1 * k1;
+  for (int a = 0; a < k1; ++a) {
+    const double x = __dadd_rn(s0, __dmul_rn(s1 - s0, g.t[a]));   // as written, no FMA
+    for (int j = 0; j < k1; ++j) {
+      double v = 1.0;
+      for (int m = 0; m < k1; ++m)
+        if (m != j) v *= (x - g.t[m]) / (g.t[j] - g.t[m]);
+      Je[a * k1 + j] = s0 < 0.0 ? 0.0 : v;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int mg_macro_edge_transfer(int64_t nedge, const double* s, int32_t p, double* J,
+                                      void* stream) {
+  if (nedge <= 0 || p < 1 || p > 7 || !s || !J) return MG_ERR_ARG;
+  const std::vector<double> t = mgdtn::gll_nodes01(p);
+  Gll g{};
+  for (int a = 0; a <= p; ++a) g.t[a] = t[a];
+  cudaStream_t st = (cudaStream_t)stream;
+  k_me_transfer<<<nblk(nedge, 128), 128, 0, st>>>(s, nedge, p, g, J);
+  if (cudaGetLastError() != cudaSuccess) return MG_ERR_CUDA;
+  return cudaStreamSynchronize(st) == cudaSuccess ? MG_OK : MG_ERR_CUDA;
 }

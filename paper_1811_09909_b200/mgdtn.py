@@ -95,6 +95,7 @@ _SIGS = {
     "mg_agglomerate_seeds": [C.c_int64, C.c_int64, _P, _P, _P, C.c_int32, _P, C.c_int32, _P, _P, _P,
                              _P, _P, C.POINTER(C.c_int64)],
     "mg_macro_edge_params": [C.c_int64, _P, C.c_int64, _P, C.c_int64, _P, _P, _P, _P],
+    "mg_macro_edge_transfer": [C.c_int64, _P, C.c_int32, _P, _P],
     "mg_last_error": [_P],
     "mg_last_error_index": [_P],
     "mg_destroy": [_P],
@@ -267,6 +268,22 @@ def macro_edge_params(medge, nmedge: int, edge_vert, vx, vy, stream=None):
     if rc != 0:
         raise MGError(f"mg_macro_edge_params: {ERRORS.get(rc, rc)}")
     return s
+
+
+def macro_edge_transfer(s, p: int, stream=None):
+    """P^p transfer blocks J_e of the parameterised macro-edges (mg_macro_edge_transfer,
+    reading A6): device float64 [nedge, 2] in, device float64 [nedge, p+1, p+1] out."""
+    import torch
+    lib = load_library()
+    if not s.is_cuda or s.dtype != torch.float64 or not s.is_contiguous():
+        raise MGError("macro_edge_transfer: expected a contiguous CUDA float64 tensor")
+    nedge = int(s.shape[0])
+    J = torch.empty((nedge, p + 1, p + 1), dtype=torch.float64, device=s.device)
+    st = torch.cuda.current_stream(s.device) if stream is None else stream
+    rc = lib.mg_macro_edge_transfer(nedge, _ptr(s), int(p), _ptr(J), C.c_void_p(st.cuda_stream))
+    if rc != 0:
+        raise MGError(f"mg_macro_edge_transfer: {ERRORS.get(rc, rc)}")
+    return J
 
 
 def partition_plan(nx: int, ny: int, p: int, part: Partition, n_h_levels: int = 0):

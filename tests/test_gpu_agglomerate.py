@@ -3,7 +3,7 @@ quad mesh (mg_agglomerate_seeds; readings A1-A3) against
 oracle/agglomerate.py, bit for bit (integer output): level labels and level
 skeletons on holed, jittered meshes (the Example II stand-in, DESIGN.md
 section 4), a 2^m grid, a strip, and the edge cases (one seed, every element a
-seed, duplicate seeds, macro-edges (A4) and their arc-length parameters (A5), levels past one element per agglomerate, a disconnected
+seed, duplicate seeds, macro-edges (A4) their arc-length parameters (A5) and P^p transfer blocks (A6), levels past one element per agglomerate, a disconnected
 mesh, bad ids)."""
 import numpy as np
 import pytest
@@ -44,7 +44,15 @@ def _check(m: QuadMesh, nlev: int, params: bool = True):
         if params and m.edge_vert is not None:
             # A5: the same additions in the same order on both sides -> bit for bit
             want_p = A.macro_edge_params(want_me, want_n, m.edge_vert, m.vx, m.vy)
-            np.testing.assert_array_equal(_gpu_params(m, got_me[k], got_n[k]), want_p)
+            got_p = _gpu_params(m, got_me[k], got_n[k])
+            np.testing.assert_array_equal(got_p, want_p)
+            if k == nlev - 2:   # A6 transfer blocks on the finest agglomerated level
+                from paper_1811_09909_b200 import macro_edge_transfer
+                for p in (1, 4):
+                    J = macro_edge_transfer(torch.from_numpy(got_p).cuda().contiguous(), p)
+                    # the two sides' GLL nodes come from different root finders (ulps)
+                    np.testing.assert_allclose(J.cpu().numpy(), A.macro_edge_transfer(want_p, p),
+                                               rtol=0, atol=1e-13)
 
 
 def _gpu_params(m: QuadMesh, me: np.ndarray, nme: int):
