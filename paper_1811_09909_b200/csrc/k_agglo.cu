@@ -15,6 +15,8 @@
 //                boundary or its two elements carry different labels (A3).
 // Integer output only: the comparisons are exact, so the labels are bit-equal
 // to any implementation of the same readings (tests/test_gpu_agglomerate.py).
+// Also here: the arc-length parameterisation of the macro-edges (A5,
+// mg_macro_edge_params) and their P^p transfer blocks (A6, mg_macro_edge_transfer).
 // This is setup-time work (once per mesh), not part of the solve.
 #include <cuda_runtime.h>
 
